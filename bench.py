@@ -1,0 +1,457 @@
+#!/usr/bin/env python
+"""bench.py -- effective permutation bandwidth on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Metric: "permute effective GB/s (read+write bytes/s) and % of HBM peak at
+1/2/4/8 B200" = algorithmic bytes (2 * N * elem) / kernel time.
+
+Workload: cfg5 of BASELINE.json (rank-28 all-2 complex64, 2 GiB, seeded
+random axes) -- the configuration the metric is quoted on at 1/2/4/8 GPUs.
+At N=1 it is one kernel launch per step on one B200; at N>1 it is the
+sharded permutation (local pack permute -> NCCL all-to-all -> local unpack
+permute), total work fixed ("scaling": "strong").  The other BASELINE
+configs (cfg1-cfg4) are timed in the same run with the same protocol and
+reported under "configs".
+
+Timing: W untimed warm-up steps; K timed steps, each preceded by an L2 flush
+(write of a 2x-L2 buffer followed by a read of another 2x-L2 buffer, so the
+timed kernel neither hits in L2 nor pays for write-backs of dirty flush
+lines); CUDA events on the launching stream around the permutation only;
+barrier + synchronize on both sides; max over ranks.  nvidia-smi-equivalent
+clocks (NVML) are sampled during the timed region.
+
+--impl reference: the reference's own CPU path (its emitted x86 AVX-512
+kernel, oracle/_ref, built by oracle/build_ref.py) on the box's host cores,
+all usable threads, each thread permuting the full workload (shared input,
+private outputs); rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DEFAULT_CFG = "cfg5"
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------- clocks
+NVML_REASONS = {
+    0x1: "gpu_idle",
+    0x2: "applications_clocks_setting",
+    0x4: "sw_power_cap",
+    0x8: "hw_slowdown",
+    0x10: "sync_boost",
+    0x20: "sw_thermal_slowdown",
+    0x40: "hw_thermal_slowdown",
+    0x80: "hw_power_brake_slowdown",
+    0x100: "display_clock_setting",
+}
+
+
+class ClockSampler:
+    """Samples SM clock and clock-event reasons every 20 ms via NVML."""
+
+    def __init__(self, device_index=0):
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._h = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            import torch
+
+            uuid = str(torch.cuda.get_device_properties(device_index).uuid)
+            uuid = uuid if uuid.startswith("GPU-") else "GPU-" + uuid
+            try:
+                self._h = pynvml.nvmlDeviceGetHandleByUUID(uuid)
+            except Exception:
+                self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._nv = pynvml
+        except Exception as e:  # pragma: no cover - depends on the box
+            self.error = str(e)
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in NVML_REASONS.items():
+                    if mask & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self._h is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._h is not None:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {
+            "sm_mhz": statistics.median(self.samples),
+            "sm_max_mhz": self.max_mhz,
+            "reasons": sorted(self.reasons - {"gpu_idle"}),
+            "samples": len(self.samples),
+        }
+
+
+# ---------------------------------------------------------------- device timing
+class Flusher:
+    """Evicts L2 between timed steps: write a 2xL2 buffer, then read another."""
+
+    def __init__(self, torch, device):
+        l2 = getattr(torch.cuda.get_device_properties(device), "L2_cache_size", 126 << 20)
+        self.l2 = int(l2)
+        nbytes = max(2 * self.l2, 256 << 20)
+        self.w = torch.empty(nbytes // 4, dtype=torch.float32, device=device)
+        self.r = torch.zeros(nbytes // 4, dtype=torch.float32, device=device)
+        self.nbytes = nbytes
+
+    def __call__(self):
+        self.w.fill_(1.0)
+        self.r.sum()
+
+
+def time_device(torch, launch, steps, warmup, flush, stream):
+    """Per-step CUDA-event times (ms) of `launch` on `stream`, L2 flushed."""
+    for _ in range(warmup):
+        flush()
+        launch()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for a, b in evs:
+        flush()
+        a.record(stream)
+        launch()
+        b.record(stream)
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in evs]
+
+
+def _traffic_from_profiles(cfg):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        e = d.get("kernels", {}).get(cfg)
+        if e and e.get("dram_bytes") is not None:
+            return int(e["dram_bytes"])
+    except Exception:
+        pass
+    return None
+
+
+# ---------------------------------------------------------------- reference CPU arm
+def _mem_available():
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 16 << 30
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference_cpu(cfg, steps, warmup, threads=None, x=None):
+    """The reference's emitted CPU kernel, `threads` concurrent replicas.
+
+    Returns (GB/s, per-step seconds list, threads, target)."""
+    import numpy as np
+
+    from oracle.refkernels import RefKernel
+    from paper_2506_03686_b200.workloads import CONFIGS, make_input
+
+    wl = CONFIGS[cfg]
+    rk = RefKernel(cfg)
+    ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    cap_mem = max(1, int(_mem_available() * 0.5 // max(rk.nbytes, 1)) - 1)
+    if threads is None:
+        threads = ncpu
+    threads = max(1, min(threads, ncpu, cap_mem, 64))
+    if x is None:
+        x = make_input(wl, threads=min(ncpu, 32))
+    src = rk.alloc()
+    src.data[:] = x.reshape(-1).view(np.uint8)
+    outs = [rk.alloc() for _ in range(threads)]
+    # parity of the baseline itself (cheap: numpy transpose comparison on a sample)
+    rk.run_ptr(src.ptr, outs[0].ptr)
+    want = np.ascontiguousarray(np.transpose(x, wl.axes)).reshape(-1).view(np.uint8)
+    if not np.array_equal(outs[0].data, want):
+        raise RuntimeError("reference kernel output differs from numpy transpose")
+    del want
+    barrier = threading.Barrier(threads + 1)
+    stop = [False]
+
+    def worker(i):
+        while True:
+            barrier.wait()
+            if stop[0]:
+                return
+            rk.run_ptr(src.ptr, outs[i].ptr)
+            barrier.wait()
+
+    ts = [threading.Thread(target=worker, args=(i,), daemon=True) for i in range(threads)]
+    for t in ts:
+        t.start()
+    times = []
+    for s in range(warmup + steps):
+        t0 = time.perf_counter()
+        barrier.wait()      # release
+        barrier.wait()      # all done
+        dt = time.perf_counter() - t0
+        if s >= warmup:
+            times.append(dt)
+    stop[0] = True
+    barrier.wait()
+    for t in ts:
+        t.join()
+    gbs = threads * wl.algorithmic_bytes / (sum(times) / len(times)) / 1e9
+    return gbs, times, threads, rk.target
+
+
+def sample_parity(torch, x, y, shape, axes, nsamp=1 << 20, seed=0):
+    """y[i] == x[f(i)] on random output offsets i (f per core.py:173-178)."""
+    n = x.numel()
+    g = torch.Generator(device=x.device).manual_seed(seed)
+    idx = torch.randint(0, n, (nsamp,), device=x.device, generator=g, dtype=torch.int64)
+    in_strides = [1] * len(shape)
+    for k in range(len(shape) - 2, -1, -1):
+        in_strides[k] = in_strides[k + 1] * shape[k + 1]
+    rem = idx.clone()
+    src = torch.zeros_like(idx)
+    for a in reversed(axes):              # output dims, innermost first
+        d = shape[a]
+        src += (rem % d) * in_strides[a]
+        rem //= d
+    return bool(torch.equal(y[idx], x[src]))
+
+
+# ---------------------------------------------------------------- our arm
+def bench_one_gpu(args, torch, cfg, with_e2e, peak):
+    from paper_2506_03686_b200 import TensorLayout, build_program, execute, from_numpy_convention
+    from paper_2506_03686_b200.api import execute_device
+    from paper_2506_03686_b200.workloads import CONFIGS, make_input
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    wl = CONFIGS[cfg]
+    prog = build_program(TensorLayout.from_shape(wl.shape, wl.elem_bytes), from_numpy_convention(wl.axes))
+    nbytes = wl.numel * wl.elem_bytes
+    res = {"config": cfg, "kernel": prog.kernel}
+    host_in = None
+    if with_e2e:
+        x = make_input(wl, threads=16)
+        host_in = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+        host_in.numpy()[:] = x.reshape(-1).view("u1")
+        xd = host_in.to(dev)
+        del x
+    else:
+        xd = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        g = torch.Generator(device=dev).manual_seed(0)
+        xd.view(torch.int32).copy_(torch.randint(-2**31, 2**31 - 1, (nbytes // 4,), device=dev,
+                                                 dtype=torch.int32, generator=g))
+    yd = torch.empty_like(xd)
+    stream = torch.cuda.current_stream(dev)
+    flush = args._flusher
+    launch = lambda: execute_device(prog, xd, out=yd, stream=stream)  # noqa: E731
+    times = time_device(torch, launch, args.steps, args.warmup, flush, stream)
+    # sampled parity (2^20 random output positions through the closed-form
+    # bijection of core.py:173-178, in torch on device; tests/ hold the full
+    # oracle checks -- torch.permute itself is limited to 25 dims)
+    tdt = {"float32": torch.int32, "float64": torch.int64, "complex64": torch.int64}[wl.dtype]
+    res["parity_sampled"] = sample_parity(torch, xd.view(tdt), yd.view(tdt), wl.shape, wl.axes)
+    ms = sum(times) / len(times)
+    res["ms_per_launch"] = ms
+    res["ms_best"] = min(times)
+    res["gbs"] = wl.algorithmic_bytes / (ms * 1e-3) / 1e9
+    res["frac_of_hbm"] = res["gbs"] / peak
+    res["times_ms"] = times
+    res["algorithmic_bytes"] = wl.algorithmic_bytes
+    if with_e2e:
+        host_out = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+        e2e_t = []
+        for s in range(args.warmup + args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            out, _ = execute(prog, host_in, out=host_out)
+            t1 = time.perf_counter()
+            if s >= args.warmup:
+                e2e_t.append(t1 - t0)
+        res["e2e_s"] = sum(e2e_t) / len(e2e_t)
+        res["e2e_gbs"] = wl.algorithmic_bytes / res["e2e_s"] / 1e9
+        res["h2d_bytes"] = nbytes
+        res["d2h_bytes"] = nbytes
+    del xd, yd
+    torch.cuda.empty_cache()
+    return res
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=DEFAULT_CFG)
+    ap.add_argument("--no-extra", action="store_true", help="skip cfg1-4 side measurements")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-threads", type=int, default=None)
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        args.warmup = 3   # contract: W >= 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    peak, peak_kind = _peaks()
+    from paper_2506_03686_b200.workloads import CONFIGS
+
+    wl = CONFIGS[args.config]
+    base = {
+        "metric": "permute effective GB/s (read+write bytes/s)",
+        "unit": "GB/s",
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "c64 words (u64)" if wl.dtype == "complex64" else wl.dtype,
+        "data": "synthetic (seeded numpy PCG64, block-seeded; BASELINE.json cfg5 distribution)",
+    }
+    config = {
+        "workload": f"{args.config}: {wl.title}",
+        "shape": list(wl.shape),
+        "axes": list(wl.axes),
+        "elem_bytes": wl.elem_bytes,
+        "algorithmic_bytes_per_step": wl.algorithmic_bytes,
+        "parallelism": f"sharded{args.gpus}" if args.gpus > 1 else "single-gpu",
+        "l2_flush": "write 2xL2 + read 2xL2 before every timed step",
+    }
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        gbs, times, threads, target = run_reference_cpu(args.config, args.steps, args.warmup,
+                                                        threads=args.cpu_threads)
+        line = dict(base)
+        line.update({
+            "impl": "reference",
+            "value": gbs,
+            "ms_per_step": 1e3 * sum(times) / len(times),
+            "config": config,
+            "cpu_baseline": {
+                "value": gbs, "unit": "GB/s", "cores": threads, "kind": "reference",
+                "sample": f"{threads} concurrent full {args.config} permutations per step "
+                          f"(reference emitted {target} kernel, shared input, private outputs); "
+                          f"host {_cpu_model()}, {os.cpu_count()} logical CPUs",
+            },
+            "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        })
+        print(json.dumps(line), flush=True)
+        return 0
+
+    import torch
+
+    if world > 1:
+        from paper_2506_03686_b200 import sharded
+
+        return sharded.bench_main(args, torch, base, config, peak, peak_kind)
+
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    args._flusher = Flusher(torch, dev)
+    config["l2_bytes"] = args._flusher.l2
+    with ClockSampler(0) as clk:
+        main_res = bench_one_gpu(args, torch, args.config, True, peak)
+    extra = {}
+    if not args.no_extra:
+        for k in sorted(CONFIGS):
+            if k == args.config:
+                continue
+            r = bench_one_gpu(args, torch, k, False, peak)
+            extra[k] = {"gbs": round(r["gbs"], 1), "frac_of_hbm": round(r["frac_of_hbm"], 4),
+                        "us_per_launch": round(r["ms_per_launch"] * 1e3, 2), "kernel": r["kernel"],
+                        "parity_sampled": r["parity_sampled"]}
+    extra[args.config] = {"gbs": round(main_res["gbs"], 1), "frac_of_hbm": round(main_res["frac_of_hbm"], 4),
+                          "us_per_launch": round(main_res["ms_per_launch"] * 1e3, 2),
+                          "kernel": main_res["kernel"], "parity_sampled": main_res["parity_sampled"]}
+    cpu = None
+    if not args.no_cpu:
+        try:
+            gbs, times, threads, target = run_reference_cpu(args.config, 2, 1, threads=args.cpu_threads)
+            cpu = {"value": round(gbs, 2), "unit": "GB/s", "cores": threads, "kind": "reference",
+                   "sample": f"{threads} concurrent full {args.config} permutations x 2 timed steps "
+                             f"(reference emitted {target} kernel); host {_cpu_model()}"}
+        except Exception as e:  # reported, not fatal
+            cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+    ms = main_res["ms_per_launch"]
+    line = dict(base)
+    line.update({
+        "value": round(main_res["gbs"], 2),
+        "ms_per_step": ms,
+        "config": config,
+        "e2e": {"value": round(main_res["e2e_gbs"], 3), "unit": "GB/s",
+                "h2d_bytes_per_step": main_res["h2d_bytes"], "d2h_bytes_per_step": main_res["d2h_bytes"],
+                "api": "paper_2506_03686_b200.execute(program, pinned CPU tensor) -> vpg_permute_host"},
+        "gpu_launches": args.steps,
+        "roofline": {"bound": "hbm", "achieved": round(main_res["gbs"], 2), "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": round(main_res["gbs"] / peak, 4),
+                     "traffic": _traffic_from_profiles(args.config),
+                     "kernel": f"{main_res['kernel']} ({args.config})"},
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+        "parity_sampled": main_res["parity_sampled"],
+        "configs": extra,
+    })
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

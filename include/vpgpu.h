@@ -1,0 +1,131 @@
+/*
+ * vpgpu.h -- C ABI of the B200 (sm_100a) N-D tensor permutation library
+ * (libvpgpu.so).  Drop-in boundary for the permutation hot path of the
+ * reference package `vecperm` (/root/reference/pkg).
+ *
+ * Conventions (identical to the reference, core.py:1-7):
+ *   - dims are innermost-first: dims[0] is the stride-1 dimension;
+ *   - sigma[j] is the SOURCE dim that lands at DESTINATION position j
+ *     (inner-first), so the output's innermost dim is source dim sigma[0];
+ *   - output layout: out.dims[j] = dims[sigma[j]], dense (core.py:128-132);
+ *   - bijection: out[i] = in[f(i)] (core.py:173-178, 192-204);
+ *   - elements are opaque words of elem_bytes bytes.  The reference accepts
+ *     4 and 8 (core.py:29); this library accepts 1, 2, 4, 8 and 16.
+ *
+ * Buffers are DEVICE pointers owned by the caller (e.g. torch tensors).
+ * The library never allocates tensor memory.  src and dst must not overlap
+ * (out-of-place only, as the reference).  Unlike the reference's emitted
+ * kernels (emit.py:5-8) there is NO slack requirement past either buffer.
+ *
+ * Threading: plans are immutable after creation and may be shared between
+ * host threads; vpg_permute may be called concurrently on distinct streams.
+ * vpg_last_error() is thread-local.
+ */
+#ifndef VPGPU_H
+#define VPGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VPG_ABI_VERSION 1
+#define VPG_MAX_RANK 64
+
+typedef enum {
+    VPG_OK = 0,
+    VPG_EINVAL = 1,        /* bad layout / map / buffer: maps to LayoutError (core.py:32-33) */
+    VPG_EUNSUPPORTED = 2,  /* valid request the library cannot serve (e.g. > 2^32 tiles)     */
+    VPG_ECUDA = 3,         /* CUDA runtime error: maps to RuntimeError                         */
+    VPG_ENOMEM = 4
+} vpg_status;
+
+/* Kernel classes chosen by the planner. */
+typedef enum {
+    VPG_KERNEL_COPY = 0,     /* merged to rank 1: vectorised flat copy                      */
+    VPG_KERNEL_ROWS = 1,     /* K1: stride-1 preserved, long rows: 128-bit copy-with-remap  */
+    VPG_KERNEL_TILE = 2,     /* K2/K3: smem-staged tile transpose over merged/odd dims      */
+    VPG_KERNEL_GATHER = 3    /* K0: per-element gather (tiny tensors / forced)              */
+} vpg_kernel_class;
+
+typedef struct vpg_plan vpg_plan;   /* opaque, immutable */
+
+/* Summary of a plan (the format_plan / IRProgram.metadata analog,
+ * planner.py:386-419, ir.py:96-108). */
+typedef struct {
+    int32_t kernel_class;           /* vpg_kernel_class */
+    int32_t elem_bytes;
+    int32_t rank;                   /* after merge_dimensions */
+    int64_t dims[VPG_MAX_RANK];     /* merged dims, inner-first */
+    int32_t sigma[VPG_MAX_RANK];    /* merged sigma, inner-first */
+    int64_t num_elements;
+    /* TILE: tile geometry */
+    int64_t tile_elems;             /* elements in one full tile */
+    int64_t src_run;                /* contiguous source run (elements) */
+    int64_t dst_run;                /* contiguous destination run (elements) */
+    int64_t num_tiles;
+    int32_t smem_pitch;             /* padded source-run pitch in smem (elements) */
+    int32_t smem_bytes;             /* dynamic shared memory per CTA */
+    /* ROWS/COPY: vector width in elements; TILE: 1 */
+    int32_t vec_elems;
+    int32_t threads;                /* CTA size */
+    int64_t grid_hint;              /* CTAs launched when the device has 148 SMs */
+    double  predicted_efficiency;   /* planner's sector-efficiency estimate, 0..1 */
+} vpg_plan_info;
+
+/* Library ABI version (VPG_ABI_VERSION). */
+int vpg_version(void);
+
+/* Thread-local message for the last non-OK status on this thread. */
+const char *vpg_last_error(void);
+
+/* Replaces vecperm.planner.merge_dimensions (planner.py:211-241): drops
+ * size-1 dims and fuses adjacent dims whose adjacency and order survive the
+ * map.  out_dims/out_sigma must hold `rank` entries. */
+vpg_status vpg_merge_dimensions(int rank, const int64_t *dims, const int32_t *sigma,
+                                int *out_rank, int64_t *out_dims, int32_t *out_sigma);
+
+/* Replaces vecperm.ir.build_program (ir.py:441-456): merge + classify +
+ * tile selection for (shape, map, element width).  Host-only; needs no GPU.
+ * `flags`: 0 = planner's choice; VPG_FORCE_* to pin a kernel class (tests). */
+#define VPG_FORCE_GATHER 0x1
+#define VPG_FORCE_TILE   0x2
+#define VPG_NO_MERGE     0x4
+vpg_status vpg_plan_create(int rank, const int64_t *dims_inner_first,
+                           const int32_t *sigma_inner_first, int elem_bytes,
+                           unsigned flags, vpg_plan **out);
+
+/* Replaces the emitted kernel `void permute_<hash>(const void *src, void *dst)`
+ * (emit.py:118-128, 212-266) and the VM's execute (vm.py:105-110):
+ * dst = permute(src) on device memory, asynchronously on `cuda_stream`
+ * (a cudaStream_t; NULL = legacy default stream). */
+vpg_status vpg_permute(const vpg_plan *plan, const void *src, void *dst, void *cuda_stream);
+
+/* End-to-end variant over HOST buffers (the reference's execute() takes a host
+ * buffer, vm.py:105-110): copies host_src -> dev_src, permutes into dev_dst,
+ * copies dev_dst -> host_dst, all on `cuda_stream`; synchronises the stream
+ * before returning.  Device buffers are caller-provided scratch of
+ * num_elements*elem_bytes bytes each.  Pinned host memory gives full-rate copies. */
+vpg_status vpg_permute_host(const vpg_plan *plan, const void *host_src, void *host_dst,
+                            void *dev_src, void *dev_dst, void *cuda_stream);
+
+/* One-shot convenience with an internal plan cache keyed by
+ * (dims, sigma, elem_bytes): the closest analog of the reference's
+ * shape-specialised kernel call. */
+vpg_status vpg_permute_nd(int rank, const int64_t *dims_inner_first,
+                          const int32_t *sigma_inner_first, int elem_bytes,
+                          const void *src, void *dst, void *cuda_stream);
+
+/* Plan inspection (format_plan analog, planner.py:386-419). */
+vpg_status vpg_plan_info_get(const vpg_plan *plan, vpg_plan_info *info);
+vpg_status vpg_plan_describe(const vpg_plan *plan, char *buf, size_t len);
+
+void vpg_plan_destroy(vpg_plan *plan);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VPGPU_H */

@@ -1,0 +1,363 @@
+"""Public plan / permute API -- the drop-in for vecperm's hot path.
+
+Reference boundary (pkg/src/vecperm/__init__.py:3-34; README "Library in
+five lines"):
+
+    ir = build_program(layout, pmap, machine)        # ir.py:441-456
+    out, counters = execute(ir, input_buf)           # vm.py:105-110
+
+Here ``build_program`` calls the native planner in libvpgpu.so (merge +
+classify + tile selection) and returns an immutable :class:`GpuProgram`;
+``execute`` runs it on the B200 through the C ABI.  ``permute(x, axes)`` is
+the torch-convention convenience (``out = x.permute(axes).contiguous()``).
+
+There is no CPU fallback: every element move is a CUDA kernel launch in
+libvpgpu.so; host buffers given to ``execute`` are staged through device
+memory (that is the end-to-end path the bench times).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .core import (
+    LayoutError,
+    PermutationMap,
+    TensorLayout,
+    from_numpy_convention,
+    permuted_layout,
+)
+
+__all__ = [
+    "GpuTarget",
+    "GpuProgram",
+    "VpgError",
+    "merge_dimensions",
+    "build_program",
+    "execute",
+    "permute",
+    "format_plan",
+    "program_cache_clear",
+]
+
+
+class VpgError(RuntimeError):
+    """CUDA-side failure (VPG_ECUDA / VPG_ENOMEM)."""
+
+
+def _check(status: int, what: str):
+    if status == _lib.VPG_OK:
+        return
+    msg = f"{what}: {_lib.last_error()}"
+    if status in (_lib.VPG_EINVAL,):
+        raise LayoutError(msg)
+    if status == _lib.VPG_EUNSUPPORTED:
+        raise LayoutError("unsupported: " + msg)
+    raise VpgError(msg)
+
+
+@dataclass(frozen=True)
+class GpuTarget:
+    """GPU target descriptor (the MachineConfig analog, machine.py:13-40).
+
+    The planner is device-agnostic (plans are POD kernel arguments); the
+    descriptor records what the numbers in DESIGN.md assume.
+    """
+
+    name: str = "B200"
+    arch: str = "sm_100a"
+    sms: int = 148
+    smem_per_sm: int = 228 * 1024
+    hbm_gbs: float = 6542.7      # MEASURED_PEAKS.json (copy, read+write)
+
+
+# ------------------------------------------------------------------ merge
+def merge_dimensions(layout: TensorLayout, pmap: PermutationMap):
+    """Fuse adjacent dims whose adjacency and order survive the map.
+
+    Same contract as planner.py:211-241 (size-1 dims dropped first; the
+    element bijection is preserved); computed by the native planner.
+    """
+    if pmap.rank != layout.rank:
+        raise LayoutError("map rank does not match layout rank")
+    L = _lib.lib()
+    rank, d, s = _lib.arrays(layout.dims, pmap.sigma)
+    od = (ctypes.c_int64 * rank)()
+    os_ = (ctypes.c_int32 * rank)()
+    orank = ctypes.c_int(0)
+    _check(L.vpg_merge_dimensions(rank, d, s, ctypes.byref(orank), od, os_), "merge_dimensions")
+    r = orank.value
+    return TensorLayout(tuple(od[:r]), layout.elem_width), PermutationMap(tuple(os_[:r]))
+
+
+# ------------------------------------------------------------------ program
+class _Handle:
+    """Owns one vpg_plan*; destroyed with the program."""
+
+    __slots__ = ("ptr",)
+
+    def __init__(self, ptr):
+        self.ptr = ptr
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                _lib.lib().vpg_plan_destroy(self.ptr)
+                self.ptr = None
+        except Exception:
+            pass
+
+
+@dataclass(frozen=True)
+class GpuProgram:
+    """Immutable, shareable plan (the IRProgram analog, ir.py:96-108)."""
+
+    layout: TensorLayout
+    pmap: PermutationMap
+    merged_layout: TensorLayout
+    merged_pmap: PermutationMap
+    kernel: str
+    metadata: dict = field(compare=False)
+    text: str = field(compare=False)
+    _handle: _Handle = field(compare=False, repr=False)
+
+    @property
+    def num_elements(self) -> int:
+        return self.layout.num_elements
+
+    @property
+    def out_layout(self) -> TensorLayout:
+        return permuted_layout(self.layout, self.pmap)
+
+    @property
+    def nbytes(self) -> int:
+        return self.layout.num_elements * self.layout.elem_width
+
+    @property
+    def algorithmic_bytes(self) -> int:
+        """One read + one write per element."""
+        return 2 * self.nbytes
+
+    @property
+    def handle(self) -> int:
+        return self._handle.ptr
+
+
+_cache: dict = {}
+_cache_lock = threading.Lock()
+
+
+def program_cache_clear():
+    with _cache_lock:
+        _cache.clear()
+
+
+def build_program(layout: TensorLayout, pmap: PermutationMap, machine=None, merge: bool = True,
+                  opt: bool = True, force: str | None = None) -> GpuProgram:
+    """Plan a permutation (ir.py:441-456 signature; ``machine``/``opt`` kept
+    for drop-in compatibility).
+
+    ``force`` pins a kernel class for tests: ``"tile"`` or ``"gather"``.
+    """
+    if pmap.rank != layout.rank:
+        raise LayoutError("map rank does not match layout rank")
+    if machine is not None and hasattr(machine, "elem_width") and machine.elem_width != layout.elem_width:
+        raise LayoutError("layout and machine element widths differ")   # planner.py:307-308
+    flags = 0
+    if not merge:
+        flags |= _lib.VPG_NO_MERGE
+    if force == "tile":
+        flags |= _lib.VPG_FORCE_TILE
+    elif force == "gather":
+        flags |= _lib.VPG_FORCE_GATHER
+    elif force is not None:
+        raise ValueError(f"unknown force={force!r}")
+    key = (layout.dims, layout.elem_width, pmap.sigma, flags)
+    with _cache_lock:
+        hit = _cache.get(key)
+    if hit is not None:
+        return hit
+    L = _lib.lib()
+    rank, d, s = _lib.arrays(layout.dims, pmap.sigma)
+    ptr = ctypes.c_void_p()
+    _check(L.vpg_plan_create(rank, d, s, layout.elem_width, flags, ctypes.byref(ptr)), "build_program")
+    handle = _Handle(ptr)
+    info = _lib.PlanInfo()
+    _check(L.vpg_plan_info_get(ptr, ctypes.byref(info)), "plan_info")
+    buf = ctypes.create_string_buffer(4096)
+    _check(L.vpg_plan_describe(ptr, buf, 4096), "plan_describe")
+    r = info.rank
+    merged_layout = TensorLayout(tuple(info.dims[:r]), layout.elem_width)
+    merged_pmap = PermutationMap(tuple(info.sigma[:r]))
+    kernel = _lib.KERNEL_NAMES[info.kernel_class]
+    meta = {
+        "kernel": kernel,
+        "merged_dims": merged_layout.dims,
+        "merged_sigma": merged_pmap.sigma,
+        "tile_elems": info.tile_elems,
+        "src_run": info.src_run,
+        "dst_run": info.dst_run,
+        "num_tiles": info.num_tiles,
+        "smem_pitch": info.smem_pitch,
+        "smem_bytes": info.smem_bytes,
+        "vec_elems": info.vec_elems,
+        "threads": info.threads,
+        "grid_hint": info.grid_hint,
+        "predicted_efficiency": info.predicted_efficiency,
+        "source_shape": layout.dims,
+        "source_map": pmap.sigma,
+    }
+    prog = GpuProgram(layout, pmap, merged_layout, merged_pmap, kernel, meta,
+                      buf.value.decode(), handle)
+    with _cache_lock:
+        _cache.setdefault(key, prog)
+        return _cache[key]
+
+
+def format_plan(program: GpuProgram) -> str:
+    """Human-readable plan dump (format_plan analog, planner.py:386-419)."""
+    return program.text
+
+
+# ------------------------------------------------------------------ execute
+def _torch():
+    import torch
+
+    return torch
+
+
+def _stream_ptr(torch, device, stream):
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _launch(program: GpuProgram, src_ptr: int, dst_ptr: int, stream_ptr) -> None:
+    st = _lib.lib().vpg_permute(program.handle, ctypes.c_void_p(src_ptr), ctypes.c_void_p(dst_ptr), stream_ptr)
+    _check(st, "permute")
+
+
+def _counters(program: GpuProgram) -> dict:
+    c = dict(program.metadata)
+    c["launches"] = 1 if program.num_elements > 0 else 0
+    c["bytes_read"] = program.nbytes
+    c["bytes_written"] = program.nbytes
+    return c
+
+
+def execute_device(program: GpuProgram, x, out=None, stream=None):
+    """Permute a CUDA tensor (any dtype whose itemsize is the element width).
+
+    Returns a tensor shaped like the output layout (outer-first)."""
+    torch = _torch()
+    if not isinstance(x, torch.Tensor) or not x.is_cuda:
+        raise LayoutError("execute_device needs a CUDA tensor")
+    if x.element_size() != program.layout.elem_width and not (
+            x.dtype == torch.uint8 and x.numel() == program.nbytes):
+        raise LayoutError(f"tensor itemsize {x.element_size()} != element width {program.layout.elem_width}")
+    if x.numel() * x.element_size() != program.nbytes:
+        raise LayoutError(f"tensor holds {x.numel()} elements, program expects {program.num_elements}")
+    if not x.is_contiguous():
+        raise LayoutError("input tensor must be contiguous (dense layout)")
+    shape = program.out_layout.shape_outer_first()
+    if out is None:
+        if x.element_size() == program.layout.elem_width:
+            out = torch.empty(shape, dtype=x.dtype, device=x.device)
+        else:
+            out = torch.empty(program.nbytes, dtype=torch.uint8, device=x.device)
+    else:
+        if not out.is_cuda or not out.is_contiguous() or out.numel() * out.element_size() != program.nbytes:
+            raise LayoutError("out must be a contiguous CUDA tensor of the output size")
+        if out.device != x.device:
+            raise LayoutError("out must be on the input's device")
+    if program.num_elements == 0:
+        return out
+    if out.data_ptr() == x.data_ptr():
+        raise LayoutError("out-of-place only: out aliases the input")
+    with torch.cuda.device(x.device):
+        _launch(program, x.data_ptr(), out.data_ptr(), _stream_ptr(torch, x.device, stream))
+    return out
+
+
+def execute(program: GpuProgram, input_buf, trace: bool = False, out=None, stream=None):
+    """Run a program; returns ``(output, counters)`` like vm.py:105-110.
+
+    * CUDA tensor input -> CUDA output tensor (outer-first output shape).
+    * numpy array / bytes / CPU tensor input -> staged through device memory
+      (H2D copy, kernel, D2H copy); returns a flat numpy array of opaque
+      words (``program.layout.dtype``) like the reference, or a CPU tensor
+      for a CPU-tensor input.
+    """
+    torch = _torch()
+    if isinstance(input_buf, torch.Tensor) and input_buf.is_cuda:
+        res = execute_device(program, input_buf, out=out, stream=stream)
+        return res, _counters(program)
+    return _execute_host(program, input_buf, out=out, stream=stream), _counters(program)
+
+
+def _execute_host(program: GpuProgram, input_buf, out=None, stream=None):
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise VpgError("no CUDA device: the permutation runs only on the GPU (no CPU fallback)")
+    lay = program.layout
+    as_tensor = isinstance(input_buf, torch.Tensor)
+    if as_tensor:
+        host = input_buf.contiguous().reshape(-1)
+        if host.numel() * host.element_size() != program.nbytes:
+            raise LayoutError(f"input holds {host.numel()} elements, program expects {program.num_elements}")
+        hbytes = host.view(torch.uint8)
+    else:
+        if isinstance(input_buf, (bytes, bytearray, memoryview)):
+            data = np.frombuffer(input_buf, dtype=np.uint8)
+        else:
+            data = np.ascontiguousarray(input_buf).reshape(-1).view(np.uint8)
+        if data.size != program.nbytes:
+            raise LayoutError(f"input holds {data.size // lay.elem_width} elements, "
+                              f"program expects {program.num_elements}")
+        hbytes = torch.from_numpy(data.copy() if not data.flags.writeable else data)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    d_in = torch.empty(program.nbytes, dtype=torch.uint8, device=dev)
+    d_out = torch.empty(program.nbytes, dtype=torch.uint8, device=dev)
+    if out is None:
+        h_out = torch.empty(program.nbytes, dtype=torch.uint8, pin_memory=hbytes.is_pinned())
+    else:
+        h_out = out.reshape(-1).view(torch.uint8)
+    if program.num_elements:
+        st = torch.cuda.current_stream(dev) if stream is None else stream
+        status = _lib.lib().vpg_permute_host(
+            program.handle, ctypes.c_void_p(hbytes.data_ptr()), ctypes.c_void_p(h_out.data_ptr()),
+            ctypes.c_void_p(d_in.data_ptr()), ctypes.c_void_p(d_out.data_ptr()),
+            ctypes.c_void_p(st.cuda_stream))
+        _check(status, "permute_host")
+    if as_tensor:
+        res = h_out.view(input_buf.dtype) if out is None else out
+        return res.reshape(program.out_layout.shape_outer_first()) if out is None else res
+    return h_out.numpy().view(lay.dtype)
+
+
+# ------------------------------------------------------------------ permute
+def permute(x, axes, out=None, stream=None):
+    """``x.permute(axes).contiguous()`` on the GPU through libvpgpu.so.
+
+    ``x`` is a contiguous CUDA tensor; ``axes`` use the torch/numpy
+    convention (BASELINE.json's configs are stated this way)."""
+    torch = _torch()
+    if not isinstance(x, torch.Tensor) or not x.is_cuda:
+        raise LayoutError("permute needs a CUDA tensor (no CPU fallback)")
+    axes = tuple(int(a) for a in axes)
+    if len(axes) != x.dim():
+        raise LayoutError(f"axes {axes} do not match tensor rank {x.dim()}")
+    if x.numel() == 0:                       # nothing to move
+        shape = tuple(x.shape[a] for a in axes)
+        return torch.empty(shape, dtype=x.dtype, device=x.device) if out is None else out
+    if x.dim() == 0:
+        res = permute(x.reshape(1), (0,), stream=stream).reshape(())
+        return res if out is None else out.copy_(res)
+    layout = TensorLayout.from_shape(tuple(x.shape), x.element_size())
+    prog = build_program(layout, from_numpy_convention(axes))
+    return execute_device(prog, x, out=out, stream=stream)

@@ -1,0 +1,164 @@
+// capi.cpp -- the extern "C" boundary of libvpgpu.so (declared in
+// include/vpgpu.h).  Plain pointers and sizes only; no torch types.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "plan.h"
+
+namespace vpg {
+int merge_dims(int rank, const int64_t *dims, const int32_t *sigma, int64_t *od, int32_t *os);
+vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E, unsigned flags,
+                     vpg_plan **out, std::string *err);
+}  // namespace vpg
+
+namespace {
+thread_local std::string t_err;
+
+vpg_status fail(vpg_status s, const std::string &msg) {
+    t_err = msg;
+    return s;
+}
+
+std::mutex g_cache_mu;
+std::map<std::vector<int64_t>, vpg_plan *> g_cache;  // never freed (process lifetime)
+}  // namespace
+
+extern "C" {
+
+int vpg_version(void) { return VPG_ABI_VERSION; }
+
+const char *vpg_last_error(void) { return t_err.c_str(); }
+
+vpg_status vpg_merge_dimensions(int rank, const int64_t *dims, const int32_t *sigma, int *out_rank,
+                                int64_t *out_dims, int32_t *out_sigma) {
+    if (!dims || !sigma || !out_rank || !out_dims || !out_sigma)
+        return fail(VPG_EINVAL, "null argument");
+    if (rank < 1 || rank > VPG_MAX_RANK) return fail(VPG_EINVAL, "rank out of range");
+    std::vector<int> seen(rank, 0);
+    for (int k = 0; k < rank; ++k) {
+        if (dims[k] < 1) return fail(VPG_EINVAL, "dimension is not positive");
+        if (sigma[k] < 0 || sigma[k] >= rank || seen[sigma[k]])
+            return fail(VPG_EINVAL, "map is not a bijection");
+        seen[sigma[k]] = 1;
+    }
+    *out_rank = vpg::merge_dims(rank, dims, sigma, out_dims, out_sigma);
+    return VPG_OK;
+}
+
+vpg_status vpg_plan_create(int rank, const int64_t *dims, const int32_t *sigma, int elem_bytes,
+                           unsigned flags, vpg_plan **out) {
+    if (!dims || !sigma || !out) return fail(VPG_EINVAL, "null argument");
+    std::string err;
+    vpg_status s = vpg::make_plan(rank, dims, sigma, elem_bytes, flags, out, &err);
+    if (s != VPG_OK) return fail(s, err);
+    return VPG_OK;
+}
+
+vpg_status vpg_permute(const vpg_plan *plan, const void *src, void *dst, void *cuda_stream) {
+    if (!plan) return fail(VPG_EINVAL, "null plan");
+    if (plan->n > 0 && (!src || !dst)) return fail(VPG_EINVAL, "null buffer");
+    if (src == dst && plan->n > 0) return fail(VPG_EINVAL, "src and dst must not overlap (out-of-place only)");
+    std::string err;
+    vpg_status s = vpg::launch_plan(plan, src, dst, cuda_stream, &err);
+    if (s != VPG_OK) return fail(s, err);
+    return VPG_OK;
+}
+
+vpg_status vpg_permute_host(const vpg_plan *plan, const void *host_src, void *host_dst, void *dev_src,
+                            void *dev_dst, void *cuda_stream) {
+    if (!plan || !host_src || !host_dst || !dev_src || !dev_dst) return fail(VPG_EINVAL, "null argument");
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    size_t nbytes = (size_t)plan->n * plan->elem_bytes;
+    cudaError_t e = cudaMemcpyAsync(dev_src, host_src, nbytes, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return fail(VPG_ECUDA, std::string("H2D copy: ") + cudaGetErrorString(e));
+    vpg_status s = vpg_permute(plan, dev_src, dev_dst, cuda_stream);
+    if (s != VPG_OK) return s;
+    e = cudaMemcpyAsync(host_dst, dev_dst, nbytes, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return fail(VPG_ECUDA, std::string("D2H copy: ") + cudaGetErrorString(e));
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return fail(VPG_ECUDA, std::string("stream sync: ") + cudaGetErrorString(e));
+    return VPG_OK;
+}
+
+vpg_status vpg_permute_nd(int rank, const int64_t *dims, const int32_t *sigma, int elem_bytes,
+                          const void *src, void *dst, void *cuda_stream) {
+    if (!dims || !sigma) return fail(VPG_EINVAL, "null argument");
+    if (rank < 1 || rank > VPG_MAX_RANK) return fail(VPG_EINVAL, "rank out of range");
+    std::vector<int64_t> key;
+    key.reserve(2 * rank + 2);
+    key.push_back(rank);
+    key.push_back(elem_bytes);
+    for (int k = 0; k < rank; ++k) key.push_back(dims[k]);
+    for (int k = 0; k < rank; ++k) key.push_back(sigma[k]);
+    vpg_plan *p = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        auto it = g_cache.find(key);
+        if (it != g_cache.end()) p = it->second;
+    }
+    if (!p) {
+        vpg_status s = vpg_plan_create(rank, dims, sigma, elem_bytes, 0, &p);
+        if (s != VPG_OK) return s;
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        auto ins = g_cache.emplace(key, p);
+        if (!ins.second) {
+            vpg_plan_destroy(p);
+            p = ins.first->second;
+        }
+    }
+    return vpg_permute(p, src, dst, cuda_stream);
+}
+
+vpg_status vpg_plan_info_get(const vpg_plan *p, vpg_plan_info *info) {
+    if (!p || !info) return fail(VPG_EINVAL, "null argument");
+    memset(info, 0, sizeof(*info));
+    info->kernel_class = p->kernel_class;
+    info->elem_bytes = p->elem_bytes;
+    info->rank = p->rank;
+    for (int k = 0; k < p->rank; ++k) {
+        info->dims[k] = p->dims[k];
+        info->sigma[k] = p->sigma[k];
+    }
+    info->num_elements = p->n;
+    info->threads = p->threads;
+    info->grid_hint = p->grid_hint;
+    info->predicted_efficiency = p->predicted_eff;
+    if (p->kernel_class == VPG_KERNEL_TILE) {
+        info->tile_elems = p->tile.T;
+        info->src_run = p->tile.Ls;
+        info->dst_run = p->tile.Ld;
+        info->num_tiles = p->tile.num_tiles;
+        info->smem_pitch = (int32_t)p->tile.pitch;
+        info->smem_bytes = (int32_t)p->tile.smem_bytes;
+        info->vec_elems = 1;
+    } else if (p->kernel_class == VPG_KERNEL_ROWS) {
+        info->src_run = p->rows.row_len;
+        info->dst_run = p->rows.row_len;
+        info->vec_elems = (int32_t)p->rows.vec;
+        info->num_tiles = p->rows.nrows;
+    } else if (p->kernel_class == VPG_KERNEL_COPY) {
+        info->src_run = info->dst_run = p->n;
+        info->vec_elems = 16 / p->elem_bytes > 0 ? 16 / p->elem_bytes : 1;
+    } else {
+        info->src_run = info->dst_run = 1;
+        info->vec_elems = 1;
+    }
+    return VPG_OK;
+}
+
+vpg_status vpg_plan_describe(const vpg_plan *p, char *buf, size_t len) {
+    if (!p || !buf || len == 0) return fail(VPG_EINVAL, "null argument");
+    size_t n = std::min(len - 1, p->text.size());
+    memcpy(buf, p->text.data(), n);
+    buf[n] = 0;
+    return VPG_OK;
+}
+
+void vpg_plan_destroy(vpg_plan *p) { delete p; }
+
+}  // extern "C"

@@ -1,0 +1,157 @@
+// plan.h -- internal plan representation shared by the host planner
+// (planner.cpp) and the sm_100a kernels (kernels.cu).
+//
+// A plan is the GPU analog of the reference's BlockPlan + IRProgram
+// (/root/reference/pkg/src/vecperm/planner.py:86-201, ir.py:96-108): it
+// carries the merged problem, the kernel class and a POD parameter block
+// that is passed BY VALUE as the kernel argument (no device-side plan
+// memory, so a plan is valid on every device and needs no GPU to build).
+#pragma once
+
+#include <stdint.h>
+#include <string>
+
+#include "vpgpu.h"
+
+namespace vpg {
+
+// Merged ranks are bounded by log2(numel) since size-1 dims are dropped:
+// 40 covers any tensor that fits in HBM (2^40 elements).
+constexpr int kMaxRank = 40;
+// Dims inside one tile (each >= 2 after merge, tile <= 2^14 elements).
+constexpr int kMaxTileDims = 16;
+
+// Division by a run-time invariant 32-bit divisor via multiply-high
+// (round-up method): q = (umulhi(n, m) + n) >> s, exact for all n < 2^32.
+struct FastDiv {
+    uint32_t d;
+    uint32_t m;
+    uint32_t s;
+};
+
+inline FastDiv make_fastdiv(uint32_t d) {
+    uint32_t l = 0;
+    while (l < 32 && (1ull << l) < d) ++l;
+    uint64_t m = (((1ull << 32) * ((1ull << l) - d)) / d) + 1;
+    FastDiv f;
+    f.d = d;
+    f.m = (uint32_t)m;
+    f.s = l;
+    return f;
+}
+
+inline uint32_t host_fastdiv(uint32_t n, FastDiv f) {
+    uint64_t t = ((uint64_t)n * f.m) >> 32;
+    return (uint32_t)((t + n) >> f.s);
+}
+
+// --------------------------------------------------------------------------
+// TILE (K2/K3) parameters.
+//
+// The tile is a sub-box of the merged tensor made of
+//   * the source run: dims 0..s-1 in source order, the last possibly
+//     partial (extent e < d): one contiguous source range of Ls elements;
+//   * the destination run: dims sigma[0..t-1], the last possibly partial:
+//     one contiguous destination range of Ld elements;
+//   * the union of both (the tile).  Tile elements are staged in shared
+//     memory in source order with the run pitch padded to kill bank
+//     conflicts on the transposed side.
+// The remaining dims (and the tile positions along partial dims) form the
+// grid digits, ordered by destination stride (fastest first) like the
+// reference's counter digits (planner.py:324-342).
+struct TableDim {
+    uint32_t extent;     // tile extent along this dim
+    FastDiv div;         // divides by extent
+    int64_t gstride;     // global stride (src for S dims, dst for W dims) in elements
+    uint32_t sstride;    // shared-memory stride in elements
+    uint32_t pad_;
+};
+
+struct GridDigit {
+    FastDiv cum;         // divides tile index by the product of faster digits
+    FastDiv ext;         // divides by this digit's extent
+    int64_t src_stride;  // elements, already multiplied by the tile extent
+    int64_t dst_stride;
+};
+
+struct TileParams {
+    uint32_t num_tiles;
+    int32_t ngrid;
+    uint32_t Ls, Ns;           // source run length / number of source runs per tile
+    uint32_t Ld, Nd;           // destination run length / number of destination runs
+    uint32_t T;                // tile elements (= Ls*Ns = Ld*Nd)
+    uint32_t pitch;            // smem pitch of one source run (elements, >= Ls)
+    uint32_t Ls_unit, Ld_unit; // Ls / e_a, Ld / e_c (elements per step of a partial boundary dim)
+    // ragged boundary dims: a = source-run boundary, c = destination-run boundary
+    int32_t grid_a, grid_c;    // grid digit carrying the tile position along a / c (-1: not partial)
+    uint32_t e_a, d_a, e_c, d_c;
+    int32_t s_c_dim;           // index into S[] of dim c when c is a source run-index dim, else -1
+    int32_t w_a_dim;           // index into W[] of dim a when a is a destination run-index dim, else -1
+    int32_t nS, nA, nW;
+    TableDim S[kMaxTileDims];  // source run-index dims (source order): gstride = src stride
+    TableDim A[kMaxTileDims];  // destination-run dims (dest order): sstride only
+    TableDim W[kMaxTileDims];  // destination run-index dims (dest order): gstride = dst stride
+    GridDigit grid[kMaxRank];
+    // dynamic smem layout (byte offsets)
+    uint32_t off_S_off, off_S_c, off_W_off, off_W_sm, off_W_a, off_A, off_tile;
+    uint32_t smem_bytes;
+};
+
+// --------------------------------------------------------------------------
+// ROWS (K1): stride-1 preserved; each destination row of Lr elements is a
+// contiguous source row.  Row q (destination order) starts at q*Lr in dst
+// and at sum_j digit_j(q) * in_stride[sigma[j]] in src.
+struct RowDigit {
+    FastDiv ext;
+    int64_t src_stride;
+};
+
+struct RowsParams {
+    uint32_t nrows;
+    uint32_t row_vecs;         // Lr / V
+    uint32_t vec;              // V: elements per vector
+    uint32_t tpr_log2;         // threads per row group (log2)
+    int64_t row_len;           // Lr (elements)
+    int32_t ndig;
+    RowDigit dig[kMaxRank];    // destination dims 1..r-1, fastest first
+};
+
+// --------------------------------------------------------------------------
+// COPY: merged to rank 1.
+struct CopyParams {
+    int64_t n;                 // elements
+};
+
+// --------------------------------------------------------------------------
+// GATHER (K0): out[i] = in[f(i)], per element (core.py:173-178).
+struct GatherParams {
+    uint32_t n;
+    int32_t rank;
+    FastDiv ext[kMaxRank];     // destination dims, fastest first
+    int64_t src_stride[kMaxRank];
+};
+
+}  // namespace vpg
+
+struct vpg_plan {
+    int32_t kernel_class;      // vpg_kernel_class
+    int32_t elem_bytes;
+    int32_t rank;              // merged
+    int64_t dims[VPG_MAX_RANK];
+    int32_t sigma[VPG_MAX_RANK];
+    int64_t n;
+    int32_t threads;
+    int64_t grid_hint;
+    double predicted_eff;
+    vpg::TileParams tile;
+    vpg::RowsParams rows;
+    vpg::CopyParams copy;
+    vpg::GatherParams gather;
+    std::string text;          // describe() output
+};
+
+namespace vpg {
+// kernels.cu
+vpg_status launch_plan(const vpg_plan *p, const void *src, void *dst, void *stream, std::string *err);
+int device_sm_count();
+}  // namespace vpg

@@ -1,0 +1,624 @@
+// planner.cpp -- host-side planner for the B200 permutation kernels.
+//
+// GPU analog of the reference's planning layer:
+//   merge_dimensions   /root/reference/pkg/src/vecperm/planner.py:211-241 (verbatim semantics)
+//   select_block       planner.py:277-352 (re-done at GPU scale: tiles of KBs,
+//                      not w <= 16 lanes; no power-of-two padding)
+//   BlockPlan.phases   planner.py:178-201 (ragged tiles are predicated in-kernel
+//                      instead of separate main/tail loops)
+//   format_plan        planner.py:386-419 (vpg_plan_describe)
+//
+// Classification:
+//   merged rank 1                         -> COPY
+//   sigma[0] == 0 and row >= 512 B        -> ROWS (K1, 128-bit copy-with-remap)
+//   everything else                       -> TILE (K2/K3: smem-staged tile)
+//   tiny tensors                          -> GATHER (K0)
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "plan.h"
+
+namespace vpg {
+
+namespace {
+
+constexpr int kTileThreads = 256;
+constexpr int64_t kGatherMaxN = 1024;
+constexpr int64_t kRowsMinBytes = 512;
+constexpr double kRunOverheadBytes = 32.0;   // cost of starting one contiguous run
+constexpr double kTileOverheadBytes = 2048.0;  // cost of one tile (decode + 2 barriers)
+constexpr int64_t kTileBudgetBytes = 48 * 1024;  // staged elements per CTA
+
+int64_t gcd64(int64_t a, int64_t b) {
+    a = a < 0 ? -a : a;
+    b = b < 0 ? -b : b;
+    while (b) {
+        int64_t t = a % b;
+        a = b;
+        b = t;
+    }
+    return a;
+}
+
+// Expected 32-byte sectors touched by a run of `bytes` whose start is a
+// multiple of `align` bytes, uniformly distributed modulo 32.
+double expected_sectors(int64_t bytes, int64_t align) {
+    if (align >= 32 || align <= 0) return (double)((bytes + 31) / 32);
+    int64_t cnt = 0, tot = 0;
+    for (int64_t o = 0; o < 32; o += align) {
+        tot += (o + bytes + 31) / 32;
+        ++cnt;
+    }
+    return (double)tot / (double)cnt;
+}
+
+struct Problem {
+    int r;
+    int64_t d[kMaxRank];
+    int sigma[kMaxRank];
+    int pos[kMaxRank];
+    int64_t in_stride[kMaxRank];
+    int64_t out_stride_of_dim[kMaxRank];  // destination stride of source dim k
+    int E;
+    int64_t n;
+};
+
+void fill_problem(Problem &P) {
+    for (int j = 0; j < P.r; ++j) P.pos[P.sigma[j]] = j;
+    P.in_stride[0] = 1;
+    for (int k = 1; k < P.r; ++k) P.in_stride[k] = P.in_stride[k - 1] * P.d[k - 1];
+    int64_t os = 1;
+    for (int j = 0; j < P.r; ++j) {
+        P.out_stride_of_dim[P.sigma[j]] = os;
+        os *= P.d[P.sigma[j]];
+    }
+    P.n = os;
+}
+
+// ---------------------------------------------------------------- tile geometry
+struct TileGeom {
+    int64_t ext[kMaxRank];   // 0 = not in tile
+    int src_dims[kMaxRank], nsrc;   // source run dims (source order)
+    int dst_dims[kMaxRank], ndst;   // destination run dims (dest order)
+    int a_part, c_part;             // partial boundary dims (-1 none)
+    int64_t Ls, Ld, T;
+    double cost, eff_s, eff_d;
+};
+
+bool build_geom(const Problem &P, const int64_t *ext, TileGeom &g) {
+    const int r = P.r;
+    memcpy(g.ext, ext, sizeof(int64_t) * r);
+    // source run: greedy over source order
+    g.nsrc = 0;
+    g.Ls = 1;
+    g.a_part = -1;
+    for (int k = 0; k < r && ext[k] > 0; ++k) {
+        g.src_dims[g.nsrc++] = k;
+        g.Ls *= ext[k];
+        if (ext[k] < P.d[k]) {
+            g.a_part = k;
+            break;
+        }
+    }
+    g.ndst = 0;
+    g.Ld = 1;
+    g.c_part = -1;
+    for (int j = 0; j < r && ext[P.sigma[j]] > 0; ++j) {
+        int k = P.sigma[j];
+        g.dst_dims[g.ndst++] = k;
+        g.Ld *= ext[k];
+        if (ext[k] < P.d[k]) {
+            g.c_part = k;
+            break;
+        }
+    }
+    if (g.nsrc == 0 || g.ndst == 0) return false;
+    g.T = 1;
+    int ntile = 0;
+    for (int k = 0; k < r; ++k) {
+        if (ext[k] > 0) {
+            g.T *= ext[k];
+            ++ntile;
+            // every partial dim must be a run boundary
+            if (ext[k] < P.d[k] && k != g.a_part && k != g.c_part) return false;
+        }
+    }
+    if (ntile > kMaxTileDims) return false;
+    int n_s_runidx = ntile - g.nsrc, n_w_runidx = ntile - g.ndst;
+    if (n_s_runidx > kMaxTileDims || n_w_runidx > kMaxTileDims || g.ndst > kMaxTileDims) return false;
+    return true;
+}
+
+// alignment (elements) shared by all run starts on one side: gcd of the
+// strides that move a run start (grid digits and run-index dims).
+int64_t run_align_elems(const Problem &P, const TileGeom &g, bool src_side) {
+    const int *dims = src_side ? g.src_dims : g.dst_dims;
+    const int nd = src_side ? g.nsrc : g.ndst;
+    int64_t gg = 0;
+    for (int k = 0; k < P.r; ++k) {
+        if (P.d[k] <= 1) continue;
+        bool in_run = false;
+        for (int i = 0; i < nd; ++i)
+            if (dims[i] == k) in_run = true;
+        int64_t stride = src_side ? P.in_stride[k] : P.out_stride_of_dim[k];
+        if (!in_run) gg = gcd64(gg, stride);
+        else if (g.ext[k] < P.d[k]) gg = gcd64(gg, stride * g.ext[k]);
+    }
+    return gg == 0 ? (int64_t)1 << 40 : gg;
+}
+
+void score_geom(const Problem &P, TileGeom &g) {
+    const int E = P.E;
+    int64_t as = run_align_elems(P, g, true) * E;
+    int64_t ad = run_align_elems(P, g, false) * E;
+    int64_t bs = g.Ls * E, bd = g.Ld * E;
+    g.eff_s = (double)bs / (32.0 * expected_sectors(bs, gcd64(as, 32)));
+    g.eff_d = (double)bd / (32.0 * expected_sectors(bd, gcd64(ad, 32)));
+    // average valid elements per tile (ragged tiles carry fewer)
+    double ntiles = 1.0;
+    for (int k = 0; k < P.r; ++k) {
+        if (g.ext[k] == 0) ntiles *= (double)P.d[k];
+        else if (g.ext[k] < P.d[k]) ntiles *= std::ceil((double)P.d[k] / (double)g.ext[k]);
+    }
+    double t_avg = (double)P.n / ntiles;
+    g.cost = E / g.eff_s + E / g.eff_d + kRunOverheadBytes * (1.0 / g.Ls + 1.0 / g.Ld) +
+             kTileOverheadBytes / t_avg;
+    // lanes idle in ragged tiles still cost issue slots: small penalty
+    g.cost += 0.05 * E * ((double)g.T / t_avg - 1.0);
+}
+
+std::vector<int64_t> extent_candidates(int64_t d, int64_t cap) {
+    std::vector<int64_t> v;
+    if (d <= cap) v.push_back(d);
+    for (int64_t p = 1; p < d && p <= cap; p <<= 1) v.push_back(p);
+    for (int64_t k = 2; k <= 16; ++k) {
+        int64_t e = (d + k - 1) / k;
+        if (e >= 1 && e < d && e <= cap) v.push_back(e);
+    }
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+    return v;
+}
+
+bool select_tile(const Problem &P, TileGeom &best) {
+    const int r = P.r;
+    const int64_t maxT = std::max<int64_t>(kTileBudgetBytes / P.E, 64);
+    bool found = false;
+    best.cost = 1e300;
+    int64_t ext[kMaxRank];
+    int64_t pre_s = 1;
+    for (int a = 0; a < r && pre_s <= maxT; pre_s *= P.d[a], ++a) {
+        for (int64_t ea : extent_candidates(P.d[a], maxT / pre_s)) {
+            int64_t pre_d = 1;
+            for (int b = 0; b < r; ++b) {
+                for (int k = 0; k < r; ++k) ext[k] = 0;
+                for (int k = 0; k < a; ++k) ext[k] = P.d[k];
+                ext[a] = ea;
+                for (int j = 0; j < b; ++j) ext[P.sigma[j]] = P.d[P.sigma[j]];
+                int c = P.sigma[b];
+                int64_t T0 = 1;
+                for (int k = 0; k < r; ++k)
+                    if (ext[k] > 0) T0 *= ext[k];
+                if (T0 > maxT) break;
+                std::vector<int64_t> ecs;
+                if (ext[c] == P.d[c]) ecs.push_back(P.d[c]);
+                else if (c == a) ecs.push_back(ea);
+                else ecs = extent_candidates(P.d[c], maxT / T0);
+                for (int64_t ec : ecs) {
+                    int64_t e2[kMaxRank];
+                    memcpy(e2, ext, sizeof(int64_t) * r);
+                    if (e2[c] != P.d[c]) e2[c] = ec;
+                    TileGeom g;
+                    if (!build_geom(P, e2, g)) continue;
+                    if (g.T > maxT) continue;
+                    score_geom(P, g);
+                    if (!found || g.cost < best.cost - 1e-9 ||
+                        (std::fabs(g.cost - best.cost) <= 1e-9 && g.T < best.T)) {
+                        best = g;
+                        found = true;
+                    }
+                }
+                pre_d *= P.d[P.sigma[b]];
+                (void)pre_d;
+            }
+        }
+    }
+    return found;
+}
+
+// Shared-memory bank model: wavefronts for one warp access of 32 lanes to
+// element offsets `off` (elements of E bytes).
+int warp_wavefronts(const uint32_t *off, int nlanes, int E) {
+    int wb = std::max(4, E);             // bytes per bank word
+    int lanes_per_phase = 32 / (wb / 4);
+    int nbanks = 128 / wb;
+    int total = 0;
+    for (int p0 = 0; p0 < nlanes; p0 += lanes_per_phase) {
+        std::vector<std::vector<uint64_t>> bank(nbanks);
+        int deg = 0;
+        for (int l = p0; l < std::min(nlanes, p0 + lanes_per_phase); ++l) {
+            uint64_t w = ((uint64_t)off[l] * E) / wb;
+            auto &b = bank[w % nbanks];
+            if (std::find(b.begin(), b.end(), w) == b.end()) b.push_back(w);
+            deg = std::max(deg, (int)b.size());
+        }
+        total += std::max(deg, 1);
+    }
+    return total;
+}
+
+uint32_t decode_sm(const TableDim *dims, int n, uint32_t idx) {
+    uint32_t s = 0;
+    for (int i = 0; i < n; ++i) {
+        uint32_t c = idx % dims[i].extent;
+        idx /= dims[i].extent;
+        s += c * dims[i].sstride;
+    }
+    return s;
+}
+
+void set_table_dim(TableDim &t, int64_t extent, int64_t gstride, int64_t sstride) {
+    t.extent = (uint32_t)extent;
+    t.div = make_fastdiv((uint32_t)extent);
+    t.gstride = gstride;
+    t.sstride = (uint32_t)sstride;
+    t.pad_ = 0;
+}
+
+// Fill TileParams for geometry g with smem pitch P (elements).
+void fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, TileParams &tp) {
+    memset(&tp, 0, sizeof(tp));
+    const int r = Pb.r;
+    tp.Ls = (uint32_t)g.Ls;
+    tp.Ld = (uint32_t)g.Ld;
+    tp.T = (uint32_t)g.T;
+    tp.Ns = (uint32_t)(g.T / g.Ls);
+    tp.Nd = (uint32_t)(g.T / g.Ld);
+    tp.pitch = pitch;
+    // smem strides: source run dims dense, then run-index dims scaled by pitch
+    int64_t sstr[kMaxRank];
+    bool in_src[kMaxRank] = {false}, in_dst[kMaxRank] = {false};
+    int64_t acc = 1;
+    for (int i = 0; i < g.nsrc; ++i) {
+        int k = g.src_dims[i];
+        in_src[k] = true;
+        sstr[k] = acc;
+        acc *= g.ext[k];
+    }
+    for (int i = 0; i < g.ndst; ++i) in_dst[g.dst_dims[i]] = true;
+    acc = pitch;
+    tp.nS = 0;
+    tp.s_c_dim = -1;
+    for (int k = 0; k < r; ++k) {
+        if (g.ext[k] == 0 || in_src[k]) continue;
+        sstr[k] = acc;
+        if (k == g.c_part) tp.s_c_dim = tp.nS;
+        set_table_dim(tp.S[tp.nS++], g.ext[k], Pb.in_stride[k], acc);
+        acc *= g.ext[k];
+    }
+    tp.nA = 0;
+    for (int i = 0; i < g.ndst; ++i) {
+        int k = g.dst_dims[i];
+        set_table_dim(tp.A[tp.nA++], g.ext[k], Pb.out_stride_of_dim[k], sstr[k]);
+    }
+    tp.nW = 0;
+    tp.w_a_dim = -1;
+    for (int j = 0; j < r; ++j) {
+        int k = Pb.sigma[j];
+        if (g.ext[k] == 0 || in_dst[k]) continue;
+        if (k == g.a_part) tp.w_a_dim = tp.nW;
+        set_table_dim(tp.W[tp.nW++], g.ext[k], Pb.out_stride_of_dim[k], sstr[k]);
+    }
+    // grid digits
+    struct Dg {
+        int64_t ext, ss, ds;
+        int dim;
+    };
+    std::vector<Dg> dg;
+    for (int k = 0; k < r; ++k) {
+        if (g.ext[k] == 0) dg.push_back({Pb.d[k], Pb.in_stride[k], Pb.out_stride_of_dim[k], -1});
+        else if (g.ext[k] < Pb.d[k])
+            dg.push_back({(Pb.d[k] + g.ext[k] - 1) / g.ext[k], Pb.in_stride[k] * g.ext[k],
+                          Pb.out_stride_of_dim[k] * g.ext[k], k});
+    }
+    std::stable_sort(dg.begin(), dg.end(), [](const Dg &x, const Dg &y) { return x.ds < y.ds; });
+    tp.ngrid = (int32_t)dg.size();
+    tp.grid_a = tp.grid_c = -1;
+    uint64_t cum = 1;
+    for (size_t i = 0; i < dg.size(); ++i) {
+        tp.grid[i].cum = make_fastdiv((uint32_t)cum);
+        tp.grid[i].ext = make_fastdiv((uint32_t)dg[i].ext);
+        tp.grid[i].src_stride = dg[i].ss;
+        tp.grid[i].dst_stride = dg[i].ds;
+        if (dg[i].dim >= 0 && dg[i].dim == g.a_part) tp.grid_a = (int32_t)i;
+        if (dg[i].dim >= 0 && dg[i].dim == g.c_part) tp.grid_c = (int32_t)i;
+        cum *= (uint64_t)dg[i].ext;
+    }
+    tp.num_tiles = (uint32_t)cum;
+    if (g.a_part >= 0) {
+        tp.e_a = (uint32_t)g.ext[g.a_part];
+        tp.d_a = (uint32_t)Pb.d[g.a_part];
+    } else {
+        tp.e_a = tp.d_a = 1;
+    }
+    if (g.c_part >= 0) {
+        tp.e_c = (uint32_t)g.ext[g.c_part];
+        tp.d_c = (uint32_t)Pb.d[g.c_part];
+    } else {
+        tp.e_c = tp.d_c = 1;
+    }
+    tp.Ls_unit = g.a_part >= 0 ? (uint32_t)(g.Ls / g.ext[g.a_part]) : tp.Ls;
+    tp.Ld_unit = g.c_part >= 0 ? (uint32_t)(g.Ld / g.ext[g.c_part]) : tp.Ld;
+    // dynamic smem layout
+    uint32_t o = 0;
+    auto take = [&](uint32_t bytes, uint32_t al) {
+        o = (o + al - 1) / al * al;
+        uint32_t at = o;
+        o += bytes;
+        return at;
+    };
+    tp.off_S_off = take(8 * tp.Ns, 16);
+    tp.off_W_off = take(8 * tp.Nd, 16);
+    tp.off_W_sm = take(4 * tp.Nd, 16);
+    tp.off_A = take(4 * tp.Ld, 16);
+    tp.off_S_c = take(tp.s_c_dim >= 0 ? 4 * tp.Ns : 0, 16);
+    tp.off_W_a = take(tp.w_a_dim >= 0 ? 4 * tp.Nd : 0, 16);
+    tp.off_tile = take((uint32_t)((uint64_t)tp.Ns * pitch * Pb.E), 16);
+    tp.smem_bytes = (o + 15) / 16 * 16;
+}
+
+// Choose the source-run pitch that minimises modelled smem wavefronts of
+// both phases (read: flattened (r,c); write: flattened (rd,cd)).
+uint32_t choose_pitch(const Problem &Pb, const TileGeom &g, int threads) {
+    uint32_t best_p = (uint32_t)g.Ls;
+    int64_t best_w = -1;
+    const int maxpad = 32;
+    for (int pad = 0; pad <= maxpad; ++pad) {
+        uint32_t pitch = (uint32_t)g.Ls + pad;
+        if ((int64_t)(g.T / g.Ls) * pitch * Pb.E > kTileBudgetBytes + 8192) break;
+        TileParams tp;
+        fill_tile_params(Pb, g, pitch, tp);
+        int64_t waves = 0;
+        // simulate the first `threads` lanes of each phase, warp by warp
+        uint32_t off[32];
+        int64_t nel = std::min<int64_t>(g.T, (int64_t)threads * 4);
+        for (int64_t w0 = 0; w0 < nel; w0 += 32) {
+            int nl = (int)std::min<int64_t>(32, g.T - w0);
+            for (int l = 0; l < nl; ++l) {
+                uint32_t v = (uint32_t)(w0 + l);
+                off[l] = (v / tp.Ls) * pitch + v % tp.Ls;
+            }
+            waves += warp_wavefronts(off, nl, Pb.E);
+            for (int l = 0; l < nl; ++l) {
+                uint32_t v = (uint32_t)(w0 + l);
+                uint32_t rd = v / tp.Ld, cd = v % tp.Ld;
+                off[l] = decode_sm(tp.W, tp.nW, rd) + decode_sm(tp.A, tp.nA, cd);
+            }
+            waves += warp_wavefronts(off, nl, Pb.E);
+        }
+        if (best_w < 0 || waves < best_w) {
+            best_w = waves;
+            best_p = pitch;
+        }
+    }
+    return best_p;
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------- merge
+// planner.py:211-241
+int merge_dims(int rank, const int64_t *dims, const int32_t *sigma, int64_t *od, int32_t *os) {
+    std::vector<int> keep;
+    for (int k = 0; k < rank; ++k)
+        if (dims[k] > 1) keep.push_back(k);
+    if (keep.empty()) {
+        od[0] = 1;
+        os[0] = 0;
+        return 1;
+    }
+    std::vector<int> renum(rank, -1);
+    for (size_t i = 0; i < keep.size(); ++i) renum[keep[i]] = (int)i;
+    int m = (int)keep.size();
+    std::vector<int64_t> d(m);
+    for (int i = 0; i < m; ++i) d[i] = dims[keep[i]];
+    std::vector<int> sg;
+    for (int j = 0; j < rank; ++j)
+        if (renum[sigma[j]] >= 0) sg.push_back(renum[sigma[j]]);
+    std::vector<int> pos(m);
+    for (int j = 0; j < m; ++j) pos[sg[j]] = j;
+    std::vector<std::vector<int>> groups{{0}};
+    for (int k = 1; k < m; ++k) {
+        if (pos[k] == pos[k - 1] + 1) groups.back().push_back(k);
+        else groups.push_back({k});
+    }
+    int ng = (int)groups.size();
+    for (int gi = 0; gi < ng; ++gi) {
+        int64_t p = 1;
+        for (int k : groups[gi]) p *= d[k];
+        od[gi] = p;
+    }
+    std::vector<int> order(ng);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int x, int y) { return pos[groups[x][0]] < pos[groups[y][0]]; });
+    for (int j = 0; j < ng; ++j) os[j] = order[j];
+    return ng;
+}
+
+// ----------------------------------------------------------------- plan
+static void describe(vpg_plan *p) {
+    char buf[4096];
+    int o = 0;
+    auto put = [&](const char *fmt, auto... args) {
+        if (o < (int)sizeof(buf)) o += snprintf(buf + o, sizeof(buf) - o, fmt, args...);
+    };
+    static const char *names[] = {"copy", "rows(K1)", "tile(K2/K3)", "gather(K0)"};
+    put("kernel class: %s\n", names[p->kernel_class]);
+    put("elem bytes: %d\n", p->elem_bytes);
+    put("merged dims (inner-first): (");
+    for (int k = 0; k < p->rank; ++k) put(k ? ",%lld" : "%lld", (long long)p->dims[k]);
+    put(")\nmerged sigma (inner-first): (");
+    for (int k = 0; k < p->rank; ++k) put(k ? ",%d" : "%d", p->sigma[k]);
+    put(")\nelements: %lld\n", (long long)p->n);
+    if (p->kernel_class == VPG_KERNEL_TILE) {
+        const TileParams &t = p->tile;
+        put("tile elements: %u (src run %u x %u runs, dst run %u x %u runs)\n", t.T, t.Ls, t.Ns,
+            t.Ld, t.Nd);
+        put("smem pitch: %u, smem bytes: %u\n", t.pitch, t.smem_bytes);
+        put("ragged boundary dims: a(extent %u of %u) c(extent %u of %u)\n", t.e_a, t.d_a, t.e_c,
+            t.d_c);
+        put("tiles: %u, grid digits: %d\n", t.num_tiles, t.ngrid);
+    } else if (p->kernel_class == VPG_KERNEL_ROWS) {
+        put("rows: %u x %lld elements, vector %u elements, %u threads/row\n", p->rows.nrows,
+            (long long)p->rows.row_len, p->rows.vec, 1u << p->rows.tpr_log2);
+    }
+    put("predicted sector efficiency: %.3f\n", p->predicted_eff);
+    p->text.assign(buf, std::min<int>(o, sizeof(buf) - 1));
+}
+
+vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E, unsigned flags,
+                     vpg_plan **out, std::string *err) {
+    if (rank < 1 || rank > VPG_MAX_RANK) {
+        *err = "rank must be in 1.." + std::to_string(VPG_MAX_RANK);
+        return VPG_EINVAL;
+    }
+    if (!(E == 1 || E == 2 || E == 4 || E == 8 || E == 16)) {
+        *err = "element width must be one of 1, 2, 4, 8, 16 bytes";
+        return VPG_EINVAL;
+    }
+    std::vector<int> seen(rank, 0);
+    for (int k = 0; k < rank; ++k) {
+        if (dims[k] < 1) {
+            *err = "dimension " + std::to_string(dims[k]) + " is not positive";
+            return VPG_EINVAL;
+        }
+        if (sigma[k] < 0 || sigma[k] >= rank || seen[sigma[k]]) {
+            *err = "map is not a bijection on 0.." + std::to_string(rank - 1);
+            return VPG_EINVAL;
+        }
+        seen[sigma[k]] = 1;
+    }
+    Problem P;
+    P.E = E;
+    if (flags & VPG_NO_MERGE) {
+        P.r = rank;
+        for (int k = 0; k < rank; ++k) {
+            P.d[k] = dims[k];
+            P.sigma[k] = sigma[k];
+        }
+    } else {
+        int64_t md[VPG_MAX_RANK];
+        int32_t ms[VPG_MAX_RANK];
+        P.r = merge_dims(rank, dims, sigma, md, ms);
+        if (P.r > kMaxRank) {
+            *err = "merged rank exceeds " + std::to_string(kMaxRank);
+            return VPG_EUNSUPPORTED;
+        }
+        for (int k = 0; k < P.r; ++k) {
+            P.d[k] = md[k];
+            P.sigma[k] = ms[k];
+        }
+    }
+    if (P.r > kMaxRank) {
+        *err = "rank exceeds " + std::to_string(kMaxRank);
+        return VPG_EUNSUPPORTED;
+    }
+    fill_problem(P);
+    vpg_plan *p = new vpg_plan();
+    p->elem_bytes = E;
+    p->rank = P.r;
+    for (int k = 0; k < P.r; ++k) {
+        p->dims[k] = P.d[k];
+        p->sigma[k] = P.sigma[k];
+    }
+    p->n = P.n;
+    p->predicted_eff = 1.0;
+    bool identity = true;
+    for (int k = 0; k < P.r; ++k)
+        if (P.sigma[k] != k) identity = false;
+
+    if ((flags & VPG_FORCE_GATHER) || (P.n <= kGatherMaxN && !(flags & VPG_FORCE_TILE))) {
+        if (P.n >= (int64_t)1 << 32) {
+            delete p;
+            *err = "gather kernel limited to 2^32 elements";
+            return VPG_EUNSUPPORTED;
+        }
+        p->kernel_class = VPG_KERNEL_GATHER;
+        GatherParams &gp = p->gather;
+        gp.n = (uint32_t)P.n;
+        gp.rank = P.r;
+        for (int j = 0; j < P.r; ++j) {
+            gp.ext[j] = make_fastdiv((uint32_t)P.d[P.sigma[j]]);
+            gp.src_stride[j] = P.in_stride[P.sigma[j]];
+        }
+        p->threads = 256;
+        p->grid_hint = (P.n + 255) / 256;
+        p->predicted_eff = 0.25;
+    } else if (identity && !(flags & VPG_FORCE_TILE)) {
+        p->kernel_class = VPG_KERNEL_COPY;
+        p->copy.n = P.n;
+        p->threads = 256;
+        p->grid_hint = 148 * 8;
+    } else if (P.sigma[0] == 0 && P.d[0] * E >= kRowsMinBytes && !(flags & VPG_FORCE_TILE)) {
+        p->kernel_class = VPG_KERNEL_ROWS;
+        RowsParams &rp = p->rows;
+        int64_t Lr = P.d[0];
+        int64_t nrows = P.n / Lr;
+        if (nrows >= ((int64_t)1 << 32)) {
+            delete p;
+            *err = "rows kernel limited to 2^32 rows";
+            return VPG_EUNSUPPORTED;
+        }
+        uint32_t V = std::max(1, 16 / E);
+        while (V > 1 && Lr % V) V >>= 1;
+        rp.vec = V;
+        rp.row_len = Lr;
+        rp.nrows = (uint32_t)nrows;
+        rp.row_vecs = (uint32_t)(Lr / V);
+        uint32_t tpr = 32;
+        while (tpr > 1 && tpr / 2 >= rp.row_vecs) tpr >>= 1;
+        rp.tpr_log2 = 0;
+        while ((1u << rp.tpr_log2) < tpr) ++rp.tpr_log2;
+        rp.ndig = P.r - 1;
+        for (int j = 1; j < P.r; ++j) {
+            rp.dig[j - 1].ext = make_fastdiv((uint32_t)P.d[P.sigma[j]]);
+            rp.dig[j - 1].src_stride = P.in_stride[P.sigma[j]];
+        }
+        p->threads = 256;
+        p->grid_hint = 148 * 8;
+        int64_t bytes = Lr * E;
+        p->predicted_eff = (double)bytes / (32.0 * expected_sectors(bytes, gcd64(bytes, 32)));
+    } else {
+        TileGeom g;
+        if (!select_tile(P, g)) {
+            delete p;
+            *err = "no tile fits the shared-memory budget";
+            return VPG_EUNSUPPORTED;
+        }
+        p->kernel_class = VPG_KERNEL_TILE;
+        int threads = g.T >= 1024 ? kTileThreads : (g.T >= 256 ? 128 : 64);
+        uint32_t pitch = choose_pitch(P, g, threads);
+        fill_tile_params(P, g, pitch, p->tile);
+        // the tile count must fit the 32-bit tile index
+        double nt = 1.0;
+        for (int i = 0; i < p->tile.ngrid; ++i) nt *= p->tile.grid[i].ext.d;
+        if (nt >= 4294967296.0) {
+            delete p;
+            *err = "more than 2^32 tiles";
+            return VPG_EUNSUPPORTED;
+        }
+        p->threads = threads;
+        p->grid_hint = std::min<int64_t>(p->tile.num_tiles, 148 * 4);
+        p->predicted_eff = 2.0 / (1.0 / g.eff_s + 1.0 / g.eff_d);
+    }
+    describe(p);
+    *out = p;
+    return VPG_OK;
+}
+
+}  // namespace vpg

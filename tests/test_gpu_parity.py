@@ -1,0 +1,118 @@
+"""GPU parity: the CUDA path against the reference's own golden vectors and
+the CPU oracle, bit-exact (pure data movement: any byte difference is a bug).
+
+Golden vectors come from the reference itself (tests/golden/make_golden.py);
+the C oracle (oracle/naive_permute.c) is pinned against the same vectors in
+tests/test_oracle.py.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from tests.golden.pattern import golden_pattern
+from tests.helpers import golden, gpu_permute_bytes, sha256
+
+pytestmark = pytest.mark.gpu
+
+
+def _cases(families=None):
+    return [c for c in golden()["cases"] if families is None or c["family"] in families]
+
+
+@pytest.mark.parametrize("force", [None, "tile", "gather"])
+def test_golden_small_cases(cuda, force):
+    """Known answers, paper shape, Appendix-A edges, merge cases, ragged sweep
+    (test_core.py:93-100,147-151; test_cli.py:69-83; test_acceptance.py:239-274)."""
+    cases = _cases({"known", "paper", "merge", "edge", "ragged"})
+    assert len(cases) > 100
+    for c in cases:
+        data = golden_pattern(c["n"], c["elem"])
+        out, prog = gpu_permute_bytes(c["dims"], c["sigma"], c["elem"], data, force=force)
+        assert sha256(out) == c["sha256"], (c["name"], prog.text)
+        if "out" in c:
+            words = out.view(np.uint32 if c["elem"] == 4 else np.uint64)
+            assert words.tolist() == c["out"], c["name"]
+
+
+def test_known_answer_2x3(cuda):
+    """test_core.py:147-151: (2,3) transpose of arange -> [0,3,1,4,2,5]."""
+    data = np.arange(6, dtype=np.uint32)
+    for force in (None, "tile", "gather"):
+        out, _ = gpu_permute_bytes((3, 2), (1, 0), 4, data, force=force)
+        assert out.view(np.uint32).tolist() == [0, 3, 1, 4, 2, 5]
+
+
+def test_bit_reversal_2x2x2(cuda):
+    """test_core.py:93-100: full role reversal on (2,2,2) is bit reversal."""
+    data = np.arange(8, dtype=np.uint32)
+    for force in (None, "tile", "gather"):
+        out, _ = gpu_permute_bytes((2, 2, 2), (2, 1, 0), 4, data, force=force)
+        assert out.view(np.uint32).tolist() == [0, 4, 2, 6, 1, 5, 3, 7]
+
+
+@pytest.mark.parametrize("force", [None, "tile"])
+def test_reference_campaign_1000(cuda, force):
+    """The reference's 1000-case randomized campaign (seed 2024, ranks 2-16,
+    <= 2^16 elements; test_acceptance.py:25-33), bitwise on the GPU."""
+    cases = [c for c in golden()["cases"] if c["family"].startswith("campaign_")]
+    assert len(cases) == 1000
+    fams = {}
+    bad = []
+    for c in cases:
+        data = golden_pattern(c["n"], c["elem"])
+        out, prog = gpu_permute_bytes(c["dims"], c["sigma"], c["elem"], data, force=force)
+        fams[c["family"]] = fams.get(c["family"], 0) + 1
+        if sha256(out) != c["sha256"]:
+            bad.append((c["name"], c["shape"], c["axes"], prog.kernel))
+    assert not bad, bad[:5]
+    assert all(v > 0 for v in fams.values()) and len(fams) == 3
+
+
+def test_full_size_2pow20(cuda):
+    """N = 2^20 transpose (test_acceptance.py:35-44)."""
+    c = next(c for c in golden()["cases"] if c["name"] == "full_1024x1024")
+    out, _ = gpu_permute_bytes(c["dims"], c["sigma"], 4, golden_pattern(c["n"], 4))
+    assert sha256(out) == c["sha256"]
+
+
+@pytest.mark.parametrize("elem", [1, 2, 16])
+def test_extra_elem_widths_vs_oracle(cuda, elem):
+    """Superset element widths (the reference accepts 4/8 only, core.py:29)
+    against the C oracle, which is pinned on 4/8 by the golden vectors."""
+    import oracle
+
+    rng = np.random.default_rng(100 + elem)
+    for t in range(40):
+        rank = int(rng.integers(1, 6))
+        dims = tuple(int(rng.integers(1, 12)) for _ in range(rank))
+        sigma = tuple(int(x) for x in rng.permutation(rank))
+        n = int(np.prod(dims))
+        data = rng.integers(0, 256, size=n * elem, dtype=np.uint8)
+        want = oracle.naive_permute_c(data.view(np.uint8), dims, sigma, elem_bytes=elem)
+        for force in (None, "tile", "gather"):
+            out, prog = gpu_permute_bytes(dims, sigma, elem, data, force=force)
+            assert np.array_equal(out, want.view(np.uint8)), (dims, sigma, force, prog.text)
+
+
+def test_random_general_vs_oracle_large(cuda):
+    """Larger random shapes (odd dims, up to ~4M elements) against the C
+    oracle, 64-bit random words (high halves set)."""
+    import oracle
+
+    rng = np.random.default_rng(7)
+    for t in range(60):
+        rank = int(rng.integers(2, 7))
+        while True:
+            dims = tuple(int(rng.integers(1, 40)) for _ in range(rank))
+            if np.prod(dims) <= (1 << 22):
+                break
+        sigma = tuple(int(x) for x in rng.permutation(rank))
+        elem = int(rng.choice([4, 8]))
+        n = int(np.prod(dims))
+        data = rng.integers(0, 2**63, size=n, dtype=np.uint64)
+        data = data.view(np.uint32)[:n].copy() if elem == 4 else data
+        want = oracle.naive_permute_c(data, dims, sigma)
+        out, prog = gpu_permute_bytes(dims, sigma, elem, data)
+        assert np.array_equal(out, want.view(np.uint8)), (dims, sigma, elem, prog.text)
