@@ -113,163 +113,272 @@ __global__ void __launch_bounds__(256) rows_kernel(const __grid_constant__ RowsP
 }
 
 // ------------------------------------------------------------------ TILE (K2/K3)
+struct OuterEntry {
+    int64_t g;
+    uint32_t s;
+    uint16_t c0, c1;
+};
+
+struct ThreadPart {
+    int64_t g;
+    uint32_t s;
+    uint32_t c[kNumSlots];
+    uint32_t grp;
+    bool active;
+};
+
+template <int E>
+__device__ __forceinline__ void cp_async(void *sp, const void *gp) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(sp);
+    if constexpr (E == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gp) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gp), "n"(E) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+__device__ __forceinline__ ThreadPart decode_thread(const PhaseDesc &d, uint32_t tid) {
+    ThreadPart t;
+    t.grp = tid / d.nthr;
+    uint32_t tr = tid - t.grp * d.nthr;
+    t.active = t.grp < d.ngroups;
+    t.g = 0;
+    t.s = 0;
+    t.c[0] = t.c[1] = t.c[2] = 0;
+    for (int i = 0; i < d.nthr_dims; ++i) {
+        uint32_t q = fdiv(tr, d.thr[i].div);
+        uint32_t c = tr - q * d.thr[i].div.d;
+        tr = q;
+        t.g += (int64_t)c * d.thr[i].gstride;
+        t.s += c * d.thr[i].sstride;
+        if (d.thr[i].slot >= 0) t.c[d.thr[i].slot] = c;
+    }
+    return t;
+}
+
+__device__ __forceinline__ bool slot_ok(uint32_t mask, uint32_t c0, uint32_t c1, uint32_t c2, const uint32_t *lim) {
+    return (!(mask & 1u) || c0 < lim[0]) && (!(mask & 2u) || c1 < lim[1]) && (!(mask & 4u) || c2 < lim[2]);
+}
+
+// R phase: global (source order) -> smem.  ASYNC: cp.async, else LDG+STS.
+template <typename W, bool ASYNC>
+__device__ __forceinline__ void tile_read(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
+                                          const W *__restrict__ gsrc, W *buf, uint32_t mask,
+                                          const uint32_t *lim) {
+    if (!t.active) return;
+    constexpr int U = 4;
+    const OuterEntry *tab = reinterpret_cast<const OuterEntry *>(smem + d.off_tab);
+    const uint32_t n_in = d.n_in;
+    const int64_t g_in = d.g_in;
+    const uint32_t s_in = d.s_in;
+    for (uint32_t o = t.grp; o < d.n_outer; o += d.ngroups) {
+        const OuterEntry e = tab[o];
+        const W *gp = gsrc + (t.g + e.g);
+        W *sp = buf + (t.s + e.s);
+        if (mask == 0) {
+            uint32_t i = 0;
+            for (; i + U <= n_in; i += U) {
+                if constexpr (ASYNC) {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) cp_async<sizeof(W)>(sp + u * s_in, gp + u * g_in);
+                } else {
+                    W v[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) v[u] = __ldg(gp + u * g_in);
+#pragma unroll
+                    for (int u = 0; u < U; ++u) sp[u * s_in] = v[u];
+                }
+                gp += U * g_in;
+                sp += U * s_in;
+            }
+            for (; i < n_in; ++i) {
+                if constexpr (ASYNC) cp_async<sizeof(W)>(sp, gp);
+                else *sp = __ldg(gp);
+                gp += g_in;
+                sp += s_in;
+            }
+        } else {
+            uint32_t c0 = t.c[0] + e.c0, c1 = t.c[1] + e.c1, c2 = t.c[2];
+            for (uint32_t i = 0; i < n_in; ++i) {
+                if (slot_ok(mask, c0, c1, c2, lim)) {
+                    if constexpr (ASYNC) cp_async<sizeof(W)>(sp, gp);
+                    else *sp = __ldg(gp);
+                }
+                gp += g_in;
+                sp += s_in;
+                c0 += d.c_in[0];
+                c1 += d.c_in[1];
+                c2 += d.c_in[2];
+            }
+        }
+    }
+}
+
+// W phase: smem -> global (destination order).
 template <typename W>
+__device__ __forceinline__ void tile_write(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
+                                           W *__restrict__ gdst, const W *buf, uint32_t mask,
+                                           const uint32_t *lim) {
+    if (!t.active) return;
+    constexpr int U = 4;
+    const OuterEntry *tab = reinterpret_cast<const OuterEntry *>(smem + d.off_tab);
+    const uint32_t n_in = d.n_in;
+    const int64_t g_in = d.g_in;
+    const uint32_t s_in = d.s_in;
+    for (uint32_t o = t.grp; o < d.n_outer; o += d.ngroups) {
+        const OuterEntry e = tab[o];
+        W *gp = gdst + (t.g + e.g);
+        const W *sp = buf + (t.s + e.s);
+        if (mask == 0) {
+            uint32_t i = 0;
+            for (; i + U <= n_in; i += U) {
+                W v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) v[u] = sp[u * s_in];
+#pragma unroll
+                for (int u = 0; u < U; ++u) gp[u * g_in] = v[u];
+                gp += U * g_in;
+                sp += U * s_in;
+            }
+            for (; i < n_in; ++i) {
+                *gp = *sp;
+                gp += g_in;
+                sp += s_in;
+            }
+        } else {
+            uint32_t c0 = t.c[0] + e.c0, c1 = t.c[1] + e.c1, c2 = t.c[2];
+            for (uint32_t i = 0; i < n_in; ++i) {
+                if (slot_ok(mask, c0, c1, c2, lim)) *gp = *sp;
+                gp += g_in;
+                sp += s_in;
+                c0 += d.c_in[0];
+                c1 += d.c_in[1];
+                c2 += d.c_in[2];
+            }
+        }
+    }
+}
+
+// Warp 0 decodes tile `t` into slot `k`: source/destination base offsets and
+// the valid extents of the ragged boundary dims a and c.
+__device__ __forceinline__ void decode_tile(const TileParams &p, uint32_t t, int64_t (*s_base)[2],
+                                            uint32_t (*s_valid)[2], int k) {
+    const uint32_t lane = threadIdx.x & 31;
+    int64_t sb = 0, db = 0;
+    uint32_t va = p.e_a, vc = p.e_c;
+    for (int i = (int)lane; i < p.ngrid; i += 32) {
+        uint32_t q = fdiv(t, p.grid[i].cum);
+        uint32_t c = q - fdiv(q, p.grid[i].ext) * p.grid[i].ext.d;
+        sb += (int64_t)c * p.grid[i].src_stride;
+        db += (int64_t)c * p.grid[i].dst_stride;
+        if (i == p.grid_a) va = min(p.e_a, p.d_a - c * p.e_a);
+        if (i == p.grid_c) vc = min(p.e_c, p.d_c - c * p.e_c);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        sb += __shfl_xor_sync(0xffffffffu, sb, o);
+        db += __shfl_xor_sync(0xffffffffu, db, o);
+        va = min(va, __shfl_xor_sync(0xffffffffu, va, o));
+        vc = min(vc, __shfl_xor_sync(0xffffffffu, vc, o));
+    }
+    if (lane == 0) {
+        s_base[k][0] = sb;
+        s_base[k][1] = db;
+        s_valid[k][0] = va;
+        s_valid[k][1] = vc;
+    }
+}
+
+// Persistent CTAs walk tiles t = blockIdx.x + k*gridDim.x.  With ASYNC the
+// next tile's source runs stream into the second smem buffer (cp.async)
+// while the current tile is written out: one barrier per tile.
+template <typename W, bool ASYNC>
 __global__ void __launch_bounds__(256) tile_kernel(const __grid_constant__ TileParams p,
                                                    const W *__restrict__ src, W *__restrict__ dst) {
-    constexpr int U = 8;
     extern __shared__ __align__(16) unsigned char smem[];
-    int64_t *S_off = reinterpret_cast<int64_t *>(smem + p.off_S_off);
-    int64_t *W_off = reinterpret_cast<int64_t *>(smem + p.off_W_off);
-    uint32_t *W_sm = reinterpret_cast<uint32_t *>(smem + p.off_W_sm);
-    uint32_t *A_sm = reinterpret_cast<uint32_t *>(smem + p.off_A);
-    uint32_t *S_c = reinterpret_cast<uint32_t *>(smem + p.off_S_c);
-    uint32_t *W_a = reinterpret_cast<uint32_t *>(smem + p.off_W_a);
-    W *tile = reinterpret_cast<W *>(smem + p.off_tile);
-    __shared__ int64_t s_base[2];
-    __shared__ uint32_t s_valid[2];
-
+    __shared__ int64_t s_base[4][2];
+    __shared__ uint32_t s_valid[4][2];
     const uint32_t tid = threadIdx.x, NT = blockDim.x;
+    const uint32_t first = blockIdx.x, step = gridDim.x;
+    if (first >= p.num_tiles) return;
 
-    // ---- per-CTA run tables (identical for every tile)
-    for (uint32_t r = tid; r < p.Ns; r += NT) {
-        uint32_t idx = r, cc = 0;
-        int64_t off = 0;
-        for (int i = 0; i < p.nS; ++i) {
-            uint32_t q = fdiv(idx, p.S[i].div);
-            uint32_t c = idx - q * p.S[i].extent;
-            idx = q;
-            off += (int64_t)c * p.S[i].gstride;
-            if (i == p.s_c_dim) cc = c;
+    // per-CTA outer tables of both phases
+    for (int ph = 0; ph < 2; ++ph) {
+        const PhaseDesc &d = p.ph[ph];
+        OuterEntry *tab = reinterpret_cast<OuterEntry *>(smem + d.off_tab);
+        for (uint32_t o = tid; o < d.n_outer; o += NT) {
+            uint32_t idx = o, s = 0, c0 = 0, c1 = 0;
+            int64_t g = 0;
+            for (int i = 0; i < d.nout_dims; ++i) {
+                uint32_t q = fdiv(idx, d.out[i].div);
+                uint32_t c = idx - q * d.out[i].div.d;
+                idx = q;
+                g += (int64_t)c * d.out[i].gstride;
+                s += c * d.out[i].sstride;
+                if (d.out[i].slot == 0) c0 = c;
+                else if (d.out[i].slot == 1) c1 = c;
+            }
+            OuterEntry e;
+            e.g = g;
+            e.s = s;
+            e.c0 = (uint16_t)c0;
+            e.c1 = (uint16_t)c1;
+            tab[o] = e;
         }
-        S_off[r] = off;
-        if (p.s_c_dim >= 0) S_c[r] = cc;
     }
-    for (uint32_t r = tid; r < p.Nd; r += NT) {
-        uint32_t idx = r, ca = 0, sm = 0;
-        int64_t off = 0;
-        for (int i = 0; i < p.nW; ++i) {
-            uint32_t q = fdiv(idx, p.W[i].div);
-            uint32_t c = idx - q * p.W[i].extent;
-            idx = q;
-            off += (int64_t)c * p.W[i].gstride;
-            sm += c * p.W[i].sstride;
-            if (i == p.w_a_dim) ca = c;
-        }
-        W_off[r] = off;
-        W_sm[r] = sm;
-        if (p.w_a_dim >= 0) W_a[r] = ca;
-    }
-    for (uint32_t c0 = tid; c0 < p.Ld; c0 += NT) {
-        uint32_t idx = c0, sm = 0;
-        for (int i = 0; i < p.nA; ++i) {
-            uint32_t q = fdiv(idx, p.A[i].div);
-            sm += (idx - q * p.A[i].extent) * p.A[i].sstride;
-            idx = q;
-        }
-        A_sm[c0] = sm;
-    }
+    const ThreadPart tr = decode_thread(p.ph[0], tid);
+    const ThreadPart tw = decode_thread(p.ph[1], tid);
+    W *buf0 = reinterpret_cast<W *>(smem + p.off_buf);
+    W *buf1 = buf0 + ((size_t)p.tile_elems_alloc * sizeof(W) + 15) / 16 * 16 / sizeof(W);
 
-    // ---- incremental (run, column) walkers: v advances by NT per step
-    const uint32_t r0 = tid / p.Ls, c0 = tid - r0 * p.Ls;
-    const uint32_t dR = NT / p.Ls, dC = NT - dR * p.Ls;
-    const uint32_t q0 = tid / p.Ld, k0 = tid - q0 * p.Ld;
-    const uint32_t dQ = NT / p.Ld, dK = NT - dQ * p.Ld;
-
-    for (uint32_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        if (tid < 32) {
-            int64_t sb = 0, db = 0;
-            uint32_t va = p.e_a, vc = p.e_c;
-            for (int i = (int)tid; i < p.ngrid; i += 32) {
-                uint32_t q = fdiv(t, p.grid[i].cum);
-                uint32_t c = q - fdiv(q, p.grid[i].ext) * p.grid[i].ext.d;
-                sb += (int64_t)c * p.grid[i].src_stride;
-                db += (int64_t)c * p.grid[i].dst_stride;
-                if (i == p.grid_a) va = min(p.e_a, p.d_a - c * p.e_a);
-                if (i == p.grid_c) vc = min(p.e_c, p.d_c - c * p.e_c);
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                sb += __shfl_xor_sync(0xffffffffu, sb, o);
-                db += __shfl_xor_sync(0xffffffffu, db, o);
-                va = min(va, __shfl_xor_sync(0xffffffffu, va, o));
-                vc = min(vc, __shfl_xor_sync(0xffffffffu, vc, o));
-            }
-            if (tid == 0) {
-                s_base[0] = sb;
-                s_base[1] = db;
-                s_valid[0] = va;
-                s_valid[1] = vc;
-            }
-        }
-        __syncthreads();
-        const int64_t sb = s_base[0], db = s_base[1];
-        const uint32_t va = s_valid[0], vc = s_valid[1];
+    if (tid < 32) {
+        decode_tile(p, first, s_base, s_valid, 0);
+        if (first + step < p.num_tiles) decode_tile(p, first + step, s_base, s_valid, 1);
+    }
+    __syncthreads();
+    auto limits = [&](int k, int ph, uint32_t *lim) -> uint32_t {
+        const uint32_t va = s_valid[k][0], vc = s_valid[k][1];
+        lim[0] = va;
+        lim[1] = vc;
+        lim[2] = p.lim_split[ph];
         const bool full = (va == p.e_a) && (vc == p.e_c);
-        const uint32_t Ls_valid = (va == p.e_a) ? p.Ls : p.Ls_unit * va;
-        const uint32_t Ld_valid = (vc == p.e_c) ? p.Ld : p.Ld_unit * vc;
-
-        // ---- read phase: contiguous source runs -> smem (source order, padded pitch)
-        {
-            const W *sp = src + sb;
-            uint32_t r = r0, c = c0;
-            for (uint32_t v = tid; v < p.T; v += NT * U) {
-                W reg[U];
-                uint32_t sidx[U];
-                bool ok[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const uint32_t vv = v + u * NT;
-                    bool valid = vv < p.T;
-                    if (valid && !full)
-                        valid = (c < Ls_valid) && (p.s_c_dim < 0 || S_c[r] < vc);
-                    ok[u] = valid;
-                    sidx[u] = r * p.pitch + c;
-                    if (valid) reg[u] = ld_stream(sp + S_off[r] + c);
-                    c += dC;
-                    r += dR;
-                    if (c >= p.Ls) {
-                        c -= p.Ls;
-                        ++r;
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u)
-                    if (ok[u]) tile[sidx[u]] = reg[u];
+        return full ? p.ph[ph].mask_full : p.ph[ph].mask_ragged;
+    };
+    {
+        uint32_t lim[3];
+        uint32_t m = limits(0, 0, lim);
+        tile_read<W, ASYNC>(p.ph[0], tr, smem, src + s_base[0][0], buf0, m, lim);
+        if constexpr (ASYNC) cp_async_commit();
+    }
+    uint32_t k = 0;
+    for (uint32_t t = first; t < p.num_tiles; t += step, ++k) {
+        const uint32_t tn = t + step;
+        if (tid < 32 && tn + step < p.num_tiles) decode_tile(p, tn + step, s_base, s_valid, (k + 2) & 3);
+        if constexpr (ASYNC) cp_async_wait_all();
+        __syncthreads();
+        const int cur = k & 3, nxt = (k + 1) & 3;
+        W *bcur = (k & 1) ? buf1 : buf0;
+        if constexpr (ASYNC) {
+            if (tn < p.num_tiles) {
+                uint32_t lim[3];
+                uint32_t m = limits(nxt, 0, lim);
+                tile_read<W, true>(p.ph[0], tr, smem, src + s_base[nxt][0], (k & 1) ? buf0 : buf1, m, lim);
+                cp_async_commit();
+            }
+            uint32_t lim[3];
+            uint32_t m = limits(cur, 1, lim);
+            tile_write<W>(p.ph[1], tw, smem, dst + s_base[cur][1], bcur, m, lim);
+        } else {
+            uint32_t lim[3];
+            uint32_t m = limits(cur, 1, lim);
+            tile_write<W>(p.ph[1], tw, smem, dst + s_base[cur][1], buf0, m, lim);
+            __syncthreads();
+            if (tn < p.num_tiles) {
+                m = limits(nxt, 0, lim);
+                tile_read<W, false>(p.ph[0], tr, smem, src + s_base[nxt][0], buf0, m, lim);
             }
         }
-        __syncthreads();
-        // ---- write phase: smem -> contiguous destination runs
-        {
-            W *dp = dst + db;
-            uint32_t q = q0, k = k0;
-            for (uint32_t v = tid; v < p.T; v += NT * U) {
-                W reg[U];
-                int64_t didx[U];
-                bool ok[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const uint32_t vv = v + u * NT;
-                    bool valid = vv < p.T;
-                    if (valid && !full)
-                        valid = (k < Ld_valid) && (p.w_a_dim < 0 || W_a[q] < va);
-                    ok[u] = valid;
-                    if (valid) {
-                        reg[u] = tile[W_sm[q] + A_sm[k]];
-                        didx[u] = W_off[q] + k;
-                    }
-                    k += dK;
-                    q += dQ;
-                    if (k >= p.Ld) {
-                        k -= p.Ld;
-                        ++q;
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u)
-                    if (ok[u]) dp[didx[u]] = reg[u];
-            }
-        }
-        __syncthreads();
     }
 }
 
@@ -331,12 +440,20 @@ int occupancy(K kernel, int threads, int smem) {
 template <int E>
 vpg_status launch_tile(const vpg_plan *p, const void *src, void *dst, cudaStream_t st) {
     using W = typename WordOf<E>::T;
-    auto k = tile_kernel<W>;
     const int smem = (int)p->tile.smem_bytes;
-    int nb = occupancy(k, p->threads, smem);
-    int64_t grid = std::min<int64_t>(p->tile.num_tiles, (int64_t)nb * sm_count_for_current());
-    if (grid < 1) grid = 1;
-    k<<<(unsigned)grid, p->threads, smem, st>>>(p->tile, (const W *)src, (W *)dst);
+    auto launch = [&](auto k) {
+        int nb = occupancy(k, p->threads, smem);
+        int64_t grid = std::min<int64_t>(p->tile.num_tiles, (int64_t)nb * sm_count_for_current());
+        if (grid < 1) grid = 1;
+        k<<<(unsigned)grid, p->threads, smem, st>>>(p->tile, (const W *)src, (W *)dst);
+    };
+    if constexpr (E >= 4) {
+        if (p->tile.nbuf == 2) {
+            launch(tile_kernel<W, true>);
+            return VPG_OK;
+        }
+    }
+    launch(tile_kernel<W, false>);
     return VPG_OK;
 }
 

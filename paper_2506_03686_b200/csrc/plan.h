@@ -59,13 +59,18 @@ inline uint32_t host_fastdiv(uint32_t n, FastDiv f) {
 // The remaining dims (and the tile positions along partial dims) form the
 // grid digits, ordered by destination stride (fastest first) like the
 // reference's counter digits (planner.py:324-342).
-struct TableDim {
-    uint32_t extent;     // tile extent along this dim
-    FastDiv div;         // divides by extent
-    int64_t gstride;     // global stride (src for S dims, dst for W dims) in elements
-    uint32_t sstride;    // shared-memory stride in elements
-    uint32_t pad_;
-};
+//
+// Each of the two phases (R: global->smem in source order, W: smem->global
+// in destination order) walks the tile as a separable 3-level nest so the
+// per-element work is two adds, one predicate and the memory op:
+//   thread part  -- the first phase dims (partial last one, factor f),
+//                   decoded once per CTA: per-thread global/smem offsets;
+//   inner dim    -- one dim with constant strides (stepped by f when it is
+//                   the split dim), unrolled;
+//   outer dims   -- the rest, through a per-CTA table in shared memory.
+// Threads beyond one thread part form G groups that share the outer loop.
+constexpr int kNumSlots = 3;      // checked coordinates: 0 = dim a, 1 = dim c, 2 = split padding
+constexpr int kMaxPhaseDims = 12; // thread-part / outer dims per phase
 
 struct GridDigit {
     FastDiv cum;         // divides tile index by the product of faster digits
@@ -74,28 +79,48 @@ struct GridDigit {
     int64_t dst_stride;
 };
 
+struct PhaseDim {
+    FastDiv div;         // divides by extent
+    int64_t gstride;     // global stride (elements; src for R, dst for W)
+    uint32_t sstride;    // smem stride (elements)
+    int32_t slot;        // coordinate slot fed by this dim (-1 none)
+};
+
+struct PhaseDesc {
+    uint32_t nthr;                 // threads in one thread part (NTP)
+    uint32_t ngroups;              // G
+    int32_t nthr_dims;
+    PhaseDim thr[kMaxPhaseDims];    // thread-part dims (fastest first)
+    uint32_t n_in;                 // inner-dim steps
+    int64_t g_in;                  // inner-dim global stride per step
+    uint32_t s_in;                 // inner-dim smem stride per step
+    uint32_t c_in[kNumSlots];      // inner-dim coordinate increment per slot
+    uint32_t n_outer;
+    int32_t nout_dims;
+    PhaseDim out[kMaxPhaseDims];    // outer dims (fastest first)
+    uint32_t mask_full;            // slots checked in every tile (padding)
+    uint32_t mask_ragged;          // slots checked in ragged tiles
+    uint32_t off_tab;              // smem byte offset of this phase's outer table
+};
+
 struct TileParams {
     uint32_t num_tiles;
     int32_t ngrid;
-    uint32_t Ls, Ns;           // source run length / number of source runs per tile
-    uint32_t Ld, Nd;           // destination run length / number of destination runs
-    uint32_t T;                // tile elements (= Ls*Ns = Ld*Nd)
-    uint32_t pitch;            // smem pitch of one source run (elements, >= Ls)
-    uint32_t Ls_unit, Ld_unit; // Ls / e_a, Ld / e_c (elements per step of a partial boundary dim)
+    uint32_t Ls, Ld;               // source / destination run lengths (elements)
+    uint32_t T;                    // tile elements
+    uint32_t pitch;                // smem pitch of one source run (elements, >= Ls)
+    uint32_t tile_elems_alloc;     // elements of one smem tile buffer (Ns * pitch)
     // ragged boundary dims: a = source-run boundary, c = destination-run boundary
-    int32_t grid_a, grid_c;    // grid digit carrying the tile position along a / c (-1: not partial)
+    int32_t grid_a, grid_c;        // grid digit carrying the tile position along a / c (-1: not partial)
     uint32_t e_a, d_a, e_c, d_c;
-    int32_t s_c_dim;           // index into S[] of dim c when c is a source run-index dim, else -1
-    int32_t w_a_dim;           // index into W[] of dim a when a is a destination run-index dim, else -1
-    int32_t nS, nA, nW;
-    TableDim S[kMaxTileDims];  // source run-index dims (source order): gstride = src stride
-    TableDim A[kMaxTileDims];  // destination-run dims (dest order): sstride only
-    TableDim W[kMaxTileDims];  // destination run-index dims (dest order): gstride = dst stride
+    uint32_t lim_split[2];         // static limit of slot 2 per phase (R, W)
+    PhaseDesc ph[2];               // 0 = R (read), 1 = W (write)
     GridDigit grid[kMaxRank];
-    // dynamic smem layout (byte offsets)
-    uint32_t off_S_off, off_S_c, off_W_off, off_W_sm, off_W_a, off_A, off_tile;
+    uint32_t off_buf;              // smem byte offset of the tile buffers
+    uint32_t nbuf;                 // 1 or 2 (double-buffered cp.async)
     uint32_t smem_bytes;
 };
+static_assert(sizeof(TileParams) <= 4096, "kernel parameter block must stay under 4 KB");
 
 // --------------------------------------------------------------------------
 // ROWS (K1): stride-1 preserved; each destination row of Lr elements is a
@@ -143,6 +168,7 @@ struct vpg_plan {
     int32_t threads;
     int64_t grid_hint;
     double predicted_eff;
+    double tile_util;
     vpg::TileParams tile;
     vpg::RowsParams rows;
     vpg::CopyParams copy;

@@ -251,37 +251,172 @@ int warp_wavefronts(const uint32_t *off, int nlanes, int E) {
     return total;
 }
 
-uint32_t decode_sm(const TableDim *dims, int n, uint32_t idx) {
-    uint32_t s = 0;
-    for (int i = 0; i < n; ++i) {
-        uint32_t c = idx % dims[i].extent;
-        idx /= dims[i].extent;
-        s += c * dims[i].sstride;
+// ------------------------------------------------------------- phase walks
+struct PDimH {
+    int64_t e, g, s;
+    int slot;
+};
+
+// Phase dims (fastest first) with adjacent dims fused when they are
+// contiguous in BOTH global and shared memory (and carry no checked slot).
+std::vector<PDimH> phase_dims(const Problem &Pb, const TileGeom &g, const int64_t *sstr,
+                              const int *slot_of_dim, bool write) {
+    std::vector<PDimH> L;
+    for (int i = 0; i < Pb.r; ++i) {
+        int k = write ? Pb.sigma[i] : i;
+        if (g.ext[k] == 0) continue;
+        PDimH d{g.ext[k], write ? Pb.out_stride_of_dim[k] : Pb.in_stride[k], sstr[k], slot_of_dim[k]};
+        if (!L.empty()) {
+            PDimH &p = L.back();
+            if (p.slot < 0 && d.slot < 0 && d.g == p.g * p.e && d.s == p.s * p.e) {
+                p.e *= d.e;
+                continue;
+            }
+        }
+        L.push_back(d);
     }
-    return s;
+    return L;
 }
 
-void set_table_dim(TableDim &t, int64_t extent, int64_t gstride, int64_t sstride) {
-    t.extent = (uint32_t)extent;
-    t.div = make_fastdiv((uint32_t)extent);
-    t.gstride = gstride;
-    t.sstride = (uint32_t)sstride;
-    t.pad_ = 0;
+void set_pdim(PhaseDim &pd, int64_t e, int64_t g, int64_t s, int slot) {
+    pd.div = make_fastdiv((uint32_t)e);
+    pd.gstride = g;
+    pd.sstride = (uint32_t)s;
+    pd.slot = slot;
+}
+
+// Choose the thread part (prefix dims, split factor f) maximising lane use;
+// fill the phase descriptor.  Returns the utilisation estimate.
+double make_phase(const std::vector<PDimH> &L, int NT, PhaseDesc &pd, uint32_t &lim_split) {
+    memset(&pd, 0, sizeof(pd));
+    const int m = (int)L.size();
+    double best = -1.0, best_u = 0.0;
+    int bh = 0;
+    int64_t bf = 1;
+    int64_t P = 1;
+    for (int h = 0; h < m && P <= NT; P *= L[h].e, ++h) {
+        for (int64_t f = 1; f <= L[h].e && P * f <= NT; ++f) {
+            int64_t ntp = P * f;
+            int64_t G = NT / ntp;
+            int64_t steps = (L[h].e + f - 1) / f;
+            int64_t rest = 1;
+            for (int i = h + 1; i < m; ++i) rest *= L[i].e;
+            // inner dim = h (if steps > 1) else h+1; outer count:
+            int64_t n_outer = steps > 1 ? rest : (h + 1 < m ? rest / L[h + 1].e : 1);
+            int64_t n_in = steps > 1 ? steps : (h + 1 < m ? L[h + 1].e : 1);
+            if (n_outer < 1) n_outer = 1;
+            if (G > n_outer) G = n_outer;
+            double lane = (double)(G * ntp) / NT;
+            double pad = (double)L[h].e / (double)(f * steps);
+            double bal = (double)n_outer / (double)(G * ((n_outer + G - 1) / G));
+            // coalescing: consecutive lanes must walk the stride-1 dim L[0]
+            double cover0 = (double)(h == 0 ? f : L[0].e);
+            double coal = std::min(1.0, cover0 / (double)std::min<int64_t>(32, L[0].e));
+            double u = lane * pad * bal * coal;
+            // ties: bigger thread parts (fewer outer-table steps), longer inner loops
+            double score = u + 1e-3 * std::log2((double)ntp) + 1e-4 * (steps * f == L[h].e) +
+                           1e-6 * std::min<int64_t>(n_in, 64);
+            if (h + (steps > 1 ? 1 : 2) > kMaxPhaseDims + 1) continue;
+            if (score > best) {
+                best = score;
+                best_u = u;
+                bh = h;
+                bf = f;
+            }
+        }
+    }
+    const int h = bh;
+    const int64_t f = bf;
+    int64_t ntp = 1;
+    pd.nthr_dims = 0;
+    for (int i = 0; i < h; ++i) {
+        set_pdim(pd.thr[pd.nthr_dims++], L[i].e, L[i].g, L[i].s, L[i].slot);
+        ntp *= L[i].e;
+    }
+    int64_t steps = (L[h].e + f - 1) / f;
+    int split_slot = L[h].slot;
+    bool padded = steps * f != L[h].e;
+    if (padded && split_slot < 0) {
+        split_slot = 2;
+        lim_split = (uint32_t)L[h].e;
+    }
+    set_pdim(pd.thr[pd.nthr_dims++], f, L[h].g, L[h].s, split_slot);
+    ntp *= f;
+    int first_outer;
+    if (steps > 1) {
+        pd.n_in = (uint32_t)steps;
+        pd.g_in = L[h].g * f;
+        pd.s_in = (uint32_t)(L[h].s * f);
+        if (split_slot >= 0) pd.c_in[split_slot] = (uint32_t)f;
+        first_outer = h + 1;
+    } else if (h + 1 < m) {
+        pd.n_in = (uint32_t)L[h + 1].e;
+        pd.g_in = L[h + 1].g;
+        pd.s_in = (uint32_t)L[h + 1].s;
+        if (L[h + 1].slot >= 0) pd.c_in[L[h + 1].slot] = 1;
+        first_outer = h + 2;
+    } else {
+        pd.n_in = 1;
+        pd.g_in = 0;
+        pd.s_in = 0;
+        first_outer = m;
+    }
+    pd.nout_dims = 0;
+    int64_t n_outer = 1;
+    for (int i = first_outer; i < m; ++i) {
+        set_pdim(pd.out[pd.nout_dims++], L[i].e, L[i].g, L[i].s, L[i].slot);
+        n_outer *= L[i].e;
+    }
+    pd.n_outer = (uint32_t)n_outer;
+    pd.nthr = (uint32_t)ntp;
+    int64_t G = NT / ntp;
+    if (G > n_outer) G = n_outer;
+    if (G < 1) G = 1;
+    pd.ngroups = (uint32_t)G;
+    pd.mask_full = padded ? (1u << split_slot) : 0u;
+    pd.mask_ragged = pd.mask_full;
+    for (const PDimH &d : L)
+        if (d.slot == 0 || d.slot == 1) pd.mask_ragged |= 1u << d.slot;
+    return best_u;
+}
+
+// smem offsets seen by the lanes of one warp at inner step 0 (simulation of
+// the kernel's mapping, for the bank-conflict model).
+void phase_warp_offsets(const PhaseDesc &pd, int warp, uint32_t *off, int &nl) {
+    nl = 0;
+    for (int l = 0; l < 32; ++l) {
+        uint32_t t = (uint32_t)(warp * 32 + l);
+        if (t >= pd.nthr * pd.ngroups) break;
+        uint32_t grp = t / pd.nthr, tr = t % pd.nthr;
+        uint32_t s = 0;
+        for (int i = 0; i < pd.nthr_dims; ++i) {
+            uint32_t q = tr / pd.thr[i].div.d;
+            s += (tr - q * pd.thr[i].div.d) * pd.thr[i].sstride;
+            tr = q;
+        }
+        uint32_t o = grp;
+        for (int i = 0; i < pd.nout_dims; ++i) {
+            uint32_t q = o / pd.out[i].div.d;
+            s += (o - q * pd.out[i].div.d) * pd.out[i].sstride;
+            o = q;
+        }
+        off[nl++] = s;
+    }
 }
 
 // Fill TileParams for geometry g with smem pitch P (elements).
-void fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, TileParams &tp) {
+double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, int NT, TileParams &tp) {
     memset(&tp, 0, sizeof(tp));
     const int r = Pb.r;
     tp.Ls = (uint32_t)g.Ls;
     tp.Ld = (uint32_t)g.Ld;
     tp.T = (uint32_t)g.T;
-    tp.Ns = (uint32_t)(g.T / g.Ls);
-    tp.Nd = (uint32_t)(g.T / g.Ld);
     tp.pitch = pitch;
-    // smem strides: source run dims dense, then run-index dims scaled by pitch
+    const uint32_t Ns = (uint32_t)(g.T / g.Ls);
+    tp.tile_elems_alloc = Ns * pitch;
+    // smem strides: source run dims dense, run-index dims scaled by the pitch
     int64_t sstr[kMaxRank];
-    bool in_src[kMaxRank] = {false}, in_dst[kMaxRank] = {false};
+    bool in_src[kMaxRank] = {false};
     int64_t acc = 1;
     for (int i = 0; i < g.nsrc; ++i) {
         int k = g.src_dims[i];
@@ -289,30 +424,18 @@ void fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, Tile
         sstr[k] = acc;
         acc *= g.ext[k];
     }
-    for (int i = 0; i < g.ndst; ++i) in_dst[g.dst_dims[i]] = true;
     acc = pitch;
-    tp.nS = 0;
-    tp.s_c_dim = -1;
     for (int k = 0; k < r; ++k) {
         if (g.ext[k] == 0 || in_src[k]) continue;
         sstr[k] = acc;
-        if (k == g.c_part) tp.s_c_dim = tp.nS;
-        set_table_dim(tp.S[tp.nS++], g.ext[k], Pb.in_stride[k], acc);
         acc *= g.ext[k];
     }
-    tp.nA = 0;
-    for (int i = 0; i < g.ndst; ++i) {
-        int k = g.dst_dims[i];
-        set_table_dim(tp.A[tp.nA++], g.ext[k], Pb.out_stride_of_dim[k], sstr[k]);
-    }
-    tp.nW = 0;
-    tp.w_a_dim = -1;
-    for (int j = 0; j < r; ++j) {
-        int k = Pb.sigma[j];
-        if (g.ext[k] == 0 || in_dst[k]) continue;
-        if (k == g.a_part) tp.w_a_dim = tp.nW;
-        set_table_dim(tp.W[tp.nW++], g.ext[k], Pb.out_stride_of_dim[k], sstr[k]);
-    }
+    int slot_of_dim[kMaxRank];
+    for (int k = 0; k < r; ++k) slot_of_dim[k] = -1;
+    if (g.a_part >= 0) slot_of_dim[g.a_part] = 0;
+    if (g.c_part >= 0 && g.c_part != g.a_part) slot_of_dim[g.c_part] = 1;
+    double u0 = make_phase(phase_dims(Pb, g, sstr, slot_of_dim, false), NT, tp.ph[0], tp.lim_split[0]);
+    double u1 = make_phase(phase_dims(Pb, g, sstr, slot_of_dim, true), NT, tp.ph[1], tp.lim_split[1]);
     // grid digits
     struct Dg {
         int64_t ext, ss, ds;
@@ -330,76 +453,55 @@ void fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, Tile
     tp.grid_a = tp.grid_c = -1;
     uint64_t cum = 1;
     for (size_t i = 0; i < dg.size(); ++i) {
-        tp.grid[i].cum = make_fastdiv((uint32_t)cum);
+        tp.grid[i].cum = make_fastdiv((uint32_t)std::min<uint64_t>(cum, 0xffffffffull));
         tp.grid[i].ext = make_fastdiv((uint32_t)dg[i].ext);
         tp.grid[i].src_stride = dg[i].ss;
         tp.grid[i].dst_stride = dg[i].ds;
         if (dg[i].dim >= 0 && dg[i].dim == g.a_part) tp.grid_a = (int32_t)i;
-        if (dg[i].dim >= 0 && dg[i].dim == g.c_part) tp.grid_c = (int32_t)i;
+        if (dg[i].dim >= 0 && dg[i].dim == g.c_part && g.c_part != g.a_part) tp.grid_c = (int32_t)i;
         cum *= (uint64_t)dg[i].ext;
     }
-    tp.num_tiles = (uint32_t)cum;
-    if (g.a_part >= 0) {
-        tp.e_a = (uint32_t)g.ext[g.a_part];
-        tp.d_a = (uint32_t)Pb.d[g.a_part];
-    } else {
-        tp.e_a = tp.d_a = 1;
-    }
-    if (g.c_part >= 0) {
-        tp.e_c = (uint32_t)g.ext[g.c_part];
-        tp.d_c = (uint32_t)Pb.d[g.c_part];
-    } else {
-        tp.e_c = tp.d_c = 1;
-    }
-    tp.Ls_unit = g.a_part >= 0 ? (uint32_t)(g.Ls / g.ext[g.a_part]) : tp.Ls;
-    tp.Ld_unit = g.c_part >= 0 ? (uint32_t)(g.Ld / g.ext[g.c_part]) : tp.Ld;
+    tp.num_tiles = (uint32_t)std::min<uint64_t>(cum, 0xffffffffull);
+    tp.e_a = g.a_part >= 0 ? (uint32_t)g.ext[g.a_part] : 1u;
+    tp.d_a = g.a_part >= 0 ? (uint32_t)Pb.d[g.a_part] : 1u;
+    bool c_slot = g.c_part >= 0 && g.c_part != g.a_part;
+    tp.e_c = c_slot ? (uint32_t)g.ext[g.c_part] : 1u;
+    tp.d_c = c_slot ? (uint32_t)Pb.d[g.c_part] : 1u;
     // dynamic smem layout
     uint32_t o = 0;
-    auto take = [&](uint32_t bytes, uint32_t al) {
+    auto take = [&](uint64_t bytes, uint32_t al) {
         o = (o + al - 1) / al * al;
         uint32_t at = o;
-        o += bytes;
+        o += (uint32_t)bytes;
         return at;
     };
-    tp.off_S_off = take(8 * tp.Ns, 16);
-    tp.off_W_off = take(8 * tp.Nd, 16);
-    tp.off_W_sm = take(4 * tp.Nd, 16);
-    tp.off_A = take(4 * tp.Ld, 16);
-    tp.off_S_c = take(tp.s_c_dim >= 0 ? 4 * tp.Ns : 0, 16);
-    tp.off_W_a = take(tp.w_a_dim >= 0 ? 4 * tp.Nd : 0, 16);
-    tp.off_tile = take((uint32_t)((uint64_t)tp.Ns * pitch * Pb.E), 16);
+    tp.ph[0].off_tab = take(16ull * tp.ph[0].n_outer, 16);
+    tp.ph[1].off_tab = take(16ull * tp.ph[1].n_outer, 16);
+    tp.nbuf = Pb.E >= 4 ? 2 : 1;
+    uint64_t buf_bytes = ((uint64_t)tp.tile_elems_alloc * Pb.E + 15) / 16 * 16;
+    tp.off_buf = take(buf_bytes * tp.nbuf, 16);
     tp.smem_bytes = (o + 15) / 16 * 16;
+    return u0 * u1;
 }
 
 // Choose the source-run pitch that minimises modelled smem wavefronts of
-// both phases (read: flattened (r,c); write: flattened (rd,cd)).
-uint32_t choose_pitch(const Problem &Pb, const TileGeom &g, int threads) {
+// both phases' warp accesses.
+uint32_t choose_pitch(const Problem &Pb, const TileGeom &g, int NT) {
     uint32_t best_p = (uint32_t)g.Ls;
     int64_t best_w = -1;
-    const int maxpad = 32;
-    for (int pad = 0; pad <= maxpad; ++pad) {
+    for (int pad = 0; pad <= 32; ++pad) {
         uint32_t pitch = (uint32_t)g.Ls + pad;
         if ((int64_t)(g.T / g.Ls) * pitch * Pb.E > kTileBudgetBytes + 8192) break;
         TileParams tp;
-        fill_tile_params(Pb, g, pitch, tp);
+        fill_tile_params(Pb, g, pitch, NT, tp);
         int64_t waves = 0;
-        // simulate the first `threads` lanes of each phase, warp by warp
         uint32_t off[32];
-        int64_t nel = std::min<int64_t>(g.T, (int64_t)threads * 4);
-        for (int64_t w0 = 0; w0 < nel; w0 += 32) {
-            int nl = (int)std::min<int64_t>(32, g.T - w0);
-            for (int l = 0; l < nl; ++l) {
-                uint32_t v = (uint32_t)(w0 + l);
-                off[l] = (v / tp.Ls) * pitch + v % tp.Ls;
+        int nl;
+        for (int ph = 0; ph < 2; ++ph)
+            for (int w = 0; w < NT / 32; ++w) {
+                phase_warp_offsets(tp.ph[ph], w, off, nl);
+                if (nl) waves += warp_wavefronts(off, nl, Pb.E);
             }
-            waves += warp_wavefronts(off, nl, Pb.E);
-            for (int l = 0; l < nl; ++l) {
-                uint32_t v = (uint32_t)(w0 + l);
-                uint32_t rd = v / tp.Ld, cd = v % tp.Ld;
-                off[l] = decode_sm(tp.W, tp.nW, rd) + decode_sm(tp.A, tp.nA, cd);
-            }
-            waves += warp_wavefronts(off, nl, Pb.E);
-        }
         if (best_w < 0 || waves < best_w) {
             best_w = waves;
             best_p = pitch;
@@ -467,11 +569,19 @@ static void describe(vpg_plan *p) {
     put(")\nelements: %lld\n", (long long)p->n);
     if (p->kernel_class == VPG_KERNEL_TILE) {
         const TileParams &t = p->tile;
-        put("tile elements: %u (src run %u x %u runs, dst run %u x %u runs)\n", t.T, t.Ls, t.Ns,
-            t.Ld, t.Nd);
-        put("smem pitch: %u, smem bytes: %u\n", t.pitch, t.smem_bytes);
+        put("tile elements: %u (src run %u x %u runs, dst run %u x %u runs)\n", t.T, t.Ls, t.T / t.Ls,
+            t.Ld, t.T / t.Ld);
+        put("smem pitch: %u, smem bytes: %u, buffers: %u\n", t.pitch, t.smem_bytes, t.nbuf);
         put("ragged boundary dims: a(extent %u of %u) c(extent %u of %u)\n", t.e_a, t.d_a, t.e_c,
             t.d_c);
+        for (int ph = 0; ph < 2; ++ph) {
+            const PhaseDesc &d = t.ph[ph];
+            put("phase %s: %u threads x %u groups, thread dims %d, inner %u steps, outer %u (dims %d), "
+                "check mask full=%u ragged=%u\n",
+                ph ? "W" : "R", d.nthr, d.ngroups, d.nthr_dims, d.n_in, d.n_outer, d.nout_dims,
+                d.mask_full, d.mask_ragged);
+        }
+        put("lane utilisation (R*W): %.3f\n", p->tile_util);
         put("tiles: %u, grid digits: %d\n", t.num_tiles, t.ngrid);
     } else if (p->kernel_class == VPG_KERNEL_ROWS) {
         put("rows: %u x %lld elements, vector %u elements, %u threads/row\n", p->rows.nrows,
@@ -603,7 +713,7 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         p->kernel_class = VPG_KERNEL_TILE;
         int threads = g.T >= 1024 ? kTileThreads : (g.T >= 256 ? 128 : 64);
         uint32_t pitch = choose_pitch(P, g, threads);
-        fill_tile_params(P, g, pitch, p->tile);
+        p->tile_util = fill_tile_params(P, g, pitch, threads, p->tile);
         // the tile count must fit the 32-bit tile index
         double nt = 1.0;
         for (int i = 0; i < p->tile.ngrid; ++i) nt *= p->tile.grid[i].ext.d;
