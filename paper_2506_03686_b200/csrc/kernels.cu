@@ -122,7 +122,7 @@ struct OuterEntry {
 struct ThreadPart {
     int64_t g;
     uint32_t s;
-    uint32_t c[kNumSlots];
+    uint32_t c0, c1, c2;
     uint32_t grp;
     bool active;
 };
@@ -145,29 +145,37 @@ __device__ __forceinline__ ThreadPart decode_thread(const PhaseDesc &d, uint32_t
     t.active = t.grp < d.ngroups;
     t.g = 0;
     t.s = 0;
-    t.c[0] = t.c[1] = t.c[2] = 0;
+    t.c0 = t.c1 = t.c2 = 0;
     for (int i = 0; i < d.nthr_dims; ++i) {
         uint32_t q = fdiv(tr, d.thr[i].div);
         uint32_t c = tr - q * d.thr[i].div.d;
         tr = q;
         t.g += (int64_t)c * d.thr[i].gstride;
         t.s += c * d.thr[i].sstride;
-        if (d.thr[i].slot >= 0) t.c[d.thr[i].slot] = c;
+        const uint32_t cv = c * d.thr[i].cmul;
+        if (d.thr[i].slot == 0) t.c0 = cv;
+        else if (d.thr[i].slot == 1) t.c1 = cv;
+        else if (d.thr[i].slot == 2) t.c2 = cv;
     }
     return t;
 }
 
-__device__ __forceinline__ bool slot_ok(uint32_t mask, uint32_t c0, uint32_t c1, uint32_t c2, const uint32_t *lim) {
-    return (!(mask & 1u) || c0 < lim[0]) && (!(mask & 2u) || c1 < lim[1]) && (!(mask & 4u) || c2 < lim[2]);
+struct Lim {
+    uint32_t l0, l1, l2;
+};
+
+__device__ __forceinline__ bool slot_ok(uint32_t mask, uint32_t c0, uint32_t c1, uint32_t c2, const Lim &lim) {
+    return (!(mask & 1u) || c0 < lim.l0) && (!(mask & 2u) || c1 < lim.l1) && (!(mask & 4u) || c2 < lim.l2);
 }
 
-// R phase: global (source order) -> smem.  ASYNC: cp.async, else LDG+STS.
-template <typename W, bool ASYNC>
-__device__ __forceinline__ void tile_read(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
-                                          const W *__restrict__ gsrc, W *buf, uint32_t mask,
-                                          const uint32_t *lim) {
-    if (!t.active) return;
+// R phase: global (source order) -> smem.  ASYNC: cp.async (16-byte chunks
+// when d.vec > 1), else LDG+STS.
+template <typename W, bool ASYNC, bool VEC>
+__device__ __forceinline__ void tile_read_impl(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
+                                               const W *__restrict__ gsrc, W *buf, uint32_t mask,
+                                               const Lim lim) {
     constexpr int U = 4;
+    constexpr int CP = VEC ? 16 : (int)sizeof(W);
     const OuterEntry *tab = reinterpret_cast<const OuterEntry *>(smem + d.off_tab);
     const uint32_t n_in = d.n_in;
     const int64_t g_in = d.g_in;
@@ -181,7 +189,7 @@ __device__ __forceinline__ void tile_read(const PhaseDesc &d, const ThreadPart &
             for (; i + U <= n_in; i += U) {
                 if constexpr (ASYNC) {
 #pragma unroll
-                    for (int u = 0; u < U; ++u) cp_async<sizeof(W)>(sp + u * s_in, gp + u * g_in);
+                    for (int u = 0; u < U; ++u) cp_async<CP>(sp + u * s_in, gp + u * g_in);
                 } else {
                     W v[U];
 #pragma unroll
@@ -193,16 +201,16 @@ __device__ __forceinline__ void tile_read(const PhaseDesc &d, const ThreadPart &
                 sp += U * s_in;
             }
             for (; i < n_in; ++i) {
-                if constexpr (ASYNC) cp_async<sizeof(W)>(sp, gp);
+                if constexpr (ASYNC) cp_async<CP>(sp, gp);
                 else *sp = __ldg(gp);
                 gp += g_in;
                 sp += s_in;
             }
         } else {
-            uint32_t c0 = t.c[0] + e.c0, c1 = t.c[1] + e.c1, c2 = t.c[2];
+            uint32_t c0 = t.c0 + e.c0, c1 = t.c1 + e.c1, c2 = t.c2;
             for (uint32_t i = 0; i < n_in; ++i) {
                 if (slot_ok(mask, c0, c1, c2, lim)) {
-                    if constexpr (ASYNC) cp_async<sizeof(W)>(sp, gp);
+                    if constexpr (ASYNC) cp_async<CP>(sp, gp);
                     else *sp = __ldg(gp);
                 }
                 gp += g_in;
@@ -215,17 +223,35 @@ __device__ __forceinline__ void tile_read(const PhaseDesc &d, const ThreadPart &
     }
 }
 
-// W phase: smem -> global (destination order).
-template <typename W>
-__device__ __forceinline__ void tile_write(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
-                                           W *__restrict__ gdst, const W *buf, uint32_t mask,
-                                           const uint32_t *lim) {
+template <typename W, bool ASYNC>
+__device__ __forceinline__ void tile_read(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
+                                          const W *__restrict__ gsrc, W *buf, uint32_t mask,
+                                          const Lim lim) {
     if (!t.active) return;
-    constexpr int U = 4;
+    if constexpr (ASYNC && sizeof(W) < 16) {
+        if (d.vec > 1) {
+            tile_read_impl<W, true, true>(d, t, smem, gsrc, buf, mask, lim);
+            return;
+        }
+    }
+    tile_read_impl<W, ASYNC, false>(d, t, smem, gsrc, buf, mask, lim);
+}
+
+// W phase: smem -> global (destination order).  VEC: each position is a
+// 16-byte smem vector of V consecutive dim-0 elements, stored to V
+// destinations d.vstride apart (each store instruction stays coalesced
+// across the warp's lanes).
+template <typename W, bool VEC>
+__device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
+                                                W *__restrict__ gdst, const W *buf, uint32_t mask,
+                                                const Lim lim) {
+    constexpr int U = VEC ? 2 : 4;
+    constexpr int V = VEC ? 16 / (int)sizeof(W) : 1;
     const OuterEntry *tab = reinterpret_cast<const OuterEntry *>(smem + d.off_tab);
     const uint32_t n_in = d.n_in;
     const int64_t g_in = d.g_in;
     const uint32_t s_in = d.s_in;
+    const int64_t vs = d.vstride;
     for (uint32_t o = t.grp; o < d.n_outer; o += d.ngroups) {
         const OuterEntry e = tab[o];
         W *gp = gdst + (t.g + e.g);
@@ -233,23 +259,51 @@ __device__ __forceinline__ void tile_write(const PhaseDesc &d, const ThreadPart 
         if (mask == 0) {
             uint32_t i = 0;
             for (; i + U <= n_in; i += U) {
-                W v[U];
+                if constexpr (VEC) {
+                    uint4 v[U];
 #pragma unroll
-                for (int u = 0; u < U; ++u) v[u] = sp[u * s_in];
+                    for (int u = 0; u < U; ++u) v[u] = *reinterpret_cast<const uint4 *>(sp + u * s_in);
 #pragma unroll
-                for (int u = 0; u < U; ++u) gp[u * g_in] = v[u];
+                    for (int u = 0; u < U; ++u) {
+                        const W *w = reinterpret_cast<const W *>(&v[u]);
+#pragma unroll
+                        for (int j = 0; j < V; ++j) gp[u * g_in + j * vs] = w[j];
+                    }
+                } else {
+                    W v[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) v[u] = sp[u * s_in];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) gp[u * g_in] = v[u];
+                }
                 gp += U * g_in;
                 sp += U * s_in;
             }
             for (; i < n_in; ++i) {
-                *gp = *sp;
+                if constexpr (VEC) {
+                    uint4 v = *reinterpret_cast<const uint4 *>(sp);
+                    const W *w = reinterpret_cast<const W *>(&v);
+#pragma unroll
+                    for (int j = 0; j < V; ++j) gp[j * vs] = w[j];
+                } else {
+                    *gp = *sp;
+                }
                 gp += g_in;
                 sp += s_in;
             }
         } else {
-            uint32_t c0 = t.c[0] + e.c0, c1 = t.c[1] + e.c1, c2 = t.c[2];
+            uint32_t c0 = t.c0 + e.c0, c1 = t.c1 + e.c1, c2 = t.c2;
             for (uint32_t i = 0; i < n_in; ++i) {
-                if (slot_ok(mask, c0, c1, c2, lim)) *gp = *sp;
+                if (slot_ok(mask, c0, c1, c2, lim)) {
+                    if constexpr (VEC) {
+                        uint4 v = *reinterpret_cast<const uint4 *>(sp);
+                        const W *w = reinterpret_cast<const W *>(&v);
+#pragma unroll
+                        for (int j = 0; j < V; ++j) gp[j * vs] = w[j];
+                    } else {
+                        *gp = *sp;
+                    }
+                }
                 gp += g_in;
                 sp += s_in;
                 c0 += d.c_in[0];
@@ -258,6 +312,20 @@ __device__ __forceinline__ void tile_write(const PhaseDesc &d, const ThreadPart 
             }
         }
     }
+}
+
+template <typename W>
+__device__ __forceinline__ void tile_write(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
+                                           W *__restrict__ gdst, const W *buf, uint32_t mask,
+                                           const Lim lim) {
+    if (!t.active) return;
+    if constexpr (sizeof(W) == 4 || sizeof(W) == 8) {
+        if (d.vec > 1) {
+            tile_write_impl<W, true>(d, t, smem, gdst, buf, mask, lim);
+            return;
+        }
+    }
+    tile_write_impl<W, false>(d, t, smem, gdst, buf, mask, lim);
 }
 
 // Warp 0 decodes tile `t` into slot `k`: source/destination base offsets and
@@ -316,8 +384,8 @@ __global__ void __launch_bounds__(256) tile_kernel(const __grid_constant__ TileP
                 idx = q;
                 g += (int64_t)c * d.out[i].gstride;
                 s += c * d.out[i].sstride;
-                if (d.out[i].slot == 0) c0 = c;
-                else if (d.out[i].slot == 1) c1 = c;
+                if (d.out[i].slot == 0) c0 = c * d.out[i].cmul;
+                else if (d.out[i].slot == 1) c1 = c * d.out[i].cmul;
             }
             OuterEntry e;
             e.g = g;
@@ -337,16 +405,16 @@ __global__ void __launch_bounds__(256) tile_kernel(const __grid_constant__ TileP
         if (first + step < p.num_tiles) decode_tile(p, first + step, s_base, s_valid, 1);
     }
     __syncthreads();
-    auto limits = [&](int k, int ph, uint32_t *lim) -> uint32_t {
+    auto limits = [&](int k, int ph, Lim &lim) -> uint32_t {
         const uint32_t va = s_valid[k][0], vc = s_valid[k][1];
-        lim[0] = va;
-        lim[1] = vc;
-        lim[2] = p.lim_split[ph];
+        lim.l0 = va;
+        lim.l1 = vc;
+        lim.l2 = p.lim_split[ph];
         const bool full = (va == p.e_a) && (vc == p.e_c);
         return full ? p.ph[ph].mask_full : p.ph[ph].mask_ragged;
     };
     {
-        uint32_t lim[3];
+        Lim lim;
         uint32_t m = limits(0, 0, lim);
         tile_read<W, ASYNC>(p.ph[0], tr, smem, src + s_base[0][0], buf0, m, lim);
         if constexpr (ASYNC) cp_async_commit();
@@ -361,16 +429,16 @@ __global__ void __launch_bounds__(256) tile_kernel(const __grid_constant__ TileP
         W *bcur = (k & 1) ? buf1 : buf0;
         if constexpr (ASYNC) {
             if (tn < p.num_tiles) {
-                uint32_t lim[3];
+                Lim lim;
                 uint32_t m = limits(nxt, 0, lim);
                 tile_read<W, true>(p.ph[0], tr, smem, src + s_base[nxt][0], (k & 1) ? buf0 : buf1, m, lim);
                 cp_async_commit();
             }
-            uint32_t lim[3];
+            Lim lim;
             uint32_t m = limits(cur, 1, lim);
             tile_write<W>(p.ph[1], tw, smem, dst + s_base[cur][1], bcur, m, lim);
         } else {
-            uint32_t lim[3];
+            Lim lim;
             uint32_t m = limits(cur, 1, lim);
             tile_write<W>(p.ph[1], tw, smem, dst + s_base[cur][1], buf0, m, lim);
             __syncthreads();
@@ -443,9 +511,11 @@ vpg_status launch_tile(const vpg_plan *p, const void *src, void *dst, cudaStream
     const int smem = (int)p->tile.smem_bytes;
     auto launch = [&](auto k) {
         int nb = occupancy(k, p->threads, smem);
-        int64_t grid = std::min<int64_t>(p->tile.num_tiles, (int64_t)nb * sm_count_for_current());
+        int64_t grid = p->tile.num_tiles;
+        if (p->tile.persistent) grid = std::min<int64_t>(grid, (int64_t)nb * sm_count_for_current());
         if (grid < 1) grid = 1;
-        k<<<(unsigned)grid, p->threads, smem, st>>>(p->tile, (const W *)src, (W *)dst);
+        const TileParams &tp = (p->tile.ph[0].vec > 1 && ((uintptr_t)src % 16)) ? p->tile_unaligned : p->tile;
+        k<<<(unsigned)grid, p->threads, smem, st>>>(tp, (const W *)src, (W *)dst);
     };
     if constexpr (E >= 4) {
         if (p->tile.nbuf == 2) {

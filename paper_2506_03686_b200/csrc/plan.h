@@ -83,7 +83,8 @@ struct PhaseDim {
     FastDiv div;         // divides by extent
     int64_t gstride;     // global stride (elements; src for R, dst for W)
     uint32_t sstride;    // smem stride (elements)
-    int32_t slot;        // coordinate slot fed by this dim (-1 none)
+    int16_t slot;        // coordinate slot fed by this dim (-1 none)
+    uint16_t cmul;       // coordinate units per step (V for vector-grouped dims)
 };
 
 struct PhaseDesc {
@@ -98,6 +99,8 @@ struct PhaseDesc {
     uint32_t n_outer;
     int32_t nout_dims;
     PhaseDim out[kMaxPhaseDims];    // outer dims (fastest first)
+    uint32_t vec;                  // elements per access: 1, or V = 16/E (16-byte accesses)
+    int64_t vstride;               // W with vec > 1: global stride between the V elements
     uint32_t mask_full;            // slots checked in every tile (padding)
     uint32_t mask_ragged;          // slots checked in ragged tiles
     uint32_t off_tab;              // smem byte offset of this phase's outer table
@@ -118,6 +121,7 @@ struct TileParams {
     GridDigit grid[kMaxRank];
     uint32_t off_buf;              // smem byte offset of the tile buffers
     uint32_t nbuf;                 // 1 or 2 (double-buffered cp.async)
+    uint32_t persistent;           // 1: grid = resident CTAs, 0: one CTA per tile
     uint32_t smem_bytes;
 };
 static_assert(sizeof(TileParams) <= 4096, "kernel parameter block must stay under 4 KB");
@@ -170,6 +174,7 @@ struct vpg_plan {
     double predicted_eff;
     double tile_util;
     vpg::TileParams tile;
+    vpg::TileParams tile_unaligned;   // same tile, scalar source reads
     vpg::RowsParams rows;
     vpg::CopyParams copy;
     vpg::GatherParams gather;

@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <vector>
@@ -57,6 +58,8 @@ double expected_sectors(int64_t bytes, int64_t align) {
 }
 
 struct Problem {
+    int64_t budget;       // staged tile bytes per CTA buffer
+    int nbuf;             // 1 or 2 smem buffers
     int r;
     int64_t d[kMaxRank];
     int sigma[kMaxRank];
@@ -186,7 +189,7 @@ std::vector<int64_t> extent_candidates(int64_t d, int64_t cap) {
 
 bool select_tile(const Problem &P, TileGeom &best) {
     const int r = P.r;
-    const int64_t maxT = std::max<int64_t>(kTileBudgetBytes / P.E, 64);
+    const int64_t maxT = std::max<int64_t>(P.budget / P.E, 64);
     bool found = false;
     best.cost = 1e300;
     int64_t ext[kMaxRank];
@@ -255,34 +258,78 @@ int warp_wavefronts(const uint32_t *off, int nlanes, int E) {
 struct PDimH {
     int64_t e, g, s;
     int slot;
+    int64_t cmul;
 };
+
+// Vectorisation choice for one tile: R groups the leading source-run entry
+// into 16-byte cp.async chunks; W groups V consecutive dim-0 elements into
+// one 16-byte shared-memory load feeding V coalesced scalar stores.
+struct VecChoice {
+    int vr = 1, vw = 1;
+};
+
+// smem strides of the tile dims for a given pitch (source run dense, run
+// index dims scaled by the pitch).
+void tile_sstrides(const Problem &Pb, const TileGeom &g, uint32_t pitch, int64_t *sstr, bool *in_src) {
+    for (int k = 0; k < Pb.r; ++k) in_src[k] = false;
+    int64_t acc = 1;
+    for (int i = 0; i < g.nsrc; ++i) {
+        int k = g.src_dims[i];
+        in_src[k] = true;
+        sstr[k] = acc;
+        acc *= g.ext[k];
+    }
+    acc = pitch;
+    for (int k = 0; k < Pb.r; ++k) {
+        if (g.ext[k] == 0 || in_src[k]) continue;
+        sstr[k] = acc;
+        acc *= g.ext[k];
+    }
+}
 
 // Phase dims (fastest first) with adjacent dims fused when they are
 // contiguous in BOTH global and shared memory (and carry no checked slot).
+// R with vr > 1: the leading entry is grouped by vr.  W with vw > 1: dim 0
+// is grouped by vw (its V elements are one smem vector, stored separately).
 std::vector<PDimH> phase_dims(const Problem &Pb, const TileGeom &g, const int64_t *sstr,
-                              const int *slot_of_dim, bool write) {
+                              const int *slot_of_dim, bool write, int vec) {
     std::vector<PDimH> L;
     for (int i = 0; i < Pb.r; ++i) {
         int k = write ? Pb.sigma[i] : i;
         if (g.ext[k] == 0) continue;
-        PDimH d{g.ext[k], write ? Pb.out_stride_of_dim[k] : Pb.in_stride[k], sstr[k], slot_of_dim[k]};
+        PDimH d{g.ext[k], write ? Pb.out_stride_of_dim[k] : Pb.in_stride[k], sstr[k], slot_of_dim[k], 1};
+        if (write && vec > 1 && k == 0) {
+            d.e /= vec;
+            d.g *= vec;
+            d.s *= vec;
+            d.cmul = vec;
+        }
         if (!L.empty()) {
             PDimH &p = L.back();
-            if (p.slot < 0 && d.slot < 0 && d.g == p.g * p.e && d.s == p.s * p.e) {
+            if (p.slot < 0 && d.slot < 0 && d.g == p.g * p.e && d.s == p.s * p.e &&
+                !(write && vec > 1 && k == 0)) {
                 p.e *= d.e;
                 continue;
             }
         }
         L.push_back(d);
     }
+    if (!write && vec > 1) {
+        PDimH &f = L.front();
+        f.e /= vec;
+        f.g *= vec;
+        f.s *= vec;
+        f.cmul *= vec;
+    }
     return L;
 }
 
-void set_pdim(PhaseDim &pd, int64_t e, int64_t g, int64_t s, int slot) {
+void set_pdim(PhaseDim &pd, int64_t e, int64_t g, int64_t s, int slot, int64_t cmul) {
     pd.div = make_fastdiv((uint32_t)e);
     pd.gstride = g;
     pd.sstride = (uint32_t)s;
-    pd.slot = slot;
+    pd.slot = (int16_t)slot;
+    pd.cmul = (uint16_t)cmul;
 }
 
 // Choose the thread part (prefix dims, split factor f) maximising lane use;
@@ -295,15 +342,17 @@ double make_phase(const std::vector<PDimH> &L, int NT, PhaseDesc &pd, uint32_t &
     int64_t bf = 1;
     int64_t P = 1;
     for (int h = 0; h < m && P <= NT; P *= L[h].e, ++h) {
+        if (h + 1 > kMaxPhaseDims) break;
         for (int64_t f = 1; f <= L[h].e && P * f <= NT; ++f) {
             int64_t ntp = P * f;
             int64_t G = NT / ntp;
             int64_t steps = (L[h].e + f - 1) / f;
             int64_t rest = 1;
             for (int i = h + 1; i < m; ++i) rest *= L[i].e;
-            // inner dim = h (if steps > 1) else h+1; outer count:
             int64_t n_outer = steps > 1 ? rest : (h + 1 < m ? rest / L[h + 1].e : 1);
             int64_t n_in = steps > 1 ? steps : (h + 1 < m ? L[h + 1].e : 1);
+            int nout_dims = m - (steps > 1 ? h + 1 : h + 2);
+            if (nout_dims > kMaxPhaseDims) continue;
             if (n_outer < 1) n_outer = 1;
             if (G > n_outer) G = n_outer;
             double lane = (double)(G * ntp) / NT;
@@ -316,7 +365,6 @@ double make_phase(const std::vector<PDimH> &L, int NT, PhaseDesc &pd, uint32_t &
             // ties: bigger thread parts (fewer outer-table steps), longer inner loops
             double score = u + 1e-3 * std::log2((double)ntp) + 1e-4 * (steps * f == L[h].e) +
                            1e-6 * std::min<int64_t>(n_in, 64);
-            if (h + (steps > 1 ? 1 : 2) > kMaxPhaseDims + 1) continue;
             if (score > best) {
                 best = score;
                 best_u = u;
@@ -330,7 +378,7 @@ double make_phase(const std::vector<PDimH> &L, int NT, PhaseDesc &pd, uint32_t &
     int64_t ntp = 1;
     pd.nthr_dims = 0;
     for (int i = 0; i < h; ++i) {
-        set_pdim(pd.thr[pd.nthr_dims++], L[i].e, L[i].g, L[i].s, L[i].slot);
+        set_pdim(pd.thr[pd.nthr_dims++], L[i].e, L[i].g, L[i].s, L[i].slot, L[i].cmul);
         ntp *= L[i].e;
     }
     int64_t steps = (L[h].e + f - 1) / f;
@@ -338,22 +386,22 @@ double make_phase(const std::vector<PDimH> &L, int NT, PhaseDesc &pd, uint32_t &
     bool padded = steps * f != L[h].e;
     if (padded && split_slot < 0) {
         split_slot = 2;
-        lim_split = (uint32_t)L[h].e;
+        lim_split = (uint32_t)(L[h].e * L[h].cmul);
     }
-    set_pdim(pd.thr[pd.nthr_dims++], f, L[h].g, L[h].s, split_slot);
+    set_pdim(pd.thr[pd.nthr_dims++], f, L[h].g, L[h].s, split_slot, L[h].cmul);
     ntp *= f;
     int first_outer;
     if (steps > 1) {
         pd.n_in = (uint32_t)steps;
         pd.g_in = L[h].g * f;
         pd.s_in = (uint32_t)(L[h].s * f);
-        if (split_slot >= 0) pd.c_in[split_slot] = (uint32_t)f;
+        if (split_slot >= 0) pd.c_in[split_slot] = (uint32_t)(f * L[h].cmul);
         first_outer = h + 1;
     } else if (h + 1 < m) {
         pd.n_in = (uint32_t)L[h + 1].e;
         pd.g_in = L[h + 1].g;
         pd.s_in = (uint32_t)L[h + 1].s;
-        if (L[h + 1].slot >= 0) pd.c_in[L[h + 1].slot] = 1;
+        if (L[h + 1].slot >= 0) pd.c_in[L[h + 1].slot] = (uint32_t)L[h + 1].cmul;
         first_outer = h + 2;
     } else {
         pd.n_in = 1;
@@ -364,7 +412,7 @@ double make_phase(const std::vector<PDimH> &L, int NT, PhaseDesc &pd, uint32_t &
     pd.nout_dims = 0;
     int64_t n_outer = 1;
     for (int i = first_outer; i < m; ++i) {
-        set_pdim(pd.out[pd.nout_dims++], L[i].e, L[i].g, L[i].s, L[i].slot);
+        set_pdim(pd.out[pd.nout_dims++], L[i].e, L[i].g, L[i].s, L[i].slot, L[i].cmul);
         n_outer *= L[i].e;
     }
     pd.n_outer = (uint32_t)n_outer;
@@ -380,8 +428,8 @@ double make_phase(const std::vector<PDimH> &L, int NT, PhaseDesc &pd, uint32_t &
     return best_u;
 }
 
-// smem offsets seen by the lanes of one warp at inner step 0 (simulation of
-// the kernel's mapping, for the bank-conflict model).
+// smem element offsets seen by the lanes of one warp at inner step 0 of its
+// first outer entry (simulation of the kernel's mapping, for the bank model).
 void phase_warp_offsets(const PhaseDesc &pd, int warp, uint32_t *off, int &nl) {
     nl = 0;
     for (int l = 0; l < 32; ++l) {
@@ -404,8 +452,37 @@ void phase_warp_offsets(const PhaseDesc &pd, int warp, uint32_t *off, int &nl) {
     }
 }
 
-// Fill TileParams for geometry g with smem pitch P (elements).
-double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, int NT, TileParams &tp) {
+// Can phase R / W be vectorised by V for this geometry (pitch-independent part)?
+bool r_vectorizable(const Problem &Pb, const TileGeom &g, int V) {
+    if (V <= 1) return false;
+    bool in_run[kMaxRank] = {false};
+    for (int i = 0; i < g.nsrc; ++i) in_run[g.src_dims[i]] = true;
+    // run starts move by the strides of run-index dims, grid dims and the
+    // tile step along a partial run boundary: all must keep 16-byte alignment
+    for (int k = 0; k < Pb.r; ++k) {
+        if (Pb.d[k] <= 1) continue;
+        if (!in_run[k] && Pb.in_stride[k] % V) return false;
+        if (in_run[k] && g.ext[k] < Pb.d[k] && (Pb.in_stride[k] * g.ext[k]) % V) return false;
+    }
+    // the grouped leading R entry: whole run, dims 0..a-1, or dim 0 alone (a == 0)
+    int64_t unit = g.a_part >= 0 ? g.Ls / g.ext[g.a_part] : g.Ls;
+    int64_t lead = g.a_part < 0 ? g.Ls : (g.a_part == 0 ? g.ext[0] : unit);
+    if (lead % V) return false;
+    if (g.a_part == 0 && (Pb.d[0] % g.ext[0]) % V) return false;   // ragged run lengths
+    return true;
+}
+
+bool w_vectorizable(const Problem &Pb, const TileGeom &g, int V) {
+    if (V <= 1) return false;
+    if (g.ext[0] == 0 || g.ext[0] % V) return false;
+    if (Pb.sigma[0] == 0) return false;     // dim 0 is the destination's stride-1 dim: not this mode
+    if (g.ext[0] < Pb.d[0] && (Pb.d[0] % g.ext[0]) % V) return false;  // ragged dim-0 extents
+    return true;
+}
+
+// Fill TileParams for geometry g, smem pitch (elements) and vector choice.
+double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, int NT, VecChoice vc,
+                        TileParams &tp) {
     memset(&tp, 0, sizeof(tp));
     const int r = Pb.r;
     tp.Ls = (uint32_t)g.Ls;
@@ -414,28 +491,18 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
     tp.pitch = pitch;
     const uint32_t Ns = (uint32_t)(g.T / g.Ls);
     tp.tile_elems_alloc = Ns * pitch;
-    // smem strides: source run dims dense, run-index dims scaled by the pitch
     int64_t sstr[kMaxRank];
-    bool in_src[kMaxRank] = {false};
-    int64_t acc = 1;
-    for (int i = 0; i < g.nsrc; ++i) {
-        int k = g.src_dims[i];
-        in_src[k] = true;
-        sstr[k] = acc;
-        acc *= g.ext[k];
-    }
-    acc = pitch;
-    for (int k = 0; k < r; ++k) {
-        if (g.ext[k] == 0 || in_src[k]) continue;
-        sstr[k] = acc;
-        acc *= g.ext[k];
-    }
+    bool in_src[kMaxRank];
+    tile_sstrides(Pb, g, pitch, sstr, in_src);
     int slot_of_dim[kMaxRank];
     for (int k = 0; k < r; ++k) slot_of_dim[k] = -1;
     if (g.a_part >= 0) slot_of_dim[g.a_part] = 0;
     if (g.c_part >= 0 && g.c_part != g.a_part) slot_of_dim[g.c_part] = 1;
-    double u0 = make_phase(phase_dims(Pb, g, sstr, slot_of_dim, false), NT, tp.ph[0], tp.lim_split[0]);
-    double u1 = make_phase(phase_dims(Pb, g, sstr, slot_of_dim, true), NT, tp.ph[1], tp.lim_split[1]);
+    double u0 = make_phase(phase_dims(Pb, g, sstr, slot_of_dim, false, vc.vr), NT, tp.ph[0], tp.lim_split[0]);
+    double u1 = make_phase(phase_dims(Pb, g, sstr, slot_of_dim, true, vc.vw), NT, tp.ph[1], tp.lim_split[1]);
+    tp.ph[0].vec = (uint32_t)vc.vr;
+    tp.ph[1].vec = (uint32_t)vc.vw;
+    tp.ph[1].vstride = vc.vw > 1 ? Pb.out_stride_of_dim[0] : 0;
     // grid digits
     struct Dg {
         int64_t ext, ss, ds;
@@ -477,37 +544,69 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
     };
     tp.ph[0].off_tab = take(16ull * tp.ph[0].n_outer, 16);
     tp.ph[1].off_tab = take(16ull * tp.ph[1].n_outer, 16);
-    tp.nbuf = Pb.E >= 4 ? 2 : 1;
+    tp.nbuf = Pb.E >= 4 ? Pb.nbuf : 1;
     uint64_t buf_bytes = ((uint64_t)tp.tile_elems_alloc * Pb.E + 15) / 16 * 16;
     tp.off_buf = take(buf_bytes * tp.nbuf, 16);
     tp.smem_bytes = (o + 15) / 16 * 16;
     return u0 * u1;
 }
 
-// Choose the source-run pitch that minimises modelled smem wavefronts of
-// both phases' warp accesses.
-uint32_t choose_pitch(const Problem &Pb, const TileGeom &g, int NT) {
-    uint32_t best_p = (uint32_t)g.Ls;
-    int64_t best_w = -1;
-    for (int pad = 0; pad <= 32; ++pad) {
-        uint32_t pitch = (uint32_t)g.Ls + pad;
-        if ((int64_t)(g.T / g.Ls) * pitch * Pb.E > kTileBudgetBytes + 8192) break;
-        TileParams tp;
-        fill_tile_params(Pb, g, pitch, NT, tp);
-        int64_t waves = 0;
-        uint32_t off[32];
-        int nl;
-        for (int ph = 0; ph < 2; ++ph)
-            for (int w = 0; w < NT / 32; ++w) {
-                phase_warp_offsets(tp.ph[ph], w, off, nl);
-                if (nl) waves += warp_wavefronts(off, nl, Pb.E);
+// Modelled per-tile cost of a (pitch, vector) choice: smem wavefronts of
+// both phases (simulated warp by warp) plus issued memory instructions.
+double tile_cost(const Problem &Pb, const TileParams &tp) {
+    double cost = 0.0;
+    uint32_t off[32];
+    int nl;
+    for (int ph = 0; ph < 2; ++ph) {
+        const PhaseDesc &d = tp.ph[ph];
+        const int V = (int)d.vec;
+        const int abytes = Pb.E * V;
+        int64_t waves = 0, warps = 0;
+        for (int w = 0; w < 8; ++w) {
+            phase_warp_offsets(d, w, off, nl);
+            if (!nl) continue;
+            for (int l = 0; l < nl; ++l) off[l] /= (uint32_t)V;     // in access units
+            waves += warp_wavefronts(off, nl, abytes);
+            ++warps;
+        }
+        if (!warps) continue;
+        double ops = (double)tp.T / V / 32.0;                      // warp memory ops per tile
+        double avg_w = (double)waves / (double)warps;
+        cost += ops * avg_w;                                        // smem wavefronts
+        cost += ops * (ph == 1 ? 1.0 + V : 1.0);                    // issued LDS/STG/LDGSTS
+    }
+    return cost;
+}
+
+// Choose pitch and vectorisation that minimise the modelled tile cost.
+void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pitch_out, VecChoice &vc_out) {
+    const int V = (Pb.E == 4 || Pb.E == 8) ? 16 / Pb.E : 1;
+    const bool rv = r_vectorizable(Pb, g, V);
+    const bool wv = w_vectorizable(Pb, g, V);
+    double best = -1.0;
+    pitch_out = (uint32_t)g.Ls;
+    for (int vr : {1, V}) {
+        if (vr > 1 && !rv) continue;
+        for (int vw : {1, V}) {
+            if (vw > 1 && !wv) continue;
+            const int step = (vr > 1 || vw > 1) ? V : 1;
+            for (int pad = 0; pad <= 32; pad += step) {
+                uint32_t pitch = (uint32_t)g.Ls + pad;
+                if ((int64_t)(g.T / g.Ls) * pitch * Pb.E > Pb.budget + 8192) break;
+                TileParams tp;
+                VecChoice vc;
+                vc.vr = vr;
+                vc.vw = vw;
+                fill_tile_params(Pb, g, pitch, NT, vc, tp);
+                double c = tile_cost(Pb, tp);
+                if (best < 0 || c < best - 1e-9) {
+                    best = c;
+                    pitch_out = pitch;
+                    vc_out = vc;
+                }
             }
-        if (best_w < 0 || waves < best_w) {
-            best_w = waves;
-            best_p = pitch;
         }
     }
-    return best_p;
 }
 
 }  // namespace
@@ -581,6 +680,7 @@ static void describe(vpg_plan *p) {
                 ph ? "W" : "R", d.nthr, d.ngroups, d.nthr_dims, d.n_in, d.n_outer, d.nout_dims,
                 d.mask_full, d.mask_ragged);
         }
+        put("vector elems: R %u, W %u\n", t.ph[0].vec, t.ph[1].vec);
         put("lane utilisation (R*W): %.3f\n", p->tile_util);
         put("tiles: %u, grid digits: %d\n", t.num_tiles, t.ngrid);
     } else if (p->kernel_class == VPG_KERNEL_ROWS) {
@@ -615,6 +715,15 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
     }
     Problem P;
     P.E = E;
+    // development knobs (documented in DESIGN.md): override the tiling policy
+    P.budget = kTileBudgetBytes;
+    P.nbuf = 2;
+    int persist_mode = -1;  // -1 auto, 0 one tile per CTA, 1 persistent
+    int force_threads = 0;
+    if (const char *e = getenv("VPG_TILE_BUDGET")) P.budget = std::max(1024L, atol(e));
+    if (const char *e = getenv("VPG_NBUF")) P.nbuf = atoi(e) == 1 ? 1 : 2;
+    if (const char *e = getenv("VPG_PERSIST")) persist_mode = atoi(e);
+    if (const char *e = getenv("VPG_THREADS")) force_threads = atoi(e);
     if (flags & VPG_NO_MERGE) {
         P.r = rank;
         for (int k = 0; k < rank; ++k) {
@@ -712,8 +821,15 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         }
         p->kernel_class = VPG_KERNEL_TILE;
         int threads = g.T >= 1024 ? kTileThreads : (g.T >= 256 ? 128 : 64);
-        uint32_t pitch = choose_pitch(P, g, threads);
-        p->tile_util = fill_tile_params(P, g, pitch, threads, p->tile);
+        if (force_threads >= 32 && force_threads <= 1024) threads = force_threads / 32 * 32;
+        uint32_t pitch;
+        VecChoice vc;
+        choose_pitch_vec(P, g, threads, pitch, vc);
+        p->tile_util = fill_tile_params(P, g, pitch, threads, vc, p->tile);
+        // variant without 16-byte source reads, for misaligned base pointers
+        VecChoice vs = vc;
+        vs.vr = 1;
+        fill_tile_params(P, g, pitch, threads, vs, p->tile_unaligned);
         // the tile count must fit the 32-bit tile index
         double nt = 1.0;
         for (int i = 0; i < p->tile.ngrid; ++i) nt *= p->tile.grid[i].ext.d;
@@ -723,6 +839,8 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
             return VPG_EUNSUPPORTED;
         }
         p->threads = threads;
+        p->tile.persistent = persist_mode < 0 ? 1u : (uint32_t)persist_mode;
+        p->tile_unaligned.persistent = p->tile.persistent;
         p->grid_hint = std::min<int64_t>(p->tile.num_tiles, 148 * 4);
         p->predicted_eff = 2.0 / (1.0 / g.eff_s + 1.0 / g.eff_d);
     }

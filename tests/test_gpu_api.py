@@ -1,0 +1,157 @@
+"""GPU tests of the public API surface: guard bands, misaligned buffers,
+streams, host-buffer execute(), dtypes, degenerate shapes, error mapping."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [
+    ((64, 48), (1, 0)),                       # 2-D transpose (vectorised tile)
+    ((8, 24, 20, 12), (0, 2, 3, 1)),          # NCHW->NHWC
+    ((7, 9, 13, 5, 11), (4, 1, 0, 3, 2)),     # misaligned dims
+    ((6, 5, 7, 3), (1, 0, 2, 3)),             # merged preserved row
+    ((16, 8, 64), (1, 0, 2)),                 # stride-1 preserved
+    ((2,) * 12, tuple(np.random.default_rng(3).permutation(12).tolist())),
+]
+
+
+def _want(x_np, axes):
+    return np.ascontiguousarray(np.transpose(x_np, axes))
+
+
+@pytest.mark.parametrize("shape,axes", SHAPES)
+@pytest.mark.parametrize("dtype", ["int32", "int64", "int16", "uint8", "complex128"])
+def test_permute_matches_numpy(cuda, shape, axes, dtype):
+    import torch
+
+    from paper_2506_03686_b200 import permute
+
+    rng = np.random.default_rng(0)
+    if dtype == "complex128":
+        x = (rng.standard_normal(shape) + 1j * rng.standard_normal(shape)).astype(np.complex128)
+    else:
+        x = rng.integers(np.iinfo(dtype).min, np.iinfo(dtype).max, size=shape, dtype=dtype)
+    y = permute(torch.from_numpy(x).to(cuda), axes)
+    assert np.array_equal(y.cpu().numpy(), _want(x, axes))
+
+
+@pytest.mark.parametrize("shape,axes", SHAPES)
+@pytest.mark.parametrize("offset", [1, 2, 3])
+def test_misaligned_base_pointers(cuda, shape, axes, offset):
+    """Buffers at element (not 16-byte) alignment take the scalar-read variant."""
+    import torch
+
+    from paper_2506_03686_b200 import TensorLayout, build_program, from_numpy_convention
+    from paper_2506_03686_b200.api import execute_device
+
+    n = int(np.prod(shape))
+    rng = np.random.default_rng(offset)
+    base = rng.integers(0, 2**31, size=n + 8, dtype=np.int64).astype(np.int32)
+    xd = torch.from_numpy(base).to(cuda)
+    x = xd[offset:offset + n]
+    out_full = torch.zeros(n + 8, dtype=torch.int32, device=cuda)
+    out = out_full[offset:offset + n]
+    prog = build_program(TensorLayout.from_shape(shape, 4), from_numpy_convention(axes), force="tile")
+    execute_device(prog, x, out=out)
+    want = _want(base[offset:offset + n].reshape(shape), axes).reshape(-1)
+    assert np.array_equal(out.cpu().numpy(), want)
+    # guard band around the destination untouched
+    full = out_full.cpu().numpy()
+    assert not full[:offset].any() and not full[offset + n:].any()
+
+
+def test_guard_bands_and_sentinels(cuda):
+    """Destination guard bands filled with sentinels stay intact (the VM's
+    guard-band method, vm.py:28-33/220-224), for every kernel class."""
+    import torch
+
+    from paper_2506_03686_b200 import TensorLayout, build_program, from_numpy_convention
+    from paper_2506_03686_b200.api import execute_device
+
+    G = 4096
+    rng = np.random.default_rng(11)
+    for shape, axes in SHAPES + [((3, 5, 1024), (1, 0, 2)), ((1000,), (0,))]:
+        for force in (None, "tile", "gather"):
+            n = int(np.prod(shape))
+            x = rng.integers(0, 2**63, size=n, dtype=np.int64)
+            buf = torch.full((n + 2 * G,), -0x5A5A5A5A5A5A5A5B, dtype=torch.int64, device=cuda)
+            prog = build_program(TensorLayout.from_shape(shape, 8), from_numpy_convention(axes), force=force)
+            execute_device(prog, torch.from_numpy(x).to(cuda), out=buf[G:G + n])
+            h = buf.cpu().numpy()
+            assert (h[:G] == -0x5A5A5A5A5A5A5A5B).all() and (h[G + n:] == -0x5A5A5A5A5A5A5A5B).all()
+            assert np.array_equal(h[G:G + n], _want(x.reshape(shape), axes).reshape(-1)), (shape, force)
+
+
+def test_nondefault_stream(cuda):
+    import torch
+
+    from paper_2506_03686_b200 import permute
+
+    s = torch.cuda.Stream()
+    x = torch.randint(0, 1 << 30, (512, 768), dtype=torch.int32, device=cuda)
+    with torch.cuda.stream(s):
+        y = permute(x, (1, 0), stream=s)
+    s.synchronize()
+    assert torch.equal(y, x.t().contiguous())
+
+
+def test_execute_host_buffers(cuda):
+    """execute() on host numpy/bytes/pinned tensors mirrors vm.execute's
+    (output, counters) contract (vm.py:105-110) through the GPU."""
+    import torch
+
+    from paper_2506_03686_b200 import PermutationMap, TensorLayout, build_program, execute
+
+    lay = TensorLayout((3, 32, 32, 7))                 # README "library in five lines"
+    pm = PermutationMap((2, 0, 1, 3))
+    prog = build_program(lay, pm)
+    data = np.arange(lay.num_elements, dtype=np.uint32)
+    out, counters = execute(prog, data)
+    assert out.dtype == np.dtype("<u4")
+    assert np.array_equal(out, oracle.naive_permute_np(data, lay.dims, pm.sigma))
+    assert counters["launches"] == 1 and counters["bytes_read"] == data.nbytes
+    out2, _ = execute(prog, data.tobytes())
+    assert np.array_equal(out2, out)
+    pinned = torch.from_numpy(data.view(np.int32)).pin_memory()
+    out3, _ = execute(prog, pinned)
+    assert np.array_equal(out3.numpy().reshape(-1).view(np.uint32), out)
+
+
+def test_degenerate_shapes(cuda):
+    import torch
+
+    from paper_2506_03686_b200 import permute
+
+    x = torch.arange(7, dtype=torch.int32, device=cuda)
+    assert torch.equal(permute(x, (0,)), x)
+    s = torch.tensor(5, dtype=torch.int32, device=cuda)
+    assert permute(s, ()).item() == 5
+    e = torch.empty((0, 3), dtype=torch.float32, device=cuda)
+    assert tuple(permute(e, (1, 0)).shape) == (3, 0)
+    one = torch.ones((1, 1), dtype=torch.float64, device=cuda)
+    assert torch.equal(permute(one, (1, 0)), one)
+
+
+def test_errors_are_loud(cuda):
+    import torch
+
+    from paper_2506_03686_b200 import LayoutError, TensorLayout, PermutationMap, build_program, permute
+    from paper_2506_03686_b200.api import execute_device
+
+    x = torch.zeros((4, 5), dtype=torch.int32, device=cuda)
+    with pytest.raises(LayoutError):
+        permute(x, (0, 0))
+    with pytest.raises(LayoutError):
+        permute(x, (0,))
+    with pytest.raises(LayoutError):
+        permute(x.cpu(), (1, 0))                       # no CPU fallback
+    prog = build_program(TensorLayout((5, 4)), PermutationMap((1, 0)))
+    with pytest.raises(LayoutError):
+        execute_device(prog, x, out=x)                 # in-place refused (out-of-place only)
+    with pytest.raises(LayoutError):
+        execute_device(prog, torch.zeros(21, dtype=torch.int32, device=cuda))

@@ -12,5 +12,5 @@ for k, wl in CONFIGS.items():
     p = vp.build_program(lay, vp.from_numpy_convention(wl.axes))
     print("==", k)
     for line in p.text.splitlines():
-        if full or any(w in line for w in ("phase", "pitch", "util", "tile elements", "rows:")):
+        if full or any(w in line for w in ("phase", "pitch", "util", "tile elements", "rows:", "vector")):
             print("  ", line)

@@ -1,0 +1,40 @@
+"""Sweep planner knobs (VPG_* env overrides) over configs; flushed median us."""
+import itertools
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2506_03686_b200 import TensorLayout, build_program, from_numpy_convention, program_cache_clear  # noqa: E402
+from paper_2506_03686_b200.api import execute_device  # noqa: E402
+from paper_2506_03686_b200.workloads import CONFIGS  # noqa: E402
+
+cfgs = sys.argv[1].split(",") if len(sys.argv) > 1 else ["cfg1", "cfg2", "cfg3"]
+grid = {
+    "VPG_TILE_BUDGET": ["8192", "16384", "32768", "49152"],
+    "VPG_NBUF": ["1", "2"],
+    "VPG_PERSIST": ["0", "1"],
+}
+dev = torch.device("cuda", 0)
+fl = bench.Flusher(torch, dev)
+st = torch.cuda.current_stream()
+for k in cfgs:
+    wl = CONFIGS[k]
+    n = wl.numel * wl.elem_bytes
+    x = torch.randint(0, 255, (n,), dtype=torch.uint8, device=dev)
+    y = torch.empty_like(x)
+    res = []
+    for vals in itertools.product(*grid.values()):
+        env = dict(zip(grid.keys(), vals))
+        os.environ.update(env)
+        program_cache_clear()
+        prog = build_program(TensorLayout.from_shape(wl.shape, wl.elem_bytes), from_numpy_convention(wl.axes))
+        t = bench.time_device(torch, lambda: execute_device(prog, x, out=y), 15, 3, fl, st)
+        med = sorted(t)[len(t) // 2] * 1e3
+        res.append((med, env, prog.metadata["tile_elems"], prog.metadata["smem_bytes"]))
+    res.sort(key=lambda r: r[0])
+    for med, env, te, sm in res[:6]:
+        print(f"{k} {med:7.1f} us {wl.algorithmic_bytes/med/1e3:7.0f} GB/s tile={te} smem={sm} {env}", flush=True)
+    print(f"{k} worst {res[-1][0]:.1f} us", flush=True)
