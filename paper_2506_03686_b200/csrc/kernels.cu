@@ -358,18 +358,46 @@ __device__ __forceinline__ void decode_tile(const TileParams &p, uint32_t t, int
     }
 }
 
-// Persistent CTAs walk tiles t = blockIdx.x + k*gridDim.x.  With ASYNC the
-// next tile's source runs stream into the second smem buffer (cp.async)
-// while the current tile is written out: one barrier per tile.
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+// wait until at most n committed cp.async groups are pending (n < 8)
+__device__ __forceinline__ void cp_async_wait_pending(uint32_t n) {
+    switch (n) {
+        case 0: cp_async_wait_group<0>(); break;
+        case 1: cp_async_wait_group<1>(); break;
+        case 2: cp_async_wait_group<2>(); break;
+        case 3: cp_async_wait_group<3>(); break;
+        case 4: cp_async_wait_group<4>(); break;
+        case 5: cp_async_wait_group<5>(); break;
+        case 6: cp_async_wait_group<6>(); break;
+        default: cp_async_wait_group<7>(); break;
+    }
+}
+
+constexpr int kMaxStages = 8;
+constexpr int kRing = kMaxStages + 2;
+
+// Persistent CTAs walk tiles t_k = blockIdx.x + k*gridDim.x through an
+// S-stage cp.async pipeline (S = p.nbuf smem tile buffers): the prologue
+// streams the source runs of the first S tiles; each iteration writes tile
+// k out of its buffer and refills that buffer with tile k+S.  Small
+// problems are thereby staged in one wave; large ones keep S-1 tiles of
+// loads in flight per CTA.  Without ASYNC (1- and 2-byte words) a single
+// buffer is filled by LDG+STS.
 template <typename W, bool ASYNC>
 __global__ void __launch_bounds__(256) tile_kernel(const __grid_constant__ TileParams p,
                                                    const W *__restrict__ src, W *__restrict__ dst) {
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ int64_t s_base[4][2];
-    __shared__ uint32_t s_valid[4][2];
+    __shared__ int64_t s_base[kRing][2];
+    __shared__ uint32_t s_valid[kRing][2];
     const uint32_t tid = threadIdx.x, NT = blockDim.x;
     const uint32_t first = blockIdx.x, step = gridDim.x;
     if (first >= p.num_tiles) return;
+    const uint32_t cnt = (p.num_tiles - first + step - 1) / step;   // tiles of this CTA
+    const uint32_t S = ASYNC ? p.nbuf : 1u;
+    const uint32_t R = S + 2;
 
     // per-CTA outer tables of both phases
     for (int ph = 0; ph < 2; ++ph) {
@@ -397,56 +425,45 @@ __global__ void __launch_bounds__(256) tile_kernel(const __grid_constant__ TileP
     }
     const ThreadPart tr = decode_thread(p.ph[0], tid);
     const ThreadPart tw = decode_thread(p.ph[1], tid);
-    W *buf0 = reinterpret_cast<W *>(smem + p.off_buf);
-    W *buf1 = buf0 + ((size_t)p.tile_elems_alloc * sizeof(W) + 15) / 16 * 16 / sizeof(W);
+    W *const buf0 = reinterpret_cast<W *>(smem + p.off_buf);
+    const size_t bstride = ((size_t)p.tile_elems_alloc * sizeof(W) + 15) / 16 * 16 / sizeof(W);
 
-    if (tid < 32) {
-        decode_tile(p, first, s_base, s_valid, 0);
-        if (first + step < p.num_tiles) decode_tile(p, first + step, s_base, s_valid, 1);
-    }
+    if (tid < 32)
+        for (uint32_t j = 0; j < S && j < cnt; ++j) decode_tile(p, first + j * step, s_base, s_valid, (int)j);
     __syncthreads();
-    auto limits = [&](int k, int ph, Lim &lim) -> uint32_t {
-        const uint32_t va = s_valid[k][0], vc = s_valid[k][1];
+    auto limits = [&](uint32_t slot, int ph, Lim &lim) -> uint32_t {
+        const uint32_t va = s_valid[slot][0], vc = s_valid[slot][1];
         lim.l0 = va;
         lim.l1 = vc;
         lim.l2 = p.lim_split[ph];
         const bool full = (va == p.e_a) && (vc == p.e_c);
         return full ? p.ph[ph].mask_full : p.ph[ph].mask_ragged;
     };
-    {
+    auto load = [&](uint32_t k, W *b) {
         Lim lim;
-        uint32_t m = limits(0, 0, lim);
-        tile_read<W, ASYNC>(p.ph[0], tr, smem, src + s_base[0][0], buf0, m, lim);
+        const uint32_t slot = k % R;
+        const uint32_t m = limits(slot, 0, lim);
+        tile_read<W, ASYNC>(p.ph[0], tr, smem, src + s_base[slot][0], b, m, lim);
+    };
+    // prologue: fill every stage
+    for (uint32_t j = 0; j < S; ++j) {
+        if (j < cnt) load(j, buf0 + j * bstride);
         if constexpr (ASYNC) cp_async_commit();
     }
-    uint32_t k = 0;
-    for (uint32_t t = first; t < p.num_tiles; t += step, ++k) {
-        const uint32_t tn = t + step;
-        if (tid < 32 && tn + step < p.num_tiles) decode_tile(p, tn + step, s_base, s_valid, (k + 2) & 3);
-        if constexpr (ASYNC) cp_async_wait_all();
+    for (uint32_t k = 0; k < cnt; ++k) {
+        if (tid < 32 && k + S < cnt) decode_tile(p, first + (k + S) * step, s_base, s_valid, (int)((k + S) % R));
+        if constexpr (ASYNC) cp_async_wait_pending(S - 1);
         __syncthreads();
-        const int cur = k & 3, nxt = (k + 1) & 3;
-        W *bcur = (k & 1) ? buf1 : buf0;
-        if constexpr (ASYNC) {
-            if (tn < p.num_tiles) {
-                Lim lim;
-                uint32_t m = limits(nxt, 0, lim);
-                tile_read<W, true>(p.ph[0], tr, smem, src + s_base[nxt][0], (k & 1) ? buf0 : buf1, m, lim);
-                cp_async_commit();
-            }
+        W *b = buf0 + (k % S) * bstride;
+        {
             Lim lim;
-            uint32_t m = limits(cur, 1, lim);
-            tile_write<W>(p.ph[1], tw, smem, dst + s_base[cur][1], bcur, m, lim);
-        } else {
-            Lim lim;
-            uint32_t m = limits(cur, 1, lim);
-            tile_write<W>(p.ph[1], tw, smem, dst + s_base[cur][1], buf0, m, lim);
-            __syncthreads();
-            if (tn < p.num_tiles) {
-                m = limits(nxt, 0, lim);
-                tile_read<W, false>(p.ph[0], tr, smem, src + s_base[nxt][0], buf0, m, lim);
-            }
+            const uint32_t slot = k % R;
+            const uint32_t m = limits(slot, 1, lim);
+            tile_write<W>(p.ph[1], tw, smem, dst + s_base[slot][1], b, m, lim);
         }
+        __syncthreads();
+        if (k + S < cnt) load(k + S, b);
+        if constexpr (ASYNC) cp_async_commit();
     }
 }
 
@@ -495,7 +512,12 @@ int occupancy(K kernel, int threads, int smem) {
     auto it = g_occ.find(key);
     if (it != g_occ.end()) return it->second;
     if (!g_attr_set[(const void *)kernel]) {
-        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        int optin = 0;
+        if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || optin <= 0)
+            optin = 227 * 1024;
+        cudaFuncAttributes fa;
+        size_t stat = cudaFuncGetAttributes(&fa, kernel) == cudaSuccess ? fa.sharedSizeBytes : 1024;
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)stat);
         g_attr_set[(const void *)kernel] = true;
     }
     int nb = 0;
@@ -518,12 +540,10 @@ vpg_status launch_tile(const vpg_plan *p, const void *src, void *dst, cudaStream
         k<<<(unsigned)grid, p->threads, smem, st>>>(tp, (const W *)src, (W *)dst);
     };
     if constexpr (E >= 4) {
-        if (p->tile.nbuf == 2) {
-            launch(tile_kernel<W, true>);
-            return VPG_OK;
-        }
+        launch(tile_kernel<W, true>);
+        return VPG_OK;
     }
-    launch(tile_kernel<W, false>);
+    if constexpr (E < 4) launch(tile_kernel<W, false>);
     return VPG_OK;
 }
 

@@ -59,7 +59,8 @@ double expected_sectors(int64_t bytes, int64_t align) {
 
 struct Problem {
     int64_t budget;       // staged tile bytes per CTA buffer
-    int nbuf;             // 1 or 2 smem buffers
+    int nbuf;             // forced pipeline stages (0 = planner's choice)
+    int64_t cta_smem;     // per-CTA shared-memory target (bytes)
     int r;
     int64_t d[kMaxRank];
     int sigma[kMaxRank];
@@ -544,8 +545,16 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
     };
     tp.ph[0].off_tab = take(16ull * tp.ph[0].n_outer, 16);
     tp.ph[1].off_tab = take(16ull * tp.ph[1].n_outer, 16);
-    tp.nbuf = Pb.E >= 4 ? Pb.nbuf : 1;
     uint64_t buf_bytes = ((uint64_t)tp.tile_elems_alloc * Pb.E + 15) / 16 * 16;
+    // pipeline depth: as many stages as fit the per-CTA smem target (two
+    // CTAs per SM), at least 2, at most 8; 1- and 2-byte words use 1.
+    uint32_t stages = 1;
+    if (Pb.E >= 4) {
+        uint64_t room = (uint64_t)Pb.cta_smem > o + 1024 ? (uint64_t)Pb.cta_smem - o - 1024 : 0;
+        stages = (uint32_t)std::min<uint64_t>(8, std::max<uint64_t>(2, room / buf_bytes));
+        if (Pb.nbuf > 0) stages = (uint32_t)Pb.nbuf;
+    }
+    tp.nbuf = stages;
     tp.off_buf = take(buf_bytes * tp.nbuf, 16);
     tp.smem_bytes = (o + 15) / 16 * 16;
     return u0 * u1;
@@ -717,11 +726,13 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
     P.E = E;
     // development knobs (documented in DESIGN.md): override the tiling policy
     P.budget = kTileBudgetBytes;
-    P.nbuf = 2;
+    P.nbuf = 0;
+    P.cta_smem = 110 * 1024;
     int persist_mode = -1;  // -1 auto, 0 one tile per CTA, 1 persistent
     int force_threads = 0;
     if (const char *e = getenv("VPG_TILE_BUDGET")) P.budget = std::max(1024L, atol(e));
-    if (const char *e = getenv("VPG_NBUF")) P.nbuf = atoi(e) == 1 ? 1 : 2;
+    if (const char *e = getenv("VPG_NBUF")) P.nbuf = std::max(1, std::min(8, atoi(e)));
+    if (const char *e = getenv("VPG_CTA_SMEM")) P.cta_smem = std::min(220L * 1024, std::max(16L * 1024, atol(e)));
     if (const char *e = getenv("VPG_PERSIST")) persist_mode = atoi(e);
     if (const char *e = getenv("VPG_THREADS")) force_threads = atoi(e);
     if (flags & VPG_NO_MERGE) {

@@ -12,10 +12,10 @@ from paper_2506_03686_b200.api import execute_device  # noqa: E402
 from paper_2506_03686_b200.workloads import CONFIGS  # noqa: E402
 
 cfgs = sys.argv[1].split(",") if len(sys.argv) > 1 else ["cfg1", "cfg2", "cfg3"]
-grid = {
-    "VPG_TILE_BUDGET": ["8192", "16384", "32768", "49152"],
-    "VPG_NBUF": ["1", "2"],
-    "VPG_PERSIST": ["0", "1"],
+import json  # noqa: E402
+grid = json.loads(os.environ.get("SWEEP_GRID", "{}")) or {
+    "VPG_TILE_BUDGET": ["16384", "32768", "49152"],
+    "VPG_CTA_SMEM": ["70000", "110000", "150000", "220000"],
 }
 dev = torch.device("cuda", 0)
 fl = bench.Flusher(torch, dev)
