@@ -1,0 +1,328 @@
+"""Sharded multi-GPU permutation: local pack permute -> all-to-all -> local
+unpack permute (BASELINE.json cfg5 at 2/4/8 B200).
+
+Input and output are each sharded along their own leading axis: rank r owns
+the contiguous slice [r*N/G, (r+1)*N/G) of the flattened input and of the
+flattened output.  When the leading axis is shorter than G (cfg5: extent 2,
+G = 8) "leading axis" means the leading axes whose product is G; a dim that
+straddles the boundary is split into (outer, inner) factors.  After that
+refinement:
+
+  I  = input axes that index the source rank (input-leading axes)
+  O  = input axes that index the destination rank (output-leading axes)
+  D  = O \\ I   (axes a rank sends along: one contiguous chunk per value)
+  M  = axes in neither I nor O (they survive to the local output)
+
+  P1 (local GPU permute):  local input [all axes but I, input order]
+                           -> [D (output order)] + [M (output order)]
+  all-to-all (NCCL over NVLink/NVSwitch): chunk d of P1 goes to rank s(d);
+                           ranks whose I∩O coordinates differ exchange nothing
+  P2 (local GPU permute):  received [I\\O (input order)] + [M (output order)]
+                           -> local output [all axes but O, output order]
+
+If I and O coincide (same set, same order) the step is purely local; if the
+sets match in a different order it is a fixed pairwise exchange.  Both fall
+out of the general formula (one chunk per rank).  There is no collective
+other than the one all-to-all the permutation needs.
+
+The local permutes default to the GPU kernels (``permute``); the CPU tests
+inject the oracle to exercise the exchange logic with the gloo backend.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+from .core import LayoutError
+
+__all__ = ["ShardPlan", "plan_sharded", "permute_sharded", "shard_bounds"]
+
+
+def _lead_split(shape, G):
+    """Walk `shape` from the outermost dim taking factors until their product
+    is G.  Returns {dim: outer_factor} for every dim touched (outer_factor ==
+    shape[dim] for whole dims).  Raises LayoutError if G does not divide the
+    leading dims cleanly."""
+    rem = G
+    cuts = {}
+    for i, d in enumerate(shape):
+        if rem == 1:
+            break
+        if d <= rem and rem % d == 0:
+            cuts[i] = d
+            rem //= d
+        elif d % rem == 0:
+            cuts[i] = rem
+            rem = 1
+        else:
+            g = math.gcd(d, rem)
+            raise LayoutError(f"cannot shard: dim {i} of size {d} vs remaining factor {rem} (gcd {g})")
+    if rem != 1:
+        raise LayoutError(f"tensor of shape {tuple(shape)} has fewer than {G} leading elements")
+    return cuts
+
+
+@dataclass(frozen=True)
+class ShardPlan:
+    G: int
+    shape: tuple            # global input shape (outer-first)
+    axes: tuple             # global permutation (numpy convention)
+    rshape: tuple           # refined input shape
+    raxes: tuple            # refined permutation
+    I: tuple                # refined input axes indexing the source rank (input order)
+    O: tuple                # refined input axes indexing the destination rank (output order)
+    D: tuple                # O \ I in output order
+    M: tuple                # the rest, output order
+    IO: tuple               # I \ O in input order
+
+    @property
+    def numel(self):
+        n = 1
+        for d in self.rshape:
+            n *= d
+        return n
+
+    @property
+    def local_numel(self):
+        return self.numel // self.G
+
+    def local_in_axes(self):
+        return tuple(a for a in range(len(self.rshape)) if a not in self.I)
+
+    def local_in_shape(self):
+        return tuple(self.rshape[a] for a in self.local_in_axes())
+
+    def out_shape(self):
+        return tuple(self.shape[a] for a in self.axes)
+
+    def local_out_axes(self):
+        return tuple(a for a in self.raxes if a not in self.O)
+
+    def local_out_shape(self):
+        return tuple(self.rshape[a] for a in self.local_out_axes())
+
+    def p1(self):
+        """(local input shape, axes) of the pack permute."""
+        L = self.local_in_axes()
+        order = list(self.D) + list(self.M)
+        return self.local_in_shape(), tuple(L.index(a) for a in order)
+
+    def p2(self):
+        """(received shape, axes) of the unpack permute."""
+        recv = list(self.IO) + list(self.M)
+        tgt = self.local_out_axes()
+        return tuple(self.rshape[a] for a in recv), tuple(recv.index(a) for a in tgt)
+
+    def _coords(self, index, axes_list):
+        c = {}
+        for a in reversed(axes_list):
+            c[a] = index % self.rshape[a]
+            index //= self.rshape[a]
+        return c
+
+    def _index(self, coords, axes_list):
+        i = 0
+        for a in axes_list:
+            i = i * self.rshape[a] + coords[a]
+        return i
+
+    def send_counts(self, r):
+        """Elements rank r sends to each destination rank."""
+        cin = self._coords(r, self.I)
+        chunk = 1
+        for a in self.M:
+            chunk *= self.rshape[a]
+        counts = [0] * self.G
+        nd = 1
+        for a in self.D:
+            nd *= self.rshape[a]
+        for d in range(nd):
+            c = dict(cin)
+            c.update(self._coords(d, self.D))
+            counts[self._index(c, self.O)] += chunk
+        return counts
+
+    def recv_counts(self, s):
+        """Elements rank s receives from each source rank."""
+        return [self.send_counts(r)[s] for r in range(self.G)]
+
+    def describe(self):
+        return (f"G={self.G} refined shape {self.rshape} axes {self.raxes}; I={self.I} O={self.O} "
+                f"D={self.D} M={self.M}; P1 {self.p1()} P2 {self.p2()}")
+
+
+def plan_sharded(shape, axes, G) -> ShardPlan:
+    shape = tuple(int(d) for d in shape)
+    axes = tuple(int(a) for a in axes)
+    n = len(shape)
+    if sorted(axes) != list(range(n)):
+        raise LayoutError(f"axes {axes} are not a permutation of 0..{n - 1}")
+    if G < 1:
+        raise LayoutError("G must be >= 1")
+    in_cuts = _lead_split(shape, G)
+    out_cuts_pos = _lead_split([shape[a] for a in axes], G)
+    out_cuts = {axes[j]: f for j, f in out_cuts_pos.items()}
+    # refine every dim into nested (outer -> inner) factors
+    pieces = []        # per original dim: list of (refined extent)
+    for i, d in enumerate(shape):
+        cuts = sorted({c for c in (in_cuts.get(i), out_cuts.get(i)) if c is not None and 1 < c < d})
+        if len(cuts) == 2 and cuts[1] % cuts[0]:
+            raise LayoutError(f"cannot shard: dim {i} needs incompatible splits {cuts}")
+        fac = []
+        prev = 1
+        for c in cuts:
+            fac.append(c // prev)
+            prev = c
+        fac.append(d // prev)
+        pieces.append(fac)
+    first = []
+    acc = 0
+    for fac in pieces:
+        first.append(acc)
+        acc += len(fac)
+    rshape = tuple(x for fac in pieces for x in fac)
+    raxes = tuple(first[a] + k for a in axes for k in range(len(pieces[a])))
+
+    def lead(ax_order):
+        got, prod = [], 1
+        for a in ax_order:
+            if prod == G:
+                break
+            got.append(a)
+            prod *= rshape[a]
+        if prod != G:
+            raise LayoutError("internal: refined leading product mismatch")
+        return tuple(got)
+
+    I = lead(range(len(rshape))) if G > 1 else ()
+    O = lead(raxes) if G > 1 else ()
+    Iset, Oset = set(I), set(O)
+    D = tuple(a for a in O if a not in Iset)
+    M = tuple(a for a in raxes if a not in Iset and a not in Oset)
+    IO = tuple(a for a in I if a not in Oset)
+    return ShardPlan(G, shape, axes, rshape, raxes, I, O, D, M, IO)
+
+
+def shard_bounds(numel, G, r):
+    """Element range of rank r's contiguous shard."""
+    per = numel // G
+    return r * per, (r + 1) * per
+
+
+def permute_sharded(local_in, global_shape, axes, group=None, local_permute=None, plan=None):
+    """Permute a tensor sharded across the ranks of `group`.
+
+    local_in: this rank's contiguous input shard (any shape, numel N/G).
+    Returns this rank's contiguous output shard, shaped as the local output
+    (output axes beyond the rank-indexing ones).  Collective: every rank of
+    the group must call it with the same shape/axes.
+    """
+    import torch
+    import torch.distributed as dist
+
+    G = dist.get_world_size(group) if dist.is_initialized() else 1
+    r = dist.get_rank(group) if dist.is_initialized() else 0
+    sp = plan or plan_sharded(global_shape, axes, G)
+    if local_permute is None:
+        from .api import permute as local_permute  # GPU kernels; no CPU fallback
+    if local_in.numel() != sp.local_numel:
+        raise LayoutError(f"rank {r}: shard holds {local_in.numel()} elements, expected {sp.local_numel}")
+    if G == 1:
+        return local_permute(local_in.reshape(sp.shape), sp.axes)
+    s1, a1 = sp.p1()
+    packed = local_permute(local_in.reshape(s1), a1).reshape(-1)
+    es = packed.element_size()
+    send = [c * es for c in sp.send_counts(r)]
+    recv_c = [c * es for c in sp.recv_counts(r)]
+    recv = torch.empty(sum(recv_c), dtype=torch.uint8, device=packed.device)
+    dist.all_to_all_single(recv, packed.view(torch.uint8), recv_c, send, group=group)
+    s2, a2 = sp.p2()
+    got = recv.view(packed.dtype).reshape(s2)
+    return local_permute(got, a2).reshape(sp.local_out_shape())
+
+
+def emulate_sharded(x_flat, global_shape, axes, G, local_permute=None):
+    """Run the G-rank algorithm on ONE device, rank after rank (P1 of every
+    virtual rank, the all-to-all as buffer slicing, then P2 of every rank).
+    Nothing waits on another rank's kernels; this validates the exact P1/P2
+    programs and chunk bookkeeping the ranks execute.  Returns the list of
+    per-rank output shards."""
+    import torch
+
+    if local_permute is None:
+        from .api import permute as local_permute
+    sp = plan_sharded(global_shape, axes, G)
+    n = sp.numel
+    s1, a1 = sp.p1()
+    packed = []
+    for r in range(G):
+        lo, hi = shard_bounds(n, G, r)
+        packed.append(local_permute(x_flat[lo:hi].reshape(s1), a1).reshape(-1))
+    outs = []
+    s2, a2 = sp.p2()
+    for s in range(G):
+        parts = []
+        for r in range(G):
+            sc = sp.send_counts(r)
+            off = sum(sc[:s])
+            if sc[s]:
+                parts.append(packed[r][off:off + sc[s]])
+        got = torch.cat(parts).reshape(s2)
+        outs.append(local_permute(got, a2).reshape(sp.local_out_shape()))
+    return outs
+
+
+# ------------------------------------------------------------------ bench
+def bench_main(args, torch, base, config, peak, peak_kind):
+    """bench.py at N>1: cfg5 sharded over the torchrun ranks (strong scaling)."""
+    import json
+    import os
+
+    import torch.distributed as dist
+
+    from .api import permute
+    from .workloads import CONFIGS, make_input_slice
+
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    G, r = dist.get_world_size(), dist.get_rank()
+    wl = CONFIGS[args.config]
+    sp = plan_sharded(wl.shape, wl.axes, G)
+    import numpy as np
+
+    lo, hi = shard_bounds(wl.numel, G, r)
+    full = make_input_slice(wl, lo, hi)          # this rank's slice of the seeded global input
+    dev = torch.device("cuda", local_rank)
+    x = torch.from_numpy(full.reshape(-1).view(np.uint8)).to(dev).view(torch.int64)
+    st = torch.cuda.current_stream()
+    step = lambda: permute_sharded(x, wl.shape, wl.axes, local_permute=permute, plan=sp)  # noqa: E731
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    evs = []
+    for _ in range(args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        step()
+        b.record(st)
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    dist.barrier()
+    tot = torch.tensor([sum(a.elapsed_time(b) for a, b in evs)], device=dev, dtype=torch.float64)
+    dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    ms = tot.item() / args.steps
+    gbs = wl.algorithmic_bytes / (ms * 1e-3) / 1e9
+    if r == 0:
+        line = dict(base)
+        line.update({"value": round(gbs, 2), "ms_per_step": ms, "config": config,
+                     "gpu_launches": 2 * args.steps,
+                     "roofline": {"bound": "nvlink+hbm", "achieved": round(gbs, 2), "peak": peak,
+                                  "peak_kind": peak_kind, "unit": "GB/s", "frac": round(gbs / peak / G, 4),
+                                  "traffic": None, "kernel": "tile (P1/P2) + NCCL all_to_all"},
+                     "shard_plan": sp.describe()})
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+    return 0

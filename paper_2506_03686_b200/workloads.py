@@ -19,7 +19,7 @@ import numpy as np
 
 BLOCK = 1 << 22
 
-__all__ = ["Workload", "CONFIGS", "cfg5_axes", "make_input", "get_config"]
+__all__ = ["Workload", "CONFIGS", "cfg5_axes", "make_input", "make_input_slice", "get_config"]
 
 
 def cfg5_axes(seed: int = 0, rank: int = 28) -> tuple[int, ...]:
@@ -108,3 +108,25 @@ def make_input(wl: Workload | str, seed: int = 0, threads: int = 8) -> np.ndarra
         with ThreadPoolExecutor(max_workers=threads) as ex:
             list(ex.map(lambda b: _fill_block(out, wl, seed, b), range(nblocks)))
     return out.reshape(wl.shape)
+
+
+def make_input_slice(wl: Workload | str, lo: int, hi: int, seed: int = 0) -> np.ndarray:
+    """Elements [lo, hi) of the flattened seeded input (each rank of the
+    sharded mode regenerates only its own shard)."""
+    if isinstance(wl, str):
+        wl = get_config(wl)
+    out = np.empty(hi - lo, dtype=np.dtype(wl.dtype))
+    for b in range(lo // BLOCK, -(-hi // BLOCK)):
+        b0 = b * BLOCK
+        m = min(BLOCK, wl.numel - b0)
+        blk = np.empty(m, dtype=out.dtype)
+        rng = np.random.default_rng([seed, b])
+        if wl.dtype == "complex64":
+            blk[:] = rng.standard_normal(2 * m, dtype=np.float32).view(np.complex64)
+        elif wl.dist == "uniform":
+            blk[:] = rng.random(m, dtype=np.dtype(wl.dtype)) * 2 - 1
+        else:
+            blk[:] = rng.standard_normal(m, dtype=np.dtype(wl.dtype))
+        s0, s1 = max(lo, b0), min(hi, b0 + m)
+        out[s0 - lo:s1 - lo] = blk[s0 - b0:s1 - b0]
+    return out

@@ -155,3 +155,20 @@ def test_errors_are_loud(cuda):
         execute_device(prog, x, out=x)                 # in-place refused (out-of-place only)
     with pytest.raises(LayoutError):
         execute_device(prog, torch.zeros(21, dtype=torch.int32, device=cuda))
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_sharded_algorithm_on_one_gpu_cfg5(cuda, G):
+    """The sharded P1 -> all-to-all -> P2 programs for cfg5 at G ranks, run
+    rank after rank on one GPU, reproduce the single-GPU permutation."""
+    import torch
+
+    from paper_2506_03686_b200 import permute
+    from paper_2506_03686_b200.sharded import emulate_sharded
+    from paper_2506_03686_b200.workloads import CONFIGS
+
+    wl = CONFIGS["cfg5"]
+    x = torch.randint(-2**62, 2**62, (wl.numel,), dtype=torch.int64, device=cuda)
+    want = permute(x.reshape(wl.shape), wl.axes).reshape(-1)
+    outs = emulate_sharded(x, wl.shape, wl.axes, G)
+    assert torch.equal(torch.cat([o.reshape(-1) for o in outs]), want)

@@ -1,0 +1,144 @@
+"""Host-side planner and API algebra (no GPU needed).
+
+Mirrors the reference's own unit tests for the same names
+(/root/reference/pkg/tests/test_core.py, test_planner.py): merge results are
+checked against the reference's merge_dimensions output recorded in the
+golden file for all 1150 cases.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2506_03686_b200 as vp
+from paper_2506_03686_b200 import LayoutError, PermutationMap, TensorLayout
+from tests.helpers import golden
+
+
+# ------------------------------------------------------------ core algebra
+def test_strides():
+    assert vp.compute_strides((7, 5, 3)) == (1, 7, 35)          # test_core.py:45-48
+    assert vp.compute_strides((4, 8, 16, 2)) == (1, 4, 32, 512)
+    with pytest.raises(LayoutError):
+        vp.compute_strides(())
+    with pytest.raises(LayoutError):
+        vp.compute_strides((4, 0, 2))
+
+
+def test_permuted_layout_and_conventions():
+    lay = TensorLayout((4, 8, 16, 2))
+    assert vp.permuted_layout(lay, PermutationMap((3, 1, 2, 0))).shape_outer_first() == (4, 16, 8, 2)
+    assert vp.to_numpy_convention(PermutationMap((2, 0, 1, 3))) == (0, 2, 3, 1)   # test_core.py:104-107
+    rng = np.random.default_rng(1)
+    for _ in range(50):
+        n = int(rng.integers(1, 9))
+        pm = PermutationMap(tuple(int(x) for x in rng.permutation(n)))
+        assert vp.from_numpy_convention(vp.to_numpy_convention(pm)).sigma == pm.sigma
+    with pytest.raises(LayoutError):
+        PermutationMap((0, 0, 1))
+    with pytest.raises(LayoutError):
+        vp.permuted_layout(TensorLayout((2, 2)), PermutationMap((0, 1, 2)))
+    with pytest.raises(LayoutError):
+        TensorLayout((2, 2), 3)
+
+
+def test_map_algebra():
+    pm = PermutationMap((2, 0, 1))
+    assert pm.compose(pm.inverse()).is_identity
+    assert pm.dest_position(0) == 1
+
+
+# ------------------------------------------------------------ merge (native planner)
+def test_merge_matches_reference_on_all_golden_cases():
+    """planner.py:211-241 semantics, compared with the reference's own output."""
+    for c in golden()["cases"]:
+        ml, mp = vp.merge_dimensions(TensorLayout(tuple(c["dims"]), c["elem"]), PermutationMap(tuple(c["sigma"])))
+        assert list(ml.dims) == c["merged_dims"] and list(mp.sigma) == c["merged_sigma"], c["name"]
+
+
+def test_merge_known_answers():
+    # test_planner.py:24-52
+    ml, mp = vp.merge_dimensions(TensorLayout((3, 5, 7)), PermutationMap((2, 0, 1)))
+    assert ml.dims == (15, 7) and mp.sigma == (1, 0)
+    ml, _ = vp.merge_dimensions(TensorLayout((9, 8, 4)), PermutationMap((2, 0, 1)))
+    assert ml.dims == (72, 4)
+    ml, mp = vp.merge_dimensions(TensorLayout((3, 4, 5)), PermutationMap((0, 1, 2)))
+    assert ml.dims == (60,) and mp.sigma == (0,)
+    ml, _ = vp.merge_dimensions(TensorLayout((3, 1, 5, 2)), PermutationMap((3, 0, 1, 2)))
+    assert ml.dims == (15, 2)
+    ml, mp = vp.merge_dimensions(TensorLayout((1, 1)), PermutationMap((1, 0)))
+    assert ml.dims == (1,) and mp.sigma == (0,)
+
+
+# ------------------------------------------------------------ classification
+def _plan(shape, axes, elem=4, **kw):
+    return vp.build_program(TensorLayout.from_shape(shape, elem), vp.from_numpy_convention(axes), **kw)
+
+
+def test_classification_of_baseline_configs():
+    from paper_2506_03686_b200.workloads import CONFIGS
+
+    kinds = {k: _plan(w.shape, w.axes, w.elem_bytes).kernel for k, w in CONFIGS.items()}
+    assert kinds == {"cfg1": "tile", "cfg2": "tile", "cfg3": "tile", "cfg4": "rows", "cfg5": "tile"}
+    # merged forms
+    assert _plan((32, 64, 56, 56), (0, 2, 3, 1)).merged_layout.dims == (3136, 64, 32)
+    assert _plan((128, 64, 32, 512), (2, 0, 1, 3), 8).merged_layout.dims == (512, 32, 8192)
+    assert _plan((17, 9, 13, 15, 11, 27), (5, 2, 0, 4, 1, 3)).merged_layout.rank == 6
+
+
+def test_classification_edges():
+    assert _plan((5, 7, 9), (0, 1, 2)).kernel in ("copy", "gather")           # identity
+    assert _plan((50, 70, 90), (0, 1, 2)).kernel == "copy"
+    assert _plan((8, 16, 3), (1, 0, 2)).kernel == "gather"                      # tiny
+    assert _plan((640, 320, 3), (1, 0, 2)).kernel == "tile"                     # 12 B rows -> K3 tile
+    assert _plan((64, 32, 1024), (1, 0, 2)).kernel == "rows"                    # 4 KiB rows -> K1
+    assert _plan((1, 1), (1, 0)).kernel == "gather"
+
+
+@pytest.mark.parametrize("elem", [1, 2, 4, 8, 16])
+def test_tile_plan_invariants(elem):
+    """Tiles fit the smem budget, cover the tensor, and runs are >= 1."""
+    rng = np.random.default_rng(elem)
+    for _ in range(60):
+        rank = int(rng.integers(2, 7))
+        shape = tuple(int(rng.integers(1, 40)) for _ in range(rank))
+        axes = tuple(int(a) for a in rng.permutation(rank))
+        p = _plan(shape, axes, elem, force="tile")
+        m = p.metadata
+        assert p.kernel == "tile"
+        assert m["smem_bytes"] <= 227 * 1024
+        assert m["tile_elems"] * m["num_tiles"] >= p.num_elements
+        assert m["src_run"] >= 1 and m["dst_run"] >= 1
+        assert m["tile_elems"] % m["src_run"] == 0 and m["tile_elems"] % m["dst_run"] == 0
+
+
+def test_vectorisation_choices():
+    p = _plan((4096, 4096), (1, 0))
+    assert "vector elems: R 4, W 4" in p.text
+    p = _plan((2,) * 20, tuple(np.random.default_rng(0).permutation(20).tolist()), 8)
+    assert p.kernel == "tile"
+    p = _plan((17, 9, 13, 15, 11, 27), (5, 2, 0, 4, 1, 3))
+    assert "vector elems: R 1" in p.text        # 108-byte runs cannot take 16-byte loads
+
+
+def test_plan_cache_and_immutability():
+    a = _plan((30, 40), (1, 0))
+    b = _plan((30, 40), (1, 0))
+    assert a is b
+    with pytest.raises(Exception):
+        a.kernel = "x"
+
+
+def test_format_plan_mentions_key_facts():
+    text = vp.format_plan(_plan((4096, 4096), (1, 0)))
+    for key in ("kernel class", "merged dims", "tile elements", "smem pitch", "tiles:"):
+        assert key in text
+
+
+def test_machine_elem_width_mismatch_rejected():
+    class M:
+        elem_width = 8
+
+    with pytest.raises(LayoutError):
+        vp.build_program(TensorLayout((4, 4), 4), PermutationMap((1, 0)), M())
