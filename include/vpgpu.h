@@ -73,6 +73,7 @@ typedef struct {
     int32_t threads;                /* CTA size */
     int64_t grid_hint;              /* CTAs launched when the device has 148 SMs */
     double  predicted_efficiency;   /* planner's sector-efficiency estimate, 0..1 */
+    int32_t host_chunks;            /* vpg_permute_host pipeline chunks (0 = single shot) */
 } vpg_plan_info;
 
 /* Library ABI version (VPG_ABI_VERSION). */

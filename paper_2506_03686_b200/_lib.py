@@ -53,6 +53,7 @@ class PlanInfo(ctypes.Structure):
         ("threads", ctypes.c_int32),
         ("grid_hint", ctypes.c_int64),
         ("predicted_efficiency", ctypes.c_double),
+        ("host_chunks", ctypes.c_int32),
     ]
 
 

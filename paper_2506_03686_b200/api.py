@@ -209,6 +209,7 @@ def build_program(layout: TensorLayout, pmap: PermutationMap, machine=None, merg
         "threads": info.threads,
         "grid_hint": info.grid_hint,
         "predicted_efficiency": info.predicted_efficiency,
+        "host_chunks": info.host_chunks,
         "source_shape": layout.dims,
         "source_map": pmap.sigma,
     }

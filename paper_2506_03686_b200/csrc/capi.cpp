@@ -11,6 +11,10 @@
 #include "plan.h"
 
 namespace vpg {
+vpg_status permute_host_pipelined(const vpg_plan *p, const void *host_src, void *host_dst, void *dev_src,
+                                  void *dev_dst, cudaStream_t user, std::string *err);
+int host_pipeline_chunks(const vpg_plan *p);
+void host_pipeline_forget(const vpg_plan *p);
 int merge_dims(int rank, const int64_t *dims, const int32_t *sigma, int64_t *od, int32_t *os);
 vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E, unsigned flags,
                      vpg_plan **out, std::string *err);
@@ -74,6 +78,12 @@ vpg_status vpg_permute_host(const vpg_plan *plan, const void *host_src, void *ho
     if (!plan || !host_src || !host_dst || !dev_src || !dev_dst) return fail(VPG_EINVAL, "null argument");
     cudaStream_t st = (cudaStream_t)cuda_stream;
     size_t nbytes = (size_t)plan->n * plan->elem_bytes;
+    {
+        std::string err;
+        vpg_status ps = vpg::permute_host_pipelined(plan, host_src, host_dst, dev_src, dev_dst, st, &err);
+        if (ps == VPG_OK) return VPG_OK;
+        if (ps != VPG_EUNSUPPORTED) return fail(ps, err);
+    }
     cudaError_t e = cudaMemcpyAsync(dev_src, host_src, nbytes, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return fail(VPG_ECUDA, std::string("H2D copy: ") + cudaGetErrorString(e));
     vpg_status s = vpg_permute(plan, dev_src, dev_dst, cuda_stream);
@@ -128,6 +138,7 @@ vpg_status vpg_plan_info_get(const vpg_plan *p, vpg_plan_info *info) {
     info->threads = p->threads;
     info->grid_hint = p->grid_hint;
     info->predicted_efficiency = p->predicted_eff;
+    info->host_chunks = vpg::host_pipeline_chunks(p);
     if (p->kernel_class == VPG_KERNEL_TILE) {
         info->tile_elems = p->tile.T;
         info->src_run = p->tile.Ls;
@@ -159,6 +170,10 @@ vpg_status vpg_plan_describe(const vpg_plan *p, char *buf, size_t len) {
     return VPG_OK;
 }
 
-void vpg_plan_destroy(vpg_plan *p) { delete p; }
+void vpg_plan_destroy(vpg_plan *p) {
+    if (!p) return;
+    vpg::host_pipeline_forget(p);
+    delete p;
+}
 
 }  // extern "C"

@@ -172,3 +172,24 @@ def test_sharded_algorithm_on_one_gpu_cfg5(cuda, G):
     want = permute(x.reshape(wl.shape), wl.axes).reshape(-1)
     outs = emulate_sharded(x, wl.shape, wl.axes, G)
     assert torch.equal(torch.cat([o.reshape(-1) for o in outs]), want)
+
+
+def test_execute_host_pipelined_chunks(cuda):
+    """Large host buffers go through the chunked H2D/kernel/D2H pipeline;
+    the result equals the device-resident permutation."""
+    import torch
+
+    from paper_2506_03686_b200 import TensorLayout, build_program, execute, from_numpy_convention, permute
+
+    rng = np.random.default_rng(5)
+    for shape, axes in [((2,) * 24, tuple(rng.permutation(24).tolist())),
+                        ((8, 16, 64, 2048), (3, 0, 2, 1)),
+                        ((4, 4, 8, 8, 4096), (1, 0, 3, 2, 4)),
+                        ((16, 8, 128, 1024), (0, 2, 1, 3))]:
+        prog = build_program(TensorLayout.from_shape(shape, 8), from_numpy_convention(axes))
+        n = prog.num_elements
+        host = torch.randint(-2**62, 2**62, (n,), dtype=torch.int64).pin_memory()
+        out = torch.empty(n, dtype=torch.int64).pin_memory()
+        execute(prog, host, out=out)
+        want = permute(host.to(cuda).reshape(shape), axes).reshape(-1).cpu()
+        assert torch.equal(out, want), (shape, axes, prog.metadata["host_chunks"])
