@@ -74,6 +74,7 @@ typedef struct {
     int64_t grid_hint;              /* CTAs launched when the device has 148 SMs */
     double  predicted_efficiency;   /* planner's sector-efficiency estimate, 0..1 */
     int32_t host_chunks;            /* vpg_permute_host pipeline chunks (0 = single shot) */
+    int32_t jit_state;              /* 0 no specialisation, 1 pending, 2 specialised kernel loaded, -1 failed */
 } vpg_plan_info;
 
 /* Library ABI version (VPG_ABI_VERSION). */
@@ -94,6 +95,8 @@ vpg_status vpg_merge_dimensions(int rank, const int64_t *dims, const int32_t *si
 #define VPG_FORCE_GATHER 0x1
 #define VPG_FORCE_TILE   0x2
 #define VPG_NO_MERGE     0x4
+#define VPG_FORCE_JIT    0x8    /* TILE: always use the per-case NVRTC-specialised kernel  */
+#define VPG_NO_JIT       0x10   /* TILE: always use the ahead-of-time kernel                */
 vpg_status vpg_plan_create(int rank, const int64_t *dims_inner_first,
                            const int32_t *sigma_inner_first, int elem_bytes,
                            unsigned flags, vpg_plan **out);
@@ -122,6 +125,16 @@ vpg_status vpg_permute_nd(int rank, const int64_t *dims_inner_first,
 /* Plan inspection (format_plan analog, planner.py:386-419). */
 vpg_status vpg_plan_info_get(const vpg_plan *plan, vpg_plan_info *info);
 vpg_status vpg_plan_describe(const vpg_plan *plan, char *buf, size_t len);
+
+/* Generated CUDA source of the per-case specialised tile kernel (the
+ * reference's emit_source, emit.py:343-363: shape, map and element width
+ * baked in; kernel cubins are cached under an fnv1a64 name like
+ * kernel_name, emit.py:118-128).  TILE plans only. */
+vpg_status vpg_plan_emit_source(const vpg_plan *plan, char *buf, size_t len);
+
+/* Compile the specialised source with NVRTC without loading it (needs no
+ * GPU; the analog of verify_native's compile step, emit.py:444-483). */
+vpg_status vpg_plan_jit_compile(const vpg_plan *plan);
 
 void vpg_plan_destroy(vpg_plan *plan);
 

@@ -23,8 +23,10 @@ from .api import (
     GpuTarget,
     VpgError,
     build_program,
+    emit_source,
     execute,
     format_plan,
+    jit_compile,
     merge_dimensions,
     permute,
     program_cache_clear,
@@ -47,7 +49,9 @@ __all__ = [
     "VpgError",
     "build_program",
     "execute",
+    "emit_source",
     "format_plan",
+    "jit_compile",
     "merge_dimensions",
     "permute",
     "program_cache_clear",

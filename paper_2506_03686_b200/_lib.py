@@ -18,6 +18,8 @@ KERNEL_NAMES = {0: "copy", 1: "rows", 2: "tile", 3: "gather"}
 VPG_FORCE_GATHER = 0x1
 VPG_FORCE_TILE = 0x2
 VPG_NO_MERGE = 0x4
+VPG_FORCE_JIT = 0x8
+VPG_NO_JIT = 0x10
 VPG_MAX_RANK = 64
 
 # symbols declared in include/vpgpu.h (checked by tests/test_abi.py)
@@ -31,6 +33,8 @@ EXPORTED = (
     "vpg_permute_nd",
     "vpg_plan_info_get",
     "vpg_plan_describe",
+    "vpg_plan_emit_source",
+    "vpg_plan_jit_compile",
     "vpg_plan_destroy",
 )
 
@@ -54,6 +58,7 @@ class PlanInfo(ctypes.Structure):
         ("grid_hint", ctypes.c_int64),
         ("predicted_efficiency", ctypes.c_double),
         ("host_chunks", ctypes.c_int32),
+        ("jit_state", ctypes.c_int32),
     ]
 
 
@@ -92,10 +97,13 @@ def lib():
         L.vpg_permute_nd.argtypes = [ctypes.c_int, i64p, i32p, ctypes.c_int, vp, vp, vp]
         L.vpg_plan_info_get.argtypes = [vp, ctypes.POINTER(PlanInfo)]
         L.vpg_plan_describe.argtypes = [vp, ctypes.c_char_p, ctypes.c_size_t]
+        L.vpg_plan_emit_source.argtypes = [vp, ctypes.c_char_p, ctypes.c_size_t]
+        L.vpg_plan_jit_compile.argtypes = [vp]
         L.vpg_plan_destroy.argtypes = [vp]
         L.vpg_plan_destroy.restype = None
         for name in ("vpg_merge_dimensions", "vpg_plan_create", "vpg_permute", "vpg_permute_host",
-                     "vpg_permute_nd", "vpg_plan_info_get", "vpg_plan_describe"):
+                     "vpg_permute_nd", "vpg_plan_info_get", "vpg_plan_describe", "vpg_plan_emit_source",
+                     "vpg_plan_jit_compile"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
         return L

@@ -42,6 +42,8 @@ __all__ = [
     "execute",
     "permute",
     "format_plan",
+    "emit_source",
+    "jit_compile",
     "program_cache_clear",
 ]
 
@@ -147,6 +149,14 @@ class GpuProgram:
     def handle(self) -> int:
         return self._handle.ptr
 
+    @property
+    def jit_state(self) -> int:
+        """0: ahead-of-time kernel, 1: specialisation pending (first launch
+        compiles it), 2: NVRTC-specialised kernel loaded, -1: failed."""
+        info = _lib.PlanInfo()
+        _check(_lib.lib().vpg_plan_info_get(self.handle, ctypes.byref(info)), "plan_info")
+        return info.jit_state
+
 
 _cache: dict = {}
 _cache_lock = threading.Lock()
@@ -158,11 +168,13 @@ def program_cache_clear():
 
 
 def build_program(layout: TensorLayout, pmap: PermutationMap, machine=None, merge: bool = True,
-                  opt: bool = True, force: str | None = None) -> GpuProgram:
+                  opt: bool = True, force: str | None = None, jit: bool | None = None) -> GpuProgram:
     """Plan a permutation (ir.py:441-456 signature; ``machine``/``opt`` kept
     for drop-in compatibility).
 
     ``force`` pins a kernel class for tests: ``"tile"`` or ``"gather"``.
+    ``jit`` pins the per-case NVRTC specialisation of tile plans on/off
+    (default: on for tensors of 4 MiB and more).
     """
     if pmap.rank != layout.rank:
         raise LayoutError("map rank does not match layout rank")
@@ -177,6 +189,10 @@ def build_program(layout: TensorLayout, pmap: PermutationMap, machine=None, merg
         flags |= _lib.VPG_FORCE_GATHER
     elif force is not None:
         raise ValueError(f"unknown force={force!r}")
+    if jit is True:
+        flags |= _lib.VPG_FORCE_JIT
+    elif jit is False:
+        flags |= _lib.VPG_NO_JIT
     key = (layout.dims, layout.elem_width, pmap.sigma, flags)
     with _cache_lock:
         hit = _cache.get(key)
@@ -218,6 +234,21 @@ def build_program(layout: TensorLayout, pmap: PermutationMap, machine=None, merg
     with _cache_lock:
         _cache.setdefault(key, prog)
         return _cache[key]
+
+
+def emit_source(program: GpuProgram) -> str:
+    """CUDA source of the program's specialised kernel (the reference's
+    emit_source, emit.py:343-363).  Tile programs only."""
+    L = _lib.lib()
+    buf = ctypes.create_string_buffer(1 << 16)
+    _check(L.vpg_plan_emit_source(program.handle, buf, len(buf)), "emit_source")
+    return buf.value.decode()
+
+
+def jit_compile(program: GpuProgram) -> None:
+    """Compile the specialised kernel with NVRTC without a GPU (raises
+    LayoutError with the NVRTC log on failure)."""
+    _check(_lib.lib().vpg_plan_jit_compile(program.handle), "jit_compile")
 
 
 def format_plan(program: GpuProgram) -> str:

@@ -139,6 +139,7 @@ vpg_status vpg_plan_info_get(const vpg_plan *p, vpg_plan_info *info) {
     info->grid_hint = p->grid_hint;
     info->predicted_efficiency = p->predicted_eff;
     info->host_chunks = vpg::host_pipeline_chunks(p);
+    info->jit_state = vpg::jit_state(p);
     if (p->kernel_class == VPG_KERNEL_TILE) {
         info->tile_elems = p->tile.T;
         info->src_run = p->tile.Ls;
@@ -170,9 +171,27 @@ vpg_status vpg_plan_describe(const vpg_plan *p, char *buf, size_t len) {
     return VPG_OK;
 }
 
+vpg_status vpg_plan_emit_source(const vpg_plan *p, char *buf, size_t len) {
+    if (!p || !buf || len == 0) return fail(VPG_EINVAL, "null argument");
+    if (p->kernel_class != VPG_KERNEL_TILE) return fail(VPG_EUNSUPPORTED, "only tile plans are specialised");
+    const std::string src = vpg::jit_source(p);
+    if (src.size() + 1 > len) return fail(VPG_EINVAL, "buffer too small: need " + std::to_string(src.size() + 1));
+    memcpy(buf, src.c_str(), src.size() + 1);
+    return VPG_OK;
+}
+
+vpg_status vpg_plan_jit_compile(const vpg_plan *p) {
+    if (!p) return fail(VPG_EINVAL, "null argument");
+    if (p->kernel_class != VPG_KERNEL_TILE) return fail(VPG_EUNSUPPORTED, "only tile plans are specialised");
+    std::string log;
+    if (!vpg::jit_compile_check(p, &log)) return fail(VPG_EUNSUPPORTED, "NVRTC: " + log);
+    return VPG_OK;
+}
+
 void vpg_plan_destroy(vpg_plan *p) {
     if (!p) return;
     vpg::host_pipeline_forget(p);
+    vpg::jit_forget(p);
     delete p;
 }
 

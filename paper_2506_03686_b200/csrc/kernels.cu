@@ -25,42 +25,9 @@
 #include <tuple>
 
 #include "plan.h"
+#include "tile_body.cuh"
 
 namespace vpg {
-
-// ------------------------------------------------------------------ helpers
-__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv &f) {
-    uint32_t t = __umulhi(n, f.m);
-    return (uint32_t)(((uint64_t)t + n) >> f.s);
-}
-
-template <int E>
-struct WordOf;
-template <>
-struct WordOf<1> {
-    using T = unsigned char;
-};
-template <>
-struct WordOf<2> {
-    using T = unsigned short;
-};
-template <>
-struct WordOf<4> {
-    using T = unsigned int;
-};
-template <>
-struct WordOf<8> {
-    using T = unsigned long long;
-};
-template <>
-struct WordOf<16> {
-    using T = uint4;
-};
-
-template <typename W>
-__device__ __forceinline__ W ld_stream(const W *p) {
-    return __ldg(p);
-}
 
 // ------------------------------------------------------------------ COPY
 template <typename V>
@@ -113,358 +80,13 @@ __global__ void __launch_bounds__(256) rows_kernel(const __grid_constant__ RowsP
 }
 
 // ------------------------------------------------------------------ TILE (K2/K3)
-struct OuterEntry {
-    int64_t g;
-    uint32_t s;
-    uint16_t c0, c1;
-};
-
-struct ThreadPart {
-    int64_t g;
-    uint32_t s;
-    uint32_t c0, c1, c2;
-    uint32_t grp;
-    bool active;
-};
-
-template <int E>
-__device__ __forceinline__ void cp_async(void *sp, const void *gp) {
-    const uint32_t s = (uint32_t)__cvta_generic_to_shared(sp);
-    if constexpr (E == 16)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gp) : "memory");
-    else
-        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gp), "n"(E) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
-
-__device__ __forceinline__ ThreadPart decode_thread(const PhaseDesc &d, uint32_t tid) {
-    ThreadPart t;
-    t.grp = tid / d.nthr;
-    uint32_t tr = tid - t.grp * d.nthr;
-    t.active = t.grp < d.ngroups;
-    t.g = 0;
-    t.s = 0;
-    t.c0 = t.c1 = t.c2 = 0;
-    for (int i = 0; i < d.nthr_dims; ++i) {
-        uint32_t q = fdiv(tr, d.thr[i].div);
-        uint32_t c = tr - q * d.thr[i].div.d;
-        tr = q;
-        t.g += (int64_t)c * d.thr[i].gstride;
-        t.s += c * d.thr[i].sstride;
-        const uint32_t cv = c * d.thr[i].cmul;
-        if (d.thr[i].slot == 0) t.c0 = cv;
-        else if (d.thr[i].slot == 1) t.c1 = cv;
-        else if (d.thr[i].slot == 2) t.c2 = cv;
-    }
-    return t;
-}
-
-struct Lim {
-    uint32_t l0, l1, l2;
-};
-
-__device__ __forceinline__ bool slot_ok(uint32_t mask, uint32_t c0, uint32_t c1, uint32_t c2, const Lim &lim) {
-    return (!(mask & 1u) || c0 < lim.l0) && (!(mask & 2u) || c1 < lim.l1) && (!(mask & 4u) || c2 < lim.l2);
-}
-
-// R phase: global (source order) -> smem.  ASYNC: cp.async (16-byte chunks
-// when d.vec > 1), else LDG+STS.
-template <typename W, bool ASYNC, bool VEC>
-__device__ __forceinline__ void tile_read_impl(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
-                                               const W *__restrict__ gsrc, W *buf, uint32_t mask,
-                                               const Lim lim) {
-    constexpr int U = 4;
-    constexpr int CP = VEC ? 16 : (int)sizeof(W);
-    const OuterEntry *tab = reinterpret_cast<const OuterEntry *>(smem + d.off_tab);
-    const uint32_t n_in = d.n_in;
-    const int64_t g_in = d.g_in;
-    const uint32_t s_in = d.s_in;
-    for (uint32_t o = t.grp; o < d.n_outer; o += d.ngroups) {
-        const OuterEntry e = tab[o];
-        const W *gp = gsrc + (t.g + e.g);
-        W *sp = buf + (t.s + e.s);
-        if (mask == 0) {
-            uint32_t i = 0;
-            for (; i + U <= n_in; i += U) {
-                if constexpr (ASYNC) {
-#pragma unroll
-                    for (int u = 0; u < U; ++u) cp_async<CP>(sp + u * s_in, gp + u * g_in);
-                } else {
-                    W v[U];
-#pragma unroll
-                    for (int u = 0; u < U; ++u) v[u] = __ldg(gp + u * g_in);
-#pragma unroll
-                    for (int u = 0; u < U; ++u) sp[u * s_in] = v[u];
-                }
-                gp += U * g_in;
-                sp += U * s_in;
-            }
-            for (; i < n_in; ++i) {
-                if constexpr (ASYNC) cp_async<CP>(sp, gp);
-                else *sp = __ldg(gp);
-                gp += g_in;
-                sp += s_in;
-            }
-        } else {
-            uint32_t c0 = t.c0 + e.c0, c1 = t.c1 + e.c1, c2 = t.c2;
-            for (uint32_t i = 0; i < n_in; ++i) {
-                if (slot_ok(mask, c0, c1, c2, lim)) {
-                    if constexpr (ASYNC) cp_async<CP>(sp, gp);
-                    else *sp = __ldg(gp);
-                }
-                gp += g_in;
-                sp += s_in;
-                c0 += d.c_in[0];
-                c1 += d.c_in[1];
-                c2 += d.c_in[2];
-            }
-        }
-    }
-}
-
+// Ahead-of-time instantiation: the parameter block arrives as a
+// __grid_constant__ kernel argument (run-time extents/strides).  jit.cpp
+// compiles the same body with the block baked in as constants.
 template <typename W, bool ASYNC>
-__device__ __forceinline__ void tile_read(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
-                                          const W *__restrict__ gsrc, W *buf, uint32_t mask,
-                                          const Lim lim) {
-    if (!t.active) return;
-    if constexpr (ASYNC && sizeof(W) < 16) {
-        if (d.vec > 1) {
-            tile_read_impl<W, true, true>(d, t, smem, gsrc, buf, mask, lim);
-            return;
-        }
-    }
-    tile_read_impl<W, ASYNC, false>(d, t, smem, gsrc, buf, mask, lim);
-}
-
-// W phase: smem -> global (destination order).  VEC: each position is a
-// 16-byte smem vector of V consecutive dim-0 elements, stored to V
-// destinations d.vstride apart (each store instruction stays coalesced
-// across the warp's lanes).
-template <typename W, bool VEC>
-__device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
-                                                W *__restrict__ gdst, const W *buf, uint32_t mask,
-                                                const Lim lim) {
-    constexpr int U = VEC ? 2 : 4;
-    constexpr int V = VEC ? 16 / (int)sizeof(W) : 1;
-    const OuterEntry *tab = reinterpret_cast<const OuterEntry *>(smem + d.off_tab);
-    const uint32_t n_in = d.n_in;
-    const int64_t g_in = d.g_in;
-    const uint32_t s_in = d.s_in;
-    const int64_t vs = d.vstride;
-    for (uint32_t o = t.grp; o < d.n_outer; o += d.ngroups) {
-        const OuterEntry e = tab[o];
-        W *gp = gdst + (t.g + e.g);
-        const W *sp = buf + (t.s + e.s);
-        if (mask == 0) {
-            uint32_t i = 0;
-            for (; i + U <= n_in; i += U) {
-                if constexpr (VEC) {
-                    uint4 v[U];
-#pragma unroll
-                    for (int u = 0; u < U; ++u) v[u] = *reinterpret_cast<const uint4 *>(sp + u * s_in);
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const W *w = reinterpret_cast<const W *>(&v[u]);
-#pragma unroll
-                        for (int j = 0; j < V; ++j) gp[u * g_in + j * vs] = w[j];
-                    }
-                } else {
-                    W v[U];
-#pragma unroll
-                    for (int u = 0; u < U; ++u) v[u] = sp[u * s_in];
-#pragma unroll
-                    for (int u = 0; u < U; ++u) gp[u * g_in] = v[u];
-                }
-                gp += U * g_in;
-                sp += U * s_in;
-            }
-            for (; i < n_in; ++i) {
-                if constexpr (VEC) {
-                    uint4 v = *reinterpret_cast<const uint4 *>(sp);
-                    const W *w = reinterpret_cast<const W *>(&v);
-#pragma unroll
-                    for (int j = 0; j < V; ++j) gp[j * vs] = w[j];
-                } else {
-                    *gp = *sp;
-                }
-                gp += g_in;
-                sp += s_in;
-            }
-        } else {
-            uint32_t c0 = t.c0 + e.c0, c1 = t.c1 + e.c1, c2 = t.c2;
-            for (uint32_t i = 0; i < n_in; ++i) {
-                if (slot_ok(mask, c0, c1, c2, lim)) {
-                    if constexpr (VEC) {
-                        uint4 v = *reinterpret_cast<const uint4 *>(sp);
-                        const W *w = reinterpret_cast<const W *>(&v);
-#pragma unroll
-                        for (int j = 0; j < V; ++j) gp[j * vs] = w[j];
-                    } else {
-                        *gp = *sp;
-                    }
-                }
-                gp += g_in;
-                sp += s_in;
-                c0 += d.c_in[0];
-                c1 += d.c_in[1];
-                c2 += d.c_in[2];
-            }
-        }
-    }
-}
-
-template <typename W>
-__device__ __forceinline__ void tile_write(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
-                                           W *__restrict__ gdst, const W *buf, uint32_t mask,
-                                           const Lim lim) {
-    if (!t.active) return;
-    if constexpr (sizeof(W) == 4 || sizeof(W) == 8) {
-        if (d.vec > 1) {
-            tile_write_impl<W, true>(d, t, smem, gdst, buf, mask, lim);
-            return;
-        }
-    }
-    tile_write_impl<W, false>(d, t, smem, gdst, buf, mask, lim);
-}
-
-// Warp 0 decodes tile `t` into slot `k`: source/destination base offsets and
-// the valid extents of the ragged boundary dims a and c.
-__device__ __forceinline__ void decode_tile(const TileParams &p, uint32_t t, int64_t (*s_base)[2],
-                                            uint32_t (*s_valid)[2], int k) {
-    const uint32_t lane = threadIdx.x & 31;
-    int64_t sb = 0, db = 0;
-    uint32_t va = p.e_a, vc = p.e_c;
-    for (int i = (int)lane; i < p.ngrid; i += 32) {
-        uint32_t q = fdiv(t, p.grid[i].cum);
-        uint32_t c = q - fdiv(q, p.grid[i].ext) * p.grid[i].ext.d;
-        sb += (int64_t)c * p.grid[i].src_stride;
-        db += (int64_t)c * p.grid[i].dst_stride;
-        if (i == p.grid_a) va = min(p.e_a, p.d_a - c * p.e_a);
-        if (i == p.grid_c) vc = min(p.e_c, p.d_c - c * p.e_c);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        sb += __shfl_xor_sync(0xffffffffu, sb, o);
-        db += __shfl_xor_sync(0xffffffffu, db, o);
-        va = min(va, __shfl_xor_sync(0xffffffffu, va, o));
-        vc = min(vc, __shfl_xor_sync(0xffffffffu, vc, o));
-    }
-    if (lane == 0) {
-        s_base[k][0] = sb;
-        s_base[k][1] = db;
-        s_valid[k][0] = va;
-        s_valid[k][1] = vc;
-    }
-}
-
-template <int N>
-__device__ __forceinline__ void cp_async_wait_group() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
-// wait until at most n committed cp.async groups are pending (n < 8)
-__device__ __forceinline__ void cp_async_wait_pending(uint32_t n) {
-    switch (n) {
-        case 0: cp_async_wait_group<0>(); break;
-        case 1: cp_async_wait_group<1>(); break;
-        case 2: cp_async_wait_group<2>(); break;
-        case 3: cp_async_wait_group<3>(); break;
-        case 4: cp_async_wait_group<4>(); break;
-        case 5: cp_async_wait_group<5>(); break;
-        case 6: cp_async_wait_group<6>(); break;
-        default: cp_async_wait_group<7>(); break;
-    }
-}
-
-constexpr int kMaxStages = 8;
-constexpr int kRing = kMaxStages + 2;
-
-// Persistent CTAs walk tiles t_k = blockIdx.x + k*gridDim.x through an
-// S-stage cp.async pipeline (S = p.nbuf smem tile buffers): the prologue
-// streams the source runs of the first S tiles; each iteration writes tile
-// k out of its buffer and refills that buffer with tile k+S.  Small
-// problems are thereby staged in one wave; large ones keep S-1 tiles of
-// loads in flight per CTA.  Without ASYNC (1- and 2-byte words) a single
-// buffer is filled by LDG+STS.
-template <typename W, bool ASYNC>
-__global__ void __launch_bounds__(256) tile_kernel(const __grid_constant__ TileParams p,
+__global__ void __launch_bounds__(1024) tile_kernel(const __grid_constant__ TileParams p,
                                                    const W *__restrict__ src, W *__restrict__ dst) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ int64_t s_base[kRing][2];
-    __shared__ uint32_t s_valid[kRing][2];
-    const uint32_t tid = threadIdx.x, NT = blockDim.x;
-    const uint32_t first = blockIdx.x, step = gridDim.x;
-    if (first >= p.num_tiles) return;
-    const uint32_t cnt = (p.num_tiles - first + step - 1) / step;   // tiles of this CTA
-    const uint32_t S = ASYNC ? p.nbuf : 1u;
-    const uint32_t R = S + 2;
-
-    // per-CTA outer tables of both phases
-    for (int ph = 0; ph < 2; ++ph) {
-        const PhaseDesc &d = p.ph[ph];
-        OuterEntry *tab = reinterpret_cast<OuterEntry *>(smem + d.off_tab);
-        for (uint32_t o = tid; o < d.n_outer; o += NT) {
-            uint32_t idx = o, s = 0, c0 = 0, c1 = 0;
-            int64_t g = 0;
-            for (int i = 0; i < d.nout_dims; ++i) {
-                uint32_t q = fdiv(idx, d.out[i].div);
-                uint32_t c = idx - q * d.out[i].div.d;
-                idx = q;
-                g += (int64_t)c * d.out[i].gstride;
-                s += c * d.out[i].sstride;
-                if (d.out[i].slot == 0) c0 = c * d.out[i].cmul;
-                else if (d.out[i].slot == 1) c1 = c * d.out[i].cmul;
-            }
-            OuterEntry e;
-            e.g = g;
-            e.s = s;
-            e.c0 = (uint16_t)c0;
-            e.c1 = (uint16_t)c1;
-            tab[o] = e;
-        }
-    }
-    const ThreadPart tr = decode_thread(p.ph[0], tid);
-    const ThreadPart tw = decode_thread(p.ph[1], tid);
-    W *const buf0 = reinterpret_cast<W *>(smem + p.off_buf);
-    const size_t bstride = ((size_t)p.tile_elems_alloc * sizeof(W) + 15) / 16 * 16 / sizeof(W);
-
-    if (tid < 32)
-        for (uint32_t j = 0; j < S && j < cnt; ++j) decode_tile(p, first + j * step, s_base, s_valid, (int)j);
-    __syncthreads();
-    auto limits = [&](uint32_t slot, int ph, Lim &lim) -> uint32_t {
-        const uint32_t va = s_valid[slot][0], vc = s_valid[slot][1];
-        lim.l0 = va;
-        lim.l1 = vc;
-        lim.l2 = p.lim_split[ph];
-        const bool full = (va == p.e_a) && (vc == p.e_c);
-        return full ? p.ph[ph].mask_full : p.ph[ph].mask_ragged;
-    };
-    auto load = [&](uint32_t k, W *b) {
-        Lim lim;
-        const uint32_t slot = k % R;
-        const uint32_t m = limits(slot, 0, lim);
-        tile_read<W, ASYNC>(p.ph[0], tr, smem, src + s_base[slot][0], b, m, lim);
-    };
-    // prologue: fill every stage
-    for (uint32_t j = 0; j < S; ++j) {
-        if (j < cnt) load(j, buf0 + j * bstride);
-        if constexpr (ASYNC) cp_async_commit();
-    }
-    for (uint32_t k = 0; k < cnt; ++k) {
-        if (tid < 32 && k + S < cnt) decode_tile(p, first + (k + S) * step, s_base, s_valid, (int)((k + S) % R));
-        if constexpr (ASYNC) cp_async_wait_pending(S - 1);
-        __syncthreads();
-        W *b = buf0 + (k % S) * bstride;
-        {
-            Lim lim;
-            const uint32_t slot = k % R;
-            const uint32_t m = limits(slot, 1, lim);
-            tile_write<W>(p.ph[1], tw, smem, dst + s_base[slot][1], b, m, lim);
-        }
-        __syncthreads();
-        if (k + S < cnt) load(k + S, b);
-        if constexpr (ASYNC) cp_async_commit();
-    }
+    tile_body<W, ASYNC>(p, src, dst);
 }
 
 // ------------------------------------------------------------------ GATHER (K0)
@@ -527,16 +149,47 @@ int occupancy(K kernel, int threads, int smem) {
     return nb;
 }
 
+int occupancy_ptr(const void *kernel, int threads, int smem) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto key = std::make_tuple(kernel, threads, smem + (dev << 24));
+    auto it = g_occ.find(key);
+    if (it != g_occ.end()) return it->second;
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, threads, smem) != cudaSuccess || nb < 1) {
+        cudaGetLastError();
+        nb = 1;
+    }
+    g_occ[key] = nb;
+    return nb;
+}
+
 template <int E>
 vpg_status launch_tile(const vpg_plan *p, const void *src, void *dst, cudaStream_t st) {
     using W = typename WordOf<E>::T;
     const int smem = (int)p->tile.smem_bytes;
+    const bool aligned = !(p->tile.ph[0].vec > 1 && ((uintptr_t)src % 16));
+    if (p->jit && aligned) {
+        cudaKernel_t jk = jit_tile_kernel(p);
+        if (jk) {
+            int nb = occupancy_ptr((const void *)jk, p->threads, smem);
+            int64_t grid = p->tile.num_tiles;
+            if (p->tile.persistent) grid = std::min<int64_t>(grid, (int64_t)nb * sm_count_for_current());
+            if (grid < 1) grid = 1;
+            void *args[] = {(void *)&src, (void *)&dst};
+            if (cudaLaunchKernel((const void *)jk, dim3((unsigned)grid), dim3(p->threads), args, (size_t)smem, st) ==
+                cudaSuccess)
+                return VPG_OK;
+            cudaGetLastError();   // fall through to the ahead-of-time kernel
+        }
+    }
     auto launch = [&](auto k) {
         int nb = occupancy(k, p->threads, smem);
         int64_t grid = p->tile.num_tiles;
         if (p->tile.persistent) grid = std::min<int64_t>(grid, (int64_t)nb * sm_count_for_current());
         if (grid < 1) grid = 1;
-        const TileParams &tp = (p->tile.ph[0].vec > 1 && ((uintptr_t)src % 16)) ? p->tile_unaligned : p->tile;
+        const TileParams &tp = aligned ? p->tile : p->tile_unaligned;
         k<<<(unsigned)grid, p->threads, smem, st>>>(tp, (const W *)src, (W *)dst);
     };
     if constexpr (E >= 4) {

@@ -12,155 +12,10 @@
 #include <string>
 
 #include "vpgpu.h"
+#include <cuda_runtime.h>
 
-namespace vpg {
+#include "plan_params.h"
 
-// Merged ranks are bounded by log2(numel) since size-1 dims are dropped:
-// 40 covers any tensor that fits in HBM (2^40 elements).
-constexpr int kMaxRank = 40;
-// Dims inside one tile (each >= 2 after merge, tile <= 2^14 elements).
-constexpr int kMaxTileDims = 16;
-
-// Division by a run-time invariant 32-bit divisor via multiply-high
-// (round-up method): q = (umulhi(n, m) + n) >> s, exact for all n < 2^32.
-struct FastDiv {
-    uint32_t d;
-    uint32_t m;
-    uint32_t s;
-};
-
-inline FastDiv make_fastdiv(uint32_t d) {
-    uint32_t l = 0;
-    while (l < 32 && (1ull << l) < d) ++l;
-    uint64_t m = (((1ull << 32) * ((1ull << l) - d)) / d) + 1;
-    FastDiv f;
-    f.d = d;
-    f.m = (uint32_t)m;
-    f.s = l;
-    return f;
-}
-
-inline uint32_t host_fastdiv(uint32_t n, FastDiv f) {
-    uint64_t t = ((uint64_t)n * f.m) >> 32;
-    return (uint32_t)((t + n) >> f.s);
-}
-
-// --------------------------------------------------------------------------
-// TILE (K2/K3) parameters.
-//
-// The tile is a sub-box of the merged tensor made of
-//   * the source run: dims 0..s-1 in source order, the last possibly
-//     partial (extent e < d): one contiguous source range of Ls elements;
-//   * the destination run: dims sigma[0..t-1], the last possibly partial:
-//     one contiguous destination range of Ld elements;
-//   * the union of both (the tile).  Tile elements are staged in shared
-//     memory in source order with the run pitch padded to kill bank
-//     conflicts on the transposed side.
-// The remaining dims (and the tile positions along partial dims) form the
-// grid digits, ordered by destination stride (fastest first) like the
-// reference's counter digits (planner.py:324-342).
-//
-// Each of the two phases (R: global->smem in source order, W: smem->global
-// in destination order) walks the tile as a separable 3-level nest so the
-// per-element work is two adds, one predicate and the memory op:
-//   thread part  -- the first phase dims (partial last one, factor f),
-//                   decoded once per CTA: per-thread global/smem offsets;
-//   inner dim    -- one dim with constant strides (stepped by f when it is
-//                   the split dim), unrolled;
-//   outer dims   -- the rest, through a per-CTA table in shared memory.
-// Threads beyond one thread part form G groups that share the outer loop.
-constexpr int kNumSlots = 3;      // checked coordinates: 0 = dim a, 1 = dim c, 2 = split padding
-constexpr int kMaxPhaseDims = 12; // thread-part / outer dims per phase
-
-struct GridDigit {
-    FastDiv cum;         // divides tile index by the product of faster digits
-    FastDiv ext;         // divides by this digit's extent
-    int64_t src_stride;  // elements, already multiplied by the tile extent
-    int64_t dst_stride;
-};
-
-struct PhaseDim {
-    FastDiv div;         // divides by extent
-    int64_t gstride;     // global stride (elements; src for R, dst for W)
-    uint32_t sstride;    // smem stride (elements)
-    int16_t slot;        // coordinate slot fed by this dim (-1 none)
-    uint16_t cmul;       // coordinate units per step (V for vector-grouped dims)
-};
-
-struct PhaseDesc {
-    uint32_t nthr;                 // threads in one thread part (NTP)
-    uint32_t ngroups;              // G
-    int32_t nthr_dims;
-    PhaseDim thr[kMaxPhaseDims];    // thread-part dims (fastest first)
-    uint32_t n_in;                 // inner-dim steps
-    int64_t g_in;                  // inner-dim global stride per step
-    uint32_t s_in;                 // inner-dim smem stride per step
-    uint32_t c_in[kNumSlots];      // inner-dim coordinate increment per slot
-    uint32_t n_outer;
-    int32_t nout_dims;
-    PhaseDim out[kMaxPhaseDims];    // outer dims (fastest first)
-    uint32_t vec;                  // elements per access: 1, or V = 16/E (16-byte accesses)
-    int64_t vstride;               // W with vec > 1: global stride between the V elements
-    uint32_t mask_full;            // slots checked in every tile (padding)
-    uint32_t mask_ragged;          // slots checked in ragged tiles
-    uint32_t off_tab;              // smem byte offset of this phase's outer table
-};
-
-struct TileParams {
-    uint32_t num_tiles;
-    int32_t ngrid;
-    uint32_t Ls, Ld;               // source / destination run lengths (elements)
-    uint32_t T;                    // tile elements
-    uint32_t pitch;                // smem pitch of one source run (elements, >= Ls)
-    uint32_t tile_elems_alloc;     // elements of one smem tile buffer (Ns * pitch)
-    // ragged boundary dims: a = source-run boundary, c = destination-run boundary
-    int32_t grid_a, grid_c;        // grid digit carrying the tile position along a / c (-1: not partial)
-    uint32_t e_a, d_a, e_c, d_c;
-    uint32_t lim_split[2];         // static limit of slot 2 per phase (R, W)
-    PhaseDesc ph[2];               // 0 = R (read), 1 = W (write)
-    GridDigit grid[kMaxRank];
-    uint32_t off_buf;              // smem byte offset of the tile buffers
-    uint32_t nbuf;                 // 1 or 2 (double-buffered cp.async)
-    uint32_t persistent;           // 1: grid = resident CTAs, 0: one CTA per tile
-    uint32_t smem_bytes;
-};
-static_assert(sizeof(TileParams) <= 4096, "kernel parameter block must stay under 4 KB");
-
-// --------------------------------------------------------------------------
-// ROWS (K1): stride-1 preserved; each destination row of Lr elements is a
-// contiguous source row.  Row q (destination order) starts at q*Lr in dst
-// and at sum_j digit_j(q) * in_stride[sigma[j]] in src.
-struct RowDigit {
-    FastDiv ext;
-    int64_t src_stride;
-};
-
-struct RowsParams {
-    uint32_t nrows;
-    uint32_t row_vecs;         // Lr / V
-    uint32_t vec;              // V: elements per vector
-    uint32_t tpr_log2;         // threads per row group (log2)
-    int64_t row_len;           // Lr (elements)
-    int32_t ndig;
-    RowDigit dig[kMaxRank];    // destination dims 1..r-1, fastest first
-};
-
-// --------------------------------------------------------------------------
-// COPY: merged to rank 1.
-struct CopyParams {
-    int64_t n;                 // elements
-};
-
-// --------------------------------------------------------------------------
-// GATHER (K0): out[i] = in[f(i)], per element (core.py:173-178).
-struct GatherParams {
-    uint32_t n;
-    int32_t rank;
-    FastDiv ext[kMaxRank];     // destination dims, fastest first
-    int64_t src_stride[kMaxRank];
-};
-
-}  // namespace vpg
 
 struct vpg_plan {
     int32_t kernel_class;      // vpg_kernel_class
@@ -173,6 +28,7 @@ struct vpg_plan {
     int64_t grid_hint;
     double predicted_eff;
     double tile_util;
+    int32_t jit;               // TILE: launch the NVRTC-specialised kernel (jit.cpp)
     vpg::TileParams tile;
     vpg::TileParams tile_unaligned;   // same tile, scalar source reads
     vpg::RowsParams rows;
@@ -184,5 +40,11 @@ struct vpg_plan {
 namespace vpg {
 // kernels.cu
 vpg_status launch_plan(const vpg_plan *p, const void *src, void *dst, void *stream, std::string *err);
+cudaKernel_t jit_tile_kernel(const vpg_plan *p);
+void jit_forget(const vpg_plan *p);
+int jit_state(const vpg_plan *p);
+const char *jit_last_log();
+std::string jit_source(const vpg_plan *p);
+bool jit_compile_check(const vpg_plan *p, std::string *log);
 int device_sm_count();
 }  // namespace vpg

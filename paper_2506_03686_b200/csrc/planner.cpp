@@ -691,6 +691,7 @@ static void describe(vpg_plan *p) {
         }
         put("vector elems: R %u, W %u\n", t.ph[0].vec, t.ph[1].vec);
         put("lane utilisation (R*W): %.3f\n", p->tile_util);
+        put("specialised (NVRTC) kernel: %s\n", p->jit ? "yes" : "no");
         put("tiles: %u, grid digits: %d\n", t.num_tiles, t.ngrid);
     } else if (p->kernel_class == VPG_KERNEL_ROWS) {
         put("rows: %u x %lld elements, vector %u elements, %u threads/row\n", p->rows.nrows,
@@ -852,6 +853,11 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         p->threads = threads;
         p->tile.persistent = persist_mode < 0 ? 1u : (uint32_t)persist_mode;
         p->tile_unaligned.persistent = p->tile.persistent;
+        // per-case specialisation pays off once the tensor is large enough to
+        // amortise a one-off NVRTC compile (cached in-process and on disk)
+        const char *je = getenv("VPG_JIT");
+        bool big = P.n * E >= ((int64_t)4 << 20);
+        p->jit = (flags & VPG_FORCE_JIT) ? 1 : (flags & VPG_NO_JIT) ? 0 : je ? (atoi(je) != 0) : big;
         p->grid_hint = std::min<int64_t>(p->tile.num_tiles, 148 * 4);
         p->predicted_eff = 2.0 / (1.0 / g.eff_s + 1.0 / g.eff_d);
     }

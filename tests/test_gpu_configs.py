@@ -35,6 +35,9 @@ def test_config_full_size(cuda, cfg):
     y = permute(xd, wl.axes)
     torch.cuda.synchronize()
     assert tuple(y.shape) == wl.out_shape
+    from paper_2506_03686_b200 import TensorLayout, build_program, from_numpy_convention
+    prog = build_program(TensorLayout.from_shape(wl.shape, wl.elem_bytes), from_numpy_convention(wl.axes))
+    assert prog.kernel == "rows" or prog.jit_state == 2     # large tile plans run specialised kernels
     got = y.cpu().numpy()
     assert sha256(got) == ref["output_sha256"], cfg
     # and the C oracle on the same bytes (independent of the digest)
@@ -74,3 +77,21 @@ def test_config_matches_torch_permute(cuda, cfg):
     else:
         want = x.permute(wl.axes).contiguous()
     assert torch.equal(y.reshape(-1).view(torch.int32), want.reshape(-1).view(torch.int32))
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2", "cfg3", "cfg5"])
+def test_config_ahead_of_time_kernel(cuda, cfg):
+    """The ahead-of-time (run-time parameter) tile kernel at full size too."""
+    import torch
+
+    from paper_2506_03686_b200 import TensorLayout, build_program, from_numpy_convention
+    from paper_2506_03686_b200.api import execute_device
+    from paper_2506_03686_b200.workloads import CONFIGS, make_input
+
+    wl = CONFIGS[cfg]
+    x = make_input(wl)
+    prog = build_program(TensorLayout.from_shape(wl.shape, wl.elem_bytes), from_numpy_convention(wl.axes),
+                         jit=False)
+    y = execute_device(prog, torch.from_numpy(x).to(cuda))
+    assert prog.jit_state == 0
+    assert sha256(y.cpu().numpy()) == golden()["full_configs"][cfg]["output_sha256"]

@@ -116,3 +116,27 @@ def test_random_general_vs_oracle_large(cuda):
         want = oracle.naive_permute_c(data, dims, sigma)
         out, prog = gpu_permute_bytes(dims, sigma, elem, data)
         assert np.array_equal(out, want.view(np.uint8)), (dims, sigma, elem, prog.text)
+
+
+def test_golden_cases_specialised_kernels(cuda):
+    """Per-case NVRTC-specialised tile kernels (jit.cpp) on the known-answer,
+    paper, merge, edge and ragged cases plus a seeded sample of the
+    reference campaign."""
+    import random
+
+    cases = _cases({"known", "paper", "merge", "edge"})
+    camp = [c for c in golden()["cases"] if c["family"].startswith("campaign_") and c["n"] > 1]
+    random.Random(7).shuffle(camp)
+    cases += camp[:60] + _cases({"ragged"})[:20]
+    for c in cases:
+        data = golden_pattern(c["n"], c["elem"])
+        from paper_2506_03686_b200 import PermutationMap, TensorLayout, build_program
+        from paper_2506_03686_b200.api import execute_device
+        import torch
+
+        prog = build_program(TensorLayout(tuple(c["dims"]), c["elem"]), PermutationMap(tuple(c["sigma"])),
+                             force="tile", jit=True)
+        x = torch.from_numpy(data.view(np.uint8).copy()).cuda()
+        out = execute_device(prog, x).cpu().numpy().reshape(-1)
+        assert prog.jit_state == 2, (c["name"], "specialised kernel not loaded")
+        assert sha256(out) == c["sha256"], (c["name"], prog.text)
