@@ -136,6 +136,11 @@ vpg_status vpg_plan_emit_source(const vpg_plan *plan, char *buf, size_t len);
  * GPU; the analog of verify_native's compile step, emit.py:444-483). */
 vpg_status vpg_plan_jit_compile(const vpg_plan *plan);
 
+/* Raw kernel parameter block of a TILE plan (inspection / host-side
+ * validation of the tile walk, tests/sim_tile.py -- the analog of the
+ * reference VM's role of checking a program before hardware runs it). */
+vpg_status vpg_plan_tile_params(const vpg_plan *plan, void *buf, size_t len, size_t *needed);
+
 void vpg_plan_destroy(vpg_plan *plan);
 
 #ifdef __cplusplus

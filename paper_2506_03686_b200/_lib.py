@@ -35,6 +35,7 @@ EXPORTED = (
     "vpg_plan_describe",
     "vpg_plan_emit_source",
     "vpg_plan_jit_compile",
+    "vpg_plan_tile_params",
     "vpg_plan_destroy",
 )
 
@@ -99,11 +100,12 @@ def lib():
         L.vpg_plan_describe.argtypes = [vp, ctypes.c_char_p, ctypes.c_size_t]
         L.vpg_plan_emit_source.argtypes = [vp, ctypes.c_char_p, ctypes.c_size_t]
         L.vpg_plan_jit_compile.argtypes = [vp]
+        L.vpg_plan_tile_params.argtypes = [vp, vp, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
         L.vpg_plan_destroy.argtypes = [vp]
         L.vpg_plan_destroy.restype = None
         for name in ("vpg_merge_dimensions", "vpg_plan_create", "vpg_permute", "vpg_permute_host",
                      "vpg_permute_nd", "vpg_plan_info_get", "vpg_plan_describe", "vpg_plan_emit_source",
-                     "vpg_plan_jit_compile"):
+                     "vpg_plan_jit_compile", "vpg_plan_tile_params"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
         return L

@@ -180,6 +180,15 @@ vpg_status vpg_plan_emit_source(const vpg_plan *p, char *buf, size_t len) {
     return VPG_OK;
 }
 
+vpg_status vpg_plan_tile_params(const vpg_plan *p, void *buf, size_t len, size_t *needed) {
+    if (!p) return fail(VPG_EINVAL, "null argument");
+    if (needed) *needed = sizeof(vpg::TileParams);
+    if (p->kernel_class != VPG_KERNEL_TILE) return fail(VPG_EUNSUPPORTED, "not a tile plan");
+    if (!buf || len < sizeof(vpg::TileParams)) return fail(VPG_EINVAL, "buffer too small");
+    memcpy(buf, &p->tile, sizeof(vpg::TileParams));
+    return VPG_OK;
+}
+
 vpg_status vpg_plan_jit_compile(const vpg_plan *p) {
     if (!p) return fail(VPG_EINVAL, "null argument");
     if (p->kernel_class != VPG_KERNEL_TILE) return fail(VPG_EUNSUPPORTED, "only tile plans are specialised");

@@ -15,6 +15,7 @@ typedef int int32_t;
 typedef unsigned int uint32_t;
 typedef long long int64_t;
 typedef unsigned long long uint64_t;
+typedef unsigned long long uintptr_t;
 #else
 #include <stdint.h>
 #endif
@@ -79,6 +80,7 @@ inline uint32_t host_fastdiv(uint32_t n, FastDiv f) {
 // Threads beyond one thread part form G groups that share the outer loop.
 constexpr int kNumSlots = 3;      // checked coordinates: 0 = dim a, 1 = dim c, 2 = split padding
 constexpr int kMaxPhaseDims = 12; // thread-part / outer dims per phase
+constexpr unsigned long long kOuterEntryBytes = 24;  // sizeof(OuterEntry) in tile_body.cuh
 
 struct GridDigit {
     FastDiv cum;         // divides tile index by the product of faster digits
@@ -93,6 +95,8 @@ struct PhaseDim {
     uint32_t sstride;    // smem stride (elements)
     int16_t slot;        // coordinate slot fed by this dim (-1 none)
     uint16_t cmul;       // coordinate units per step (V for vector-grouped dims)
+    uint16_t hmul;       // W in shifted-run mode: source-alignment shift per step (mod V)
+    uint16_t pad_;
 };
 
 struct PhaseDesc {
@@ -108,6 +112,8 @@ struct PhaseDesc {
     int32_t nout_dims;
     PhaseDim out[kMaxPhaseDims];    // outer dims (fastest first)
     uint32_t vec;                  // elements per access: 1, or V = 16/E (16-byte accesses)
+    uint32_t rshift;               // R: source runs read as 16-byte aligned supersets (misaligned runs)
+    uint32_t h_in;                 // W in shifted-run mode: shift increment per inner step
     int64_t vstride;               // W with vec > 1: global stride between the V elements
     uint32_t mask_full;            // slots checked in every tile (padding)
     uint32_t mask_ragged;          // slots checked in ragged tiles
@@ -115,6 +121,7 @@ struct PhaseDesc {
 };
 
 struct TileParams {
+    int64_t n_elems;               // elements of the whole tensor (source bounds in shifted-run mode)
     uint32_t num_tiles;
     int32_t ngrid;
     uint32_t Ls, Ld;               // source / destination run lengths (elements)
@@ -125,6 +132,7 @@ struct TileParams {
     int32_t grid_a, grid_c;        // grid digit carrying the tile position along a / c (-1: not partial)
     uint32_t e_a, d_a, e_c, d_c;
     uint32_t lim_split[2];         // static limit of slot 2 per phase (R, W)
+    uint32_t hmask;                // shifted-run mode: V-1 (source runs sit at offset h in their smem row), else 0
     PhaseDesc ph[2];               // 0 = R (read), 1 = W (write)
     GridDigit grid[kMaxRank];
     uint32_t off_buf;              // smem byte offset of the tile buffers

@@ -61,6 +61,7 @@ struct Problem {
     int64_t budget;       // staged tile bytes per CTA buffer
     int nbuf;             // forced pipeline stages (0 = planner's choice)
     int64_t cta_smem;     // per-CTA shared-memory target (bytes)
+    bool no_shift = false; // disable shifted-run reads (VPG_NO_SHIFT)
     int r;
     int64_t d[kMaxRank];
     int sigma[kMaxRank];
@@ -260,6 +261,7 @@ struct PDimH {
     int64_t e, g, s;
     int slot;
     int64_t cmul;
+    int64_t hmul = 0;    // shifted-run mode, W phase: source alignment shift per step
 };
 
 // Vectorisation choice for one tile: R groups the leading source-run entry
@@ -267,6 +269,7 @@ struct PDimH {
 // one 16-byte shared-memory load feeding V coalesced scalar stores.
 struct VecChoice {
     int vr = 1, vw = 1;
+    bool rshift = false;   // R reads 16-byte aligned supersets of misaligned runs
 };
 
 // smem strides of the tile dims for a given pitch (source run dense, run
@@ -293,12 +296,15 @@ void tile_sstrides(const Problem &Pb, const TileGeom &g, uint32_t pitch, int64_t
 // R with vr > 1: the leading entry is grouped by vr.  W with vw > 1: dim 0
 // is grouped by vw (its V elements are one smem vector, stored separately).
 std::vector<PDimH> phase_dims(const Problem &Pb, const TileGeom &g, const int64_t *sstr,
-                              const int *slot_of_dim, bool write, int vec) {
+                              const int *slot_of_dim, bool write, int vec, int64_t hmask = 0) {
     std::vector<PDimH> L;
+    bool in_run[kMaxRank] = {false};
+    for (int i = 0; i < g.nsrc; ++i) in_run[g.src_dims[i]] = true;
     for (int i = 0; i < Pb.r; ++i) {
         int k = write ? Pb.sigma[i] : i;
         if (g.ext[k] == 0) continue;
         PDimH d{g.ext[k], write ? Pb.out_stride_of_dim[k] : Pb.in_stride[k], sstr[k], slot_of_dim[k], 1};
+        if (write && hmask && !in_run[k]) d.hmul = Pb.in_stride[k] & hmask;
         if (write && vec > 1 && k == 0) {
             d.e /= vec;
             d.g *= vec;
@@ -308,7 +314,7 @@ std::vector<PDimH> phase_dims(const Problem &Pb, const TileGeom &g, const int64_
         if (!L.empty()) {
             PDimH &p = L.back();
             if (p.slot < 0 && d.slot < 0 && d.g == p.g * p.e && d.s == p.s * p.e &&
-                !(write && vec > 1 && k == 0)) {
+                !(write && vec > 1 && k == 0) && p.hmul == 0 && d.hmul == 0) {
                 p.e *= d.e;
                 continue;
             }
@@ -325,7 +331,33 @@ std::vector<PDimH> phase_dims(const Problem &Pb, const TileGeom &g, const int64_
     return L;
 }
 
-void set_pdim(PhaseDim &pd, int64_t e, int64_t g, int64_t s, int slot, int64_t cmul) {
+// R dims in shifted-run mode: the whole source run becomes NCK 16-byte
+// chunks (one leading entry), followed by the run-index dims.
+std::vector<PDimH> shift_r_dims(const Problem &Pb, const TileGeom &g, const int64_t *sstr, const int *slot_of_dim,
+                                int V) {
+    std::vector<PDimH> L;
+    const int64_t nck = (g.Ls + V - 1 + V - 1) / V;
+    L.push_back(PDimH{nck, V, V, -1, 1});
+    bool in_run[kMaxRank] = {false};
+    for (int i = 0; i < g.nsrc; ++i) in_run[g.src_dims[i]] = true;
+    for (int k = 0; k < Pb.r; ++k) {
+        if (g.ext[k] == 0 || in_run[k]) continue;
+        PDimH d{g.ext[k], Pb.in_stride[k], sstr[k], slot_of_dim[k], 1};
+        if (L.size() > 1) {
+            PDimH &p = L.back();
+            if (p.slot < 0 && d.slot < 0 && d.g == p.g * p.e && d.s == p.s * p.e) {
+                p.e *= d.e;
+                continue;
+            }
+        }
+        L.push_back(d);
+    }
+    return L;
+}
+
+void set_pdim(PhaseDim &pd, int64_t e, int64_t g, int64_t s, int slot, int64_t cmul, int64_t hmul = 0) {
+    pd.hmul = (uint16_t)hmul;
+    pd.pad_ = 0;
     pd.div = make_fastdiv((uint32_t)e);
     pd.gstride = g;
     pd.sstride = (uint32_t)s;
@@ -359,9 +391,21 @@ double make_phase(const std::vector<PDimH> &L, int NT, PhaseDesc &pd, uint32_t &
             double lane = (double)(G * ntp) / NT;
             double pad = (double)L[h].e / (double)(f * steps);
             double bal = (double)n_outer / (double)(G * ((n_outer + G - 1) / G));
-            // coalescing: consecutive lanes must walk the stride-1 dim L[0]
-            double cover0 = (double)(h == 0 ? f : L[0].e);
-            double coal = std::min(1.0, cover0 / (double)std::min<int64_t>(32, L[0].e));
+            // coalescing: consecutive lanes must walk globally contiguous
+            // elements; `avail` = contiguous extent of the leading dims,
+            // `cover` = how much of it one thread part spans
+            int64_t avail = L[0].e, cover = h == 0 ? f : L[0].e;
+            bool contig = true;
+            for (int i = 1; i < m; ++i) {
+                if (L[i].g != L[i - 1].g * L[i - 1].e) break;
+                avail *= L[i].e;
+                if (i < h) cover *= L[i].e;
+                else if (i == h && contig) cover *= f;
+            }
+            for (int i = 1; i <= h && i < m; ++i)
+                if (L[i].g != L[i - 1].g * L[i - 1].e) contig = false;
+            if (!contig) cover = h == 0 ? f : L[0].e;
+            double coal = std::min(1.0, (double)std::min<int64_t>(cover, 32) / (double)std::min<int64_t>(32, avail));
             double u = lane * pad * bal * coal;
             // ties: bigger thread parts (fewer outer-table steps), longer inner loops
             double score = u + 1e-3 * std::log2((double)ntp) + 1e-4 * (steps * f == L[h].e) +
@@ -379,7 +423,7 @@ double make_phase(const std::vector<PDimH> &L, int NT, PhaseDesc &pd, uint32_t &
     int64_t ntp = 1;
     pd.nthr_dims = 0;
     for (int i = 0; i < h; ++i) {
-        set_pdim(pd.thr[pd.nthr_dims++], L[i].e, L[i].g, L[i].s, L[i].slot, L[i].cmul);
+        set_pdim(pd.thr[pd.nthr_dims++], L[i].e, L[i].g, L[i].s, L[i].slot, L[i].cmul, L[i].hmul);
         ntp *= L[i].e;
     }
     int64_t steps = (L[h].e + f - 1) / f;
@@ -389,7 +433,7 @@ double make_phase(const std::vector<PDimH> &L, int NT, PhaseDesc &pd, uint32_t &
         split_slot = 2;
         lim_split = (uint32_t)(L[h].e * L[h].cmul);
     }
-    set_pdim(pd.thr[pd.nthr_dims++], f, L[h].g, L[h].s, split_slot, L[h].cmul);
+    set_pdim(pd.thr[pd.nthr_dims++], f, L[h].g, L[h].s, split_slot, L[h].cmul, L[h].hmul);
     ntp *= f;
     int first_outer;
     if (steps > 1) {
@@ -397,12 +441,14 @@ double make_phase(const std::vector<PDimH> &L, int NT, PhaseDesc &pd, uint32_t &
         pd.g_in = L[h].g * f;
         pd.s_in = (uint32_t)(L[h].s * f);
         if (split_slot >= 0) pd.c_in[split_slot] = (uint32_t)(f * L[h].cmul);
+        pd.h_in = (uint32_t)(f * L[h].hmul);
         first_outer = h + 1;
     } else if (h + 1 < m) {
         pd.n_in = (uint32_t)L[h + 1].e;
         pd.g_in = L[h + 1].g;
         pd.s_in = (uint32_t)L[h + 1].s;
         if (L[h + 1].slot >= 0) pd.c_in[L[h + 1].slot] = (uint32_t)L[h + 1].cmul;
+        pd.h_in = (uint32_t)L[h + 1].hmul;
         first_outer = h + 2;
     } else {
         pd.n_in = 1;
@@ -413,7 +459,7 @@ double make_phase(const std::vector<PDimH> &L, int NT, PhaseDesc &pd, uint32_t &
     pd.nout_dims = 0;
     int64_t n_outer = 1;
     for (int i = first_outer; i < m; ++i) {
-        set_pdim(pd.out[pd.nout_dims++], L[i].e, L[i].g, L[i].s, L[i].slot, L[i].cmul);
+        set_pdim(pd.out[pd.nout_dims++], L[i].e, L[i].g, L[i].s, L[i].slot, L[i].cmul, L[i].hmul);
         n_outer *= L[i].e;
     }
     pd.n_outer = (uint32_t)n_outer;
@@ -431,25 +477,27 @@ double make_phase(const std::vector<PDimH> &L, int NT, PhaseDesc &pd, uint32_t &
 
 // smem element offsets seen by the lanes of one warp at inner step 0 of its
 // first outer entry (simulation of the kernel's mapping, for the bank model).
-void phase_warp_offsets(const PhaseDesc &pd, int warp, uint32_t *off, int &nl) {
+void phase_warp_offsets(const PhaseDesc &pd, int warp, uint32_t *off, int &nl, uint32_t hmask = 0) {
     nl = 0;
     for (int l = 0; l < 32; ++l) {
         uint32_t t = (uint32_t)(warp * 32 + l);
         if (t >= pd.nthr * pd.ngroups) break;
         uint32_t grp = t / pd.nthr, tr = t % pd.nthr;
-        uint32_t s = 0;
+        uint32_t s = 0, h = 0;
         for (int i = 0; i < pd.nthr_dims; ++i) {
             uint32_t q = tr / pd.thr[i].div.d;
             s += (tr - q * pd.thr[i].div.d) * pd.thr[i].sstride;
+            h += (tr - q * pd.thr[i].div.d) * pd.thr[i].hmul;
             tr = q;
         }
         uint32_t o = grp;
         for (int i = 0; i < pd.nout_dims; ++i) {
             uint32_t q = o / pd.out[i].div.d;
             s += (o - q * pd.out[i].div.d) * pd.out[i].sstride;
+            h += (o - q * pd.out[i].div.d) * pd.out[i].hmul;
             o = q;
         }
-        off[nl++] = s;
+        off[nl++] = s + (h & hmask);
     }
 }
 
@@ -499,8 +547,15 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
     for (int k = 0; k < r; ++k) slot_of_dim[k] = -1;
     if (g.a_part >= 0) slot_of_dim[g.a_part] = 0;
     if (g.c_part >= 0 && g.c_part != g.a_part) slot_of_dim[g.c_part] = 1;
-    double u0 = make_phase(phase_dims(Pb, g, sstr, slot_of_dim, false, vc.vr), NT, tp.ph[0], tp.lim_split[0]);
-    double u1 = make_phase(phase_dims(Pb, g, sstr, slot_of_dim, true, vc.vw), NT, tp.ph[1], tp.lim_split[1]);
+    const int V = 16 / Pb.E;
+    const int64_t hmask = vc.rshift ? V - 1 : 0;
+    double u0 = make_phase(vc.rshift ? shift_r_dims(Pb, g, sstr, slot_of_dim, V)
+                                     : phase_dims(Pb, g, sstr, slot_of_dim, false, vc.vr),
+                           NT, tp.ph[0], tp.lim_split[0]);
+    double u1 = make_phase(phase_dims(Pb, g, sstr, slot_of_dim, true, vc.vw, hmask), NT, tp.ph[1], tp.lim_split[1]);
+    tp.ph[0].rshift = vc.rshift ? 1u : 0u;
+    tp.hmask = (uint32_t)hmask;
+    tp.n_elems = Pb.n;
     tp.ph[0].vec = (uint32_t)vc.vr;
     tp.ph[1].vec = (uint32_t)vc.vw;
     tp.ph[1].vstride = vc.vw > 1 ? Pb.out_stride_of_dim[0] : 0;
@@ -543,8 +598,8 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
         o += (uint32_t)bytes;
         return at;
     };
-    tp.ph[0].off_tab = take(16ull * tp.ph[0].n_outer, 16);
-    tp.ph[1].off_tab = take(16ull * tp.ph[1].n_outer, 16);
+    tp.ph[0].off_tab = take(kOuterEntryBytes * tp.ph[0].n_outer, 16);
+    tp.ph[1].off_tab = take(kOuterEntryBytes * tp.ph[1].n_outer, 16);
     uint64_t buf_bytes = ((uint64_t)tp.tile_elems_alloc * Pb.E + 15) / 16 * 16;
     // pipeline depth: as many stages as fit the per-CTA smem target (two
     // CTAs per SM), at least 2, at most 8; 1- and 2-byte words use 1.
@@ -572,17 +627,20 @@ double tile_cost(const Problem &Pb, const TileParams &tp) {
         const int abytes = Pb.E * V;
         int64_t waves = 0, warps = 0;
         for (int w = 0; w < 8; ++w) {
-            phase_warp_offsets(d, w, off, nl);
+            phase_warp_offsets(d, w, off, nl, ph == 1 ? tp.hmask : 0);
             if (!nl) continue;
             for (int l = 0; l < nl; ++l) off[l] /= (uint32_t)V;     // in access units
             waves += warp_wavefronts(off, nl, abytes);
             ++warps;
         }
         if (!warps) continue;
-        double ops = (double)tp.T / V / 32.0;                      // warp memory ops per tile
-        double avg_w = (double)waves / (double)warps;
-        cost += ops * avg_w;                                        // smem wavefronts
-        cost += ops * (ph == 1 ? 1.0 + V : 1.0);                    // issued LDS/STG/LDGSTS
+        // warp-level memory ops actually issued by the walk (idle lanes included)
+        const double nwarps = std::ceil((double)d.nthr * d.ngroups / 32.0);
+        const double ops = nwarps * d.n_in * std::ceil((double)d.n_outer / d.ngroups);
+        const double avg_w = (double)waves / (double)warps;
+        const bool checked = d.mask_full != 0;
+        if (ph == 0) cost += ops * (4.0 + avg_w + (checked ? 2.0 : 0.0));           // LDGSTS: ~4 issue + smem
+        else cost += ops * (avg_w + (V > 1 ? V : 1) + 1.0 + (checked ? 2.0 : 0.0)); // LDS + STGs
     }
     return cost;
 }
@@ -592,27 +650,39 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
     const int V = (Pb.E == 4 || Pb.E == 8) ? 16 / Pb.E : 1;
     const bool rv = r_vectorizable(Pb, g, V);
     const bool wv = w_vectorizable(Pb, g, V);
+    // shifted-run reads: misaligned source runs long enough to amortise the
+    // superset (up to V-1 extra elements at each end)
+    const bool rs = V > 1 && !rv && g.Ls >= 2 * V && !Pb.no_shift;
     double best = -1.0;
     pitch_out = (uint32_t)g.Ls;
-    for (int vr : {1, V}) {
-        if (vr > 1 && !rv) continue;
+    struct Opt {
+        int vr, vw;
+        bool rshift;
+    };
+    std::vector<Opt> opts;
+    for (int vr : {1, V})
         for (int vw : {1, V}) {
-            if (vw > 1 && !wv) continue;
-            const int step = (vr > 1 || vw > 1) ? V : 1;
-            for (int pad = 0; pad <= 32; pad += step) {
-                uint32_t pitch = (uint32_t)g.Ls + pad;
-                if ((int64_t)(g.T / g.Ls) * pitch * Pb.E > Pb.budget + 8192) break;
-                TileParams tp;
-                VecChoice vc;
-                vc.vr = vr;
-                vc.vw = vw;
-                fill_tile_params(Pb, g, pitch, NT, vc, tp);
-                double c = tile_cost(Pb, tp);
-                if (best < 0 || c < best - 1e-9) {
-                    best = c;
-                    pitch_out = pitch;
-                    vc_out = vc;
-                }
+            if ((vr > 1 && !rv) || (vw > 1 && !wv)) continue;
+            opts.push_back({vr, vw, false});
+        }
+    if (rs) opts.push_back({V, 1, true});
+    for (const Opt &op : opts) {
+        const int step = (op.vr > 1 || op.vw > 1) ? V : 1;
+        const int64_t base = op.rshift ? (g.Ls + V - 1 + V - 1) / V * V : g.Ls;
+        for (int pad = 0; pad <= 32; pad += step) {
+            uint32_t pitch = (uint32_t)(base + pad);
+            if ((int64_t)(g.T / g.Ls) * pitch * Pb.E > Pb.budget + 8192) break;
+            TileParams tp;
+            VecChoice vc;
+            vc.vr = op.vr;
+            vc.vw = op.vw;
+            vc.rshift = op.rshift;
+            fill_tile_params(Pb, g, pitch, NT, vc, tp);
+            double c = tile_cost(Pb, tp);
+            if (best < 0 || c < best - 1e-9) {
+                best = c;
+                pitch_out = pitch;
+                vc_out = vc;
             }
         }
     }
@@ -689,7 +759,8 @@ static void describe(vpg_plan *p) {
                 ph ? "W" : "R", d.nthr, d.ngroups, d.nthr_dims, d.n_in, d.n_outer, d.nout_dims,
                 d.mask_full, d.mask_ragged);
         }
-        put("vector elems: R %u, W %u\n", t.ph[0].vec, t.ph[1].vec);
+        put("vector elems: R %u%s, W %u\n", t.ph[0].vec, t.ph[0].rshift ? " (aligned supersets of misaligned runs)" : "",
+            t.ph[1].vec);
         put("lane utilisation (R*W): %.3f\n", p->tile_util);
         put("specialised (NVRTC) kernel: %s\n", p->jit ? "yes" : "no");
         put("tiles: %u, grid digits: %d\n", t.num_tiles, t.ngrid);
@@ -736,6 +807,7 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
     if (const char *e = getenv("VPG_CTA_SMEM")) P.cta_smem = std::min(220L * 1024, std::max(16L * 1024, atol(e)));
     if (const char *e = getenv("VPG_PERSIST")) persist_mode = atoi(e);
     if (const char *e = getenv("VPG_THREADS")) force_threads = atoi(e);
+    if (getenv("VPG_NO_SHIFT")) P.no_shift = true;
     if (flags & VPG_NO_MERGE) {
         P.r = rank;
         for (int k = 0; k < rank; ++k) {
@@ -841,6 +913,7 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         // variant without 16-byte source reads, for misaligned base pointers
         VecChoice vs = vc;
         vs.vr = 1;
+        vs.rshift = false;
         fill_tile_params(P, g, pitch, threads, vs, p->tile_unaligned);
         // the tile count must fit the 32-bit tile index
         double nt = 1.0;

@@ -54,12 +54,16 @@ struct OuterEntry {
     int64_t g;
     uint32_t s;
     uint16_t c0, c1;
+    uint32_t h;          // shifted-run mode: source-alignment shift contribution
+    uint32_t pad_;
 };
+static_assert(sizeof(OuterEntry) == kOuterEntryBytes, "planner sizes the smem tables with kOuterEntryBytes");
 
 struct ThreadPart {
     int64_t g;
     uint32_t s;
     uint32_t c0, c1, c2;
+    uint32_t h;
     uint32_t grp;
     bool active;
 };
@@ -83,6 +87,7 @@ __device__ __forceinline__ ThreadPart decode_thread(const PhaseDesc &d, uint32_t
     t.g = 0;
     t.s = 0;
     t.c0 = t.c1 = t.c2 = 0;
+    t.h = 0;
     VPG_UNROLL
     for (int i = 0; i < kMaxPhaseDims; ++i) {
         if (i >= d.nthr_dims) break;
@@ -91,6 +96,7 @@ __device__ __forceinline__ ThreadPart decode_thread(const PhaseDesc &d, uint32_t
         tr = q;
         t.g += (int64_t)c * d.thr[i].gstride;
         t.s += c * d.thr[i].sstride;
+        t.h += c * d.thr[i].hmul;
         const uint32_t cv = c * d.thr[i].cmul;
         if (d.thr[i].slot == 0) t.c0 = cv;
         else if (d.thr[i].slot == 1) t.c1 = cv;
@@ -114,6 +120,7 @@ __device__ __forceinline__ OuterEntry outer_entry(const PhaseDesc &d, const unsi
     OuterEntry e;
     e.g = 0;
     e.s = 0;
+    e.h = 0;
     uint32_t c0 = 0, c1 = 0, idx = o;
     VPG_UNROLL
     for (int i = 0; i < kMaxPhaseDims; ++i) {
@@ -123,6 +130,7 @@ __device__ __forceinline__ OuterEntry outer_entry(const PhaseDesc &d, const unsi
         idx = q;
         e.g += (int64_t)c * d.out[i].gstride;
         e.s += c * d.out[i].sstride;
+        e.h += c * d.out[i].hmul;
         if (d.out[i].slot == 0) c0 = c * d.out[i].cmul;
         else if (d.out[i].slot == 1) c1 = c * d.out[i].cmul;
     }
@@ -192,11 +200,58 @@ __device__ __forceinline__ void tile_read_impl(const PhaseDesc &d, const ThreadP
     }
 }
 
+// R phase for misaligned source runs: each run is read as the 16-byte
+// aligned superset that covers it (the address is rounded down per chunk),
+// so the run lands at offset h = (run start mod V) inside its smem row; the
+// W phase adds h back.  Chunks reaching past the end of the source buffer
+// fall back to element copies.
+template <typename W>
+__device__ __forceinline__ void tile_read_shift(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
+                                                const W *__restrict__ gsrc, const W *gend, W *buf, uint32_t mask,
+                                                const Lim lim) {
+    constexpr int V = 16 / (int)sizeof(W);
+    const uint32_t n_in = d.n_in;
+    const int64_t g_in = d.g_in;
+    const uint32_t s_in = d.s_in;
+    const uint32_t o0 = d.ngroups == 1 ? 0u : t.grp;
+    VPG_UNROLL
+    for (uint32_t o = o0; o < d.n_outer; o += d.ngroups) {
+        const OuterEntry e = outer_entry(d, smem, o);
+        const W *gp = gsrc + (t.g + e.g);
+        W *sp = buf + (t.s + e.s);
+        uint32_t c0 = t.c0 + e.c0, c1 = t.c1 + e.c1, c2 = t.c2;
+        VPG_UNROLL
+        for (uint32_t i = 0; i < n_in; ++i) {
+            if (mask == 0 || slot_ok(mask, c0, c1, c2, lim)) {
+                const W *ga = reinterpret_cast<const W *>((uintptr_t)gp & ~(uintptr_t)15);
+                if (ga + V <= gend) {
+                    cp_async<16>(sp, ga);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < V; ++j)
+                        if (ga + j < gend) cp_async<sizeof(W)>(sp + j, ga + j);
+                }
+            }
+            gp += g_in;
+            sp += s_in;
+            c0 += d.c_in[0];
+            c1 += d.c_in[1];
+            c2 += d.c_in[2];
+        }
+    }
+}
+
 template <typename W, bool ASYNC>
 __device__ __forceinline__ void tile_read(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
-                                          const W *__restrict__ gsrc, W *buf, uint32_t mask,
+                                          const W *__restrict__ gsrc, const W *gend, W *buf, uint32_t mask,
                                           const Lim lim) {
     if (!t.active) return;
+    if constexpr (ASYNC && (sizeof(W) == 4 || sizeof(W) == 8)) {
+        if (d.rshift) {
+            tile_read_shift<W>(d, t, smem, gsrc, gend, buf, mask, lim);
+            return;
+        }
+    }
     if constexpr (ASYNC && sizeof(W) < 16) {
         if (d.vec > 1) {
             tile_read_impl<W, true, true>(d, t, smem, gsrc, buf, mask, lim);
@@ -213,7 +268,7 @@ __device__ __forceinline__ void tile_read(const PhaseDesc &d, const ThreadPart &
 template <typename W, bool VEC>
 __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
                                                 W *__restrict__ gdst, const W *buf, uint32_t mask,
-                                                const Lim lim) {
+                                                const Lim lim, uint32_t hb, uint32_t hmask) {
     constexpr int U = VEC ? 2 : 4;
     constexpr int V = VEC ? 16 / (int)sizeof(W) : 1;
     const uint32_t n_in = d.n_in;
@@ -226,6 +281,8 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
         const OuterEntry e = outer_entry(d, smem, o);
         W *gp = gdst + (t.g + e.g);
         const W *sp = buf + (t.s + e.s);
+        uint32_t hh = hb + t.h + e.h;          // shifted-run mode (hmask == 0 otherwise)
+        const uint32_t h_in = d.h_in;
         if (mask == 0) {
             uint32_t i = 0;
             VPG_UNROLL
@@ -243,12 +300,13 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
                 } else {
                     W v[U];
 #pragma unroll
-                    for (int u = 0; u < U; ++u) v[u] = sp[u * s_in];
+                    for (int u = 0; u < U; ++u) v[u] = sp[u * s_in + ((hh + u * h_in) & hmask)];
 #pragma unroll
                     for (int u = 0; u < U; ++u) gp[u * g_in] = v[u];
                 }
                 gp += U * g_in;
                 sp += U * s_in;
+                hh += U * h_in;
             }
             for (; i < n_in; ++i) {
                 if constexpr (VEC) {
@@ -257,10 +315,11 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
 #pragma unroll
                     for (int j = 0; j < V; ++j) gp[j * vs] = w[j];
                 } else {
-                    *gp = *sp;
+                    *gp = sp[hh & hmask];
                 }
                 gp += g_in;
                 sp += s_in;
+                hh += h_in;
             }
         } else {
             uint32_t c0 = t.c0 + e.c0, c1 = t.c1 + e.c1, c2 = t.c2;
@@ -273,11 +332,12 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
 #pragma unroll
                         for (int j = 0; j < V; ++j) gp[j * vs] = w[j];
                     } else {
-                        *gp = *sp;
+                        *gp = sp[hh & hmask];
                     }
                 }
                 gp += g_in;
                 sp += s_in;
+                hh += h_in;
                 c0 += d.c_in[0];
                 c1 += d.c_in[1];
                 c2 += d.c_in[2];
@@ -289,15 +349,15 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
 template <typename W>
 __device__ __forceinline__ void tile_write(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
                                            W *__restrict__ gdst, const W *buf, uint32_t mask,
-                                           const Lim lim) {
+                                           const Lim lim, uint32_t hb, uint32_t hmask) {
     if (!t.active) return;
     if constexpr (sizeof(W) == 4 || sizeof(W) == 8) {
         if (d.vec > 1) {
-            tile_write_impl<W, true>(d, t, smem, gdst, buf, mask, lim);
+            tile_write_impl<W, true>(d, t, smem, gdst, buf, mask, lim, 0, 0);
             return;
         }
     }
-    tile_write_impl<W, false>(d, t, smem, gdst, buf, mask, lim);
+    tile_write_impl<W, false>(d, t, smem, gdst, buf, mask, lim, hb, hmask);
 }
 
 // Warp 0 decodes tile `t` into slot `k`: source/destination base offsets and
@@ -376,7 +436,7 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
         const PhaseDesc &d = p.ph[ph];
         OuterEntry *tab = reinterpret_cast<OuterEntry *>(smem + d.off_tab);
         for (uint32_t o = tid; o < d.n_outer; o += NT) {
-            uint32_t idx = o, s = 0, c0 = 0, c1 = 0;
+            uint32_t idx = o, s = 0, c0 = 0, c1 = 0, h = 0;
             int64_t g = 0;
             for (int i = 0; i < d.nout_dims; ++i) {
                 uint32_t q = fdiv(idx, d.out[i].div);
@@ -384,6 +444,7 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
                 idx = q;
                 g += (int64_t)c * d.out[i].gstride;
                 s += c * d.out[i].sstride;
+                h += c * d.out[i].hmul;
                 if (d.out[i].slot == 0) c0 = c * d.out[i].cmul;
                 else if (d.out[i].slot == 1) c1 = c * d.out[i].cmul;
             }
@@ -392,6 +453,8 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
             e.s = s;
             e.c0 = (uint16_t)c0;
             e.c1 = (uint16_t)c1;
+            e.h = h;
+            e.pad_ = 0;
             tab[o] = e;
         }
     }
@@ -399,6 +462,7 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
     const ThreadPart tr = decode_thread(p.ph[0], tid);
     const ThreadPart tw = decode_thread(p.ph[1], tid);
     W *const buf0 = reinterpret_cast<W *>(smem + p.off_buf);
+    const W *const gend = src + p.n_elems;
     const size_t bstride = ((size_t)p.tile_elems_alloc * sizeof(W) + 15) / 16 * 16 / sizeof(W);
 
     if (tid < 32)
@@ -416,7 +480,7 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
         Lim lim;
         const uint32_t slot = k % R;
         const uint32_t m = limits(slot, 0, lim);
-        tile_read<W, ASYNC>(p.ph[0], tr, smem, src + s_base[slot][0], b, m, lim);
+        tile_read<W, ASYNC>(p.ph[0], tr, smem, src + s_base[slot][0], gend, b, m, lim);
     };
     // prologue: fill every stage
     for (uint32_t j = 0; j < S; ++j) {
@@ -432,7 +496,8 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
             Lim lim;
             const uint32_t slot = k % R;
             const uint32_t m = limits(slot, 1, lim);
-            tile_write<W>(p.ph[1], tw, smem, dst + s_base[slot][1], b, m, lim);
+            tile_write<W>(p.ph[1], tw, smem, dst + s_base[slot][1], b, m, lim, (uint32_t)s_base[slot][0],
+                          p.hmask);
         }
         __syncthreads();
         if (k + S < cnt) load(k + S, b);

@@ -26,7 +26,7 @@ def sha256(arr) -> str:
     return hashlib.sha256(np.ascontiguousarray(arr).view(np.uint8).tobytes()).hexdigest()
 
 
-def gpu_permute_bytes(dims, sigma, elem, data: np.ndarray, force=None, merge=True):
+def gpu_permute_bytes(dims, sigma, elem, data: np.ndarray, force=None, merge=True, jit=None):
     """Run the GPU path on raw words; returns raw output bytes as uint8."""
     import torch
 
@@ -36,6 +36,6 @@ def gpu_permute_bytes(dims, sigma, elem, data: np.ndarray, force=None, merge=Tru
     raw = np.ascontiguousarray(data).reshape(-1).view(np.uint8)
     x = torch.from_numpy(raw.copy()).cuda()
     prog = build_program(TensorLayout(tuple(dims), elem), PermutationMap(tuple(sigma)),
-                         force=force, merge=merge)
+                         force=force, merge=merge, jit=jit)
     y = execute_device(prog, x)
     return y.cpu().numpy().reshape(-1), prog

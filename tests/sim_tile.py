@@ -1,0 +1,214 @@
+"""TEST INFRASTRUCTURE -- host simulation of the tile kernel's address walk.
+
+The reference validates every generated program on a guard-banded VM
+before hardware runs it (/root/reference/pkg/src/vecperm/vm.py:28-33,
+113-226).  This is the same idea for the GPU plan: it decodes the kernel
+parameter block of a TILE plan (``vpg_plan_tile_params``) and replays the
+walk of csrc/tile_body.cuh -- tile decode, thread parts, inner/outer dims,
+slot predicates, shifted-run reads, vector accesses -- in numpy, checking
+that every shared-memory and global access is in bounds and aligned and
+that the data lands where the permutation says.  It needs no GPU, so the
+CPU suite can exercise the planner on thousands of shapes.
+
+It is never used by the product (which has no CPU path).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from paper_2506_03686_b200 import _lib
+
+MAXR, MAXPD = 40, 12
+
+
+class FastDiv(ctypes.Structure):
+    _fields_ = [("d", ctypes.c_uint32), ("m", ctypes.c_uint32), ("s", ctypes.c_uint32)]
+
+
+class PhaseDim(ctypes.Structure):
+    _fields_ = [("div", FastDiv), ("gstride", ctypes.c_int64), ("sstride", ctypes.c_uint32),
+                ("slot", ctypes.c_int16), ("cmul", ctypes.c_uint16), ("hmul", ctypes.c_uint16),
+                ("pad_", ctypes.c_uint16)]
+
+
+class PhaseDesc(ctypes.Structure):
+    _fields_ = [("nthr", ctypes.c_uint32), ("ngroups", ctypes.c_uint32), ("nthr_dims", ctypes.c_int32),
+                ("thr", PhaseDim * MAXPD), ("n_in", ctypes.c_uint32), ("g_in", ctypes.c_int64),
+                ("s_in", ctypes.c_uint32), ("c_in", ctypes.c_uint32 * 3), ("n_outer", ctypes.c_uint32),
+                ("nout_dims", ctypes.c_int32), ("out", PhaseDim * MAXPD), ("vec", ctypes.c_uint32),
+                ("rshift", ctypes.c_uint32), ("h_in", ctypes.c_uint32), ("vstride", ctypes.c_int64),
+                ("mask_full", ctypes.c_uint32), ("mask_ragged", ctypes.c_uint32), ("off_tab", ctypes.c_uint32)]
+
+
+class GridDigit(ctypes.Structure):
+    _fields_ = [("cum", FastDiv), ("ext", FastDiv), ("src_stride", ctypes.c_int64), ("dst_stride", ctypes.c_int64)]
+
+
+class TileParams(ctypes.Structure):
+    _fields_ = [("n_elems", ctypes.c_int64), ("num_tiles", ctypes.c_uint32), ("ngrid", ctypes.c_int32),
+                ("Ls", ctypes.c_uint32), ("Ld", ctypes.c_uint32), ("T", ctypes.c_uint32),
+                ("pitch", ctypes.c_uint32), ("tile_elems_alloc", ctypes.c_uint32),
+                ("grid_a", ctypes.c_int32), ("grid_c", ctypes.c_int32),
+                ("e_a", ctypes.c_uint32), ("d_a", ctypes.c_uint32), ("e_c", ctypes.c_uint32),
+                ("d_c", ctypes.c_uint32), ("lim_split", ctypes.c_uint32 * 2), ("hmask", ctypes.c_uint32),
+                ("ph", PhaseDesc * 2), ("grid", GridDigit * MAXR), ("off_buf", ctypes.c_uint32),
+                ("nbuf", ctypes.c_uint32), ("persistent", ctypes.c_uint32), ("smem_bytes", ctypes.c_uint32)]
+
+
+def tile_params(program) -> TileParams:
+    L = _lib.lib()
+    need = ctypes.c_size_t(0)
+    L.vpg_plan_tile_params(program.handle, None, 0, ctypes.byref(need))
+    assert need.value == ctypes.sizeof(TileParams), (need.value, ctypes.sizeof(TileParams))
+    tp = TileParams()
+    st = L.vpg_plan_tile_params(program.handle, ctypes.byref(tp), ctypes.sizeof(tp), None)
+    assert st == 0, _lib.last_error()
+    return tp
+
+
+class SimError(AssertionError):
+    pass
+
+
+def _decode(idx, dims, n):
+    """Mixed-radix decode of an index array over `n` PhaseDims -> (g, s, c0, c1, c2, h)."""
+    idx = np.asarray(idx, dtype=np.int64).copy()
+    g = np.zeros_like(idx)
+    s = np.zeros_like(idx)
+    c = [np.zeros_like(idx) for _ in range(3)]
+    h = np.zeros_like(idx)
+    for i in range(n):
+        d = dims[i]
+        ext = d.div.d
+        dig = idx % ext
+        idx //= ext
+        g += dig * d.gstride
+        s += dig * d.sstride
+        h += dig * d.hmul
+        if d.slot >= 0:
+            c[d.slot] = dig * d.cmul
+    return g, s, c, h
+
+
+def check_layout(tp: TileParams, E: int) -> None:
+    """Shared-memory regions (two outer tables, pipeline buffers) are disjoint
+    and inside the dynamic allocation."""
+    ENTRY = 24
+    t0 = (tp.ph[0].off_tab, tp.ph[0].off_tab + ENTRY * tp.ph[0].n_outer)
+    t1 = (tp.ph[1].off_tab, tp.ph[1].off_tab + ENTRY * tp.ph[1].n_outer)
+    buf = ((tp.tile_elems_alloc * E + 15) // 16) * 16
+    b = (tp.off_buf, tp.off_buf + buf * tp.nbuf)
+    regs = sorted([t0, t1, b])
+    for (a0, a1), (b0, b1) in zip(regs, regs[1:]):
+        if a1 > b0 and a1 > a0 and b1 > b0:
+            raise SimError(f"smem regions overlap: {regs}")
+    if b[1] > tp.smem_bytes or tp.off_buf % 16:
+        raise SimError(f"buffers exceed smem_bytes or misaligned: {b} vs {tp.smem_bytes}")
+    if tp.smem_bytes > 227 * 1024:
+        raise SimError("more dynamic smem than a CTA can have")
+
+
+def simulate(program, src_words: np.ndarray, threads: int | None = None) -> np.ndarray:
+    """Replay the tile kernel on host words; returns the destination words."""
+    tp = tile_params(program)
+    check_layout(tp, program.layout.elem_width)
+    E = program.layout.elem_width
+    NT = threads or program.metadata["threads"]
+    n = tp.n_elems
+    assert src_words.size == n
+    dst = np.full(n, np.iinfo(np.uint64).max if src_words.dtype == np.uint64 else 0, dtype=src_words.dtype)
+    written = np.zeros(n, dtype=np.int32)
+    alloc = tp.tile_elems_alloc
+    tid = np.arange(NT, dtype=np.int64)
+    parts = []
+    for ph in range(2):
+        d = tp.ph[ph]
+        grp = tid // d.nthr
+        tr = tid - grp * d.nthr
+        active = grp < d.ngroups
+        g, s, c, h = _decode(tr, d.thr, d.nthr_dims)
+        parts.append((d, grp, active, g, s, c, h))
+    for t in range(tp.num_tiles):
+        # tile decode (decode_tile)
+        sb = db = 0
+        va, vc = tp.e_a, tp.e_c
+        for i in range(tp.ngrid):
+            gd = tp.grid[i]
+            cdig = (t // gd.cum.d) % gd.ext.d
+            sb += cdig * gd.src_stride
+            db += cdig * gd.dst_stride
+            if i == tp.grid_a:
+                va = min(tp.e_a, tp.d_a - cdig * tp.e_a)
+            if i == tp.grid_c:
+                vc = min(tp.e_c, tp.d_c - cdig * tp.e_c)
+        full = va == tp.e_a and vc == tp.e_c
+        lim = (va, vc)
+        smem = np.zeros(alloc + 64, dtype=src_words.dtype)
+        smem_valid = np.zeros(alloc + 64, dtype=bool)
+        for ph in range(2):
+            d, grp, active, tg, ts, tc, th = parts[ph]
+            mask = d.mask_full if full else d.mask_ragged
+            V = d.vec
+            for o_start in range(d.ngroups):
+                sel = active & (grp == o_start)
+                if not sel.any():
+                    continue
+                for o in range(o_start, d.n_outer, d.ngroups):
+                    eg, es, ec, eh = _decode([o], d.out, d.nout_dims)
+                    for i in range(d.n_in):
+                        gp = tg[sel] + eg[0] + i * d.g_in
+                        sp = ts[sel] + es[0] + i * d.s_in
+                        c0 = tc[0][sel] + ec[0][0] + i * d.c_in[0]
+                        c1 = tc[1][sel] + ec[1][0] + i * d.c_in[1]
+                        c2 = tc[2][sel] + i * d.c_in[2]
+                        ok = np.ones(gp.shape, dtype=bool)
+                        if mask & 1:
+                            ok &= c0 < lim[0]
+                        if mask & 2:
+                            ok &= c1 < lim[1]
+                        if mask & 4:
+                            ok &= c2 < tp.lim_split[ph]
+                        gp, sp = gp[ok], sp[ok]
+                        if ph == 0:
+                            gabs = sb + gp
+                            if d.rshift:
+                                ga = gabs - (gabs % V)
+                                for j in range(V):
+                                    inb = ga + j < n
+                                    _chk(sp[inb] + j, alloc, "R shifted smem")
+                                    smem[sp[inb] + j] = src_words[ga[inb] + j]
+                                    smem_valid[sp[inb] + j] = True
+                            else:
+                                if V > 1 and ((gabs % V).any() or (sp % V).any()):
+                                    raise SimError("R vector access misaligned")
+                                for j in range(V):
+                                    _chk(gabs + j, n, "R global")
+                                    _chk(sp + j, alloc, "R smem")
+                                    smem[sp + j] = src_words[gabs + j]
+                                    smem_valid[sp + j] = True
+                        else:
+                            hh = (sb + th[sel][ok] + eh[0] + i * d.h_in) & tp.hmask if tp.hmask else 0
+                            spx = sp + hh
+                            gabs = db + gp
+                            if V > 1 and (spx % V).any():
+                                raise SimError("W vector smem access misaligned")
+                            for j in range(V):
+                                _chk(spx + j, alloc, "W smem")
+                                dd = gabs + j * d.vstride
+                                _chk(dd, n, "W global")
+                                if not smem_valid[spx + j].all():
+                                    raise SimError(f"W reads smem never written (tile {t})")
+                                dst[dd] = smem[spx + j]
+                                written[dd] += 1
+    if (written != 1).any():
+        bad = np.nonzero(written != 1)[0][:5]
+        raise SimError(f"destination elements written {written[bad]} times at {bad}")
+    return dst
+
+
+def _chk(idx, bound, what):
+    if idx.size and (idx.min() < 0 or idx.max() >= bound):
+        raise SimError(f"{what} out of bounds: [{idx.min()}, {idx.max()}] vs {bound}")

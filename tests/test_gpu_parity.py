@@ -140,3 +140,31 @@ def test_golden_cases_specialised_kernels(cuda):
         out = execute_device(prog, x).cpu().numpy().reshape(-1)
         assert prog.jit_state == 2, (c["name"], "specialised kernel not loaded")
         assert sha256(out) == c["sha256"], (c["name"], prog.text)
+
+
+@pytest.mark.parametrize("elem", [4, 8])
+@pytest.mark.parametrize("jit", [False, True])
+def test_shifted_run_reads_misaligned_dims(cuda, elem, jit):
+    """Odd dims make every source run start off 16-byte alignment; the tile
+    reads 16-byte aligned supersets and shifts in smem (planner: 'aligned
+    supersets').  Checked against the C oracle, including the buffer's last
+    run (bounds-clipped final chunk) and ragged tiles."""
+    import oracle
+    from paper_2506_03686_b200 import PermutationMap, TensorLayout, build_program
+
+    rng = np.random.default_rng(elem + 10 * jit)
+    shapes = [((7, 9, 13, 5, 11, 27), (5, 2, 0, 4, 1, 3)), ((17, 9, 13, 15, 11, 27), (5, 2, 0, 4, 1, 3)),
+              ((33, 45, 19), (2, 0, 1)), ((5, 7, 9, 11, 13), (4, 3, 2, 1, 0)), ((101, 67), (1, 0)),
+              ((3, 77, 5, 31), (1, 3, 0, 2))]
+    seen_shift = 0
+    for shape, axes in shapes:
+        dims, sigma = oracle.from_numpy_axes(shape, axes)
+        n = int(np.prod(shape))
+        data = rng.integers(0, 2**63, size=n, dtype=np.uint64)
+        data = data.view(np.uint32)[:n].copy() if elem == 4 else data
+        prog = build_program(TensorLayout(dims, elem), PermutationMap(sigma), force="tile", jit=jit)
+        seen_shift += "aligned supersets" in prog.text
+        out, _ = gpu_permute_bytes(dims, sigma, elem, data, force="tile", jit=jit)
+        want = oracle.naive_permute_c(data, dims, sigma)
+        assert np.array_equal(out, want.view(np.uint8)), (shape, axes, prog.text)
+    assert seen_shift >= 2
