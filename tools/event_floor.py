@@ -28,3 +28,15 @@ flushes = {"none": lambda: None, "fill": lambda: w.fill_(1.0), "fill+sum": lambd
 works = {"empty": lambda: None, "fill1": lambda: one.fill_(1), "fill1x2": lambda: (one.fill_(1), one.fill_(2))}
 for fn, f in flushes.items():
     print(fn, {wn: round(run(f, wk), 2) for wn, wk in works.items()}, flush=True)
+
+# CUDA-graph launch of the same tiny kernel: does the per-launch floor shrink?
+g = torch.cuda.CUDAGraph()
+s = torch.cuda.Stream()
+with torch.cuda.stream(s):
+    one.fill_(1)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g, stream=s):
+        one.fill_(1)
+torch.cuda.synchronize()
+for fn, f in [("fill", lambda: w.fill_(1.0)), ("none", lambda: None)]:
+    print("graph", fn, {wn: round(run(f, wk), 2) for wn, wk in {"replay": lambda: g.replay()}.items()}, flush=True)
