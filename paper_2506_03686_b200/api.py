@@ -19,6 +19,7 @@ memory (that is the end-to-end path the bench times).
 from __future__ import annotations
 
 import ctypes
+import functools
 import threading
 from dataclasses import dataclass, field
 
@@ -135,6 +136,11 @@ class GpuProgram:
     @property
     def out_layout(self) -> TensorLayout:
         return permuted_layout(self.layout, self.pmap)
+
+    @functools.cached_property
+    def out_shape(self) -> tuple:
+        """Output shape, NumPy/torch order (outer-first)."""
+        return self.out_layout.shape_outer_first()
 
     @property
     def nbytes(self) -> int:
@@ -289,30 +295,37 @@ def execute_device(program: GpuProgram, x, out=None, stream=None):
     torch = _torch()
     if not isinstance(x, torch.Tensor) or not x.is_cuda:
         raise LayoutError("execute_device needs a CUDA tensor")
-    if x.element_size() != program.layout.elem_width and not (
-            x.dtype == torch.uint8 and x.numel() == program.nbytes):
-        raise LayoutError(f"tensor itemsize {x.element_size()} != element width {program.layout.elem_width}")
-    if x.numel() * x.element_size() != program.nbytes:
+    es = x.element_size()
+    nbytes = program.nbytes
+    if es != program.layout.elem_width and not (x.dtype == torch.uint8 and x.numel() == nbytes):
+        raise LayoutError(f"tensor itemsize {es} != element width {program.layout.elem_width}")
+    if x.numel() * es != nbytes:
         raise LayoutError(f"tensor holds {x.numel()} elements, program expects {program.num_elements}")
     if not x.is_contiguous():
         raise LayoutError("input tensor must be contiguous (dense layout)")
-    shape = program.out_layout.shape_outer_first()
     if out is None:
-        if x.element_size() == program.layout.elem_width:
-            out = torch.empty(shape, dtype=x.dtype, device=x.device)
+        if es == program.layout.elem_width:
+            out = torch.empty(program.out_shape, dtype=x.dtype, device=x.device)
         else:
-            out = torch.empty(program.nbytes, dtype=torch.uint8, device=x.device)
+            out = torch.empty(nbytes, dtype=torch.uint8, device=x.device)
     else:
-        if not out.is_cuda or not out.is_contiguous() or out.numel() * out.element_size() != program.nbytes:
+        if not out.is_cuda or not out.is_contiguous() or out.numel() * out.element_size() != nbytes:
             raise LayoutError("out must be a contiguous CUDA tensor of the output size")
         if out.device != x.device:
             raise LayoutError("out must be on the input's device")
     if program.num_elements == 0:
         return out
-    if out.data_ptr() == x.data_ptr():
-        raise LayoutError("out-of-place only: out aliases the input")
-    with torch.cuda.device(x.device):
-        _launch(program, x.data_ptr(), out.data_ptr(), _stream_ptr(torch, x.device, stream))
+    xp, op = x.data_ptr(), out.data_ptr()
+    if xp < op + nbytes and op < xp + nbytes:
+        raise LayoutError("out-of-place only: out overlaps the input")
+    dev = x.get_device()
+    if stream is None:
+        stream = torch.cuda.current_stream(dev)
+    if dev != torch.cuda.current_device():
+        with torch.cuda.device(dev):
+            _launch(program, xp, op, ctypes.c_void_p(stream.cuda_stream))
+    else:
+        _launch(program, xp, op, ctypes.c_void_p(stream.cuda_stream))
     return out
 
 
