@@ -168,3 +168,41 @@ def test_shifted_run_reads_misaligned_dims(cuda, elem, jit):
         want = oracle.naive_permute_c(data, dims, sigma)
         assert np.array_equal(out, want.view(np.uint8)), (shape, axes, prog.text)
     assert seen_shift >= 2
+
+
+@pytest.mark.parametrize("jit,count", [(False, 120), (True, 20)])
+def test_large_random_campaign(cuda, jit, count):
+    """Beyond the reference's <= 2^16-element campaign: 2^16..2^21-element
+    random shapes (odd, pow2 and all-2 families, 4/8-byte words), checked
+    against torch's own device permute and the inverse round trip."""
+    import torch
+
+    from paper_2506_03686_b200 import TensorLayout, build_program, from_numpy_convention, permuted_layout
+    from paper_2506_03686_b200.api import execute_device
+
+    rng = np.random.default_rng(31 + jit)
+    for i in range(count):
+        fam = i % 3
+        while True:
+            rank = int(rng.integers(2, 9))
+            if fam == 0:
+                shape = tuple(int(rng.integers(2, 40)) for _ in range(rank))
+            elif fam == 1:
+                shape = tuple(int(2 ** rng.integers(1, 7)) for _ in range(rank))
+            else:
+                shape = (2,) * int(rng.integers(16, 22))
+            n = int(np.prod(shape))
+            if (1 << 16) <= n <= (1 << 21):
+                break
+        axes = tuple(int(a) for a in rng.permutation(len(shape)))
+        elem = int(rng.choice([4, 8]))
+        word = torch.int32 if elem == 4 else torch.int64
+        x = torch.randint(-2**31, 2**31 - 1, shape, dtype=word, device=cuda)
+        prog = build_program(TensorLayout.from_shape(shape, elem), from_numpy_convention(axes), jit=jit)
+        y = execute_device(prog, x)
+        if len(shape) <= 25:
+            assert torch.equal(y, x.permute(axes).contiguous()), (shape, axes, prog.text)
+        inv = build_program(permuted_layout(prog.layout, prog.pmap), prog.pmap.inverse(), jit=jit)
+        assert torch.equal(execute_device(inv, y).reshape(-1), x.reshape(-1)), (shape, axes)
+        if jit and prog.kernel == "tile":
+            assert prog.jit_state == 2
