@@ -161,6 +161,15 @@ def time_device(torch, launch, steps, warmup, flush, stream):
     return [a.elapsed_time(b) for a, b in evs]
 
 
+def event_floor_us(torch, flush, stream, reps=20):
+    """Median event time of a trivial 1-element kernel after the same flush:
+    the fixed event/launch overhead inside every flushed single-launch number
+    (matters for the small configs, whose ideal times are 8-20 us)."""
+    one = torch.zeros(1, dtype=torch.int32, device=flush.w.device)
+    t = time_device(torch, lambda: one.fill_(1), reps, 3, flush, stream)
+    return sorted(t)[len(t) // 2] * 1e3
+
+
 def _traffic_from_profiles(cfg):
     """Per-launch DRAM bytes of the dominant kernel from the committed ncu summary."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -408,6 +417,7 @@ def main(argv=None):
     config["l2_bytes"] = args._flusher.l2
     with ClockSampler(0) as clk:
         main_res = bench_one_gpu(args, torch, args.config, True, peak)
+    floor = event_floor_us(torch, args._flusher, torch.cuda.current_stream())
     extra = {}
     if not args.no_extra:
         for k in sorted(CONFIGS):
@@ -448,6 +458,7 @@ def main(argv=None):
         "clocks": clk.summary(),
         "parity_sampled": main_res["parity_sampled"],
         "configs": extra,
+        "event_floor_us": round(floor, 2),
     })
     print(json.dumps(line), flush=True)
     return 0

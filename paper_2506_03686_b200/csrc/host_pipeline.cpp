@@ -131,14 +131,21 @@ PipePlan build_pipe(const vpg_plan *p) {
     auto model = [&](int64_t C, int64_t copies) {
         return bytes / 50e9 + bytes / C / 57e9 + copies * 8e-6;
     };
+    // Exhaustive search over subsets of the (at most 12 best) candidate dims.
+    if (cand.size() > 12) cand.resize(12);
     std::vector<int> K, bestK;
     int64_t C = 1, bestC = 1;
     double best_t = model(1, 2);
-    for (int k : cand) {
-        if (C * p->dims[k] > max_chunks) continue;
-        std::vector<int> K2 = K;
-        K2.push_back(k);
-        // check the copy counts of chunk 0 on both sides
+    const int nc = (int)cand.size();
+    for (uint32_t mask = 1; mask < (1u << nc); ++mask) {
+        std::vector<int> K2;
+        int64_t C2 = 1;
+        for (int b = 0; b < nc; ++b)
+            if (mask & (1u << b)) {
+                K2.push_back(cand[b]);
+                C2 *= p->dims[cand[b]];
+            }
+        if (C2 > max_chunks) continue;
         int64_t ci[kMaxRank], co[kMaxRank];
         for (int q = 0; q < r; ++q) ci[q] = co[q] = -1;
         for (int q : K2) {
@@ -150,13 +157,11 @@ PipePlan build_pipe(const vpg_plan *p) {
         if (tin.empty() || tin[0].width < kMinBlockBytes) continue;
         if (!region_copies(r, odims, co, E, tout, kMaxCopiesPerChunk)) continue;
         if (tout.empty() || tout[0].width < kMinBlockBytes) continue;
-        K = K2;
-        C *= p->dims[k];
-        double t = model(C, C * (int64_t)(tin.size() + tout.size()));
-        if (t < best_t) {
+        double t = model(C2, C2 * (int64_t)(tin.size() + tout.size()));
+        if (t < best_t - 1e-9) {
             best_t = t;
-            bestK = K;
-            bestC = C;
+            bestK = K2;
+            bestC = C2;
         }
     }
     K = bestK;
