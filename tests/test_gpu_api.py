@@ -16,8 +16,16 @@ SHAPES = [
     ((7, 9, 13, 5, 11), (4, 1, 0, 3, 2)),     # misaligned dims
     ((6, 5, 7, 3), (1, 0, 2, 3)),             # merged preserved row
     ((16, 8, 64), (1, 0, 2)),                 # stride-1 preserved
+    ((8, 4, 256), (1, 0, 2)),                 # stride-1 preserved, 1 KiB rows (rows kernel)
+    ((6, 4, 2000), (0, 1, 2)),                # identity (copy kernel)
     ((2,) * 12, tuple(np.random.default_rng(3).permutation(12).tolist())),
 ]
+
+
+def prog_kind(shape, axes):
+    from paper_2506_03686_b200 import TensorLayout, build_program, from_numpy_convention
+
+    return build_program(TensorLayout.from_shape(shape, 4), from_numpy_convention(axes)).kernel
 
 
 def _want(x_np, axes):
@@ -56,7 +64,8 @@ def test_misaligned_base_pointers(cuda, shape, axes, offset):
     x = xd[offset:offset + n]
     out_full = torch.zeros(n + 8, dtype=torch.int32, device=cuda)
     out = out_full[offset:offset + n]
-    prog = build_program(TensorLayout.from_shape(shape, 4), from_numpy_convention(axes), force="tile")
+    prog = build_program(TensorLayout.from_shape(shape, 4), from_numpy_convention(axes),
+                         force=None if prog_kind(shape, axes) in ("rows", "copy") else "tile")
     execute_device(prog, x, out=out)
     want = _want(base[offset:offset + n].reshape(shape), axes).reshape(-1)
     assert np.array_equal(out.cpu().numpy(), want)
