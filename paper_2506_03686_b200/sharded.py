@@ -235,8 +235,16 @@ def permute_sharded(local_in, global_shape, axes, group=None, local_permute=None
     es = packed.element_size()
     send = [c * es for c in sp.send_counts(r)]
     recv_c = [c * es for c in sp.recv_counts(r)]
-    recv = torch.empty(sum(recv_c), dtype=torch.uint8, device=packed.device)
-    dist.all_to_all_single(recv, packed.view(torch.uint8), recv_c, send, group=group)
+    # NCCL moves device buffers directly over NVLink/NVSwitch; the gloo
+    # backend (CPU transport) needs host buffers, so device data is staged.
+    staged = packed.is_cuda and dist.get_backend(group) == "gloo"
+    payload = packed.view(torch.uint8)
+    if staged:
+        payload = payload.cpu()
+    recv = torch.empty(sum(recv_c), dtype=torch.uint8, device=payload.device)
+    dist.all_to_all_single(recv, payload, recv_c, send, group=group)
+    if staged:
+        recv = recv.to(packed.device)
     s2, a2 = sp.p2()
     got = recv.view(packed.dtype).reshape(s2)
     return local_permute(got, a2).reshape(sp.local_out_shape())
