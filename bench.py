@@ -349,6 +349,135 @@ def bench_one_gpu(args, torch, cfg, with_e2e, peak):
     return res
 
 
+# ---------------------------------------------------------------- sharded (N > 1)
+NVLINK_GBS = 770.0   # measured peer copy per direction per GPU (B200_PROFILING.md)
+
+
+def bench_sharded(args, torch, base, config, peak, peak_kind):
+    """cfg5 sharded over the torchrun ranks (strong scaling): P1 permute ->
+    NCCL all_to_all_single -> P2 permute per step; device time max over ranks."""
+    import numpy as np
+    import torch.distributed as dist
+
+    from paper_2506_03686_b200 import permute
+    from paper_2506_03686_b200.sharded import permute_sharded, plan_sharded, shard_bounds
+    from paper_2506_03686_b200.workloads import CONFIGS, make_input_slice
+
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist.init_process_group("nccl", device_id=dev)
+    G, r = dist.get_world_size(), dist.get_rank()
+    wl = CONFIGS[args.config]
+    sp = plan_sharded(wl.shape, wl.axes, G)
+    lo, hi = shard_bounds(wl.numel, G, r)
+    host_in = torch.from_numpy(make_input_slice(wl, lo, hi).reshape(-1).view(np.uint8)).pin_memory()
+    x = host_in.to(dev).view(torch.int64)
+    st = torch.cuda.current_stream()
+    step = lambda: permute_sharded(x, wl.shape, wl.axes, local_permute=permute, plan=sp)  # noqa: E731
+    out = None
+    for _ in range(args.warmup):
+        out = step()          # same allocation pattern as the timed loop (two live outputs)
+    torch.cuda.synchronize()
+    dist.barrier()
+    evs = []
+    with ClockSampler(local_rank) as clk:
+        for _ in range(args.steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            out = step()
+            b.record(st)
+            evs.append((a, b))
+        torch.cuda.synchronize()
+    dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    if os.environ.get("VPG_BENCH_DEBUG"):
+        print(f"rank {r} step ms: {[round(v, 3) for v in step_ms]}", file=sys.stderr, flush=True)
+    tot = torch.tensor([sum(step_ms)], device=dev, dtype=torch.float64)
+    dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    ms = tot.item() / args.steps
+    gbs = wl.algorithmic_bytes / (ms * 1e-3) / 1e9
+    # parity on every rank: 2^18 sampled output positions of this rank's shard
+    want_ok = _sample_shard_parity(torch, host_in, out, wl, sp, r, G)
+    ok = torch.tensor([1 if want_ok else 0], device=dev)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    # end to end: pinned host shard -> device -> sharded permute -> host shard
+    host_out = torch.empty(out.numel() * out.element_size(), dtype=torch.uint8).pin_memory()
+    dist.barrier()
+    e2e = []
+    for s_ in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        xin = host_in.to(dev, non_blocking=True).view(torch.int64)
+        y = permute_sharded(xin, wl.shape, wl.axes, local_permute=permute, plan=sp)
+        host_out.copy_(y.reshape(-1).view(torch.uint8), non_blocking=True)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        if s_ >= args.warmup:
+            e2e.append(t1 - t0)
+    e2e_t = torch.tensor([sum(e2e) / len(e2e)], device=dev, dtype=torch.float64)
+    dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    shard_bytes = wl.numel * wl.elem_bytes // G
+    t_hbm = 2 * shard_bytes / (peak * 1e9)
+    t_nvl = shard_bytes * (G - 1) / G / (NVLINK_GBS * 1e9)
+    bound = "nvlink" if t_nvl > t_hbm else "hbm"
+    roof_gbs = wl.algorithmic_bytes / max(t_hbm, t_nvl) / 1e9
+    if r == 0:
+        line = dict(base)
+        line.update({
+            "value": round(gbs, 2), "ms_per_step": ms, "config": config,
+            "e2e": {"value": round(wl.algorithmic_bytes / e2e_t.item() / 1e9, 3), "unit": "GB/s",
+                    "h2d_bytes_per_step": shard_bytes * G, "d2h_bytes_per_step": shard_bytes * G,
+                    "api": "paper_2506_03686_b200.sharded.permute_sharded on pinned host shards"},
+            "gpu_launches": (2 if G > 1 else 1) * args.steps,
+            "roofline": {"bound": bound, "achieved": round(gbs, 2), "peak": round(roof_gbs, 1),
+                         "peak_kind": f"min over HBM ({peak_kind} {peak} GB/s per GPU) and NVLink "
+                                      f"({NVLINK_GBS} GB/s per direction per GPU) time bounds",
+                         "unit": "GB/s", "frac": round(gbs / roof_gbs, 4), "traffic": None,
+                         "kernel": "tile (P1/P2) + NCCL all_to_all_single"},
+            "parity_sampled": bool(ok.item()),
+            "clocks": clk.summary(),
+            "shard_plan": sp.describe()[:400],
+        })
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+    return 0
+
+
+def _sample_shard_parity(torch, host_in, out, wl, sp, r, G, nsamp=1 << 18):
+    """Rank-local check: sampled positions of this rank's output shard equal the
+    closed-form bijection applied to the global input, using only the inputs
+    this rank can regenerate (make_input_slice) -- no collective needed."""
+    import numpy as np
+
+    from paper_2506_03686_b200.sharded import shard_bounds
+    from paper_2506_03686_b200.workloads import make_input_slice
+
+    n = wl.numel
+    lo, hi = shard_bounds(n, G, r)
+    rng = np.random.default_rng(r)
+    pos = rng.integers(lo, hi, size=nsamp)
+    in_strides = [1] * len(wl.shape)
+    for k in range(len(wl.shape) - 2, -1, -1):
+        in_strides[k] = in_strides[k + 1] * wl.shape[k + 1]
+    rem = pos.copy()
+    src = np.zeros_like(pos)
+    for a in reversed(wl.axes):
+        d = wl.shape[a]
+        src += (rem % d) * in_strides[a]
+        rem //= d
+    got = out.reshape(-1).cpu().numpy().view(np.uint64)[pos - lo]
+    vals = np.empty(nsamp, dtype=np.uint64)
+    # regenerate the needed global input words block by block
+    blocks = np.unique(src // (1 << 22))
+    for b in blocks:
+        sel = (src // (1 << 22)) == b
+        blk = make_input_slice(wl, int(b) << 22, min(n, (int(b) + 1) << 22)).view(np.uint64)
+        vals[sel] = blk[src[sel] - (int(b) << 22)]
+    return bool(np.array_equal(got, vals))
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -359,6 +488,8 @@ def main(argv=None):
     ap.add_argument("--no-extra", action="store_true", help="skip cfg1-4 side measurements")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-threads", type=int, default=None)
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the sharded (torchrun/NCCL) code path even with one rank")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3   # contract: W >= 3
@@ -415,10 +546,8 @@ def main(argv=None):
 
     import torch
 
-    if world > 1:
-        from paper_2506_03686_b200 import sharded
-
-        return sharded.bench_main(args, torch, base, config, peak, peak_kind)
+    if world > 1 or args.sharded:
+        return bench_sharded(args, torch, base, config, peak, peak_kind)
 
     torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)

@@ -279,58 +279,3 @@ def emulate_sharded(x_flat, global_shape, axes, G, local_permute=None):
         got = torch.cat(parts).reshape(s2)
         outs.append(local_permute(got, a2).reshape(sp.local_out_shape()))
     return outs
-
-
-# ------------------------------------------------------------------ bench
-def bench_main(args, torch, base, config, peak, peak_kind):
-    """bench.py at N>1: cfg5 sharded over the torchrun ranks (strong scaling)."""
-    import json
-    import os
-
-    import torch.distributed as dist
-
-    from .api import permute
-    from .workloads import CONFIGS, make_input_slice
-
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local_rank)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    G, r = dist.get_world_size(), dist.get_rank()
-    wl = CONFIGS[args.config]
-    sp = plan_sharded(wl.shape, wl.axes, G)
-    import numpy as np
-
-    lo, hi = shard_bounds(wl.numel, G, r)
-    full = make_input_slice(wl, lo, hi)          # this rank's slice of the seeded global input
-    dev = torch.device("cuda", local_rank)
-    x = torch.from_numpy(full.reshape(-1).view(np.uint8)).to(dev).view(torch.int64)
-    st = torch.cuda.current_stream()
-    step = lambda: permute_sharded(x, wl.shape, wl.axes, local_permute=permute, plan=sp)  # noqa: E731
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    dist.barrier()
-    evs = []
-    for _ in range(args.steps):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(st)
-        step()
-        b.record(st)
-        evs.append((a, b))
-    torch.cuda.synchronize()
-    dist.barrier()
-    tot = torch.tensor([sum(a.elapsed_time(b) for a, b in evs)], device=dev, dtype=torch.float64)
-    dist.all_reduce(tot, op=dist.ReduceOp.MAX)
-    ms = tot.item() / args.steps
-    gbs = wl.algorithmic_bytes / (ms * 1e-3) / 1e9
-    if r == 0:
-        line = dict(base)
-        line.update({"value": round(gbs, 2), "ms_per_step": ms, "config": config,
-                     "gpu_launches": 2 * args.steps,
-                     "roofline": {"bound": "nvlink+hbm", "achieved": round(gbs, 2), "peak": peak,
-                                  "peak_kind": peak_kind, "unit": "GB/s", "frac": round(gbs / peak / G, 4),
-                                  "traffic": None, "kernel": "tile (P1/P2) + NCCL all_to_all"},
-                     "shard_plan": sp.describe()})
-        print(json.dumps(line), flush=True)
-    dist.destroy_process_group()
-    return 0
