@@ -115,6 +115,19 @@ vpg_status vpg_permute(const vpg_plan *plan, const void *src, void *dst, void *c
 vpg_status vpg_permute_host(const vpg_plan *plan, const void *host_src, void *host_dst,
                             void *dev_src, void *dev_dst, void *cuda_stream);
 
+/* Asynchronous variant of vpg_permute_host: enqueues the chunked
+ * H2D -> permute -> D2H pipeline on the library's copy/compute streams and
+ * returns; completion is ordered on `cuda_stream` (synchronise it before
+ * reading host_dst).  Consecutive calls overlap: the H2D of call k+1 runs
+ * while the D2H of call k drains.  Reusing the same device scratch between
+ * calls is safe (the library orders writers after earlier readers), and so
+ * is feeding an earlier call's host_dst back as host_src (the H2D waits for
+ * that D2H).  The call does not wait for other earlier work on cuda_stream:
+ * host buffers must be ready and stay alive and unmodified until
+ * completion, and the scratch must not be used by other in-flight work. */
+vpg_status vpg_permute_host_async(const vpg_plan *plan, const void *host_src, void *host_dst,
+                                  void *dev_src, void *dev_dst, void *cuda_stream);
+
 /* One-shot convenience with an internal plan cache keyed by
  * (dims, sigma, elem_bytes): the closest analog of the reference's
  * shape-specialised kernel call. */

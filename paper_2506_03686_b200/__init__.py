@@ -30,6 +30,7 @@ from .api import (
     merge_dimensions,
     permute,
     program_cache_clear,
+    release_scratch,
 )
 
 __version__ = "0.1.0"
@@ -55,4 +56,5 @@ __all__ = [
     "merge_dimensions",
     "permute",
     "program_cache_clear",
+    "release_scratch",
 ]

@@ -30,6 +30,7 @@ EXPORTED = (
     "vpg_plan_create",
     "vpg_permute",
     "vpg_permute_host",
+    "vpg_permute_host_async",
     "vpg_permute_nd",
     "vpg_plan_info_get",
     "vpg_plan_describe",
@@ -95,6 +96,7 @@ def lib():
                                       ctypes.POINTER(vp)]
         L.vpg_permute.argtypes = [vp, vp, vp, vp]
         L.vpg_permute_host.argtypes = [vp, vp, vp, vp, vp, vp]
+        L.vpg_permute_host_async.argtypes = [vp, vp, vp, vp, vp, vp]
         L.vpg_permute_nd.argtypes = [ctypes.c_int, i64p, i32p, ctypes.c_int, vp, vp, vp]
         L.vpg_plan_info_get.argtypes = [vp, ctypes.POINTER(PlanInfo)]
         L.vpg_plan_describe.argtypes = [vp, ctypes.c_char_p, ctypes.c_size_t]
@@ -104,6 +106,7 @@ def lib():
         L.vpg_plan_destroy.argtypes = [vp]
         L.vpg_plan_destroy.restype = None
         for name in ("vpg_merge_dimensions", "vpg_plan_create", "vpg_permute", "vpg_permute_host",
+                     "vpg_permute_host_async",
                      "vpg_permute_nd", "vpg_plan_info_get", "vpg_plan_describe", "vpg_plan_emit_source",
                      "vpg_plan_jit_compile", "vpg_plan_tile_params"):
             getattr(L, name).restype = ctypes.c_int

@@ -46,6 +46,7 @@ __all__ = [
     "emit_source",
     "jit_compile",
     "program_cache_clear",
+    "release_scratch",
 ]
 
 
@@ -329,23 +330,50 @@ def execute_device(program: GpuProgram, x, out=None, stream=None):
     return out
 
 
-def execute(program: GpuProgram, input_buf, trace: bool = False, out=None, stream=None):
+def execute(program: GpuProgram, input_buf, trace: bool = False, out=None, stream=None, blocking: bool = True):
     """Run a program; returns ``(output, counters)`` like vm.py:105-110.
 
     * CUDA tensor input -> CUDA output tensor (outer-first output shape).
     * numpy array / bytes / CPU tensor input -> staged through device memory
-      (H2D copy, kernel, D2H copy); returns a flat numpy array of opaque
-      words (``program.layout.dtype``) like the reference, or a CPU tensor
-      for a CPU-tensor input.
+      (chunked H2D / kernel / D2H pipeline); returns a flat numpy array of
+      opaque words (``program.layout.dtype``) like the reference, or a CPU
+      tensor for a CPU-tensor input.
+    * ``blocking=False`` (pinned CPU tensors with ``out`` given): enqueue and
+      return at once; consecutive calls overlap their transfers.  Call
+      ``stream.synchronize()`` (default: the current stream) before reading
+      ``out``.
     """
     torch = _torch()
     if isinstance(input_buf, torch.Tensor) and input_buf.is_cuda:
         res = execute_device(program, input_buf, out=out, stream=stream)
         return res, _counters(program)
-    return _execute_host(program, input_buf, out=out, stream=stream), _counters(program)
+    return _execute_host(program, input_buf, out=out, stream=stream, blocking=blocking), _counters(program)
 
 
-def _execute_host(program: GpuProgram, input_buf, out=None, stream=None):
+_scratch: dict = {}
+_scratch_lock = threading.Lock()
+
+
+def _host_scratch(torch, program, dev):
+    """Device staging buffers of the host path, kept per (program, device);
+    the library orders reuse across in-flight calls."""
+    key = (id(program), dev.index)
+    with _scratch_lock:
+        hit = _scratch.get(key)
+        if hit is None or hit[0] is not program:
+            hit = (program, torch.empty(program.nbytes, dtype=torch.uint8, device=dev),
+                   torch.empty(program.nbytes, dtype=torch.uint8, device=dev))
+            _scratch[key] = hit
+        return hit[1], hit[2]
+
+
+def release_scratch():
+    """Free the device staging buffers of the host path."""
+    with _scratch_lock:
+        _scratch.clear()
+
+
+def _execute_host(program: GpuProgram, input_buf, out=None, stream=None, blocking=True):
     torch = _torch()
     if not torch.cuda.is_available():
         raise VpgError("no CUDA device: the permutation runs only on the GPU (no CPU fallback)")
@@ -366,15 +394,17 @@ def _execute_host(program: GpuProgram, input_buf, out=None, stream=None):
                               f"program expects {program.num_elements}")
         hbytes = torch.from_numpy(data.copy() if not data.flags.writeable else data)
     dev = torch.device("cuda", torch.cuda.current_device())
-    d_in = torch.empty(program.nbytes, dtype=torch.uint8, device=dev)
-    d_out = torch.empty(program.nbytes, dtype=torch.uint8, device=dev)
+    d_in, d_out = _host_scratch(torch, program, dev)
+    if not blocking and (out is None or not as_tensor or not hbytes.is_pinned() or not out.is_pinned()):
+        raise LayoutError("blocking=False needs a pinned CPU tensor input and a pinned `out`")
     if out is None:
         h_out = torch.empty(program.nbytes, dtype=torch.uint8, pin_memory=hbytes.is_pinned())
     else:
         h_out = out.reshape(-1).view(torch.uint8)
     if program.num_elements:
         st = torch.cuda.current_stream(dev) if stream is None else stream
-        status = _lib.lib().vpg_permute_host(
+        fn = _lib.lib().vpg_permute_host if blocking else _lib.lib().vpg_permute_host_async
+        status = fn(
             program.handle, ctypes.c_void_p(hbytes.data_ptr()), ctypes.c_void_p(h_out.data_ptr()),
             ctypes.c_void_p(d_in.data_ptr()), ctypes.c_void_p(d_out.data_ptr()),
             ctypes.c_void_p(st.cuda_stream))

@@ -12,7 +12,7 @@
 
 namespace vpg {
 vpg_status permute_host_pipelined(const vpg_plan *p, const void *host_src, void *host_dst, void *dev_src,
-                                  void *dev_dst, cudaStream_t user, std::string *err);
+                                  void *dev_dst, cudaStream_t user, bool async, std::string *err);
 int host_pipeline_chunks(const vpg_plan *p);
 void host_pipeline_forget(const vpg_plan *p);
 int merge_dims(int rank, const int64_t *dims, const int32_t *sigma, int64_t *od, int32_t *os);
@@ -80,7 +80,7 @@ vpg_status vpg_permute_host(const vpg_plan *plan, const void *host_src, void *ho
     size_t nbytes = (size_t)plan->n * plan->elem_bytes;
     {
         std::string err;
-        vpg_status ps = vpg::permute_host_pipelined(plan, host_src, host_dst, dev_src, dev_dst, st, &err);
+        vpg_status ps = vpg::permute_host_pipelined(plan, host_src, host_dst, dev_src, dev_dst, st, false, &err);
         if (ps == VPG_OK) return VPG_OK;
         if (ps != VPG_EUNSUPPORTED) return fail(ps, err);
     }
@@ -92,6 +92,17 @@ vpg_status vpg_permute_host(const vpg_plan *plan, const void *host_src, void *ho
     if (e != cudaSuccess) return fail(VPG_ECUDA, std::string("D2H copy: ") + cudaGetErrorString(e));
     e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return fail(VPG_ECUDA, std::string("stream sync: ") + cudaGetErrorString(e));
+    return VPG_OK;
+}
+
+vpg_status vpg_permute_host_async(const vpg_plan *plan, const void *host_src, void *host_dst, void *dev_src,
+                                  void *dev_dst, void *cuda_stream) {
+    if (!plan || !host_src || !host_dst || !dev_src || !dev_dst) return fail(VPG_EINVAL, "null argument");
+    if (plan->n == 0) return VPG_OK;
+    std::string err;
+    vpg_status ps = vpg::permute_host_pipelined(plan, host_src, host_dst, dev_src, dev_dst,
+                                                (cudaStream_t)cuda_stream, true, &err);
+    if (ps != VPG_OK) return fail(ps, err);
     return VPG_OK;
 }
 

@@ -206,11 +206,62 @@ DevStreams streams_for_current(std::string *err) {
 
 namespace vpg {
 
-// Pipelined host->device->host permutation; returns VPG_EUNSUPPORTED when
-// the tensor is too small or has no chunkable dims (caller falls back to
-// the single-shot sequence).
+// Scratch hazards across calls: a later call may reuse the same device
+// scratch while an earlier call's chunk kernels / D2H copies are still in
+// flight on the internal streams.  Per scratch pointer we remember the event
+// after its last reader; the next writer waits on it.
+std::map<const void *, cudaEvent_t> g_src_free;   // dev_src: last kernel reading it done
+std::map<const void *, cudaEvent_t> g_dst_free;   // dev_dst: last D2H reading it done
+
+// Host-output ranges of in-flight async calls: a later call whose host
+// input overlaps one of them (chaining outputs into inputs) waits for that
+// D2H.  Bounded ring; entries are events recorded after the call's D2H.
+struct PendingOut {
+    uintptr_t lo, hi;
+    cudaEvent_t done;
+};
+std::vector<PendingOut> g_pending_out;
+
+void wait_host_input(const void *host_src, size_t nbytes, cudaStream_t waiter) {
+    const uintptr_t lo = (uintptr_t)host_src, hi = lo + nbytes;
+    std::lock_guard<std::mutex> lk(g_pipe_mu);
+    for (const PendingOut &po : g_pending_out)
+        if (lo < po.hi && po.lo < hi) cudaStreamWaitEvent(waiter, po.done, 0);
+}
+
+void remember_host_output(const void *host_dst, size_t nbytes, cudaStream_t d2h) {
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    cudaEventRecord(e, d2h);
+    std::lock_guard<std::mutex> lk(g_pipe_mu);
+    if (g_pending_out.size() >= 16) {
+        cudaEventDestroy(g_pending_out.front().done);
+        g_pending_out.erase(g_pending_out.begin());
+    }
+    g_pending_out.push_back({(uintptr_t)host_dst, (uintptr_t)host_dst + nbytes, e});
+}
+
+void wait_and_replace(std::map<const void *, cudaEvent_t> &m, const void *ptr, cudaStream_t waiter,
+                      cudaEvent_t *slot_out) {
+    std::lock_guard<std::mutex> lk(g_pipe_mu);
+    auto it = m.find(ptr);
+    if (it != m.end()) {
+        cudaStreamWaitEvent(waiter, it->second, 0);
+        *slot_out = it->second;
+    } else {
+        cudaEvent_t e;
+        cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        m[ptr] = e;
+        *slot_out = e;
+    }
+}
+
+// Pipelined host->device->host permutation.  `async`: return after
+// enqueueing (completion ordered on `user`), else synchronise `user`.
+// Returns VPG_EUNSUPPORTED when a synchronous call would not benefit (small
+// tensor, no chunkable dims): the caller then runs the plain sequence.
 vpg_status permute_host_pipelined(const vpg_plan *p, const void *host_src, void *host_dst, void *dev_src,
-                                  void *dev_dst, cudaStream_t user, std::string *err) {
+                                  void *dev_dst, cudaStream_t user, bool async, std::string *err) {
     PipePlan pp;
     bool found = false;
     {
@@ -232,42 +283,59 @@ vpg_status permute_host_pipelined(const vpg_plan *p, const void *host_src, void 
         }
         if (dup && built.sub) vpg_plan_destroy(built.sub);   // lost the race; outside the lock
     }
-    if (!pp.ok) return VPG_EUNSUPPORTED;
+    if (!pp.ok && !async) return VPG_EUNSUPPORTED;
     DevStreams s = streams_for_current(err);
     if (!s.h2d) return VPG_ECUDA;
     const int r = p->rank, E = p->elem_bytes;
+    // single-chunk form (async calls of unchunkable tensors still overlap
+    // with neighbouring calls through the three streams)
+    const int64_t chunks = pp.ok ? pp.chunks : 1;
+    const vpg_plan *kp = pp.ok ? pp.sub : p;
+    const int64_t cbytes = (pp.ok ? pp.chunk_elems : p->n) * E;
     int64_t odims[kMaxRank];
     int pos[kMaxRank];
     for (int j = 0; j < r; ++j) {
         odims[j] = p->dims[p->sigma[j]];
         pos[p->sigma[j]] = j;
     }
-    cudaEvent_t start, done_in[kMaxChunks], done_k[kMaxChunks], fin;
+    cudaEvent_t start, fin, src_free, dst_free;
+    std::vector<cudaEvent_t> done_in(chunks), done_k(chunks);
     cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&fin, cudaEventDisableTiming);
-    for (int j = 0; j < pp.chunks; ++j) {
+    for (int64_t j = 0; j < chunks; ++j) {
         cudaEventCreateWithFlags(&done_in[j], cudaEventDisableTiming);
         cudaEventCreateWithFlags(&done_k[j], cudaEventDisableTiming);
     }
-    cudaEventRecord(start, user);
-    cudaStreamWaitEvent(s.h2d, start, 0);
-    cudaStreamWaitEvent(s.comp, start, 0);
-    cudaStreamWaitEvent(s.d2h, start, 0);
-    const int64_t cbytes = pp.chunk_elems * E;
+    if (async) {
+        // no dependency on the user stream's earlier work (that would chain
+        // call k+1's H2D behind call k's D2H); only real hazards are ordered
+        wait_host_input(host_src, (size_t)p->n * E, s.h2d);
+    } else {
+        cudaEventRecord(start, user);
+        cudaStreamWaitEvent(s.h2d, start, 0);
+        cudaStreamWaitEvent(s.comp, start, 0);
+        cudaStreamWaitEvent(s.d2h, start, 0);
+    }
+    wait_and_replace(g_src_free, dev_src, s.h2d, &src_free);   // earlier kernels done reading dev_src
+    wait_and_replace(g_dst_free, dev_dst, s.comp, &dst_free);  // earlier D2H done reading dev_dst
     std::vector<Copy2D> cps;
     vpg_status st = VPG_OK;
-    for (int64_t j = 0; j < pp.chunks && st == VPG_OK; ++j) {
-        int64_t ci[kMaxRank], co[kMaxRank];
-        for (int q = 0; q < r; ++q) ci[q] = co[q] = -1;
-        int64_t rem = j;
-        for (int q : pp.K) {
-            ci[q] = rem % p->dims[q];
-            co[pos[q]] = ci[q];
-            rem /= p->dims[q];
-        }
+    for (int64_t j = 0; j < chunks && st == VPG_OK; ++j) {
         char *din = (char *)dev_src + j * cbytes;
         char *dout = (char *)dev_dst + j * cbytes;
-        region_copies(r, p->dims, ci, E, cps, 1 << 30);
+        int64_t ci[kMaxRank], co[kMaxRank];
+        for (int q = 0; q < r; ++q) ci[q] = co[q] = -1;
+        if (pp.ok) {
+            int64_t rem = j;
+            for (int q : pp.K) {
+                ci[q] = rem % p->dims[q];
+                co[pos[q]] = ci[q];
+                rem /= p->dims[q];
+            }
+            region_copies(r, p->dims, ci, E, cps, 1 << 30);
+        } else {
+            cps.assign(1, Copy2D{0, 0, cbytes, 1, cbytes});
+        }
         for (const Copy2D &c : cps)
             if (cudaMemcpy2DAsync(din + c.dev_off, c.width, (const char *)host_src + c.host_off, c.pitch, c.width,
                                   c.height, cudaMemcpyHostToDevice, s.h2d) != cudaSuccess) {
@@ -276,11 +344,11 @@ vpg_status permute_host_pipelined(const vpg_plan *p, const void *host_src, void 
             }
         cudaEventRecord(done_in[j], s.h2d);
         cudaStreamWaitEvent(s.comp, done_in[j], 0);
-        vpg_status ks = launch_plan(pp.sub, din, dout, s.comp, err);
+        vpg_status ks = launch_plan(kp, din, dout, s.comp, err);
         if (ks != VPG_OK) st = ks;
         cudaEventRecord(done_k[j], s.comp);
         cudaStreamWaitEvent(s.d2h, done_k[j], 0);
-        region_copies(r, odims, co, E, cps, 1 << 30);
+        if (pp.ok) region_copies(r, odims, co, E, cps, 1 << 30);
         for (const Copy2D &c : cps)
             if (cudaMemcpy2DAsync((char *)host_dst + c.host_off, c.pitch, dout + c.dev_off, c.width, c.width,
                                   c.height, cudaMemcpyDeviceToHost, s.d2h) != cudaSuccess) {
@@ -288,16 +356,22 @@ vpg_status permute_host_pipelined(const vpg_plan *p, const void *host_src, void 
                 st = VPG_ECUDA;
             }
     }
+    cudaEventRecord(src_free, s.comp);   // all kernels of this call done reading dev_src
     cudaEventRecord(fin, s.d2h);
+    cudaEventRecord(dst_free, s.d2h);    // all D2H of this call done reading dev_dst
+    if (async) remember_host_output(host_dst, (size_t)p->n * E, s.d2h);
     cudaStreamWaitEvent(user, fin, 0);
-    cudaError_t e = cudaStreamSynchronize(user);
-    if (e != cudaSuccess && st == VPG_OK) {
-        *err = std::string("stream sync: ") + cudaGetErrorString(e);
-        st = VPG_ECUDA;
+    if (!async) {
+        cudaError_t e = cudaStreamSynchronize(user);
+        if (e != cudaSuccess && st == VPG_OK) {
+            *err = std::string("stream sync: ") + cudaGetErrorString(e);
+            st = VPG_ECUDA;
+        }
     }
+    // destroying recorded events is safe: resources are released once complete
     cudaEventDestroy(start);
     cudaEventDestroy(fin);
-    for (int j = 0; j < pp.chunks; ++j) {
+    for (int64_t j = 0; j < chunks; ++j) {
         cudaEventDestroy(done_in[j]);
         cudaEventDestroy(done_k[j]);
     }

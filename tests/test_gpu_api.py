@@ -202,3 +202,45 @@ def test_execute_host_pipelined_chunks(cuda):
         execute(prog, host, out=out)
         want = permute(host.to(cuda).reshape(shape), axes).reshape(-1).cpu()
         assert torch.equal(out, want), (shape, axes, prog.metadata["host_chunks"])
+
+
+def test_execute_host_nonblocking_stream(cuda):
+    """blocking=False calls overlap (shared staging buffers, library-ordered
+    reuse); every result must still be exact."""
+    import torch
+
+    from paper_2506_03686_b200 import TensorLayout, build_program, execute, from_numpy_convention, permute
+
+    for shape, axes in [((2,) * 23, tuple(np.random.default_rng(2).permutation(23).tolist())),
+                        ((37, 41, 29), (2, 0, 1))]:
+        prog = build_program(TensorLayout.from_shape(shape, 8), from_numpy_convention(axes))
+        n = prog.num_elements
+        ins = [torch.randint(-2**62, 2**62, (n,), dtype=torch.int64).pin_memory() for _ in range(4)]
+        outs = [torch.empty(n, dtype=torch.int64).pin_memory() for _ in range(4)]
+        for i in range(4):
+            execute(prog, ins[i], out=outs[i], blocking=False)
+        torch.cuda.current_stream().synchronize()
+        for i in range(4):
+            want = permute(ins[i].to(cuda).reshape(shape), axes).reshape(-1).cpu()
+            assert torch.equal(outs[i], want), (shape, i)
+    with pytest.raises(Exception):
+        execute(prog, ins[0], blocking=False)          # needs a pinned `out`
+
+
+def test_execute_host_nonblocking_chained(cuda):
+    """Feeding a non-blocking call's output back as the next input is ordered
+    by the library (H2D waits for the earlier D2H)."""
+    import torch
+
+    from paper_2506_03686_b200 import TensorLayout, build_program, execute, from_numpy_convention
+
+    shape, axes = (2,) * 22, tuple(range(21, -1, -1))          # involution: applying twice = identity
+    prog = build_program(TensorLayout.from_shape(shape, 4), from_numpy_convention(axes))
+    a = torch.randint(-2**31, 2**31 - 1, (prog.num_elements,), dtype=torch.int32).pin_memory()
+    b = torch.empty_like(a).pin_memory()
+    c = torch.empty_like(a).pin_memory()
+    execute(prog, a, out=b, blocking=False)
+    execute(prog, b, out=c, blocking=False)
+    torch.cuda.current_stream().synchronize()
+    assert torch.equal(c, a)
+    assert not torch.equal(b, a)
