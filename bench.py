@@ -314,6 +314,10 @@ def bench_one_gpu(args, torch, cfg, with_e2e, peak):
     # oracle checks -- torch.permute itself is limited to 25 dims)
     tdt = {"float32": torch.int32, "float64": torch.int64, "complex64": torch.int64}[wl.dtype]
     res["parity_sampled"] = sample_parity(torch, xd.view(tdt), yd.view(tdt), wl.shape, wl.axes)
+    # same-run copy bandwidth of this box (torch copy_ of the same bytes, same
+    # protocol): the achievable ceiling for any permutation of this size
+    tc = time_device(torch, lambda: yd.copy_(xd), args.steps, args.warmup, flush, stream)
+    res["copy_gbs"] = wl.algorithmic_bytes / (sum(tc) / len(tc) * 1e-3) / 1e9
     # the paper's comparator on the same GPU: torch's own permute+contiguous
     # copy (TensorIterator), same flush/event protocol
     if len(wl.shape) <= 25:
@@ -580,12 +584,16 @@ def main(argv=None):
             extra[k] = {"gbs": round(r["gbs"], 1), "frac_of_hbm": round(r["frac_of_hbm"], 4),
                         "us_per_launch": round(r["ms_per_launch"] * 1e3, 2), "kernel": r["kernel"],
                         "parity_sampled": r["parity_sampled"],
-                        "torch_permute_copy_gbs": None if r["torch_gbs"] is None else round(r["torch_gbs"], 1)}
+                        "torch_permute_copy_gbs": None if r["torch_gbs"] is None else round(r["torch_gbs"], 1),
+                        "same_run_copy_gbs": round(r["copy_gbs"], 1),
+                        "frac_of_same_run_copy": round(r["gbs"] / r["copy_gbs"], 4)}
     extra[args.config] = {"gbs": round(main_res["gbs"], 1), "frac_of_hbm": round(main_res["frac_of_hbm"], 4),
                           "us_per_launch": round(main_res["ms_per_launch"] * 1e3, 2),
                           "kernel": main_res["kernel"], "parity_sampled": main_res["parity_sampled"],
                           "torch_permute_copy_gbs": None if main_res["torch_gbs"] is None
-                          else round(main_res["torch_gbs"], 1)}
+                          else round(main_res["torch_gbs"], 1),
+                          "same_run_copy_gbs": round(main_res["copy_gbs"], 1),
+                          "frac_of_same_run_copy": round(main_res["gbs"] / main_res["copy_gbs"], 4)}
     cpu = None
     if not args.no_cpu:
         try:

@@ -89,6 +89,12 @@ __global__ void __launch_bounds__(1024) tile_kernel(const __grid_constant__ Tile
     tile_body<W, ASYNC>(p, src, dst);
 }
 
+template <typename W>
+__global__ void __launch_bounds__(1024) tile_kernel_bulk(const __grid_constant__ TileParams p,
+                                                         const W *__restrict__ src, W *__restrict__ dst) {
+    tile_body_bulk<W>(p, src, dst);
+}
+
 // ------------------------------------------------------------------ GATHER (K0)
 template <typename W>
 __global__ void __launch_bounds__(256) gather_kernel(const __grid_constant__ GatherParams p,
@@ -173,30 +179,37 @@ vpg_status launch_tile(const vpg_plan *p, const void *src, void *dst, cudaStream
     if (p->jit && aligned) {
         cudaKernel_t jk = jit_tile_kernel(p);
         if (jk) {
-            int nb = occupancy_ptr((const void *)jk, p->threads, smem);
+            const int jthreads = p->threads + (p->tile.bulk ? 32 : 0);
+            int nb = occupancy_ptr((const void *)jk, jthreads, smem);
             int64_t grid = p->tile.num_tiles;
             if (p->tile.persistent) grid = std::min<int64_t>(grid, (int64_t)nb * sm_count_for_current());
             if (grid < 1) grid = 1;
             void *args[] = {(void *)&src, (void *)&dst};
-            if (cudaLaunchKernel((const void *)jk, dim3((unsigned)grid), dim3(p->threads), args, (size_t)smem, st) ==
+            if (cudaLaunchKernel((const void *)jk, dim3((unsigned)grid), dim3(jthreads), args, (size_t)smem, st) ==
                 cudaSuccess)
                 return VPG_OK;
             cudaGetLastError();   // fall through to the ahead-of-time kernel
         }
     }
-    auto launch = [&](auto k) {
-        int nb = occupancy(k, p->threads, smem);
+    auto launch = [&](auto k, int threads, const TileParams &tp) {
+        int nb = occupancy(k, threads, smem);
         int64_t grid = p->tile.num_tiles;
         if (p->tile.persistent) grid = std::min<int64_t>(grid, (int64_t)nb * sm_count_for_current());
         if (grid < 1) grid = 1;
-        const TileParams &tp = aligned ? p->tile : p->tile_unaligned;
-        k<<<(unsigned)grid, p->threads, smem, st>>>(tp, (const W *)src, (W *)dst);
+        k<<<(unsigned)grid, threads, smem, st>>>(tp, (const W *)src, (W *)dst);
     };
+    if constexpr (E == 4 || E == 8) {
+        if (aligned && p->tile.bulk) {
+            launch(tile_kernel_bulk<W>, p->threads + 32, p->tile);
+            return VPG_OK;
+        }
+    }
+    const TileParams &tp = aligned ? p->tile : p->tile_unaligned;
     if constexpr (E >= 4) {
-        launch(tile_kernel<W, true>);
+        launch(tile_kernel<W, true>, p->threads, tp);
         return VPG_OK;
     }
-    if constexpr (E < 4) launch(tile_kernel<W, false>);
+    if constexpr (E < 4) launch(tile_kernel<W, false>, p->threads, tp);
     return VPG_OK;
 }
 

@@ -90,8 +90,8 @@ struct GridDigit {
 };
 
 struct PhaseDim {
-    FastDiv div;         // divides by extent
     int64_t gstride;     // global stride (elements; src for R, dst for W)
+    FastDiv div;         // divides by extent
     uint32_t sstride;    // smem stride (elements)
     int16_t slot;        // coordinate slot fed by this dim (-1 none)
     uint16_t cmul;       // coordinate units per step (V for vector-grouped dims)
@@ -133,6 +133,14 @@ struct TileParams {
     uint32_t e_a, d_a, e_c, d_c;
     uint32_t lim_split[2];         // static limit of slot 2 per phase (R, W)
     uint32_t hmask;                // shifted-run mode: V-1 (source runs sit at offset h in their smem row), else 0
+    // bulk mode: the R phase is one cp.async.bulk (TMA bulk copy) per source
+    // run, issued by a producer warp and tracked by mbarriers
+    uint32_t bulk;
+    uint32_t nruns;                // source runs per tile
+    int32_t nrdims;
+    uint32_t run_bytes;            // full run length in bytes
+    uint32_t run_unit_bytes;       // bytes per step of the partial source-boundary dim a
+    PhaseDim rdims[kMaxPhaseDims]; // run-index dims: gstride = src stride, sstride = smem row offset
     PhaseDesc ph[2];               // 0 = R (read), 1 = W (write)
     GridDigit grid[kMaxRank];
     uint32_t off_buf;              // smem byte offset of the tile buffers

@@ -62,6 +62,7 @@ struct Problem {
     int nbuf;             // forced pipeline stages (0 = planner's choice)
     int64_t cta_smem;     // per-CTA shared-memory target (bytes)
     bool no_shift = false; // disable shifted-run reads (VPG_NO_SHIFT)
+    bool no_bulk = true;   // TMA bulk source reads are opt-in (VPG_BULK=1)
     int r;
     int64_t d[kMaxRank];
     int sigma[kMaxRank];
@@ -88,6 +89,7 @@ void fill_problem(Problem &P) {
 struct TileGeom {
     int64_t ext[kMaxRank];   // 0 = not in tile
     int src_dims[kMaxRank], nsrc;   // source run dims (source order)
+    int n_runidx;                   // tile dims outside the source run
     int dst_dims[kMaxRank], ndst;   // destination run dims (dest order)
     int a_part, c_part;             // partial boundary dims (-1 none)
     int64_t Ls, Ld, T;
@@ -134,6 +136,7 @@ bool build_geom(const Problem &P, const int64_t *ext, TileGeom &g) {
     }
     if (ntile > kMaxTileDims) return false;
     int n_s_runidx = ntile - g.nsrc, n_w_runidx = ntile - g.ndst;
+    g.n_runidx = n_s_runidx;
     if (n_s_runidx > kMaxTileDims || n_w_runidx > kMaxTileDims || g.ndst > kMaxTileDims) return false;
     return true;
 }
@@ -270,6 +273,7 @@ struct PDimH {
 struct VecChoice {
     int vr = 1, vw = 1;
     bool rshift = false;   // R reads 16-byte aligned supersets of misaligned runs
+    bool bulk = false;     // R as one cp.async.bulk per source run (producer warp + mbarriers)
 };
 
 // smem strides of the tile dims for a given pitch (source run dense, run
@@ -283,8 +287,14 @@ void tile_sstrides(const Problem &Pb, const TileGeom &g, uint32_t pitch, int64_t
         sstr[k] = acc;
         acc *= g.ext[k];
     }
+    // rows (source runs) are ordered by the destination order of their
+    // run-index dims: the W phase's lanes then walk consecutive rows, which
+    // an odd chunk pitch spreads over all banks (in source order a
+    // run-index dim that W visits early can land on a row stride that is a
+    // multiple of 8 chunks and alias banks)
     acc = pitch;
-    for (int k = 0; k < Pb.r; ++k) {
+    for (int j = 0; j < Pb.r; ++j) {
+        const int k = Pb.sigma[j];
         if (g.ext[k] == 0 || in_src[k]) continue;
         sstr[k] = acc;
         acc *= g.ext[k];
@@ -555,6 +565,17 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
     double u1 = make_phase(phase_dims(Pb, g, sstr, slot_of_dim, true, vc.vw, hmask), NT, tp.ph[1], tp.lim_split[1]);
     tp.ph[0].rshift = vc.rshift ? 1u : 0u;
     tp.hmask = (uint32_t)hmask;
+    if (vc.bulk) {
+        tp.bulk = 1;
+        tp.nruns = (uint32_t)(g.T / g.Ls);
+        tp.run_bytes = (uint32_t)(g.Ls * Pb.E);
+        tp.run_unit_bytes = (uint32_t)((g.a_part >= 0 ? g.Ls / g.ext[g.a_part] : g.Ls) * Pb.E);
+        tp.nrdims = 0;
+        for (int k = 0; k < r; ++k) {
+            if (g.ext[k] == 0 || in_src[k]) continue;
+            set_pdim(tp.rdims[tp.nrdims++], g.ext[k], Pb.in_stride[k], sstr[k], slot_of_dim[k], 1);
+        }
+    }
     tp.n_elems = Pb.n;
     tp.ph[0].vec = (uint32_t)vc.vr;
     tp.ph[1].vec = (uint32_t)vc.vw;
@@ -759,7 +780,9 @@ static void describe(vpg_plan *p) {
                 ph ? "W" : "R", d.nthr, d.ngroups, d.nthr_dims, d.n_in, d.n_outer, d.nout_dims,
                 d.mask_full, d.mask_ragged);
         }
-        put("vector elems: R %u%s, W %u\n", t.ph[0].vec, t.ph[0].rshift ? " (aligned supersets of misaligned runs)" : "",
+        put("vector elems: R %u%s, W %u\n", t.ph[0].vec,
+            t.bulk ? " (TMA bulk copy per source run, producer warp)"
+                   : (t.ph[0].rshift ? " (aligned supersets of misaligned runs)" : ""),
             t.ph[1].vec);
         put("lane utilisation (R*W): %.3f\n", p->tile_util);
         put("specialised (NVRTC) kernel: %s\n", p->jit ? "yes" : "no");
@@ -808,6 +831,10 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
     if (const char *e = getenv("VPG_PERSIST")) persist_mode = atoi(e);
     if (const char *e = getenv("VPG_THREADS")) force_threads = atoi(e);
     if (getenv("VPG_NO_SHIFT")) P.no_shift = true;
+    // TMA bulk copies per source run measured slower than per-lane 16-byte
+    // cp.async on B200 (one bulk op per 256 B-1 KiB run costs more TMA issue
+    // time than it saves): opt-in only, VPG_BULK=1
+    P.no_bulk = !(getenv("VPG_BULK") && atoi(getenv("VPG_BULK")) != 0);
     if (flags & VPG_NO_MERGE) {
         P.r = rank;
         for (int k = 0; k < rank; ++k) {
@@ -910,10 +937,18 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         VecChoice vc;
         choose_pitch_vec(P, g, threads, pitch, vc);
         p->tile_util = fill_tile_params(P, g, pitch, threads, vc, p->tile);
+        // optionally the vectorised R phase runs as TMA bulk copies, one per
+        // source run (16-byte aligned runs of whole 16-byte chunks; VPG_BULK=1)
+        vc.bulk = vc.vr > 1 && !vc.rshift && !P.no_bulk && (g.Ls * E) % 16 == 0 &&
+                  (g.a_part < 0 ||
+                   ((g.Ls / g.ext[g.a_part]) * (P.d[g.a_part] % g.ext[g.a_part]) * E) % 16 == 0) &&
+                  g.n_runidx <= kMaxPhaseDims;
+        if (vc.bulk) p->tile_util = fill_tile_params(P, g, pitch, threads, vc, p->tile);
         // variant without 16-byte source reads, for misaligned base pointers
         VecChoice vs = vc;
         vs.vr = 1;
         vs.rshift = false;
+        vs.bulk = false;
         fill_tile_params(P, g, pitch, threads, vs, p->tile_unaligned);
         // the tile count must fit the 32-bit tile index
         double nt = 1.0;

@@ -507,3 +507,163 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
 
 
 }  // namespace vpg
+
+namespace vpg {
+
+// ------------------------------------------------------------------ bulk mode
+// The R phase as TMA bulk copies: a producer warp (the last warp of the
+// CTA) issues one cp.async.bulk per source run into the stage buffer and
+// arms the stage's `full` mbarrier with the expected byte count; the
+// consumer warps wait on it, run the W phase, and release the stage through
+// its `empty` mbarrier.  No CTA-wide barriers in the steady state.
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *sdst, const void *gsrc, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(sdst)),
+                 "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+template <typename W>
+__device__ __forceinline__ void tile_body_bulk(const TileParams &p, const W *__restrict__ src, W *__restrict__ dst) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
+    __shared__ int64_t s_base[kMaxStages][2];
+    __shared__ uint32_t s_valid[kMaxStages][2];
+    const uint32_t tid = threadIdx.x;
+    const uint32_t NC = blockDim.x - 32;              // consumer threads (the W phase was planned for NC)
+    const uint32_t first = blockIdx.x, step = gridDim.x;
+    if (first >= p.num_tiles) return;
+    const uint32_t cnt = (p.num_tiles - first + step - 1) / step;
+    const uint32_t S = p.nbuf;
+
+#ifndef VPG_JIT
+    {   // W-phase outer table (the producer needs no table)
+        const PhaseDesc &d = p.ph[1];
+        OuterEntry *tab = reinterpret_cast<OuterEntry *>(smem + d.off_tab);
+        for (uint32_t o = tid; o < d.n_outer; o += blockDim.x) {
+            uint32_t idx = o, s = 0, c0 = 0, c1 = 0, h = 0;
+            int64_t g = 0;
+            for (int i = 0; i < d.nout_dims; ++i) {
+                uint32_t q = fdiv(idx, d.out[i].div);
+                uint32_t c = idx - q * d.out[i].div.d;
+                idx = q;
+                g += (int64_t)c * d.out[i].gstride;
+                s += c * d.out[i].sstride;
+                h += c * d.out[i].hmul;
+                if (d.out[i].slot == 0) c0 = c * d.out[i].cmul;
+                else if (d.out[i].slot == 1) c1 = c * d.out[i].cmul;
+            }
+            OuterEntry e;
+            e.g = g;
+            e.s = s;
+            e.c0 = (uint16_t)c0;
+            e.c1 = (uint16_t)c1;
+            e.h = h;
+            e.pad_ = 0;
+            tab[o] = e;
+        }
+    }
+#endif
+    if (tid == 0) {
+        for (uint32_t s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NC / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    }
+    __syncthreads();
+    W *const buf0 = reinterpret_cast<W *>(smem + p.off_buf);
+    const size_t bstride = ((size_t)p.tile_elems_alloc * sizeof(W) + 15) / 16 * 16 / sizeof(W);
+
+    if (tid >= NC) {
+        // ---------------- producer warp
+        const uint32_t lane = tid - NC;
+        for (uint32_t k = 0; k < cnt; ++k) {
+            const uint32_t st = k % S;
+            if (k >= S) mbar_wait(&empty[st], ((k / S) - 1) & 1);
+            decode_tile(p, first + k * step, s_base, s_valid, (int)st);
+            __syncwarp();
+            const int64_t sb = s_base[st][0];
+            const uint32_t va = s_valid[st][0], vc = s_valid[st][1];
+            const uint32_t rbytes = va == p.e_a ? p.run_bytes : p.run_unit_bytes * va;
+            W *b = buf0 + st * bstride;
+            // valid runs of this lane and the total byte count of the stage
+            uint32_t mine = 0;
+            for (uint32_t r = lane; r < p.nruns; r += 32) {
+                uint32_t idx = r, cc = 0;
+                VPG_UNROLL
+                for (int i = 0; i < kMaxPhaseDims; ++i) {
+                    if (i >= p.nrdims) break;
+                    const uint32_t q = fdiv(idx, p.rdims[i].div);
+                    const uint32_t c = idx - q * p.rdims[i].div.d;
+                    idx = q;
+                    if (p.rdims[i].slot == 1) cc = c;
+                }
+                if (p.grid_c < 0 || cc < vc) mine += rbytes;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+            if (lane == 0) mbar_arrive_expect_tx(&full[st], mine);
+            __syncwarp();
+            for (uint32_t r = lane; r < p.nruns; r += 32) {
+                uint32_t idx = r, cc = 0, soff = 0;
+                int64_t goff = 0;
+                VPG_UNROLL
+                for (int i = 0; i < kMaxPhaseDims; ++i) {
+                    if (i >= p.nrdims) break;
+                    const uint32_t q = fdiv(idx, p.rdims[i].div);
+                    const uint32_t c = idx - q * p.rdims[i].div.d;
+                    idx = q;
+                    goff += (int64_t)c * p.rdims[i].gstride;
+                    soff += c * p.rdims[i].sstride;
+                    if (p.rdims[i].slot == 1) cc = c;
+                }
+                if (p.grid_c < 0 || cc < vc) bulk_g2s(b + soff, src + sb + goff, rbytes, &full[st]);
+            }
+        }
+        return;
+    }
+    // ---------------- consumer warps: the W phase
+    const ThreadPart tw = decode_thread(p.ph[1], tid);
+    for (uint32_t k = 0; k < cnt; ++k) {
+        const uint32_t st = k % S;
+        mbar_wait(&full[st], (k / S) & 1);
+        const uint32_t va = s_valid[st][0], vc = s_valid[st][1];
+        Lim lim;
+        lim.l0 = va;
+        lim.l1 = vc;
+        lim.l2 = p.lim_split[1];
+        const bool full_tile = (va == p.e_a) && (vc == p.e_c);
+        const uint32_t m = full_tile ? p.ph[1].mask_full : p.ph[1].mask_ragged;
+        tile_write<W>(p.ph[1], tw, smem, dst + s_base[st][1], buf0 + st * bstride, m, lim,
+                      (uint32_t)s_base[st][0], p.hmask);
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(&empty[st]);
+    }
+}
+
+}  // namespace vpg

@@ -29,7 +29,7 @@ class FastDiv(ctypes.Structure):
 
 
 class PhaseDim(ctypes.Structure):
-    _fields_ = [("div", FastDiv), ("gstride", ctypes.c_int64), ("sstride", ctypes.c_uint32),
+    _fields_ = [("gstride", ctypes.c_int64), ("div", FastDiv), ("sstride", ctypes.c_uint32),
                 ("slot", ctypes.c_int16), ("cmul", ctypes.c_uint16), ("hmul", ctypes.c_uint16),
                 ("pad_", ctypes.c_uint16)]
 
@@ -54,6 +54,9 @@ class TileParams(ctypes.Structure):
                 ("grid_a", ctypes.c_int32), ("grid_c", ctypes.c_int32),
                 ("e_a", ctypes.c_uint32), ("d_a", ctypes.c_uint32), ("e_c", ctypes.c_uint32),
                 ("d_c", ctypes.c_uint32), ("lim_split", ctypes.c_uint32 * 2), ("hmask", ctypes.c_uint32),
+                ("bulk", ctypes.c_uint32), ("nruns", ctypes.c_uint32), ("nrdims", ctypes.c_int32),
+                ("run_bytes", ctypes.c_uint32), ("run_unit_bytes", ctypes.c_uint32),
+                ("rdims", PhaseDim * MAXPD),
                 ("ph", PhaseDesc * 2), ("grid", GridDigit * MAXR), ("off_buf", ctypes.c_uint32),
                 ("nbuf", ctypes.c_uint32), ("persistent", ctypes.c_uint32), ("smem_bytes", ctypes.c_uint32)]
 
@@ -148,7 +151,26 @@ def simulate(program, src_words: np.ndarray, threads: int | None = None) -> np.n
         lim = (va, vc)
         smem = np.zeros(alloc + 64, dtype=src_words.dtype)
         smem_valid = np.zeros(alloc + 64, dtype=bool)
+        if tp.bulk:
+            # R as one bulk copy per source run (producer warp)
+            rbytes = tp.run_bytes if va == tp.e_a else tp.run_unit_bytes * va
+            if rbytes % 16 or tp.run_bytes % 16:
+                raise SimError("bulk copy size not a multiple of 16 bytes")
+            nel = rbytes // E
+            for r in range(tp.nruns):
+                g_, s_, c_, _ = _decode([r], tp.rdims, tp.nrdims)
+                if tp.grid_c >= 0 and c_[1][0] >= vc:
+                    continue
+                ga, sa = sb + g_[0], s_[0]
+                if (ga * E) % 16 or (sa * E) % 16:
+                    raise SimError("bulk copy address not 16-byte aligned")
+                _chk(np.array([ga, ga + nel - 1]), n, "bulk global")
+                _chk(np.array([sa, sa + nel - 1]), alloc, "bulk smem")
+                smem[sa:sa + nel] = src_words[ga:ga + nel]
+                smem_valid[sa:sa + nel] = True
         for ph in range(2):
+            if ph == 0 and tp.bulk:
+                continue
             d, grp, active, tg, ts, tc, th = parts[ph]
             mask = d.mask_full if full else d.mask_ragged
             V = d.vec

@@ -206,3 +206,28 @@ def test_large_random_campaign(cuda, jit, count):
         assert torch.equal(execute_device(inv, y).reshape(-1), x.reshape(-1)), (shape, axes)
         if jit and prog.kernel == "tile":
             assert prog.jit_state == 2
+
+
+@pytest.mark.parametrize("jit", [False, True])
+def test_bulk_tma_mode(cuda, jit, monkeypatch):
+    """Opt-in R phase as TMA bulk copies (producer warp + mbarriers,
+    VPG_BULK=1): bit-exact on transposes, batched transposes, all-2 ranks and
+    ragged tiles."""
+    import torch
+
+    from paper_2506_03686_b200 import TensorLayout, build_program, from_numpy_convention, program_cache_clear
+    from paper_2506_03686_b200.api import execute_device
+
+    monkeypatch.setenv("VPG_BULK", "1")
+    program_cache_clear()
+    seen = 0
+    for shape, axes, E in [((256, 384), (1, 0), 4), ((1000, 776), (1, 0), 4), ((8, 24, 20, 12), (0, 2, 3, 1), 4),
+                           ((2,) * 18, tuple(np.random.default_rng(4).permutation(18).tolist()), 8),
+                           ((36, 100, 52), (2, 0, 1), 8)]:
+        prog = build_program(TensorLayout.from_shape(shape, E), from_numpy_convention(axes), force="tile", jit=jit)
+        seen += "TMA bulk" in prog.text
+        dt = torch.int32 if E == 4 else torch.int64
+        x = torch.randint(-2**30, 2**30, shape, dtype=dt, device=cuda)
+        assert torch.equal(execute_device(prog, x), x.permute(axes).contiguous()), (shape, prog.text)
+    program_cache_clear()
+    assert seen >= 3

@@ -60,3 +60,16 @@ def test_sim_campaign_sample():
                                 force="tile")
         out = simulate(prog, golden_pattern(c["n"], c["elem"]))
         assert sha256(out) == c["sha256"], c["name"]
+
+
+def test_sim_bulk_mode(monkeypatch):
+    monkeypatch.setenv("VPG_BULK", "1")
+    vp.program_cache_clear()
+    rng = np.random.default_rng(3)
+    seen = 0
+    for shape, axes, E in [((256, 96), (1, 0), 4), ((100, 76), (1, 0), 4), ((8, 24, 20, 12), (0, 2, 3, 1), 4),
+                           ((2,) * 12, (3, 9, 0, 7, 1, 5, 2, 11, 8, 6, 4, 10), 8), ((36, 10, 52), (2, 0, 1), 8)]:
+        p = _run(shape, axes, E, rng)
+        seen += "TMA bulk" in p.text
+    vp.program_cache_clear()
+    assert seen >= 3
