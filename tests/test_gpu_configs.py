@@ -95,3 +95,26 @@ def test_config_ahead_of_time_kernel(cuda, cfg):
     y = execute_device(prog, torch.from_numpy(x).to(cuda))
     assert prog.jit_state == 0
     assert sha256(y.cpu().numpy()) == golden()["full_configs"][cfg]["output_sha256"]
+
+
+@pytest.mark.parametrize("shape,axes,kind", [
+    ((3, 46341, 15467), (2, 0, 1), "tile"),       # 2.15e9 elements: offsets beyond 2^31 elements
+    ((2, 8192, 140000), (1, 0, 2), "rows"),       # stride-1 preserved, > 2^31 elements
+])
+def test_beyond_2pow31_elements(cuda, shape, axes, kind):
+    """64-bit addressing: tensors of more than 2^31 int32 elements (8.6 GB),
+    checked against torch's own device permute."""
+    import torch
+
+    from paper_2506_03686_b200 import TensorLayout, build_program, from_numpy_convention
+    from paper_2506_03686_b200.api import execute_device
+
+    prog = build_program(TensorLayout.from_shape(shape, 4), from_numpy_convention(axes))
+    assert prog.kernel == kind and prog.num_elements > 2**31
+    g = torch.Generator(device=cuda).manual_seed(3)
+    x = torch.randint(-2**31, 2**31 - 1, shape, dtype=torch.int32, device=cuda, generator=g)
+    y = execute_device(prog, x)
+    want = x.permute(axes).contiguous()
+    assert torch.equal(y, want)
+    del x, y, want
+    torch.cuda.empty_cache()
