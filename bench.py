@@ -289,9 +289,13 @@ def bench_one_gpu(args, torch, cfg, with_e2e, peak):
 
     dev = torch.device("cuda", torch.cuda.current_device())
     wl = CONFIGS[cfg]
-    prog = build_program(TensorLayout.from_shape(wl.shape, wl.elem_bytes), from_numpy_convention(wl.axes))
+    # measured planning (autotune, untimed): the fastest of the cost model's
+    # best tile shapes on this GPU; --no-tune keeps the model's first choice
+    prog = build_program(TensorLayout.from_shape(wl.shape, wl.elem_bytes), from_numpy_convention(wl.axes),
+                         tune=not args.no_tune)
     nbytes = wl.numel * wl.elem_bytes
-    res = {"config": cfg, "kernel": prog.kernel}
+    res = {"config": cfg, "kernel": prog.kernel,
+           "tile": [prog.metadata["src_run"], prog.metadata["dst_run"]] if prog.kernel == "tile" else None}
     host_in = None
     if with_e2e:
         x = make_input(wl, threads=16)
@@ -335,6 +339,7 @@ def bench_one_gpu(args, torch, cfg, with_e2e, peak):
     res["times_ms"] = times
     res["algorithmic_bytes"] = wl.algorithmic_bytes
     if with_e2e:
+        launch()                          # yd held the copy/torch comparators' output
         host_out = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
         # (1) one blocking call per step: latency of a single host permutation
         e2e_t = []
@@ -506,6 +511,7 @@ def main(argv=None):
     ap.add_argument("--config", default=DEFAULT_CFG)
     ap.add_argument("--no-extra", action="store_true", help="skip cfg1-4 side measurements")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-tune", action="store_true", help="skip measured planning (autotune)")
     ap.add_argument("--cpu-threads", type=int, default=None)
     ap.add_argument("--sharded", action="store_true",
                     help="use the sharded (torchrun/NCCL) code path even with one rank")
@@ -539,6 +545,7 @@ def main(argv=None):
         "algorithmic_bytes_per_step": wl.algorithmic_bytes,
         "parallelism": f"sharded{args.gpus}" if args.gpus > 1 else "single-gpu",
         "l2_flush": "write 2xL2 + read 2xL2 before every timed step",
+        "planning": "none" if args.no_tune else "autotune: fastest of the cost model's best tile shapes (untimed)",
     }
 
     if args.impl == "reference":
@@ -583,6 +590,7 @@ def main(argv=None):
             r = bench_one_gpu(args, torch, k, False, peak)
             extra[k] = {"gbs": round(r["gbs"], 1), "frac_of_hbm": round(r["frac_of_hbm"], 4),
                         "us_per_launch": round(r["ms_per_launch"] * 1e3, 2), "kernel": r["kernel"],
+                        "tile_src_dst_run": r["tile"],
                         "parity_sampled": r["parity_sampled"],
                         "torch_permute_copy_gbs": None if r["torch_gbs"] is None else round(r["torch_gbs"], 1),
                         "same_run_copy_gbs": round(r["copy_gbs"], 1),
@@ -590,6 +598,7 @@ def main(argv=None):
     extra[args.config] = {"gbs": round(main_res["gbs"], 1), "frac_of_hbm": round(main_res["frac_of_hbm"], 4),
                           "us_per_launch": round(main_res["ms_per_launch"] * 1e3, 2),
                           "kernel": main_res["kernel"], "parity_sampled": main_res["parity_sampled"],
+                          "tile_src_dst_run": main_res["tile"],
                           "torch_permute_copy_gbs": None if main_res["torch_gbs"] is None
                           else round(main_res["torch_gbs"], 1),
                           "same_run_copy_gbs": round(main_res["copy_gbs"], 1),

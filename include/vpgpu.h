@@ -97,6 +97,10 @@ vpg_status vpg_merge_dimensions(int rank, const int64_t *dims, const int32_t *si
 #define VPG_NO_MERGE     0x4
 #define VPG_FORCE_JIT    0x8    /* TILE: always use the per-case NVRTC-specialised kernel  */
 #define VPG_NO_JIT       0x10   /* TILE: always use the ahead-of-time kernel                */
+/* TILE: use the n-th best tile candidate of the planner's cost model
+ * (n >= 0); plan creation fails with VPG_EUNSUPPORTED past the last one.
+ * Autotuners time a few candidates and keep the fastest. */
+#define VPG_TILE_CANDIDATE(n) ((unsigned)(((n) + 1) & 0xff) << 8)
 vpg_status vpg_plan_create(int rank, const int64_t *dims_inner_first,
                            const int32_t *sigma_inner_first, int elem_bytes,
                            unsigned flags, vpg_plan **out);

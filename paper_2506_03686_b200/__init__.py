@@ -30,6 +30,7 @@ from .api import (
     merge_dimensions,
     permute,
     program_cache_clear,
+    autotune,
     release_scratch,
 )
 
@@ -56,5 +57,6 @@ __all__ = [
     "merge_dimensions",
     "permute",
     "program_cache_clear",
+    "autotune",
     "release_scratch",
 ]

@@ -46,6 +46,7 @@ __all__ = [
     "emit_source",
     "jit_compile",
     "program_cache_clear",
+    "autotune",
     "release_scratch",
 ]
 
@@ -175,14 +176,22 @@ def program_cache_clear():
 
 
 def build_program(layout: TensorLayout, pmap: PermutationMap, machine=None, merge: bool = True,
-                  opt: bool = True, force: str | None = None, jit: bool | None = None) -> GpuProgram:
+                  opt: bool = True, force: str | None = None, jit: bool | None = None,
+                  candidate: int | None = None, tune: bool = False) -> GpuProgram:
     """Plan a permutation (ir.py:441-456 signature; ``machine``/``opt`` kept
     for drop-in compatibility).
 
     ``force`` pins a kernel class for tests: ``"tile"`` or ``"gather"``.
     ``jit`` pins the per-case NVRTC specialisation of tile plans on/off
     (default: on for tensors of 4 MiB and more).
+    ``candidate`` picks the n-th best tile shape of the cost model (tile
+    plans; LayoutError past the last one).
+    ``tune`` times the best few tile candidates on the current GPU and keeps
+    the fastest (measured planning, like FFTW_MEASURE): the tuned program
+    then answers later calls with the same arguments and ``tune=False``.
     """
+    if tune:
+        return autotune(layout, pmap, merge=merge, force=force, jit=jit)
     if pmap.rank != layout.rank:
         raise LayoutError("map rank does not match layout rank")
     if machine is not None and hasattr(machine, "elem_width") and machine.elem_width != layout.elem_width:
@@ -200,6 +209,10 @@ def build_program(layout: TensorLayout, pmap: PermutationMap, machine=None, merg
         flags |= _lib.VPG_FORCE_JIT
     elif jit is False:
         flags |= _lib.VPG_NO_JIT
+    if candidate is not None:
+        if not 0 <= candidate < 255:
+            raise ValueError(f"candidate {candidate} out of range")
+        flags |= ((candidate + 1) & 0xFF) << 8
     key = (layout.dims, layout.elem_width, pmap.sigma, flags)
     with _cache_lock:
         hit = _cache.get(key)
@@ -241,6 +254,60 @@ def build_program(layout: TensorLayout, pmap: PermutationMap, machine=None, merg
     with _cache_lock:
         _cache.setdefault(key, prog)
         return _cache[key]
+
+
+def _time_program(torch, program, src, dst, flush, reps):
+    """Median device time (ms) of one launch after an L2 flush."""
+    stream = torch.cuda.current_stream(src.device)
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    times = []
+    for i in range(reps + 2):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        _launch(program, src.data_ptr(), dst.data_ptr(), sp)
+        b.record(stream)
+        b.synchronize()
+        if i >= 2:                       # first launches compile/load the kernel
+            times.append(a.elapsed_time(b))
+    times.sort()
+    return times[len(times) // 2]
+
+
+def autotune(layout: TensorLayout, pmap: PermutationMap, candidates: int = 10, reps: int = 5,
+             merge: bool = True, force: str | None = None, jit: bool | None = None,
+             device=None) -> GpuProgram:
+    """Time the ``candidates`` best tile shapes of the cost model on the GPU
+    and cache the fastest as the program for these arguments.  Non-tile
+    plans are returned unchanged.  Needs a GPU (raises on CPU)."""
+    base = build_program(layout, pmap, merge=merge, force=force, jit=jit)
+    if base.kernel != "tile" or base.num_elements == 0:
+        return base
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise CudaError("autotune needs a CUDA device")
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    with torch.cuda.device(dev):
+        src = torch.empty(base.nbytes, dtype=torch.uint8, device=dev)
+        dst = torch.empty(base.nbytes, dtype=torch.uint8, device=dev)
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        best, best_t = base, _time_program(torch, base, src, dst, flush, reps)
+        for c in range(1, candidates):
+            try:
+                prog = build_program(layout, pmap, merge=merge, force=force, jit=jit, candidate=c)
+            except LayoutError:
+                break                     # fewer candidates than asked for
+            t = _time_program(torch, prog, src, dst, flush, reps)
+            if t < best_t:
+                best, best_t = prog, t
+        del src, dst, flush
+    with _cache_lock:
+        for k, v in list(_cache.items()):
+            if v is base:
+                _cache[k] = best
+    best.metadata["tuned_ms"] = best_t
+    return best
 
 
 def emit_source(program: GpuProgram) -> str:

@@ -192,11 +192,12 @@ std::vector<int64_t> extent_candidates(int64_t d, int64_t cap) {
     return v;
 }
 
-bool select_tile(const Problem &P, TileGeom &best) {
+bool select_tile(const Problem &P, TileGeom &best, int pick = -1) {
     const int r = P.r;
     const int64_t maxT = std::max<int64_t>(P.budget / P.E, 64);
     bool found = false;
     best.cost = 1e300;
+    std::vector<TileGeom> all;   // every candidate, for VPG_TILE_PICK (tuning sweeps)
     int64_t ext[kMaxRank];
     int64_t pre_s = 1;
     for (int a = 0; a < r && pre_s <= maxT; pre_s *= P.d[a], ++a) {
@@ -224,6 +225,7 @@ bool select_tile(const Problem &P, TileGeom &best) {
                     if (!build_geom(P, e2, g)) continue;
                     if (g.T > maxT) continue;
                     score_geom(P, g);
+                    all.push_back(g);
                     if (!found || g.cost < best.cost - 1e-9 ||
                         (std::fabs(g.cost - best.cost) <= 1e-9 && g.T < best.T)) {
                         best = g;
@@ -234,6 +236,19 @@ bool select_tile(const Problem &P, TileGeom &best) {
                 (void)pre_d;
             }
         }
+    }
+    if (const char *e = getenv("VPG_TILE_PICK")) pick = atoi(e);
+    if (pick >= 0) {
+        std::stable_sort(all.begin(), all.end(), [](const TileGeom &x, const TileGeom &y) { return x.cost < y.cost; });
+        std::vector<TileGeom> uniq;   // distinct (Ls, Ld, T)
+        for (const TileGeom &g : all) {
+            bool dup = false;
+            for (const TileGeom &u : uniq)
+                if (u.Ls == g.Ls && u.Ld == g.Ld && u.T == g.T) dup = true;
+            if (!dup) uniq.push_back(g);
+        }
+        if ((size_t)pick >= uniq.size()) return false;       // no such candidate
+        best = uniq[(size_t)pick];
     }
     return found;
 }
@@ -925,9 +940,11 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         p->predicted_eff = (double)bytes / (32.0 * expected_sectors(bytes, gcd64(bytes, 32)));
     } else {
         TileGeom g;
-        if (!select_tile(P, g)) {
+        // flags bits 8..15: pick the n-th best tile candidate (autotuning)
+        const int pick = (int)((flags >> 8) & 0xff) - 1;
+        if (!select_tile(P, g, pick)) {
             delete p;
-            *err = "no tile fits the shared-memory budget";
+            *err = pick >= 0 ? "no such tile candidate" : "no tile fits the shared-memory budget";
             return VPG_EUNSUPPORTED;
         }
         p->kernel_class = VPG_KERNEL_TILE;

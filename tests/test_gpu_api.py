@@ -244,3 +244,31 @@ def test_execute_host_nonblocking_chained(cuda):
     torch.cuda.current_stream().synchronize()
     assert torch.equal(c, a)
     assert not torch.equal(b, a)
+
+
+def test_autotune_candidates_are_exact(cuda):
+    """Every tile candidate the autotuner may pick is a valid plan: bit-exact
+    against the oracle; the tuned program replaces the cached default."""
+    import torch
+
+    import paper_2506_03686_b200 as vp
+    shape, axes = (96, 70, 130), (2, 0, 1)
+    lay, pm = vp.TensorLayout.from_shape(shape, 4), vp.from_numpy_convention(axes)
+    x = np.random.default_rng(3).integers(0, 2**31, size=shape, dtype=np.int32)
+    want = oracle.naive_permute_np(x.reshape(-1), lay.dims, pm.sigma).reshape(np.transpose(x, axes).shape)
+    assert np.array_equal(want, np.transpose(x, axes))
+    xd = torch.from_numpy(x).cuda()
+    n = 0
+    for c in range(12):
+        try:
+            p = vp.build_program(lay, pm, force="tile", candidate=c)
+        except vp.LayoutError:
+            break
+        y = execute_device(p, xd)
+        assert np.array_equal(y.cpu().numpy(), want), (c, p.metadata["src_run"], p.metadata["dst_run"])
+        n += 1
+    assert n >= 3
+    best = vp.autotune(lay, pm, force="tile", candidates=4)
+    assert vp.build_program(lay, pm, force="tile") is best
+    assert np.array_equal(execute_device(best, xd).cpu().numpy(), want)
+    assert best.metadata["tuned_ms"] > 0

@@ -176,3 +176,18 @@ def test_specialised_random_plans_compile():
         shape = tuple(int(rng.integers(2, 30)) for _ in range(rank))
         axes = tuple(int(a) for a in rng.permutation(rank))
         vp.jit_compile(_plan(shape, axes, elem, force="tile"))
+
+
+def test_tile_candidates_for_autotuning():
+    """VPG_TILE_CANDIDATE(n): distinct tile shapes, each a complete plan;
+    past the last candidate plan creation fails."""
+    shapes = set()
+    for c in range(6):
+        p = _plan((64, 48, 80), (2, 0, 1), candidate=c)
+        m = p.metadata
+        assert p.kernel == "tile" and m["tile_elems"] * m["num_tiles"] >= p.num_elements
+        shapes.add((m["src_run"], m["dst_run"], m["tile_elems"]))
+    assert len(shapes) == 6
+    assert _plan((64, 48, 80), (2, 0, 1), candidate=0).text == _plan((64, 48, 80), (2, 0, 1)).text
+    with pytest.raises(LayoutError):
+        _plan((6, 5), (1, 0), force="tile", candidate=200)
