@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define VPG_ABI_VERSION 1
+#define VPG_ABI_VERSION 2
 #define VPG_MAX_RANK 64
 
 typedef enum {
@@ -75,6 +75,8 @@ typedef struct {
     double  predicted_efficiency;   /* planner's sector-efficiency estimate, 0..1 */
     int32_t host_chunks;            /* vpg_permute_host pipeline chunks (0 = single shot) */
     int32_t jit_state;              /* 0 no specialisation, 1 pending, 2 specialised kernel loaded, -1 failed */
+    int32_t shards;                 /* sharded exchange plans: G (0 = ordinary plan) */
+    int32_t shard_index;            /* sharded exchange plans: this plan's input shard */
 } vpg_plan_info;
 
 /* Library ABI version (VPG_ABI_VERSION). */
@@ -138,6 +140,38 @@ vpg_status vpg_permute_host_async(const vpg_plan *plan, const void *host_src, vo
 vpg_status vpg_permute_nd(int rank, const int64_t *dims_inner_first,
                           const int32_t *sigma_inner_first, int elem_bytes,
                           const void *src, void *dst, void *cuda_stream);
+
+/* Fused sharded exchange.  The tensor (dims, sigma as
+ * in vpg_plan_create) is split into `shards` contiguous input shards and
+ * `shards` contiguous output shards of num_elements/shards elements each:
+ * input shard r is flat input [r*N/G, (r+1)*N/G), output shard q is flat
+ * output [q*N/G, (q+1)*N/G) -- the leading-axis sharding of both sides.
+ * A plan for input shard `shard_index` permutes that shard with ONE kernel
+ * that stores every tile straight into the output shard that owns it:
+ * dst_shards[q] is shard q's buffer as seen from this device (the local
+ * buffer for q == shard_index, CUDA IPC / peer-mapped pointers over
+ * NVLink/NVSwitch for the others).  No staging buffer, no collective.
+ * Requires the leading dims on each side to split into factors whose
+ * product is `shards` (VPG_EUNSUPPORTED otherwise, as when no tile avoids
+ * the shard-indexing dims).  The caller orders the exchange: every shard's
+ * buffer must be free before any rank launches, and no rank may read its
+ * output before every rank's kernel has completed (e.g. a device-side
+ * barrier such as a one-element NCCL all-reduce on each side).
+ * shards <= 64. */
+vpg_status vpg_plan_create_sharded(int rank, const int64_t *dims_inner_first,
+                                   const int32_t *sigma_inner_first, int elem_bytes,
+                                   unsigned flags, int shards, int shard_index, vpg_plan **out);
+vpg_status vpg_permute_sharded(const vpg_plan *plan, const void *src_shard,
+                               void *const *dst_shards, void *cuda_stream);
+
+/* CUDA IPC for the exchange's peer table: export a device pointer (any
+ * pointer inside a cudaMalloc allocation) as a VPG_IPC_HANDLE_BYTES handle
+ * plus offset, import it in another process on this or a peer GPU (mapped
+ * with lazy peer access), release the mapping. */
+#define VPG_IPC_HANDLE_BYTES 64
+vpg_status vpg_ipc_export(const void *dev_ptr, void *handle, uint64_t *offset);
+vpg_status vpg_ipc_import(const void *handle, uint64_t offset, void **dev_ptr);
+vpg_status vpg_ipc_release(void *dev_ptr);
 
 /* Plan inspection (format_plan analog, planner.py:386-419). */
 vpg_status vpg_plan_info_get(const vpg_plan *plan, vpg_plan_info *info);

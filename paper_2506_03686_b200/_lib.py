@@ -21,6 +21,8 @@ VPG_NO_MERGE = 0x4
 VPG_FORCE_JIT = 0x8
 VPG_NO_JIT = 0x10
 VPG_MAX_RANK = 64
+VPG_MAX_SHARDS = 64
+VPG_IPC_HANDLE_BYTES = 64
 
 # symbols declared in include/vpgpu.h (checked by tests/test_abi.py)
 EXPORTED = (
@@ -28,7 +30,12 @@ EXPORTED = (
     "vpg_last_error",
     "vpg_merge_dimensions",
     "vpg_plan_create",
+    "vpg_plan_create_sharded",
     "vpg_permute",
+    "vpg_permute_sharded",
+    "vpg_ipc_export",
+    "vpg_ipc_import",
+    "vpg_ipc_release",
     "vpg_permute_host",
     "vpg_permute_host_async",
     "vpg_permute_nd",
@@ -61,6 +68,8 @@ class PlanInfo(ctypes.Structure):
         ("predicted_efficiency", ctypes.c_double),
         ("host_chunks", ctypes.c_int32),
         ("jit_state", ctypes.c_int32),
+        ("shards", ctypes.c_int32),
+        ("shard_index", ctypes.c_int32),
     ]
 
 
@@ -94,7 +103,13 @@ def lib():
         L.vpg_merge_dimensions.argtypes = [ctypes.c_int, i64p, i32p, ctypes.POINTER(ctypes.c_int), i64p, i32p]
         L.vpg_plan_create.argtypes = [ctypes.c_int, i64p, i32p, ctypes.c_int, ctypes.c_uint,
                                       ctypes.POINTER(vp)]
+        L.vpg_plan_create_sharded.argtypes = [ctypes.c_int, i64p, i32p, ctypes.c_int, ctypes.c_uint,
+                                              ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]
         L.vpg_permute.argtypes = [vp, vp, vp, vp]
+        L.vpg_permute_sharded.argtypes = [vp, vp, ctypes.POINTER(vp), vp]
+        L.vpg_ipc_export.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_uint64)]
+        L.vpg_ipc_import.argtypes = [vp, ctypes.c_uint64, ctypes.POINTER(vp)]
+        L.vpg_ipc_release.argtypes = [vp]
         L.vpg_permute_host.argtypes = [vp, vp, vp, vp, vp, vp]
         L.vpg_permute_host_async.argtypes = [vp, vp, vp, vp, vp, vp]
         L.vpg_permute_nd.argtypes = [ctypes.c_int, i64p, i32p, ctypes.c_int, vp, vp, vp]
@@ -106,6 +121,8 @@ def lib():
         L.vpg_plan_destroy.argtypes = [vp]
         L.vpg_plan_destroy.restype = None
         for name in ("vpg_merge_dimensions", "vpg_plan_create", "vpg_permute", "vpg_permute_host",
+                     "vpg_plan_create_sharded", "vpg_permute_sharded", "vpg_ipc_export", "vpg_ipc_import",
+                     "vpg_ipc_release",
                      "vpg_permute_host_async",
                      "vpg_permute_nd", "vpg_plan_info_get", "vpg_plan_describe", "vpg_plan_emit_source",
                      "vpg_plan_jit_compile", "vpg_plan_tile_params"):

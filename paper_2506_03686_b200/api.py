@@ -47,6 +47,8 @@ __all__ = [
     "jit_compile",
     "program_cache_clear",
     "autotune",
+    "build_sharded_program",
+    "launch_sharded",
     "release_scratch",
 ]
 
@@ -175,6 +177,41 @@ def program_cache_clear():
         _cache.clear()
 
 
+def _wrap(ptr, layout: TensorLayout, pmap: PermutationMap) -> "GpuProgram":
+    """GpuProgram around a freshly created plan handle."""
+    L = _lib.lib()
+    handle = _Handle(ptr)
+    info = _lib.PlanInfo()
+    _check(L.vpg_plan_info_get(ptr, ctypes.byref(info)), "plan_info")
+    buf = ctypes.create_string_buffer(4096)
+    _check(L.vpg_plan_describe(ptr, buf, 4096), "plan_describe")
+    r = info.rank
+    merged_layout = TensorLayout(tuple(info.dims[:r]), layout.elem_width)
+    merged_pmap = PermutationMap(tuple(info.sigma[:r]))
+    kernel = _lib.KERNEL_NAMES[info.kernel_class]
+    meta = {
+        "kernel": kernel,
+        "merged_dims": merged_layout.dims,
+        "merged_sigma": merged_pmap.sigma,
+        "tile_elems": info.tile_elems,
+        "src_run": info.src_run,
+        "dst_run": info.dst_run,
+        "num_tiles": info.num_tiles,
+        "smem_pitch": info.smem_pitch,
+        "smem_bytes": info.smem_bytes,
+        "vec_elems": info.vec_elems,
+        "threads": info.threads,
+        "grid_hint": info.grid_hint,
+        "predicted_efficiency": info.predicted_efficiency,
+        "host_chunks": info.host_chunks,
+        "shards": info.shards,
+        "shard_index": info.shard_index,
+        "source_shape": layout.dims,
+        "source_map": pmap.sigma,
+    }
+    return GpuProgram(layout, pmap, merged_layout, merged_pmap, kernel, meta, buf.value.decode(), handle)
+
+
 def build_program(layout: TensorLayout, pmap: PermutationMap, machine=None, merge: bool = True,
                   opt: bool = True, force: str | None = None, jit: bool | None = None,
                   candidate: int | None = None, tune: bool = False) -> GpuProgram:
@@ -222,38 +259,55 @@ def build_program(layout: TensorLayout, pmap: PermutationMap, machine=None, merg
     rank, d, s = _lib.arrays(layout.dims, pmap.sigma)
     ptr = ctypes.c_void_p()
     _check(L.vpg_plan_create(rank, d, s, layout.elem_width, flags, ctypes.byref(ptr)), "build_program")
-    handle = _Handle(ptr)
-    info = _lib.PlanInfo()
-    _check(L.vpg_plan_info_get(ptr, ctypes.byref(info)), "plan_info")
-    buf = ctypes.create_string_buffer(4096)
-    _check(L.vpg_plan_describe(ptr, buf, 4096), "plan_describe")
-    r = info.rank
-    merged_layout = TensorLayout(tuple(info.dims[:r]), layout.elem_width)
-    merged_pmap = PermutationMap(tuple(info.sigma[:r]))
-    kernel = _lib.KERNEL_NAMES[info.kernel_class]
-    meta = {
-        "kernel": kernel,
-        "merged_dims": merged_layout.dims,
-        "merged_sigma": merged_pmap.sigma,
-        "tile_elems": info.tile_elems,
-        "src_run": info.src_run,
-        "dst_run": info.dst_run,
-        "num_tiles": info.num_tiles,
-        "smem_pitch": info.smem_pitch,
-        "smem_bytes": info.smem_bytes,
-        "vec_elems": info.vec_elems,
-        "threads": info.threads,
-        "grid_hint": info.grid_hint,
-        "predicted_efficiency": info.predicted_efficiency,
-        "host_chunks": info.host_chunks,
-        "source_shape": layout.dims,
-        "source_map": pmap.sigma,
-    }
-    prog = GpuProgram(layout, pmap, merged_layout, merged_pmap, kernel, meta,
-                      buf.value.decode(), handle)
+    prog = _wrap(ptr, layout, pmap)
     with _cache_lock:
         _cache.setdefault(key, prog)
         return _cache[key]
+
+
+def build_sharded_program(layout: TensorLayout, pmap: PermutationMap, shards: int, shard_index: int,
+                          jit: bool | None = None, candidate: int | None = None) -> GpuProgram:
+    """Plan of the fused sharded exchange for input shard ``shard_index`` of
+    ``shards`` (vpg_plan_create_sharded): ONE tile kernel that reads the
+    local input shard and stores every tile straight into the output shard
+    that owns it.  Raises LayoutError when the shapes do not shard or no tile
+    avoids the shard-indexing dims (callers then use the all-to-all path)."""
+    if pmap.rank != layout.rank:
+        raise LayoutError("map rank does not match layout rank")
+    if not 1 <= shards <= _lib.VPG_MAX_SHARDS:
+        raise LayoutError(f"shards must be in 1..{_lib.VPG_MAX_SHARDS}")
+    flags = 0
+    if jit is True:
+        flags |= _lib.VPG_FORCE_JIT
+    elif jit is False:
+        flags |= _lib.VPG_NO_JIT
+    if candidate is not None:
+        flags |= ((candidate + 1) & 0xFF) << 8
+    key = ("sharded", layout.dims, layout.elem_width, pmap.sigma, flags, shards, shard_index)
+    with _cache_lock:
+        hit = _cache.get(key)
+    if hit is not None:
+        return hit
+    L = _lib.lib()
+    rank, d, s = _lib.arrays(layout.dims, pmap.sigma)
+    ptr = ctypes.c_void_p()
+    _check(L.vpg_plan_create_sharded(rank, d, s, layout.elem_width, flags, shards, shard_index,
+                                     ctypes.byref(ptr)), "build_sharded_program")
+    prog = _wrap(ptr, layout, pmap)
+    with _cache_lock:
+        _cache.setdefault(key, prog)
+        return _cache[key]
+
+
+def launch_sharded(program: GpuProgram, src_ptr: int, dst_ptrs, stream_ptr) -> None:
+    """Enqueue the exchange kernel of one input shard (vpg_permute_sharded):
+    ``dst_ptrs[q]`` = output shard q's buffer as seen from this device."""
+    G = program.metadata["shards"]
+    if len(dst_ptrs) != G:
+        raise LayoutError(f"expected {G} destination shards, got {len(dst_ptrs)}")
+    arr = (ctypes.c_void_p * G)(*[int(p) for p in dst_ptrs])
+    st = _lib.lib().vpg_permute_sharded(program.handle, ctypes.c_void_p(src_ptr), arr, stream_ptr)
+    _check(st, "permute_sharded")
 
 
 def _time_program(torch, program, src, dst, flush, reps):

@@ -15,9 +15,6 @@ vpg_status permute_host_pipelined(const vpg_plan *p, const void *host_src, void 
                                   void *dev_dst, cudaStream_t user, bool async, std::string *err);
 int host_pipeline_chunks(const vpg_plan *p);
 void host_pipeline_forget(const vpg_plan *p);
-int merge_dims(int rank, const int64_t *dims, const int32_t *sigma, int64_t *od, int32_t *os);
-vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E, unsigned flags,
-                     vpg_plan **out, std::string *err);
 }  // namespace vpg
 
 namespace {
@@ -63,8 +60,54 @@ vpg_status vpg_plan_create(int rank, const int64_t *dims, const int32_t *sigma, 
     return VPG_OK;
 }
 
+vpg_status vpg_plan_create_sharded(int rank, const int64_t *dims, const int32_t *sigma, int elem_bytes,
+                                   unsigned flags, int shards, int shard_index, vpg_plan **out) {
+    if (!dims || !sigma || !out) return fail(VPG_EINVAL, "null argument");
+    if (shards < 1) return fail(VPG_EINVAL, "shards must be >= 1");
+    std::string err;
+    vpg_status s = vpg::make_plan(rank, dims, sigma, elem_bytes, flags, out, &err, shards, shard_index);
+    if (s != VPG_OK) return fail(s, err);
+    return VPG_OK;
+}
+
+vpg_status vpg_permute_sharded(const vpg_plan *plan, const void *src_shard, void *const *dst_shards,
+                               void *cuda_stream) {
+    if (!plan || !dst_shards) return fail(VPG_EINVAL, "null argument");
+    if (plan->shards < 1) return fail(VPG_EINVAL, "not a sharded plan (use vpg_permute)");
+    if (plan->n > 0 && !src_shard) return fail(VPG_EINVAL, "null buffer");
+    for (int q = 0; q < plan->shards; ++q)
+        if (dst_shards[q] == src_shard && plan->n > 0)
+            return fail(VPG_EINVAL, "src and dst must not overlap (out-of-place only)");
+    std::string err;
+    vpg_status s = vpg::launch_plan(plan, src_shard, dst_shards, plan->shards, cuda_stream, &err);
+    if (s != VPG_OK) return fail(s, err);
+    return VPG_OK;
+}
+
+vpg_status vpg_ipc_export(const void *dev_ptr, void *handle, uint64_t *offset) {
+    if (!dev_ptr || !handle || !offset) return fail(VPG_EINVAL, "null argument");
+    std::string err;
+    vpg_status s = vpg::ipc_export(dev_ptr, handle, offset, &err);
+    return s == VPG_OK ? s : fail(s, err);
+}
+
+vpg_status vpg_ipc_import(const void *handle, uint64_t offset, void **dev_ptr) {
+    if (!handle || !dev_ptr) return fail(VPG_EINVAL, "null argument");
+    std::string err;
+    vpg_status s = vpg::ipc_import(handle, offset, dev_ptr, &err);
+    return s == VPG_OK ? s : fail(s, err);
+}
+
+vpg_status vpg_ipc_release(void *dev_ptr) {
+    if (!dev_ptr) return fail(VPG_EINVAL, "null argument");
+    std::string err;
+    vpg_status s = vpg::ipc_release(dev_ptr, &err);
+    return s == VPG_OK ? s : fail(s, err);
+}
+
 vpg_status vpg_permute(const vpg_plan *plan, const void *src, void *dst, void *cuda_stream) {
     if (!plan) return fail(VPG_EINVAL, "null plan");
+    if (plan->shards > 1) return fail(VPG_EINVAL, "sharded plan: use vpg_permute_sharded");
     if (plan->n > 0 && (!src || !dst)) return fail(VPG_EINVAL, "null buffer");
     if (src == dst && plan->n > 0) return fail(VPG_EINVAL, "src and dst must not overlap (out-of-place only)");
     std::string err;
@@ -76,6 +119,7 @@ vpg_status vpg_permute(const vpg_plan *plan, const void *src, void *dst, void *c
 vpg_status vpg_permute_host(const vpg_plan *plan, const void *host_src, void *host_dst, void *dev_src,
                             void *dev_dst, void *cuda_stream) {
     if (!plan || !host_src || !host_dst || !dev_src || !dev_dst) return fail(VPG_EINVAL, "null argument");
+    if (plan->shards > 0) return fail(VPG_EINVAL, "sharded plans run through vpg_permute_sharded");
     cudaStream_t st = (cudaStream_t)cuda_stream;
     size_t nbytes = (size_t)plan->n * plan->elem_bytes;
     {
@@ -98,6 +142,7 @@ vpg_status vpg_permute_host(const vpg_plan *plan, const void *host_src, void *ho
 vpg_status vpg_permute_host_async(const vpg_plan *plan, const void *host_src, void *host_dst, void *dev_src,
                                   void *dev_dst, void *cuda_stream) {
     if (!plan || !host_src || !host_dst || !dev_src || !dev_dst) return fail(VPG_EINVAL, "null argument");
+    if (plan->shards > 0) return fail(VPG_EINVAL, "sharded plans run through vpg_permute_sharded");
     if (plan->n == 0) return VPG_OK;
     std::string err;
     vpg_status ps = vpg::permute_host_pipelined(plan, host_src, host_dst, dev_src, dev_dst,
@@ -151,6 +196,8 @@ vpg_status vpg_plan_info_get(const vpg_plan *p, vpg_plan_info *info) {
     info->predicted_efficiency = p->predicted_eff;
     info->host_chunks = vpg::host_pipeline_chunks(p);
     info->jit_state = vpg::jit_state(p);
+    info->shards = p->shards;
+    info->shard_index = p->shard_index;
     if (p->kernel_class == VPG_KERNEL_TILE) {
         info->tile_elems = p->tile.T;
         info->src_run = p->tile.Ls;

@@ -27,11 +27,6 @@
 
 #include "plan.h"
 
-namespace vpg {
-vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E, unsigned flags,
-                     vpg_plan **out, std::string *err);
-}
-
 namespace {
 
 using vpg::kMaxRank;

@@ -1,0 +1,98 @@
+// ipc.cpp -- CUDA IPC helpers for the fused sharded exchange's peer table
+// (include/vpgpu.h vpg_ipc_*).  One process per GPU: each rank exports its
+// output shard, imports the others' and passes the mapped pointers to
+// vpg_permute_sharded, whose kernel stores straight into them over
+// NVLink/NVSwitch.  Allocation bases come from the driver (pointers handed
+// out by caching allocators sit inside larger cudaMalloc segments).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+
+#include "plan.h"
+
+namespace {
+
+typedef CUresult (*PfnGetAddressRange)(CUdeviceptr *, size_t *, CUdeviceptr);
+
+std::mutex g_mu;
+std::map<void *, void *> g_base_of;   // imported pointer -> mapped base
+
+PfnGetAddressRange address_range_fn() {
+    static PfnGetAddressRange fn = [] {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return (PfnGetAddressRange)f;
+    }();
+    return fn;
+}
+
+}  // namespace
+
+namespace vpg {
+
+vpg_status ipc_export(const void *ptr, void *handle, uint64_t *offset, std::string *err) {
+    PfnGetAddressRange fn = address_range_fn();
+    if (!fn) {
+        *err = "cuMemGetAddressRange unavailable";
+        return VPG_ECUDA;
+    }
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (fn(&base, &size, (CUdeviceptr)ptr) != CUDA_SUCCESS) {
+        *err = "pointer is not a device allocation";
+        return VPG_EINVAL;
+    }
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, (void *)base);
+    if (e != cudaSuccess) {
+        *err = std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e);
+        return VPG_ECUDA;
+    }
+    memcpy(handle, &h, sizeof(h));
+    *offset = (uint64_t)((CUdeviceptr)ptr - base);
+    return VPG_OK;
+}
+
+vpg_status ipc_import(const void *handle, uint64_t offset, void **ptr, std::string *err) {
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    void *base = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+        *err = std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e);
+        return VPG_ECUDA;
+    }
+    *ptr = (char *)base + offset;
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_base_of[*ptr] = base;
+    return VPG_OK;
+}
+
+vpg_status ipc_release(void *ptr, std::string *err) {
+    void *base = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        auto it = g_base_of.find(ptr);
+        if (it == g_base_of.end()) {
+            *err = "pointer was not imported by vpg_ipc_import";
+            return VPG_EINVAL;
+        }
+        base = it->second;
+        g_base_of.erase(it);
+    }
+    cudaError_t e = cudaIpcCloseMemHandle(base);
+    if (e != cudaSuccess) {
+        *err = std::string("cudaIpcCloseMemHandle: ") + cudaGetErrorString(e);
+        return VPG_ECUDA;
+    }
+    return VPG_OK;
+}
+
+}  // namespace vpg

@@ -19,6 +19,7 @@
 //   gather_kernel  K0: out[i] = in[f(i)] per element (core.py:173-178)
 #include <cuda_runtime.h>
 
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <string>
@@ -85,14 +86,16 @@ __global__ void __launch_bounds__(256) rows_kernel(const __grid_constant__ RowsP
 // compiles the same body with the block baked in as constants.
 template <typename W, bool ASYNC>
 __global__ void __launch_bounds__(1024) tile_kernel(const __grid_constant__ TileParams p,
-                                                   const W *__restrict__ src, W *__restrict__ dst) {
-    tile_body<W, ASYNC>(p, src, dst);
+                                                   const W *__restrict__ src, W *__restrict__ dst,
+                                                   const __grid_constant__ ShardArgs sa) {
+    tile_body<W, ASYNC>(p, src, dst, sa);
 }
 
 template <typename W>
 __global__ void __launch_bounds__(1024) tile_kernel_bulk(const __grid_constant__ TileParams p,
-                                                         const W *__restrict__ src, W *__restrict__ dst) {
-    tile_body_bulk<W>(p, src, dst);
+                                                         const W *__restrict__ src, W *__restrict__ dst,
+                                                         const __grid_constant__ ShardArgs sa) {
+    tile_body_bulk<W>(p, src, dst, sa);
 }
 
 // ------------------------------------------------------------------ GATHER (K0)
@@ -172,7 +175,7 @@ int occupancy_ptr(const void *kernel, int threads, int smem) {
 }
 
 template <int E>
-vpg_status launch_tile(const vpg_plan *p, const void *src, void *dst, cudaStream_t st) {
+vpg_status launch_tile(const vpg_plan *p, const void *src, void *dst, const ShardArgs &sa, cudaStream_t st) {
     using W = typename WordOf<E>::T;
     const int smem = (int)p->tile.smem_bytes;
     const bool aligned = !(p->tile.ph[0].vec > 1 && ((uintptr_t)src % 16));
@@ -184,7 +187,7 @@ vpg_status launch_tile(const vpg_plan *p, const void *src, void *dst, cudaStream
             int64_t grid = p->tile.num_tiles;
             if (p->tile.persistent) grid = std::min<int64_t>(grid, (int64_t)nb * sm_count_for_current());
             if (grid < 1) grid = 1;
-            void *args[] = {(void *)&src, (void *)&dst};
+            void *args[] = {(void *)&src, (void *)&dst, (void *)&sa};
             if (cudaLaunchKernel((const void *)jk, dim3((unsigned)grid), dim3(jthreads), args, (size_t)smem, st) ==
                 cudaSuccess)
                 return VPG_OK;
@@ -196,7 +199,7 @@ vpg_status launch_tile(const vpg_plan *p, const void *src, void *dst, cudaStream
         int64_t grid = p->tile.num_tiles;
         if (p->tile.persistent) grid = std::min<int64_t>(grid, (int64_t)nb * sm_count_for_current());
         if (grid < 1) grid = 1;
-        k<<<(unsigned)grid, threads, smem, st>>>(tp, (const W *)src, (W *)dst);
+        k<<<(unsigned)grid, threads, smem, st>>>(tp, (const W *)src, (W *)dst, sa);
     };
     if constexpr (E == 4 || E == 8) {
         if (aligned && p->tile.bulk) {
@@ -290,10 +293,27 @@ vpg_status launch_copy(const vpg_plan *p, const void *src, void *dst, cudaStream
 
 int device_sm_count() { return sm_count_for_current(); }
 
-vpg_status launch_plan(const vpg_plan *p, const void *src, void *dst, void *stream, std::string *err) {
+vpg_status launch_plan(const vpg_plan *p, const void *src, void *const *dsts, int ndst, void *stream,
+                       std::string *err) {
     cudaStream_t st = (cudaStream_t)stream;
     const int E = p->elem_bytes;
-    if (((uintptr_t)src % E) || ((uintptr_t)dst % E)) {
+    const int G = p->shards > 0 ? p->shards : 1;
+    if (ndst != G) {
+        *err = "plan expects " + std::to_string(G) + " destination shard(s)";
+        return VPG_EINVAL;
+    }
+    void *dst = dsts[0];
+    ShardArgs sa;
+    memset(&sa, 0, sizeof(sa));
+    for (int q = 0; q < G; ++q) {
+        if (!dsts[q] || ((uintptr_t)dsts[q] % E)) {
+            *err = "destination buffers must be non-null and aligned to the element width";
+            return VPG_EINVAL;
+        }
+        const int64_t diff = (int64_t)((uintptr_t)dsts[q] - (uintptr_t)dst);
+        sa.off[q] = diff / E;
+    }
+    if ((uintptr_t)src % E) {
         *err = "buffers must be aligned to the element width";
         return VPG_EINVAL;
     }
@@ -308,11 +328,11 @@ vpg_status launch_plan(const vpg_plan *p, const void *src, void *dst, void *stre
             break;
         case VPG_KERNEL_TILE:
             switch (E) {
-                case 1: s = launch_tile<1>(p, src, dst, st); break;
-                case 2: s = launch_tile<2>(p, src, dst, st); break;
-                case 4: s = launch_tile<4>(p, src, dst, st); break;
-                case 8: s = launch_tile<8>(p, src, dst, st); break;
-                case 16: s = launch_tile<16>(p, src, dst, st); break;
+                case 1: s = launch_tile<1>(p, src, dst, sa, st); break;
+                case 2: s = launch_tile<2>(p, src, dst, sa, st); break;
+                case 4: s = launch_tile<4>(p, src, dst, sa, st); break;
+                case 8: s = launch_tile<8>(p, src, dst, sa, st); break;
+                case 16: s = launch_tile<16>(p, src, dst, sa, st); break;
                 default: s = VPG_EUNSUPPORTED;
             }
             break;

@@ -29,6 +29,8 @@ struct vpg_plan {
     double predicted_eff;
     double tile_util;
     int32_t jit;               // TILE: launch the NVRTC-specialised kernel (jit.cpp)
+    int32_t shards;            // 0: ordinary plan; G >= 1: fused sharded exchange plan of rank shard_index
+    int32_t shard_index;
     vpg::TileParams tile;
     vpg::TileParams tile_unaligned;   // same tile, scalar source reads
     vpg::RowsParams rows;
@@ -38,8 +40,23 @@ struct vpg_plan {
 };
 
 namespace vpg {
+// planner.cpp
+int merge_dims(int rank, const int64_t *dims, const int32_t *sigma, int64_t *od, int32_t *os,
+               const uint8_t *pin = nullptr, uint8_t *opin = nullptr);
+// shards > 0: fused sharded exchange plan for input shard shard_index
+vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E, unsigned flags,
+                     vpg_plan **out, std::string *err, int shards = 0, int shard_index = 0);
+// ipc.cpp
+vpg_status ipc_export(const void *ptr, void *handle, uint64_t *offset, std::string *err);
+vpg_status ipc_import(const void *handle, uint64_t offset, void **ptr, std::string *err);
+vpg_status ipc_release(void *ptr, std::string *err);
 // kernels.cu
-vpg_status launch_plan(const vpg_plan *p, const void *src, void *dst, void *stream, std::string *err);
+// dsts: one destination per output shard (1 for ordinary plans)
+vpg_status launch_plan(const vpg_plan *p, const void *src, void *const *dsts, int ndst, void *stream,
+                       std::string *err);
+inline vpg_status launch_plan(const vpg_plan *p, const void *src, void *dst, void *stream, std::string *err) {
+    return launch_plan(p, src, &dst, 1, stream, err);
+}
 cudaKernel_t jit_tile_kernel(const vpg_plan *p);
 void jit_forget(const vpg_plan *p);
 int jit_state(const vpg_plan *p);

@@ -147,8 +147,28 @@ struct TileParams {
     uint32_t nbuf;                 // 1 or 2 (double-buffered cp.async)
     uint32_t persistent;           // 1: grid = resident CTAs, 0: one CTA per tile
     uint32_t smem_bytes;
+    // fused sharded exchange (nshards > 1): the tensor is split into nshards
+    // contiguous input shards and nshards contiguous output shards.  This
+    // plan walks the tiles [tile_begin, tile_begin + num_tiles) of the global
+    // tile grid -- exactly the tiles whose source lies in input shard
+    // (src_bias / shard_elems), because the input-shard digits are the
+    // slowest grid digits -- reads them from the local shard (source offsets
+    // minus src_bias) and stores each tile straight into output shard
+    // q = dst / shard_elems through ShardArgs::off[q] (peer memory).
+    uint32_t nshards;
+    uint32_t tile_begin;
+    int64_t src_bias;
+    int64_t shard_elems;
 };
 static_assert(sizeof(TileParams) <= 4096, "kernel parameter block must stay under 4 KB");
+
+// Per-launch destination table of a sharded tile plan: element offset of
+// output shard q relative to the kernel's dst pointer (shard 0).  Passed by
+// value next to the parameter block (CUDA >= 12.1 kernel parameter space).
+constexpr int kMaxShards = 64;
+struct ShardArgs {
+    int64_t off[kMaxShards];
+};
 
 // --------------------------------------------------------------------------
 // ROWS (K1): stride-1 preserved; each destination row of Lr elements is a

@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <numeric>
 #include <vector>
 
@@ -71,6 +72,13 @@ struct Problem {
     int64_t out_stride_of_dim[kMaxRank];  // destination stride of source dim k
     int E;
     int64_t n;
+    // fused sharded exchange: pin[k] = 2 for the leading input dims (they
+    // index the source shard), 1 for the other leading output dims (they
+    // index the destination shard), 0 otherwise.  Pinned dims never enter a
+    // tile, and the input-shard digits are the slowest grid digits.
+    uint8_t pin[kMaxRank] = {};
+    int G = 0;          // shards (0: ordinary plan)
+    int shard = 0;      // this plan's input shard
 };
 
 void fill_problem(Problem &P) {
@@ -128,6 +136,7 @@ bool build_geom(const Problem &P, const int64_t *ext, TileGeom &g) {
     int ntile = 0;
     for (int k = 0; k < r; ++k) {
         if (ext[k] > 0) {
+            if (P.pin[k]) return false;   // shard-indexing dims stay grid digits
             g.T *= ext[k];
             ++ntile;
             // every partial dim must be a run boundary
@@ -598,16 +607,25 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
     // grid digits
     struct Dg {
         int64_t ext, ss, ds;
-        int dim;
+        int dim;     // partial tile dim (-1: whole grid dim)
+        int src;     // input-shard dim index (-1: other)
     };
     std::vector<Dg> dg;
     for (int k = 0; k < r; ++k) {
-        if (g.ext[k] == 0) dg.push_back({Pb.d[k], Pb.in_stride[k], Pb.out_stride_of_dim[k], -1});
+        if (g.ext[k] == 0)
+            dg.push_back({Pb.d[k], Pb.in_stride[k], Pb.out_stride_of_dim[k], -1, Pb.pin[k] == 2 ? k : -1});
         else if (g.ext[k] < Pb.d[k])
             dg.push_back({(Pb.d[k] + g.ext[k] - 1) / g.ext[k], Pb.in_stride[k] * g.ext[k],
-                          Pb.out_stride_of_dim[k] * g.ext[k], k});
+                          Pb.out_stride_of_dim[k] * g.ext[k], k, -1});
     }
-    std::stable_sort(dg.begin(), dg.end(), [](const Dg &x, const Dg &y) { return x.ds < y.ds; });
+    // destination-stride order (the reference's counter digits,
+    // planner.py:324-342); input-shard digits last, inner to outer, so a
+    // shard's tiles form one contiguous range of the tile index
+    std::stable_sort(dg.begin(), dg.end(), [](const Dg &x, const Dg &y) {
+        if ((x.src >= 0) != (y.src >= 0)) return y.src >= 0;
+        if (x.src >= 0) return x.src < y.src;
+        return x.ds < y.ds;
+    });
     tp.ngrid = (int32_t)dg.size();
     tp.grid_a = tp.grid_c = -1;
     uint64_t cum = 1;
@@ -621,6 +639,15 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
         cum *= (uint64_t)dg[i].ext;
     }
     tp.num_tiles = (uint32_t)std::min<uint64_t>(cum, 0xffffffffull);
+    if (Pb.G >= 1) {
+        const uint64_t per = cum / (uint64_t)Pb.G;
+        tp.nshards = (uint32_t)Pb.G;
+        tp.num_tiles = (uint32_t)std::min<uint64_t>(per, 0xffffffffull);
+        tp.tile_begin = (uint32_t)std::min<uint64_t>(per * (uint64_t)Pb.shard, 0xffffffffull);
+        tp.shard_elems = Pb.n / Pb.G;
+        tp.src_bias = tp.shard_elems * Pb.shard;
+        tp.n_elems = tp.shard_elems;      // source bounds: the local shard
+    }
     tp.e_a = g.a_part >= 0 ? (uint32_t)g.ext[g.a_part] : 1u;
     tp.d_a = g.a_part >= 0 ? (uint32_t)Pb.d[g.a_part] : 1u;
     bool c_slot = g.c_part >= 0 && g.c_part != g.a_part;
@@ -728,13 +755,17 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
 
 // ----------------------------------------------------------------- merge
 // planner.py:211-241
-int merge_dims(int rank, const int64_t *dims, const int32_t *sigma, int64_t *od, int32_t *os) {
+// `pin` (optional): pinned dims (sharded plans) never fuse with a neighbour;
+// `opin` receives the pin of every merged dim.
+int merge_dims(int rank, const int64_t *dims, const int32_t *sigma, int64_t *od, int32_t *os, const uint8_t *pin,
+               uint8_t *opin) {
     std::vector<int> keep;
     for (int k = 0; k < rank; ++k)
         if (dims[k] > 1) keep.push_back(k);
     if (keep.empty()) {
         od[0] = 1;
         os[0] = 0;
+        if (opin) opin[0] = 0;
         return 1;
     }
     std::vector<int> renum(rank, -1);
@@ -747,9 +778,10 @@ int merge_dims(int rank, const int64_t *dims, const int32_t *sigma, int64_t *od,
         if (renum[sigma[j]] >= 0) sg.push_back(renum[sigma[j]]);
     std::vector<int> pos(m);
     for (int j = 0; j < m; ++j) pos[sg[j]] = j;
+    auto pinned = [&](int k) { return pin && pin[keep[k]]; };
     std::vector<std::vector<int>> groups{{0}};
     for (int k = 1; k < m; ++k) {
-        if (pos[k] == pos[k - 1] + 1) groups.back().push_back(k);
+        if (pos[k] == pos[k - 1] + 1 && !pinned(k) && !pinned(k - 1)) groups.back().push_back(k);
         else groups.push_back({k});
     }
     int ng = (int)groups.size();
@@ -757,6 +789,7 @@ int merge_dims(int rank, const int64_t *dims, const int32_t *sigma, int64_t *od,
         int64_t p = 1;
         for (int k : groups[gi]) p *= d[k];
         od[gi] = p;
+        if (opin) opin[gi] = pin ? pin[keep[groups[gi][0]]] : 0;
     }
     std::vector<int> order(ng);
     std::iota(order.begin(), order.end(), 0);
@@ -764,6 +797,97 @@ int merge_dims(int rank, const int64_t *dims, const int32_t *sigma, int64_t *od,
                      [&](int x, int y) { return pos[groups[x][0]] < pos[groups[y][0]]; });
     for (int j = 0; j < ng; ++j) os[j] = order[j];
     return ng;
+}
+
+// ----------------------------------------------------------------- shards
+// Leading factors: walk dims outermost first taking whole dims, or the
+// outer factor of the dim that completes the product, until it equals G
+// (sharded.py _lead_split).  cuts[k] = outer factor taken from dim k.
+static bool lead_cuts(const std::vector<int> &outer_first, const int64_t *dims, int64_t G,
+                      std::map<int, int64_t> &cuts, std::string *err) {
+    int64_t rem = G;
+    for (int k : outer_first) {
+        if (rem == 1) break;
+        const int64_t d = dims[k];
+        if (d <= rem && rem % d == 0) {
+            cuts[k] = d;
+            rem /= d;
+        } else if (d % rem == 0) {
+            cuts[k] = rem;
+            rem = 1;
+        } else {
+            *err = "cannot shard: dim of size " + std::to_string(d) + " vs remaining factor " + std::to_string(rem);
+            return false;
+        }
+    }
+    if (rem != 1) {
+        *err = "tensor has fewer than " + std::to_string(G) + " leading elements";
+        return false;
+    }
+    return true;
+}
+
+// Split dims so that the leading input dims and the leading output dims each
+// multiply to exactly G; pin those (2 = input shard digits, 1 = output).
+// Inner-first in and out.
+static bool refine_for_shards(int rank, const int64_t *dims, const int32_t *sigma, int G,
+                              std::vector<int64_t> &rd, std::vector<int32_t> &rs, std::vector<uint8_t> &pin,
+                              std::string *err) {
+    std::vector<int> in_of, out_of;
+    for (int k = rank - 1; k >= 0; --k) in_of.push_back(k);
+    for (int j = rank - 1; j >= 0; --j) out_of.push_back(sigma[j]);
+    std::map<int, int64_t> cin, cout;
+    if (!lead_cuts(in_of, dims, G, cin, err) || !lead_cuts(out_of, dims, G, cout, err)) return false;
+    std::vector<std::vector<int64_t>> pieces(rank);   // inner-first factors of each dim
+    for (int k = 0; k < rank; ++k) {
+        std::vector<int64_t> cuts;
+        for (auto *m : {&cin, &cout}) {
+            auto it = m->find(k);
+            if (it != m->end() && it->second > 1 && it->second < dims[k]) cuts.push_back(it->second);
+        }
+        std::sort(cuts.begin(), cuts.end());
+        cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
+        if (cuts.size() == 2 && cuts[1] % cuts[0]) {
+            *err = "cannot shard: dim " + std::to_string(k) + " needs incompatible splits";
+            return false;
+        }
+        std::vector<int64_t> outer_first;
+        int64_t prev = 1;
+        for (int64_t c : cuts) {
+            outer_first.push_back(c / prev);
+            prev = c;
+        }
+        outer_first.push_back(dims[k] / prev);
+        pieces[k].assign(outer_first.rbegin(), outer_first.rend());
+    }
+    std::vector<int> first(rank);
+    rd.clear();
+    for (int k = 0; k < rank; ++k) {
+        first[k] = (int)rd.size();
+        for (int64_t f : pieces[k]) rd.push_back(f);
+    }
+    const int rr = (int)rd.size();
+    if (rr > VPG_MAX_RANK) {
+        *err = "refined rank exceeds " + std::to_string(VPG_MAX_RANK);
+        return false;
+    }
+    rs.clear();
+    for (int j = 0; j < rank; ++j)
+        for (size_t i = 0; i < pieces[sigma[j]].size(); ++i) rs.push_back(first[sigma[j]] + (int)i);
+    pin.assign(rr, 0);
+    if (G > 1) {
+        int64_t prod = 1;
+        for (int k = rr - 1; k >= 0 && prod < G; --k) {
+            pin[k] = 2;
+            prod *= rd[k];
+        }
+        prod = 1;
+        for (int j = rr - 1; j >= 0 && prod < G; --j) {
+            if (!pin[rs[j]]) pin[rs[j]] = 1;
+            prod *= rd[rs[j]];
+        }
+    }
+    return true;
 }
 
 // ----------------------------------------------------------------- plan
@@ -802,6 +926,9 @@ static void describe(vpg_plan *p) {
         put("lane utilisation (R*W): %.3f\n", p->tile_util);
         put("specialised (NVRTC) kernel: %s\n", p->jit ? "yes" : "no");
         put("tiles: %u, grid digits: %d\n", t.num_tiles, t.ngrid);
+        if (p->shards > 0)
+            put("sharded exchange: shard %d of %d, tiles [%u, %u), stores into %d output shards\n",
+                p->shard_index, p->shards, t.tile_begin, t.tile_begin + t.num_tiles, p->shards);
     } else if (p->kernel_class == VPG_KERNEL_ROWS) {
         put("rows: %u x %lld elements, vector %u elements, %u threads/row\n", p->rows.nrows,
             (long long)p->rows.row_len, p->rows.vec, 1u << p->rows.tpr_log2);
@@ -811,7 +938,7 @@ static void describe(vpg_plan *p) {
 }
 
 vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E, unsigned flags,
-                     vpg_plan **out, std::string *err) {
+                     vpg_plan **out, std::string *err, int shards, int shard_index) {
     if (rank < 1 || rank > VPG_MAX_RANK) {
         *err = "rank must be in 1.." + std::to_string(VPG_MAX_RANK);
         return VPG_EINVAL;
@@ -850,16 +977,33 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
     // cp.async on B200 (one bulk op per 256 B-1 KiB run costs more TMA issue
     // time than it saves): opt-in only, VPG_BULK=1
     P.no_bulk = !(getenv("VPG_BULK") && atoi(getenv("VPG_BULK")) != 0);
-    if (flags & VPG_NO_MERGE) {
-        P.r = rank;
-        for (int k = 0; k < rank; ++k) {
-            P.d[k] = dims[k];
-            P.sigma[k] = sigma[k];
+    // sharded exchange plans: refine and pin the shard-indexing dims first
+    std::vector<int64_t> rdims(dims, dims + rank);
+    std::vector<int32_t> rsig(sigma, sigma + rank);
+    std::vector<uint8_t> rpin(rank, 0);
+    if (shards > 0) {
+        if (shards > kMaxShards || shard_index < 0 || shard_index >= shards) {
+            *err = "shards must be in 1.." + std::to_string(kMaxShards) + " and shard_index in 0..shards-1";
+            return VPG_EINVAL;
         }
+        if (!refine_for_shards(rank, dims, sigma, shards, rdims, rsig, rpin, err)) return VPG_EUNSUPPORTED;
+        P.G = shards;
+        P.shard = shard_index;
+    }
+    const int rrank = (int)rdims.size();
+    if (flags & VPG_NO_MERGE) {
+        P.r = 0;
+        for (int k = 0; k < rrank && k < kMaxRank; ++k) {
+            P.d[k] = rdims[k];
+            P.sigma[k] = rsig[k];
+            P.pin[k] = rpin[k];
+        }
+        P.r = rrank;
     } else {
         int64_t md[VPG_MAX_RANK];
         int32_t ms[VPG_MAX_RANK];
-        P.r = merge_dims(rank, dims, sigma, md, ms);
+        uint8_t mp[VPG_MAX_RANK];
+        P.r = merge_dims(rrank, rdims.data(), rsig.data(), md, ms, rpin.data(), mp);
         if (P.r > kMaxRank) {
             *err = "merged rank exceeds " + std::to_string(kMaxRank);
             return VPG_EUNSUPPORTED;
@@ -867,6 +1011,7 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         for (int k = 0; k < P.r; ++k) {
             P.d[k] = md[k];
             P.sigma[k] = ms[k];
+            P.pin[k] = mp[k];
         }
     }
     if (P.r > kMaxRank) {
@@ -882,7 +1027,14 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         p->sigma[k] = P.sigma[k];
     }
     p->n = P.n;
+    p->shards = shards;
+    p->shard_index = shard_index;
     p->predicted_eff = 1.0;
+    // a sharded exchange is always a tile plan (per-tile destination shard)
+    if (shards > 0) {
+        flags |= VPG_FORCE_TILE;
+        flags &= ~(unsigned)VPG_FORCE_GATHER;
+    }
     bool identity = true;
     for (int k = 0; k < P.r; ++k)
         if (P.sigma[k] != k) identity = false;
@@ -981,7 +1133,7 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         // per-case specialisation pays off once the tensor is large enough to
         // amortise a one-off NVRTC compile (cached in-process and on disk)
         const char *je = getenv("VPG_JIT");
-        bool big = P.n * E >= ((int64_t)4 << 20);
+        bool big = P.n / std::max(1, P.G) * E >= ((int64_t)4 << 20);
         p->jit = (flags & VPG_FORCE_JIT) ? 1 : (flags & VPG_NO_JIT) ? 0 : je ? (atoi(je) != 0) : big;
         p->grid_hint = std::min<int64_t>(p->tile.num_tiles, 148 * 4);
         p->predicted_eff = 2.0 / (1.0 / g.eff_s + 1.0 / g.eff_d);

@@ -361,10 +361,13 @@ __device__ __forceinline__ void tile_write(const PhaseDesc &d, const ThreadPart 
 }
 
 // Warp 0 decodes tile `t` into slot `k`: source/destination base offsets and
-// the valid extents of the ragged boundary dims a and c.
-__device__ __forceinline__ void decode_tile(const TileParams &p, uint32_t t, int64_t (*s_base)[2],
-                                            uint32_t (*s_valid)[2], int k) {
+// the valid extents of the ragged boundary dims a and c.  Sharded plans
+// rebase the source offset onto the local input shard and the destination
+// offset onto the owning output shard's buffer (sa.off, relative to dst).
+__device__ __forceinline__ void decode_tile(const TileParams &p, const ShardArgs &sa, uint32_t t,
+                                            int64_t (*s_base)[2], uint32_t (*s_valid)[2], int k) {
     const uint32_t lane = threadIdx.x & 31;
+    t += p.tile_begin;
     int64_t sb = 0, db = 0;
     uint32_t va = p.e_a, vc = p.e_c;
     for (int i = (int)lane; i < p.ngrid; i += 32) {
@@ -383,6 +386,11 @@ __device__ __forceinline__ void decode_tile(const TileParams &p, uint32_t t, int
         vc = min(vc, __shfl_xor_sync(0xffffffffu, vc, o));
     }
     if (lane == 0) {
+        if (p.nshards > 1) {
+            const uint64_t q = (uint64_t)db / (uint64_t)p.shard_elems;
+            sb -= p.src_bias;
+            db += sa.off[q] - (int64_t)q * p.shard_elems;
+        }
         s_base[k][0] = sb;
         s_base[k][1] = db;
         s_valid[k][0] = va;
@@ -419,7 +427,8 @@ constexpr int kRing = kMaxStages + 2;
 // loads in flight per CTA.  Without ASYNC (1- and 2-byte words) a single
 // buffer is filled by LDG+STS.
 template <typename W, bool ASYNC>
-__device__ __forceinline__ void tile_body(const TileParams &p, const W *__restrict__ src, W *__restrict__ dst) {
+__device__ __forceinline__ void tile_body(const TileParams &p, const W *__restrict__ src, W *__restrict__ dst,
+                                          const ShardArgs &sa) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int64_t s_base[kRing][2];
     __shared__ uint32_t s_valid[kRing][2];
@@ -466,7 +475,7 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
     const size_t bstride = ((size_t)p.tile_elems_alloc * sizeof(W) + 15) / 16 * 16 / sizeof(W);
 
     if (tid < 32)
-        for (uint32_t j = 0; j < S && j < cnt; ++j) decode_tile(p, first + j * step, s_base, s_valid, (int)j);
+        for (uint32_t j = 0; j < S && j < cnt; ++j) decode_tile(p, sa, first + j * step, s_base, s_valid, (int)j);
     __syncthreads();
     auto limits = [&](uint32_t slot, int ph, Lim &lim) -> uint32_t {
         const uint32_t va = s_valid[slot][0], vc = s_valid[slot][1];
@@ -488,7 +497,7 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
         if constexpr (ASYNC) cp_async_commit();
     }
     for (uint32_t k = 0; k < cnt; ++k) {
-        if (tid < 32 && k + S < cnt) decode_tile(p, first + (k + S) * step, s_base, s_valid, (int)((k + S) % R));
+        if (tid < 32 && k + S < cnt) decode_tile(p, sa, first + (k + S) * step, s_base, s_valid, (int)((k + S) % R));
         if constexpr (ASYNC) cp_async_wait_pending(S - 1);
         __syncthreads();
         W *b = buf0 + (k % S) * bstride;
@@ -503,6 +512,9 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
         if (k + S < cnt) load(k + S, b);
         if constexpr (ASYNC) cp_async_commit();
     }
+    // peer stores of a sharded plan: performed system-wide before the grid
+    // retires, so the exchange's completion barrier orders them
+    if (p.nshards > 1) __threadfence_system();
 }
 
 
@@ -547,7 +559,8 @@ __device__ __forceinline__ void bulk_g2s(void *sdst, const void *gsrc, uint32_t 
 }
 
 template <typename W>
-__device__ __forceinline__ void tile_body_bulk(const TileParams &p, const W *__restrict__ src, W *__restrict__ dst) {
+__device__ __forceinline__ void tile_body_bulk(const TileParams &p, const W *__restrict__ src, W *__restrict__ dst,
+                                               const ShardArgs &sa) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
     __shared__ int64_t s_base[kMaxStages][2];
@@ -605,7 +618,7 @@ __device__ __forceinline__ void tile_body_bulk(const TileParams &p, const W *__r
         for (uint32_t k = 0; k < cnt; ++k) {
             const uint32_t st = k % S;
             if (k >= S) mbar_wait(&empty[st], ((k / S) - 1) & 1);
-            decode_tile(p, first + k * step, s_base, s_valid, (int)st);
+            decode_tile(p, sa, first + k * step, s_base, s_valid, (int)st);
             __syncwarp();
             const int64_t sb = s_base[st][0];
             const uint32_t va = s_valid[st][0], vc = s_valid[st][1];
@@ -664,6 +677,7 @@ __device__ __forceinline__ void tile_body_bulk(const TileParams &p, const W *__r
         __syncwarp();
         if ((tid & 31) == 0) mbar_arrive(&empty[st]);
     }
+    if (p.nshards > 1) __threadfence_system();
 }
 
 }  // namespace vpg

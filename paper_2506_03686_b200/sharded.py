@@ -31,12 +31,14 @@ inject the oracle to exercise the exchange logic with the gloo backend.
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass
 
 from .core import LayoutError
 
-__all__ = ["ShardPlan", "plan_sharded", "permute_sharded", "shard_bounds"]
+__all__ = ["ShardPlan", "plan_sharded", "permute_sharded", "shard_bounds", "ShardExchange", "emulate_fused",
+           "fused_supported"]
 
 
 def _lead_split(shape, G):
@@ -210,19 +212,32 @@ def shard_bounds(numel, G, r):
     return r * per, (r + 1) * per
 
 
-def permute_sharded(local_in, global_shape, axes, group=None, local_permute=None, plan=None):
+def permute_sharded(local_in, global_shape, axes, group=None, local_permute=None, plan=None,
+                    method: str = "alltoall"):
     """Permute a tensor sharded across the ranks of `group`.
 
     local_in: this rank's contiguous input shard (any shape, numel N/G).
     Returns this rank's contiguous output shard, shaped as the local output
     (output axes beyond the rank-indexing ones).  Collective: every rank of
     the group must call it with the same shape/axes.
+
+    method: "alltoall" -- P1 permute -> all_to_all_single -> P2 permute;
+    "fused" -- one exchange kernel per rank storing into the peers' output
+    shards (ShardExchange; the result is the exchange's buffer, overwritten
+    by the next fused call with the same arguments); "auto" -- fused when
+    every destination run is at least 128 bytes (fused_supported).
     """
     import torch
     import torch.distributed as dist
 
     G = dist.get_world_size(group) if dist.is_initialized() else 1
     r = dist.get_rank(group) if dist.is_initialized() else 0
+    if method not in ("alltoall", "fused", "auto"):
+        raise ValueError(f"unknown method {method!r}")
+    if method != "alltoall" and local_permute is None and local_in.is_cuda:
+        if method == "fused" or fused_supported(global_shape, axes, local_in.element_size(), G):
+            ex = _exchange_for(tuple(global_shape), tuple(axes), local_in.dtype, local_in.device, group)
+            return ex(local_in)
     sp = plan or plan_sharded(global_shape, axes, G)
     if local_permute is None:
         from .api import permute as local_permute  # GPU kernels; no CPU fallback
@@ -278,4 +293,169 @@ def emulate_sharded(x_flat, global_shape, axes, G, local_permute=None):
                 parts.append(packed[r][off:off + sc[s]])
         got = torch.cat(parts).reshape(s2)
         outs.append(local_permute(got, a2).reshape(sp.local_out_shape()))
+    return outs
+
+
+# ------------------------------------------------------------------ fused exchange (K5)
+MIN_FUSED_RUN_BYTES = 128      # K5 when destination runs are >= 128 B
+
+
+def _programs(global_shape, axes, elem_bytes, G, ranks, jit=None):
+    from .api import build_sharded_program
+    from .core import TensorLayout, from_numpy_convention
+
+    lay = TensorLayout.from_shape(tuple(global_shape), elem_bytes)
+    pm = from_numpy_convention(tuple(axes))
+    return [build_sharded_program(lay, pm, G, r, jit=jit) for r in ranks]
+
+
+def fused_supported(global_shape, axes, elem_bytes, G) -> bool:
+    """True when the fused exchange plans and its destination runs are at
+    least MIN_FUSED_RUN_BYTES (same answer on every rank: the tile geometry
+    does not depend on the shard index)."""
+    try:
+        (p,) = _programs(global_shape, axes, elem_bytes, G, [0])
+    except LayoutError:
+        return False
+    return p.metadata["dst_run"] * elem_bytes >= MIN_FUSED_RUN_BYTES
+
+
+class ShardExchange:
+    """Fused sharded permutation for one process per GPU.
+
+    Every rank owns one output shard buffer; the buffers are exported with
+    CUDA IPC and mapped into every other rank (NVLink/NVSwitch peer memory).
+    A call runs ONE kernel per rank (vpg_permute_sharded): it reads the
+    local input shard tile by tile and stores each tile straight into the
+    output shard that owns it -- one HBM read, one write (local or remote),
+    no staging buffers and no all-to-all.  Two stream-ordered barriers order
+    the exchange: before (every output buffer is free) and after (every
+    rank's stores have landed).  With NCCL they are one-element all-reduces
+    on the current stream; with gloo (CPU transport, tests) the stream is
+    synchronised and the group barrier runs on the host.
+
+    The result is a view of this rank's output buffer, overwritten by the
+    next call; copy it to keep it.  Collective: all ranks construct and call
+    it with the same arguments."""
+
+    def __init__(self, global_shape, axes, dtype, group=None, device=None, jit=None):
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+
+        self.group = group
+        self.G = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.dtype = dtype
+        es = torch.empty((), dtype=dtype).element_size()
+        (self.program,) = _programs(global_shape, axes, es, self.G, [self.rank], jit=jit)
+        self.splan = plan_sharded(global_shape, axes, self.G)
+        self.local_numel = self.splan.local_numel
+        self.out = torch.empty(self.local_numel, dtype=dtype, device=self.device)
+        self.backend = dist.get_backend(group) if dist.is_initialized() else None
+        self._flag = torch.zeros(1, dtype=torch.float32, device=self.device)
+        self._imported = []
+        L = _lib.lib()
+        mine = (self.rank, bytes(0), 0)
+        if self.G > 1:
+            h = ctypes.create_string_buffer(_lib.VPG_IPC_HANDLE_BYTES)
+            off = ctypes.c_uint64(0)
+            with torch.cuda.device(self.device):
+                _check_ipc(L.vpg_ipc_export(ctypes.c_void_p(self.out.data_ptr()), h, ctypes.byref(off)))
+            mine = (self.rank, h.raw, off.value)
+            allh = [None] * self.G
+            dist.all_gather_object(allh, mine, group=group)
+        else:
+            allh = [mine]
+        self.peers = []
+        with torch.cuda.device(self.device):
+            for q, hraw, off in sorted(allh):
+                if q == self.rank:
+                    self.peers.append(self.out.data_ptr())
+                    continue
+                ptr = ctypes.c_void_p()
+                buf = ctypes.create_string_buffer(hraw, _lib.VPG_IPC_HANDLE_BYTES)
+                _check_ipc(L.vpg_ipc_import(buf, ctypes.c_uint64(off), ctypes.byref(ptr)))
+                self.peers.append(ptr.value)
+                self._imported.append(ptr.value)
+
+    def _barrier(self):
+        import torch
+        import torch.distributed as dist
+
+        if self.G == 1:
+            return
+        if self.backend == "nccl":
+            dist.all_reduce(self._flag, group=self.group)        # device-side, stream-ordered
+        else:
+            torch.cuda.current_stream(self.device).synchronize()
+            dist.barrier(group=self.group)
+
+    def __call__(self, local_in, stream=None):
+        import torch
+
+        from .api import launch_sharded
+
+        if local_in.numel() != self.local_numel or local_in.dtype != self.dtype:
+            raise LayoutError(f"rank {self.rank}: expected {self.local_numel} elements of {self.dtype}")
+        if local_in.device != self.device or not local_in.is_contiguous():
+            raise LayoutError("input shard must be a contiguous tensor on the exchange's device")
+        st = stream or torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(st):
+            self._barrier()
+            launch_sharded(self.program, local_in.data_ptr(), self.peers, ctypes.c_void_p(st.cuda_stream))
+            self._barrier()
+        return self.out.view(self.splan.local_out_shape())
+
+    def close(self):
+        from . import _lib
+
+        L = _lib.lib()
+        for p in self._imported:
+            L.vpg_ipc_release(ctypes.c_void_p(p))
+        self._imported = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _check_ipc(status):
+    from . import _lib
+
+    if status != _lib.VPG_OK:
+        raise RuntimeError(f"CUDA IPC: {_lib.last_error()}")
+
+
+_exchanges: dict = {}
+
+
+def _exchange_for(shape, axes, dtype, device, group):
+    key = (shape, axes, dtype, str(device), id(group))
+    ex = _exchanges.get(key)
+    if ex is None:
+        ex = _exchanges[key] = ShardExchange(shape, axes, dtype, group=group, device=device)
+    return ex
+
+
+def emulate_fused(x_flat, global_shape, axes, G, jit=None):
+    """Run the G exchange kernels of the fused path on ONE device (virtual
+    ranks, output shards as local buffers; every kernel is independent).
+    Returns the list of per-rank output shards (flat)."""
+    import torch
+
+    from .api import launch_sharded
+
+    n = x_flat.numel()
+    progs = _programs(global_shape, axes, x_flat.element_size(), G, range(G), jit=jit)
+    outs = [torch.empty(n // G, dtype=x_flat.dtype, device=x_flat.device) for _ in range(G)]
+    ptrs = [o.data_ptr() for o in outs]
+    st = torch.cuda.current_stream(x_flat.device)
+    for r in range(G):
+        lo, hi = shard_bounds(n, G, r)
+        launch_sharded(progs[r], x_flat[lo:hi].data_ptr(), ptrs, ctypes.c_void_p(st.cuda_stream))
     return outs

@@ -58,7 +58,9 @@ class TileParams(ctypes.Structure):
                 ("run_bytes", ctypes.c_uint32), ("run_unit_bytes", ctypes.c_uint32),
                 ("rdims", PhaseDim * MAXPD),
                 ("ph", PhaseDesc * 2), ("grid", GridDigit * MAXR), ("off_buf", ctypes.c_uint32),
-                ("nbuf", ctypes.c_uint32), ("persistent", ctypes.c_uint32), ("smem_bytes", ctypes.c_uint32)]
+                ("nbuf", ctypes.c_uint32), ("persistent", ctypes.c_uint32), ("smem_bytes", ctypes.c_uint32),
+                ("nshards", ctypes.c_uint32), ("tile_begin", ctypes.c_uint32), ("src_bias", ctypes.c_int64),
+                ("shard_elems", ctypes.c_int64)]
 
 
 def tile_params(program) -> TileParams:
@@ -114,16 +116,26 @@ def check_layout(tp: TileParams, E: int) -> None:
         raise SimError("more dynamic smem than a CTA can have")
 
 
-def simulate(program, src_words: np.ndarray, threads: int | None = None) -> np.ndarray:
-    """Replay the tile kernel on host words; returns the destination words."""
+def simulate(program, src_words: np.ndarray, threads: int | None = None, shard_out=None):
+    """Replay the tile kernel on host words; returns the destination words.
+
+    Sharded exchange plans: ``src_words`` is the plan's input shard and
+    ``shard_out = (dsts, counts)`` holds every output shard and its
+    per-element write counters, updated in place (the caller checks the
+    coverage after replaying every rank)."""
     tp = tile_params(program)
     check_layout(tp, program.layout.elem_width)
     E = program.layout.elem_width
     NT = threads or program.metadata["threads"]
     n = tp.n_elems
     assert src_words.size == n
-    dst = np.full(n, np.iinfo(np.uint64).max if src_words.dtype == np.uint64 else 0, dtype=src_words.dtype)
-    written = np.zeros(n, dtype=np.int32)
+    sharded = shard_out is not None
+    if sharded:
+        dsts, counts = shard_out
+        assert len(dsts) == tp.nshards and all(d.size == tp.shard_elems for d in dsts)
+    else:
+        dst = np.full(n, np.iinfo(np.uint64).max if src_words.dtype == np.uint64 else 0, dtype=src_words.dtype)
+        written = np.zeros(n, dtype=np.int32)
     alloc = tp.tile_elems_alloc
     tid = np.arange(NT, dtype=np.int64)
     parts = []
@@ -138,15 +150,24 @@ def simulate(program, src_words: np.ndarray, threads: int | None = None) -> np.n
         # tile decode (decode_tile)
         sb = db = 0
         va, vc = tp.e_a, tp.e_c
+        tg_ = t + tp.tile_begin
         for i in range(tp.ngrid):
             gd = tp.grid[i]
-            cdig = (t // gd.cum.d) % gd.ext.d
+            cdig = (tg_ // gd.cum.d) % gd.ext.d
             sb += cdig * gd.src_stride
             db += cdig * gd.dst_stride
             if i == tp.grid_a:
                 va = min(tp.e_a, tp.d_a - cdig * tp.e_a)
             if i == tp.grid_c:
                 vc = min(tp.e_c, tp.d_c - cdig * tp.e_c)
+        if sharded:
+            q = db // tp.shard_elems
+            sb -= tp.src_bias
+            db -= q * tp.shard_elems
+            dst, written = dsts[q], counts[q]
+            dbound = tp.shard_elems
+        else:
+            dbound = n
         full = va == tp.e_a and vc == tp.e_c
         lim = (va, vc)
         smem = np.zeros(alloc + 64, dtype=src_words.dtype)
@@ -220,15 +241,34 @@ def simulate(program, src_words: np.ndarray, threads: int | None = None) -> np.n
                             for j in range(V):
                                 _chk(spx + j, alloc, "W smem")
                                 dd = gabs + j * d.vstride
-                                _chk(dd, n, "W global")
+                                _chk(dd, dbound, "W global")
                                 if not smem_valid[spx + j].all():
                                     raise SimError(f"W reads smem never written (tile {t})")
                                 dst[dd] = smem[spx + j]
                                 written[dd] += 1
+    if sharded:
+        return dsts
     if (written != 1).any():
         bad = np.nonzero(written != 1)[0][:5]
         raise SimError(f"destination elements written {written[bad]} times at {bad}")
     return dst
+
+
+def simulate_exchange(programs, src_words: np.ndarray) -> np.ndarray:
+    """Replay every rank's exchange kernel; returns the concatenated output
+    shards after checking that each output element was written exactly once."""
+    tp0 = tile_params(programs[0])
+    G, S = tp0.nshards, tp0.shard_elems
+    fill = np.iinfo(np.uint64).max if src_words.dtype == np.uint64 else 0
+    dsts = [np.full(S, fill, dtype=src_words.dtype) for _ in range(G)]
+    counts = [np.zeros(S, dtype=np.int32) for _ in range(G)]
+    for r, prog in enumerate(programs):
+        simulate(prog, src_words[r * S:(r + 1) * S], shard_out=(dsts, counts))
+    c = np.concatenate(counts)
+    if (c != 1).any():
+        bad = np.nonzero(c != 1)[0][:5]
+        raise SimError(f"destination elements written {c[bad]} times at {bad}")
+    return np.concatenate(dsts)
 
 
 def _chk(idx, bound, what):

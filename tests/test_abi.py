@@ -36,7 +36,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_version_and_last_error():
     L = _lib.lib()
-    assert L.vpg_version() == 1
+    assert L.vpg_version() == 2
     rank, d, s = _lib.arrays((3, 2), (0, 0))
     p = ctypes.c_void_p()
     assert L.vpg_plan_create(rank, d, s, 4, 0, ctypes.byref(p)) == _lib.VPG_EINVAL
@@ -88,3 +88,23 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cpp", ".h")):
                 text = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in text and "from oracle" not in text, f
+
+
+def test_sharded_plan_errors_without_gpu():
+    """Sharded plans are created host-side; bad shard arguments and
+    non-sharding shapes fail with the documented statuses."""
+    import ctypes
+
+    L = _lib.lib()
+    rank, d, s = _lib.arrays((4, 8), (1, 0))
+    p = ctypes.c_void_p()
+    assert L.vpg_plan_create_sharded(rank, d, s, 4, 0, 2, 2, ctypes.byref(p)) == _lib.VPG_EINVAL
+    assert L.vpg_plan_create_sharded(rank, d, s, 4, 0, 0, 0, ctypes.byref(p)) == _lib.VPG_EINVAL
+    assert L.vpg_plan_create_sharded(rank, d, s, 4, 0, 3, 0, ctypes.byref(p)) == _lib.VPG_EUNSUPPORTED
+    assert "cannot shard" in _lib.last_error()
+    rank, d, s = _lib.arrays((32, 16), (1, 0))
+    assert L.vpg_plan_create_sharded(rank, d, s, 4, 0, 2, 1, ctypes.byref(p)) == _lib.VPG_OK
+    # ordinary entry points refuse a sharded plan
+    assert L.vpg_permute(p, ctypes.c_void_p(16), ctypes.c_void_p(4096), None) == _lib.VPG_EINVAL
+    assert "vpg_permute_sharded" in _lib.last_error()
+    L.vpg_plan_destroy(p)

@@ -252,6 +252,8 @@ def test_autotune_candidates_are_exact(cuda):
     import torch
 
     import paper_2506_03686_b200 as vp
+    from paper_2506_03686_b200.api import execute_device
+
     shape, axes = (96, 70, 130), (2, 0, 1)
     lay, pm = vp.TensorLayout.from_shape(shape, 4), vp.from_numpy_convention(axes)
     x = np.random.default_rng(3).integers(0, 2**31, size=shape, dtype=np.int32)

@@ -9,7 +9,7 @@ import pytest
 
 import oracle
 import paper_2506_03686_b200 as vp
-from tests.sim_tile import simulate
+from tests.sim_tile import simulate, simulate_exchange
 
 
 def _run(shape, axes, E, rng, **kw):
@@ -73,3 +73,49 @@ def test_sim_bulk_mode(monkeypatch):
         seen += "TMA bulk" in p.text
     vp.program_cache_clear()
     assert seen >= 3
+
+
+# ------------------------------------------------------------ fused sharded exchange
+EXCHANGE_CASES = [
+    ((8, 6, 16, 4), (2, 0, 3, 1)),
+    ((16, 12, 16, 8), (3, 1, 0, 2)),
+    ((4, 64, 128), (2, 1, 0)),
+    ((8, 40, 32), (0, 2, 1)),
+    ((16, 6, 10, 8), (3, 2, 1, 0)),
+    ((8, 8, 24, 10), (1, 3, 0, 2)),
+    ((32, 5, 7, 16), (3, 1, 2, 0)),
+    ((8, 3, 64, 64), (2, 3, 1, 0)),
+    ((12, 2, 12, 8, 6, 6), (5, 0, 1, 3, 2, 4)),
+    ((2, 2, 2, 2, 2), (2, 0, 3, 4, 1)),
+    ((8, 6, 8), (0, 1, 2)),
+    ((2, 16, 6, 16, 4, 8), (3, 2, 0, 1, 4, 5)),
+    ((12, 12, 4), (1, 2, 0)),
+    ((12, 2, 4, 16), (3, 2, 1, 0)),
+    ((2,) * 12, (11, 4, 10, 1, 2, 7, 6, 0, 3, 9, 8, 5)),   # innermost source dim indexes the output shard
+]
+
+
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+@pytest.mark.parametrize("E", [4, 8])
+def test_sim_fused_exchange(G, E):
+    """Every rank's exchange kernel reads only its input shard and, together,
+    they write each output element exactly once with the permuted value."""
+    from paper_2506_03686_b200.sharded import _programs
+    from tests.golden.pattern import golden_pattern
+
+    done = 0
+    for shape, axes in EXCHANGE_CASES:
+        try:
+            progs = _programs(shape, axes, E, G, range(G))
+        except vp.LayoutError:
+            continue
+        n = int(np.prod(shape))
+        words = golden_pattern(n, E)
+        got = simulate_exchange(progs, words)
+        want = np.ascontiguousarray(np.transpose(words.reshape(shape), axes)).reshape(-1)
+        assert np.array_equal(got, want), (shape, axes, G)
+        for r, p in enumerate(progs):
+            m = p.metadata
+            assert m["shards"] == G and m["shard_index"] == r
+        done += 1
+    assert done >= (len(EXCHANGE_CASES) - 1 if G == 1 else 3)
