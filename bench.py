@@ -378,13 +378,17 @@ NVLINK_GBS = 770.0   # measured peer copy per direction per GPU (B200_PROFILING.
 
 
 def bench_sharded(args, torch, base, config, peak, peak_kind):
-    """cfg5 sharded over the torchrun ranks (strong scaling): P1 permute ->
-    NCCL all_to_all_single -> P2 permute per step; device time max over ranks."""
+    """cfg5 sharded over the torchrun ranks (strong scaling); device time max
+    over ranks.  Per step either the fused exchange (one tile kernel per rank
+    storing into the owning peers' output shards over NVLink, ShardExchange)
+    or P1 permute -> NCCL all_to_all_single -> P2 permute; --shard-method
+    auto picks the fused kernel when its destination runs are >= 128 B."""
     import numpy as np
     import torch.distributed as dist
 
     from paper_2506_03686_b200 import permute
-    from paper_2506_03686_b200.sharded import permute_sharded, plan_sharded, shard_bounds
+    from paper_2506_03686_b200.sharded import (ShardExchange, fused_supported, permute_sharded, plan_sharded,
+                                               shard_bounds)
     from paper_2506_03686_b200.workloads import CONFIGS, make_input_slice
 
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -398,7 +402,15 @@ def bench_sharded(args, torch, base, config, peak, peak_kind):
     host_in = torch.from_numpy(make_input_slice(wl, lo, hi).reshape(-1).view(np.uint8)).pin_memory()
     x = host_in.to(dev).view(torch.int64)
     st = torch.cuda.current_stream()
-    step = lambda: permute_sharded(x, wl.shape, wl.axes, local_permute=permute, plan=sp)  # noqa: E731
+    method = args.shard_method
+    if method == "auto":
+        method = "fused" if fused_supported(wl.shape, wl.axes, wl.elem_bytes, G) else "alltoall"
+    if method == "fused":
+        ex = ShardExchange(wl.shape, wl.axes, torch.int64, device=dev)
+        run = ex
+    else:
+        run = lambda xin: permute_sharded(xin, wl.shape, wl.axes, local_permute=permute, plan=sp)  # noqa: E731
+    step = lambda: run(x)  # noqa: E731
     out = None
     for _ in range(args.warmup):
         out = step()          # same allocation pattern as the timed loop (two live outputs)
@@ -434,7 +446,7 @@ def bench_sharded(args, torch, base, config, peak, peak_kind):
         dist.barrier()
         t0 = time.perf_counter()
         xin = host_in.to(dev, non_blocking=True).view(torch.int64)
-        y = permute_sharded(xin, wl.shape, wl.axes, local_permute=permute, plan=sp)
+        y = run(xin)
         host_out.copy_(y.reshape(-1).view(torch.uint8), non_blocking=True)
         torch.cuda.synchronize()
         t1 = time.perf_counter()
@@ -453,13 +465,16 @@ def bench_sharded(args, torch, base, config, peak, peak_kind):
             "value": round(gbs, 2), "ms_per_step": ms, "config": config,
             "e2e": {"value": round(wl.algorithmic_bytes / e2e_t.item() / 1e9, 3), "unit": "GB/s",
                     "h2d_bytes_per_step": shard_bytes * G, "d2h_bytes_per_step": shard_bytes * G,
-                    "api": "paper_2506_03686_b200.sharded.permute_sharded on pinned host shards"},
-            "gpu_launches": (2 if G > 1 else 1) * args.steps,
+                    "api": ("paper_2506_03686_b200.sharded.ShardExchange" if method == "fused" else
+                            "paper_2506_03686_b200.sharded.permute_sharded") + " on pinned host shards"},
+            "gpu_launches": (1 if method == "fused" or G == 1 else 2) * args.steps,
+            "shard_method": method,
             "roofline": {"bound": bound, "achieved": round(gbs, 2), "peak": round(roof_gbs, 1),
                          "peak_kind": f"min over HBM ({peak_kind} {peak} GB/s per GPU) and NVLink "
                                       f"({NVLINK_GBS} GB/s per direction per GPU) time bounds",
                          "unit": "GB/s", "frac": round(gbs / roof_gbs, 4), "traffic": None,
-                         "kernel": "tile (P1/P2) + NCCL all_to_all_single"},
+                         "kernel": "fused exchange tile kernel (peer stores over NVLink)" if method == "fused"
+                         else "tile (P1/P2) + NCCL all_to_all_single"},
             "parity_sampled": bool(ok.item()),
             "clocks": clk.summary(),
             "shard_plan": sp.describe()[:400],
@@ -512,6 +527,8 @@ def main(argv=None):
     ap.add_argument("--no-extra", action="store_true", help="skip cfg1-4 side measurements")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-tune", action="store_true", help="skip measured planning (autotune)")
+    ap.add_argument("--shard-method", default="auto", choices=["auto", "fused", "alltoall"],
+                    help="N>1: fused exchange kernel or P1 -> all-to-all -> P2")
     ap.add_argument("--cpu-threads", type=int, default=None)
     ap.add_argument("--sharded", action="store_true",
                     help="use the sharded (torchrun/NCCL) code path even with one rank")
