@@ -68,13 +68,41 @@ struct ThreadPart {
     bool active;
 };
 
+// VPG_HINTS (specialised kernels, experiments): bit 0 = source reads with an
+// L2 evict_first policy, bit 1 = streaming (.cs) destination stores.
+#ifndef VPG_HINTS
+#define VPG_HINTS 0
+#endif
+
 template <int E>
 __device__ __forceinline__ void cp_async(void *sp, const void *gp) {
     const uint32_t s = (uint32_t)__cvta_generic_to_shared(sp);
+#if VPG_HINTS & 1
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+    if constexpr (E == 16)
+        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gp), "l"(pol)
+                     : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], %2, %3;\n" ::"r"(s), "l"(gp), "n"(E),
+                     "l"(pol)
+                     : "memory");
+#else
     if constexpr (E == 16)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gp) : "memory");
     else
         asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gp), "n"(E) : "memory");
+#endif
+}
+
+template <typename W>
+__device__ __forceinline__ void st_out(W *p, const W &v) {
+#if VPG_HINTS & 2
+    if constexpr (sizeof(W) >= 4) __stcs(p, v);
+    else *p = v;
+#else
+    *p = v;
+#endif
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
@@ -295,14 +323,14 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
                     for (int u = 0; u < U; ++u) {
                         const W *w = reinterpret_cast<const W *>(&v[u]);
 #pragma unroll
-                        for (int j = 0; j < V; ++j) gp[u * g_in + j * vs] = w[j];
+                        for (int j = 0; j < V; ++j) st_out(gp + u * g_in + j * vs, w[j]);
                     }
                 } else {
                     W v[U];
 #pragma unroll
                     for (int u = 0; u < U; ++u) v[u] = sp[u * s_in + ((hh + u * h_in) & hmask)];
 #pragma unroll
-                    for (int u = 0; u < U; ++u) gp[u * g_in] = v[u];
+                    for (int u = 0; u < U; ++u) st_out(gp + u * g_in, v[u]);
                 }
                 gp += U * g_in;
                 sp += U * s_in;
@@ -313,7 +341,7 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
                     uint4 v = *reinterpret_cast<const uint4 *>(sp);
                     const W *w = reinterpret_cast<const W *>(&v);
 #pragma unroll
-                    for (int j = 0; j < V; ++j) gp[j * vs] = w[j];
+                    for (int j = 0; j < V; ++j) st_out(gp + j * vs, w[j]);
                 } else {
                     *gp = sp[hh & hmask];
                 }
@@ -330,7 +358,7 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
                         uint4 v = *reinterpret_cast<const uint4 *>(sp);
                         const W *w = reinterpret_cast<const W *>(&v);
 #pragma unroll
-                        for (int j = 0; j < V; ++j) gp[j * vs] = w[j];
+                        for (int j = 0; j < V; ++j) st_out(gp + j * vs, w[j]);
                     } else {
                         *gp = sp[hh & hmask];
                     }
