@@ -197,3 +197,31 @@ def test_sharded_ranks_with_gpu_kernels(cuda, world):
         p.join(timeout=120)
     for rank, errs in res:
         assert not errs, (rank, errs)
+
+
+@pytest.mark.parametrize("dtype_name,jit", [("uint8", False), ("int16", False), ("int32", True), ("int32", False),
+                                            ("float64", True), ("complex128", False)])
+def test_fused_exchange_word_sizes(cuda, dtype_name, jit):
+    """1/2/4/8/16-byte words through both the specialised and the
+    ahead-of-time exchange kernels (emulated ranks on one device)."""
+    import torch
+
+    import paper_2506_03686_b200 as vp
+    from paper_2506_03686_b200.sharded import emulate_fused
+
+    tdt = getattr(torch, dtype_name)
+    ran = 0
+    for ci, (shape, axes) in enumerate(FUSED_CASES):
+        n = int(np.prod(shape))
+        g = torch.Generator().manual_seed(ci)
+        x = (torch.randint(-100, 100, (n,), generator=g).to(tdt) if not tdt.is_complex
+             else torch.randn(n, dtype=tdt, generator=g))
+        for G in (2, 4):
+            try:
+                outs = emulate_fused(x.cuda(), shape, axes, G, jit=jit)
+            except vp.LayoutError:
+                continue
+            got = torch.cat(outs).cpu()
+            assert torch.equal(got, x.reshape(shape).permute(axes).reshape(-1)), (shape, axes, G)
+            ran += 1
+    assert ran >= 4
