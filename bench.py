@@ -281,6 +281,23 @@ def sample_parity(torch, x, y, shape, axes, nsamp=1 << 20, seed=0):
     return bool(torch.equal(y[idx], x[src]))
 
 
+def _numpy_baseline(cfg):
+    """The paper's CPU comparator (SURVEY.md §8(d) secondary line): numpy
+    transpose + contiguous copy of the full workload, one run, 1 thread."""
+    import numpy as np
+
+    from paper_2506_03686_b200.workloads import CONFIGS, make_input
+
+    wl = CONFIGS[cfg]
+    x = make_input(wl, threads=8)
+    t0 = time.perf_counter()
+    y = np.ascontiguousarray(np.transpose(x, wl.axes))
+    dt = time.perf_counter() - t0
+    del x, y
+    return {"value": round(wl.algorithmic_bytes / dt / 1e9, 3), "unit": "GB/s", "cores": 1,
+            "sample": f"np.ascontiguousarray(np.transpose(x, axes)) on the full {cfg} input, 1 run ({dt:.2f} s)"}
+
+
 # ---------------------------------------------------------------- our arm
 def bench_one_gpu(args, torch, cfg, with_e2e, peak):
     from paper_2506_03686_b200 import TensorLayout, build_program, execute, from_numpy_convention
@@ -630,6 +647,7 @@ def main(argv=None):
         except Exception as e:  # reported, not fatal
             cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {e}"}
+        cpu_numpy = _numpy_baseline(args.config)
     ms = main_res["ms_per_launch"]
     line = dict(base)
     line.update({
@@ -648,6 +666,7 @@ def main(argv=None):
                      "traffic": _traffic_from_profiles(args.config),
                      "kernel": f"{main_res['kernel']} ({args.config})"},
         "cpu_baseline": cpu,
+        "cpu_numpy": None if args.no_cpu else cpu_numpy,
         "clocks": clk.summary(),
         "parity_sampled": main_res["parity_sampled"],
         "configs": extra,
