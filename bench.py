@@ -207,10 +207,14 @@ def _cpu_model():
     return "unknown"
 
 
-def run_reference_cpu(cfg, steps, warmup, threads=None, x=None):
+def run_reference_cpu(cfg, steps, warmup, threads=None, x=None, private=None):
     """The reference's emitted CPU kernel, `threads` concurrent replicas.
 
-    Returns (GB/s, per-step seconds list, threads, target)."""
+    Each replica permutes its own copy of the input into its own output
+    (`private`, the default when host memory allows): replicas that share
+    one input in lockstep would serve each other's reads from the shared
+    L3 and overstate the host's throughput.
+    Returns (GB/s, per-step seconds list, threads, target, private)."""
     import numpy as np
 
     from oracle.refkernels import RefKernel
@@ -219,14 +223,21 @@ def run_reference_cpu(cfg, steps, warmup, threads=None, x=None):
     wl = CONFIGS[cfg]
     rk = RefKernel(cfg)
     ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    cap_mem = max(1, int(_mem_available() * 0.5 // max(rk.nbytes, 1)) - 1)
+    budget = int(_mem_available() * 0.5)
     if threads is None:
         threads = ncpu
-    threads = max(1, min(threads, ncpu, cap_mem, 64))
+    threads = max(1, min(threads, ncpu, 64))
+    if private is None:
+        private = 2 * threads * rk.nbytes <= budget
+    cap_mem = max(1, budget // max(rk.nbytes, 1) // (2 if private else 1) - 1)
+    threads = max(1, min(threads, cap_mem))
     if x is None:
         x = make_input(wl, threads=min(ncpu, 32))
-    src = rk.alloc()
-    src.data[:] = x.reshape(-1).view(np.uint8)
+    xb = x.reshape(-1).view(np.uint8)
+    srcs = [rk.alloc() for _ in range(threads if private else 1)]
+    for sb in srcs:
+        sb.data[:] = xb
+    src = srcs[0]
     outs = [rk.alloc() for _ in range(threads)]
     # parity of the baseline itself (cheap: numpy transpose comparison on a sample)
     rk.run_ptr(src.ptr, outs[0].ptr)
@@ -242,7 +253,7 @@ def run_reference_cpu(cfg, steps, warmup, threads=None, x=None):
             barrier.wait()
             if stop[0]:
                 return
-            rk.run_ptr(src.ptr, outs[i].ptr)
+            rk.run_ptr(srcs[i % len(srcs)].ptr, outs[i].ptr)
             barrier.wait()
 
     ts = [threading.Thread(target=worker, args=(i,), daemon=True) for i in range(threads)]
@@ -261,7 +272,7 @@ def run_reference_cpu(cfg, steps, warmup, threads=None, x=None):
     for t in ts:
         t.join()
     gbs = threads * wl.algorithmic_bytes / (sum(times) / len(times)) / 1e9
-    return gbs, times, threads, rk.target
+    return gbs, times, threads, rk.target, private
 
 
 def sample_parity(torch, x, y, shape, axes, nsamp=1 << 20, seed=0):
@@ -585,8 +596,8 @@ def main(argv=None):
     if args.impl == "reference":
         if rank != 0:
             return 0
-        gbs, times, threads, target = run_reference_cpu(args.config, args.steps, args.warmup,
-                                                        threads=args.cpu_threads)
+        gbs, times, threads, target, private = run_reference_cpu(args.config, args.steps, args.warmup,
+                                                                 threads=args.cpu_threads)
         line = dict(base)
         line.update({
             "impl": "reference",
@@ -596,7 +607,8 @@ def main(argv=None):
             "cpu_baseline": {
                 "value": gbs, "unit": "GB/s", "cores": threads, "kind": "reference",
                 "sample": f"{threads} concurrent full {args.config} permutations per step "
-                          f"(reference emitted {target} kernel, shared input, private outputs); "
+                          f"(reference emitted {target} kernel, "
+                          f"{'private inputs and outputs' if private else 'shared input, private outputs'}); "
                           f"host {_cpu_model()}, {os.cpu_count()} logical CPUs",
             },
             "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -640,10 +652,11 @@ def main(argv=None):
     cpu = None
     if not args.no_cpu:
         try:
-            gbs, times, threads, target = run_reference_cpu(args.config, 2, 1, threads=args.cpu_threads)
+            gbs, times, threads, target, private = run_reference_cpu(args.config, 2, 1, threads=args.cpu_threads)
             cpu = {"value": round(gbs, 2), "unit": "GB/s", "cores": threads, "kind": "reference",
                    "sample": f"{threads} concurrent full {args.config} permutations x 2 timed steps "
-                             f"(reference emitted {target} kernel); host {_cpu_model()}"}
+                             f"(reference emitted {target} kernel, "
+                             f"{'private inputs' if private else 'shared input'}); host {_cpu_model()}"}
         except Exception as e:  # reported, not fatal
             cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {e}"}
