@@ -540,8 +540,9 @@ def _execute_host(program: GpuProgram, input_buf, out=None, stream=None, blockin
 def permute(x, axes, out=None, stream=None):
     """``x.permute(axes).contiguous()`` on the GPU through libvpgpu.so.
 
-    ``x`` is a contiguous CUDA tensor; ``axes`` use the torch/numpy
-    convention (BASELINE.json's configs are stated this way)."""
+    ``x`` is a CUDA tensor, contiguous or a permuted view of contiguous
+    memory; ``axes`` use the torch/numpy convention (BASELINE.json's configs
+    are stated this way)."""
     torch = _torch()
     if not isinstance(x, torch.Tensor) or not x.is_cuda:
         raise LayoutError("permute needs a CUDA tensor (no CPU fallback)")
@@ -554,6 +555,37 @@ def permute(x, axes, out=None, stream=None):
     if x.dim() == 0:
         res = permute(x.reshape(1), (0,), stream=stream).reshape(())
         return res if out is None else out.copy_(res)
+    if not x.is_contiguous():
+        x, axes = _dense_base(torch, x, axes)
     layout = TensorLayout.from_shape(tuple(x.shape), x.element_size())
     prog = build_program(layout, from_numpy_convention(axes))
     return execute_device(prog, x, out=out, stream=stream)
+
+
+def _dense_base(torch, x, axes):
+    """A non-contiguous ``x`` that is a permuted view of dense memory
+    (``y.permute(p)``, ``y.transpose(i, j)``, ``y.mT``) is permuted from its
+    dense base with the composed axes: still one kernel, no copy.  Other
+    strided views raise LayoutError."""
+    dims = list(range(x.dim()))
+    # dense order: descending stride (size-1 dims anywhere; ties keep order)
+    order = sorted(dims, key=lambda d: (-x.stride(d) if x.shape[d] > 1 else 0, d))
+    order = [d for d in order if x.shape[d] > 1] + [d for d in order if x.shape[d] == 1]
+    expect = 1
+    for d in reversed(order):
+        if x.shape[d] > 1 and x.stride(d) != expect:
+            raise LayoutError("input must be contiguous or a permuted view of contiguous memory")
+        expect *= x.shape[d]
+    base = x.as_strided([x.shape[d] for d in order], _dense_strides([x.shape[d] for d in order]))
+    if not base.is_contiguous():
+        raise LayoutError("input must be contiguous or a permuted view of contiguous memory")
+    pos = {d: i for i, d in enumerate(order)}            # view dim d is base dim pos[d]
+    return base, tuple(pos[a] for a in axes)
+
+
+def _dense_strides(shape):
+    st, acc = [], 1
+    for n in reversed(shape):
+        st.append(acc)
+        acc *= n
+    return list(reversed(st))

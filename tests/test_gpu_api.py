@@ -274,3 +274,24 @@ def test_autotune_candidates_are_exact(cuda):
     assert vp.build_program(lay, pm, force="tile") is best
     assert np.array_equal(execute_device(best, xd).cpu().numpy(), want)
     assert best.metadata["tuned_ms"] > 0
+
+
+def test_permute_of_permuted_views(cuda):
+    """Permuted views of dense memory are permuted from their base with the
+    composed axes (one kernel); other strided views are rejected."""
+    import torch
+
+    import paper_2506_03686_b200 as vp
+    from paper_2506_03686_b200 import permute
+
+    base = torch.randint(-2**31, 2**31 - 1, (6, 1, 10, 12, 7), dtype=torch.int32, device="cuda")
+    rng = np.random.default_rng(4)
+    for _ in range(20):
+        p1 = tuple(int(a) for a in rng.permutation(5))
+        p2 = tuple(int(a) for a in rng.permutation(5))
+        v = base.permute(p1)
+        assert torch.equal(permute(v, p2), v.permute(p2).contiguous())
+    m = base.reshape(60, 84)
+    assert torch.equal(permute(m.mT, (1, 0)), m)
+    with pytest.raises(vp.LayoutError):
+        permute(base[:, :, ::2], (0, 1, 2, 3, 4))

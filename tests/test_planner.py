@@ -191,3 +191,23 @@ def test_tile_candidates_for_autotuning():
     assert _plan((64, 48, 80), (2, 0, 1), candidate=0).text == _plan((64, 48, 80), (2, 0, 1)).text
     with pytest.raises(LayoutError):
         _plan((6, 5), (1, 0), force="tile", candidate=200)
+
+
+def test_dense_base_of_permuted_views():
+    """permute() accepts permuted views of dense memory: the view is mapped
+    back to its dense base and the axes are composed (host logic only)."""
+    import torch
+
+    from paper_2506_03686_b200.api import _dense_base
+
+    base = torch.arange(6 * 1 * 10 * 12 * 7).reshape(6, 1, 10, 12, 7)
+    rng = np.random.default_rng(4)
+    for _ in range(200):
+        p1 = tuple(int(a) for a in rng.permutation(5))
+        p2 = tuple(int(a) for a in rng.permutation(5))
+        v = base.permute(p1)
+        b, ax = _dense_base(torch, v, p2)
+        assert b.is_contiguous() and b.data_ptr() == base.data_ptr()
+        assert torch.equal(b.permute(ax), v.permute(p2))
+    with pytest.raises(LayoutError):
+        _dense_base(torch, base[:, :, ::2], (0, 1, 2, 3, 4))
