@@ -116,14 +116,15 @@ def check_layout(tp: TileParams, E: int) -> None:
         raise SimError("more dynamic smem than a CTA can have")
 
 
-def simulate(program, src_words: np.ndarray, threads: int | None = None, shard_out=None):
+def simulate(program, src_words: np.ndarray, threads: int | None = None, shard_out=None, tp=None):
     """Replay the tile kernel on host words; returns the destination words.
 
     Sharded exchange plans: ``src_words`` is the plan's input shard and
     ``shard_out = (dsts, counts)`` holds every output shard and its
     per-element write counters, updated in place (the caller checks the
-    coverage after replaying every rank)."""
-    tp = tile_params(program)
+    coverage after replaying every rank).  ``tp`` replaces the plan's
+    parameter block (negative controls)."""
+    tp = tp if tp is not None else tile_params(program)
     check_layout(tp, program.layout.elem_width)
     E = program.layout.elem_width
     NT = threads or program.metadata["threads"]

@@ -231,3 +231,32 @@ def test_bulk_tma_mode(cuda, jit, monkeypatch):
         assert torch.equal(execute_device(prog, x), x.permute(axes).contiguous()), (shape, prog.text)
     program_cache_clear()
     assert seen >= 3
+
+
+def test_negative_controls(cuda):
+    """The parity checks are not vacuous: a kernel run with a different map,
+    or an output with one word changed, fails the same comparisons the
+    parity tests use (digest and oracle)."""
+    import oracle
+
+    cases = [c for c in golden()["cases"] if c["family"].startswith("campaign_") and c["n"] >= 256][:20]
+    assert cases
+    ran = 0
+    for c in cases:
+        data = golden_pattern(c["n"], c["elem"])
+        out, _ = gpu_permute_bytes(c["dims"], c["sigma"], c["elem"], data)
+        assert sha256(out) == c["sha256"]
+        flipped = out.copy()
+        flipped[len(flipped) // 2] ^= 1
+        assert sha256(flipped) != c["sha256"]
+        # a different (rotated) map over the same dims must not reproduce the digest
+        rot = tuple(c["sigma"][1:]) + (c["sigma"][0],)
+        want = oracle.naive_permute_c(data, c["dims"], c["sigma"]).reshape(-1).view(np.uint8)
+        other = oracle.naive_permute_c(data, c["dims"], rot).reshape(-1).view(np.uint8)
+        if np.array_equal(want, other):
+            continue                     # the rotated map is the same bijection here
+        wrong, _ = gpu_permute_bytes(c["dims"], rot, c["elem"], data)
+        assert sha256(wrong) != c["sha256"], c["name"]
+        assert not np.array_equal(wrong, want)
+        ran += 1
+    assert ran >= 10

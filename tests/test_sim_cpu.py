@@ -119,3 +119,36 @@ def test_sim_fused_exchange(G, E):
             assert m["shards"] == G and m["shard_index"] == r
         done += 1
     assert done >= (len(EXCHANGE_CASES) - 1 if G == 1 else 3)
+
+
+def test_sim_negative_controls():
+    """The checker is not vacuous (the reference's corrupted-table control,
+    test_emit.py:156-171): corrupting one stride or extent of a valid
+    parameter block is caught as an out-of-bounds access, a double write or
+    a wrong value."""
+    from tests.sim_tile import SimError, tile_params
+
+    shape, axes, E = (36, 40, 44), (2, 0, 1), 4
+    prog = vp.build_program(vp.TensorLayout.from_shape(shape, E), vp.from_numpy_convention(axes), force="tile")
+    n = prog.num_elements
+    words = np.arange(1, n + 1, dtype=np.uint32)
+    dims, sigma = oracle.from_numpy_axes(shape, axes)
+    want = oracle.naive_permute_c(words, dims, sigma)
+    assert np.array_equal(simulate(prog, words), want)
+    corruptions = []
+    tp = tile_params(prog)
+    for i in range(tp.ngrid):
+        corruptions.append(("grid dst_stride", lambda t, i=i: setattr(t.grid[i], "dst_stride", t.grid[i].dst_stride + 1)))
+        corruptions.append(("grid src_stride", lambda t, i=i: setattr(t.grid[i], "src_stride", t.grid[i].src_stride + 1)))
+    corruptions.append(("W inner stride", lambda t: setattr(t.ph[1], "g_in", t.ph[1].g_in + 1)))
+    corruptions.append(("R inner smem stride", lambda t: setattr(t.ph[0], "s_in", t.ph[0].s_in + 1)))
+    corruptions.append(("tile count", lambda t: setattr(t, "num_tiles", t.num_tiles - 1)))
+    assert len(corruptions) >= 5
+    for what, fn in corruptions:
+        bad = tile_params(prog)
+        fn(bad)
+        try:
+            got = simulate(prog, words, tp=bad)
+        except SimError:
+            continue
+        assert not np.array_equal(got, want), f"corruption of {what} went unnoticed"
