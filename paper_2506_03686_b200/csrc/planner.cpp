@@ -206,12 +206,11 @@ bool select_tile(const Problem &P, TileGeom &best, int pick = -1) {
     const int64_t maxT = std::max<int64_t>(P.budget / P.E, 64);
     bool found = false;
     best.cost = 1e300;
-    std::vector<TileGeom> all;   // every candidate, for VPG_TILE_PICK (tuning sweeps)
+    std::vector<TileGeom> all;   // every candidate, for candidate picks (autotuning, VPG_TILE_PICK)
     int64_t ext[kMaxRank];
     int64_t pre_s = 1;
     for (int a = 0; a < r && pre_s <= maxT; pre_s *= P.d[a], ++a) {
         for (int64_t ea : extent_candidates(P.d[a], maxT / pre_s)) {
-            int64_t pre_d = 1;
             for (int b = 0; b < r; ++b) {
                 for (int k = 0; k < r; ++k) ext[k] = 0;
                 for (int k = 0; k < a; ++k) ext[k] = P.d[k];
@@ -241,8 +240,6 @@ bool select_tile(const Problem &P, TileGeom &best, int pick = -1) {
                         found = true;
                     }
                 }
-                pre_d *= P.d[P.sigma[b]];
-                (void)pre_d;
             }
         }
     }
