@@ -94,6 +94,8 @@ def main():
     ap.add_argument("--labels", required=True)
     ap.add_argument("--launches", default=None)
     ap.add_argument("--round", default="r1")
+    ap.add_argument("--launch-cmd", default="python bench.py --steps 2 --warmup 3 --no-cpu")
+    ap.add_argument("--launch-note", default="")
     a = ap.parse_args()
     labels = a.labels.split(",")
     hdr, units, rows = raw_rows(a.rep)
@@ -123,13 +125,15 @@ def main():
            "126 MB L2 when the kernel ended (small configs); the flushed bench times include no such hits",
            "on the read side (inputs are evicted before every timed launch).", ""]
     if a.launches:
-        md += ["## Launch list of `python bench.py --steps 3 --warmup 3 --no-cpu` (device-time shares)", "",
+        md += [f"## Launch list of `{a.launch_cmd}` (device-time shares)", "",
                "| kernel | launches | total us | share |", "|---|---|---|---|"]
         for n, c, t, sh in launch_shares(a.launches):
             md.append(f"| `{n[:90]}` | {c} | {t:.1f} | {sh*100:.1f}% |")
         md.append("")
-        md.append("The flush kernels (torch fill/reduce) are outside the timed region; among the timed kernels the "
-                  "tile/rows kernels are the only ones launched.")
+        md.append("The flush kernels (torch fill/reduce) and the parity/comparator kernels (torch index, "
+                  "remainder, copy) are outside the timed region; inside it the tile/rows kernels are the only "
+                  "kernels launched (one per step).  The tile launches also include the untimed measured "
+                  "planning (autotune) and warm-ups.  " + (a.launch_note or ""))
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     with open(os.path.join(ROOT, "profiles", "ncu_summary.json"), "w") as f:
         json.dump(summ, f, indent=1)

@@ -1,0 +1,37 @@
+"""Launch each BASELINE config's kernel twice inside an NVTX range
+"capture", with the plans bench.py uses (measured planning), for ncu:
+
+  ncu --set full --clock-control none --import-source on --nvtx \
+      --nvtx-include "capture/" -o gpurun_out/full_rN python tools/profile_configs.py
+
+Order: cfg5, cfg4, cfg3, cfg1, cfg2 (labels for tools/ncu_summary.py)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2506_03686_b200 as vp  # noqa: E402
+from paper_2506_03686_b200.api import execute_device  # noqa: E402
+from paper_2506_03686_b200.workloads import CONFIGS  # noqa: E402
+
+ORDER = ["cfg5", "cfg4", "cfg3", "cfg1", "cfg2"]
+dev = torch.device("cuda", 0)
+runs = []
+for k in ORDER:
+    wl = CONFIGS[k]
+    prog = vp.build_program(vp.TensorLayout.from_shape(wl.shape, wl.elem_bytes), vp.from_numpy_convention(wl.axes),
+                            tune=True)
+    n = wl.numel * wl.elem_bytes
+    x = torch.randint(0, 255, (n,), dtype=torch.uint8, device=dev)
+    y = torch.empty_like(x)
+    execute_device(prog, x, out=y)          # compile/load outside the capture
+    runs.append((k, prog, x, y))
+    print(k, prog.kernel, prog.metadata["src_run"], prog.metadata["dst_run"], flush=True)
+torch.cuda.synchronize()
+torch.cuda.nvtx.range_push("capture")
+for k, prog, x, y in runs:
+    for _ in range(2):
+        execute_device(prog, x, out=y)
+torch.cuda.synchronize()
+torch.cuda.nvtx.range_pop()
