@@ -115,9 +115,13 @@ vpg_status vpg_permute(const vpg_plan *plan, const void *src, void *dst, void *c
 
 /* End-to-end variant over HOST buffers (the reference's execute() takes a host
  * buffer, vm.py:105-110): copies host_src -> dev_src, permutes into dev_dst,
- * copies dev_dst -> host_dst, all on `cuda_stream`; synchronises the stream
- * before returning.  Device buffers are caller-provided scratch of
- * num_elements*elem_bytes bytes each.  Pinned host memory gives full-rate copies. */
+ * copies dev_dst -> host_dst -- chunked and pipelined over the library's
+ * copy/compute streams for large tensors -- ordered after earlier work on
+ * `cuda_stream`, and synchronises that stream before returning.  Device
+ * buffers are caller-provided scratch of num_elements*elem_bytes bytes
+ * each; calls from several host threads may share them (the library orders
+ * every writer of a scratch buffer after its earlier readers).  Pinned host
+ * memory gives full-rate copies. */
 vpg_status vpg_permute_host(const vpg_plan *plan, const void *host_src, void *host_dst,
                             void *dev_src, void *dev_dst, void *cuda_stream);
 

@@ -120,23 +120,11 @@ vpg_status vpg_permute_host(const vpg_plan *plan, const void *host_src, void *ho
                             void *dev_dst, void *cuda_stream) {
     if (!plan || !host_src || !host_dst || !dev_src || !dev_dst) return fail(VPG_EINVAL, "null argument");
     if (plan->shards > 0) return fail(VPG_EINVAL, "sharded plans run through vpg_permute_sharded");
-    cudaStream_t st = (cudaStream_t)cuda_stream;
-    size_t nbytes = (size_t)plan->n * plan->elem_bytes;
-    {
-        std::string err;
-        vpg_status ps = vpg::permute_host_pipelined(plan, host_src, host_dst, dev_src, dev_dst, st, false, &err);
-        if (ps == VPG_OK) return VPG_OK;
-        if (ps != VPG_EUNSUPPORTED) return fail(ps, err);
-    }
-    cudaError_t e = cudaMemcpyAsync(dev_src, host_src, nbytes, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) return fail(VPG_ECUDA, std::string("H2D copy: ") + cudaGetErrorString(e));
-    vpg_status s = vpg_permute(plan, dev_src, dev_dst, cuda_stream);
-    if (s != VPG_OK) return s;
-    e = cudaMemcpyAsync(host_dst, dev_dst, nbytes, cudaMemcpyDeviceToHost, st);
-    if (e != cudaSuccess) return fail(VPG_ECUDA, std::string("D2H copy: ") + cudaGetErrorString(e));
-    e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) return fail(VPG_ECUDA, std::string("stream sync: ") + cudaGetErrorString(e));
-    return VPG_OK;
+    if (plan->n == 0) return VPG_OK;
+    std::string err;
+    vpg_status s = vpg::permute_host_pipelined(plan, host_src, host_dst, dev_src, dev_dst, (cudaStream_t)cuda_stream,
+                                               false, &err);
+    return s == VPG_OK ? s : fail(s, err);
 }
 
 vpg_status vpg_permute_host_async(const vpg_plan *plan, const void *host_src, void *host_dst, void *dev_src,

@@ -217,6 +217,11 @@ struct PendingOut {
 };
 std::vector<PendingOut> g_pending_out;
 
+// One call enqueues at a time: the scratch hazard events above are read and
+// re-recorded during the enqueue, so calls from several host threads that
+// share scratch buffers must not interleave there (execution stays async).
+std::mutex g_enqueue_mu;
+
 void wait_host_input(const void *host_src, size_t nbytes, cudaStream_t waiter) {
     const uintptr_t lo = (uintptr_t)host_src, hi = lo + nbytes;
     std::lock_guard<std::mutex> lk(g_pipe_mu);
@@ -253,8 +258,8 @@ void wait_and_replace(std::map<const void *, cudaEvent_t> &m, const void *ptr, c
 
 // Pipelined host->device->host permutation.  `async`: return after
 // enqueueing (completion ordered on `user`), else synchronise `user`.
-// Returns VPG_EUNSUPPORTED when a synchronous call would not benefit (small
-// tensor, no chunkable dims): the caller then runs the plain sequence.
+// Tensors without a chunked plan run as one H2D -> kernel -> D2H chunk on
+// the same streams, so scratch reuse is ordered the same way.
 vpg_status permute_host_pipelined(const vpg_plan *p, const void *host_src, void *host_dst, void *dev_src,
                                   void *dev_dst, cudaStream_t user, bool async, std::string *err) {
     PipePlan pp;
@@ -278,7 +283,6 @@ vpg_status permute_host_pipelined(const vpg_plan *p, const void *host_src, void 
         }
         if (dup && built.sub) vpg_plan_destroy(built.sub);   // lost the race; outside the lock
     }
-    if (!pp.ok && !async) return VPG_EUNSUPPORTED;
     DevStreams s = streams_for_current(err);
     if (!s.h2d) return VPG_ECUDA;
     const int r = p->rank, E = p->elem_bytes;
@@ -293,6 +297,7 @@ vpg_status permute_host_pipelined(const vpg_plan *p, const void *host_src, void 
         odims[j] = p->dims[p->sigma[j]];
         pos[p->sigma[j]] = j;
     }
+    std::unique_lock<std::mutex> enqueue_lock(g_enqueue_mu);
     cudaEvent_t start, fin, src_free, dst_free;
     std::vector<cudaEvent_t> done_in(chunks), done_k(chunks);
     cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
@@ -356,6 +361,7 @@ vpg_status permute_host_pipelined(const vpg_plan *p, const void *host_src, void 
     cudaEventRecord(dst_free, s.d2h);    // all D2H of this call done reading dev_dst
     if (async) remember_host_output(host_dst, (size_t)p->n * E, s.d2h);
     cudaStreamWaitEvent(user, fin, 0);
+    enqueue_lock.unlock();
     if (!async) {
         cudaError_t e = cudaStreamSynchronize(user);
         if (e != cudaSuccess && st == VPG_OK) {

@@ -295,3 +295,52 @@ def test_permute_of_permuted_views(cuda):
     assert torch.equal(permute(m.mT, (1, 0)), m)
     with pytest.raises(vp.LayoutError):
         permute(base[:, :, ::2], (0, 1, 2, 3, 4))
+
+
+def test_concurrent_host_threads(cuda):
+    """Plans are shareable and vpg_permute is safe from several host threads
+    on distinct streams (include/vpgpu.h threading contract), including the
+    first launch of specialised kernels (NVRTC compile under contention) and
+    the host-buffer pipeline."""
+    import threading
+
+    import torch
+
+    import paper_2506_03686_b200 as vp
+    from paper_2506_03686_b200.api import execute_device
+
+    shapes = [((64, 96, 130), (2, 0, 1)), ((33, 65, 129), (1, 2, 0)), ((2,) * 22, tuple(range(21, -1, -1))),
+              ((128, 40, 3, 64), (3, 1, 0, 2))]
+    progs = [vp.build_program(vp.TensorLayout.from_shape(s, 4), vp.from_numpy_convention(a), jit=True)
+             for s, a in shapes]
+    vp.program_cache_clear()
+    inputs = [torch.randint(-2**31, 2**31 - 1, s, dtype=torch.int32, device="cuda") for s, _ in shapes]
+    wants = [x.permute(a).contiguous() for x, (_, a) in zip(inputs, shapes)]
+    torch.cuda.synchronize()
+    errors = []
+
+    def worker(tid):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                for it in range(6):
+                    k = (tid + it) % len(shapes)
+                    y = execute_device(progs[k], inputs[k], stream=st)
+                    st.synchronize()
+                    if not torch.equal(y, wants[k]):
+                        errors.append((tid, k, "device"))
+            if tid % 2 == 0:                               # host-buffer pipeline from threads too
+                k = tid % len(shapes)
+                out, _ = vp.execute(progs[k], inputs[k].cpu())
+                if not torch.equal(torch.as_tensor(out).reshape(wants[k].shape), wants[k].cpu()):
+                    errors.append((tid, k, "host"))
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append((tid, repr(e)))
+
+    ts = [threading.Thread(target=worker, args=(i,)) for i in range(8)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    assert all(p.jit_state == 2 for p in progs)
