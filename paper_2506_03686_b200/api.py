@@ -334,7 +334,9 @@ def autotune(layout: TensorLayout, pmap: PermutationMap, candidates: int = 10, r
              device=None) -> GpuProgram:
     """Time the ``candidates`` best tile shapes of the cost model on the GPU
     and cache the fastest as the program for these arguments.  Non-tile
-    plans are returned unchanged.  Needs a GPU (raises on CPU)."""
+    plans are returned unchanged.  Needs a GPU (raises on CPU) and, while it
+    runs, two scratch buffers of the tensor's size plus a 256 MiB L2-flush
+    buffer."""
     base = build_program(layout, pmap, merge=merge, force=force, jit=jit)
     if base.kernel != "tile" or base.num_elements == 0:
         return base

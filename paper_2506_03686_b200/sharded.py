@@ -38,7 +38,7 @@ from dataclasses import dataclass
 from .core import LayoutError
 
 __all__ = ["ShardPlan", "plan_sharded", "permute_sharded", "shard_bounds", "ShardExchange", "emulate_fused",
-           "fused_supported"]
+           "fused_supported", "release_exchanges"]
 
 
 def _lead_split(shape, G):
@@ -432,6 +432,15 @@ def _check_ipc(status):
 
 
 _exchanges: dict = {}
+
+
+def release_exchanges():
+    """Drop the cached ShardExchange objects of permute_sharded(method=
+    "fused"/"auto") and their peer mappings and output buffers.  Collective
+    in effect: call it on every rank."""
+    for ex in list(_exchanges.values()):
+        ex.close()
+    _exchanges.clear()
 
 
 def _exchange_for(shape, axes, dtype, device, group):
