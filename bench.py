@@ -420,10 +420,18 @@ def bench_sharded(args, torch, base, config, peak, peak_kind):
     from paper_2506_03686_b200.workloads import CONFIGS, make_input_slice
 
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    dist.init_process_group("nccl", device_id=dev)
+    backend = args.dist_backend
+    # gloo: code-path check only -- ranks may share a GPU, so its timings are
+    # not multi-GPU results (the JSON line says so)
+    dev_index = local_rank if backend == "nccl" else local_rank % torch.cuda.device_count()
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group("gloo")
     G, r = dist.get_world_size(), dist.get_rank()
+    red_dev = dev if backend == "nccl" else torch.device("cpu")
     wl = CONFIGS[args.config]
     sp = plan_sharded(wl.shape, wl.axes, G)
     lo, hi = shard_bounds(wl.numel, G, r)
@@ -445,7 +453,7 @@ def bench_sharded(args, torch, base, config, peak, peak_kind):
     torch.cuda.synchronize()
     dist.barrier()
     evs = []
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(dev_index) as clk:
         for _ in range(args.steps):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(st)
@@ -457,13 +465,13 @@ def bench_sharded(args, torch, base, config, peak, peak_kind):
     step_ms = [a.elapsed_time(b) for a, b in evs]
     if os.environ.get("VPG_BENCH_DEBUG"):
         print(f"rank {r} step ms: {[round(v, 3) for v in step_ms]}", file=sys.stderr, flush=True)
-    tot = torch.tensor([sum(step_ms)], device=dev, dtype=torch.float64)
+    tot = torch.tensor([sum(step_ms)], device=red_dev, dtype=torch.float64)
     dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     ms = tot.item() / args.steps
     gbs = wl.algorithmic_bytes / (ms * 1e-3) / 1e9
     # parity on every rank: 2^18 sampled output positions of this rank's shard
     want_ok = _sample_shard_parity(torch, host_in, out, wl, sp, r, G)
-    ok = torch.tensor([1 if want_ok else 0], device=dev)
+    ok = torch.tensor([1 if want_ok else 0], device=red_dev)
     dist.all_reduce(ok, op=dist.ReduceOp.MIN)
     # end to end: pinned host shard -> device -> sharded permute -> host shard
     host_out = torch.empty(out.numel() * out.element_size(), dtype=torch.uint8).pin_memory()
@@ -480,7 +488,7 @@ def bench_sharded(args, torch, base, config, peak, peak_kind):
         t1 = time.perf_counter()
         if s_ >= args.warmup:
             e2e.append(t1 - t0)
-    e2e_t = torch.tensor([sum(e2e) / len(e2e)], device=dev, dtype=torch.float64)
+    e2e_t = torch.tensor([sum(e2e) / len(e2e)], device=red_dev, dtype=torch.float64)
     dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     shard_bytes = wl.numel * wl.elem_bytes // G
     t_hbm = 2 * shard_bytes / (peak * 1e9)
@@ -506,6 +514,8 @@ def bench_sharded(args, torch, base, config, peak, peak_kind):
             "parity_sampled": bool(ok.item()),
             "clocks": clk.summary(),
             "shard_plan": sp.describe()[:400],
+            "dist_backend": backend if backend == "nccl" else
+            "gloo (code-path check: ranks may share one GPU; not a multi-GPU timing)",
         })
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
@@ -555,6 +565,8 @@ def main(argv=None):
     ap.add_argument("--no-extra", action="store_true", help="skip cfg1-4 side measurements")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-tune", action="store_true", help="skip measured planning (autotune)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="N>1 process group; gloo only checks the code path (ranks may share a GPU)")
     ap.add_argument("--shard-method", default="auto", choices=["auto", "fused", "alltoall"],
                     help="N>1: fused exchange kernel or P1 -> all-to-all -> P2")
     ap.add_argument("--cpu-threads", type=int, default=None)
