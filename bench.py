@@ -436,13 +436,14 @@ def bench_sharded(args, torch, base, config, peak, peak_kind):
     sp = plan_sharded(wl.shape, wl.axes, G)
     lo, hi = shard_bounds(wl.numel, G, r)
     host_in = torch.from_numpy(make_input_slice(wl, lo, hi).reshape(-1).view(np.uint8)).pin_memory()
-    x = host_in.to(dev).view(torch.int64)
+    wdt = {4: torch.int32, 8: torch.int64}[wl.elem_bytes]     # opaque words of the element width
+    x = host_in.to(dev).view(wdt)
     st = torch.cuda.current_stream()
     method = args.shard_method
     if method == "auto":
         method = "fused" if fused_supported(wl.shape, wl.axes, wl.elem_bytes, G) else "alltoall"
     if method == "fused":
-        ex = ShardExchange(wl.shape, wl.axes, torch.int64, device=dev)
+        ex = ShardExchange(wl.shape, wl.axes, wdt, device=dev)
         run = ex
     else:
         run = lambda xin: permute_sharded(xin, wl.shape, wl.axes, local_permute=permute, plan=sp)  # noqa: E731
@@ -481,7 +482,7 @@ def bench_sharded(args, torch, base, config, peak, peak_kind):
         torch.cuda.synchronize()
         dist.barrier()
         t0 = time.perf_counter()
-        xin = host_in.to(dev, non_blocking=True).view(torch.int64)
+        xin = host_in.to(dev, non_blocking=True).view(wdt)
         y = run(xin)
         host_out.copy_(y.reshape(-1).view(torch.uint8), non_blocking=True)
         torch.cuda.synchronize()
@@ -544,13 +545,14 @@ def _sample_shard_parity(torch, host_in, out, wl, sp, r, G, nsamp=1 << 18):
         d = wl.shape[a]
         src += (rem % d) * in_strides[a]
         rem //= d
-    got = out.reshape(-1).cpu().numpy().view(np.uint64)[pos - lo]
-    vals = np.empty(nsamp, dtype=np.uint64)
+    wnp = np.uint64 if wl.elem_bytes == 8 else np.uint32
+    got = out.reshape(-1).cpu().numpy().view(wnp)[pos - lo]
+    vals = np.empty(nsamp, dtype=wnp)
     # regenerate the needed global input words block by block
     blocks = np.unique(src // (1 << 22))
     for b in blocks:
         sel = (src // (1 << 22)) == b
-        blk = make_input_slice(wl, int(b) << 22, min(n, (int(b) + 1) << 22)).view(np.uint64)
+        blk = make_input_slice(wl, int(b) << 22, min(n, (int(b) + 1) << 22)).view(wnp)
         vals[sel] = blk[src[sel] - (int(b) << 22)]
     return bool(np.array_equal(got, vals))
 

@@ -225,3 +225,24 @@ def test_fused_exchange_word_sizes(cuda, dtype_name, jit):
             assert torch.equal(got, x.reshape(shape).permute(axes).reshape(-1)), (shape, axes, G)
             ran += 1
     assert ran >= 4
+
+
+@pytest.mark.parametrize("method", ["fused", "alltoall"])
+def test_bench_two_ranks_code_path(cuda, method):
+    """bench.py's N>1 path (torchrun, two ranks) end to end with the gloo
+    backend on one GPU: the same code the 8-GPU NCCL run takes, checked for
+    per-rank sampled parity (timings of this run are not multi-GPU results)."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
+           "--dist-backend", "gloo", "--shard-method", method, "--config", "cfg1", "--steps", "2", "--warmup", "3"]
+    res = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    line = json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["parity_sampled"] is True
+    assert line["shard_method"] == method and line["n_gpus"] == 2
+    assert "gloo" in line["dist_backend"]
