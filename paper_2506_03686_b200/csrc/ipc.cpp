@@ -19,7 +19,15 @@ namespace {
 typedef CUresult (*PfnGetAddressRange)(CUdeviceptr *, size_t *, CUdeviceptr);
 
 std::mutex g_mu;
-std::map<void *, void *> g_base_of;   // imported pointer -> mapped base
+// A process maps each exported allocation once: buffers handed out by a
+// caching allocator often share one cudaMalloc segment, so several imports
+// can name the same handle.  Mappings are refcounted per handle.
+struct Mapping {
+    void *base;
+    int refs;
+};
+std::map<std::string, Mapping> g_by_handle;          // handle bytes -> mapping
+std::map<void *, std::pair<std::string, int>> g_imports;   // imported pointer -> (handle, count)
 
 PfnGetAddressRange address_range_fn() {
     static PfnGetAddressRange fn = [] {
@@ -63,15 +71,25 @@ vpg_status ipc_export(const void *ptr, void *handle, uint64_t *offset, std::stri
 vpg_status ipc_import(const void *handle, uint64_t offset, void **ptr, std::string *err) {
     cudaIpcMemHandle_t h;
     memcpy(&h, handle, sizeof(h));
+    const std::string key((const char *)&h, sizeof(h));
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_by_handle.find(key);
     void *base = nullptr;
-    cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
-    if (e != cudaSuccess) {
-        *err = std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e);
-        return VPG_ECUDA;
+    if (it != g_by_handle.end()) {
+        base = it->second.base;
+        ++it->second.refs;
+    } else {
+        cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+            *err = std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e);
+            return VPG_ECUDA;
+        }
+        g_by_handle[key] = Mapping{base, 1};
     }
     *ptr = (char *)base + offset;
-    std::lock_guard<std::mutex> lk(g_mu);
-    g_base_of[*ptr] = base;
+    auto &imp = g_imports[*ptr];
+    imp.first = key;
+    ++imp.second;
     return VPG_OK;
 }
 
@@ -79,13 +97,17 @@ vpg_status ipc_release(void *ptr, std::string *err) {
     void *base = nullptr;
     {
         std::lock_guard<std::mutex> lk(g_mu);
-        auto it = g_base_of.find(ptr);
-        if (it == g_base_of.end()) {
+        auto it = g_imports.find(ptr);
+        if (it == g_imports.end()) {
             *err = "pointer was not imported by vpg_ipc_import";
             return VPG_EINVAL;
         }
-        base = it->second;
-        g_base_of.erase(it);
+        const std::string key = it->second.first;
+        if (--it->second.second == 0) g_imports.erase(it);
+        auto m = g_by_handle.find(key);
+        if (m == g_by_handle.end() || --m->second.refs > 0) return VPG_OK;
+        base = m->second.base;
+        g_by_handle.erase(m);
     }
     cudaError_t e = cudaIpcCloseMemHandle(base);
     if (e != cudaSuccess) {

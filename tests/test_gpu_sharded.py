@@ -72,7 +72,7 @@ def _fused_worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2506_03686_b200.sharded import ShardExchange, permute_sharded, shard_bounds
 
-    errs, ran = [], 0
+    errs, ran, live = [], 0, []
     for ci, (shape, axes) in enumerate(FUSED_CASES):
         try:
             ex = ShardExchange(shape, axes, torch.int64)
@@ -90,13 +90,20 @@ def _fused_worker(rank, world, port, q):
             torch.cuda.synchronize()
             if not np.array_equal(out.cpu().numpy().reshape(-1), want):
                 errs.append((shape, axes, step))
-        # the method="fused" entry point lands on the same exchange
+        # permute_sharded(method="fused") builds its own cached exchange (a second mapping of the peers)
         out = permute_sharded(torch.from_numpy(g[lo:hi].copy()).cuda(), shape, axes, method="fused")
         torch.cuda.synchronize()
         if not np.array_equal(out.cpu().numpy().reshape(-1), want):
             errs.append((shape, axes, "permute_sharded"))
-        ex.close()
+        live.append((ex, local, want))  # exchanges stay mapped together (shared allocator segments)
         ran += 1
+    for ex, local, want in live:        # every exchange still works with all mappings open
+        out = ex(local)
+        torch.cuda.synchronize()
+        if not np.array_equal(out.cpu().numpy().reshape(-1), want):
+            errs.append(("live", ex.splan.shape))
+    for ex, _, _ in live:
+        ex.close()
     q.put((rank, errs, ran))
     dist.barrier()
     dist.destroy_process_group()
