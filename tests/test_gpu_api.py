@@ -344,3 +344,34 @@ def test_concurrent_host_threads(cuda):
         t.join()
     assert not errors, errors
     assert all(p.jit_state == 2 for p in progs)
+
+
+def test_cuda_graph_capture_and_replay(cuda):
+    """Launches are capturable in a CUDA graph (stream-ordered, no host
+    synchronisation inside vpg_permute); replays stay bit-exact as the
+    input buffer changes."""
+    import torch
+
+    import paper_2506_03686_b200 as vp
+    from paper_2506_03686_b200.api import execute_device
+
+    cases = [((64, 96, 130), (2, 0, 1)), ((2,) * 21, tuple(range(20, -1, -1))), ((128, 8, 1024), (1, 0, 2))]
+    progs = [vp.build_program(vp.TensorLayout.from_shape(s, 4), vp.from_numpy_convention(a)) for s, a in cases]
+    xs = [torch.empty(s, dtype=torch.int32, device="cuda") for s, _ in cases]
+    ys = [torch.empty(p.out_shape, dtype=torch.int32, device="cuda") for p in progs]
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        for p, x, y in zip(progs, xs, ys):       # first launches (kernel loading) outside the capture
+            execute_device(p, x, out=y, stream=st)
+    st.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        for p, x, y in zip(progs, xs, ys):
+            execute_device(p, x, out=y, stream=st)
+    for it in range(3):
+        for x in xs:
+            x.copy_(torch.randint(-2**31, 2**31 - 1, x.shape, dtype=torch.int32, device="cuda"))
+        g.replay()
+        torch.cuda.synchronize()
+        for x, y, (_, a) in zip(xs, ys, cases):
+            assert torch.equal(y, x.permute(a).contiguous()), it
