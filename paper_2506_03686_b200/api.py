@@ -331,22 +331,31 @@ def _time_program(torch, program, src, dst, flush, reps):
 
 def autotune(layout: TensorLayout, pmap: PermutationMap, candidates: int = 10, reps: int = 5,
              merge: bool = True, force: str | None = None, jit: bool | None = None,
-             device=None) -> GpuProgram:
+             device=None, src=None, dst=None) -> GpuProgram:
     """Time the ``candidates`` best tile shapes of the cost model on the GPU
     and cache the fastest as the program for these arguments.  Non-tile
     plans are returned unchanged.  Needs a GPU (raises on CPU) and, while it
     runs, two scratch buffers of the tensor's size plus a 256 MiB L2-flush
-    buffer."""
+    buffer; pass the CUDA tensors the program will run on as ``src``/``dst``
+    to time on them instead (their contents are overwritten: ``dst`` only)."""
     base = build_program(layout, pmap, merge=merge, force=force, jit=jit)
     if base.kernel != "tile" or base.num_elements == 0:
         return base
     torch = _torch()
     if not torch.cuda.is_available():
         raise CudaError("autotune needs a CUDA device")
-    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    if src is not None:
+        dev = src.device
+    else:
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
     with torch.cuda.device(dev):
-        src = torch.empty(base.nbytes, dtype=torch.uint8, device=dev)
-        dst = torch.empty(base.nbytes, dtype=torch.uint8, device=dev)
+        if src is None:
+            src = torch.empty(base.nbytes, dtype=torch.uint8, device=dev)
+        if dst is None:
+            dst = torch.empty(base.nbytes, dtype=torch.uint8, device=dev)
+        for t in (src, dst):
+            if not t.is_cuda or t.numel() * t.element_size() != base.nbytes or not t.is_contiguous():
+                raise LayoutError("autotune buffers must be contiguous CUDA tensors of the tensor's size")
         flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
         best, best_t = base, _time_program(torch, base, src, dst, flush, reps)
         for c in range(1, candidates):

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -229,6 +230,10 @@ vpg_status launch_tile(const vpg_plan *p, const void *src, void *dst, const Shar
             if (p->tile.persistent) grid = std::min<int64_t>(grid, (int64_t)nb * sm_count_for_current());
             if (grid < 1) grid = 1;
             void *args[] = {(void *)&src, (void *)&dst, (void *)&sa};
+            static const bool dbg = getenv("VPG_DEBUG_LAUNCH") != nullptr;
+            if (dbg)
+                fprintf(stderr, "[vpg] jit launch kernel %p grid %lld threads %d smem %d nb %d src %p dst %p\n",
+                        (const void *)jk, (long long)grid, jthreads, smem, nb, src, dst);
             if (cudaLaunchKernel((const void *)jk, dim3((unsigned)grid), dim3(jthreads), args, (size_t)smem, st) ==
                 cudaSuccess)
                 return VPG_OK;

@@ -243,7 +243,8 @@ bool select_tile(const Problem &P, TileGeom &best, int pick = -1) {
             }
         }
     }
-    if (const char *e = getenv("VPG_TILE_PICK")) pick = atoi(e);
+    if (const char *e = getenv("VPG_TILE_PICK"))
+        if (*e) pick = atoi(e);
     if (pick >= 0) {
         std::stable_sort(all.begin(), all.end(), [](const TileGeom &x, const TileGeom &y) { return x.cost < y.cost; });
         std::vector<TileGeom> uniq;   // distinct (Ls, Ld, T)

@@ -1,0 +1,107 @@
+"""Process-order probe: time candidate 1 of cfg5 when built directly (A),
+as the autotune winner (B), or rebuilt after an autotune (C)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2506_03686_b200 as vp  # noqa: E402
+from paper_2506_03686_b200.api import execute_device  # noqa: E402
+from paper_2506_03686_b200.workloads import CONFIGS  # noqa: E402
+
+mode = sys.argv[1]
+pre = len(sys.argv) > 2 and sys.argv[2] == "pre"     # allocate flush/x/y before the prelude
+wl = CONFIGS["cfg5"]
+dev = torch.device("cuda", 0)
+n = wl.numel * wl.elem_bytes
+lay, pm = vp.TensorLayout.from_shape(wl.shape, wl.elem_bytes), vp.from_numpy_convention(wl.axes)
+if pre:
+    fl = bench.Flusher(torch, dev)
+    x = torch.randint(0, 255, (n,), dtype=torch.uint8, device=dev)
+    y = torch.empty_like(x)
+if mode == "A":
+    p = vp.build_program(lay, pm, candidate=1)
+elif mode == "B":
+    p = vp.autotune(lay, pm)
+elif mode == "U":          # autotune on the bench buffers
+    assert pre
+    p = vp.autotune(lay, pm, src=x, dst=y)
+elif mode in ("W1", "W0"):  # one launch of candidate 1 / 0 on the bench buffers, then autotune
+    assert pre
+    execute_device(vp.build_program(lay, pm, candidate=int(mode[1])), x, out=y)
+    torch.cuda.synchronize()
+    p = vp.autotune(lay, pm)
+elif mode == "C":
+    vp.autotune(lay, pm)
+    vp.program_cache_clear()
+    p = vp.build_program(lay, pm, candidate=1)
+elif mode == "D":          # autotune, then return its scratch to the driver
+    p = vp.autotune(lay, pm)
+    torch.cuda.empty_cache()
+elif mode in ("F", "G"):  # launch another candidate's kernel first (F: 0, G: 3)
+    other = vp.build_program(lay, pm, candidate=0 if mode == "F" else 3)
+    p = vp.build_program(lay, pm, candidate=1)
+    xa = torch.empty(n, dtype=torch.uint8, device=dev)
+    ya = torch.empty(n, dtype=torch.uint8, device=dev)
+    for _ in range(3):
+        execute_device(other, xa, out=ya)
+    torch.cuda.synchronize()
+    del xa, ya
+elif mode == "H":          # as much traffic as an autotune, with the same kernel
+    p = vp.build_program(lay, pm, candidate=1)
+    xa = torch.empty(n, dtype=torch.uint8, device=dev)
+    ya = torch.empty(n, dtype=torch.uint8, device=dev)
+    for _ in range(70):
+        execute_device(p, xa, out=ya)
+    torch.cuda.synchronize()
+    del xa, ya
+elif mode in ("J", "K"):   # as H, then idle 2 s (J) or 10 s (K) before timing
+    import time
+    p = vp.build_program(lay, pm, candidate=1)
+    xa = torch.empty(n, dtype=torch.uint8, device=dev)
+    ya = torch.empty(n, dtype=torch.uint8, device=dev)
+    for _ in range(70):
+        execute_device(p, xa, out=ya)
+    torch.cuda.synchronize()
+    del xa, ya
+    time.sleep(2 if mode == "J" else 10)
+elif mode == "I":          # autotune with a single candidate
+    p = vp.autotune(lay, pm, candidates=1)
+    p = vp.build_program(lay, pm, candidate=1)
+elif mode.startswith("P"):  # 7 launches of candidate k first ("P7")
+    other = vp.build_program(lay, pm, candidate=int(mode[1:]))
+    p = vp.build_program(lay, pm, candidate=1)
+    xa = torch.empty(n, dtype=torch.uint8, device=dev)
+    ya = torch.empty(n, dtype=torch.uint8, device=dev)
+    for _ in range(7):
+        execute_device(other, xa, out=ya)
+    torch.cuda.synchronize()
+    del xa, ya
+elif mode == "E":          # no autotune: allocate and free dummy blocks first
+    p = vp.build_program(lay, pm, candidate=1)
+    a = torch.empty(n, dtype=torch.uint8, device=dev)
+    b = torch.empty(n, dtype=torch.uint8, device=dev)
+    c = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    del a, b, c
+if not pre:
+    fl = bench.Flusher(torch, dev)
+    x = torch.randint(0, 255, (n,), dtype=torch.uint8, device=dev)
+    y = torch.empty_like(x)
+st = torch.cuda.current_stream()
+t = bench.time_device(torch, lambda: execute_device(p, x, out=y), 15, 3, fl, st)
+t2 = bench.time_device(torch, lambda: execute_device(p, x, out=y), 15, 3, fl, st)
+extra = ""
+try:
+    import pynvml
+    pynvml.nvmlInit()
+    h = pynvml.nvmlDeviceGetHandleByIndex(0)
+    extra = (f" mem {pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_MEM)} MHz sm "
+             f"{pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)} MHz temp "
+             f"{pynvml.nvmlDeviceGetTemperature(h, pynvml.NVML_TEMPERATURE_GPU)} C pstate "
+             f"{pynvml.nvmlDeviceGetPerformanceState(h)} reasons {pynvml.nvmlDeviceGetCurrentClocksEventReasons(h):#x}")
+except Exception as e:
+    extra = f" nvml: {e}"
+print(mode + ("/pre" if pre else ""), p.metadata["src_run"], p.metadata["dst_run"], round(sorted(t)[7] * 1e3, 1), round(sorted(t2)[7] * 1e3, 1),
+      extra)
