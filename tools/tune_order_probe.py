@@ -25,6 +25,33 @@ if mode == "A":
     p = vp.build_program(lay, pm, candidate=1)
 elif mode == "B":
     p = vp.autotune(lay, pm)
+elif mode.startswith("T"):  # autotune with k candidates ("T4")
+    p = vp.autotune(lay, pm, candidates=int(mode[1:]))
+elif mode in ("Z", "Zi", "Zs"):  # autotune's timing helper on c1 alone (Zi: initialised src, Zs: no per-launch sync)
+    from paper_2506_03686_b200.api import _time_program
+    p = vp.build_program(lay, pm, candidate=1)
+    sa = torch.empty(n, dtype=torch.uint8, device=dev)
+    if mode == "Zi":
+        sa.fill_(7)
+    da = torch.empty(n, dtype=torch.uint8, device=dev)
+    flb = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    if mode == "Zs":
+        for _ in range(7):
+            flb.zero_()
+            execute_device(p, sa, out=da)
+        torch.cuda.synchronize()
+    else:
+        _time_program(torch, p, sa, da, flb, 5)
+    del sa, da, flb
+elif mode in ("S1", "S2"):   # flush buffers carved from a freed 2 GiB block (S1), or x/y from it (S2)
+    p = vp.build_program(lay, pm, candidate=1)
+    big = torch.empty(n, dtype=torch.uint8, device=dev)
+    del big
+    if mode == "S1":
+        fl = bench.Flusher(torch, dev)
+        x = torch.randint(0, 255, (n,), dtype=torch.uint8, device=dev)
+        y = torch.empty_like(x)
+        pre = True
 elif mode == "U":          # autotune on the bench buffers
     assert pre
     p = vp.autotune(lay, pm, src=x, dst=y)
