@@ -201,6 +201,17 @@ std::vector<int64_t> extent_candidates(int64_t d, int64_t cap) {
     return v;
 }
 
+// Candidate order: modelled cost; ties (mirror-image tiles) go to the
+// smaller tile, then to the longer SOURCE run -- reads gain more from long
+// runs than the write-back-cached writes (cfg5: 2 KiB reads x 1 KiB writes
+// 670 us vs 1 KiB x 2 KiB 682 us; tools/pick_ab.py).
+static bool better(const TileGeom &a, const TileGeom &b) {
+    if (a.cost < b.cost - 1e-9) return true;
+    if (a.cost > b.cost + 1e-9) return false;
+    if (a.T != b.T) return a.T < b.T;
+    return a.Ls > b.Ls;
+}
+
 bool select_tile(const Problem &P, TileGeom &best, int pick = -1) {
     const int r = P.r;
     const int64_t maxT = std::max<int64_t>(P.budget / P.E, 64);
@@ -234,8 +245,7 @@ bool select_tile(const Problem &P, TileGeom &best, int pick = -1) {
                     if (g.T > maxT) continue;
                     score_geom(P, g);
                     all.push_back(g);
-                    if (!found || g.cost < best.cost - 1e-9 ||
-                        (std::fabs(g.cost - best.cost) <= 1e-9 && g.T < best.T)) {
+                    if (!found || better(g, best)) {
                         best = g;
                         found = true;
                     }
@@ -246,7 +256,7 @@ bool select_tile(const Problem &P, TileGeom &best, int pick = -1) {
     if (const char *e = getenv("VPG_TILE_PICK"))
         if (*e) pick = atoi(e);
     if (pick >= 0) {
-        std::stable_sort(all.begin(), all.end(), [](const TileGeom &x, const TileGeom &y) { return x.cost < y.cost; });
+        std::stable_sort(all.begin(), all.end(), better);
         std::vector<TileGeom> uniq;   // distinct (Ls, Ld, T)
         for (const TileGeom &g : all) {
             bool dup = false;

@@ -52,6 +52,35 @@ elif mode in ("S1", "S2"):   # flush buffers carved from a freed 2 GiB block (S1
         x = torch.randint(0, 255, (n,), dtype=torch.uint8, device=dev)
         y = torch.empty_like(x)
         pre = True
+elif mode in ("Q", "Q2"):   # bench-like input: pinned host buffer copied to the device (Q2: + NVML sampler)
+    p = vp.build_program(lay, pm, candidate=1)
+    host_in = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    host_in.fill_(3)
+    fl = bench.Flusher(torch, dev)
+    x = host_in.to(dev)
+    y = torch.empty_like(x)
+    pre = True
+    if mode == "Q2":
+        _clk = bench.ClockSampler(0)
+        _clk.__enter__()
+elif mode in ("Q3", "Q4", "Q5"):
+    # Q3: 2 GiB pinned host allocation, device input written by a kernel
+    # Q4: pageable host buffer copied in;  Q5: device input written by a kernel, then a 2 GiB D2D copy into it
+    p = vp.build_program(lay, pm, candidate=1)
+    fl = bench.Flusher(torch, dev)
+    if mode == "Q3":
+        host_in = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        host_in.fill_(3)
+        x = torch.randint(0, 255, (n,), dtype=torch.uint8, device=dev)
+    elif mode == "Q4":
+        host_in = torch.empty(n, dtype=torch.uint8)
+        host_in.fill_(3)
+        x = host_in.to(dev)
+    else:
+        x = torch.randint(0, 255, (n,), dtype=torch.uint8, device=dev)
+        x.copy_(torch.randint(0, 255, (n,), dtype=torch.uint8, device=dev))
+    y = torch.empty_like(x)
+    pre = True
 elif mode == "U":          # autotune on the bench buffers
     assert pre
     p = vp.autotune(lay, pm, src=x, dst=y)
