@@ -375,3 +375,23 @@ def test_cuda_graph_capture_and_replay(cuda):
         torch.cuda.synchronize()
         for x, y, (_, a) in zip(xs, ys, cases):
             assert torch.equal(y, x.permute(a).contiguous()), it
+
+
+def test_c_api_demo_program(cuda, tmp_path):
+    """The C ABI from plain C (examples/c_api_demo.c): plan, permute and the
+    fused sharded exchange on caller-owned cudaMalloc buffers, checked on the
+    host against the closed-form bijection."""
+    import os
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "c_api_demo")
+    lib = os.path.join(root, "paper_2506_03686_b200")
+    cmd = ["gcc", "-O2", "-I", os.path.join(root, "include"), "-I", "/usr/local/cuda/include",
+           os.path.join(root, "examples", "c_api_demo.c"), "-o", exe, "-L", lib, "-lvpgpu",
+           "-L", "/usr/local/cuda/lib64", "-lcudart", f"-Wl,-rpath,{lib}"]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    res = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert "permute: 0 mismatches" in res.stdout
+    assert "sharded exchange (G=4): 0 mismatches" in res.stdout
