@@ -1,0 +1,41 @@
+"""Same-segment vs separate-segment src/dst for the cfg5 kernel."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2506_03686_b200 as vp  # noqa: E402
+from paper_2506_03686_b200.api import execute_device  # noqa: E402
+from paper_2506_03686_b200.workloads import CONFIGS  # noqa: E402
+
+mode = sys.argv[1]
+wl = CONFIGS["cfg5"]
+dev = torch.device("cuda", 0)
+n = wl.numel * wl.elem_bytes
+p = vp.build_program(vp.TensorLayout.from_shape(wl.shape, 8), vp.from_numpy_convention(wl.axes))
+fl = bench.Flusher(torch, dev)
+st = torch.cuda.current_stream()
+if mode == "separate":
+    x = torch.empty(n, dtype=torch.uint8, device=dev)
+    y = torch.empty(n, dtype=torch.uint8, device=dev)
+elif mode == "one":
+    pool = torch.empty(2 * n, dtype=torch.uint8, device=dev)
+    x, y = pool[:n], pool[n:]
+elif mode in ("tinyrand", "bigrand_other"):
+    if mode == "tinyrand":
+        torch.randint(0, 255, (1024,), dtype=torch.uint8, device=dev)
+    else:
+        z = torch.randint(0, 255, (n,), dtype=torch.uint8, device=dev)
+        del z
+    x = torch.empty(n, dtype=torch.uint8, device=dev)
+    y = torch.empty(n, dtype=torch.uint8, device=dev)
+elif mode == "randint":
+    x = torch.randint(0, 255, (n,), dtype=torch.uint8, device=dev)
+    y = torch.empty_like(x)
+x.fill_(7)
+t = bench.time_device(torch, lambda: execute_device(p, x, out=y), 15, 3, fl, st)
+t2 = bench.time_device(torch, lambda: execute_device(p, x, out=y), 15, 3, fl, st)
+print(mode, round(sorted(t)[7] * 1e3, 1), round(sorted(t2)[7] * 1e3, 1), hex(x.data_ptr()), hex(y.data_ptr()),
+      torch.cuda.memory_reserved() >> 20, "MiB reserved", flush=True)
