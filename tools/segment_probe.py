@@ -23,6 +23,13 @@ if mode == "separate":
 elif mode == "one":
     pool = torch.empty(2 * n, dtype=torch.uint8, device=dev)
     x, y = pool[:n], pool[n:]
+elif mode in ("smallalloc", "smallalloc_after"):
+    if mode == "smallalloc":
+        keep = torch.empty(1024, dtype=torch.uint8, device=dev)
+    x = torch.empty(n, dtype=torch.uint8, device=dev)
+    y = torch.empty(n, dtype=torch.uint8, device=dev)
+    if mode == "smallalloc_after":
+        keep = torch.empty(1024, dtype=torch.uint8, device=dev)
 elif mode in ("tinyrand", "bigrand_other"):
     if mode == "tinyrand":
         torch.randint(0, 255, (1024,), dtype=torch.uint8, device=dev)
