@@ -14,7 +14,8 @@ mode = sys.argv[1]
 wl = CONFIGS["cfg5"]
 dev = torch.device("cuda", 0)
 n = wl.numel * wl.elem_bytes
-p = vp.build_program(vp.TensorLayout.from_shape(wl.shape, 8), vp.from_numpy_convention(wl.axes))
+p = vp.build_program(vp.TensorLayout.from_shape(wl.shape, 8), vp.from_numpy_convention(wl.axes),
+                     candidate=int(os.environ.get("CAND", "0")))
 fl = bench.Flusher(torch, dev)
 st = torch.cuda.current_stream()
 if mode == "separate":
