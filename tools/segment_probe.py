@@ -24,6 +24,17 @@ if mode == "separate":
 elif mode == "one":
     pool = torch.empty(2 * n, dtype=torch.uint8, device=dev)
     x, y = pool[:n], pool[n:]
+elif mode in ("seed", "rand", "randn", "gen"):
+    if mode == "seed":
+        torch.cuda.manual_seed(0)
+    elif mode == "rand":
+        torch.rand(1024, device=dev)
+    elif mode == "randn":
+        torch.randn(1024, device=dev)
+    else:
+        torch.cuda.default_generators[0].initial_seed()
+    x = torch.empty(n, dtype=torch.uint8, device=dev)
+    y = torch.empty(n, dtype=torch.uint8, device=dev)
 elif mode in ("smallalloc", "smallalloc_after"):
     if mode == "smallalloc":
         keep = torch.empty(1024, dtype=torch.uint8, device=dev)
