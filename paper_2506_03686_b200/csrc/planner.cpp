@@ -31,7 +31,10 @@ namespace {
 constexpr int kTileThreads = 256;
 constexpr int64_t kGatherMaxN = 1024;
 constexpr int64_t kRowsMinBytes = 512;
-constexpr double kRunOverheadBytes = 32.0;   // cost of starting one contiguous run
+// cost of starting one contiguous run; with the ragged-tile factor below,
+// tuned on 80 random 64-512 MiB permutations (tools/perf_sweep.py): worst
+// case 0.585 -> 0.655 of copy, BASELINE choices unchanged
+constexpr double kRunOverheadBytes = 128.0;
 constexpr double kTileOverheadBytes = 2048.0;  // cost of one tile (decode + 2 barriers)
 constexpr int64_t kTileBudgetBytes = 48 * 1024;  // staged elements per CTA
 
@@ -172,6 +175,8 @@ void score_geom(const Problem &P, TileGeom &g) {
     const int E = P.E;
     int64_t as = run_align_elems(P, g, true) * E;
     int64_t ad = run_align_elems(P, g, false) * E;
+    const double ovh_s = getenv("VPG_RUNOVH_S") ? atof(getenv("VPG_RUNOVH_S")) : kRunOverheadBytes;
+    const double ovh_d = getenv("VPG_RUNOVH_D") ? atof(getenv("VPG_RUNOVH_D")) : kRunOverheadBytes;
     int64_t bs = g.Ls * E, bd = g.Ld * E;
     g.eff_s = (double)bs / (32.0 * expected_sectors(bs, gcd64(as, 32)));
     g.eff_d = (double)bd / (32.0 * expected_sectors(bd, gcd64(ad, 32)));
@@ -182,10 +187,14 @@ void score_geom(const Problem &P, TileGeom &g) {
         else if (g.ext[k] < P.d[k]) ntiles *= std::ceil((double)P.d[k] / (double)g.ext[k]);
     }
     double t_avg = (double)P.n / ntiles;
-    g.cost = E / g.eff_s + E / g.eff_d + kRunOverheadBytes * (1.0 / g.Ls + 1.0 / g.Ld) +
+    // ragged tiles run their full walk with idle lanes: the per-element
+    // cost grows with the slots per valid element (beta measured on random
+    // shapes, tools/perf_sweep.py: a 256-wide tile over a 300-long dim ran
+    // at 59% of copy)
+    const double beta = getenv("VPG_RAGGED_BETA") ? atof(getenv("VPG_RAGGED_BETA")) : 0.5;
+    g.cost = (E / g.eff_s + E / g.eff_d + ovh_s / g.Ls + ovh_d / g.Ld) *
+                 (1.0 + beta * ((double)g.T / t_avg - 1.0)) +
              kTileOverheadBytes / t_avg;
-    // lanes idle in ragged tiles still cost issue slots: small penalty
-    g.cost += 0.05 * E * ((double)g.T / t_avg - 1.0);
 }
 
 std::vector<int64_t> extent_candidates(int64_t d, int64_t cap) {
