@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(256) copy_kernel_chunked(const uint4 *__restri
 // RPW consecutive destination rows with U vectors per lane per row in
 // flight before the stores (U = 4, RPW = 2 measured best on cfg4: 346.8 vs
 // 351.3 us for one row at a time, 353.2 for U = 8).
-template <typename V, int U, int RPW>
+template <typename V, int U, int RPW, bool CHUNKED>
 __global__ void __launch_bounds__(256) rows_kernel(const __grid_constant__ RowsParams p,
                                                    const V *__restrict__ src, V *__restrict__ dst,
                                                    uint32_t vec_log2) {
@@ -82,43 +82,52 @@ __global__ void __launch_bounds__(256) rows_kernel(const __grid_constant__ RowsP
     const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t lane = gtid & (tpr - 1);
     const uint32_t ngroups = (gridDim.x * blockDim.x) >> p.tpr_log2;
-    const uint32_t rv = p.row_vecs;
-    for (uint32_t q0 = (gtid >> p.tpr_log2) * RPW; q0 < p.nrows; q0 += ngroups * RPW) {
+    const uint32_t rv = p.row_vecs, cv = CHUNKED ? p.chunk_vecs : p.row_vecs;
+    for (uint32_t w0 = (gtid >> p.tpr_log2) * RPW; w0 < p.nitems; w0 += ngroups * RPW) {
         const V *s[RPW];
         V *d[RPW];
-        bool ok[RPW];
+        uint32_t len[RPW];
+        uint32_t maxlen = 0;
 #pragma unroll
         for (int r = 0; r < RPW; ++r) {
-            const uint32_t q = q0 + r;
-            ok[r] = q < p.nrows;
-            uint32_t rem = ok[r] ? q : 0u;
+            const uint32_t w = w0 + r;
+            const bool ok = w < p.nitems;
+            uint32_t q = ok ? w : 0u, c0 = 0;
+            if constexpr (CHUNKED) {
+                q = ok ? fdiv(w, p.nchunks) : 0u;
+                c0 = ok ? (w - q * p.nchunks.d) * cv : 0u;
+            }
+            uint32_t rem = q;
             int64_t so = 0;
             for (int i = 0; i < p.ndig; ++i) {
                 uint32_t qq = fdiv(rem, p.dig[i].ext);
                 so += (int64_t)(rem - qq * p.dig[i].ext.d) * p.dig[i].src_stride;
                 rem = qq;
             }
-            s[r] = src + (so >> vec_log2);
-            d[r] = dst + (int64_t)(ok[r] ? q : 0u) * rv;
+            s[r] = src + (so >> vec_log2) + c0;
+            d[r] = dst + (int64_t)q * rv + c0;
+            len[r] = ok ? min(cv, rv - c0) : 0u;
+            maxlen = max(maxlen, len[r]);
         }
+        if constexpr (!CHUNKED) maxlen = rv;
         uint32_t i = lane;
-        for (; i + (U - 1) * tpr < rv; i += U * tpr) {
+        for (; i + (U - 1) * tpr < maxlen; i += U * tpr) {
             V v[RPW][U];
 #pragma unroll
             for (int r = 0; r < RPW; ++r)
 #pragma unroll
                 for (int u = 0; u < U; ++u)
-                    if (ok[r]) v[r][u] = ld_stream(s[r] + i + u * tpr);
+                    if (CHUNKED ? i + u * tpr < len[r] : len[r] != 0) v[r][u] = ld_stream(s[r] + i + u * tpr);
 #pragma unroll
             for (int r = 0; r < RPW; ++r)
 #pragma unroll
                 for (int u = 0; u < U; ++u)
-                    if (ok[r]) d[r][i + u * tpr] = v[r][u];
+                    if (CHUNKED ? i + u * tpr < len[r] : len[r] != 0) d[r][i + u * tpr] = v[r][u];
         }
-        for (; i < rv; i += tpr)
+        for (; i < maxlen; i += tpr)
 #pragma unroll
             for (int r = 0; r < RPW; ++r)
-                if (ok[r]) d[r][i] = ld_stream(s[r] + i);
+                if (i < len[r]) d[r][i] = ld_stream(s[r] + i);
     }
 }
 
@@ -295,11 +304,37 @@ vpg_status launch_rows(const vpg_plan *p, const void *src, void *dst, cudaStream
     uint32_t vlog = 0;
     while ((1u << vlog) < V) ++vlog;
     const int vb = (int)(V * E);
-    int64_t need = ((int64_t)rp.nrows << rp.tpr_log2) + 255;
+    // cut long rows into chunks until there are enough work items to fill
+    // every SM (few long rows would otherwise leave most warps idle)
+    {
+        const int64_t want = (int64_t)sm_count_for_current() * 64 * 2;   // two warps' worth per warp slot
+        uint64_t cv = rp.row_vecs;
+        if ((int64_t)rp.nrows < want) {
+            const uint64_t per = ((uint64_t)rp.nrows * rp.row_vecs + want - 1) / want;
+            const uint64_t unit = 32u * 4u;                                  // one warp x U vectors
+            cv = std::max<uint64_t>(unit * 2, (per + unit - 1) / unit * unit);
+            cv = std::min<uint64_t>(cv, rp.row_vecs);
+        }
+        const uint64_t nch = (rp.row_vecs + cv - 1) / cv;
+        if ((uint64_t)rp.nrows * nch >= 0xffffffffull) {
+            rp.chunk_vecs = rp.row_vecs;
+            rp.nchunks = make_fastdiv(1);
+            rp.nitems = rp.nrows;
+        } else {
+            rp.chunk_vecs = (uint32_t)cv;
+            rp.nchunks = make_fastdiv((uint32_t)nch);
+            rp.nitems = (uint32_t)(rp.nrows * nch);
+        }
+        uint32_t tpr = 32;
+        while (tpr > 1 && tpr / 2 >= rp.chunk_vecs) tpr >>= 1;
+        rp.tpr_log2 = 0;
+        while ((1u << rp.tpr_log2) < tpr) ++rp.tpr_log2;
+    }
+    int64_t need = ((int64_t)rp.nitems << rp.tpr_log2) + 255;
     need /= 256;
 #define VPG_ROWS_LAUNCH(TYPE, U, R)                                                            \
     {                                                                                          \
-        auto k = rows_kernel<TYPE, U, R>;                                                      \
+        auto k = rp.nchunks.d > 1 ? rows_kernel<TYPE, U, R, true> : rows_kernel<TYPE, U, R, false>; \
         int nb = occupancy(k, 256, 0);                                                         \
         int64_t grid = std::min<int64_t>(need, (int64_t)nb * sm_count_for_current());          \
         if (grid < 1) grid = 1;                                                                \

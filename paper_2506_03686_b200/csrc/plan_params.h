@@ -186,6 +186,11 @@ struct RowsParams {
     uint32_t tpr_log2;         // threads per row group (log2)
     int64_t row_len;           // Lr (elements)
     int32_t ndig;
+    // work items: each row is cut into nchunks chunks of chunk_vecs vectors
+    // (the last one shorter) so that few long rows still fill the GPU
+    uint32_t chunk_vecs;
+    FastDiv nchunks;
+    uint32_t nitems;           // nrows * nchunks
     RowDigit dig[kMaxRank];    // destination dims 1..r-1, fastest first
 };
 

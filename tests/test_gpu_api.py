@@ -395,3 +395,33 @@ def test_c_api_demo_program(cuda, tmp_path):
     assert res.returncode == 0, res.stdout + res.stderr
     assert "permute: 0 mismatches" in res.stdout
     assert "sharded exchange (G=4): 0 mismatches" in res.stdout
+
+
+@pytest.mark.parametrize("shape,axes,elem", [
+    ((5, 3, 99, 29, 95), (1, 0, 2, 3, 4), 4),       # 15 rows of 272745 words: rows cut into chunks
+    ((3, 2, 61, 1001), (1, 0, 2, 3), 8),            # 6 rows of 61061 words, odd length
+    ((7, 5, 1, 20011), (1, 0, 2, 3), 2),            # prime row length, 2-byte words
+    ((2, 3, 7, 4097), (1, 0, 2, 3), 16),            # 16-byte words
+])
+def test_rows_kernel_few_long_rows(cuda, shape, axes, elem):
+    """Few long rows are cut into chunks (work items) so they fill the GPU;
+    every chunk boundary and the short last chunk land bit-exact."""
+    import torch
+
+    import paper_2506_03686_b200 as vp
+    from paper_2506_03686_b200.api import execute_device
+
+    n = int(np.prod(shape))
+    prog = vp.build_program(vp.TensorLayout.from_shape(shape, elem), vp.from_numpy_convention(axes))
+    assert prog.kernel == "rows"
+    words = np.random.default_rng(elem).integers(0, 256, size=n * elem, dtype=np.uint8)
+    x = torch.from_numpy(words).cuda()
+    y = execute_device(prog, x)
+    want = np.ascontiguousarray(np.transpose(words.view(f"V{elem}").reshape(shape), axes)).reshape(-1).view(np.uint8)
+    assert np.array_equal(y.cpu().numpy().reshape(-1), want)
+    # misaligned base pointer: narrower vectors, same chunking
+    xb = torch.empty(n * elem + 16, dtype=torch.uint8, device="cuda")
+    xs = xb[elem:elem + n * elem]
+    xs.copy_(x)
+    y2 = execute_device(prog, xs)
+    assert np.array_equal(y2.cpu().numpy().reshape(-1), want)
