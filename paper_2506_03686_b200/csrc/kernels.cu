@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(256) copy_kernel_chunked(const uint4 *__restri
 // RPW consecutive destination rows with U vectors per lane per row in
 // flight before the stores (U = 4, RPW = 2 measured best on cfg4: 346.8 vs
 // 351.3 us for one row at a time, 353.2 for U = 8).
-template <typename V, int U, int RPW, bool CHUNKED>
+template <typename V, int U, int RPW, bool CHUNKED, bool EXACT>
 __global__ void __launch_bounds__(256) rows_kernel(const __grid_constant__ RowsParams p,
                                                    const V *__restrict__ src, V *__restrict__ dst,
                                                    uint32_t vec_log2) {
@@ -110,24 +110,21 @@ __global__ void __launch_bounds__(256) rows_kernel(const __grid_constant__ RowsP
             maxlen = max(maxlen, len[r]);
         }
         if constexpr (!CHUNKED) maxlen = rv;
-        uint32_t i = lane;
-        for (; i + (U - 1) * tpr < maxlen; i += U * tpr) {
+        // every block of U x tpr vectors is loaded before it is stored,
+        // predicated at the row end, so short rows keep U loads in flight
+        for (uint32_t i = lane; i < maxlen; i += U * tpr) {
             V v[RPW][U];
 #pragma unroll
             for (int r = 0; r < RPW; ++r)
 #pragma unroll
                 for (int u = 0; u < U; ++u)
-                    if (CHUNKED ? i + u * tpr < len[r] : len[r] != 0) v[r][u] = ld_stream(s[r] + i + u * tpr);
+                    if (EXACT ? len[r] != 0 : i + u * tpr < len[r]) v[r][u] = ld_stream(s[r] + i + u * tpr);
 #pragma unroll
             for (int r = 0; r < RPW; ++r)
 #pragma unroll
                 for (int u = 0; u < U; ++u)
-                    if (CHUNKED ? i + u * tpr < len[r] : len[r] != 0) d[r][i + u * tpr] = v[r][u];
+                    if (EXACT ? len[r] != 0 : i + u * tpr < len[r]) d[r][i + u * tpr] = v[r][u];
         }
-        for (; i < maxlen; i += tpr)
-#pragma unroll
-            for (int r = 0; r < RPW; ++r)
-                if (i < len[r]) d[r][i] = ld_stream(s[r] + i);
     }
 }
 
@@ -325,8 +322,10 @@ vpg_status launch_rows(const vpg_plan *p, const void *src, void *dst, cudaStream
             rp.nchunks = make_fastdiv((uint32_t)nch);
             rp.nitems = (uint32_t)(rp.nrows * nch);
         }
-        uint32_t tpr = 32;
-        while (tpr > 1 && tpr / 2 >= rp.chunk_vecs) tpr >>= 1;
+        // lanes per row (work item): enough that each lane moves at most
+        // U = 4 vectors per pass; short rows share a warp
+        uint32_t tpr = 1;
+        while (tpr < 32 && tpr * 4 < rp.chunk_vecs) tpr <<= 1;
         rp.tpr_log2 = 0;
         while ((1u << rp.tpr_log2) < tpr) ++rp.tpr_log2;
     }
@@ -334,7 +333,9 @@ vpg_status launch_rows(const vpg_plan *p, const void *src, void *dst, cudaStream
     need /= 256;
 #define VPG_ROWS_LAUNCH(TYPE, U, R)                                                            \
     {                                                                                          \
-        auto k = rp.nchunks.d > 1 ? rows_kernel<TYPE, U, R, true> : rows_kernel<TYPE, U, R, false>; \
+        auto k = rp.nchunks.d > 1 ? rows_kernel<TYPE, U, R, true, false>                       \
+                 : (rp.row_vecs % ((U) << rp.tpr_log2) == 0 ? rows_kernel<TYPE, U, R, false, true>  \
+                                                             : rows_kernel<TYPE, U, R, false, false>); \
         int nb = occupancy(k, 256, 0);                                                         \
         int64_t grid = std::min<int64_t>(need, (int64_t)nb * sm_count_for_current());          \
         if (grid < 1) grid = 1;                                                                \

@@ -907,6 +907,18 @@ static bool refine_for_shards(int rank, const int64_t *dims, const int32_t *sigm
     return true;
 }
 
+// Stride-1-preserving permutations go to the ROWS kernel when its rows are
+// long enough and 16-byte vectorisable; rows of odd length fall back to
+// narrow accesses there, and the tile kernel (aligned-superset reads) moves
+// them faster unless they are long 8-byte rows (tools/shape_ab.py: 69 x 8 B
+// rows 0.56 vs 0.98 of copy through the tile kernel; 1001 x 4 B 0.58 vs 0.79;
+// 1025 x 8 B 0.85 both).
+static bool rows_suitable(int64_t Lr, int E) {
+    const int64_t V = std::max(1, 16 / E);
+    if (Lr * E < kRowsMinBytes) return false;
+    return Lr % V == 0 || (E >= 8 && Lr * E >= 2048);
+}
+
 // ----------------------------------------------------------------- plan
 static void describe(vpg_plan *p) {
     char buf[4096];
@@ -1078,7 +1090,7 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         p->copy.n = P.n;
         p->threads = 256;
         p->grid_hint = 148 * 8;
-    } else if (P.sigma[0] == 0 && P.d[0] * E >= kRowsMinBytes && !(flags & VPG_FORCE_TILE)) {
+    } else if (P.sigma[0] == 0 && rows_suitable(P.d[0], E) && !(flags & VPG_FORCE_TILE)) {
         p->kernel_class = VPG_KERNEL_ROWS;
         RowsParams &rp = p->rows;
         int64_t Lr = P.d[0];

@@ -398,9 +398,9 @@ def test_c_api_demo_program(cuda, tmp_path):
 
 
 @pytest.mark.parametrize("shape,axes,elem", [
-    ((5, 3, 99, 29, 95), (1, 0, 2, 3, 4), 4),       # 15 rows of 272745 words: rows cut into chunks
-    ((3, 2, 61, 1001), (1, 0, 2, 3), 8),            # 6 rows of 61061 words, odd length
-    ((7, 5, 1, 20011), (1, 0, 2, 3), 2),            # prime row length, 2-byte words
+    ((5, 3, 96, 29, 95), (1, 0, 2, 3, 4), 4),       # 15 rows of 264480 words: rows cut into chunks
+    ((3, 2, 61, 1001), (1, 0, 2, 3), 8),            # 6 rows of 61061 words, odd length (8-byte words)
+    ((7, 5, 1, 20016), (1, 0, 2, 3), 2),            # 2-byte words
     ((2, 3, 7, 4097), (1, 0, 2, 3), 16),            # 16-byte words
 ])
 def test_rows_kernel_few_long_rows(cuda, shape, axes, elem):
