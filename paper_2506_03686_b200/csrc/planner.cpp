@@ -719,7 +719,11 @@ double tile_cost(const Problem &Pb, const TileParams &tp) {
         const double ops = nwarps * d.n_in * std::ceil((double)d.n_outer / d.ngroups);
         const double avg_w = (double)waves / (double)warps;
         const bool checked = d.mask_full != 0;
-        if (ph == 0) cost += ops * (4.0 + avg_w + (checked ? 2.0 : 0.0));           // LDGSTS: ~4 issue + smem
+        // LDGSTS: issue + global request + smem; 8 (was 4) lets 16-byte
+        // aligned-superset reads win over 4-byte ones on misaligned runs
+        // (odd 2-D transposes 0.70 -> 0.78 of copy; random-shape p10 +1-3%)
+        const double kr = getenv("VPG_R_OP_COST") ? atof(getenv("VPG_R_OP_COST")) : 8.0;
+        if (ph == 0) cost += ops * (kr + avg_w + (checked ? 2.0 : 0.0));
         else cost += ops * (avg_w + (V > 1 ? V : 1) + 1.0 + (checked ? 2.0 : 0.0)); // LDS + STGs
     }
     return cost;
@@ -759,6 +763,9 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
             vc.rshift = op.rshift;
             fill_tile_params(Pb, g, pitch, NT, vc, tp);
             double c = tile_cost(Pb, tp);
+            if (getenv("VPG_DEBUG_PLAN"))
+                fprintf(stderr, "[plan] Ls %lld Ld %lld pitch %u vr %d vw %d shift %d cost %.1f per-elem %.3f\n",
+                        (long long)g.Ls, (long long)g.Ld, pitch, vc.vr, vc.vw, (int)vc.rshift, c, c / (double)g.T);
             if (best < 0 || c < best - 1e-9) {
                 best = c;
                 pitch_out = pitch;
