@@ -425,3 +425,23 @@ def test_rows_kernel_few_long_rows(cuda, shape, axes, elem):
     xs.copy_(x)
     y2 = execute_device(prog, xs)
     assert np.array_equal(y2.cpu().numpy().reshape(-1), want)
+
+
+def test_env_measured_planning(cuda, monkeypatch):
+    """VPG_TUNE=1: large tile plans are tuned on first build, bit-exact,
+    and later builds return the tuned program."""
+    import torch
+
+    import paper_2506_03686_b200 as vp
+    from paper_2506_03686_b200.api import execute_device
+
+    monkeypatch.setenv("VPG_TUNE", "1")
+    vp.program_cache_clear()
+    shape, axes = (1031, 4099), (1, 0)
+    lay, pm = vp.TensorLayout.from_shape(shape, 4), vp.from_numpy_convention(axes)
+    p = vp.build_program(lay, pm)
+    assert p.kernel == "tile" and p.metadata.get("tuned_ms", 0) > 0
+    assert vp.build_program(lay, pm) is p
+    x = torch.randint(-2**31, 2**31 - 1, shape, dtype=torch.int32, device="cuda")
+    assert torch.equal(execute_device(p, x), x.permute(axes).contiguous())
+    vp.program_cache_clear()
