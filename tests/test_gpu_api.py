@@ -445,3 +445,37 @@ def test_env_measured_planning(cuda, monkeypatch):
     x = torch.randint(-2**31, 2**31 - 1, shape, dtype=torch.int32, device="cuda")
     assert torch.equal(execute_device(p, x), x.permute(axes).contiguous())
     vp.program_cache_clear()
+
+
+def test_rows_kernel_random_campaign(cuda):
+    """Stride-1-preserving permutations of random shapes and word sizes (the
+    ROWS kernel's row/chunk/lane-count choices, and the tile kernel where
+    rows are narrow): bit-exact against numpy, aligned and offset bases."""
+    import torch
+
+    import paper_2506_03686_b200 as vp
+    from paper_2506_03686_b200.api import execute_device
+
+    rng = np.random.default_rng(77)
+    kinds = set()
+    for it in range(60):
+        E = int(rng.choice([1, 2, 4, 8, 16]))
+        r = int(rng.integers(2, 5))
+        lead = [int(rng.integers(1, 12)) for _ in range(r - 1)]
+        row = int(rng.choice([int(rng.integers(1, 3000)), int(rng.integers(3000, 200000))]))
+        shape = tuple(lead + [row])
+        n = int(np.prod(shape))
+        if n * E > (64 << 20):
+            continue
+        axes = tuple(int(a) for a in rng.permutation(r - 1)) + (r - 1,)
+        prog = vp.build_program(vp.TensorLayout.from_shape(shape, E), vp.from_numpy_convention(axes))
+        kinds.add(prog.kernel)
+        words = rng.integers(0, 256, size=n * E, dtype=np.uint8)
+        want = np.ascontiguousarray(np.transpose(words.view(f"V{E}").reshape(shape), axes)).reshape(-1).view(np.uint8)
+        off = int(rng.choice([0, E, 16]))
+        buf = torch.empty(n * E + 32, dtype=torch.uint8, device="cuda")
+        x = buf[off:off + n * E]
+        x.copy_(torch.from_numpy(words))
+        y = execute_device(prog, x)
+        assert np.array_equal(y.cpu().numpy().reshape(-1), want), (shape, axes, E, off, prog.kernel)
+    assert "rows" in kinds
