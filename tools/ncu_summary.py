@@ -110,8 +110,9 @@ def main():
     for lab, row in zip(labels, rows):
         vals = {k: value(hdr, units, row, m, s) for k, (m, s) in METRICS.items()}
         kname = row[hdr.index("Kernel Name")].split("(")[0].replace("void ", "")
-        wl = CONFIGS.get(lab)
-        alg = wl.algorithmic_bytes if wl else None
+        base_cfg, _, shards = lab.partition("/")          # "cfg5/2": one rank's exchange kernel of 2
+        wl = CONFIGS.get(base_cfg)
+        alg = wl.algorithmic_bytes // (int(shards) if shards else 1) if wl else None
         traffic = (vals["dram_read"] or 0) + (vals["dram_write"] or 0)
         e = {"kernel": kname, **vals, "dram_bytes": traffic, "algorithmic_bytes": alg,
              "traffic_ratio": traffic / alg if alg else None}

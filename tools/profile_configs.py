@@ -4,7 +4,8 @@
   ncu --set full --clock-control none --import-source on --nvtx \
       --nvtx-include "capture/" -o gpurun_out/full_rN python tools/profile_configs.py
 
-Order: cfg5, cfg4, cfg3, cfg1, cfg2 (labels for tools/ncu_summary.py)."""
+Order: cfg5, cfg4, cfg3, cfg1, cfg2, then the cfg5 exchange kernel of
+rank 0 of 2 (label cfg5/2; labels for tools/ncu_summary.py)."""
 import os
 import sys
 
@@ -28,10 +29,25 @@ for k in ORDER:
     execute_device(prog, x, out=y)          # compile/load outside the capture
     runs.append((k, prog, x, y))
     print(k, prog.kernel, prog.metadata["src_run"], prog.metadata["dst_run"], flush=True)
+# the fused sharded exchange kernel of rank 0 of 2 (cfg5), both output
+# shards local (tools/exchange_probe.py): label "cfg5/2"
+import ctypes  # noqa: E402
+
+from paper_2506_03686_b200.api import launch_sharded  # noqa: E402
+from paper_2506_03686_b200.sharded import _programs  # noqa: E402
+
+wl5 = CONFIGS["cfg5"]
+xprog = _programs(wl5.shape, wl5.axes, 8, 2, [0])[0]
+x5 = runs[0][2]
+outs = [torch.empty(wl5.numel * 8 // 2, dtype=torch.uint8, device=dev) for _ in range(2)]
+sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+launch_sharded(xprog, x5.data_ptr(), [o.data_ptr() for o in outs], sp)
 torch.cuda.synchronize()
 torch.cuda.nvtx.range_push("capture")
 for k, prog, x, y in runs:
     for _ in range(2):
         execute_device(prog, x, out=y)
+for _ in range(2):
+    launch_sharded(xprog, x5.data_ptr(), [o.data_ptr() for o in outs], sp)
 torch.cuda.synchronize()
 torch.cuda.nvtx.range_pop()
