@@ -118,6 +118,12 @@ struct PhaseDesc {
     uint32_t mask_full;            // slots checked in every tile (padding)
     uint32_t mask_ragged;          // slots checked in ragged tiles
     uint32_t off_tab;              // smem byte offset of this phase's outer table
+    // shifted-run mode only: 16-byte chunk swizzle of the smem rows.  Chunk
+    // j of row r = s / pitch lives at chunk j ^ ((r >> (swz - 1)) & 7), so
+    // the W lanes, which read one column across consecutive rows, spread
+    // over all banks (swz = 0: off; pitch is a multiple of 8 chunks)
+    uint32_t swz;
+    FastDiv spitch;                // divides an smem element offset by the pitch
 };
 
 struct TileParams {

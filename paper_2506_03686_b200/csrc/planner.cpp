@@ -67,6 +67,7 @@ struct Problem {
     int64_t cta_smem;     // per-CTA shared-memory target (bytes)
     bool no_shift = false; // disable shifted-run reads (VPG_NO_SHIFT)
     bool no_bulk = true;   // TMA bulk source reads are opt-in (VPG_BULK=1)
+    bool no_swz = true;    // shifted-run chunk swizzle is opt-in (VPG_SWZ=1)
     int r;
     int64_t d[kMaxRank];
     int sigma[kMaxRank];
@@ -315,6 +316,7 @@ struct VecChoice {
     int vr = 1, vw = 1;
     bool rshift = false;   // R reads 16-byte aligned supersets of misaligned runs
     bool bulk = false;     // R as one cp.async.bulk per source run (producer warp + mbarriers)
+    int swz = 0;           // shifted-run mode: chunk swizzle (0 off, else 1 + row shift)
 };
 
 // smem strides of the tile dims for a given pitch (source run dense, run
@@ -528,7 +530,13 @@ double make_phase(const std::vector<PDimH> &L, int NT, PhaseDesc &pd, uint32_t &
 
 // smem element offsets seen by the lanes of one warp at inner step 0 of its
 // first outer entry (simulation of the kernel's mapping, for the bank model).
-void phase_warp_offsets(const PhaseDesc &pd, int warp, uint32_t *off, int &nl, uint32_t hmask = 0) {
+uint32_t host_swizzle(const PhaseDesc &pd, uint32_t s, int V) {
+    if (!pd.swz) return s;
+    const uint32_t P = pd.spitch.d, r = s / P, c = s - r * P, f = (r >> (pd.swz - 1)) & 7u;
+    return r * P + ((((c / V) ^ f) * V) | (c % V));
+}
+
+void phase_warp_offsets(const PhaseDesc &pd, int warp, uint32_t *off, int &nl, uint32_t hmask = 0, int V = 1) {
     nl = 0;
     for (int l = 0; l < 32; ++l) {
         uint32_t t = (uint32_t)(warp * 32 + l);
@@ -548,7 +556,7 @@ void phase_warp_offsets(const PhaseDesc &pd, int warp, uint32_t *off, int &nl, u
             h += (o - q * pd.out[i].div.d) * pd.out[i].hmul;
             o = q;
         }
-        off[nl++] = s + (h & hmask);
+        off[nl++] = host_swizzle(pd, s + (h & hmask), V);
     }
 }
 
@@ -606,6 +614,12 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
     double u1 = make_phase(phase_dims(Pb, g, sstr, slot_of_dim, true, vc.vw, hmask), NT, tp.ph[1], tp.lim_split[1]);
     tp.ph[0].rshift = vc.rshift ? 1u : 0u;
     tp.hmask = (uint32_t)hmask;
+    if (vc.swz && vc.rshift && vc.vw == 1 && !vc.bulk) {
+        for (int ph = 0; ph < 2; ++ph) {
+            tp.ph[ph].swz = (uint32_t)vc.swz;
+            tp.ph[ph].spitch = make_fastdiv(pitch);
+        }
+    }
     if (vc.bulk) {
         tp.bulk = 1;
         tp.nruns = (uint32_t)(g.T / g.Ls);
@@ -707,7 +721,7 @@ double tile_cost(const Problem &Pb, const TileParams &tp) {
         const int abytes = Pb.E * V;
         int64_t waves = 0, warps = 0;
         for (int w = 0; w < 8; ++w) {
-            phase_warp_offsets(d, w, off, nl, ph == 1 ? tp.hmask : 0);
+            phase_warp_offsets(d, w, off, nl, ph == 1 ? tp.hmask : 0, 16 / Pb.E > 0 ? 16 / Pb.E : 1);
             if (!nl) continue;
             for (int l = 0; l < nl; ++l) off[l] /= (uint32_t)V;     // in access units
             waves += warp_wavefronts(off, nl, abytes);
@@ -751,6 +765,31 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
         }
     if (rs) opts.push_back({V, 1, true});
     for (const Opt &op : opts) {
+        if (op.rshift && !Pb.no_swz) {
+            // swizzled rows: pitch a multiple of 8 chunks, row shift 0..3
+            const int64_t base = (g.Ls + V - 1 + V - 1) / V * V;
+            const int64_t p8 = (base + 8 * V - 1) / (8 * V) * (8 * V);
+            for (int sw = 1; sw <= 4; ++sw) {
+                const uint32_t pitch = (uint32_t)p8;
+                if ((int64_t)(g.T / g.Ls) * pitch * Pb.E > Pb.budget + 16384) break;
+                TileParams tp;
+                VecChoice vc;
+                vc.vr = op.vr;
+                vc.vw = op.vw;
+                vc.rshift = true;
+                vc.swz = sw;
+                fill_tile_params(Pb, g, pitch, NT, vc, tp);
+                double c = tile_cost(Pb, tp);
+                if (getenv("VPG_DEBUG_PLAN"))
+                    fprintf(stderr, "[plan] Ls %lld Ld %lld pitch %u shift-swizzle %d cost %.1f per-elem %.3f\n",
+                            (long long)g.Ls, (long long)g.Ld, pitch, sw, c, c / (double)g.T);
+                if (best < 0 || c < best - 1e-9) {
+                    best = c;
+                    pitch_out = pitch;
+                    vc_out = vc;
+                }
+            }
+        }
         const int step = (op.vr > 1 || op.vw > 1) ? V : 1;
         const int64_t base = op.rshift ? (g.Ls + V - 1 + V - 1) / V * V : g.Ls;
         for (int pad = 0; pad <= 32; pad += step) {
@@ -955,6 +994,7 @@ static void describe(vpg_plan *p) {
                 ph ? "W" : "R", d.nthr, d.ngroups, d.nthr_dims, d.n_in, d.n_outer, d.nout_dims,
                 d.mask_full, d.mask_ragged);
         }
+        if (t.ph[0].swz) put("smem chunk swizzle: row >> %u\n", t.ph[0].swz - 1);
         put("vector elems: R %u%s, W %u\n", t.ph[0].vec,
             t.bulk ? " (TMA bulk copy per source run, producer warp)"
                    : (t.ph[0].rshift ? " (aligned supersets of misaligned runs)" : ""),
@@ -1009,6 +1049,10 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
     if (const char *e = getenv("VPG_PERSIST")) persist_mode = atoi(e);
     if (const char *e = getenv("VPG_THREADS")) force_threads = atoi(e);
     if (getenv("VPG_NO_SHIFT")) P.no_shift = true;
+    // the chunk swizzle removes the W bank conflicts of shifted runs but costs
+    // a divide and a few integer ops per element: measured 28.4 vs 20.5 us on
+    // cfg3, 216 vs 247 us on an odd 8-byte 2-D transpose -- opt-in
+    if (const char *e = getenv("VPG_SWZ")) P.no_swz = atoi(e) == 0;
     // TMA bulk copies per source run measured slower than per-lane 16-byte
     // cp.async on B200 (one bulk op per 256 B-1 KiB run costs more TMA issue
     // time than it saves): opt-in only, VPG_BULK=1

@@ -137,6 +137,16 @@ struct Lim {
     uint32_t l0, l1, l2;
 };
 
+// Physical smem element offset of logical offset s under the chunk swizzle
+// (V elements per 16-byte chunk).
+template <int V>
+__device__ __forceinline__ uint32_t swizzle(const PhaseDesc &d, uint32_t s) {
+    const uint32_t r = fdiv(s, d.spitch);
+    const uint32_t c = s - r * d.spitch.d;
+    const uint32_t f = (r >> (d.swz - 1)) & 7u;
+    return r * d.spitch.d + ((((c / V) ^ f) * V) | (c % V));
+}
+
 __device__ __forceinline__ bool slot_ok(uint32_t mask, uint32_t c0, uint32_t c1, uint32_t c2, const Lim &lim) {
     return (!(mask & 1u) || c0 < lim.l0) && (!(mask & 2u) || c1 < lim.l1) && (!(mask & 4u) || c2 < lim.l2);
 }
@@ -252,12 +262,13 @@ __device__ __forceinline__ void tile_read_shift(const PhaseDesc &d, const Thread
         for (uint32_t i = 0; i < n_in; ++i) {
             if (mask == 0 || slot_ok(mask, c0, c1, c2, lim)) {
                 const W *ga = reinterpret_cast<const W *>((uintptr_t)gp & ~(uintptr_t)15);
+                W *sd = d.swz ? buf + swizzle<V>(d, (uint32_t)(sp - buf)) : sp;   // chunk-aligned: whole chunk moves
                 if (ga + V <= gend) {
-                    cp_async<16>(sp, ga);
+                    cp_async<16>(sd, ga);
                 } else {
 #pragma unroll
                     for (int j = 0; j < V; ++j)
-                        if (ga + j < gend) cp_async<sizeof(W)>(sp + j, ga + j);
+                        if (ga + j < gend) cp_async<sizeof(W)>(sd + j, ga + j);
                 }
             }
             gp += g_in;
@@ -328,7 +339,10 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
                 } else {
                     W v[U];
 #pragma unroll
-                    for (int u = 0; u < U; ++u) v[u] = sp[u * s_in + ((hh + u * h_in) & hmask)];
+                    for (int u = 0; u < U; ++u) {
+                        const uint32_t so = (uint32_t)(sp - buf) + u * s_in + ((hh + u * h_in) & hmask);
+                        v[u] = buf[d.swz ? swizzle<16 / (int)sizeof(W)>(d, so) : so];
+                    }
 #pragma unroll
                     for (int u = 0; u < U; ++u) st_out(gp + u * g_in, v[u]);
                 }
@@ -343,7 +357,8 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
 #pragma unroll
                     for (int j = 0; j < V; ++j) st_out(gp + j * vs, w[j]);
                 } else {
-                    *gp = sp[hh & hmask];
+                    const uint32_t so = (uint32_t)(sp - buf) + (hh & hmask);
+                    *gp = buf[d.swz ? swizzle<16 / (int)sizeof(W)>(d, so) : so];
                 }
                 gp += g_in;
                 sp += s_in;
@@ -360,7 +375,8 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
 #pragma unroll
                         for (int j = 0; j < V; ++j) st_out(gp + j * vs, w[j]);
                     } else {
-                        *gp = sp[hh & hmask];
+                        const uint32_t so = (uint32_t)(sp - buf) + (hh & hmask);
+                        *gp = buf[d.swz ? swizzle<16 / (int)sizeof(W)>(d, so) : so];
                     }
                 }
                 gp += g_in;

@@ -40,7 +40,8 @@ class PhaseDesc(ctypes.Structure):
                 ("s_in", ctypes.c_uint32), ("c_in", ctypes.c_uint32 * 3), ("n_outer", ctypes.c_uint32),
                 ("nout_dims", ctypes.c_int32), ("out", PhaseDim * MAXPD), ("vec", ctypes.c_uint32),
                 ("rshift", ctypes.c_uint32), ("h_in", ctypes.c_uint32), ("vstride", ctypes.c_int64),
-                ("mask_full", ctypes.c_uint32), ("mask_ragged", ctypes.c_uint32), ("off_tab", ctypes.c_uint32)]
+                ("mask_full", ctypes.c_uint32), ("mask_ragged", ctypes.c_uint32), ("off_tab", ctypes.c_uint32),
+                ("swz", ctypes.c_uint32), ("spitch", FastDiv)]
 
 
 class GridDigit(ctypes.Structure):
@@ -220,11 +221,14 @@ def simulate(program, src_words: np.ndarray, threads: int | None = None, shard_o
                             gabs = sb + gp
                             if d.rshift:
                                 ga = gabs - (gabs % V)
+                                if d.swz and (sp % V).any():
+                                    raise SimError("swizzled R chunk not chunk-aligned")
+                                sd = _swizzle(d, sp, V)
                                 for j in range(V):
                                     inb = ga + j < n
-                                    _chk(sp[inb] + j, alloc, "R shifted smem")
-                                    smem[sp[inb] + j] = src_words[ga[inb] + j]
-                                    smem_valid[sp[inb] + j] = True
+                                    _chk(sd[inb] + j, alloc, "R shifted smem")
+                                    smem[sd[inb] + j] = src_words[ga[inb] + j]
+                                    smem_valid[sd[inb] + j] = True
                             else:
                                 if V > 1 and ((gabs % V).any() or (sp % V).any()):
                                     raise SimError("R vector access misaligned")
@@ -235,7 +239,7 @@ def simulate(program, src_words: np.ndarray, threads: int | None = None, shard_o
                                     smem_valid[sp + j] = True
                         else:
                             hh = (sb + th[sel][ok] + eh[0] + i * d.h_in) & tp.hmask if tp.hmask else 0
-                            spx = sp + hh
+                            spx = _swizzle(d, sp + hh, 16 // E if E <= 16 else 1)
                             gabs = db + gp
                             if V > 1 and (spx % V).any():
                                 raise SimError("W vector smem access misaligned")
@@ -270,6 +274,17 @@ def simulate_exchange(programs, src_words: np.ndarray) -> np.ndarray:
         bad = np.nonzero(c != 1)[0][:5]
         raise SimError(f"destination elements written {c[bad]} times at {bad}")
     return np.concatenate(dsts)
+
+
+def _swizzle(d, s, V):
+    """Chunk swizzle of smem element offsets (tile_body.cuh swizzle<V>)."""
+    if not d.swz:
+        return s
+    P = d.spitch.d
+    r = s // P
+    c = s - r * P
+    f = (r >> (d.swz - 1)) & 7
+    return r * P + (((c // V) ^ f) * V) + (c % V)
 
 
 def _chk(idx, bound, what):

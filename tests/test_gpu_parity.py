@@ -260,3 +260,37 @@ def test_negative_controls(cuda):
         assert not np.array_equal(wrong, want)
         ran += 1
     assert ran >= 10
+
+
+@pytest.mark.parametrize("jit", [False, True])
+def test_swizzled_shifted_rows_opt_in(cuda, jit, monkeypatch):
+    """The opt-in chunk swizzle of shifted rows (VPG_SWZ=1) stays bit-exact
+    on misaligned shapes, specialised and ahead-of-time kernels."""
+    import torch
+
+    import paper_2506_03686_b200 as vp
+    from paper_2506_03686_b200.api import execute_device
+
+    monkeypatch.setenv("VPG_SWZ", "1")
+    vp.program_cache_clear()
+    rng = np.random.default_rng(5)
+    done = 0
+    for _ in range(200):
+        r = int(rng.integers(2, 6))
+        shape = tuple(int(x) for x in rng.integers(2, 40, size=r))
+        axes = tuple(int(a) for a in rng.permutation(r))
+        E = int(rng.choice([4, 8]))
+        prog = vp.build_program(vp.TensorLayout.from_shape(shape, E), vp.from_numpy_convention(axes),
+                                force="tile", jit=jit)
+        if "swizzle" not in prog.text:
+            continue
+        n = int(np.prod(shape))
+        x = torch.randint(-2**31, 2**31 - 1, (n * E // 4,), dtype=torch.int32, device="cuda")
+        xv = x.view(torch.int32 if E == 4 else torch.int64).view(shape)
+        y = execute_device(prog, x.view(torch.uint8))
+        assert torch.equal(y.view(xv.dtype).view(-1), xv.permute(axes).reshape(-1)), (shape, axes, E)
+        done += 1
+        if done >= (6 if jit else 20):
+            break
+    vp.program_cache_clear()
+    assert done >= 5

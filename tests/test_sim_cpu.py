@@ -152,3 +152,30 @@ def test_sim_negative_controls():
         except SimError:
             continue
         assert not np.array_equal(got, want), f"corruption of {what} went unnoticed"
+
+
+def test_sim_swizzled_shifted_rows(monkeypatch):
+    """Plans with the shifted-run chunk swizzle (misaligned runs, opt-in
+    VPG_SWZ=1) replay bit-exact: R writes and W reads agree on the layout."""
+    monkeypatch.setenv("VPG_SWZ", "1")
+    vp.program_cache_clear()
+    rng = np.random.default_rng(11)
+    n_swz = 0
+    for _ in range(120):
+        r = int(rng.integers(2, 6))
+        shape = tuple(int(x) for x in rng.integers(2, 30, size=r))
+        axes = tuple(int(a) for a in rng.permutation(r))
+        E = int(rng.choice([4, 8]))
+        prog = vp.build_program(vp.TensorLayout.from_shape(shape, E), vp.from_numpy_convention(axes), force="tile")
+        if "swizzle" not in prog.text:
+            continue
+        n = prog.num_elements
+        words = rng.integers(0, 2**63, size=n, dtype=np.uint64)
+        words = words.view(np.uint32)[:n].copy() if E == 4 else words
+        dims, sigma = oracle.from_numpy_axes(shape, axes)
+        assert np.array_equal(simulate(prog, words), oracle.naive_permute_c(words, dims, sigma)), (shape, axes, E)
+        n_swz += 1
+        if n_swz >= 25:
+            break
+    vp.program_cache_clear()
+    assert n_swz >= 10
