@@ -138,6 +138,15 @@ vpg_status vpg_permute_host(const vpg_plan *plan, const void *host_src, void *ho
 vpg_status vpg_permute_host_async(const vpg_plan *plan, const void *host_src, void *host_dst,
                                   void *dev_src, void *dev_dst, void *cuda_stream);
 
+/* Host buffers larger than the device: the permutation is cut into chunks
+ * along dims that are outer on both sides and streamed through a ring of
+ * slots in `dev_scratch` (scratch_bytes of device memory; each slot holds
+ * one input and one output chunk, chunks are at most an eighth of the
+ * scratch).  Synchronous.  VPG_EUNSUPPORTED when the tensor cannot be cut
+ * finely enough for the scratch. */
+vpg_status vpg_permute_host_bounded(const vpg_plan *plan, const void *host_src, void *host_dst,
+                                    void *dev_scratch, size_t scratch_bytes, void *cuda_stream);
+
 /* One-shot convenience with an internal plan cache keyed by
  * (dims, sigma, elem_bytes): the closest analog of the reference's
  * shape-specialised kernel call. */

@@ -38,6 +38,7 @@ EXPORTED = (
     "vpg_ipc_release",
     "vpg_permute_host",
     "vpg_permute_host_async",
+    "vpg_permute_host_bounded",
     "vpg_permute_nd",
     "vpg_plan_info_get",
     "vpg_plan_describe",
@@ -112,6 +113,7 @@ def lib():
         L.vpg_ipc_release.argtypes = [vp]
         L.vpg_permute_host.argtypes = [vp, vp, vp, vp, vp, vp]
         L.vpg_permute_host_async.argtypes = [vp, vp, vp, vp, vp, vp]
+        L.vpg_permute_host_bounded.argtypes = [vp, vp, vp, vp, ctypes.c_size_t, vp]
         L.vpg_permute_nd.argtypes = [ctypes.c_int, i64p, i32p, ctypes.c_int, vp, vp, vp]
         L.vpg_plan_info_get.argtypes = [vp, ctypes.POINTER(PlanInfo)]
         L.vpg_plan_describe.argtypes = [vp, ctypes.c_char_p, ctypes.c_size_t]
@@ -123,7 +125,7 @@ def lib():
         for name in ("vpg_merge_dimensions", "vpg_plan_create", "vpg_permute", "vpg_permute_host",
                      "vpg_plan_create_sharded", "vpg_permute_sharded", "vpg_ipc_export", "vpg_ipc_import",
                      "vpg_ipc_release",
-                     "vpg_permute_host_async",
+                     "vpg_permute_host_async", "vpg_permute_host_bounded",
                      "vpg_permute_nd", "vpg_plan_info_get", "vpg_plan_describe", "vpg_plan_emit_source",
                      "vpg_plan_jit_compile", "vpg_plan_tile_params"):
             getattr(L, name).restype = ctypes.c_int

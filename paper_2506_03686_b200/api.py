@@ -474,7 +474,8 @@ def execute_device(program: GpuProgram, x, out=None, stream=None):
     return out
 
 
-def execute(program: GpuProgram, input_buf, trace: bool = False, out=None, stream=None, blocking: bool = True):
+def execute(program: GpuProgram, input_buf, trace: bool = False, out=None, stream=None, blocking: bool = True,
+            max_device_bytes: int | None = None):
     """Run a program; returns ``(output, counters)`` like vm.py:105-110.
 
     * CUDA tensor input -> CUDA output tensor (outer-first output shape).
@@ -486,12 +487,16 @@ def execute(program: GpuProgram, input_buf, trace: bool = False, out=None, strea
       return at once; consecutive calls overlap their transfers.  Call
       ``stream.synchronize()`` (default: the current stream) before reading
       ``out``.
+    * Host tensors larger than the device can stage (or ``max_device_bytes``
+      below twice the tensor): streamed through that much device scratch in
+      chunks (vpg_permute_host_bounded; blocking).
     """
     torch = _torch()
     if isinstance(input_buf, torch.Tensor) and input_buf.is_cuda:
         res = execute_device(program, input_buf, out=out, stream=stream)
         return res, _counters(program)
-    return _execute_host(program, input_buf, out=out, stream=stream, blocking=blocking), _counters(program)
+    return (_execute_host(program, input_buf, out=out, stream=stream, blocking=blocking,
+                          max_device_bytes=max_device_bytes), _counters(program))
 
 
 _scratch: dict = {}
@@ -517,7 +522,7 @@ def release_scratch():
         _scratch.clear()
 
 
-def _execute_host(program: GpuProgram, input_buf, out=None, stream=None, blocking=True):
+def _execute_host(program: GpuProgram, input_buf, out=None, stream=None, blocking=True, max_device_bytes=None):
     torch = _torch()
     if not torch.cuda.is_available():
         raise VpgError("no CUDA device: the permutation runs only on the GPU (no CPU fallback)")
@@ -538,6 +543,13 @@ def _execute_host(program: GpuProgram, input_buf, out=None, stream=None, blockin
                               f"program expects {program.num_elements}")
         hbytes = torch.from_numpy(data.copy() if not data.flags.writeable else data)
     dev = torch.device("cuda", torch.cuda.current_device())
+    need = 2 * program.nbytes
+    if max_device_bytes is None and (id(program), dev.index) not in _scratch:
+        free = torch.cuda.mem_get_info(dev)[0]
+        if need > 0.9 * free:
+            max_device_bytes = int(0.5 * free)
+    if max_device_bytes is not None and max_device_bytes < need and program.num_elements:
+        return _execute_host_bounded(torch, program, hbytes, input_buf, out, stream, dev, int(max_device_bytes))
     d_in, d_out = _host_scratch(torch, program, dev)
     if not blocking and (out is None or not as_tensor or not hbytes.is_pinned() or not out.is_pinned()):
         raise LayoutError("blocking=False needs a pinned CPU tensor input and a pinned `out`")
@@ -554,9 +566,37 @@ def _execute_host(program: GpuProgram, input_buf, out=None, stream=None, blockin
             ctypes.c_void_p(st.cuda_stream))
         _check(status, "permute_host")
     if as_tensor:
-        res = h_out.view(input_buf.dtype) if out is None else out
-        return res.reshape(program.out_layout.shape_outer_first()) if out is None else res
+        if out is not None:
+            return out
+        res = h_out.view(input_buf.dtype)
+        if input_buf.element_size() != program.layout.elem_width:
+            return res                                  # opaque bytes: flat
+        return res.reshape(program.out_layout.shape_outer_first())
     return h_out.numpy().view(lay.dtype)
+
+
+def _execute_host_bounded(torch, program, hbytes, input_buf, out, stream, dev, scratch_bytes):
+    """Host permutation through a bounded device scratch (vpg_permute_host_bounded)."""
+    as_tensor = isinstance(input_buf, torch.Tensor)
+    if out is None:
+        h_out = torch.empty(program.nbytes, dtype=torch.uint8, pin_memory=hbytes.is_pinned())
+    else:
+        h_out = out.reshape(-1).view(torch.uint8)
+    scratch = torch.empty(scratch_bytes, dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream(dev) if stream is None else stream
+    status = _lib.lib().vpg_permute_host_bounded(
+        program.handle, ctypes.c_void_p(hbytes.data_ptr()), ctypes.c_void_p(h_out.data_ptr()),
+        ctypes.c_void_p(scratch.data_ptr()), ctypes.c_size_t(scratch_bytes), ctypes.c_void_p(st.cuda_stream))
+    _check(status, "permute_host_bounded")
+    del scratch
+    if as_tensor:
+        if out is not None:
+            return out
+        res = h_out.view(input_buf.dtype)
+        if input_buf.element_size() != program.layout.elem_width:
+            return res                                  # opaque bytes: flat
+        return res.reshape(program.out_layout.shape_outer_first())
+    return h_out.numpy().view(program.layout.dtype)
 
 
 # ------------------------------------------------------------------ permute

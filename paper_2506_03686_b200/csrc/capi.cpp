@@ -13,6 +13,8 @@
 namespace vpg {
 vpg_status permute_host_pipelined(const vpg_plan *p, const void *host_src, void *host_dst, void *dev_src,
                                   void *dev_dst, cudaStream_t user, bool async, std::string *err);
+vpg_status permute_host_bounded(const vpg_plan *p, const void *host_src, void *host_dst, void *scratch,
+                                size_t scratch_bytes, cudaStream_t user, std::string *err);
 int host_pipeline_chunks(const vpg_plan *p);
 void host_pipeline_forget(const vpg_plan *p);
 }  // namespace vpg
@@ -124,6 +126,17 @@ vpg_status vpg_permute_host(const vpg_plan *plan, const void *host_src, void *ho
     std::string err;
     vpg_status s = vpg::permute_host_pipelined(plan, host_src, host_dst, dev_src, dev_dst, (cudaStream_t)cuda_stream,
                                                false, &err);
+    return s == VPG_OK ? s : fail(s, err);
+}
+
+vpg_status vpg_permute_host_bounded(const vpg_plan *plan, const void *host_src, void *host_dst, void *dev_scratch,
+                                    size_t scratch_bytes, void *cuda_stream) {
+    if (!plan || !host_src || !host_dst || !dev_scratch) return fail(VPG_EINVAL, "null argument");
+    if (plan->shards > 0) return fail(VPG_EINVAL, "sharded plans run through vpg_permute_sharded");
+    if (plan->n == 0) return VPG_OK;
+    std::string err;
+    vpg_status s = vpg::permute_host_bounded(plan, host_src, host_dst, dev_scratch, scratch_bytes,
+                                             (cudaStream_t)cuda_stream, &err);
     return s == VPG_OK ? s : fail(s, err);
 }
 

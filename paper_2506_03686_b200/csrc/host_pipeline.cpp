@@ -85,7 +85,9 @@ bool region_copies(int r, const int64_t *dims, const int64_t *coord, int E, std:
 
 struct PipePlan {
     bool ok = false;
-    std::vector<int> K;            // chunk dims (merged, inner-first source numbering)
+    std::vector<int64_t> dims;     // the dims the chunking works on (the plan's, or a refinement)
+    std::vector<int32_t> sigma;
+    std::vector<int> K;            // chunk dims (inner-first source numbering of `dims`)
     int64_t chunks = 1;
     int64_t chunk_elems = 0;
     vpg_plan *sub = nullptr;       // permutation of one chunk
@@ -94,12 +96,24 @@ struct PipePlan {
 std::mutex g_pipe_mu;
 std::map<const vpg_plan *, PipePlan> g_pipe;   // keyed by parent plan (plans are immutable)
 
-PipePlan build_pipe(const vpg_plan *p) {
+// min_chunks > 0 (bounded device scratch): at least that many chunks, up to
+// kMaxBoundedChunks, whatever the tensor size.
+constexpr int64_t kMaxBoundedChunks = 1 << 16;
+
+PipePlan build_pipe_dims(int r, const int64_t *dims, const int32_t *sigma, int E, int64_t n,
+                         int64_t min_chunks, bool relaxed) {
     PipePlan pp;
-    const int r = p->rank, E = p->elem_bytes;
-    int64_t max_chunks = kMaxChunks;     // the cost model below picks the count
-    if (const char *e = getenv("VPG_HOST_CHUNKS")) max_chunks = std::max(1, std::min(kMaxChunks, atoi(e)));
-    if (p->n * E < kMinPipelineBytes || r < 2 || max_chunks < 2) return pp;
+    struct PlanView {
+        const int64_t *dims;
+        const int32_t *sigma;
+        int64_t n;
+    } pv{dims, sigma, n}, *p = &pv;
+    if (r > kMaxRank) return pp;
+    int64_t max_chunks = min_chunks > 0 ? kMaxBoundedChunks : kMaxChunks;   // the cost model picks the count
+    if (const char *e = getenv("VPG_HOST_CHUNKS"); e && min_chunks == 0)
+        max_chunks = std::max(1, std::min(kMaxChunks, atoi(e)));
+    if (min_chunks > max_chunks) return pp;
+    if ((min_chunks == 0 && p->n * E < kMinPipelineBytes) || r < 2 || max_chunks < 2) return pp;
     int64_t in_stride[kMaxRank], out_stride[kMaxRank], odims[kMaxRank];
     in_stride[0] = 1;
     for (int k = 1; k < r; ++k) in_stride[k] = in_stride[k - 1] * p->dims[k - 1];
@@ -111,9 +125,12 @@ PipePlan build_pipe(const vpg_plan *p) {
         odims[j] = p->dims[p->sigma[j]];
         acc *= odims[j];
     }
+    // bounded scratch: any block length that keeps copies reasonable
+    const int64_t min_block = min_chunks > 0 ? (relaxed ? 512 : (16ll << 10)) : kMinBlockBytes;
+    const int max_copies = min_chunks > 0 ? (relaxed ? (1 << 16) : 4096) : kMaxCopiesPerChunk;
     std::vector<int> cand;
     for (int k = 0; k < r; ++k)
-        if (p->dims[k] >= 2 && std::min(in_stride[k], out_stride[k]) * E >= kMinBlockBytes) cand.push_back(k);
+        if (p->dims[k] >= 2 && std::min(in_stride[k], out_stride[k]) * E >= min_block) cand.push_back(k);
     std::sort(cand.begin(), cand.end(), [&](int a, int b) {
         return std::min(in_stride[a], out_stride[a]) > std::min(in_stride[b], out_stride[b]);
     });
@@ -130,7 +147,7 @@ PipePlan build_pipe(const vpg_plan *p) {
     if (cand.size() > 12) cand.resize(12);
     std::vector<int> K, bestK;
     int64_t C = 1, bestC = 1;
-    double best_t = model(1, 2);
+    double best_t = min_chunks > 1 ? 1e300 : model(1, 2);
     const int nc = (int)cand.size();
     for (uint32_t mask = 1; mask < (1u << nc); ++mask) {
         std::vector<int> K2;
@@ -140,7 +157,7 @@ PipePlan build_pipe(const vpg_plan *p) {
                 K2.push_back(cand[b]);
                 C2 *= p->dims[cand[b]];
             }
-        if (C2 > max_chunks) continue;
+        if (C2 > max_chunks || C2 < min_chunks) continue;
         int64_t ci[kMaxRank], co[kMaxRank];
         for (int q = 0; q < r; ++q) ci[q] = co[q] = -1;
         for (int q : K2) {
@@ -148,10 +165,10 @@ PipePlan build_pipe(const vpg_plan *p) {
             co[pos[q]] = 0;
         }
         std::vector<Copy2D> tin, tout;
-        if (!region_copies(r, p->dims, ci, E, tin, kMaxCopiesPerChunk)) continue;
-        if (tin.empty() || tin[0].width < kMinBlockBytes) continue;
-        if (!region_copies(r, odims, co, E, tout, kMaxCopiesPerChunk)) continue;
-        if (tout.empty() || tout[0].width < kMinBlockBytes) continue;
+        if (!region_copies(r, p->dims, ci, E, tin, max_copies)) continue;
+        if (tin.empty() || tin[0].width < min_block) continue;
+        if (!region_copies(r, odims, co, E, tout, max_copies)) continue;
+        if (tout.empty() || tout[0].width < min_block) continue;
         double t = model(C2, C2 * (int64_t)(tin.size() + tout.size()));
         if (t < best_t - 1e-9) {
             best_t = t;
@@ -168,11 +185,60 @@ PipePlan build_pipe(const vpg_plan *p) {
     for (int k : K) sd[k] = 1;
     std::string err;
     if (vpg::make_plan(r, sd, p->sigma, E, 0, &pp.sub, &err) != VPG_OK) return pp;
+    pp.dims.assign(dims, dims + r);
+    pp.sigma.assign(sigma, sigma + r);
     pp.K = K;
     pp.chunks = C;
     pp.chunk_elems = p->n / C;
     pp.ok = true;
     return pp;
+}
+
+PipePlan build_pipe(const vpg_plan *p, int64_t min_chunks = 0, bool relaxed = false) {
+    return build_pipe_dims(p->rank, p->dims, p->sigma, p->elem_bytes, p->n, min_chunks, relaxed);
+}
+
+// Bounded scratch on a plan whose merged dims offer no dim outer on both
+// sides (a 2-D transpose): split one dim into (inner, outer factor) pieces
+// so the outer factor can be the chunk dim.  Largest dims first, smallest
+// sufficient factor first.
+PipePlan build_pipe_refined(const vpg_plan *p, int64_t min_chunks) {
+    const int r = p->rank;
+    if (r + 1 > VPG_MAX_RANK) return PipePlan{};
+    std::vector<int> order(r);
+    for (int k = 0; k < r; ++k) order[k] = k;
+    std::sort(order.begin(), order.end(), [&](int a, int b) { return p->dims[a] > p->dims[b]; });
+    for (int k : order) {
+        const int64_t d = p->dims[k];
+        for (int64_t f = 2; f <= std::min<int64_t>(d / 2, kMaxBoundedChunks); ++f) {
+            if (d % f) continue;
+            std::vector<int64_t> rd;
+            std::vector<int32_t> rs;
+            for (int q = 0; q < r; ++q) {
+                if (q == k) {
+                    rd.push_back(d / f);
+                    rd.push_back(f);
+                } else {
+                    rd.push_back(p->dims[q]);
+                }
+            }
+            for (int j = 0; j < r; ++j) {
+                const int q = p->sigma[j];
+                if (q == k) {
+                    rs.push_back(k);
+                    rs.push_back(k + 1);
+                } else {
+                    rs.push_back(q > k ? q + 1 : q);
+                }
+            }
+            for (bool relaxed : {false, true}) {
+                PipePlan pp = build_pipe_dims(r + 1, rd.data(), rs.data(), p->elem_bytes, p->n, min_chunks, relaxed);
+                if (pp.ok) return pp;
+                if (pp.sub) vpg_plan_destroy(pp.sub);
+            }
+        }
+    }
+    return PipePlan{};
 }
 
 struct DevStreams {
@@ -375,6 +441,117 @@ vpg_status permute_host_pipelined(const vpg_plan *p, const void *host_src, void 
     for (int64_t j = 0; j < chunks; ++j) {
         cudaEventDestroy(done_in[j]);
         cudaEventDestroy(done_k[j]);
+    }
+    return st;
+}
+
+// Host buffers larger than the device can stage: the tensor is cut into
+// chunks (dims outer on both sides, as above) and streamed through a ring of
+// R = scratch / (2 x chunk) slots of caller-provided device scratch -- H2D
+// of chunk j into slot j % R, its sub-permutation, its D2H -- so the device
+// holds at most R chunks at once.  Synchronous.
+vpg_status permute_host_bounded(const vpg_plan *p, const void *host_src, void *host_dst, void *scratch,
+                                size_t scratch_bytes, cudaStream_t user, std::string *err) {
+    const int E = p->elem_bytes;
+    const int64_t total = p->n * E;
+    // at least four slots in flight: chunks of at most an eighth of the scratch
+    const int64_t min_chunks = std::max<int64_t>(2, (8 * total + (int64_t)scratch_bytes - 1) / (int64_t)scratch_bytes);
+    PipePlan pp = build_pipe(p, min_chunks);
+    if (!pp.ok) {                                        // finer copies before giving up
+        if (pp.sub) vpg_plan_destroy(pp.sub);
+        pp = build_pipe(p, min_chunks, true);
+    }
+    if (!pp.ok) {                                        // split a dim to get a chunk dim
+        if (pp.sub) vpg_plan_destroy(pp.sub);
+        pp = build_pipe_refined(p, min_chunks);
+    }
+    if (!pp.ok) {
+        if (pp.sub) vpg_plan_destroy(pp.sub);
+        *err = "cannot cut this permutation into chunks that fit " + std::to_string(scratch_bytes) +
+               " bytes of device scratch";
+        return VPG_EUNSUPPORTED;
+    }
+    struct SubGuard {
+        vpg_plan *s;
+        ~SubGuard() { if (s) vpg_plan_destroy(s); }
+    } guard{pp.sub};
+    DevStreams s = streams_for_current(err);
+    if (!s.h2d) return VPG_ECUDA;
+    const int64_t cbytes = pp.chunk_elems * E;
+    const int64_t R = std::max<int64_t>(1, (int64_t)scratch_bytes / (2 * cbytes));
+    const int r = (int)pp.dims.size();
+    const int64_t *dims = pp.dims.data();
+    int64_t odims[VPG_MAX_RANK];
+    int pos[VPG_MAX_RANK];
+    for (int j = 0; j < r; ++j) {
+        odims[j] = dims[pp.sigma[j]];
+        pos[pp.sigma[j]] = j;
+    }
+    std::unique_lock<std::mutex> enqueue_lock(g_enqueue_mu);
+    cudaEvent_t start, fin;
+    cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&fin, cudaEventDisableTiming);
+    std::vector<cudaEvent_t> slot_free((size_t)R), done_in((size_t)R), done_k((size_t)R);
+    for (int64_t i = 0; i < R; ++i) {
+        cudaEventCreateWithFlags(&slot_free[i], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&done_in[i], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&done_k[i], cudaEventDisableTiming);
+    }
+    cudaEventRecord(start, user);
+    cudaStreamWaitEvent(s.h2d, start, 0);
+    cudaStreamWaitEvent(s.comp, start, 0);
+    cudaStreamWaitEvent(s.d2h, start, 0);
+    std::vector<Copy2D> cps;
+    vpg_status st = VPG_OK;
+    for (int64_t j = 0; j < pp.chunks && st == VPG_OK; ++j) {
+        const int64_t slot = j % R;
+        char *din = (char *)scratch + slot * 2 * cbytes;
+        char *dout = din + cbytes;
+        if (j >= R) cudaStreamWaitEvent(s.h2d, slot_free[slot], 0);   // chunk j - R has left the slot
+        int64_t ci[VPG_MAX_RANK], co[VPG_MAX_RANK];
+        for (int q = 0; q < r; ++q) ci[q] = co[q] = -1;
+        int64_t rem = j;
+        for (int q : pp.K) {
+            ci[q] = rem % dims[q];
+            co[pos[q]] = ci[q];
+            rem /= dims[q];
+        }
+        region_copies(r, dims, ci, E, cps, 1 << 30);
+        for (const Copy2D &c : cps)
+            if (cudaMemcpy2DAsync(din + c.dev_off, c.width, (const char *)host_src + c.host_off, c.pitch, c.width,
+                                  c.height, cudaMemcpyHostToDevice, s.h2d) != cudaSuccess) {
+                *err = "H2D copy failed";
+                st = VPG_ECUDA;
+            }
+        cudaEventRecord(done_in[slot], s.h2d);
+        cudaStreamWaitEvent(s.comp, done_in[slot], 0);
+        vpg_status ks = launch_plan(pp.sub, din, dout, s.comp, err);
+        if (ks != VPG_OK) st = ks;
+        cudaEventRecord(done_k[slot], s.comp);
+        cudaStreamWaitEvent(s.d2h, done_k[slot], 0);
+        region_copies(r, odims, co, E, cps, 1 << 30);
+        for (const Copy2D &c : cps)
+            if (cudaMemcpy2DAsync((char *)host_dst + c.host_off, c.pitch, dout + c.dev_off, c.width, c.width,
+                                  c.height, cudaMemcpyDeviceToHost, s.d2h) != cudaSuccess) {
+                *err = "D2H copy failed";
+                st = VPG_ECUDA;
+            }
+        cudaEventRecord(slot_free[slot], s.d2h);
+    }
+    cudaEventRecord(fin, s.d2h);
+    cudaStreamWaitEvent(user, fin, 0);
+    enqueue_lock.unlock();
+    cudaError_t e = cudaStreamSynchronize(user);
+    if (e != cudaSuccess && st == VPG_OK) {
+        *err = std::string("stream sync: ") + cudaGetErrorString(e);
+        st = VPG_ECUDA;
+    }
+    cudaEventDestroy(start);
+    cudaEventDestroy(fin);
+    for (int64_t i = 0; i < R; ++i) {
+        cudaEventDestroy(slot_free[i]);
+        cudaEventDestroy(done_in[i]);
+        cudaEventDestroy(done_k[i]);
     }
     return st;
 }

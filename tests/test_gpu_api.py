@@ -479,3 +479,43 @@ def test_rows_kernel_random_campaign(cuda):
         y = execute_device(prog, x)
         assert np.array_equal(y.cpu().numpy().reshape(-1), want), (shape, axes, E, off, prog.kernel)
     assert "rows" in kinds
+
+
+@pytest.mark.parametrize("shape,axes,elem,scratch_mib", [
+    ((64, 48, 40, 512), (2, 0, 3, 1), 4, 64),       # 240 MiB through 64 MiB of scratch
+    ((2,) * 26, tuple(range(25, -1, -1)), 8, 48),    # 512 MiB, rank 26
+    ((96, 130, 4097), (1, 2, 0), 2, 40),             # odd extents, 2-byte words
+])
+def test_host_path_bounded_scratch(cuda, shape, axes, elem, scratch_mib):
+    """Host tensors streamed through device scratch smaller than the tensor
+    (chunk ring): bit-exact, and the device never holds the whole tensor."""
+    import torch
+
+    import paper_2506_03686_b200 as vp
+
+    n = int(np.prod(shape))
+    prog = vp.build_program(vp.TensorLayout.from_shape(shape, elem), vp.from_numpy_convention(axes))
+    words = np.random.default_rng(elem).integers(0, 256, size=n * elem, dtype=np.uint8)
+    x = torch.from_numpy(words).pin_memory()
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated()
+    torch.cuda.reset_peak_memory_stats()
+    out, _ = vp.execute(prog, x, max_device_bytes=scratch_mib << 20)
+    peak = torch.cuda.max_memory_allocated() - base
+    assert peak <= (scratch_mib << 20) + (1 << 20)
+    want = np.ascontiguousarray(np.transpose(words.view(f"V{elem}").reshape(shape), axes)).reshape(-1).view(np.uint8)
+    assert np.array_equal(out.view(torch.uint8).numpy().reshape(-1), want)
+
+
+def test_host_path_bounded_scratch_unsplittable(cuda):
+    """A 2-D transpose of prime extents cannot be cut into chunks: the
+    bounded path reports it (LayoutError), it does not fall back."""
+    import torch
+
+    import paper_2506_03686_b200 as vp
+
+    shape = (1009, 4093)
+    prog = vp.build_program(vp.TensorLayout.from_shape(shape, 4), vp.from_numpy_convention((1, 0)))
+    x = torch.zeros(shape, dtype=torch.int32)
+    with pytest.raises(vp.LayoutError):
+        vp.execute(prog, x, max_device_bytes=1 << 20)
