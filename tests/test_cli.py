@@ -63,3 +63,20 @@ def test_run_against_oracle_file(cuda, tmp_path):
 def test_check_campaign(cuda, capsys):
     assert main(["check", "--cases", "200", "--seed", "2024"]) == 0
     assert "passed 200/200" in capsys.readouterr().out
+
+
+@pytest.mark.gpu
+def test_run_bounded_device_scratch(cuda, tmp_path):
+    """`run --max-device-bytes` streams the tensor through a small device
+    scratch; the output file matches the oracle."""
+    import oracle
+
+    shape, axes = (16, 64, 56, 56), (0, 2, 3, 1)
+    x = np.random.default_rng(3).integers(0, 2**31, size=shape, dtype=np.uint32)
+    src, dst = tmp_path / "x.vpt", tmp_path / "y.vpt"
+    write_tensor(str(src), x.reshape(-1), TensorLayout.from_shape(shape, 4))
+    assert main(["run", "--in", str(src), "--map", "0,2,3,1", "--out", str(dst),
+                 "--max-device-bytes", str(4 << 20)]) == 0
+    _, got = read_tensor(str(dst))
+    dims, sigma = oracle.from_numpy_axes(shape, axes)
+    assert np.array_equal(np.asarray(got).view(np.uint32).reshape(-1), oracle.naive_permute_c(x.reshape(-1), dims, sigma))
