@@ -1,3 +1,5 @@
+// copy_pattern_probe.cu -- SM copy kernels of 2 GiB: grid-stride vs per-warp contiguous chunks at
+// several CTAs per SM, against cudaMemcpyAsync D2D (nvcc -O3 -gencode arch=compute_100a,code=sm_100a).
 #include <cuda_runtime.h>
 #include <cstdio>
 #include <cstdint>

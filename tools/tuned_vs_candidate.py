@@ -1,3 +1,4 @@
+"""The autotuned cfg5 program vs the same candidate built directly (same object, same timing)."""
 import os, sys
 sys.path.insert(0, os.getcwd())
 import torch, bench
