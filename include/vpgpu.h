@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define VPG_ABI_VERSION 2
+#define VPG_ABI_VERSION 3
 #define VPG_MAX_RANK 64
 
 typedef enum {
