@@ -519,3 +519,34 @@ def test_host_path_bounded_scratch_unsplittable(cuda):
     x = torch.zeros(shape, dtype=torch.int32)
     with pytest.raises(vp.LayoutError):
         vp.execute(prog, x, max_device_bytes=1 << 20)
+
+
+@pytest.mark.parametrize("shape,axes,elem", [
+    ((3, 2, 64, 1001), (1, 0, 2, 3), 8),        # rows cut into chunks
+    ((20, 12, 66), (1, 0, 2), 8),               # short predicated rows
+    ((7, 3, 4100), (1, 0, 2), 4),               # rows, exact-multiple fast path off
+    ((3, 1000003), (0, 1), 4),                  # chunked copy with a tail
+    ((2, 3, 7, 4097), (1, 0, 2, 3), 16),        # 16-byte words, rows
+])
+def test_guard_bands_new_paths(cuda, shape, axes, elem):
+    """Guard bands around source AND destination for the chunked rows and
+    copy kernels: no write outside the destination, no change to the
+    source, bit-exact result (compute-sanitizer is unavailable here)."""
+    import torch
+
+    import paper_2506_03686_b200 as vp
+    from paper_2506_03686_b200.api import execute_device
+
+    n = int(np.prod(shape)) * elem
+    G = 1 << 16
+    words = np.random.default_rng(n).integers(0, 256, size=n, dtype=np.uint8)
+    sbuf = torch.full((n + 2 * G,), 0xA5, dtype=torch.uint8, device="cuda")
+    dbuf = torch.full((n + 2 * G,), 0x5A, dtype=torch.uint8, device="cuda")
+    sbuf[G:G + n] = torch.from_numpy(words).cuda()
+    prog = vp.build_program(vp.TensorLayout.from_shape(shape, elem), vp.from_numpy_convention(axes))
+    execute_device(prog, sbuf[G:G + n], out=dbuf[G:G + n])
+    d, s_ = dbuf.cpu().numpy(), sbuf.cpu().numpy()
+    assert (d[:G] == 0x5A).all() and (d[G + n:] == 0x5A).all()
+    assert (s_[:G] == 0xA5).all() and (s_[G + n:] == 0xA5).all() and np.array_equal(s_[G:G + n], words)
+    want = np.ascontiguousarray(np.transpose(words.view(f"V{elem}").reshape(shape), axes)).reshape(-1).view(np.uint8)
+    assert np.array_equal(d[G:G + n], want), prog.kernel
