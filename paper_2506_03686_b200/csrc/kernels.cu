@@ -26,6 +26,7 @@
 #include <mutex>
 #include <string>
 #include <tuple>
+#include <utility>
 
 #include "plan.h"
 #include "tile_body.cuh"
@@ -36,6 +37,8 @@ namespace vpg {
 template <typename V>
 __global__ void __launch_bounds__(256) copy_kernel(const V *__restrict__ src, V *__restrict__ dst,
                                                    int64_t nvec) {
+    pdl_trigger();
+    pdl_wait();
     constexpr int U = 4;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -55,6 +58,8 @@ __global__ void __launch_bounds__(256) copy_kernel(const V *__restrict__ src, V 
 __global__ void __launch_bounds__(256) copy_kernel_chunked(const uint4 *__restrict__ src, uint4 *__restrict__ dst,
                                                            int64_t nvec) {
     constexpr int CH = 512;   // vectors per warp chunk (8 KiB)
+    pdl_trigger();
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -78,6 +83,8 @@ template <typename V, int U, int RPW, bool CHUNKED, bool EXACT>
 __global__ void __launch_bounds__(256) rows_kernel(const __grid_constant__ RowsParams p,
                                                    const V *__restrict__ src, V *__restrict__ dst,
                                                    uint32_t vec_log2) {
+    pdl_trigger();
+    pdl_wait();
     const uint32_t tpr = 1u << p.tpr_log2;
     const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t lane = gtid & (tpr - 1);
@@ -150,6 +157,8 @@ __global__ void __launch_bounds__(1024) tile_kernel_bulk(const __grid_constant__
 template <typename W>
 __global__ void __launch_bounds__(256) gather_kernel(const __grid_constant__ GatherParams p,
                                                      const W *__restrict__ src, W *__restrict__ dst) {
+    pdl_trigger();
+    pdl_wait();
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += gridDim.x * blockDim.x) {
         uint32_t rem = i;
         int64_t s = 0;
@@ -180,6 +189,40 @@ int sm_count_for_current() {
     if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
     g_sm_count[dev] = n;
     return n;
+}
+
+// Launches carry the programmatic stream-serialisation attribute (PDL, see
+// pdl_wait in tile_body.cuh) unless VPG_PDL=0 or the plan is sharded (the
+// exchange's barriers are collectives on the same stream).
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("VPG_PDL");
+        return !(e && atoi(e) == 0);
+    }();
+    return on;
+}
+
+struct LaunchCfg {
+    cudaLaunchConfig_t cfg;
+    cudaLaunchAttribute attr[1];
+    LaunchCfg(int64_t grid, int threads, int smem, cudaStream_t st, bool pdl) {
+        memset(&cfg, 0, sizeof(cfg));
+        cfg.gridDim = dim3((unsigned)grid);
+        cfg.blockDim = dim3((unsigned)threads);
+        cfg.dynamicSmemBytes = (size_t)smem;
+        cfg.stream = st;
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = pdl && pdl_enabled() ? 1 : 0;
+    }
+};
+
+template <typename... KArgs, typename... Args>
+void launch_k(void (*k)(KArgs...), int64_t grid, int threads, int smem, cudaStream_t st, bool pdl,
+              Args &&...args) {
+    LaunchCfg lc(grid, threads, smem, st, pdl);
+    cudaLaunchKernelEx(&lc.cfg, k, std::forward<Args>(args)...);
 }
 
 template <typename K>
@@ -240,8 +283,8 @@ vpg_status launch_tile(const vpg_plan *p, const void *src, void *dst, const Shar
             if (dbg)
                 fprintf(stderr, "[vpg] jit launch kernel %p grid %lld threads %d smem %d nb %d src %p dst %p\n",
                         (const void *)jk, (long long)grid, jthreads, smem, nb, src, dst);
-            if (cudaLaunchKernel((const void *)jk, dim3((unsigned)grid), dim3(jthreads), args, (size_t)smem, st) ==
-                cudaSuccess)
+            LaunchCfg lc(grid, jthreads, smem, st, p->shards <= 1);
+            if (cudaLaunchKernelExC(&lc.cfg, (const void *)jk, args) == cudaSuccess)
                 return VPG_OK;
             cudaGetLastError();   // fall through to the ahead-of-time kernel
         }
@@ -251,7 +294,7 @@ vpg_status launch_tile(const vpg_plan *p, const void *src, void *dst, const Shar
         int64_t grid = p->tile.num_tiles;
         if (p->tile.persistent) grid = std::min<int64_t>(grid, (int64_t)nb * sm_count_for_current());
         if (grid < 1) grid = 1;
-        k<<<(unsigned)grid, threads, smem, st>>>(tp, (const W *)src, (W *)dst, sa);
+        launch_k(k, grid, threads, smem, st, p->shards <= 1, tp, (const W *)src, (W *)dst, sa);
     };
     if constexpr (E == 4 || E == 8) {
         if (aligned && p->tile.bulk) {
@@ -273,7 +316,7 @@ vpg_status launch_gather(const vpg_plan *p, const void *src, void *dst, cudaStre
     using W = typename WordOf<E>::T;
     int64_t grid = std::min<int64_t>((p->gather.n + 255) / 256, (int64_t)sm_count_for_current() * 8);
     if (grid < 1) grid = 1;
-    gather_kernel<W><<<(unsigned)grid, 256, 0, st>>>(p->gather, (const W *)src, (W *)dst);
+    launch_k(gather_kernel<W>, grid, 256, 0, st, true, p->gather, (const W *)src, (W *)dst);
     return VPG_OK;
 }
 
@@ -339,7 +382,7 @@ vpg_status launch_rows(const vpg_plan *p, const void *src, void *dst, cudaStream
         int nb = occupancy(k, 256, 0);                                                         \
         int64_t grid = std::min<int64_t>(need, (int64_t)nb * sm_count_for_current());          \
         if (grid < 1) grid = 1;                                                                \
-        k<<<(unsigned)grid, 256, 0, st>>>(rp, (const TYPE *)src, (TYPE *)dst, vlog);           \
+        launch_k(k, grid, 256, 0, st, true, rp, (const TYPE *)src, (TYPE *)dst, vlog);         \
         return VPG_OK;                                                                         \
     }
 #define VPG_ROWS_CASE(BYTES, TYPE)                                                             \
@@ -370,15 +413,15 @@ vpg_status launch_copy(const vpg_plan *p, const void *src, void *dst, cudaStream
         case 16:
             if (nvec >= (1 << 16)) {   // >= 1 MiB: chunked form, 16 CTAs per SM
                 const int64_t g16 = std::min<int64_t>((nvec + 511) / 512 / 8 + 1, (int64_t)sm_count_for_current() * 16);
-                copy_kernel_chunked<<<(unsigned)g16, 256, 0, st>>>((const uint4 *)src, (uint4 *)dst, nvec);
+                launch_k(copy_kernel_chunked, g16, 256, 0, st, true, (const uint4 *)src, (uint4 *)dst, nvec);
             } else {
-                copy_kernel<uint4><<<(unsigned)grid, 256, 0, st>>>((const uint4 *)src, (uint4 *)dst, nvec);
+                launch_k(copy_kernel<uint4>, grid, 256, 0, st, true, (const uint4 *)src, (uint4 *)dst, nvec);
             }
             break;
-        case 8: copy_kernel<unsigned long long><<<(unsigned)grid, 256, 0, st>>>((const unsigned long long *)src, (unsigned long long *)dst, nvec); break;
-        case 4: copy_kernel<unsigned int><<<(unsigned)grid, 256, 0, st>>>((const unsigned int *)src, (unsigned int *)dst, nvec); break;
-        case 2: copy_kernel<unsigned short><<<(unsigned)grid, 256, 0, st>>>((const unsigned short *)src, (unsigned short *)dst, nvec); break;
-        default: copy_kernel<unsigned char><<<(unsigned)grid, 256, 0, st>>>((const unsigned char *)src, (unsigned char *)dst, nvec); break;
+        case 8: launch_k(copy_kernel<unsigned long long>, grid, 256, 0, st, true, (const unsigned long long *)src, (unsigned long long *)dst, nvec); break;
+        case 4: launch_k(copy_kernel<unsigned int>, grid, 256, 0, st, true, (const unsigned int *)src, (unsigned int *)dst, nvec); break;
+        case 2: launch_k(copy_kernel<unsigned short>, grid, 256, 0, st, true, (const unsigned short *)src, (unsigned short *)dst, nvec); break;
+        default: launch_k(copy_kernel<unsigned char>, grid, 256, 0, st, true, (const unsigned char *)src, (unsigned char *)dst, nvec); break;
     }
     return VPG_OK;
 }

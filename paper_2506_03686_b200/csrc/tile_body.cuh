@@ -104,6 +104,17 @@ __device__ __forceinline__ void st_out(W *p, const W &v) {
     *p = v;
 #endif
 }
+// Programmatic dependent launch (PDL): a launch with the programmatic
+// stream-serialisation attribute may start while the previous kernel on
+// the stream is still draining.  Every kernel here triggers its dependents
+// at entry (the dependent grid can only start once every CTA of this grid
+// has started, so a one-wave grid never loses SM slots to it) and waits for
+// the previous grid's completion -- and the visibility of its memory --
+// before its first global-memory access.  Without the attribute both are
+// no-ops.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
@@ -485,6 +496,7 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
     const uint32_t cnt = (p.num_tiles - first + step - 1) / step;   // tiles of this CTA
     const uint32_t S = ASYNC ? p.nbuf : 1u;
     const uint32_t R = S + 2;
+    pdl_trigger();
 
     // per-CTA outer tables of both phases (JIT builds decode entries inline)
 #ifndef VPG_JIT
@@ -538,6 +550,7 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
         const uint32_t m = limits(slot, 0, lim);
         tile_read<W, ASYNC>(p.ph[0], tr, smem, src + s_base[slot][0], gend, b, m, lim);
     };
+    pdl_wait();
     // prologue: fill every stage
     for (uint32_t j = 0; j < S; ++j) {
         if (j < cnt) load(j, buf0 + j * bstride);
@@ -618,6 +631,7 @@ __device__ __forceinline__ void tile_body_bulk(const TileParams &p, const W *__r
     if (first >= p.num_tiles) return;
     const uint32_t cnt = (p.num_tiles - first + step - 1) / step;
     const uint32_t S = p.nbuf;
+    pdl_trigger();
 
 #ifndef VPG_JIT
     {   // W-phase outer table (the producer needs no table)
@@ -655,6 +669,7 @@ __device__ __forceinline__ void tile_body_bulk(const TileParams &p, const W *__r
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     }
+    pdl_wait();
     __syncthreads();
     W *const buf0 = reinterpret_cast<W *>(smem + p.off_buf);
     const size_t bstride = ((size_t)p.tile_elems_alloc * sizeof(W) + 15) / 16 * 16 / sizeof(W);

@@ -550,3 +550,34 @@ def test_guard_bands_new_paths(cuda, shape, axes, elem):
     assert (s_[:G] == 0xA5).all() and (s_[G + n:] == 0xA5).all() and np.array_equal(s_[G:G + n], words)
     want = np.ascontiguousarray(np.transpose(words.view(f"V{elem}").reshape(shape), axes)).reshape(-1).view(np.uint8)
     assert np.array_equal(d[G:G + n], want), prog.kernel
+
+
+@pytest.mark.parametrize("shape,axes", [((4096, 4096), (1, 0)),                 # tile, specialised
+                                        ((32, 64, 56, 56), (0, 2, 3, 1)),       # tile, multi-dim
+                                        ((64, 32, 2048), (1, 0, 2)),            # rows
+                                        ((1 << 24,), (0,)),                     # copy
+                                        ((7, 9, 13, 5, 11), (4, 1, 0, 3, 2))])  # misaligned tile
+def test_back_to_back_dependent_launches(cuda, shape, axes):
+    """Launches carry the programmatic-dependent-launch attribute: a chain
+    in which every launch reads the previous launch's output (x -> y -> x'
+    -> y' ...) must still see complete inputs (the kernels' griddepcontrol
+    wait precedes their first global load)."""
+    import torch
+
+    from paper_2506_03686_b200 import TensorLayout, build_program, from_numpy_convention
+    from paper_2506_03686_b200.api import execute_device
+
+    inv = tuple(int(i) for i in np.argsort(axes))
+    out_shape = tuple(shape[a] for a in axes)
+    fwd = build_program(TensorLayout.from_shape(shape, 4), from_numpy_convention(axes))
+    bwd = build_program(TensorLayout.from_shape(out_shape, 4), from_numpy_convention(inv))
+    g = torch.Generator(device=cuda).manual_seed(11)
+    x0 = torch.randint(-2**31, 2**31 - 1, (int(np.prod(shape)),), dtype=torch.int32, device=cuda, generator=g)
+    a, b = x0.clone(), torch.empty_like(x0)
+    for _ in range(24):
+        execute_device(fwd, a, out=b)
+        execute_device(bwd, b, out=a)
+    want_b = _want(x0.cpu().numpy().reshape(shape), axes).reshape(-1)
+    torch.cuda.synchronize()
+    assert torch.equal(a, x0)
+    assert np.array_equal(b.cpu().numpy(), want_b)
