@@ -112,7 +112,8 @@ struct PhaseDesc {
     int32_t nout_dims;
     PhaseDim out[kMaxPhaseDims];    // outer dims (fastest first)
     uint32_t vec;                  // elements per access: 1, or V = 16/E (16-byte accesses)
-    uint32_t rshift;               // R: source runs read as 16-byte aligned supersets (misaligned runs)
+    uint32_t rshift;               // R: source runs read as 16-byte aligned supersets (misaligned runs);
+                                   // 2 = residue row strides (TileParams::rres)
     uint32_t h_in;                 // W in shifted-run mode: shift increment per inner step
     int64_t vstride;               // W with vec > 1: global stride between the V elements
     uint32_t mask_full;            // slots checked in every tile (padding)
@@ -165,6 +166,14 @@ struct TileParams {
     uint32_t tile_begin;
     int64_t src_bias;
     int64_t shard_elems;
+    // shifted-run mode with residue row strides (rshift == 2): V-1, else 0.
+    // Run-index dims have smem strides congruent to their source strides
+    // modulo V and each tile buffer is used from offset (source tile base &
+    // rres), so a misaligned run sits at the same offset modulo V in shared
+    // and global memory: R copies 16-byte aligned chunks to 16-byte aligned
+    // smem, W reads at affine offsets (no per-element shift, hmask == 0).
+    uint32_t rres;
+    uint32_t pad_rres_;
 };
 static_assert(sizeof(TileParams) <= 4096, "kernel parameter block must stay under 4 KB");
 

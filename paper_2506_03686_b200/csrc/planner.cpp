@@ -37,6 +37,8 @@ constexpr int64_t kRowsMinBytes = 512;
 constexpr double kRunOverheadBytes = 128.0;
 constexpr double kTileOverheadBytes = 2048.0;  // cost of one tile (decode + 2 barriers)
 constexpr int64_t kTileBudgetBytes = 48 * 1024;  // staged elements per CTA
+constexpr double kResidueCostFactor = 0.9;   // residue-stride shifted tiles: no W shift arithmetic
+constexpr double kSmallProblemBytes = 512.0 * 1024 * 1024;   // algorithmic bytes below which tiles shrink
 
 int64_t gcd64(int64_t a, int64_t b) {
     a = a < 0 ? -a : a;
@@ -66,6 +68,7 @@ struct Problem {
     int nbuf;             // forced pipeline stages (0 = planner's choice)
     int64_t cta_smem;     // per-CTA shared-memory target (bytes)
     bool no_shift = false; // disable shifted-run reads (VPG_NO_SHIFT)
+    bool no_res = false;   // disable residue row strides for shifted runs (VPG_NO_RES)
     bool no_bulk = true;   // TMA bulk source reads are opt-in (VPG_BULK=1)
     bool no_swz = true;    // shifted-run chunk swizzle is opt-in (VPG_SWZ=1)
     int r;
@@ -317,6 +320,7 @@ struct VecChoice {
     bool rshift = false;   // R reads 16-byte aligned supersets of misaligned runs
     bool bulk = false;     // R as one cp.async.bulk per source run (producer warp + mbarriers)
     int swz = 0;           // shifted-run mode: chunk swizzle (0 off, else 1 + row shift)
+    bool rres = false;     // shifted-run mode with residue row strides (no per-element shift in W)
 };
 
 // smem strides of the tile dims for a given pitch (source run dense, run
@@ -342,6 +346,43 @@ void tile_sstrides(const Problem &Pb, const TileGeom &g, uint32_t pitch, int64_t
         sstr[k] = acc;
         acc *= g.ext[k];
     }
+}
+
+// Residue row strides for misaligned source runs (shifted-run mode without
+// a per-element shift).  Each run-index dim k gets an smem stride S_k with
+// S_k == in_stride[k] (mod V), and the tile sits at smem offset
+// (source tile base mod V).  Every run then starts at the same offset
+// modulo V in shared and in global memory, so its 16-byte aligned global
+// superset lands on a 16-byte aligned smem chunk (R) and the W phase reads
+// element (run, e) at an affine offset.  S_1 >= NCK*V (chunks per run) and
+// S_{k+1} >= e_k * S_k keep the aligned row spans disjoint.  Returns the
+// elements one tile buffer needs (V - 1 of base shift included).
+int64_t tile_sstrides_res(const Problem &Pb, const TileGeom &g, uint32_t pitch, int V, int64_t *sstr,
+                          bool *in_src) {
+    for (int k = 0; k < Pb.r; ++k) in_src[k] = false;
+    int64_t acc = 1;
+    for (int i = 0; i < g.nsrc; ++i) {
+        int k = g.src_dims[i];
+        in_src[k] = true;
+        sstr[k] = acc;
+        acc *= g.ext[k];
+    }
+    const int64_t nck = (g.Ls + V - 1 + V - 1) / V;
+    auto with_res = [&](int64_t lo, int64_t res) {
+        int64_t r = ((res % V) + V) % V;
+        int64_t x = lo + (((r - lo) % V) + V) % V;
+        return x;
+    };
+    int64_t need = std::max<int64_t>((int64_t)pitch, nck * V);
+    int64_t last = 0;   // offset of the last run
+    for (int j = 0; j < Pb.r; ++j) {
+        const int k = Pb.sigma[j];
+        if (g.ext[k] == 0 || in_src[k]) continue;
+        sstr[k] = with_res(need, Pb.in_stride[k]);
+        last += (g.ext[k] - 1) * sstr[k];
+        need = sstr[k] * g.ext[k];
+    }
+    return (last + (V - 1) + nck * V + V - 1) / V * V;
 }
 
 // Phase dims (fastest first) with adjacent dims fused when they are
@@ -420,30 +461,39 @@ void set_pdim(PhaseDim &pd, int64_t e, int64_t g, int64_t s, int slot, int64_t c
 
 // Choose the thread part (prefix dims, split factor f) maximising lane use;
 // fill the phase descriptor.  Returns the utilisation estimate.
+//
+// Threads beyond one thread part share the outer loop.  Two ways:
+//   * separable groups: G divides the extent of one outer dim j, and the
+//     group index becomes one more thread dim (coordinate g of dim j, the
+//     outer dim keeps extent E_j/G at G times the stride).  Every thread
+//     then walks the same outer entries (ngroups = 1), so a specialised
+//     kernel unrolls the whole walk with constant offsets;
+//   * interleaved groups (ngroups = G): thread group g takes outer entries
+//     g, g+G, ...; each entry is decoded at run time (about a dozen
+//     instructions per entry, amortised over the n_in inner steps).
+// The score charges interleaved groups that decode cost.
 double make_phase(const std::vector<PDimH> &L, int NT, PhaseDesc &pd, uint32_t &lim_split) {
     memset(&pd, 0, sizeof(pd));
     const int m = (int)L.size();
     double best = -1.0, best_u = 0.0;
-    int bh = 0;
-    int64_t bf = 1;
+    int bh = 0, bj = -1;
+    int64_t bf = 1, bG = 1;
     int64_t P = 1;
+    const bool no_sep = getenv("VPG_NO_SEPGROUPS") != nullptr;
     for (int h = 0; h < m && P <= NT; P *= L[h].e, ++h) {
         if (h + 1 > kMaxPhaseDims) break;
         for (int64_t f = 1; f <= L[h].e && P * f <= NT; ++f) {
             int64_t ntp = P * f;
-            int64_t G = NT / ntp;
             int64_t steps = (L[h].e + f - 1) / f;
             int64_t rest = 1;
             for (int i = h + 1; i < m; ++i) rest *= L[i].e;
             int64_t n_outer = steps > 1 ? rest : (h + 1 < m ? rest / L[h + 1].e : 1);
             int64_t n_in = steps > 1 ? steps : (h + 1 < m ? L[h + 1].e : 1);
-            int nout_dims = m - (steps > 1 ? h + 1 : h + 2);
+            const int first_outer = steps > 1 ? h + 1 : h + 2;
+            int nout_dims = m - first_outer;
             if (nout_dims > kMaxPhaseDims) continue;
             if (n_outer < 1) n_outer = 1;
-            if (G > n_outer) G = n_outer;
-            double lane = (double)(G * ntp) / NT;
             double pad = (double)L[h].e / (double)(f * steps);
-            double bal = (double)n_outer / (double)(G * ((n_outer + G - 1) / G));
             // coalescing: consecutive lanes must walk globally contiguous
             // elements; `avail` = contiguous extent of the leading dims,
             // `cover` = how much of it one thread part spans
@@ -459,16 +509,32 @@ double make_phase(const std::vector<PDimH> &L, int NT, PhaseDesc &pd, uint32_t &
                 if (L[i].g != L[i - 1].g * L[i - 1].e) contig = false;
             if (!contig) cover = h == 0 ? f : L[0].e;
             double coal = std::min(1.0, (double)std::min<int64_t>(cover, 32) / (double)std::min<int64_t>(32, avail));
-            double u = lane * pad * bal * coal;
-            // ties: bigger thread parts (fewer outer-table steps), longer inner loops
-            double score = u + 1e-3 * std::log2((double)ntp) + 1e-4 * (steps * f == L[h].e) +
-                           1e-6 * std::min<int64_t>(n_in, 64);
-            if (score > best) {
-                best = score;
-                best_u = u;
-                bh = h;
-                bf = f;
-            }
+            auto consider = [&](int64_t G, int j, bool sep) {
+                double lane = (double)(G * ntp) / NT;
+                double bal = sep ? 1.0 : (double)n_outer / (double)(G * ((n_outer + G - 1) / G));
+                double u = lane * pad * bal * coal;
+                // interleaved groups decode every outer entry at run time
+                double eff = (!sep && G > 1) ? u / (1.0 + 2.0 / (double)n_in) : u;
+                // ties: bigger thread parts (fewer outer-table steps), longer inner loops
+                double score = eff + 1e-3 * std::log2((double)ntp) + 1e-4 * (steps * f == L[h].e) +
+                               1e-6 * std::min<int64_t>(n_in, 64) + (sep ? 1e-5 : 0.0);
+                if (score > best) {
+                    best = score;
+                    best_u = u;
+                    bh = h;
+                    bf = f;
+                    bG = G;
+                    bj = sep ? j : -1;
+                }
+            };
+            int64_t G = NT / ntp;
+            if (G > n_outer) G = n_outer;
+            if (G < 1) G = 1;
+            consider(G, -1, G == 1);
+            if (!no_sep && pd.nthr_dims + 2 <= kMaxPhaseDims && h + 2 <= kMaxPhaseDims)
+                for (int j = first_outer; j < m; ++j)
+                    for (int64_t Gs = 2; Gs <= L[j].e && ntp * Gs <= NT; ++Gs)
+                        if (L[j].e % Gs == 0) consider(Gs, j, true);
         }
     }
     const int h = bh;
@@ -488,6 +554,12 @@ double make_phase(const std::vector<PDimH> &L, int NT, PhaseDesc &pd, uint32_t &
     }
     set_pdim(pd.thr[pd.nthr_dims++], f, L[h].g, L[h].s, split_slot, L[h].cmul, L[h].hmul);
     ntp *= f;
+    // separable groups: coordinate g of outer dim bj as the last thread dim
+    if (bj >= 0) {
+        const PDimH &dj = L[bj];
+        set_pdim(pd.thr[pd.nthr_dims++], bG, dj.g, dj.s, dj.slot, dj.cmul, dj.hmul);
+        ntp *= bG;
+    }
     int first_outer;
     if (steps > 1) {
         pd.n_in = (uint32_t)steps;
@@ -512,12 +584,20 @@ double make_phase(const std::vector<PDimH> &L, int NT, PhaseDesc &pd, uint32_t &
     pd.nout_dims = 0;
     int64_t n_outer = 1;
     for (int i = first_outer; i < m; ++i) {
+        if (i == bj) {
+            if (L[i].e / bG > 1) {
+                set_pdim(pd.out[pd.nout_dims++], L[i].e / bG, L[i].g * bG, L[i].s * bG, L[i].slot,
+                         L[i].cmul * bG, L[i].hmul * bG);
+                n_outer *= L[i].e / bG;
+            }
+            continue;
+        }
         set_pdim(pd.out[pd.nout_dims++], L[i].e, L[i].g, L[i].s, L[i].slot, L[i].cmul, L[i].hmul);
         n_outer *= L[i].e;
     }
     pd.n_outer = (uint32_t)n_outer;
     pd.nthr = (uint32_t)ntp;
-    int64_t G = NT / ntp;
+    int64_t G = bj >= 0 ? 1 : NT / ntp;
     if (G > n_outer) G = n_outer;
     if (G < 1) G = 1;
     pd.ngroups = (uint32_t)G;
@@ -601,19 +681,21 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
     tp.tile_elems_alloc = Ns * pitch;
     int64_t sstr[kMaxRank];
     bool in_src[kMaxRank];
-    tile_sstrides(Pb, g, pitch, sstr, in_src);
+    const int V = 16 / Pb.E;
+    if (vc.rres) tp.tile_elems_alloc = (uint32_t)tile_sstrides_res(Pb, g, pitch, V, sstr, in_src);
+    else tile_sstrides(Pb, g, pitch, sstr, in_src);
     int slot_of_dim[kMaxRank];
     for (int k = 0; k < r; ++k) slot_of_dim[k] = -1;
     if (g.a_part >= 0) slot_of_dim[g.a_part] = 0;
     if (g.c_part >= 0 && g.c_part != g.a_part) slot_of_dim[g.c_part] = 1;
-    const int V = 16 / Pb.E;
-    const int64_t hmask = vc.rshift ? V - 1 : 0;
+    const int64_t hmask = vc.rshift && !vc.rres ? V - 1 : 0;
     double u0 = make_phase(vc.rshift ? shift_r_dims(Pb, g, sstr, slot_of_dim, V)
                                      : phase_dims(Pb, g, sstr, slot_of_dim, false, vc.vr),
                            NT, tp.ph[0], tp.lim_split[0]);
     double u1 = make_phase(phase_dims(Pb, g, sstr, slot_of_dim, true, vc.vw, hmask), NT, tp.ph[1], tp.lim_split[1]);
-    tp.ph[0].rshift = vc.rshift ? 1u : 0u;
+    tp.ph[0].rshift = vc.rshift ? (vc.rres ? 2u : 1u) : 0u;
     tp.hmask = (uint32_t)hmask;
+    tp.rres = vc.rres ? (uint32_t)(V - 1) : 0u;
     if (vc.swz && vc.rshift && vc.vw == 1 && !vc.bulk) {
         for (int ph = 0; ph < 2; ++ph) {
             tp.ph[ph].swz = (uint32_t)vc.swz;
@@ -783,6 +865,32 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
                 if (getenv("VPG_DEBUG_PLAN"))
                     fprintf(stderr, "[plan] Ls %lld Ld %lld pitch %u shift-swizzle %d cost %.1f per-elem %.3f\n",
                             (long long)g.Ls, (long long)g.Ld, pitch, sw, c, c / (double)g.T);
+                if (best < 0 || c < best - 1e-9) {
+                    best = c;
+                    pitch_out = pitch;
+                    vc_out = vc;
+                }
+            }
+        }
+        if (op.rshift && !Pb.no_res) {
+            // residue row strides: pitch candidates NCK*V + pad (rounded up to
+            // the first run-index dim's residue inside tile_sstrides_res)
+            const int64_t base = (g.Ls + V - 1 + V - 1) / V * V;
+            for (int pad = 0; pad <= 32; ++pad) {
+                const uint32_t pitch = (uint32_t)(base + pad);
+                if ((int64_t)(g.T / g.Ls) * pitch * Pb.E > Pb.budget + 8192) break;
+                TileParams tp;
+                VecChoice vc;
+                vc.vr = op.vr;
+                vc.vw = op.vw;
+                vc.rshift = true;
+                vc.rres = true;
+                fill_tile_params(Pb, g, pitch, NT, vc, tp);
+                // no per-element shift arithmetic in W: cheaper per element
+                double c = tile_cost(Pb, tp) * kResidueCostFactor;
+                if (getenv("VPG_DEBUG_PLAN"))
+                    fprintf(stderr, "[plan] Ls %lld Ld %lld pitch %u residue cost %.1f per-elem %.3f\n",
+                            (long long)g.Ls, (long long)g.Ld, pitch, c, c / (double)g.T);
                 if (best < 0 || c < best - 1e-9) {
                     best = c;
                     pitch_out = pitch;
@@ -997,7 +1105,8 @@ static void describe(vpg_plan *p) {
         if (t.ph[0].swz) put("smem chunk swizzle: row >> %u\n", t.ph[0].swz - 1);
         put("vector elems: R %u%s, W %u\n", t.ph[0].vec,
             t.bulk ? " (TMA bulk copy per source run, producer warp)"
-                   : (t.ph[0].rshift ? " (aligned supersets of misaligned runs)" : ""),
+                   : (t.ph[0].rshift == 2 ? " (aligned supersets of misaligned runs, residue row strides)"
+                                       : t.ph[0].rshift ? " (aligned supersets of misaligned runs)" : ""),
             t.ph[1].vec);
         put("lane utilisation (R*W): %.3f\n", p->tile_util);
         put("specialised (NVRTC) kernel: %s\n", p->jit ? "yes" : "no");
@@ -1041,6 +1150,19 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
     P.budget = kTileBudgetBytes;
     P.nbuf = 0;
     P.cta_smem = 110 * 1024;
+    {
+        // small problems (a few tiles per CTA): half-size tiles and a smaller
+        // per-CTA staging target, so twice as many CTAs per SM run
+        // independent pipelines (steady-state, tools/sweep.py SWEEP_MODE=
+        // steady: cfg2 10.6 -> 10.1 us, cfg3 18.3 -> 17.0 us, cfg1 25.8 ->
+        // 24.7 us; cfg5's 4 GiB keeps the large tiles: 664 vs 686 us)
+        int64_t nel = 1;
+        for (int k = 0; k < rank; ++k) nel *= dims[k];
+        if ((double)nel * E * 2.0 < kSmallProblemBytes) {
+            P.budget = 24 * 1024;
+            P.cta_smem = 75 * 1024;
+        }
+    }
     int persist_mode = -1;  // -1 auto, 0 one tile per CTA, 1 persistent
     int force_threads = 0;
     if (const char *e = getenv("VPG_TILE_BUDGET")) P.budget = std::max(1024L, atol(e));
@@ -1049,6 +1171,7 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
     if (const char *e = getenv("VPG_PERSIST")) persist_mode = atoi(e);
     if (const char *e = getenv("VPG_THREADS")) force_threads = atoi(e);
     if (getenv("VPG_NO_SHIFT")) P.no_shift = true;
+    if (getenv("VPG_NO_RES")) P.no_res = true;
     // the chunk swizzle removes the W bank conflicts of shifted runs but costs
     // a divide and a few integer ops per element: measured 28.4 vs 20.5 us on
     // cfg3, 216 vs 247 us on an odd 8-byte 2-D transpose -- opt-in

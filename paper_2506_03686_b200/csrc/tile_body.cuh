@@ -273,7 +273,11 @@ __device__ __forceinline__ void tile_read_shift(const PhaseDesc &d, const Thread
         for (uint32_t i = 0; i < n_in; ++i) {
             if (mask == 0 || slot_ok(mask, c0, c1, c2, lim)) {
                 const W *ga = reinterpret_cast<const W *>((uintptr_t)gp & ~(uintptr_t)15);
-                W *sd = d.swz ? buf + swizzle<V>(d, (uint32_t)(sp - buf)) : sp;   // chunk-aligned: whole chunk moves
+                // chunk-aligned: whole chunk moves.  Residue mode: sp is the
+                // run element's own (unaligned) smem slot, congruent to gp
+                // modulo 16 bytes; the chunk goes to its aligned-down slot
+                W *sd = d.rshift == 2 ? reinterpret_cast<W *>((uintptr_t)sp & ~(uintptr_t)15)
+                        : (d.swz ? buf + swizzle<V>(d, (uint32_t)(sp - buf)) : sp);
                 if (ga + V <= gend) {
                     cp_async<16>(sd, ga);
                 } else {
@@ -548,7 +552,8 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
         Lim lim;
         const uint32_t slot = k % R;
         const uint32_t m = limits(slot, 0, lim);
-        tile_read<W, ASYNC>(p.ph[0], tr, smem, src + s_base[slot][0], gend, b, m, lim);
+        tile_read<W, ASYNC>(p.ph[0], tr, smem, src + s_base[slot][0], gend,
+                            b + (p.rres ? ((uint32_t)s_base[slot][0] & p.rres) : 0u), m, lim);
     };
     pdl_wait();
     // prologue: fill every stage
@@ -565,8 +570,9 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
             Lim lim;
             const uint32_t slot = k % R;
             const uint32_t m = limits(slot, 1, lim);
-            tile_write<W>(p.ph[1], tw, smem, dst + s_base[slot][1], b, m, lim, (uint32_t)s_base[slot][0],
-                          p.hmask);
+            tile_write<W>(p.ph[1], tw, smem, dst + s_base[slot][1],
+                          b + (p.rres ? ((uint32_t)s_base[slot][0] & p.rres) : 0u), m, lim,
+                          (uint32_t)s_base[slot][0], p.hmask);
         }
         __syncthreads();
         if (k + S < cnt) load(k + S, b);

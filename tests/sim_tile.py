@@ -61,7 +61,7 @@ class TileParams(ctypes.Structure):
                 ("ph", PhaseDesc * 2), ("grid", GridDigit * MAXR), ("off_buf", ctypes.c_uint32),
                 ("nbuf", ctypes.c_uint32), ("persistent", ctypes.c_uint32), ("smem_bytes", ctypes.c_uint32),
                 ("nshards", ctypes.c_uint32), ("tile_begin", ctypes.c_uint32), ("src_bias", ctypes.c_int64),
-                ("shard_elems", ctypes.c_int64)]
+                ("shard_elems", ctypes.c_int64), ("rres", ctypes.c_uint32), ("pad_rres_", ctypes.c_uint32)]
 
 
 def tile_params(program) -> TileParams:
@@ -172,6 +172,7 @@ def simulate(program, src_words: np.ndarray, threads: int | None = None, shard_o
             dbound = n
         full = va == tp.e_a and vc == tp.e_c
         lim = (va, vc)
+        tbase = (sb & tp.rres) if tp.rres else 0     # residue mode: tile offset in its buffer
         smem = np.zeros(alloc + 64, dtype=src_words.dtype)
         smem_valid = np.zeros(alloc + 64, dtype=bool)
         if tp.bulk:
@@ -223,7 +224,13 @@ def simulate(program, src_words: np.ndarray, threads: int | None = None, shard_o
                                 ga = gabs - (gabs % V)
                                 if d.swz and (sp % V).any():
                                     raise SimError("swizzled R chunk not chunk-aligned")
-                                sd = _swizzle(d, sp, V)
+                                if d.rshift == 2:
+                                    spl = sp + tbase
+                                    sd = spl - (spl % V)
+                                    if ((spl - sd) != (gabs - ga)).any():
+                                        raise SimError("residue mode: smem and global offsets differ mod V")
+                                else:
+                                    sd = _swizzle(d, sp, V)
                                 for j in range(V):
                                     inb = ga + j < n
                                     _chk(sd[inb] + j, alloc, "R shifted smem")
@@ -239,7 +246,7 @@ def simulate(program, src_words: np.ndarray, threads: int | None = None, shard_o
                                     smem_valid[sp + j] = True
                         else:
                             hh = (sb + th[sel][ok] + eh[0] + i * d.h_in) & tp.hmask if tp.hmask else 0
-                            spx = _swizzle(d, sp + hh, 16 // E if E <= 16 else 1)
+                            spx = _swizzle(d, sp + hh + tbase, 16 // E if E <= 16 else 1)
                             gabs = db + gp
                             if V > 1 and (spx % V).any():
                                 raise SimError("W vector smem access misaligned")

@@ -9,7 +9,7 @@ import pytest
 
 import oracle
 import paper_2506_03686_b200 as vp
-from tests.sim_tile import simulate, simulate_exchange
+from tests.sim_tile import simulate, simulate_exchange, tile_params
 
 
 def _run(shape, axes, E, rng, **kw):
@@ -158,6 +158,7 @@ def test_sim_swizzled_shifted_rows(monkeypatch):
     """Plans with the shifted-run chunk swizzle (misaligned runs, opt-in
     VPG_SWZ=1) replay bit-exact: R writes and W reads agree on the layout."""
     monkeypatch.setenv("VPG_SWZ", "1")
+    monkeypatch.setenv("VPG_NO_RES", "1")      # residue row strides would win the cost model
     vp.program_cache_clear()
     rng = np.random.default_rng(11)
     n_swz = 0
@@ -179,3 +180,30 @@ def test_sim_swizzled_shifted_rows(monkeypatch):
             break
     vp.program_cache_clear()
     assert n_swz >= 10
+
+
+def test_sim_residue_rows():
+    """Misaligned runs with residue row strides (the default shifted-run
+    layout): R lands every 16-byte aligned source chunk on an aligned smem
+    chunk and W reads affine offsets; replays bit-exact against the C
+    oracle, including ragged tiles and 8-byte words."""
+    vp.program_cache_clear()
+    rng = np.random.default_rng(23)
+    n_res = 0
+    for _ in range(300):
+        r = int(rng.integers(2, 6))
+        shape = tuple(int(x) for x in rng.integers(2, 40, size=r))
+        axes = tuple(int(a) for a in rng.permutation(r))
+        E = int(rng.choice([4, 8]))
+        prog = vp.build_program(vp.TensorLayout.from_shape(shape, E), vp.from_numpy_convention(axes), force="tile")
+        if tile_params(prog).rres == 0:
+            continue
+        n = prog.num_elements
+        words = rng.integers(0, 2**63, size=n, dtype=np.uint64)
+        words = words.view(np.uint32)[:n].copy() if E == 4 else words
+        dims, sigma = oracle.from_numpy_axes(shape, axes)
+        assert np.array_equal(simulate(prog, words), oracle.naive_permute_c(words, dims, sigma)), (shape, axes, E)
+        n_res += 1
+        if n_res >= 40:
+            break
+    assert n_res >= 20

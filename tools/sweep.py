@@ -1,4 +1,5 @@
-"""Sweep planner knobs (VPG_* env overrides) over configs; flushed median us."""
+"""Sweep planner knobs (VPG_* env overrides) over configs; flushed median us
+(SWEEP_MODE=steady: best steady-state per-launch us)."""
 import itertools
 import os
 import sys
@@ -23,16 +24,23 @@ st = torch.cuda.current_stream()
 for k in cfgs:
     wl = CONFIGS[k]
     n = wl.numel * wl.elem_bytes
-    x = torch.randint(0, 255, (n,), dtype=torch.uint8, device=dev)
-    y = torch.empty_like(x)
+    steady = os.environ.get("SWEEP_MODE") == "steady"     # back-to-back over rotating buffers (PDL)
+    nb = bench.steady_buffers(fl.l2, n) if steady else 1
+    xs = [torch.randint(0, 255, (n,), dtype=torch.uint8, device=dev) for _ in range(nb)]
+    ys = [torch.empty_like(x) for x in xs]
+    x, y = xs[0], ys[0]
     res = []
     for vals in itertools.product(*grid.values()):
         env = dict(zip(grid.keys(), vals))
         os.environ.update(env)
         program_cache_clear()
         prog = build_program(TensorLayout.from_shape(wl.shape, wl.elem_bytes), from_numpy_convention(wl.axes))
-        t = bench.time_device(torch, lambda: execute_device(prog, x, out=y), 15, 3, fl, st)
-        med = sorted(t)[len(t) // 2] * 1e3
+        if steady:
+            med = min(bench.time_steady(torch, lambda i: execute_device(prog, xs[i], out=ys[i]), nb, 10, st)
+                      for _ in range(3)) * 1e3
+        else:
+            t = bench.time_device(torch, lambda: execute_device(prog, x, out=y), 15, 3, fl, st)
+            med = sorted(t)[len(t) // 2] * 1e3
         res.append((med, env, prog.metadata["tile_elems"], prog.metadata["smem_bytes"]))
     res.sort(key=lambda r: r[0])
     for med, env, te, sm in res[:6]:
