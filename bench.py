@@ -790,6 +790,8 @@ def main(argv=None):
         "parity_sampled": main_res["parity_sampled"],
         "configs": extra,
         "event_floor_us": round(floor, 2),
+        "step_ms_stats": {"mean": round(ms, 5), "median": round(statistics.median(main_res["times_ms"]), 5),
+                          "min": round(min(main_res["times_ms"]), 5), "max": round(max(main_res["times_ms"]), 5)},
     })
     print(json.dumps(line), flush=True)
     return 0

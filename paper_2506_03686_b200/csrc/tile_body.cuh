@@ -431,7 +431,16 @@ __device__ __forceinline__ void decode_tile(const TileParams &p, const ShardArgs
     t += p.tile_begin;
     int64_t sb = 0, db = 0;
     uint32_t va = p.e_a, vc = p.e_c;
+#ifdef VPG_JIT
+    // specialised kernels: every digit's divisors and strides are
+    // compile-time constants (no parameter loads from global memory)
+    VPG_UNROLL
+    for (int i = 0; i < kMaxRank; ++i) {
+        if (i >= p.ngrid) break;
+        if ((i & 31) != (int)lane) continue;
+#else
     for (int i = (int)lane; i < p.ngrid; i += 32) {
+#endif
         const GridDigit &gd = p.grid[i];
         uint32_t q = fdiv(t, gd.cum);
         uint32_t c = q - fdiv(q, gd.ext) * gd.ext.d;

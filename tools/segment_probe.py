@@ -50,6 +50,43 @@ elif mode in ("tinyrand", "bigrand_other"):
         del z
     x = torch.empty(n, dtype=torch.uint8, device=dev)
     y = torch.empty(n, dtype=torch.uint8, device=dev)
+elif mode.startswith("off"):
+    # x, y as slices of one pool at a byte offset (VA / page alignment)
+    off = int(mode[3:])
+    pool = torch.empty(2 * n + 2 * off + (4 << 20), dtype=torch.uint8, device=dev)
+    x, y = pool[off:off + n], pool[n + 2 * off:2 * n + 2 * off]
+elif mode.startswith("pre"):
+    # a big allocation first, released to the driver before x, y (physical placement)
+    gb = int(mode[3:])
+    z = torch.empty(gb << 30, dtype=torch.uint8, device=dev)
+    del z
+    torch.cuda.empty_cache()
+    x = torch.empty(n, dtype=torch.uint8, device=dev)
+    y = torch.empty(n, dtype=torch.uint8, device=dev)
+elif mode.startswith("hold"):
+    # a big allocation held while x, y are created
+    gb = int(mode[4:])
+    z = torch.empty(gb << 30, dtype=torch.uint8, device=dev)
+    x = torch.empty(n, dtype=torch.uint8, device=dev)
+    y = torch.empty(n, dtype=torch.uint8, device=dev)
+elif mode in ("cumsum", "sort", "randint_after", "manual_seed_dev"):
+    if mode == "cumsum":
+        torch.ones(1024, device=dev).cumsum(0)
+    elif mode == "sort":
+        torch.ones(1024, device=dev).sort()
+    elif mode == "manual_seed_dev":
+        torch.cuda.manual_seed(0)
+        torch.empty(16, device=dev).uniform_()
+    x = torch.empty(n, dtype=torch.uint8, device=dev)
+    y = torch.empty(n, dtype=torch.uint8, device=dev)
+    if mode == "randint_after":
+        torch.randint(0, 255, (1024,), dtype=torch.uint8, device=dev)
+elif mode == "randint_late":
+    x = torch.empty(n, dtype=torch.uint8, device=dev)
+    y = torch.empty(n, dtype=torch.uint8, device=dev)
+    execute_device(p, x, out=y)            # our specialised module loads first
+    torch.cuda.synchronize()
+    torch.randint(0, 255, (1024,), dtype=torch.uint8, device=dev)
 elif mode == "randint":
     x = torch.randint(0, 255, (n,), dtype=torch.uint8, device=dev)
     y = torch.empty_like(x)
