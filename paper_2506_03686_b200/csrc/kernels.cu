@@ -290,6 +290,7 @@ vpg_status launch_tile(const vpg_plan *p, const void *src, void *dst, const Shar
         }
     }
     auto launch = [&](auto k, int threads, const TileParams &tp) {
+        const int smem = (int)tp.smem_bytes;     // the variants' tables differ in size
         int nb = occupancy(k, threads, smem);
         int64_t grid = p->tile.num_tiles;
         if (p->tile.persistent) grid = std::min<int64_t>(grid, (int64_t)nb * sm_count_for_current());
