@@ -495,11 +495,19 @@ def bench_sharded(args, torch, base, config, peak, peak_kind):
     x = host_in.to(dev).view(wdt)
     st = torch.cuda.current_stream()
     method = args.shard_method
+    xmode = None
     if method == "auto":
         method = "fused" if fused_supported(wl.shape, wl.axes, wl.elem_bytes, G) else "alltoall"
+    if method in ("push", "pull"):
+        method, xmode = "fused", method
     if method == "fused":
-        ex = ShardExchange(wl.shape, wl.axes, wdt, device=dev)
+        ex = ShardExchange(wl.shape, wl.axes, wdt, device=dev, mode=xmode or "auto")
+        xmode = ex.mode
         run = ex
+        if xmode == "pull":
+            # the peers read this rank's input from the exchange's shared buffer
+            ex.input.copy_(x)
+            x = ex.input
     else:
         run = lambda xin: permute_sharded(xin, wl.shape, wl.axes, local_permute=permute, plan=sp)  # noqa: E731
     step = lambda: run(x)  # noqa: E731
@@ -593,12 +601,13 @@ def bench_sharded(args, torch, base, config, peak, peak_kind):
                            " on pinned host shards, streamed (H2D of step k+1 overlaps D2H of step k)",
                     "parity": e2e_ok},
             "gpu_launches": (1 if method == "fused" or G == 1 else 2) * args.steps,
-            "shard_method": method,
+            "shard_method": method if method != "fused" else f"fused ({xmode})",
             "roofline": {"bound": bound, "achieved": round(gbs, 2), "peak": round(roof_gbs, 1),
                          "peak_kind": f"min over HBM ({peak_kind} {peak} GB/s per GPU) and NVLink "
                                       f"({NVLINK_GBS} GB/s per direction per GPU) time bounds",
                          "unit": "GB/s", "frac": round(gbs / roof_gbs, 4), "traffic": None,
-                         "kernel": "fused exchange tile kernel (peer stores over NVLink)" if method == "fused"
+                         "kernel": ("fused exchange tile kernel (peer stores over NVLink)" if xmode == "push" else
+                                    "fused exchange tile kernel (peer reads over NVLink)") if method == "fused"
                          else "tile (P1/P2) + NCCL all_to_all_single"},
             "parity_sampled": bool(ok.item()),
             "clocks": clk.summary(),
@@ -657,8 +666,9 @@ def main(argv=None):
     ap.add_argument("--tune", action="store_true", help="measured planning (autotune) before timing")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="N>1 process group; gloo only checks the code path (ranks may share a GPU)")
-    ap.add_argument("--shard-method", default="auto", choices=["auto", "fused", "alltoall"],
-                    help="N>1: fused exchange kernel or P1 -> all-to-all -> P2")
+    ap.add_argument("--shard-method", default="auto", choices=["auto", "fused", "push", "pull", "alltoall"],
+                    help="N>1: fused exchange kernel (push: peer stores, pull: peer reads, fused: whichever "
+                         "keeps long remote runs) or P1 -> all-to-all -> P2")
     ap.add_argument("--cpu-threads", type=int, default=None)
     ap.add_argument("--sharded", action="store_true",
                     help="use the sharded (torchrun/NCCL) code path even with one rank")

@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define VPG_ABI_VERSION 3
+#define VPG_ABI_VERSION 4
 #define VPG_MAX_RANK 64
 
 typedef enum {
@@ -99,6 +99,7 @@ vpg_status vpg_merge_dimensions(int rank, const int64_t *dims, const int32_t *si
 #define VPG_NO_MERGE     0x4
 #define VPG_FORCE_JIT    0x8    /* TILE: always use the per-case NVRTC-specialised kernel  */
 #define VPG_NO_JIT       0x10   /* TILE: always use the ahead-of-time kernel                */
+#define VPG_SHARD_PULL   0x20   /* sharded plans: pull exchange (see vpg_permute_sharded_pull) */
 /* TILE: use the n-th best tile candidate of the planner's cost model
  * (n >= 0); plan creation fails with VPG_EUNSUPPORTED past the last one.
  * Autotuners time a few candidates and keep the fastest. */
@@ -176,6 +177,20 @@ vpg_status vpg_plan_create_sharded(int rank, const int64_t *dims_inner_first,
                                    unsigned flags, int shards, int shard_index, vpg_plan **out);
 vpg_status vpg_permute_sharded(const vpg_plan *plan, const void *src_shard,
                                void *const *dst_shards, void *cuda_stream);
+
+/* Pull variant of the fused exchange (plans created with VPG_SHARD_PULL;
+ * shard_index then names the OUTPUT shard this plan produces).  ONE kernel
+ * per rank reads the source runs of its output tiles straight from every
+ * input shard -- src_shards[q] is input shard q's buffer as seen from this
+ * device (peer-mapped pointers over NVLink/NVSwitch for q != own) -- and
+ * writes its local output shard.  Destination runs are local, so the plan
+ * keeps long runs on both sides even when an input-shard axis is the
+ * output's second-innermost axis (where the push exchange would store
+ * 16-byte runs across ranks).  Ordering as for vpg_permute_sharded: every
+ * input shard must be complete before any rank launches, and no input shard
+ * may be overwritten before every rank's kernel has completed. */
+vpg_status vpg_permute_sharded_pull(const vpg_plan *plan, const void *const *src_shards,
+                                    void *dst_shard, void *cuda_stream);
 
 /* CUDA IPC for the exchange's peer table: export a device pointer (any
  * pointer inside a cudaMalloc allocation) as a VPG_IPC_HANDLE_BYTES handle

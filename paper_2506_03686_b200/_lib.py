@@ -20,6 +20,7 @@ VPG_FORCE_TILE = 0x2
 VPG_NO_MERGE = 0x4
 VPG_FORCE_JIT = 0x8
 VPG_NO_JIT = 0x10
+VPG_SHARD_PULL = 0x20
 VPG_MAX_RANK = 64
 VPG_MAX_SHARDS = 64
 VPG_IPC_HANDLE_BYTES = 64
@@ -33,6 +34,7 @@ EXPORTED = (
     "vpg_plan_create_sharded",
     "vpg_permute",
     "vpg_permute_sharded",
+    "vpg_permute_sharded_pull",
     "vpg_ipc_export",
     "vpg_ipc_import",
     "vpg_ipc_release",
@@ -108,6 +110,7 @@ def lib():
                                               ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]
         L.vpg_permute.argtypes = [vp, vp, vp, vp]
         L.vpg_permute_sharded.argtypes = [vp, vp, ctypes.POINTER(vp), vp]
+        L.vpg_permute_sharded_pull.argtypes = [vp, ctypes.POINTER(vp), vp, vp]
         L.vpg_ipc_export.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_uint64)]
         L.vpg_ipc_import.argtypes = [vp, ctypes.c_uint64, ctypes.POINTER(vp)]
         L.vpg_ipc_release.argtypes = [vp]
@@ -123,7 +126,7 @@ def lib():
         L.vpg_plan_destroy.argtypes = [vp]
         L.vpg_plan_destroy.restype = None
         for name in ("vpg_merge_dimensions", "vpg_plan_create", "vpg_permute", "vpg_permute_host",
-                     "vpg_plan_create_sharded", "vpg_permute_sharded", "vpg_ipc_export", "vpg_ipc_import",
+                     "vpg_plan_create_sharded", "vpg_permute_sharded", "vpg_permute_sharded_pull", "vpg_ipc_export", "vpg_ipc_import",
                      "vpg_ipc_release",
                      "vpg_permute_host_async", "vpg_permute_host_bounded",
                      "vpg_permute_nd", "vpg_plan_info_get", "vpg_plan_describe", "vpg_plan_emit_source",

@@ -278,12 +278,16 @@ def build_program(layout: TensorLayout, pmap: PermutationMap, machine=None, merg
 
 
 def build_sharded_program(layout: TensorLayout, pmap: PermutationMap, shards: int, shard_index: int,
-                          jit: bool | None = None, candidate: int | None = None) -> GpuProgram:
-    """Plan of the fused sharded exchange for input shard ``shard_index`` of
-    ``shards`` (vpg_plan_create_sharded): ONE tile kernel that reads the
-    local input shard and stores every tile straight into the output shard
-    that owns it.  Raises LayoutError when the shapes do not shard or no tile
-    avoids the shard-indexing dims (callers then use the all-to-all path)."""
+                          jit: bool | None = None, candidate: int | None = None, pull: bool = False) -> GpuProgram:
+    """Plan of the fused sharded exchange (vpg_plan_create_sharded).
+
+    push (default): the plan of input shard ``shard_index`` -- ONE tile
+    kernel that reads the local input shard and stores every tile straight
+    into the output shard that owns it.  pull: the plan of OUTPUT shard
+    ``shard_index`` -- ONE tile kernel that reads its tiles' source runs from
+    every input shard (peer memory) and writes the local output shard.
+    Raises LayoutError when the shapes do not shard or no tile avoids the
+    shard-indexing dims (callers then use the all-to-all path)."""
     if pmap.rank != layout.rank:
         raise LayoutError("map rank does not match layout rank")
     if not 1 <= shards <= _lib.VPG_MAX_SHARDS:
@@ -295,6 +299,8 @@ def build_sharded_program(layout: TensorLayout, pmap: PermutationMap, shards: in
         flags |= _lib.VPG_NO_JIT
     if candidate is not None:
         flags |= ((candidate + 1) & 0xFF) << 8
+    if pull:
+        flags |= _lib.VPG_SHARD_PULL
     key = ("sharded", layout.dims, layout.elem_width, pmap.sigma, flags, shards, shard_index)
     with _cache_lock:
         hit = _cache.get(key)
@@ -306,9 +312,22 @@ def build_sharded_program(layout: TensorLayout, pmap: PermutationMap, shards: in
     _check(L.vpg_plan_create_sharded(rank, d, s, layout.elem_width, flags, shards, shard_index,
                                      ctypes.byref(ptr)), "build_sharded_program")
     prog = _wrap(ptr, layout, pmap)
+    prog.metadata["pull"] = bool(pull)
     with _cache_lock:
         _cache.setdefault(key, prog)
         return _cache[key]
+
+
+def launch_sharded_pull(program: GpuProgram, src_ptrs, dst_ptr: int, stream_ptr) -> None:
+    """Enqueue the pull exchange kernel of one output shard
+    (vpg_permute_sharded_pull): ``src_ptrs[q]`` = input shard q's buffer as
+    seen from this device, ``dst_ptr`` = the local output shard."""
+    G = program.metadata["shards"]
+    if len(src_ptrs) != G:
+        raise LayoutError(f"expected {G} source shards, got {len(src_ptrs)}")
+    arr = (ctypes.c_void_p * G)(*[int(p) for p in src_ptrs])
+    st = _lib.lib().vpg_permute_sharded_pull(program.handle, arr, ctypes.c_void_p(dst_ptr), stream_ptr)
+    _check(st, "permute_sharded_pull")
 
 
 def launch_sharded(program: GpuProgram, src_ptr: int, dst_ptrs, stream_ptr) -> None:

@@ -76,12 +76,29 @@ vpg_status vpg_permute_sharded(const vpg_plan *plan, const void *src_shard, void
                                void *cuda_stream) {
     if (!plan || !dst_shards) return fail(VPG_EINVAL, "null argument");
     if (plan->shards < 1) return fail(VPG_EINVAL, "not a sharded plan (use vpg_permute)");
+    if (plan->tile.pull) return fail(VPG_EINVAL, "pull exchange plan: use vpg_permute_sharded_pull");
     if (plan->n > 0 && !src_shard) return fail(VPG_EINVAL, "null buffer");
     for (int q = 0; q < plan->shards; ++q)
         if (dst_shards[q] == src_shard && plan->n > 0)
             return fail(VPG_EINVAL, "src and dst must not overlap (out-of-place only)");
     std::string err;
     vpg_status s = vpg::launch_plan(plan, src_shard, dst_shards, plan->shards, cuda_stream, &err);
+    if (s != VPG_OK) return fail(s, err);
+    return VPG_OK;
+}
+
+vpg_status vpg_permute_sharded_pull(const vpg_plan *plan, const void *const *src_shards, void *dst_shard,
+                                    void *cuda_stream) {
+    if (!plan || !src_shards) return fail(VPG_EINVAL, "null argument");
+    if (plan->shards < 1 || !plan->tile.pull) return fail(VPG_EINVAL, "not a pull exchange plan (VPG_SHARD_PULL)");
+    if (plan->n > 0 && !dst_shard) return fail(VPG_EINVAL, "null buffer");
+    for (int q = 0; q < plan->shards; ++q) {
+        if (plan->n > 0 && !src_shards[q]) return fail(VPG_EINVAL, "null buffer");
+        if (src_shards[q] == dst_shard && plan->n > 0)
+            return fail(VPG_EINVAL, "src and dst must not overlap (out-of-place only)");
+    }
+    std::string err;
+    vpg_status s = vpg::launch_plan_pull(plan, src_shards, dst_shard, cuda_stream, &err);
     if (s != VPG_OK) return fail(s, err);
     return VPG_OK;
 }

@@ -269,7 +269,13 @@ template <int E>
 vpg_status launch_tile(const vpg_plan *p, const void *src, void *dst, const ShardArgs &sa, cudaStream_t st) {
     using W = typename WordOf<E>::T;
     const int smem = (int)p->tile.smem_bytes;
-    const bool aligned = !(p->tile.ph[0].vec > 1 && ((uintptr_t)src % 16));
+    bool aligned = !(p->tile.ph[0].vec > 1 && ((uintptr_t)src % 16));
+    if (p->tile.pull && p->tile.ph[0].vec > 1) {
+        // vectorised pull reads: 16-byte chunks of every shard, none straddling two
+        if ((p->tile.shard_elems * E) % 16) aligned = false;
+        for (int q = 0; q < (int)p->tile.nshards; ++q)
+            if (((uintptr_t)src + sa.off[q] * E) % 16) aligned = false;
+    }
     if (p->jit && aligned) {
         cudaKernel_t jk = jit_tile_kernel(p);
         if (jk) {
@@ -430,6 +436,51 @@ vpg_status launch_copy(const vpg_plan *p, const void *src, void *dst, cudaStream
 }  // namespace
 
 int device_sm_count() { return sm_count_for_current(); }
+
+vpg_status launch_plan_pull(const vpg_plan *p, const void *const *srcs, void *dst, void *stream, std::string *err) {
+    cudaStream_t st = (cudaStream_t)stream;
+    const int E = p->elem_bytes;
+    const int G = p->shards;
+    if (p->kernel_class != VPG_KERNEL_TILE || !p->tile.pull || G < 1) {
+        *err = "not a pull exchange plan";
+        return VPG_EINVAL;
+    }
+    ShardArgs sa;
+    memset(&sa, 0, sizeof(sa));
+    const void *src = srcs[0];
+    for (int q = 0; q < G; ++q) {
+        if (!srcs[q] || ((uintptr_t)srcs[q] % E)) {
+            *err = "source buffers must be non-null and aligned to the element width";
+            return VPG_EINVAL;
+        }
+        const int64_t diff = (int64_t)((uintptr_t)srcs[q] - (uintptr_t)src);
+        sa.off[q] = diff / E;
+    }
+    if (!dst || (uintptr_t)dst % E) {
+        *err = "destination buffer must be non-null and aligned to the element width";
+        return VPG_EINVAL;
+    }
+    if (p->n == 0) return VPG_OK;
+    vpg_status s = VPG_OK;
+    switch (E) {
+        case 1: s = launch_tile<1>(p, src, dst, sa, st); break;
+        case 2: s = launch_tile<2>(p, src, dst, sa, st); break;
+        case 4: s = launch_tile<4>(p, src, dst, sa, st); break;
+        case 8: s = launch_tile<8>(p, src, dst, sa, st); break;
+        case 16: s = launch_tile<16>(p, src, dst, sa, st); break;
+        default: s = VPG_EUNSUPPORTED;
+    }
+    if (s != VPG_OK) {
+        *err = "unsupported plan/element width";
+        return s;
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        *err = std::string("kernel launch failed: ") + cudaGetErrorString(e);
+        return VPG_ECUDA;
+    }
+    return VPG_OK;
+}
 
 vpg_status launch_plan(const vpg_plan *p, const void *src, void *const *dsts, int ndst, void *stream,
                        std::string *err) {

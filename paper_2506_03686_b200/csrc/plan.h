@@ -54,6 +54,8 @@ vpg_status ipc_release(void *ptr, std::string *err);
 // dsts: one destination per output shard (1 for ordinary plans)
 vpg_status launch_plan(const vpg_plan *p, const void *src, void *const *dsts, int ndst, void *stream,
                        std::string *err);
+// pull exchange plans: srcs = every input shard's buffer, dst = the local output shard
+vpg_status launch_plan_pull(const vpg_plan *p, const void *const *srcs, void *dst, void *stream, std::string *err);
 inline vpg_status launch_plan(const vpg_plan *p, const void *src, void *dst, void *stream, std::string *err) {
     return launch_plan(p, src, &dst, 1, stream, err);
 }

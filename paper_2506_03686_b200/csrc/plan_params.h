@@ -173,7 +173,18 @@ struct TileParams {
     // and global memory: R copies 16-byte aligned chunks to 16-byte aligned
     // smem, W reads at affine offsets (no per-element shift, hmask == 0).
     uint32_t rres;
-    uint32_t pad_rres_;
+    // pull exchange (nshards > 1, pull = 1): this plan produces output shard
+    // (dst_bias / shard_elems) and reads its source runs from every input
+    // shard.  Source offsets stay global; each 16-byte chunk or element at
+    // global offset o is read from input shard q = o / shard_elems (a shift
+    // when shard_shift != 0, else shard_div) through ShardArgs::off[q]
+    // (relative to src).  Destination offsets are rebased by dst_bias onto
+    // the local output shard.
+    uint32_t pull;
+    uint32_t shard_shift;
+    FastDiv shard_div;
+    uint32_t pad_pull_;
+    int64_t dst_bias;
 };
 static_assert(sizeof(TileParams) <= 4096, "kernel parameter block must stay under 4 KB");
 

@@ -85,7 +85,8 @@ struct Problem {
     // tile, and the input-shard digits are the slowest grid digits.
     uint8_t pin[kMaxRank] = {};
     int G = 0;          // shards (0: ordinary plan)
-    int shard = 0;      // this plan's input shard
+    int shard = 0;      // this plan's input shard (push) or output shard (pull)
+    bool pull = false;  // pull exchange: pin[k] = 2 marks the leading OUTPUT dims
 };
 
 void fill_problem(Problem &P) {
@@ -734,9 +735,11 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
     // destination-stride order (the reference's counter digits,
     // planner.py:324-342); input-shard digits last, inner to outer, so a
     // shard's tiles form one contiguous range of the tile index
-    std::stable_sort(dg.begin(), dg.end(), [](const Dg &x, const Dg &y) {
+    // (pull exchange: the pinned digits index the OUTPUT shard, so they rank
+    // by output position)
+    std::stable_sort(dg.begin(), dg.end(), [&Pb](const Dg &x, const Dg &y) {
         if ((x.src >= 0) != (y.src >= 0)) return y.src >= 0;
-        if (x.src >= 0) return x.src < y.src;
+        if (x.src >= 0) return Pb.pull ? Pb.pos[x.src] < Pb.pos[y.src] : x.src < y.src;
         return x.ds < y.ds;
     });
     tp.ngrid = (int32_t)dg.size();
@@ -758,8 +761,20 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
         tp.num_tiles = (uint32_t)std::min<uint64_t>(per, 0xffffffffull);
         tp.tile_begin = (uint32_t)std::min<uint64_t>(per * (uint64_t)Pb.shard, 0xffffffffull);
         tp.shard_elems = Pb.n / Pb.G;
-        tp.src_bias = tp.shard_elems * Pb.shard;
-        tp.n_elems = tp.shard_elems;      // source bounds: the local shard
+        if (Pb.pull) {
+            tp.pull = 1;
+            tp.src_bias = 0;
+            tp.dst_bias = tp.shard_elems * Pb.shard;
+            tp.n_elems = Pb.n;            // source offsets are global
+            const uint64_t S = (uint64_t)tp.shard_elems;
+            tp.shard_shift = 0;
+            if (S > 1 && (S & (S - 1)) == 0)
+                while ((1ull << tp.shard_shift) < S) ++tp.shard_shift;
+            tp.shard_div = make_fastdiv((uint32_t)std::min<uint64_t>(S, 0xffffffffull));
+        } else {
+            tp.src_bias = tp.shard_elems * Pb.shard;
+            tp.n_elems = tp.shard_elems;  // source bounds: the local shard
+        }
     }
     tp.e_a = g.a_part >= 0 ? (uint32_t)g.ext[g.a_part] : 1u;
     tp.d_a = g.a_part >= 0 ? (uint32_t)Pb.d[g.a_part] : 1u;
@@ -1003,7 +1018,7 @@ static bool lead_cuts(const std::vector<int> &outer_first, const int64_t *dims, 
 // Inner-first in and out.
 static bool refine_for_shards(int rank, const int64_t *dims, const int32_t *sigma, int G,
                               std::vector<int64_t> &rd, std::vector<int32_t> &rs, std::vector<uint8_t> &pin,
-                              std::string *err) {
+                              std::string *err, bool pull = false) {
     std::vector<int> in_of, out_of;
     for (int k = rank - 1; k >= 0; --k) in_of.push_back(k);
     for (int j = rank - 1; j >= 0; --j) out_of.push_back(sigma[j]);
@@ -1046,7 +1061,16 @@ static bool refine_for_shards(int rank, const int64_t *dims, const int32_t *sigm
     for (int j = 0; j < rank; ++j)
         for (size_t i = 0; i < pieces[sigma[j]].size(); ++i) rs.push_back(first[sigma[j]] + (int)i);
     pin.assign(rr, 0);
-    if (G > 1) {
+    if (G > 1 && pull) {
+        // pull: the leading OUTPUT dims index the plan's output shard -- the
+        // slowest grid digits; the input-shard dims stay free (every source
+        // chunk finds its shard at run time)
+        int64_t prod = 1;
+        for (int j = rr - 1; j >= 0 && prod < G; --j) {
+            pin[rs[j]] = 2;
+            prod *= rd[rs[j]];
+        }
+    } else if (G > 1) {
         int64_t prod = 1;
         for (int k = rr - 1; k >= 0 && prod < G; --k) {
             pin[k] = 2;
@@ -1189,9 +1213,15 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
             *err = "shards must be in 1.." + std::to_string(kMaxShards) + " and shard_index in 0..shards-1";
             return VPG_EINVAL;
         }
-        if (!refine_for_shards(rank, dims, sigma, shards, rdims, rsig, rpin, err)) return VPG_EUNSUPPORTED;
+        const bool pull = (flags & VPG_SHARD_PULL) != 0;
+        if (!refine_for_shards(rank, dims, sigma, shards, rdims, rsig, rpin, err, pull)) return VPG_EUNSUPPORTED;
         P.G = shards;
         P.shard = shard_index;
+        P.pull = pull;
+        if (pull) {
+            P.no_swz = true;     // chunk swizzle and TMA bulk reads assume one source buffer
+            P.no_bulk = true;
+        }
     }
     const int rrank = (int)rdims.size();
     if (flags & VPG_NO_MERGE) {

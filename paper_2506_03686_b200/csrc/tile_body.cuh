@@ -457,7 +457,9 @@ __device__ __forceinline__ void decode_tile(const TileParams &p, const ShardArgs
         vc = min(vc, __shfl_xor_sync(0xffffffffu, vc, o));
     }
     if (lane == 0) {
-        if (p.nshards > 1) {
+        if (p.nshards > 1 && p.pull) {
+            db -= p.dst_bias;           // pull: local output shard; sources stay global
+        } else if (p.nshards > 1) {
             const uint64_t q = (uint64_t)db / (uint64_t)p.shard_elems;
             sb -= p.src_bias;
             db += sa.off[q] - (int64_t)q * p.shard_elems;
@@ -466,6 +468,60 @@ __device__ __forceinline__ void decode_tile(const TileParams &p, const ShardArgs
         s_base[k][1] = db;
         s_valid[k][0] = va;
         s_valid[k][1] = vc;
+    }
+}
+
+// ------------------------------------------------------------------ pull exchange
+// Source word at GLOBAL offset o of a pull exchange plan: input shard
+// q = o / shard_elems, read through the per-launch shard table (peer memory
+// for the other ranks' shards).
+template <typename W>
+__device__ __forceinline__ const W *pull_ptr(const TileParams &p, const ShardArgs &sa, const W *src, int64_t o) {
+    const uint32_t q = p.shard_shift ? (uint32_t)((uint64_t)o >> p.shard_shift) : fdiv((uint32_t)o, p.shard_div);
+    return src + (sa.off[q] + (o - (int64_t)q * p.shard_elems));
+}
+
+// R phase of a pull plan: the walk of tile_read_impl / tile_read_shift with
+// every 16-byte chunk (or word) addressed through pull_ptr.  Chunks never
+// straddle shards (launch_plan_pull requires shard_elems % V == 0 and
+// 16-byte aligned shard buffers for the vectorised variants).
+template <typename W, bool ASYNC>
+__device__ __forceinline__ void tile_read_pull(const TileParams &p, const ShardArgs &sa, const PhaseDesc &d,
+                                               const ThreadPart &t, const unsigned char *smem, const W *src,
+                                               int64_t sbase, W *buf, uint32_t mask, const Lim lim) {
+    if (!t.active) return;
+    constexpr int V = 16 / (int)sizeof(W);
+    const uint32_t o0 = d.ngroups == 1 ? 0u : t.grp;
+    VPG_UNROLL
+    for (uint32_t o = o0; o < d.n_outer; o += d.ngroups) {
+        const OuterEntry e = outer_entry(d, smem, o);
+        int64_t go = sbase + t.g + e.g;
+        W *sp = buf + (t.s + e.s);
+        uint32_t c0 = t.c0 + e.c0, c1 = t.c1 + e.c1, c2 = t.c2;
+        VPG_UNROLL
+        for (uint32_t i = 0; i < d.n_in; ++i) {
+            if (mask == 0 || slot_ok(mask, c0, c1, c2, lim)) {
+                if constexpr (ASYNC && sizeof(W) < 16) {
+                    if (d.rshift) {
+                        W *sd = d.rshift == 2 ? reinterpret_cast<W *>((uintptr_t)sp & ~(uintptr_t)15) : sp;
+                        cp_async<16>(sd, pull_ptr(p, sa, src, go & ~(int64_t)(V - 1)));
+                    } else if (d.vec > 1) {
+                        cp_async<16>(sp, pull_ptr(p, sa, src, go));
+                    } else {
+                        cp_async<sizeof(W)>(sp, pull_ptr(p, sa, src, go));
+                    }
+                } else if constexpr (ASYNC) {
+                    cp_async<16>(sp, pull_ptr(p, sa, src, go));
+                } else {
+                    *sp = __ldg(pull_ptr(p, sa, src, go));
+                }
+            }
+            go += d.g_in;
+            sp += d.s_in;
+            c0 += d.c_in[0];
+            c1 += d.c_in[1];
+            c2 += d.c_in[2];
+        }
     }
 }
 
@@ -561,8 +617,9 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
         Lim lim;
         const uint32_t slot = k % R;
         const uint32_t m = limits(slot, 0, lim);
-        tile_read<W, ASYNC>(p.ph[0], tr, smem, src + s_base[slot][0], gend,
-                            b + (p.rres ? ((uint32_t)s_base[slot][0] & p.rres) : 0u), m, lim);
+        W *bt = b + (p.rres ? ((uint32_t)s_base[slot][0] & p.rres) : 0u);
+        if (p.pull) tile_read_pull<W, ASYNC>(p, sa, p.ph[0], tr, smem, src, s_base[slot][0], bt, m, lim);
+        else tile_read<W, ASYNC>(p.ph[0], tr, smem, src + s_base[slot][0], gend, bt, m, lim);
     };
     pdl_wait();
     // prologue: fill every stage

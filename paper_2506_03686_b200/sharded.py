@@ -38,7 +38,7 @@ from dataclasses import dataclass
 from .core import LayoutError
 
 __all__ = ["ShardPlan", "plan_sharded", "permute_sharded", "shard_bounds", "ShardExchange", "emulate_fused",
-           "fused_supported", "release_exchanges"]
+           "fused_supported", "fused_method", "release_exchanges"]
 
 
 def _lead_split(shape, G):
@@ -222,10 +222,12 @@ def permute_sharded(local_in, global_shape, axes, group=None, local_permute=None
     the group must call it with the same shape/axes.
 
     method: "alltoall" -- P1 permute -> all_to_all_single -> P2 permute;
-    "fused" -- one exchange kernel per rank storing into the peers' output
-    shards (ShardExchange; the result is the exchange's buffer, overwritten
-    by the next fused call with the same arguments); "auto" -- fused when
-    every destination run is at least 128 bytes (fused_supported).
+    "fused" -- one exchange kernel per rank over peer memory (ShardExchange:
+    push = stores into the peers' output shards, pull = reads from the
+    peers' input shards; the result is the exchange's buffer, overwritten by
+    the next fused call with the same arguments); "auto" -- fused when one
+    of the two keeps runs of at least 128 bytes on the remote side
+    (fused_method), else the all-to-all.
     """
     import torch
     import torch.distributed as dist
@@ -297,27 +299,44 @@ def emulate_sharded(x_flat, global_shape, axes, G, local_permute=None):
 
 
 # ------------------------------------------------------------------ fused exchange (K5)
-MIN_FUSED_RUN_BYTES = 128      # K5 when destination runs are >= 128 B
+MIN_FUSED_RUN_BYTES = 128      # K5 when the remote-side runs are >= 128 B
 
 
-def _programs(global_shape, axes, elem_bytes, G, ranks, jit=None):
+def _programs(global_shape, axes, elem_bytes, G, ranks, jit=None, pull=False):
     from .api import build_sharded_program
     from .core import TensorLayout, from_numpy_convention
 
     lay = TensorLayout.from_shape(tuple(global_shape), elem_bytes)
     pm = from_numpy_convention(tuple(axes))
-    return [build_sharded_program(lay, pm, G, r, jit=jit) for r in ranks]
+    return [build_sharded_program(lay, pm, G, r, jit=jit, pull=pull) for r in ranks]
+
+
+def fused_method(global_shape, axes, elem_bytes, G):
+    """Which fused exchange suits this permutation: "push" when the push
+    plan's destination runs are at least MIN_FUSED_RUN_BYTES (remote stores
+    in whole sectors), else "pull" when the pull plan's source runs are
+    (remote reads of whole sectors; its stores are local), else None (the
+    all-to-all path).  Same answer on every rank: the tile geometry does not
+    depend on the shard index."""
+    try:
+        (p,) = _programs(global_shape, axes, elem_bytes, G, [0])
+        if p.metadata["dst_run"] * elem_bytes >= MIN_FUSED_RUN_BYTES:
+            return "push"
+    except LayoutError:
+        pass
+    try:
+        (p,) = _programs(global_shape, axes, elem_bytes, G, [0], pull=True)
+        if (p.metadata["src_run"] * elem_bytes >= MIN_FUSED_RUN_BYTES
+                and p.metadata["dst_run"] * elem_bytes >= MIN_FUSED_RUN_BYTES):
+            return "pull"
+    except LayoutError:
+        pass
+    return None
 
 
 def fused_supported(global_shape, axes, elem_bytes, G) -> bool:
-    """True when the fused exchange plans and its destination runs are at
-    least MIN_FUSED_RUN_BYTES (same answer on every rank: the tile geometry
-    does not depend on the shard index)."""
-    try:
-        (p,) = _programs(global_shape, axes, elem_bytes, G, [0])
-    except LayoutError:
-        return False
-    return p.metadata["dst_run"] * elem_bytes >= MIN_FUSED_RUN_BYTES
+    """True when one of the fused exchanges suits this permutation (fused_method)."""
+    return fused_method(global_shape, axes, elem_bytes, G) is not None
 
 
 class ShardExchange:
@@ -338,7 +357,7 @@ class ShardExchange:
     next call; copy it to keep it.  Collective: all ranks construct and call
     it with the same arguments."""
 
-    def __init__(self, global_shape, axes, dtype, group=None, device=None, jit=None):
+    def __init__(self, global_shape, axes, dtype, group=None, device=None, jit=None, mode="auto"):
         import torch
         import torch.distributed as dist
 
@@ -350,10 +369,19 @@ class ShardExchange:
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.dtype = dtype
         es = torch.empty((), dtype=dtype).element_size()
-        (self.program,) = _programs(global_shape, axes, es, self.G, [self.rank], jit=jit)
+        if mode == "auto":
+            mode = fused_method(global_shape, axes, es, self.G) or "push"
+        if mode not in ("push", "pull"):
+            raise ValueError(f"unknown exchange mode {mode!r}")
+        self.mode = mode
+        (self.program,) = _programs(global_shape, axes, es, self.G, [self.rank], jit=jit, pull=mode == "pull")
         self.splan = plan_sharded(global_shape, axes, self.G)
         self.local_numel = self.splan.local_numel
         self.out = torch.empty(self.local_numel, dtype=dtype, device=self.device)
+        # pull: the peers read this rank's input from `self.input` (callers
+        # may fill it directly; __call__ copies any other tensor into it)
+        self.input = torch.empty(self.local_numel, dtype=dtype, device=self.device) if mode == "pull" else None
+        shared = self.input if mode == "pull" else self.out
         self.backend = dist.get_backend(group) if dist.is_initialized() else None
         self._flag = torch.zeros(1, dtype=torch.float32, device=self.device)
         self._imported = []
@@ -363,7 +391,7 @@ class ShardExchange:
             h = ctypes.create_string_buffer(_lib.VPG_IPC_HANDLE_BYTES)
             off = ctypes.c_uint64(0)
             with torch.cuda.device(self.device):
-                _check_ipc(L.vpg_ipc_export(ctypes.c_void_p(self.out.data_ptr()), h, ctypes.byref(off)))
+                _check_ipc(L.vpg_ipc_export(ctypes.c_void_p(shared.data_ptr()), h, ctypes.byref(off)))
             mine = (self.rank, h.raw, off.value)
             allh = [None] * self.G
             dist.all_gather_object(allh, mine, group=group)
@@ -373,7 +401,7 @@ class ShardExchange:
         with torch.cuda.device(self.device):
             for q, hraw, off in sorted(allh):
                 if q == self.rank:
-                    self.peers.append(self.out.data_ptr())
+                    self.peers.append(shared.data_ptr())
                     continue
                 ptr = ctypes.c_void_p()
                 buf = ctypes.create_string_buffer(hraw, _lib.VPG_IPC_HANDLE_BYTES)
@@ -396,7 +424,7 @@ class ShardExchange:
     def __call__(self, local_in, stream=None):
         import torch
 
-        from .api import launch_sharded
+        from .api import launch_sharded, launch_sharded_pull
 
         if local_in.numel() != self.local_numel or local_in.dtype != self.dtype:
             raise LayoutError(f"rank {self.rank}: expected {self.local_numel} elements of {self.dtype}")
@@ -404,9 +432,16 @@ class ShardExchange:
             raise LayoutError("input shard must be a contiguous tensor on the exchange's device")
         st = stream or torch.cuda.current_stream(self.device)
         with torch.cuda.stream(st):
-            self._barrier()
-            launch_sharded(self.program, local_in.data_ptr(), self.peers, ctypes.c_void_p(st.cuda_stream))
-            self._barrier()
+            if self.mode == "pull":
+                if local_in.data_ptr() != self.input.data_ptr():
+                    self.input.copy_(local_in.reshape(-1))
+                self._barrier()           # every input shard complete
+                launch_sharded_pull(self.program, self.peers, self.out.data_ptr(), ctypes.c_void_p(st.cuda_stream))
+                self._barrier()           # every reader done before inputs change
+            else:
+                self._barrier()
+                launch_sharded(self.program, local_in.data_ptr(), self.peers, ctypes.c_void_p(st.cuda_stream))
+                self._barrier()
         return self.out.view(self.splan.local_out_shape())
 
     def close(self):
@@ -451,20 +486,28 @@ def _exchange_for(shape, axes, dtype, device, group):
     return ex
 
 
-def emulate_fused(x_flat, global_shape, axes, G, jit=None):
+def emulate_fused(x_flat, global_shape, axes, G, jit=None, mode="push", in_shards=None):
     """Run the G exchange kernels of the fused path on ONE device (virtual
-    ranks, output shards as local buffers; every kernel is independent).
-    Returns the list of per-rank output shards (flat)."""
+    ranks, every shard a local buffer; every kernel is independent).
+    mode "push": rank r reads input shard r and stores into every output
+    shard; "pull": rank r reads every input shard (``in_shards``, default
+    the slices of x_flat) and writes output shard r.  Returns the list of
+    per-rank output shards (flat)."""
     import torch
 
-    from .api import launch_sharded
+    from .api import launch_sharded, launch_sharded_pull
 
     n = x_flat.numel()
-    progs = _programs(global_shape, axes, x_flat.element_size(), G, range(G), jit=jit)
+    progs = _programs(global_shape, axes, x_flat.element_size(), G, range(G), jit=jit, pull=mode == "pull")
     outs = [torch.empty(n // G, dtype=x_flat.dtype, device=x_flat.device) for _ in range(G)]
     ptrs = [o.data_ptr() for o in outs]
     st = torch.cuda.current_stream(x_flat.device)
+    if in_shards is None:
+        in_shards = [x_flat[slice(*shard_bounds(n, G, r))] for r in range(G)]
+    srcs = [t.data_ptr() for t in in_shards]
     for r in range(G):
-        lo, hi = shard_bounds(n, G, r)
-        launch_sharded(progs[r], x_flat[lo:hi].data_ptr(), ptrs, ctypes.c_void_p(st.cuda_stream))
+        if mode == "pull":
+            launch_sharded_pull(progs[r], srcs, ptrs[r], ctypes.c_void_p(st.cuda_stream))
+        else:
+            launch_sharded(progs[r], srcs[r], ptrs, ctypes.c_void_p(st.cuda_stream))
     return outs

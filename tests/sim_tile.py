@@ -61,7 +61,9 @@ class TileParams(ctypes.Structure):
                 ("ph", PhaseDesc * 2), ("grid", GridDigit * MAXR), ("off_buf", ctypes.c_uint32),
                 ("nbuf", ctypes.c_uint32), ("persistent", ctypes.c_uint32), ("smem_bytes", ctypes.c_uint32),
                 ("nshards", ctypes.c_uint32), ("tile_begin", ctypes.c_uint32), ("src_bias", ctypes.c_int64),
-                ("shard_elems", ctypes.c_int64), ("rres", ctypes.c_uint32), ("pad_rres_", ctypes.c_uint32)]
+                ("shard_elems", ctypes.c_int64), ("rres", ctypes.c_uint32), ("pull", ctypes.c_uint32),
+                ("shard_shift", ctypes.c_uint32), ("shard_div", FastDiv), ("pad_pull_", ctypes.c_uint32),
+                ("dst_bias", ctypes.c_int64)]
 
 
 def tile_params(program) -> TileParams:
@@ -162,7 +164,15 @@ def simulate(program, src_words: np.ndarray, threads: int | None = None, shard_o
                 va = min(tp.e_a, tp.d_a - cdig * tp.e_a)
             if i == tp.grid_c:
                 vc = min(tp.e_c, tp.d_c - cdig * tp.e_c)
-        if sharded:
+        if sharded and tp.pull:
+            # pull exchange: global source offsets, local output shard
+            q = tp.dst_bias // tp.shard_elems
+            db -= tp.dst_bias
+            if not 0 <= db < tp.shard_elems:
+                raise SimError(f"pull tile {t} outside the plan's output shard")
+            dst, written = dsts[q], counts[q]
+            dbound = tp.shard_elems
+        elif sharded:
             q = db // tp.shard_elems
             sb -= tp.src_bias
             db -= q * tp.shard_elems
@@ -220,6 +230,11 @@ def simulate(program, src_words: np.ndarray, threads: int | None = None, shard_o
                         gp, sp = gp[ok], sp[ok]
                         if ph == 0:
                             gabs = sb + gp
+                            if tp.pull and V > 1:
+                                S = tp.shard_elems
+                                ga0 = gabs - (gabs % V)
+                                if ((ga0 // S) != ((ga0 + V - 1) // S)).any():
+                                    raise SimError("pull: 16-byte chunk straddles two input shards")
                             if d.rshift:
                                 ga = gabs - (gabs % V)
                                 if d.swz and (sp % V).any():
@@ -267,15 +282,18 @@ def simulate(program, src_words: np.ndarray, threads: int | None = None, shard_o
 
 
 def simulate_exchange(programs, src_words: np.ndarray) -> np.ndarray:
-    """Replay every rank's exchange kernel; returns the concatenated output
-    shards after checking that each output element was written exactly once."""
+    """Replay every rank's exchange kernel (push: rank r reads input shard r;
+    pull: rank r reads the whole input through the shard table and writes
+    output shard r); returns the concatenated output shards after checking
+    that each output element was written exactly once."""
     tp0 = tile_params(programs[0])
     G, S = tp0.nshards, tp0.shard_elems
     fill = np.iinfo(np.uint64).max if src_words.dtype == np.uint64 else 0
     dsts = [np.full(S, fill, dtype=src_words.dtype) for _ in range(G)]
     counts = [np.zeros(S, dtype=np.int32) for _ in range(G)]
     for r, prog in enumerate(programs):
-        simulate(prog, src_words[r * S:(r + 1) * S], shard_out=(dsts, counts))
+        words = src_words if tp0.pull else src_words[r * S:(r + 1) * S]
+        simulate(prog, words, shard_out=(dsts, counts))
     c = np.concatenate(counts)
     if (c != 1).any():
         bad = np.nonzero(c != 1)[0][:5]

@@ -60,9 +60,10 @@ def _worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-def _fused_worker(rank, world, port, q):
+def _fused_worker(rank, world, port, q, mode="push"):
     """Fused exchange (ShardExchange): CUDA IPC peer table between processes
-    sharing the GPU; each rank's kernel stores into the others' buffers."""
+    sharing the GPU; each rank's kernel stores into the others' output
+    buffers (push) or reads the others' input buffers (pull)."""
     import torch
     import torch.distributed as dist
 
@@ -75,7 +76,7 @@ def _fused_worker(rank, world, port, q):
     errs, ran, live = [], 0, []
     for ci, (shape, axes) in enumerate(FUSED_CASES):
         try:
-            ex = ShardExchange(shape, axes, torch.int64)
+            ex = ShardExchange(shape, axes, torch.int64, mode=mode)
         except Exception as e:          # shapes that do not shard over `world`
             if "unsupported" not in str(e):
                 errs.append((shape, axes, repr(e)))
@@ -118,14 +119,15 @@ FUSED_CASES = [
 ]
 
 
+@pytest.mark.parametrize("mode", ["push", "pull"])
 @pytest.mark.parametrize("world", [2, 4])
-def test_fused_exchange_processes(cuda, world):
+def test_fused_exchange_processes(cuda, world, mode):
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_fused_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_fused_worker, args=(r, world, port, q, mode)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=600) for _ in procs]
@@ -136,8 +138,9 @@ def test_fused_exchange_processes(cuda, world):
         assert ran >= 3, (rank, ran)
 
 
+@pytest.mark.parametrize("mode", ["push", "pull"])
 @pytest.mark.parametrize("G", [1, 2, 4, 8])
-def test_fused_exchange_emulated(cuda, G):
+def test_fused_exchange_emulated(cuda, G, mode):
     """All G exchange kernels on one device (independent launches into G
     local output shards): bit-exact against numpy."""
     import torch
@@ -150,7 +153,7 @@ def test_fused_exchange_emulated(cuda, G):
         n = int(np.prod(shape))
         g = np.random.default_rng(100 + ci).integers(-2**62, 2**62, size=n, dtype=np.int64)
         try:
-            outs = emulate_fused(torch.from_numpy(g).cuda(), shape, axes, G)
+            outs = emulate_fused(torch.from_numpy(g).cuda(), shape, axes, G, mode=mode)
         except vp.LayoutError:
             continue
         torch.cuda.synchronize()
@@ -160,8 +163,9 @@ def test_fused_exchange_emulated(cuda, G):
     assert ran >= 3
 
 
+@pytest.mark.parametrize("mode", ["push", "pull"])
 @pytest.mark.parametrize("G", [2, 4, 8])
-def test_fused_exchange_cfg5(cuda, G):
+def test_fused_exchange_cfg5(cuda, G, mode):
     """BASELINE cfg5 (2 GiB) through the G exchange kernels on one device,
     compared with the single-GPU permutation (itself pinned to the oracle in
     test_gpu_configs) and the closed-form bijection on sampled positions."""
@@ -174,7 +178,7 @@ def test_fused_exchange_cfg5(cuda, G):
     w = CONFIGS["cfg5"]
     x = torch.randint(-2**62, 2**62, (w.numel,), dtype=torch.int64, device="cuda",
                       generator=torch.Generator(device="cuda").manual_seed(G))
-    outs = emulate_fused(x, w.shape, w.axes, G)
+    outs = emulate_fused(x, w.shape, w.axes, G, mode=mode)
     whole = permute(x.view(w.shape), w.axes).reshape(-1)
     torch.cuda.synchronize()
     assert torch.equal(torch.cat(outs), whole)
@@ -208,7 +212,8 @@ def test_sharded_ranks_with_gpu_kernels(cuda, world):
 
 @pytest.mark.parametrize("dtype_name,jit", [("uint8", False), ("int16", False), ("int32", True), ("int32", False),
                                             ("float64", True), ("complex128", False)])
-def test_fused_exchange_word_sizes(cuda, dtype_name, jit):
+@pytest.mark.parametrize("mode", ["push", "pull"])
+def test_fused_exchange_word_sizes(cuda, dtype_name, jit, mode):
     """1/2/4/8/16-byte words through both the specialised and the
     ahead-of-time exchange kernels (emulated ranks on one device)."""
     import torch
@@ -225,7 +230,7 @@ def test_fused_exchange_word_sizes(cuda, dtype_name, jit):
              else torch.randn(n, dtype=tdt, generator=g))
         for G in (2, 4):
             try:
-                outs = emulate_fused(x.cuda(), shape, axes, G, jit=jit)
+                outs = emulate_fused(x.cuda(), shape, axes, G, jit=jit, mode=mode)
             except vp.LayoutError:
                 continue
             got = torch.cat(outs).cpu()
@@ -234,7 +239,7 @@ def test_fused_exchange_word_sizes(cuda, dtype_name, jit):
     assert ran >= 4
 
 
-@pytest.mark.parametrize("method", ["fused", "alltoall"])
+@pytest.mark.parametrize("method", ["push", "pull", "alltoall"])
 def test_bench_two_ranks_code_path(cuda, method):
     """bench.py's N>1 path (torchrun, two ranks) end to end with the gloo
     backend on one GPU: the same code the 8-GPU NCCL run takes, checked for
@@ -251,11 +256,12 @@ def test_bench_two_ranks_code_path(cuda, method):
     assert res.returncode == 0, res.stderr[-2000:]
     line = json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["parity_sampled"] is True
-    assert line["shard_method"] == method and line["n_gpus"] == 2
+    assert line["shard_method"] == (method if method == "alltoall" else f"fused ({method})") and line["n_gpus"] == 2
     assert "gloo" in line["dist_backend"]
 
 
-def test_fused_exchange_random_campaign(cuda):
+@pytest.mark.parametrize("mode", ["push", "pull"])
+def test_fused_exchange_random_campaign(cuda, mode):
     """Random shapes (factors of 2, 3, 4, 6, 8, 12, 16), ranks 2-7, words of
     4 and 8 bytes, G in {2, 4, 8}: every exchange plan that exists is
     bit-exact against numpy (emulated ranks on one device)."""
@@ -277,10 +283,41 @@ def test_fused_exchange_random_campaign(cuda):
         n = int(np.prod(shape))
         x = torch.randint(-2**31, 2**31 - 1, (n,), dtype=dt, device="cuda")
         try:
-            outs = emulate_fused(x, shape, axes, G)
+            outs = emulate_fused(x, shape, axes, G, mode=mode)
         except vp.LayoutError:
             continue
         got = torch.cat(outs)
         assert torch.equal(got, x.view(shape).permute(axes).reshape(-1)), (shape, axes, G)
         ran += 1
     assert ran >= 100, ran
+
+
+@pytest.mark.parametrize("offset_words", [0, 1])
+def test_pull_exchange_separate_buffers(cuda, offset_words):
+    """Pull exchange with every input shard in its own allocation (as with
+    peer-mapped buffers), including shard buffers off 16-byte alignment
+    (offset_words = 1: the plan's scalar-read variant must take over)."""
+    import torch
+
+    import paper_2506_03686_b200 as vp
+    from paper_2506_03686_b200.sharded import emulate_fused, shard_bounds
+
+    ran = 0
+    for shape, axes, G in [((2,) * 20, CASES[0][1], 4), ((2,) * 20, CASES[0][1], 8), ((8, 6, 16, 4), (2, 0, 3, 1), 2),
+                           ((16, 12, 16, 8), (3, 1, 0, 2), 4), ((8, 40, 32), (0, 2, 1), 2)]:
+        n = int(np.prod(shape))
+        x = torch.randint(-2**31, 2**31 - 1, (n,), dtype=torch.int32, device="cuda")
+        shards = []
+        for r in range(G):
+            lo, hi = shard_bounds(n, G, r)
+            buf = torch.empty(hi - lo + 4, dtype=torch.int32, device="cuda")
+            v = buf[offset_words:offset_words + hi - lo]
+            v.copy_(x[lo:hi])
+            shards.append(v)
+        try:
+            outs = emulate_fused(x, shape, axes, G, mode="pull", in_shards=shards)
+        except vp.LayoutError:          # no pull plan for this shape
+            continue
+        assert torch.equal(torch.cat(outs), x.view(shape).permute(axes).reshape(-1)), (shape, axes, G)
+        ran += 1
+    assert ran >= 3

@@ -95,18 +95,21 @@ EXCHANGE_CASES = [
 ]
 
 
+@pytest.mark.parametrize("mode", ["push", "pull"])
 @pytest.mark.parametrize("G", [1, 2, 4, 8])
 @pytest.mark.parametrize("E", [4, 8])
-def test_sim_fused_exchange(G, E):
-    """Every rank's exchange kernel reads only its input shard and, together,
-    they write each output element exactly once with the permuted value."""
+def test_sim_fused_exchange(G, E, mode):
+    """push: every rank's exchange kernel reads only its input shard; pull:
+    every rank's kernel writes only its output shard, reading 16-byte chunks
+    that never straddle two input shards.  Together they write each output
+    element exactly once with the permuted value."""
     from paper_2506_03686_b200.sharded import _programs
     from tests.golden.pattern import golden_pattern
 
     done = 0
     for shape, axes in EXCHANGE_CASES:
         try:
-            progs = _programs(shape, axes, E, G, range(G))
+            progs = _programs(shape, axes, E, G, range(G), pull=mode == "pull")
         except vp.LayoutError:
             continue
         n = int(np.prod(shape))
