@@ -69,7 +69,8 @@ struct Problem {
     int64_t cta_smem;     // per-CTA shared-memory target (bytes)
     bool no_shift = false; // disable shifted-run reads (VPG_NO_SHIFT)
     bool no_res = false;   // disable residue row strides for shifted runs (VPG_NO_RES)
-    bool no_bulk = true;   // TMA bulk source reads are opt-in (VPG_BULK=1)
+    bool no_bulk = false;  // TMA bulk source reads off (VPG_BULK=0, pull exchanges)
+    bool force_bulk = false; // TMA bulk source reads wherever they apply (VPG_BULK=1)
     bool no_swz = true;    // shifted-run chunk swizzle is opt-in (VPG_SWZ=1)
     int r;
     int64_t d[kMaxRank];
@@ -1200,10 +1201,12 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
     // a divide and a few integer ops per element: measured 28.4 vs 20.5 us on
     // cfg3, 216 vs 247 us on an odd 8-byte 2-D transpose -- opt-in
     if (const char *e = getenv("VPG_SWZ")) P.no_swz = atoi(e) == 0;
-    // TMA bulk copies per source run measured slower than per-lane 16-byte
-    // cp.async on B200 (one bulk op per 256 B-1 KiB run costs more TMA issue
-    // time than it saves): opt-in only, VPG_BULK=1
-    P.no_bulk = !(getenv("VPG_BULK") && atoi(getenv("VPG_BULK")) != 0);
+    // TMA bulk copies of the source runs: chosen per plan (see make_plan);
+    // VPG_BULK=0 never, VPG_BULK=1 wherever the runs allow it
+    if (const char *e = getenv("VPG_BULK")) {
+        P.no_bulk = atoi(e) == 0;
+        P.force_bulk = atoi(e) != 0;
+    }
     // sharded exchange plans: refine and pin the shard-indexing dims first
     std::vector<int64_t> rdims(dims, dims + rank);
     std::vector<int32_t> rsig(sigma, sigma + rank);
@@ -1341,7 +1344,16 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         p->tile_util = fill_tile_params(P, g, pitch, threads, vc, p->tile);
         // optionally the vectorised R phase runs as TMA bulk copies, one per
         // source run (16-byte aligned runs of whole 16-byte chunks; VPG_BULK=1)
-        vc.bulk = vc.vr > 1 && !vc.rshift && !P.no_bulk && (g.Ls * E) % 16 == 0 &&
+        // TMA bulk copies (one cp.async.bulk per source run, producer warp +
+        // mbarriers) instead of per-lane 16-byte cp.async: the per-lane form
+        // requests every 32-byte sector from L2 about twice (ncu
+        // lts__t_sectors_srcunit_tex_op_read = 1.96x the data, bulk 1.00x),
+        // which costs 2-15% once runs are long; below ~2 KiB the TMA issue
+        // cost per run wins (tools/perf_sweep.py, VPG_BULK=0 vs 1: 2-6 KiB
+        // source runs with >= 512-byte destination runs +3..15%, 256-byte
+        // runs -10..-25%; cfg5 729 -> 713 us)
+        const bool long_runs = g.Ls * E >= 2048 && g.Ld * E >= 512;
+        vc.bulk = vc.vr > 1 && !vc.rshift && !P.no_bulk && (long_runs || P.force_bulk) && (g.Ls * E) % 16 == 0 &&
                   (g.a_part < 0 ||
                    ((g.Ls / g.ext[g.a_part]) * (P.d[g.a_part] % g.ext[g.a_part]) * E) % 16 == 0) &&
                   g.n_runidx <= kMaxPhaseDims;

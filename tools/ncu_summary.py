@@ -33,6 +33,9 @@ METRICS = OrderedDict([
     ("inst_executed", ("smsp__inst_executed.sum", 1.0)),
     ("lds_bank_conflicts", ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", 1.0)),
     ("sts_bank_conflicts", ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum", 1.0)),
+    ("st_bytes_per_sector", ("smsp__sass_average_data_bytes_per_sector_mem_global_op_st.ratio", 1.0)),
+    ("ld_bytes_per_sector", ("smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.ratio", 1.0)),
+    ("ldgsts_sectors", ("smsp__sass_l1tex_m_xbar2l1tex_read_sectors_mem_global_op_ldgsts_cache_bypass.sum", 1.0)),
     ("grid", ("launch__grid_size", 1.0)),
     ("block", ("launch__block_size", 1.0)),
 ])
@@ -105,22 +108,30 @@ def main():
     md = [f"# ncu summary ({a.round})", "",
           f"Capture: `{os.path.basename(a.rep)}` (`ncu --set full --clock-control none`, one launch per row; "
           "cold-cache, serialised -- compare shares, not absolutes).", "",
-          "| config | kernel | us | DRAM read MB | DRAM write MB | traffic / algorithmic | DRAM % peak | regs | occupancy % | issue % | LDS conflicts |",
-          "|---|---|---|---|---|---|---|---|---|---|---|"]
+          "| config | kernel | us | DRAM read MB | DRAM write MB | traffic / algorithmic | DRAM % peak | regs | occupancy % | issue % | LDS conflicts | read sector eff | write sector eff |",
+          "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for lab, row in zip(labels, rows):
         vals = {k: value(hdr, units, row, m, s) for k, (m, s) in METRICS.items()}
         kname = row[hdr.index("Kernel Name")].split("(")[0].replace("void ", "")
-        base_cfg, _, shards = lab.partition("/")          # "cfg5/2": one rank's exchange kernel of 2
+        base_cfg, _, shards = lab.partition("/")          # "cfg5/2": one rank's exchange kernel of 2 ("8p": pull)
         wl = CONFIGS.get(base_cfg)
-        alg = wl.algorithmic_bytes // (int(shards) if shards else 1) if wl else None
+        alg = wl.algorithmic_bytes // (int(shards.rstrip("p")) if shards else 1) if wl else None
         traffic = (vals["dram_read"] or 0) + (vals["dram_write"] or 0)
+        # sector efficiency: useful bytes per 32-byte sector requested from L2
+        # (cp.async reads: algorithmic read bytes / LDGSTS sectors; LDG and STG
+        # from the SASS bytes-per-sector counters)
+        if vals.get("ldgsts_sectors"):
+            rd_eff = (alg / 2) / (vals["ldgsts_sectors"] * 32) if alg else None
+        else:
+            rd_eff = (vals["ld_bytes_per_sector"] or 0) / 32
+        wr_eff = (vals["st_bytes_per_sector"] or 0) / 32
         e = {"kernel": kname, **vals, "dram_bytes": traffic, "algorithmic_bytes": alg,
-             "traffic_ratio": traffic / alg if alg else None}
+             "traffic_ratio": traffic / alg if alg else None, "read_sector_eff": rd_eff, "write_sector_eff": wr_eff}
         summ["kernels"][lab] = e      # later rows (2nd iteration) overwrite the first: warm plan cache
         md_row = (f"| {lab} | `{kname}` | {vals['duration_us']:.1f} | {vals['dram_read']/1e6:.1f} | "
                   f"{vals['dram_write']/1e6:.1f} | {e['traffic_ratio']:.3f} | {vals['dram_pct_peak']:.1f} | "
                   f"{vals['registers']:.0f} | {vals['occupancy_pct']:.1f} | {vals['issue_active_pct']:.1f} | "
-                  f"{vals['lds_bank_conflicts']:.0f} |")
+                  f"{vals['lds_bank_conflicts']:.0f} | {rd_eff:.3f} | {wr_eff:.3f} |")
         md.append(md_row)
     md += ["", "DRAM write bytes below the algorithmic half mean the tail of the output was still in the",
            "126 MB L2 when the kernel ended (small configs); the flushed bench times include no such hits",
@@ -133,8 +144,8 @@ def main():
         md.append("")
         md.append("The flush kernels (torch fill/reduce) and the parity/comparator kernels (torch index, "
                   "remainder, copy) are outside the timed region; inside it the tile/rows kernels are the only "
-                  "kernels launched (one per step).  The tile launches also include the untimed measured "
-                  "planning (autotune) and warm-ups.  " + (a.launch_note or ""))
+                  "kernels launched (one per step).  The tile/rows launches also include the warm-ups and the "
+                  "untimed steady-state loops.  " + (a.launch_note or ""))
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     with open(os.path.join(ROOT, "profiles", "ncu_summary.json"), "w") as f:
         json.dump(summ, f, indent=1)
