@@ -119,10 +119,14 @@ struct PhaseDesc {
     uint32_t mask_full;            // slots checked in every tile (padding)
     uint32_t mask_ragged;          // slots checked in ragged tiles
     uint32_t off_tab;              // smem byte offset of this phase's outer table
-    // shifted-run mode only: 16-byte chunk swizzle of the smem rows.  Chunk
-    // j of row r = s / pitch lives at chunk j ^ ((r >> (swz - 1)) & 7), so
-    // the W lanes, which read one column across consecutive rows, spread
-    // over all banks (swz = 0: off; pitch is a multiple of 8 chunks)
+    // 16-byte chunk swizzle of the smem rows.  Chunk j of row r = s / pitch
+    // lives at chunk j ^ ((r >> (swz - 1)) & 7), so the W lanes, which read
+    // one column across consecutive rows, spread over all banks (swz = 0:
+    // off; pitch is a multiple of 8 chunks).  Shifted-run mode (opt-in), and
+    // the 128-byte congruent layout of aligned runs: unpadded rows at the
+    // same offset modulo 128 bytes as their source lines, so per-lane
+    // cp.async requests each L2 sector once (a padded row makes the LDGSTS
+    // split every line: ~2x L2 sector reads, tools/ldgsts_probe.cu)
     uint32_t swz;
     FastDiv spitch;                // divides an smem element offset by the pitch
 };

@@ -37,7 +37,8 @@ constexpr int64_t kRowsMinBytes = 512;
 constexpr double kRunOverheadBytes = 128.0;
 constexpr double kTileOverheadBytes = 2048.0;  // cost of one tile (decode + 2 barriers)
 constexpr int64_t kTileBudgetBytes = 48 * 1024;  // staged elements per CTA
-constexpr double kResidueCostFactor = 0.9;   // residue-stride shifted tiles: no W shift arithmetic
+constexpr double kResidueCostFactor = 0.9;
+constexpr double kSw128CostFactor = 0.85;    // 128-byte congruent rows: half the L2 sector requests of the R phase   // residue-stride shifted tiles: no W shift arithmetic
 constexpr double kSmallProblemBytes = 512.0 * 1024 * 1024;   // algorithmic bytes below which tiles shrink
 
 int64_t gcd64(int64_t a, int64_t b) {
@@ -69,6 +70,7 @@ struct Problem {
     int64_t cta_smem;     // per-CTA shared-memory target (bytes)
     bool no_shift = false; // disable shifted-run reads (VPG_NO_SHIFT)
     bool no_res = false;   // disable residue row strides for shifted runs (VPG_NO_RES)
+    bool no_sw128 = false; // disable the 128-byte congruent layout (VPG_NO_SW128; bulk-read plans)
     bool no_bulk = false;  // TMA bulk source reads off (VPG_BULK=0, pull exchanges)
     bool force_bulk = false; // TMA bulk source reads wherever they apply (VPG_BULK=1)
     bool no_swz = true;    // shifted-run chunk swizzle is opt-in (VPG_SWZ=1)
@@ -323,6 +325,7 @@ struct VecChoice {
     bool bulk = false;     // R as one cp.async.bulk per source run (producer warp + mbarriers)
     int swz = 0;           // shifted-run mode: chunk swizzle (0 off, else 1 + row shift)
     bool rres = false;     // shifted-run mode with residue row strides (no per-element shift in W)
+    bool sw128 = false;    // aligned runs: unpadded rows congruent to their source lines mod 128 B, chunk-swizzled
 };
 
 // smem strides of the tile dims for a given pitch (source run dense, run
@@ -670,6 +673,25 @@ bool w_vectorizable(const Problem &Pb, const TileGeom &g, int V) {
     return true;
 }
 
+// 128-byte congruent layout for 16-byte source reads: the run is a whole
+// number of 128-byte lines and a power of two (cheap swizzle divide), and
+// every stride that moves a run start (run-index dims, grid digits, the
+// partial source dim's tile step, the shard bias) keeps 128-byte alignment.
+bool sw128_possible(const Problem &Pb, const TileGeom &g) {
+    const int64_t E = Pb.E;
+    if ((g.Ls * E) % 128 || (g.Ls & (g.Ls - 1))) return false;
+    if (Pb.pull) return false;
+    if (Pb.G >= 1 && ((Pb.n / Pb.G) * E) % 128) return false;
+    bool in_run[kMaxRank] = {false};
+    for (int i = 0; i < g.nsrc; ++i) in_run[g.src_dims[i]] = true;
+    for (int k = 0; k < Pb.r; ++k) {
+        if (Pb.d[k] <= 1) continue;
+        if (!in_run[k] && (Pb.in_stride[k] * E) % 128) return false;
+        if (in_run[k] && g.ext[k] < Pb.d[k] && (Pb.in_stride[k] * g.ext[k] * E) % 128) return false;
+    }
+    return true;
+}
+
 // Fill TileParams for geometry g, smem pitch (elements) and vector choice.
 double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, int NT, VecChoice vc,
                         TileParams &tp) {
@@ -698,9 +720,9 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
     tp.ph[0].rshift = vc.rshift ? (vc.rres ? 2u : 1u) : 0u;
     tp.hmask = (uint32_t)hmask;
     tp.rres = vc.rres ? (uint32_t)(V - 1) : 0u;
-    if (vc.swz && vc.rshift && vc.vw == 1 && !vc.bulk) {
+    if ((vc.swz && vc.rshift && vc.vw == 1 && !vc.bulk) || (vc.sw128 && !vc.bulk)) {
         for (int ph = 0; ph < 2; ++ph) {
-            tp.ph[ph].swz = (uint32_t)vc.swz;
+            tp.ph[ph].swz = vc.sw128 ? 1u : (uint32_t)vc.swz;
             tp.ph[ph].spitch = make_fastdiv(pitch);
         }
     }
@@ -802,8 +824,8 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
         if (Pb.nbuf > 0) stages = (uint32_t)Pb.nbuf;
     }
     tp.nbuf = stages;
-    tp.off_buf = take(buf_bytes * tp.nbuf, 16);
-    tp.smem_bytes = (o + 15) / 16 * 16;
+    tp.off_buf = take(buf_bytes * tp.nbuf, 128);
+    tp.smem_bytes = (o + 15) / 16 * 16 + 128;     // + slack: the kernel aligns its base to 128 bytes
     return u0 * u1;
 }
 
@@ -862,7 +884,28 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
             opts.push_back({vr, vw, false});
         }
     if (rs) opts.push_back({V, 1, true});
+    const bool s128 = rv && !Pb.no_sw128 && sw128_possible(Pb, g);
     for (const Opt &op : opts) {
+        if (s128 && op.vr > 1 && !op.rshift && (int64_t)(g.T / g.Ls) * g.Ls * Pb.E <= Pb.budget + 8192) {
+            // congruent rows (pitch = run, no padding), chunk swizzle against
+            // the W bank conflicts; per-lane cp.async then requests each L2
+            // sector once instead of ~twice
+            TileParams tp;
+            VecChoice vc;
+            vc.vr = op.vr;
+            vc.vw = op.vw;
+            vc.sw128 = true;
+            fill_tile_params(Pb, g, (uint32_t)g.Ls, NT, vc, tp);
+            double c = tile_cost(Pb, tp) * kSw128CostFactor;
+            if (getenv("VPG_DEBUG_PLAN"))
+                fprintf(stderr, "[plan] Ls %lld Ld %lld pitch %lld vr %d vw %d sw128 cost %.1f per-elem %.3f\n",
+                        (long long)g.Ls, (long long)g.Ld, (long long)g.Ls, vc.vr, vc.vw, c, c / (double)g.T);
+            if (best < 0 || c < best - 1e-9) {
+                best = c;
+                pitch_out = (uint32_t)g.Ls;
+                vc_out = vc;
+            }
+        }
         if (op.rshift && !Pb.no_swz) {
             // swizzled rows: pitch a multiple of 8 chunks, row shift 0..3
             const int64_t base = (g.Ls + V - 1 + V - 1) / V * V;
@@ -916,7 +959,8 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
         }
         const int step = (op.vr > 1 || op.vw > 1) ? V : 1;
         const int64_t base = op.rshift ? (g.Ls + V - 1 + V - 1) / V * V : g.Ls;
-        for (int pad = 0; pad <= 32; pad += step) {
+        static const int pad_max = getenv("VPG_PAD_MAX") ? atoi(getenv("VPG_PAD_MAX")) : 32;   // experiments
+        for (int pad = 0; pad <= pad_max; pad += step) {
             uint32_t pitch = (uint32_t)(base + pad);
             if ((int64_t)(g.T / g.Ls) * pitch * Pb.E > Pb.budget + 8192) break;
             TileParams tp;
@@ -1197,6 +1241,7 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
     if (const char *e = getenv("VPG_THREADS")) force_threads = atoi(e);
     if (getenv("VPG_NO_SHIFT")) P.no_shift = true;
     if (getenv("VPG_NO_RES")) P.no_res = true;
+    if (getenv("VPG_NO_SW128")) P.no_sw128 = true;
     // the chunk swizzle removes the W bank conflicts of shifted runs but costs
     // a divide and a few integer ops per element: measured 28.4 vs 20.5 us on
     // cfg3, 216 vs 247 us on an odd 8-byte 2-D transpose -- opt-in
@@ -1341,7 +1386,6 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         uint32_t pitch;
         VecChoice vc;
         choose_pitch_vec(P, g, threads, pitch, vc);
-        p->tile_util = fill_tile_params(P, g, pitch, threads, vc, p->tile);
         // optionally the vectorised R phase runs as TMA bulk copies, one per
         // source run (16-byte aligned runs of whole 16-byte chunks; VPG_BULK=1)
         // TMA bulk copies (one cp.async.bulk per source run, producer warp +
@@ -1353,11 +1397,20 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         // source runs with >= 512-byte destination runs +3..15%, 256-byte
         // runs -10..-25%; cfg5 729 -> 713 us)
         const bool long_runs = g.Ls * E >= 2048 && g.Ld * E >= 512;
-        vc.bulk = vc.vr > 1 && !vc.rshift && !P.no_bulk && (long_runs || P.force_bulk) && (g.Ls * E) % 16 == 0 &&
-                  (g.a_part < 0 ||
-                   ((g.Ls / g.ext[g.a_part]) * (P.d[g.a_part] % g.ext[g.a_part]) * E) % 16 == 0) &&
-                  g.n_runidx <= kMaxPhaseDims;
-        if (vc.bulk) p->tile_util = fill_tile_params(P, g, pitch, threads, vc, p->tile);
+        auto bulk_for = [&](const VecChoice &v) {
+            return v.vr > 1 && !v.rshift && !P.no_bulk && (long_runs || P.force_bulk) && (g.Ls * E) % 16 == 0 &&
+                   (g.a_part < 0 ||
+                    ((g.Ls / g.ext[g.a_part]) * (P.d[g.a_part] % g.ext[g.a_part]) * E) % 16 == 0) &&
+                   g.n_runidx <= kMaxPhaseDims;
+        };
+        if (vc.sw128 && bulk_for(vc)) {
+            // bulk copies request each sector once anyway and do not swizzle:
+            // re-plan the padded layout for them
+            P.no_sw128 = true;
+            choose_pitch_vec(P, g, threads, pitch, vc);
+        }
+        vc.bulk = bulk_for(vc);
+        p->tile_util = fill_tile_params(P, g, pitch, threads, vc, p->tile);
         // variant without 16-byte source reads, for misaligned base pointers
         VecChoice vs = vc;
         vs.vr = 1;

@@ -158,6 +158,17 @@ __device__ __forceinline__ uint32_t swizzle(const PhaseDesc &d, uint32_t s) {
     return r * d.spitch.d + ((((c / V) ^ f) * V) | (c % V));
 }
 
+// Shared-memory slot of logical element offset s: plain, or chunk-swizzled
+// (d.swz: 16-byte chunks XOR-permuted by row inside each 128-byte block).
+template <typename W>
+__device__ __forceinline__ W *sslot(const PhaseDesc &d, W *buf, uint32_t s) {
+    return d.swz ? buf + swizzle<16 / (int)sizeof(W)>(d, s) : buf + s;
+}
+template <typename W>
+__device__ __forceinline__ const W *sslot(const PhaseDesc &d, const W *buf, uint32_t s) {
+    return d.swz ? buf + swizzle<16 / (int)sizeof(W)>(d, s) : buf + s;
+}
+
 __device__ __forceinline__ bool slot_ok(uint32_t mask, uint32_t c0, uint32_t c1, uint32_t c2, const Lim &lim) {
     return (!(mask & 1u) || c0 < lim.l0) && (!(mask & 2u) || c1 < lim.l1) && (!(mask & 4u) || c2 < lim.l2);
 }
@@ -207,40 +218,40 @@ __device__ __forceinline__ void tile_read_impl(const PhaseDesc &d, const ThreadP
     for (uint32_t o = o0; o < d.n_outer; o += d.ngroups) {
         const OuterEntry e = outer_entry(d, smem, o);
         const W *gp = gsrc + (t.g + e.g);
-        W *sp = buf + (t.s + e.s);
+        uint32_t so = t.s + e.s;
         if (mask == 0) {
             uint32_t i = 0;
             VPG_UNROLL
             for (; i + U <= n_in; i += U) {
                 if constexpr (ASYNC) {
 #pragma unroll
-                    for (int u = 0; u < U; ++u) cp_async<CP>(sp + u * s_in, gp + u * g_in);
+                    for (int u = 0; u < U; ++u) cp_async<CP>(sslot(d, buf, so + u * s_in), gp + u * g_in);
                 } else {
                     W v[U];
 #pragma unroll
                     for (int u = 0; u < U; ++u) v[u] = __ldg(gp + u * g_in);
 #pragma unroll
-                    for (int u = 0; u < U; ++u) sp[u * s_in] = v[u];
+                    for (int u = 0; u < U; ++u) *sslot(d, buf, so + u * s_in) = v[u];
                 }
                 gp += U * g_in;
-                sp += U * s_in;
+                so += U * s_in;
             }
             for (; i < n_in; ++i) {
-                if constexpr (ASYNC) cp_async<CP>(sp, gp);
-                else *sp = __ldg(gp);
+                if constexpr (ASYNC) cp_async<CP>(sslot(d, buf, so), gp);
+                else *sslot(d, buf, so) = __ldg(gp);
                 gp += g_in;
-                sp += s_in;
+                so += s_in;
             }
         } else {
             uint32_t c0 = t.c0 + e.c0, c1 = t.c1 + e.c1, c2 = t.c2;
             VPG_UNROLL
             for (uint32_t i = 0; i < n_in; ++i) {
                 if (slot_ok(mask, c0, c1, c2, lim)) {
-                    if constexpr (ASYNC) cp_async<CP>(sp, gp);
-                    else *sp = __ldg(gp);
+                    if constexpr (ASYNC) cp_async<CP>(sslot(d, buf, so), gp);
+                    else *sslot(d, buf, so) = __ldg(gp);
                 }
                 gp += g_in;
-                sp += s_in;
+                so += s_in;
                 c0 += d.c_in[0];
                 c1 += d.c_in[1];
                 c2 += d.c_in[2];
@@ -344,7 +355,8 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
                 if constexpr (VEC) {
                     uint4 v[U];
 #pragma unroll
-                    for (int u = 0; u < U; ++u) v[u] = *reinterpret_cast<const uint4 *>(sp + u * s_in);
+                    for (int u = 0; u < U; ++u)
+                        v[u] = *reinterpret_cast<const uint4 *>(sslot(d, buf, (uint32_t)(sp - buf) + u * s_in));
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         const W *w = reinterpret_cast<const W *>(&v[u]);
@@ -367,7 +379,7 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
             }
             for (; i < n_in; ++i) {
                 if constexpr (VEC) {
-                    uint4 v = *reinterpret_cast<const uint4 *>(sp);
+                    uint4 v = *reinterpret_cast<const uint4 *>(sslot(d, buf, (uint32_t)(sp - buf)));
                     const W *w = reinterpret_cast<const W *>(&v);
 #pragma unroll
                     for (int j = 0; j < V; ++j) st_out(gp + j * vs, w[j]);
@@ -385,7 +397,7 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
             for (uint32_t i = 0; i < n_in; ++i) {
                 if (slot_ok(mask, c0, c1, c2, lim)) {
                     if constexpr (VEC) {
-                        uint4 v = *reinterpret_cast<const uint4 *>(sp);
+                        uint4 v = *reinterpret_cast<const uint4 *>(sslot(d, buf, (uint32_t)(sp - buf)));
                         const W *w = reinterpret_cast<const W *>(&v);
 #pragma unroll
                         for (int j = 0; j < V; ++j) st_out(gp + j * vs, w[j]);
@@ -556,9 +568,13 @@ constexpr int kRing = kMaxStages + 2;
 template <typename W, bool ASYNC>
 __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restrict__ src, W *__restrict__ dst,
                                           const ShardArgs &sa) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ int64_t s_base[kRing][2];
     __shared__ uint32_t s_valid[kRing][2];
+    // the planner's layout is relative to a 128-byte aligned base (it
+    // allocates 128 bytes of slack): staged rows then sit at the same offset
+    // modulo 128 bytes as their source lines (see PhaseDesc::swz)
+    unsigned char *const smem = smem_raw + ((128u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 127u)) & 127u);
     const uint32_t tid = threadIdx.x, NT = blockDim.x;
     const uint32_t first = blockIdx.x, step = gridDim.x;
     if (first >= p.num_tiles) return;
@@ -693,10 +709,11 @@ __device__ __forceinline__ void bulk_g2s(void *sdst, const void *gsrc, uint32_t 
 template <typename W>
 __device__ __forceinline__ void tile_body_bulk(const TileParams &p, const W *__restrict__ src, W *__restrict__ dst,
                                                const ShardArgs &sa) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
     __shared__ int64_t s_base[kMaxStages][2];
     __shared__ uint32_t s_valid[kMaxStages][2];
+    unsigned char *const smem = smem_raw + ((128u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 127u)) & 127u);
     const uint32_t tid = threadIdx.x;
     const uint32_t NC = blockDim.x - 32;              // consumer threads (the W phase was planned for NC)
     const uint32_t first = blockIdx.x, step = gridDim.x;

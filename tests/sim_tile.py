@@ -254,11 +254,20 @@ def simulate(program, src_words: np.ndarray, threads: int | None = None, shard_o
                             else:
                                 if V > 1 and ((gabs % V).any() or (sp % V).any()):
                                     raise SimError("R vector access misaligned")
+                                # chunk swizzle (128-byte congruent layout): V-element
+                                # vectors stay contiguous, scalar words move one by one
+                                spx = _swizzle(d, sp, 16 // E if E <= 16 else 1)
+                                # (the logical slot is congruent to the source mod 128 B;
+                                # the swizzle only permutes chunks inside a 128-byte block)
+                                if d.swz and not tp.pull and V > 1 and ((sp * E) % 128 != (gabs * E) % 128).any():
+                                    raise SimError("congruent layout: smem and global offsets differ mod 128 B")
+                                if d.swz and ((spx * E) // 128 != (sp * E) // 128).any():
+                                    raise SimError("chunk swizzle left its 128-byte block")
                                 for j in range(V):
                                     _chk(gabs + j, n, "R global")
-                                    _chk(sp + j, alloc, "R smem")
-                                    smem[sp + j] = src_words[gabs + j]
-                                    smem_valid[sp + j] = True
+                                    _chk(spx + j, alloc, "R smem")
+                                    smem[spx + j] = src_words[gabs + j]
+                                    smem_valid[spx + j] = True
                         else:
                             hh = (sb + th[sel][ok] + eh[0] + i * d.h_in) & tp.hmask if tp.hmask else 0
                             spx = _swizzle(d, sp + hh + tbase, 16 // E if E <= 16 else 1)
