@@ -355,15 +355,16 @@ void tile_sstrides(const Problem &Pb, const TileGeom &g, uint32_t pitch, int64_t
 
 // Residue row strides for misaligned source runs (shifted-run mode without
 // a per-element shift).  Each run-index dim k gets an smem stride S_k with
-// S_k == in_stride[k] (mod V), and the tile sits at smem offset
-// (source tile base mod V).  Every run then starts at the same offset
-// modulo V in shared and in global memory, so its 16-byte aligned global
-// superset lands on a 16-byte aligned smem chunk (R) and the W phase reads
-// element (run, e) at an affine offset.  S_1 >= NCK*V (chunks per run) and
-// S_{k+1} >= e_k * S_k keep the aligned row spans disjoint.  Returns the
-// elements one tile buffer needs (V - 1 of base shift included).
+// S_k == in_stride[k] (mod M, M = res_modulus: 128 bytes of elements), and
+// the tile sits at smem offset (source tile base mod M).  Every run then
+// starts at the same offset modulo M in shared and in global memory, so its
+// 16-byte aligned global superset lands on a 16-byte aligned smem chunk of
+// the congruent 128-byte block (R: one L2 request per sector) and the W
+// phase reads element (run, e) at an affine offset.  S_1 >= NCK*V (chunks
+// per run) and S_{k+1} >= e_k * S_k keep the aligned row spans disjoint.
+// Returns the elements one tile buffer needs (M - 1 of base shift included).
 int64_t tile_sstrides_res(const Problem &Pb, const TileGeom &g, uint32_t pitch, int V, int64_t *sstr,
-                          bool *in_src) {
+                          bool *in_src, int64_t M) {
     for (int k = 0; k < Pb.r; ++k) in_src[k] = false;
     int64_t acc = 1;
     for (int i = 0; i < g.nsrc; ++i) {
@@ -374,8 +375,8 @@ int64_t tile_sstrides_res(const Problem &Pb, const TileGeom &g, uint32_t pitch, 
     }
     const int64_t nck = (g.Ls + V - 1 + V - 1) / V;
     auto with_res = [&](int64_t lo, int64_t res) {
-        int64_t r = ((res % V) + V) % V;
-        int64_t x = lo + (((r - lo) % V) + V) % V;
+        int64_t r = ((res % M) + M) % M;
+        int64_t x = lo + (((r - lo) % M) + M) % M;
         return x;
     };
     int64_t need = std::max<int64_t>((int64_t)pitch, nck * V);
@@ -387,7 +388,17 @@ int64_t tile_sstrides_res(const Problem &Pb, const TileGeom &g, uint32_t pitch, 
         last += (g.ext[k] - 1) * sstr[k];
         need = sstr[k] * g.ext[k];
     }
-    return (last + (V - 1) + nck * V + V - 1) / V * V;
+    return (last + (M - 1) + nck * V + V - 1) / V * V;
+}
+
+// Residue modulus (elements) of the residue row strides: 16 bytes (chunk
+// alignment).  VPG_RES_MOD=128 also puts each run at its source line's
+// offset modulo 128 B: cfg3's L2 read sectors drop 2.49M -> 1.66M (ncu), but
+// the longer row strides raise its W bank conflicts 125k -> 539k and the
+// time is unchanged (16.6-16.9 vs 16.8-16.9 us steady), so it stays opt-in.
+int64_t res_modulus(int E) {
+    static const int64_t bytes = getenv("VPG_RES_MOD") ? std::max(16L, atol(getenv("VPG_RES_MOD"))) : 16;
+    return std::max<int64_t>(16 / E, bytes / E);
 }
 
 // Phase dims (fastest first) with adjacent dims fused when they are
@@ -706,7 +717,8 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
     int64_t sstr[kMaxRank];
     bool in_src[kMaxRank];
     const int V = 16 / Pb.E;
-    if (vc.rres) tp.tile_elems_alloc = (uint32_t)tile_sstrides_res(Pb, g, pitch, V, sstr, in_src);
+    const int64_t M = res_modulus(Pb.E);
+    if (vc.rres) tp.tile_elems_alloc = (uint32_t)tile_sstrides_res(Pb, g, pitch, V, sstr, in_src, M);
     else tile_sstrides(Pb, g, pitch, sstr, in_src);
     int slot_of_dim[kMaxRank];
     for (int k = 0; k < r; ++k) slot_of_dim[k] = -1;
@@ -719,7 +731,7 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
     double u1 = make_phase(phase_dims(Pb, g, sstr, slot_of_dim, true, vc.vw, hmask), NT, tp.ph[1], tp.lim_split[1]);
     tp.ph[0].rshift = vc.rshift ? (vc.rres ? 2u : 1u) : 0u;
     tp.hmask = (uint32_t)hmask;
-    tp.rres = vc.rres ? (uint32_t)(V - 1) : 0u;
+    tp.rres = vc.rres ? (uint32_t)(M - 1) : 0u;
     if ((vc.swz && vc.rshift && vc.vw == 1 && !vc.bulk) || (vc.sw128 && !vc.bulk)) {
         for (int ph = 0; ph < 2; ++ph) {
             tp.ph[ph].swz = vc.sw128 ? 1u : (uint32_t)vc.swz;

@@ -244,6 +244,9 @@ def simulate(program, src_words: np.ndarray, threads: int | None = None, shard_o
                                     sd = spl - (spl % V)
                                     if ((spl - sd) != (gabs - ga)).any():
                                         raise SimError("residue mode: smem and global offsets differ mod V")
+                                    M = tp.rres + 1          # residue modulus (elements)
+                                    if ((spl - gabs) % M).any():
+                                        raise SimError("residue mode: smem and global offsets differ mod the residue modulus")
                                 else:
                                     sd = _swizzle(d, sp, V)
                                 for j in range(V):
