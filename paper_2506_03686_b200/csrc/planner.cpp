@@ -691,8 +691,7 @@ bool w_vectorizable(const Problem &Pb, const TileGeom &g, int V) {
 bool sw128_possible(const Problem &Pb, const TileGeom &g) {
     const int64_t E = Pb.E;
     if ((g.Ls * E) % 128 || (g.Ls & (g.Ls - 1))) return false;
-    if (Pb.pull) return false;
-    if (Pb.G >= 1 && ((Pb.n / Pb.G) * E) % 128) return false;
+    if (Pb.G >= 1 && ((Pb.n / Pb.G) * E) % 128) return false;   // shard bases keep the congruence
     bool in_run[kMaxRank] = {false};
     for (int i = 0; i < g.nsrc; ++i) in_run[g.src_dims[i]] = true;
     for (int k = 0; k < Pb.r; ++k) {

@@ -508,14 +508,15 @@ __device__ __forceinline__ void tile_read_pull(const TileParams &p, const ShardA
     for (uint32_t o = o0; o < d.n_outer; o += d.ngroups) {
         const OuterEntry e = outer_entry(d, smem, o);
         int64_t go = sbase + t.g + e.g;
-        W *sp = buf + (t.s + e.s);
+        uint32_t so = t.s + e.s;
         uint32_t c0 = t.c0 + e.c0, c1 = t.c1 + e.c1, c2 = t.c2;
         VPG_UNROLL
         for (uint32_t i = 0; i < d.n_in; ++i) {
             if (mask == 0 || slot_ok(mask, c0, c1, c2, lim)) {
+                W *sp = sslot(d, buf, so);
                 if constexpr (ASYNC && sizeof(W) < 16) {
                     if (d.rshift) {
-                        W *sd = d.rshift == 2 ? reinterpret_cast<W *>((uintptr_t)sp & ~(uintptr_t)15) : sp;
+                        W *sd = d.rshift == 2 ? reinterpret_cast<W *>((uintptr_t)(buf + so) & ~(uintptr_t)15) : buf + so;
                         cp_async<16>(sd, pull_ptr(p, sa, src, go & ~(int64_t)(V - 1)));
                     } else if (d.vec > 1) {
                         cp_async<16>(sp, pull_ptr(p, sa, src, go));
@@ -529,7 +530,7 @@ __device__ __forceinline__ void tile_read_pull(const TileParams &p, const ShardA
                 }
             }
             go += d.g_in;
-            sp += d.s_in;
+            so += d.s_in;
             c0 += d.c_in[0];
             c1 += d.c_in[1];
             c2 += d.c_in[2];

@@ -35,7 +35,8 @@ METRICS = OrderedDict([
     ("sts_bank_conflicts", ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum", 1.0)),
     ("st_bytes_per_sector", ("smsp__sass_average_data_bytes_per_sector_mem_global_op_st.ratio", 1.0)),
     ("ld_bytes_per_sector", ("smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.ratio", 1.0)),
-    ("ldgsts_sectors", ("smsp__sass_l1tex_m_xbar2l1tex_read_sectors_mem_global_op_ldgsts_cache_bypass.sum", 1.0)),
+    ("l2_read_sectors", ("lts__t_sectors_srcunit_tex_op_read.sum", 1.0)),
+    ("l2_write_sectors", ("lts__t_sectors_srcunit_tex_op_write.sum", 1.0)),
     ("grid", ("launch__grid_size", 1.0)),
     ("block", ("launch__block_size", 1.0)),
 ])
@@ -108,7 +109,7 @@ def main():
     md = [f"# ncu summary ({a.round})", "",
           f"Capture: `{os.path.basename(a.rep)}` (`ncu --set full --clock-control none`, one launch per row; "
           "cold-cache, serialised -- compare shares, not absolutes).", "",
-          "| config | kernel | us | DRAM read MB | DRAM write MB | traffic / algorithmic | DRAM % peak | regs | occupancy % | issue % | LDS conflicts | read sector eff | write sector eff |",
+          "| config | kernel | us | DRAM read MB | DRAM write MB | traffic / algorithmic | DRAM % peak | regs | occupancy % | issue % | LDS conflicts | L2 read sector eff | L2 write sector eff |",
           "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for lab, row in zip(labels, rows):
         vals = {k: value(hdr, units, row, m, s) for k, (m, s) in METRICS.items()}
@@ -117,14 +118,11 @@ def main():
         wl = CONFIGS.get(base_cfg)
         alg = wl.algorithmic_bytes // (int(shards.rstrip("p")) if shards else 1) if wl else None
         traffic = (vals["dram_read"] or 0) + (vals["dram_write"] or 0)
-        # sector efficiency: useful bytes per 32-byte sector requested from L2
-        # (cp.async reads: algorithmic read bytes / LDGSTS sectors; LDG and STG
-        # from the SASS bytes-per-sector counters)
-        if vals.get("ldgsts_sectors"):
-            rd_eff = (alg / 2) / (vals["ldgsts_sectors"] * 32) if alg else None
-        else:
-            rd_eff = (vals["ld_bytes_per_sector"] or 0) / 32
-        wr_eff = (vals["st_bytes_per_sector"] or 0) / 32
+        # sector efficiency: useful bytes per byte of 32-byte sectors the SMs
+        # request from L2 (reads: algorithmic read bytes / L2 read sectors;
+        # writes likewise) -- 1.0 = every sector requested once, whole
+        rd_eff = (alg / 2) / (vals["l2_read_sectors"] * 32) if alg and vals.get("l2_read_sectors") else float("nan")
+        wr_eff = (alg / 2) / (vals["l2_write_sectors"] * 32) if alg and vals.get("l2_write_sectors") else float("nan")
         e = {"kernel": kname, **vals, "dram_bytes": traffic, "algorithmic_bytes": alg,
              "traffic_ratio": traffic / alg if alg else None, "read_sector_eff": rd_eff, "write_sector_eff": wr_eff}
         summ["kernels"][lab] = e      # later rows (2nd iteration) overwrite the first: warm plan cache
