@@ -135,6 +135,89 @@ __global__ void __launch_bounds__(256) rows_kernel(const __grid_constant__ RowsP
     }
 }
 
+// ------------------------------------------------------------------ ROWS, TMA bulk
+// K1 for long 16-byte-aligned rows as a DMA pipeline: one thread per CTA
+// moves each work item (a row, or a chunk of a long row) global -> smem ->
+// global with two cp.async.bulk operations (TMA), S slots deep: loads run
+// S-1 items ahead, a slot is refilled once the bulk store that read it has
+// finished reading (cp.async.bulk.wait_group.read).  No register round
+// trip and no per-lane address math; several CTAs per SM keep enough bytes
+// in flight.
+constexpr int kRowsBulkSlots = 4;
+constexpr int64_t kRowsBulkMinBytes = 1024;   // shorter rows: per-lane 16-byte rows_kernel
+
+__device__ __forceinline__ void bulk_s2g(void *gdst, const void *ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst),
+                 "r"(smem_u32(ssrc)), "r"(bytes)
+                 : "memory");
+}
+
+__global__ void __launch_bounds__(32) rows_bulk_kernel(const __grid_constant__ RowsParams p,
+                                                       const unsigned char *__restrict__ src,
+                                                       unsigned char *__restrict__ dst, uint32_t E,
+                                                       uint32_t slot_bytes, uint32_t rpi) {
+    extern __shared__ __align__(128) unsigned char rb_smem[];
+    __shared__ __align__(8) uint64_t bar[kRowsBulkSlots];
+    constexpr uint32_t S = kRowsBulkSlots;
+    pdl_trigger();
+    if (threadIdx.x != 0) return;
+    for (uint32_t j = 0; j < S; ++j) mbar_init(&bar[j], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    pdl_wait();
+    const uint32_t step = gridDim.x;
+    const uint32_t cnt = p.nitems > blockIdx.x ? (p.nitems - blockIdx.x + step - 1) / step : 0u;
+    const uint32_t row_bytes = (uint32_t)(p.row_len * E), chunk_bytes = p.chunk_vecs * 16u;
+    // work item w: rows [w*rpi, w*rpi + rpi) when rows are short (rpi > 1,
+    // one load per row, one store of the contiguous destination block), else
+    // chunk (w mod nchunks) of row (w / nchunks)
+    auto src_row = [&](uint32_t q) {
+        uint32_t rem = q;
+        int64_t so = 0;
+        for (int i = 0; i < p.ndig; ++i) {
+            const uint32_t qq = fdiv(rem, p.dig[i].ext);
+            so += (int64_t)(rem - qq * p.dig[i].ext.d) * p.dig[i].src_stride;
+            rem = qq;
+        }
+        return src + so * E;
+    };
+    auto item = [&](uint32_t k, uint32_t &q0, uint32_t &nr, uint32_t &c0) -> uint32_t {
+        const uint32_t w = blockIdx.x + k * step;
+        if (rpi > 1) {
+            q0 = w * rpi;
+            nr = min(rpi, p.nrows - q0);
+            c0 = 0;
+            return nr * row_bytes;
+        }
+        q0 = fdiv(w, p.nchunks);
+        nr = 1;
+        c0 = (w - q0 * p.nchunks.d) * chunk_bytes;
+        return min(chunk_bytes, row_bytes - c0);
+    };
+    auto load = [&](uint32_t k) {
+        uint32_t q0, nr, c0;
+        const uint32_t n = item(k, q0, nr, c0);
+        const uint32_t j = k % S;
+        mbar_arrive_expect_tx(&bar[j], n);
+        for (uint32_t r = 0; r < nr; ++r)
+            bulk_g2s(rb_smem + j * slot_bytes + r * row_bytes, src_row(q0 + r) + c0, nr > 1 ? row_bytes : n, &bar[j]);
+    };
+    for (uint32_t k = 0; k + 1 < S && k < cnt; ++k) load(k);
+    for (uint32_t k = 0; k < cnt; ++k) {
+        const uint32_t j = k % S;
+        mbar_wait(&bar[j], (k / S) & 1);
+        uint32_t q0, nr, c0;
+        const uint32_t n = item(k, q0, nr, c0);
+        bulk_s2g(dst + (int64_t)q0 * row_bytes + c0, rb_smem + j * slot_bytes, n);
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        if (k + S - 1 < cnt) {
+            // slot (k + S - 1) % S held item k - 1: its store must be done reading
+            asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+            load(k + S - 1);
+        }
+    }
+    asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
 // ------------------------------------------------------------------ TILE (K2/K3)
 // Ahead-of-time instantiation: the parameter block arrives as a
 // __grid_constant__ kernel argument (run-time extents/strides).  jit.cpp
@@ -351,6 +434,43 @@ vpg_status launch_rows(const vpg_plan *p, const void *src, void *dst, cudaStream
     uint32_t vlog = 0;
     while ((1u << vlog) < V) ++vlog;
     const int vb = (int)(V * E);
+    // long 16-byte rows: the TMA bulk pipeline (rows_bulk_kernel)
+    {
+        static const int mode = getenv("VPG_ROWS_BULK") ? atoi(getenv("VPG_ROWS_BULK")) : -1;
+        const int64_t row_bytes = rp.row_len * E;
+        const bool ok = vb == 16 && row_bytes % 16 == 0 && rp.nrows < 0xffffffffull;
+        if (ok && (mode == 1 || (mode < 0 && row_bytes >= kRowsBulkMinBytes))) {
+            static const uint32_t kSlot = getenv("VPG_ROWS_SLOT") ? (uint32_t)atoi(getenv("VPG_ROWS_SLOT")) : 16384;
+            RowsParams bp = rp;
+            const uint64_t rv = (uint64_t)row_bytes / 16;                  // 16-byte units per row
+            uint64_t cv = std::min<uint64_t>(rv, kSlot / 16);
+            // short rows: several whole rows per item (one store per item)
+            uint32_t rpi = row_bytes <= (int64_t)kSlot ? (uint32_t)(kSlot / row_bytes) : 1u;
+            if (rpi > 1 && (int64_t)((rp.nrows + rpi - 1) / rpi) < (int64_t)sm_count_for_current() * 12)
+                rpi = std::max<uint32_t>(1, (uint32_t)(rp.nrows / ((int64_t)sm_count_for_current() * 12)));
+            // enough items for every CTA when rows are few
+            const int64_t want = (int64_t)sm_count_for_current() * 6 * 4;
+            if ((int64_t)rp.nrows * (int64_t)((rv + cv - 1) / cv) < want) {
+                const uint64_t per = ((uint64_t)rp.nrows * rv + want - 1) / want;
+                cv = std::max<uint64_t>(64, std::min<uint64_t>(cv, (per + 63) / 64 * 64));
+            }
+            const uint64_t nch = (rv + cv - 1) / cv;
+            if ((uint64_t)rp.nrows * nch < 0xffffffffull) {
+                bp.chunk_vecs = (uint32_t)cv;
+                bp.nchunks = make_fastdiv((uint32_t)nch);
+                bp.nitems = rpi > 1 ? (uint32_t)((rp.nrows + rpi - 1) / rpi) : (uint32_t)(rp.nrows * nch);
+                const uint32_t slot = rpi > 1 ? (uint32_t)(rpi * row_bytes) : (uint32_t)(cv * 16);
+                const int smem = (int)(slot * kRowsBulkSlots);
+                int nb = occupancy(rows_bulk_kernel, 32, smem);
+                nb = std::min(nb, 8);
+                int64_t grid = std::min<int64_t>(bp.nitems, (int64_t)nb * sm_count_for_current());
+                if (grid < 1) grid = 1;
+                launch_k(rows_bulk_kernel, grid, 32, smem, st, true, bp, (const unsigned char *)src,
+                         (unsigned char *)dst, (uint32_t)E, slot, rpi);
+                return VPG_OK;
+            }
+        }
+    }
     // cut long rows into chunks until there are enough work items to fill
     // every SM (few long rows would otherwise leave most warps idle)
     {
