@@ -774,7 +774,8 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
     std::stable_sort(dg.begin(), dg.end(), [&Pb](const Dg &x, const Dg &y) {
         if ((x.src >= 0) != (y.src >= 0)) return y.src >= 0;
         if (x.src >= 0) return Pb.pull ? Pb.pos[x.src] < Pb.pos[y.src] : x.src < y.src;
-        return x.ds < y.ds;
+        static const bool by_src = getenv("VPG_ORDER_SRC") != nullptr;   // experiments
+        return by_src ? x.ss < y.ss : x.ds < y.ds;
     });
     tp.ngrid = (int32_t)dg.size();
     tp.grid_a = tp.grid_c = -1;
