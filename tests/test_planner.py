@@ -211,3 +211,45 @@ def test_dense_base_of_permuted_views():
         assert torch.equal(b.permute(ax), v.permute(p2))
     with pytest.raises(LayoutError):
         _dense_base(torch, base[:, :, ::2], (0, 1, 2, 3, 4))
+
+
+def test_baseline_layout_choices():
+    """The layout each BASELINE config is planned with (kernels):
+    cfg1/cfg2 the 128-byte congruent swizzled rows, cfg3 residue row strides
+    for its misaligned runs, cfg5 TMA bulk reads of its 2 KiB runs, and the
+    cfg5 pull exchange at G = 8 keeping the 256 x 128 tile."""
+    from paper_2506_03686_b200.sharded import _programs, fused_method
+    from paper_2506_03686_b200.workloads import CONFIGS
+    from tests.sim_tile import tile_params
+
+    def tp(k):
+        w = CONFIGS[k]
+        return tile_params(_plan(w.shape, w.axes, w.elem_bytes)), _plan(w.shape, w.axes, w.elem_bytes)
+
+    for k in ("cfg1", "cfg2"):
+        t, p = tp(k)
+        assert t.ph[0].swz == 1 and t.ph[1].swz == 1 and t.pitch == t.Ls and not t.bulk, k
+        assert "smem chunk swizzle" in p.text
+    t, p = tp("cfg3")
+    assert t.ph[0].rshift == 2 and t.rres == 3 and t.hmask == 0
+    t, p = tp("cfg5")
+    assert t.bulk == 1 and "TMA bulk copy" in p.text
+    w = CONFIGS["cfg5"]
+    assert fused_method(w.shape, w.axes, 8, 2) == "push"
+    assert fused_method(w.shape, w.axes, 8, 8) == "pull"
+    (pp,) = _programs(w.shape, w.axes, 8, 8, [3], pull=True)
+    t = tile_params(pp)
+    assert t.pull == 1 and t.nshards == 8 and t.dst_bias == 3 * (w.numel // 8) and t.shard_shift == 25
+    assert (pp.metadata["src_run"], pp.metadata["dst_run"]) == (256, 128)
+
+
+def test_small_problem_tiles_and_groups():
+    """Problems under 512 MiB get half-size tiles; separable thread groups
+    leave ngroups == 1 (the specialised kernel unrolls the whole walk)."""
+    from tests.sim_tile import tile_params
+
+    big = tile_params(_plan((2,) * 28, tuple(int(a) for a in np.random.default_rng(0).permutation(28)), 8))
+    small = tile_params(_plan((4096, 4096), (1, 0)))
+    assert small.T * 4 <= 24 * 1024 + 8192 < big.T * 8 + 8192
+    t = tile_params(_plan((17, 9, 13, 15, 11, 27), (5, 2, 0, 4, 1, 3)))
+    assert t.ph[0].ngroups == 1 and t.ph[1].ngroups == 1
