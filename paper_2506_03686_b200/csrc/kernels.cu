@@ -353,6 +353,11 @@ vpg_status launch_tile(const vpg_plan *p, const void *src, void *dst, const Shar
     using W = typename WordOf<E>::T;
     const int smem = (int)p->tile.smem_bytes;
     bool aligned = !(p->tile.ph[0].vec > 1 && ((uintptr_t)src % 16));
+    if (p->tile.ph[1].w2) {      // 16-byte destination stores: every destination buffer 16-byte aligned
+        if ((uintptr_t)dst % 16) aligned = false;
+        for (int q = 1; q < (int)p->tile.nshards && !p->tile.pull; ++q)
+            if ((sa.off[q] * E) % 16) aligned = false;
+    }
     if (p->tile.pull && p->tile.ph[0].vec > 1) {
         // vectorised pull reads: 16-byte chunks of every shard, none straddling two
         if ((p->tile.shard_elems * E) % 16) aligned = false;

@@ -129,6 +129,16 @@ struct PhaseDesc {
     // split every line: ~2x L2 sector reads, tools/ldgsts_probe.cu)
     uint32_t swz;
     FastDiv spitch;                // divides an smem element offset by the pitch
+    // W with vec > 1 and w2 = 1 (congruent swizzled layout only): each
+    // position is a V x V block -- V smem vectors (V consecutive dim-0
+    // elements each) from V consecutive destination-innermost rows vrow
+    // elements apart, transposed in registers into V 16-byte stores of V
+    // consecutive destination elements, vstride apart.  Lanes walk the
+    // destination-innermost groups, so each store instruction writes 512
+    // contiguous bytes; the swizzle keys on the row group (swz = 1 + log2 V),
+    // so those lanes' smem vectors fall on distinct banks.
+    uint32_t w2;
+    uint32_t vrow;
 };
 
 struct TileParams {

@@ -71,6 +71,7 @@ struct Problem {
     bool no_shift = false; // disable shifted-run reads (VPG_NO_SHIFT)
     bool no_res = false;   // disable residue row strides for shifted runs (VPG_NO_RES)
     bool no_sw128 = false; // disable the 128-byte congruent layout (VPG_NO_SW128; bulk-read plans)
+    bool no_w2 = false;    // disable V x V register-transposed W blocks (VPG_NO_W2)
     bool no_bulk = false;  // TMA bulk source reads off (VPG_BULK=0, pull exchanges)
     bool force_bulk = false; // TMA bulk source reads wherever they apply (VPG_BULK=1)
     bool no_swz = true;    // shifted-run chunk swizzle is opt-in (VPG_SWZ=1)
@@ -326,6 +327,7 @@ struct VecChoice {
     int swz = 0;           // shifted-run mode: chunk swizzle (0 off, else 1 + row shift)
     bool rres = false;     // shifted-run mode with residue row strides (no per-element shift in W)
     bool sw128 = false;    // aligned runs: unpadded rows congruent to their source lines mod 128 B, chunk-swizzled
+    bool w2 = false;       // (sw128 only) W in V x V register-transposed blocks with 16-byte stores
 };
 
 // smem strides of the tile dims for a given pitch (source run dense, run
@@ -406,7 +408,7 @@ int64_t res_modulus(int E) {
 // R with vr > 1: the leading entry is grouped by vr.  W with vw > 1: dim 0
 // is grouped by vw (its V elements are one smem vector, stored separately).
 std::vector<PDimH> phase_dims(const Problem &Pb, const TileGeom &g, const int64_t *sstr,
-                              const int *slot_of_dim, bool write, int vec, int64_t hmask = 0) {
+                              const int *slot_of_dim, bool write, int vec, int64_t hmask = 0, bool w2 = false) {
     std::vector<PDimH> L;
     bool in_run[kMaxRank] = {false};
     for (int i = 0; i < g.nsrc; ++i) in_run[g.src_dims[i]] = true;
@@ -415,7 +417,9 @@ std::vector<PDimH> phase_dims(const Problem &Pb, const TileGeom &g, const int64_
         if (g.ext[k] == 0) continue;
         PDimH d{g.ext[k], write ? Pb.out_stride_of_dim[k] : Pb.in_stride[k], sstr[k], slot_of_dim[k], 1};
         if (write && hmask && !in_run[k]) d.hmul = Pb.in_stride[k] & hmask;
-        if (write && vec > 1 && k == 0) {
+        // W: dim 0 groups by V (one smem vector); with w2 the destination's
+        // innermost dim (first in W order) groups by V too (V rows per block)
+        if (write && vec > 1 && (k == 0 || (w2 && i == 0))) {
             d.e /= vec;
             d.g *= vec;
             d.s *= vec;
@@ -676,6 +680,21 @@ bool r_vectorizable(const Problem &Pb, const TileGeom &g, int V) {
     return true;
 }
 
+// W in V x V blocks: the destination-innermost dim sigma[0] is a tile dim
+// grouped by V, and every destination offset of a group start is a multiple
+// of V (16-byte stores; d[sigma[0]] % V == 0 makes all other destination
+// strides, the shard size included, multiples of V).
+bool w2_vectorizable(const Problem &Pb, const TileGeom &g, int V) {
+    const int k1 = Pb.sigma[0];
+    if (k1 == 0 || g.ext[k1] == 0 || g.ext[k1] % V || Pb.d[k1] % V) return false;
+    // the V rows of a block are smem rows (sigma[0] a run-index dim, the
+    // first in destination order: stride = pitch), so they share a swizzle group
+    for (int i = 0; i < g.nsrc; ++i)
+        if (g.src_dims[i] == k1) return false;
+    if (Pb.G >= 1 && (Pb.n / Pb.G) % V) return false;
+    return true;
+}
+
 bool w_vectorizable(const Problem &Pb, const TileGeom &g, int V) {
     if (V <= 1) return false;
     if (g.ext[0] == 0 || g.ext[0] % V) return false;
@@ -727,13 +746,22 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
     double u0 = make_phase(vc.rshift ? shift_r_dims(Pb, g, sstr, slot_of_dim, V)
                                      : phase_dims(Pb, g, sstr, slot_of_dim, false, vc.vr),
                            NT, tp.ph[0], tp.lim_split[0]);
-    double u1 = make_phase(phase_dims(Pb, g, sstr, slot_of_dim, true, vc.vw, hmask), NT, tp.ph[1], tp.lim_split[1]);
+    double u1 = make_phase(phase_dims(Pb, g, sstr, slot_of_dim, true, vc.vw, hmask, vc.w2), NT, tp.ph[1],
+                           tp.lim_split[1]);
+    if (vc.w2) {
+        tp.ph[1].w2 = 1;
+        tp.ph[1].vrow = (uint32_t)sstr[Pb.sigma[0]];    // == pitch (w2_vectorizable)
+    }
     tp.ph[0].rshift = vc.rshift ? (vc.rres ? 2u : 1u) : 0u;
     tp.hmask = (uint32_t)hmask;
     tp.rres = vc.rres ? (uint32_t)(M - 1) : 0u;
     if ((vc.swz && vc.rshift && vc.vw == 1 && !vc.bulk) || (vc.sw128 && !vc.bulk)) {
+        // congruent layout: XOR by row (W lanes walk rows), or by row group
+        // of V rows with w2 (W lanes walk V-row groups)
+        uint32_t lv = 0;
+        while ((1 << lv) < V) ++lv;
         for (int ph = 0; ph < 2; ++ph) {
-            tp.ph[ph].swz = vc.sw128 ? 1u : (uint32_t)vc.swz;
+            tp.ph[ph].swz = vc.sw128 ? (vc.w2 ? 1u + lv : 1u) : (uint32_t)vc.swz;
             tp.ph[ph].spitch = make_fastdiv(pitch);
         }
     }
@@ -870,6 +898,7 @@ double tile_cost(const Problem &Pb, const TileParams &tp) {
         // (odd 2-D transposes 0.70 -> 0.78 of copy; random-shape p10 +1-3%)
         const double kr = getenv("VPG_R_OP_COST") ? atof(getenv("VPG_R_OP_COST")) : 8.0;
         if (ph == 0) cost += ops * (kr + avg_w + (checked ? 2.0 : 0.0));
+        else if (d.w2) cost += ops * (V * avg_w + V + 1.0 + (checked ? 2.0 : 0.0));    // V LDS.128 + V STG.128
         else cost += ops * (avg_w + (V > 1 ? V : 1) + 1.0 + (checked ? 2.0 : 0.0)); // LDS + STGs
     }
     return cost;
@@ -902,20 +931,24 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
             // congruent rows (pitch = run, no padding), chunk swizzle against
             // the W bank conflicts; per-lane cp.async then requests each L2
             // sector once instead of ~twice
-            TileParams tp;
-            VecChoice vc;
-            vc.vr = op.vr;
-            vc.vw = op.vw;
-            vc.sw128 = true;
-            fill_tile_params(Pb, g, (uint32_t)g.Ls, NT, vc, tp);
-            double c = tile_cost(Pb, tp) * kSw128CostFactor;
-            if (getenv("VPG_DEBUG_PLAN"))
-                fprintf(stderr, "[plan] Ls %lld Ld %lld pitch %lld vr %d vw %d sw128 cost %.1f per-elem %.3f\n",
-                        (long long)g.Ls, (long long)g.Ld, (long long)g.Ls, vc.vr, vc.vw, c, c / (double)g.T);
-            if (best < 0 || c < best - 1e-9) {
-                best = c;
-                pitch_out = (uint32_t)g.Ls;
-                vc_out = vc;
+            for (int w2 = 0; w2 < 2; ++w2) {
+                if (w2 && !(op.vw > 1 && !Pb.no_w2 && w2_vectorizable(Pb, g, V))) continue;
+                TileParams tp;
+                VecChoice vc;
+                vc.vr = op.vr;
+                vc.vw = op.vw;
+                vc.sw128 = true;
+                vc.w2 = w2 != 0;
+                fill_tile_params(Pb, g, (uint32_t)g.Ls, NT, vc, tp);
+                double c = tile_cost(Pb, tp) * kSw128CostFactor;
+                if (getenv("VPG_DEBUG_PLAN"))
+                    fprintf(stderr, "[plan] Ls %lld Ld %lld pitch %lld vr %d vw %d sw128 w2 %d cost %.1f per-elem %.3f\n",
+                            (long long)g.Ls, (long long)g.Ld, (long long)g.Ls, vc.vr, vc.vw, w2, c, c / (double)g.T);
+                if (best < 0 || c < best - 1e-9) {
+                    best = c;
+                    pitch_out = (uint32_t)g.Ls;
+                    vc_out = vc;
+                }
             }
         }
         if (op.rshift && !Pb.no_swz) {
@@ -1184,11 +1217,11 @@ static void describe(vpg_plan *p) {
                 d.mask_full, d.mask_ragged);
         }
         if (t.ph[0].swz) put("smem chunk swizzle: row >> %u\n", t.ph[0].swz - 1);
-        put("vector elems: R %u%s, W %u\n", t.ph[0].vec,
+        put("vector elems: R %u%s, W %u%s\n", t.ph[0].vec,
             t.bulk ? " (TMA bulk copy per source run, producer warp)"
                    : (t.ph[0].rshift == 2 ? " (aligned supersets of misaligned runs, residue row strides)"
                                        : t.ph[0].rshift ? " (aligned supersets of misaligned runs)" : ""),
-            t.ph[1].vec);
+            t.ph[1].vec, t.ph[1].w2 ? " (VxV register-transposed blocks, 16-byte stores)" : "");
         put("lane utilisation (R*W): %.3f\n", p->tile_util);
         put("specialised (NVRTC) kernel: %s\n", p->jit ? "yes" : "no");
         put("tiles: %u, grid digits: %d\n", t.num_tiles, t.ngrid);
@@ -1254,6 +1287,7 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
     if (getenv("VPG_NO_SHIFT")) P.no_shift = true;
     if (getenv("VPG_NO_RES")) P.no_res = true;
     if (getenv("VPG_NO_SW128")) P.no_sw128 = true;
+    if (getenv("VPG_NO_W2")) P.no_w2 = true;
     // the chunk swizzle removes the W bank conflicts of shifted runs but costs
     // a divide and a few integer ops per element: measured 28.4 vs 20.5 us on
     // cfg3, 216 vs 247 us on an odd 8-byte 2-D transpose -- opt-in
@@ -1428,6 +1462,7 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         vs.vr = 1;
         vs.rshift = false;
         vs.bulk = false;
+        vs.w2 = false;      // 16-byte destination stores need an aligned dst too
         fill_tile_params(P, g, pitch, threads, vs, p->tile_unaligned);
         // the tile count must fit the 32-bit tile index
         double nt = 1.0;

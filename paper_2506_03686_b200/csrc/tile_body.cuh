@@ -330,6 +330,45 @@ __device__ __forceinline__ void tile_read(const PhaseDesc &d, const ThreadPart &
 // 16-byte smem vector of V consecutive dim-0 elements, stored to V
 // destinations d.vstride apart (each store instruction stays coalesced
 // across the warp's lanes).
+// W in V x V blocks (PhaseDesc::w2): V 16-byte smem vectors from V
+// consecutive destination-innermost rows (one swizzle group, so one slot
+// computation), transposed in registers into V 16-byte stores.
+template <typename W>
+__device__ __forceinline__ void w2_block(W *gp, const W *sp, uint32_t vrow, int64_t vs) {
+    constexpr int V = 16 / (int)sizeof(W);
+    uint4 v[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) v[i] = *reinterpret_cast<const uint4 *>(sp + i * vrow);
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        alignas(16) W o[V];
+#pragma unroll
+        for (int i = 0; i < V; ++i) o[i] = reinterpret_cast<const W *>(&v[i])[j];
+        st_out(reinterpret_cast<uint4 *>(gp + j * vs), *reinterpret_cast<const uint4 *>(o));
+    }
+}
+
+template <typename W>
+__device__ __forceinline__ void tile_write_w2(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
+                                              W *__restrict__ gdst, const W *buf, uint32_t mask, const Lim lim) {
+    const uint32_t o0 = d.ngroups == 1 ? 0u : t.grp;
+    VPG_UNROLL
+    for (uint32_t o = o0; o < d.n_outer; o += d.ngroups) {
+        const OuterEntry e = outer_entry(d, smem, o);
+        W *gp = gdst + (t.g + e.g);
+        const uint32_t sb = t.s + e.s;
+        uint32_t c0 = t.c0 + e.c0, c1 = t.c1 + e.c1, c2 = t.c2;
+        VPG_UNROLL
+        for (uint32_t i = 0; i < d.n_in; ++i) {
+            if (mask == 0 || slot_ok(mask, c0, c1, c2, lim))
+                w2_block<W>(gp + (int64_t)i * d.g_in, sslot(d, buf, sb + i * d.s_in), d.vrow, d.vstride);
+            c0 += d.c_in[0];
+            c1 += d.c_in[1];
+            c2 += d.c_in[2];
+        }
+    }
+}
+
 template <typename W, bool VEC>
 __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
                                                 W *__restrict__ gdst, const W *buf, uint32_t mask,
@@ -423,6 +462,10 @@ __device__ __forceinline__ void tile_write(const PhaseDesc &d, const ThreadPart 
                                            const Lim lim, uint32_t hb, uint32_t hmask) {
     if (!t.active) return;
     if constexpr (sizeof(W) == 4 || sizeof(W) == 8) {
+        if (d.w2) {
+            tile_write_w2<W>(d, t, smem, gdst, buf, mask, lim);
+            return;
+        }
         if (d.vec > 1) {
             tile_write_impl<W, true>(d, t, smem, gdst, buf, mask, lim, 0, 0);
             return;

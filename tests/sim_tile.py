@@ -41,7 +41,7 @@ class PhaseDesc(ctypes.Structure):
                 ("nout_dims", ctypes.c_int32), ("out", PhaseDim * MAXPD), ("vec", ctypes.c_uint32),
                 ("rshift", ctypes.c_uint32), ("h_in", ctypes.c_uint32), ("vstride", ctypes.c_int64),
                 ("mask_full", ctypes.c_uint32), ("mask_ragged", ctypes.c_uint32), ("off_tab", ctypes.c_uint32),
-                ("swz", ctypes.c_uint32), ("spitch", FastDiv)]
+                ("swz", ctypes.c_uint32), ("spitch", FastDiv), ("w2", ctypes.c_uint32), ("vrow", ctypes.c_uint32)]
 
 
 class GridDigit(ctypes.Structure):
@@ -272,6 +272,27 @@ def simulate(program, src_words: np.ndarray, threads: int | None = None, shard_o
                                     smem[spx + j] = src_words[gabs + j]
                                     smem_valid[spx + j] = True
                         else:
+                            if d.w2:
+                                # V x V block: V smem vectors from rows vrow apart (same
+                                # swizzle row group) -> V 16-byte stores of V consecutive
+                                # destination elements
+                                gabs = db + gp
+                                spx = _swizzle(d, sp + tbase, 16 // E)
+                                if (spx % V).any() or (d.vrow % V) or (gabs % V).any() or (d.vstride % V):
+                                    raise SimError("W 2-D block access misaligned")
+                                for ii in range(V):
+                                    if (_swizzle(d, sp + tbase + ii * d.vrow, 16 // E) != spx + ii * d.vrow).any():
+                                        raise SimError("W 2-D block rows do not share a swizzle group")
+                                    for j in range(V):
+                                        so = spx + ii * d.vrow + j
+                                        _chk(so, alloc, "W2 smem")
+                                        dd = gabs + j * d.vstride + ii
+                                        _chk(dd, dbound, "W2 global")
+                                        if not smem_valid[so].all():
+                                            raise SimError(f"W reads smem never written (tile {t})")
+                                        dst[dd] = smem[so]
+                                        written[dd] += 1
+                                continue
                             hh = (sb + th[sel][ok] + eh[0] + i * d.h_in) & tp.hmask if tp.hmask else 0
                             spx = _swizzle(d, sp + hh + tbase, 16 // E if E <= 16 else 1)
                             gabs = db + gp

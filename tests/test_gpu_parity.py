@@ -333,3 +333,46 @@ def test_residue_row_strides(cuda, jit):
             break
     assert done >= 8
 
+
+
+@pytest.mark.parametrize("jit", [False, True])
+def test_w2_blocks(cuda, jit):
+    """W in V x V register-transposed blocks with 16-byte stores (congruent
+    swizzled layout): bit-exact on shapes where the planner picks it, 4- and
+    8-byte words, specialised and ahead-of-time kernels, ragged tiles; a
+    destination off 16-byte alignment takes the scalar-store variant."""
+    import torch
+
+    import paper_2506_03686_b200 as vp
+    from paper_2506_03686_b200.api import execute_device
+    from tests.sim_tile import tile_params
+
+    rng = np.random.default_rng(41)
+    done = 0
+    shapes = [((64, 256), (1, 0)), ((4096, 4096), (1, 0)), ((32, 64, 56, 56), (0, 2, 3, 1)), ((96, 128), (1, 0))]
+    for _ in range(300):
+        r = int(rng.integers(2, 5))
+        shapes.append((tuple(int(x) for x in rng.choice([4, 8, 12, 16, 32, 64, 128, 192], size=r)),
+                       tuple(int(a) for a in rng.permutation(r))))
+    for shape, axes in shapes:
+        n = int(np.prod(shape))
+        if n > (1 << 24):
+            continue
+        E = 8 if (done % 3 == 2) else 4
+        prog = vp.build_program(vp.TensorLayout.from_shape(shape, E), vp.from_numpy_convention(axes),
+                                force="tile", jit=jit)
+        if tile_params(prog).ph[1].w2 == 0:
+            continue
+        x = torch.randint(-2**31, 2**31 - 1, (n * E // 4,), dtype=torch.int32, device="cuda")
+        xv = x.view(torch.int32 if E == 4 else torch.int64).view(shape)
+        want = xv.permute(axes).reshape(-1)
+        y = execute_device(prog, x.view(torch.uint8))
+        assert torch.equal(y.view(xv.dtype).view(-1), want), (shape, axes, E)
+        big = torch.empty(n * E + E, dtype=torch.uint8, device="cuda")
+        out = big[E:]                      # destination off 16-byte alignment by one element
+        execute_device(prog, x.view(torch.uint8), out=out)
+        assert torch.equal(out.view(xv.dtype), want), (shape, axes, E, "misaligned dst")
+        done += 1
+        if done >= (8 if jit else 24):
+            break
+    assert done >= 6

@@ -210,3 +210,56 @@ def test_sim_residue_rows():
         if n_res >= 40:
             break
     assert n_res >= 20
+
+
+def test_sim_w2_blocks():
+    """W in V x V register-transposed blocks on the congruent swizzled
+    layout (16-byte smem loads and 16-byte destination stores): bit-exact
+    replay on shapes where the planner picks it, 4- and 8-byte words, ragged
+    tiles included."""
+    vp.program_cache_clear()
+    rng = np.random.default_rng(31)
+    n_w2 = 0
+    shapes = [((64, 256), (1, 0)), ((96, 128), (1, 0)), ((8, 64, 40), (0, 2, 1)), ((3, 32, 64, 8), (1, 3, 2, 0))]
+    for _ in range(400):
+        r = int(rng.integers(2, 5))
+        shapes.append((tuple(int(x) for x in rng.choice([4, 8, 12, 16, 32, 64, 128], size=r)),
+                       tuple(int(a) for a in rng.permutation(r))))
+    for shape, axes in shapes:
+        if np.prod(shape) > 300000:
+            continue
+        for E in (4, 8):
+            prog = vp.build_program(vp.TensorLayout.from_shape(shape, E), vp.from_numpy_convention(axes), force="tile")
+            if tile_params(prog).ph[1].w2 == 0:
+                continue
+            n = prog.num_elements
+            words = rng.integers(0, 2**63, size=n, dtype=np.uint64)
+            words = words.view(np.uint32)[:n].copy() if E == 4 else words
+            dims, sigma = oracle.from_numpy_axes(shape, axes)
+            assert np.array_equal(simulate(prog, words), oracle.naive_permute_c(words, dims, sigma)), (shape, axes, E)
+            n_w2 += 1
+        if n_w2 >= 25:
+            break
+    assert n_w2 >= 10, n_w2
+
+
+def test_sim_golden_cases_with_swizzled_layouts():
+    """Every reference golden case (up to 70k elements) whose plan uses the
+    congruent swizzled layout or V x V blocks replays to the reference's
+    recorded digest."""
+    from tests.golden.pattern import golden_pattern
+    from tests.helpers import golden, sha256
+
+    ran = 0
+    for c in golden()["cases"]:
+        if c["n"] > 70000:
+            continue
+        prog = vp.build_program(vp.TensorLayout(tuple(c["dims"]), c["elem"]), vp.PermutationMap(tuple(c["sigma"])))
+        if prog.kernel != "tile":
+            continue
+        t = tile_params(prog)
+        if not (t.ph[1].w2 or t.ph[0].swz):
+            continue
+        assert sha256(simulate(prog, golden_pattern(c["n"], c["elem"]))) == c["sha256"], c["name"]
+        ran += 1
+    assert ran >= 10
