@@ -215,7 +215,7 @@ def test_dense_base_of_permuted_views():
 
 def test_baseline_layout_choices():
     """The layout each BASELINE config is planned with (kernels):
-    cfg1/cfg2 the 128-byte congruent swizzled rows, cfg3 residue row strides
+    cfg1/cfg2 the 128-byte congruent swizzled rows with V x V W blocks, cfg3 residue row strides
     for its misaligned runs, cfg5 TMA bulk reads of its 2 KiB runs, and the
     cfg5 pull exchange at G = 8 keeping the 256 x 128 tile."""
     from paper_2506_03686_b200.sharded import _programs, fused_method
@@ -228,8 +228,10 @@ def test_baseline_layout_choices():
 
     for k in ("cfg1", "cfg2"):
         t, p = tp(k)
-        assert t.ph[0].swz == 1 and t.ph[1].swz == 1 and t.pitch == t.Ls and not t.bulk, k
-        assert "smem chunk swizzle" in p.text
+        # congruent rows, V x V W blocks, swizzle keyed on the 4-row group
+        assert t.ph[0].swz == 3 and t.ph[1].swz == 3 and t.pitch == t.Ls and not t.bulk, k
+        assert t.ph[1].w2 == 1 and t.ph[1].vrow == t.pitch, k
+        assert "smem chunk swizzle" in p.text and "16-byte stores" in p.text
     t, p = tp("cfg3")
     assert t.ph[0].rshift == 2 and t.rres == 3 and t.hmask == 0
     t, p = tp("cfg5")
