@@ -1449,13 +1449,11 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
                     ((g.Ls / g.ext[g.a_part]) * (P.d[g.a_part] % g.ext[g.a_part]) * E) % 16 == 0) &&
                    g.n_runidx <= kMaxPhaseDims;
         };
-        if (vc.sw128 && bulk_for(vc)) {
-            // bulk copies request each sector once anyway and do not swizzle:
-            // re-plan the padded layout for them
-            P.no_sw128 = true;
-            choose_pitch_vec(P, g, threads, pitch, vc);
-        }
-        vc.bulk = bulk_for(vc);
+        // the congruent layout (1x L2 sectors with per-lane cp.async, V x V W
+        // blocks) beats bulk reads into padded rows where it applies (cfg5:
+        // 690 vs 708 us flushed, 703 vs 729 us steady); bulk covers the long
+        // runs it cannot take (not a power of two, or not 128-byte aligned)
+        vc.bulk = !vc.sw128 && bulk_for(vc);
         p->tile_util = fill_tile_params(P, g, pitch, threads, vc, p->tile);
         // variant without 16-byte source reads, for misaligned base pointers
         VecChoice vs = vc;

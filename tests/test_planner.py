@@ -215,8 +215,9 @@ def test_dense_base_of_permuted_views():
 
 def test_baseline_layout_choices():
     """The layout each BASELINE config is planned with (kernels):
-    cfg1/cfg2 the 128-byte congruent swizzled rows with V x V W blocks, cfg3 residue row strides
-    for its misaligned runs, cfg5 TMA bulk reads of its 2 KiB runs, and the
+    cfg1/cfg2/cfg5 the 128-byte congruent swizzled rows with V x V W blocks,
+    cfg3 residue row strides for its misaligned runs, TMA bulk reads for long
+    runs that cannot take the congruent layout, and the
     cfg5 pull exchange at G = 8 keeping the 256 x 128 tile."""
     from paper_2506_03686_b200.sharded import _programs, fused_method
     from paper_2506_03686_b200.workloads import CONFIGS
@@ -225,6 +226,10 @@ def test_baseline_layout_choices():
     def tp(k):
         w = CONFIGS[k]
         return tile_params(_plan(w.shape, w.axes, w.elem_bytes)), _plan(w.shape, w.axes, w.elem_bytes)
+
+    def tp_shape(shape, axes, e):
+        p = _plan(shape, axes, e, force="tile")
+        return tile_params(p), p
 
     for k in ("cfg1", "cfg2"):
         t, p = tp(k)
@@ -235,6 +240,10 @@ def test_baseline_layout_choices():
     t, p = tp("cfg3")
     assert t.ph[0].rshift == 2 and t.rres == 3 and t.hmask == 0
     t, p = tp("cfg5")
+    # 2 KiB power-of-two runs: congruent layout + V x V blocks (bulk reads
+    # remain for long runs that cannot take it)
+    assert t.bulk == 0 and t.ph[1].w2 == 1 and t.ph[0].swz == 2
+    t, p = tp_shape((2, 3, 1000, 500), (0, 2, 1, 3), 8)        # 4000-byte runs: not a power of two
     assert t.bulk == 1 and "TMA bulk copy" in p.text
     w = CONFIGS["cfg5"]
     assert fused_method(w.shape, w.axes, 8, 2) == "push"
