@@ -707,9 +707,16 @@ bool w_vectorizable(const Problem &Pb, const TileGeom &g, int V) {
 // number of 128-byte lines and a power of two (cheap swizzle divide), and
 // every stride that moves a run start (run-index dims, grid digits, the
 // partial source dim's tile step, the shard bias) keeps 128-byte alignment.
+// Swizzled unpadded rows need only runs of a power of two of whole 128-byte
+// lines (sw128_layout_ok); the congruence with the source lines (the L2
+// request saving) needs the strides too (sw128_possible).
+bool sw128_layout_ok(const Problem &Pb, const TileGeom &g) {
+    return (g.Ls * Pb.E) % 128 == 0 && (g.Ls & (g.Ls - 1)) == 0;
+}
+
 bool sw128_possible(const Problem &Pb, const TileGeom &g) {
     const int64_t E = Pb.E;
-    if ((g.Ls * E) % 128 || (g.Ls & (g.Ls - 1))) return false;
+    if (!sw128_layout_ok(Pb, g)) return false;
     if (Pb.G >= 1 && ((Pb.n / Pb.G) * E) % 128) return false;   // shard bases keep the congruence
     bool in_run[kMaxRank] = {false};
     for (int i = 0; i < g.nsrc; ++i) in_run[g.src_dims[i]] = true;
@@ -925,7 +932,10 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
             opts.push_back({vr, vw, false});
         }
     if (rs) opts.push_back({V, 1, true});
-    const bool s128 = rv && !Pb.no_sw128 && sw128_possible(Pb, g);
+    // swizzled unpadded rows: wherever the layout fits; the L2 saving (cost
+    // factor) only where the rows are congruent to their source lines
+    const bool s128 = rv && !Pb.no_sw128 && sw128_layout_ok(Pb, g);
+    const double s128_factor = sw128_possible(Pb, g) ? kSw128CostFactor : 1.0;
     for (const Opt &op : opts) {
         if (s128 && op.vr > 1 && !op.rshift && (int64_t)(g.T / g.Ls) * g.Ls * Pb.E <= Pb.budget + 8192) {
             // congruent rows (pitch = run, no padding), chunk swizzle against
@@ -940,7 +950,7 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
                 vc.sw128 = true;
                 vc.w2 = w2 != 0;
                 fill_tile_params(Pb, g, (uint32_t)g.Ls, NT, vc, tp);
-                double c = tile_cost(Pb, tp) * kSw128CostFactor;
+                double c = tile_cost(Pb, tp) * s128_factor;
                 if (getenv("VPG_DEBUG_PLAN"))
                     fprintf(stderr, "[plan] Ls %lld Ld %lld pitch %lld vr %d vw %d sw128 w2 %d cost %.1f per-elem %.3f\n",
                             (long long)g.Ls, (long long)g.Ld, (long long)g.Ls, vc.vr, vc.vw, w2, c, c / (double)g.T);
