@@ -78,6 +78,7 @@ inline uint32_t host_fastdiv(uint32_t n, FastDiv f) {
 //                   the split dim), unrolled;
 //   outer dims   -- the rest, through a per-CTA table in shared memory.
 // Threads beyond one thread part form G groups that share the outer loop.
+constexpr unsigned kSwzAddr = 16; // PhaseDesc::swz: chunk ^= 128-byte block index (row-layout independent)
 constexpr int kNumSlots = 3;      // checked coordinates: 0 = dim a, 1 = dim c, 2 = split padding
 constexpr int kMaxPhaseDims = 12; // thread-part / outer dims per phase
 constexpr unsigned long long kOuterEntryBytes = 24;  // sizeof(OuterEntry) in tile_body.cuh
@@ -127,7 +128,7 @@ struct PhaseDesc {
     // same offset modulo 128 bytes as their source lines, so per-lane
     // cp.async requests each L2 sector once (a padded row makes the LDGSTS
     // split every line: ~2x L2 sector reads, tools/ldgsts_probe.cu)
-    uint32_t swz;
+    uint32_t swz;                  // (kSwzAddr: address swizzle, see swizzle() in tile_body.cuh)
     FastDiv spitch;                // divides an smem element offset by the pitch
     // W with vec > 1 and w2 = 1 (congruent swizzled layout only): each
     // position is a V x V block -- V smem vectors (V consecutive dim-0

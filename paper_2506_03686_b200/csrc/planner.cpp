@@ -72,6 +72,7 @@ struct Problem {
     bool no_res = false;   // disable residue row strides for shifted runs (VPG_NO_RES)
     bool no_sw128 = false; // disable the 128-byte congruent layout (VPG_NO_SW128; bulk-read plans)
     bool no_w2 = false;    // disable V x V register-transposed W blocks (VPG_NO_W2)
+    bool no_swz_addr = false; // 128-byte residue layouts without the address swizzle (VPG_NO_SWZ_ADDR)
     bool no_bulk = false;  // TMA bulk source reads off (VPG_BULK=0, pull exchanges)
     bool force_bulk = false; // TMA bulk source reads wherever they apply (VPG_BULK=1)
     bool no_swz = true;    // shifted-run chunk swizzle is opt-in (VPG_SWZ=1)
@@ -393,13 +394,15 @@ int64_t tile_sstrides_res(const Problem &Pb, const TileGeom &g, uint32_t pitch, 
     return (last + (M - 1) + nck * V + V - 1) / V * V;
 }
 
-// Residue modulus (elements) of the residue row strides: 16 bytes (chunk
-// alignment).  VPG_RES_MOD=128 also puts each run at its source line's
-// offset modulo 128 B: cfg3's L2 read sectors drop 2.49M -> 1.66M (ncu), but
-// the longer row strides raise its W bank conflicts 125k -> 539k and the
-// time is unchanged (16.6-16.9 vs 16.8-16.9 us steady), so it stays opt-in.
+// Residue modulus (elements) of the residue row strides: 128 bytes, so each
+// run also sits at its source line's offset modulo 128 B and the per-lane
+// cp.async requests each L2 sector about once (cfg3: 2.49M -> 1.66M L2 read
+// sectors, ncu).  Those plans use the address swizzle (kSwzAddr) and 128-byte
+// aligned stage buffers: cfg3 18.4 vs 20.5 us flushed, 15.0 vs 16.7 us steady
+// (VPG_RES_MOD=16 restores the chunk-only congruence; with 128 B but no
+// swizzle, VPG_NO_SWZ_ADDR=1, the time does not improve).
 int64_t res_modulus(int E) {
-    static const int64_t bytes = getenv("VPG_RES_MOD") ? std::max(16L, atol(getenv("VPG_RES_MOD"))) : 16;
+    static const int64_t bytes = getenv("VPG_RES_MOD") ? std::max(16L, atol(getenv("VPG_RES_MOD"))) : 128;
     return std::max<int64_t>(16 / E, bytes / E);
 }
 
@@ -632,6 +635,11 @@ double make_phase(const std::vector<PDimH> &L, int NT, PhaseDesc &pd, uint32_t &
 // first outer entry (simulation of the kernel's mapping, for the bank model).
 uint32_t host_swizzle(const PhaseDesc &pd, uint32_t s, int V) {
     if (!pd.swz) return s;
+    if (pd.swz == kSwzAddr) {
+        uint32_t lv = 0;
+        while ((1 << lv) < V) ++lv;
+        return s ^ (((s >> (lv + 3)) & 7u) << lv);
+    }
     const uint32_t P = pd.spitch.d, r = s / P, c = s - r * P, f = (r >> (pd.swz - 1)) & 7u;
     return r * P + ((((c / V) ^ f) * V) | (c % V));
 }
@@ -762,6 +770,8 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
     tp.ph[0].rshift = vc.rshift ? (vc.rres ? 2u : 1u) : 0u;
     tp.hmask = (uint32_t)hmask;
     tp.rres = vc.rres ? (uint32_t)(M - 1) : 0u;
+    if (vc.rres && M * Pb.E >= 128 && !Pb.no_swz_addr)
+        for (int ph = 0; ph < 2; ++ph) tp.ph[ph].swz = kSwzAddr;
     if ((vc.swz && vc.rshift && vc.vw == 1 && !vc.bulk) || (vc.sw128 && !vc.bulk)) {
         // congruent layout: XOR by row (W lanes walk rows), or by row group
         // of V rows with w2 (W lanes walk V-row groups)
@@ -862,6 +872,11 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
     tp.ph[0].off_tab = take(kOuterEntryBytes * tp.ph[0].n_outer, 16);
     tp.ph[1].off_tab = take(kOuterEntryBytes * tp.ph[1].n_outer, 16);
     uint64_t buf_bytes = ((uint64_t)tp.tile_elems_alloc * Pb.E + 15) / 16 * 16;
+    if (vc.rres && M * Pb.E >= 128) {
+        // every stage buffer 128-byte aligned (the residue congruence is mod 128 B)
+        buf_bytes = (buf_bytes + 127) / 128 * 128;
+        tp.tile_elems_alloc = (uint32_t)(buf_bytes / Pb.E);
+    }
     // pipeline depth: as many stages as fit the per-CTA smem target (two
     // CTAs per SM), at least 2, at most 8; 1- and 2-byte words use 1.
     uint32_t stages = 1;
@@ -1001,7 +1016,8 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
                 vc.rres = true;
                 fill_tile_params(Pb, g, pitch, NT, vc, tp);
                 // no per-element shift arithmetic in W: cheaper per element
-                double c = tile_cost(Pb, tp) * kResidueCostFactor;
+                double c = tile_cost(Pb, tp) * kResidueCostFactor *
+                           (res_modulus(Pb.E) * Pb.E >= 128 ? kSw128CostFactor : 1.0);   // 128-byte congruence
                 if (getenv("VPG_DEBUG_PLAN"))
                     fprintf(stderr, "[plan] Ls %lld Ld %lld pitch %u residue cost %.1f per-elem %.3f\n",
                             (long long)g.Ls, (long long)g.Ld, pitch, c, c / (double)g.T);
@@ -1298,6 +1314,7 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
     if (getenv("VPG_NO_RES")) P.no_res = true;
     if (getenv("VPG_NO_SW128")) P.no_sw128 = true;
     if (getenv("VPG_NO_W2")) P.no_w2 = true;
+    if (getenv("VPG_NO_SWZ_ADDR")) P.no_swz_addr = true;
     // the chunk swizzle removes the W bank conflicts of shifted runs but costs
     // a divide and a few integer ops per element: measured 28.4 vs 20.5 us on
     // cfg3, 216 vs 247 us on an odd 8-byte 2-D transpose -- opt-in

@@ -158,14 +158,28 @@ __device__ __forceinline__ uint32_t swizzle(const PhaseDesc &d, uint32_t s) {
     return r * d.spitch.d + ((((c / V) ^ f) * V) | (c % V));
 }
 
-// Shared-memory slot of logical element offset s: plain, or chunk-swizzled
-// (d.swz: 16-byte chunks XOR-permuted by row inside each 128-byte block).
+// Address swizzle (PhaseDesc::swz == kSwzAddr): the 16-byte chunk index
+// inside each 128-byte block of shared memory XOR the block index (mod 8).
+// It acts on the address itself (shared-window addresses keep their low
+// bits in generic form; stage buffers are 128-byte aligned), so it needs no
+// row structure: the residue layouts use it.
+template <typename W>
+__device__ __forceinline__ W *swz_addr(W *p) {
+    const uintptr_t a = (uintptr_t)p;
+    return reinterpret_cast<W *>(a ^ (((a >> 7) & 7u) << 4));
+}
+
+// Shared-memory slot of logical element offset s: plain, row-chunk-swizzled
+// (d.swz: 16-byte chunks XOR-permuted by row inside each 128-byte block) or
+// address-swizzled (kSwzAddr).
 template <typename W>
 __device__ __forceinline__ W *sslot(const PhaseDesc &d, W *buf, uint32_t s) {
+    if (d.swz == kSwzAddr) return swz_addr(buf + s);
     return d.swz ? buf + swizzle<16 / (int)sizeof(W)>(d, s) : buf + s;
 }
 template <typename W>
 __device__ __forceinline__ const W *sslot(const PhaseDesc &d, const W *buf, uint32_t s) {
+    if (d.swz == kSwzAddr) return swz_addr(buf + s);
     return d.swz ? buf + swizzle<16 / (int)sizeof(W)>(d, s) : buf + s;
 }
 
@@ -289,6 +303,7 @@ __device__ __forceinline__ void tile_read_shift(const PhaseDesc &d, const Thread
                 // modulo 16 bytes; the chunk goes to its aligned-down slot
                 W *sd = d.rshift == 2 ? reinterpret_cast<W *>((uintptr_t)sp & ~(uintptr_t)15)
                         : (d.swz ? buf + swizzle<V>(d, (uint32_t)(sp - buf)) : sp);
+                if (d.swz == kSwzAddr) sd = swz_addr(reinterpret_cast<W *>((uintptr_t)sp & ~(uintptr_t)15));
                 if (ga + V <= gend) {
                     cp_async<16>(sd, ga);
                 } else {
@@ -407,7 +422,7 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         const uint32_t so = (uint32_t)(sp - buf) + u * s_in + ((hh + u * h_in) & hmask);
-                        v[u] = buf[d.swz ? swizzle<16 / (int)sizeof(W)>(d, so) : so];
+                        v[u] = *sslot(d, buf, so);
                     }
 #pragma unroll
                     for (int u = 0; u < U; ++u) st_out(gp + u * g_in, v[u]);
@@ -424,7 +439,7 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
                     for (int j = 0; j < V; ++j) st_out(gp + j * vs, w[j]);
                 } else {
                     const uint32_t so = (uint32_t)(sp - buf) + (hh & hmask);
-                    *gp = buf[d.swz ? swizzle<16 / (int)sizeof(W)>(d, so) : so];
+                    *gp = *sslot(d, buf, so);
                 }
                 gp += g_in;
                 sp += s_in;
@@ -442,7 +457,7 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
                         for (int j = 0; j < V; ++j) st_out(gp + j * vs, w[j]);
                     } else {
                         const uint32_t so = (uint32_t)(sp - buf) + (hh & hmask);
-                        *gp = buf[d.swz ? swizzle<16 / (int)sizeof(W)>(d, so) : so];
+                        *gp = *sslot(d, buf, so);
                     }
                 }
                 gp += g_in;
@@ -560,6 +575,7 @@ __device__ __forceinline__ void tile_read_pull(const TileParams &p, const ShardA
                 if constexpr (ASYNC && sizeof(W) < 16) {
                     if (d.rshift) {
                         W *sd = d.rshift == 2 ? reinterpret_cast<W *>((uintptr_t)(buf + so) & ~(uintptr_t)15) : buf + so;
+                        if (d.swz == kSwzAddr) sd = swz_addr(sd);
                         cp_async<16>(sd, pull_ptr(p, sa, src, go & ~(int64_t)(V - 1)));
                     } else if (d.vec > 1) {
                         cp_async<16>(sp, pull_ptr(p, sa, src, go));

@@ -237,7 +237,7 @@ def simulate(program, src_words: np.ndarray, threads: int | None = None, shard_o
                                     raise SimError("pull: 16-byte chunk straddles two input shards")
                             if d.rshift:
                                 ga = gabs - (gabs % V)
-                                if d.swz and (sp % V).any():
+                                if d.swz and d.rshift == 1 and (sp % V).any():
                                     raise SimError("swizzled R chunk not chunk-aligned")
                                 if d.rshift == 2:
                                     spl = sp + tbase
@@ -247,6 +247,8 @@ def simulate(program, src_words: np.ndarray, threads: int | None = None, shard_o
                                     M = tp.rres + 1          # residue modulus (elements)
                                     if ((spl - gabs) % M).any():
                                         raise SimError("residue mode: smem and global offsets differ mod the residue modulus")
+                                    if d.swz == 16:          # address swizzle of the aligned chunk
+                                        sd = _swizzle(d, sd, V)
                                 else:
                                     sd = _swizzle(d, sp, V)
                                 for j in range(V):
@@ -338,6 +340,9 @@ def _swizzle(d, s, V):
     """Chunk swizzle of smem element offsets (tile_body.cuh swizzle<V>)."""
     if not d.swz:
         return s
+    if d.swz == 16:                       # kSwzAddr: chunk ^= 128-byte block index
+        lv = {1: 0, 2: 1, 4: 2, 8: 3, 16: 4}[V]
+        return s ^ (((s >> (lv + 3)) & 7) << lv)
     P = d.spitch.d
     r = s // P
     c = s - r * P
