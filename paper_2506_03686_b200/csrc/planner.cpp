@@ -1251,7 +1251,10 @@ static void describe(vpg_plan *p) {
         put("lane utilisation (R*W): %.3f\n", p->tile_util);
         put("specialised (NVRTC) kernel: %s\n", p->jit ? "yes" : "no");
         put("tiles: %u, grid digits: %d\n", t.num_tiles, t.ngrid);
-        if (p->shards > 0)
+        if (p->shards > 0 && t.pull)
+            put("sharded exchange (pull): output shard %d of %d, tiles [%u, %u), reads from %d input shards\n",
+                p->shard_index, p->shards, t.tile_begin, t.tile_begin + t.num_tiles, p->shards);
+        else if (p->shards > 0)
             put("sharded exchange: shard %d of %d, tiles [%u, %u), stores into %d output shards\n",
                 p->shard_index, p->shards, t.tile_begin, t.tile_begin + t.num_tiles, p->shards);
     } else if (p->kernel_class == VPG_KERNEL_ROWS) {
