@@ -369,7 +369,10 @@ def bench_one_gpu(args, torch, cfg, with_e2e, peak):
 
         prog = autotune(lay, pm, src=xd, dst=yd)
     res = {"config": cfg, "kernel": prog.kernel,
-           "tile": [prog.metadata["src_run"], prog.metadata["dst_run"]] if prog.kernel == "tile" else None}
+           "tile": [prog.metadata["src_run"], prog.metadata["dst_run"]] if prog.kernel == "tile" else None,
+           # the plan's layout choices (vpg_plan_describe lines)
+           "plan": [ln for ln in prog.text.splitlines()
+                    if ln.startswith(("vector elems", "smem chunk swizzle", "smem pitch", "specialised"))]}
     stream = torch.cuda.current_stream(dev)
     flush = args._flusher
     launch = lambda: execute_device(prog, xd, out=yd, stream=stream)  # noqa: E731
@@ -750,7 +753,7 @@ def main(argv=None):
             r = bench_one_gpu(args, torch, k, False, peak)
             extra[k] = {"gbs": round(r["gbs"], 1), "frac_of_hbm": round(r["frac_of_hbm"], 4),
                         "us_per_launch": round(r["ms_per_launch"] * 1e3, 2), "kernel": r["kernel"],
-                        "tile_src_dst_run": r["tile"],
+                        "tile_src_dst_run": r["tile"], "plan": r["plan"],
                         "parity_sampled": r["parity_sampled"],
                         "torch_permute_copy_gbs": None if r["torch_gbs"] is None else round(r["torch_gbs"], 1),
                         "same_run_copy_gbs": round(r["copy_gbs"], 1),
@@ -759,7 +762,7 @@ def main(argv=None):
     extra[args.config] = {"gbs": round(main_res["gbs"], 1), "frac_of_hbm": round(main_res["frac_of_hbm"], 4),
                           "us_per_launch": round(main_res["ms_per_launch"] * 1e3, 2),
                           "kernel": main_res["kernel"], "parity_sampled": main_res["parity_sampled"],
-                          "tile_src_dst_run": main_res["tile"],
+                          "tile_src_dst_run": main_res["tile"], "plan": main_res["plan"],
                           "torch_permute_copy_gbs": None if main_res["torch_gbs"] is None
                           else round(main_res["torch_gbs"], 1),
                           "same_run_copy_gbs": round(main_res["copy_gbs"], 1),
