@@ -372,7 +372,8 @@ def bench_one_gpu(args, torch, cfg, with_e2e, peak):
            "tile": [prog.metadata["src_run"], prog.metadata["dst_run"]] if prog.kernel == "tile" else None,
            # the plan's layout choices (vpg_plan_describe lines)
            "plan": [ln for ln in prog.text.splitlines()
-                    if ln.startswith(("vector elems", "smem chunk swizzle", "smem pitch", "specialised"))]}
+                    if ln.startswith(("vector elems", "smem chunk swizzle", "smem address swizzle", "smem pitch",
+                                      "specialised", "rows"))]}
     stream = torch.cuda.current_stream(dev)
     flush = args._flusher
     launch = lambda: execute_device(prog, xd, out=yd, stream=stream)  # noqa: E731

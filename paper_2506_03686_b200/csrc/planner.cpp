@@ -1242,7 +1242,8 @@ static void describe(vpg_plan *p) {
                 ph ? "W" : "R", d.nthr, d.ngroups, d.nthr_dims, d.n_in, d.n_outer, d.nout_dims,
                 d.mask_full, d.mask_ragged);
         }
-        if (t.ph[0].swz) put("smem chunk swizzle: row >> %u\n", t.ph[0].swz - 1);
+        if (t.ph[0].swz == kSwzAddr) put("smem address swizzle: 16-byte chunk ^= 128-byte block index\n");
+        else if (t.ph[0].swz) put("smem chunk swizzle: row >> %u\n", t.ph[0].swz - 1);
         put("vector elems: R %u%s, W %u%s\n", t.ph[0].vec,
             t.bulk ? " (TMA bulk copy per source run, producer warp)"
                    : (t.ph[0].rshift == 2 ? " (aligned supersets of misaligned runs, residue row strides)"
@@ -1260,6 +1261,8 @@ static void describe(vpg_plan *p) {
     } else if (p->kernel_class == VPG_KERNEL_ROWS) {
         put("rows: %u x %lld elements, vector %u elements, %u threads/row\n", p->rows.nrows,
             (long long)p->rows.row_len, p->rows.vec, 1u << p->rows.tpr_log2);
+        if (p->rows.row_len * p->elem_bytes >= 2560 && (p->rows.row_len * p->elem_bytes) % 16 == 0)
+            put("rows vector elems: TMA bulk pipeline (global -> smem -> global) when the buffers are 16-byte aligned\n");
     }
     put("predicted sector efficiency: %.3f\n", p->predicted_eff);
     p->text.assign(buf, std::min<int>(o, sizeof(buf) - 1));
