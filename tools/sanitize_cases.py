@@ -1,7 +1,8 @@
 """Small cases of every kernel path for compute-sanitizer (memcheck/racecheck):
 rows (whole rows, chunked rows, short predicated rows), chunked copy with
-tails, tile kernels (aligned, shifted, ragged, specialised and AOT), gather,
-the fused exchange, and the bounded host path.  Exits non-zero on a
+tails, bulk rows, tile kernels (aligned, shifted, ragged, congruent with VxV
+W blocks, residue + address swizzle, specialised and AOT), gather, the push
+and pull exchanges, and the bounded host path.  Exits non-zero on a
 parity failure."""
 import os
 import sys
@@ -25,6 +26,12 @@ cases = [
     ((17, 9, 13, 15, 11, 27), (5, 2, 0, 4, 1, 3), 4, {"jit": True}),
     ((33, 65, 129), (1, 2, 0), 2, {}),              # 2-byte words
     ((7, 5, 3), (2, 0, 1), 16, {}),                 # gather-size, 16-byte words
+    ((6, 4, 1024), (1, 0, 2), 4, {}),               # rows, TMA bulk pipeline (4 KiB rows, grouped)
+    ((3, 2, 5000), (1, 0, 2), 8, {}),               # rows, TMA bulk pipeline (40 KB rows, chunked)
+    ((256, 512), (1, 0), 4, {}),                    # tile, congruent swizzled rows + VxV W blocks (AOT)
+    ((256, 512), (1, 0), 4, {"jit": True}),         # ... specialised
+    ((64, 48, 56, 8), (0, 2, 3, 1), 8, {}),         # congruent rows, 8-byte words
+    ((37, 11, 45), (2, 0, 1), 4, {"jit": True}),    # residue strides mod 128 B + address swizzle
 ]
 bad = 0
 for shape, axes, E, kw in cases:
@@ -37,13 +44,14 @@ for shape, axes, E, kw in cases:
     ok = np.array_equal(y.cpu().numpy().reshape(-1), want)
     bad += not ok
     print(f"{prog.kernel:6s} {shape} {axes} E={E} {kw}: {'ok' if ok else 'MISMATCH'}", flush=True)
-# fused exchange, two virtual ranks
-shape, axes = (8, 6, 16, 4), (2, 0, 3, 1)
-g = torch.randint(-2**31, 2**31 - 1, (int(np.prod(shape)),), dtype=torch.int32, device="cuda")
-got = torch.cat(emulate_fused(g, shape, axes, 2))
-ok = torch.equal(got, g.view(shape).permute(axes).reshape(-1))
-bad += not ok
-print(f"exchange {shape}: {'ok' if ok else 'MISMATCH'}", flush=True)
+# fused exchanges: push (two virtual ranks), pull (four)
+for shape, axes, G, mode in [((8, 6, 16, 4), (2, 0, 3, 1), 2, "push"),
+                             ((2,) * 16, (3, 9, 0, 7, 1, 5, 2, 11, 8, 6, 4, 10, 15, 13, 14, 12), 4, "pull")]:
+    g = torch.randint(-2**31, 2**31 - 1, (int(np.prod(shape)),), dtype=torch.int32, device="cuda")
+    got = torch.cat(emulate_fused(g, shape, axes, G, mode=mode))
+    ok = torch.equal(got, g.view(shape).permute(axes).reshape(-1))
+    bad += not ok
+    print(f"exchange {mode} {shape}: {'ok' if ok else 'MISMATCH'}", flush=True)
 # bounded host path
 shape, axes = (16, 64, 56, 56), (0, 2, 3, 1)
 h = torch.randint(-2**31, 2**31 - 1, shape, dtype=torch.int32)
