@@ -15,3 +15,11 @@ print(sorted(round(v * 1e3, 3) for v in t))
 one = torch.zeros(1, device=dev)
 t = bench.time_device(torch, lambda: one.fill_(1), 40, 3, fl, st)
 print(sorted(round(v * 1e3, 3) for v in t))
+# the same with an L2 flush done by one of our own tile kernels (a 512 MiB
+# transpose: same shared-memory configuration as the timed kernel)
+big = torch.empty(128 << 20, dtype=torch.float32, device=dev)
+bigo = torch.empty_like(big)
+pf = vp.build_program(vp.TensorLayout.from_shape((8192, 16384), 4), vp.from_numpy_convention((1, 0)))
+own_flush = lambda: execute_device(pf, big, out=bigo)  # noqa: E731
+t = bench.time_device(torch, lambda: execute_device(p, x, out=y), 40, 3, own_flush, st)
+print("own-kernel flush:", sorted(round(v * 1e3, 3) for v in t))
