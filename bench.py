@@ -301,6 +301,81 @@ def run_reference_cpu(cfg, steps, warmup, threads=None, x=None, private=None):
     return gbs, times, threads, rk.target, private
 
 
+def run_reference_cpu_1core(cfg, reps=3, x=None):
+    """BASELINE.md §2 protocol: the reference's emitted kernel on ONE pinned
+    core (the paper measures a single core; flags emit.py:433),
+    best of `reps` full permutations.  The worker thread pins itself with
+    sched_setaffinity (per-thread on Linux; the `taskset -c` equivalent).
+    Returns (GB/s, best seconds, core id)."""
+    import numpy as np
+
+    from oracle.refkernels import RefKernel
+    from paper_2506_03686_b200.workloads import CONFIGS, make_input
+
+    wl = CONFIGS[cfg]
+    rk = RefKernel(cfg)
+    if x is None:
+        x = make_input(wl, threads=16)
+    src, dst = rk.alloc(), rk.alloc()
+    src.data[:] = x.reshape(-1).view(np.uint8)
+    cores = sorted(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else [0]
+    core = cores[-1]
+    res = {}
+
+    def worker():
+        if hasattr(os, "sched_setaffinity"):
+            os.sched_setaffinity(0, {core})
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            rk.run_ptr(src.ptr, dst.ptr)
+            ts.append(time.perf_counter() - t0)
+        res["best"] = min(ts)
+
+    t = threading.Thread(target=worker)
+    t.start()
+    t.join()
+    want = np.ascontiguousarray(np.transpose(x, wl.axes)).reshape(-1).view(np.uint8)
+    if not np.array_equal(dst.data, want):
+        raise RuntimeError("reference kernel output differs from numpy transpose")
+    return wl.algorithmic_bytes / res["best"] / 1e9, res["best"], core
+
+
+def cpu_baseline_1core_only(cfg):
+    """Sharded runs (N > 1): only the single-core line (bounded: 3 full
+    permutations), run on rank 0 after every timed region."""
+    try:
+        g1, best, core = run_reference_cpu_1core(cfg)
+        return {"value": round(g1, 3), "unit": "GB/s", "cores": 1, "kind": "reference",
+                "sample": f"1 full {cfg} permutation, best of 3, worker pinned to core {core}; "
+                          f"reference emitted kernel ({best * 1e3:.1f} ms); host {_cpu_model()}, "
+                          f"nproc {os.cpu_count()}"}
+    except Exception as e:
+        return {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
+
+
+def cpu_baseline_entry(cfg, cpu_threads=None):
+    """cpu_baseline of the JSON line: the 1-core line of BASELINE.md §2
+    (value, cores = 1) with the all-threads aggregate beside it."""
+    try:
+        g1, best, core = run_reference_cpu_1core(cfg)
+        out = {"value": round(g1, 3), "unit": "GB/s", "cores": 1, "kind": "reference",
+               "sample": f"1 full {cfg} permutation, best of 3, worker pinned to core {core} "
+                         f"(sched_setaffinity); reference emitted kernel ({best * 1e3:.1f} ms); "
+                         f"host {_cpu_model()}, nproc {os.cpu_count()}"}
+    except Exception as e:  # reported, not fatal
+        return {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
+    try:
+        gbs, times, threads, target, private = run_reference_cpu(cfg, 2, 1, threads=cpu_threads)
+        out["all_threads"] = {"value": round(gbs, 2), "unit": "GB/s", "cores": threads,
+                              "sample": f"{threads} concurrent full {cfg} permutations x 2 timed steps "
+                                        f"(reference emitted {target} kernel, "
+                                        f"{'private inputs' if private else 'shared input'})"}
+    except Exception as e:
+        out["all_threads"] = {"value": None, "sample": f"unavailable: {e}"}
+    return out
+
+
 def sample_parity(torch, x, y, shape, axes, nsamp=1 << 20, seed=0):
     """y[i] == x[f(i)] on random output offsets i (f per core.py:173-178)."""
     n = x.numel()
@@ -461,7 +536,69 @@ def _steady_entry(r, peak):
 
 
 # ---------------------------------------------------------------- sharded (N > 1)
-NVLINK_GBS = 770.0   # measured peer copy per direction per GPU (B200_PROFILING.md)
+NVLINK_GBS = 770.0   # fallback only: peer copy per direction per GPU (B200_PROFILING.md)
+
+
+def torchrun_cmd(argv, n, port):
+    """The command `bench.py --gpus N` re-executes itself with when it was not
+    started under torchrun: one rank per GPU on this node, rendezvous on
+    127.0.0.1 (the container hostname may not resolve)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + list(argv)
+
+
+def _free_port():
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(args, argv):
+    """--gpus N > 1 without WORLD_SIZE: refuse loudly if this node has fewer
+    than N GPUs (never print a 1-GPU line labelled N GPUs), else run N ranks
+    under torch.distributed.run; rank 0 prints the one JSON line."""
+    import subprocess
+
+    if args.dist_backend == "nccl":
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs on this node, found {have}; "
+                  f"refusing to report a {have}-GPU run as {args.gpus} GPUs", file=sys.stderr, flush=True)
+            return 2
+    cmd = torchrun_cmd(argv, args.gpus, _free_port())
+    print("bench.py: launching " + " ".join(cmd), file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
+def measure_alltoall(torch, dist, dev, G, nbytes=256 << 20, iters=10, warm=3):
+    """NCCL all_to_all_single on a 256 MiB per-rank buffer:
+    device time of `iters` back-to-back collectives, max over ranks.
+    Returns (algbw, busbw) in GB/s; busbw = algbw * (G-1)/G is the per-GPU
+    NVLink traffic rate (the nccl-tests convention), the NVLink roofline
+    denominator of the sharded line."""
+    nbytes -= nbytes % G
+    x = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    y = torch.empty_like(x)
+    for _ in range(warm):
+        dist.all_to_all_single(y, x)
+    torch.cuda.synchronize()
+    dist.barrier()
+    st = torch.cuda.current_stream()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(st)
+    for _ in range(iters):
+        dist.all_to_all_single(y, x)
+    b.record(st)
+    torch.cuda.synchronize()
+    t = torch.tensor([a.elapsed_time(b) / iters], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    algbw = nbytes / (t.item() * 1e-3) / 1e9
+    del x, y
+    return algbw, algbw * (G - 1) / G
 
 
 def bench_sharded(args, torch, base, config, peak, peak_kind):
@@ -478,6 +615,10 @@ def bench_sharded(args, torch, base, config, peak, peak_kind):
                                                shard_bounds)
     from paper_2506_03686_b200.workloads import CONFIGS, make_input_slice
 
+    # --sharded without torchrun: a one-rank process group on this node
+    for k, v in (("MASTER_ADDR", "127.0.0.1"), ("RANK", "0"), ("WORLD_SIZE", "1"), ("LOCAL_RANK", "0")):
+        os.environ.setdefault(k, v)
+    os.environ.setdefault("MASTER_PORT", str(_free_port()))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     backend = args.dist_backend
     # gloo: code-path check only -- ranks may share a GPU, so its timings are
@@ -491,6 +632,9 @@ def bench_sharded(args, torch, base, config, peak, peak_kind):
         dist.init_process_group("gloo")
     G, r = dist.get_world_size(), dist.get_rank()
     red_dev = dev if backend == "nccl" else torch.device("cpu")
+    a2a = None
+    if backend == "nccl" and G > 1:
+        a2a = measure_alltoall(torch, dist, dev, G)
     wl = CONFIGS[args.config]
     sp = plan_sharded(wl.shape, wl.axes, G)
     lo, hi = shard_bounds(wl.numel, G, r)
@@ -591,7 +735,10 @@ def bench_sharded(args, torch, base, config, peak, peak_kind):
     dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     shard_bytes = wl.numel * wl.elem_bytes // G
     t_hbm = 2 * shard_bytes / (peak * 1e9)
-    t_nvl = shard_bytes * (G - 1) / G / (NVLINK_GBS * 1e9)
+    nvl_gbs = a2a[1] if a2a else NVLINK_GBS
+    nvl_kind = ("measured all_to_all_single bus bandwidth, 256 MiB per rank, this run" if a2a else
+                "fallback peer-copy figure (B200_PROFILING.md; no NCCL all-to-all measured at this N)")
+    t_nvl = shard_bytes * (G - 1) / G / (nvl_gbs * 1e9)
     bound = "nvlink" if t_nvl > t_hbm else "hbm"
     roof_gbs = wl.algorithmic_bytes / max(t_hbm, t_nvl) / 1e9
     if r == 0:
@@ -608,12 +755,17 @@ def bench_sharded(args, torch, base, config, peak, peak_kind):
             "shard_method": method if method != "fused" else f"fused ({xmode})",
             "roofline": {"bound": bound, "achieved": round(gbs, 2), "peak": round(roof_gbs, 1),
                          "peak_kind": f"min over HBM ({peak_kind} {peak} GB/s per GPU) and NVLink "
-                                      f"({NVLINK_GBS} GB/s per direction per GPU) time bounds",
+                                      f"({nvl_gbs:.1f} GB/s per direction per GPU: {nvl_kind}) time bounds",
+                         "nvlink_gbs": round(nvl_gbs, 1),
+                         "frac_of_nvlink": round(gbs / (wl.algorithmic_bytes / t_nvl / 1e9), 4) if G > 1 else None,
                          "unit": "GB/s", "frac": round(gbs / roof_gbs, 4), "traffic": None,
                          "kernel": ("fused exchange tile kernel (peer stores over NVLink)" if xmode == "push" else
                                     "fused exchange tile kernel (peer reads over NVLink)") if method == "fused"
                          else "tile (P1/P2) + NCCL all_to_all_single"},
             "parity_sampled": bool(ok.item()),
+            "alltoall_256MiB": None if a2a is None else {"algbw_gbs": round(a2a[0], 1),
+                                                          "busbw_gbs": round(a2a[1], 1)},
+            "cpu_baseline": None if args.no_cpu else cpu_baseline_1core_only(args.config),
             "clocks": clk.summary(),
             "shard_plan": sp.describe()[:400],
             "dist_backend": backend if backend == "nccl" else
@@ -680,8 +832,15 @@ def main(argv=None):
     if args.warmup < 3:
         args.warmup = 3   # contract: W >= 3
 
+    if argv is None:
+        argv = sys.argv[1:]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        return self_launch(args, argv)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world > 1 and world != args.gpus:
+        print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}; reporting n_gpus={world}", file=sys.stderr)
+        args.gpus = world
     peak, peak_kind = _peaks()
     from paper_2506_03686_b200.workloads import CONFIGS
 
@@ -742,7 +901,6 @@ def main(argv=None):
     torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
     args._flusher = Flusher(torch, dev)
-    config["l2_bytes"] = args._flusher.l2
     with ClockSampler(0) as clk:
         main_res = bench_one_gpu(args, torch, args.config, True, peak)
     floor = event_floor_us(torch, args._flusher, torch.cuda.current_stream())
@@ -771,15 +929,7 @@ def main(argv=None):
                           "steady": _steady_entry(main_res, peak)}
     cpu = None
     if not args.no_cpu:
-        try:
-            gbs, times, threads, target, private = run_reference_cpu(args.config, 2, 1, threads=args.cpu_threads)
-            cpu = {"value": round(gbs, 2), "unit": "GB/s", "cores": threads, "kind": "reference",
-                   "sample": f"{threads} concurrent full {args.config} permutations x 2 timed steps "
-                             f"(reference emitted {target} kernel, "
-                             f"{'private inputs' if private else 'shared input'}); host {_cpu_model()}"}
-        except Exception as e:  # reported, not fatal
-            cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference",
-                   "sample": f"unavailable: {e}"}
+        cpu = cpu_baseline_entry(args.config, args.cpu_threads)
         cpu_numpy = _numpy_baseline(args.config)
     ms = main_res["ms_per_launch"]
     line = dict(base)
@@ -804,6 +954,7 @@ def main(argv=None):
         "parity_sampled": main_res["parity_sampled"],
         "configs": extra,
         "event_floor_us": round(floor, 2),
+        "l2_bytes": args._flusher.l2,
         "step_ms_stats": {"mean": round(ms, 5), "median": round(statistics.median(main_res["times_ms"]), 5),
                           "min": round(min(main_res["times_ms"]), 5), "max": round(max(main_res["times_ms"]), 5)},
     })

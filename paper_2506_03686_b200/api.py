@@ -69,6 +69,20 @@ def _check(status: int, what: str):
     raise VpgError(msg)
 
 
+def _measured_hbm_gbs(default: float = 6555.2) -> float:
+    """HBM copy bandwidth (read+write GB/s) from the driver-written
+    MEASURED_PEAKS.json at the repo root, when present."""
+    import json
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except (OSError, ValueError, KeyError, TypeError):
+        return default
+
+
 @dataclass(frozen=True)
 class GpuTarget:
     """GPU target descriptor (the MachineConfig analog, machine.py:13-40).
@@ -81,7 +95,7 @@ class GpuTarget:
     arch: str = "sm_100a"
     sms: int = 148
     smem_per_sm: int = 228 * 1024
-    hbm_gbs: float = 6542.7      # MEASURED_PEAKS.json (copy, read+write)
+    hbm_gbs: float = field(default_factory=_measured_hbm_gbs)   # MEASURED_PEAKS.json (copy, read+write)
 
 
 # ------------------------------------------------------------------ merge
@@ -374,7 +388,7 @@ def autotune(layout: TensorLayout, pmap: PermutationMap, candidates: int = 10, r
         return base
     torch = _torch()
     if not torch.cuda.is_available():
-        raise CudaError("autotune needs a CUDA device")
+        raise VpgError("autotune needs a CUDA device")
     if src is not None:
         dev = src.device
     else:
@@ -518,27 +532,47 @@ def execute(program: GpuProgram, input_buf, trace: bool = False, out=None, strea
                           max_device_bytes=max_device_bytes), _counters(program))
 
 
-_scratch: dict = {}
+_scratch: "collections.OrderedDict" = None      # (id(program), device) -> (program, d_in, d_out), LRU
 _scratch_lock = threading.Lock()
+SCRATCH_PROGRAMS = 4        # host-path programs whose device staging buffers stay cached
 
 
 def _host_scratch(torch, program, dev):
-    """Device staging buffers of the host path, kept per (program, device);
-    the library orders reuse across in-flight calls."""
+    """Device staging buffers of the host path, kept per (program, device)
+    for the last SCRATCH_PROGRAMS programs; the library orders reuse across
+    in-flight calls.  An evicted pair is released only after the device has
+    finished every call that may still use it (the library's internal
+    streams are not known to torch's allocator)."""
+    import collections
+
+    global _scratch
     key = (id(program), dev.index)
     with _scratch_lock:
+        if _scratch is None:
+            _scratch = collections.OrderedDict()
         hit = _scratch.get(key)
         if hit is None or hit[0] is not program:
             hit = (program, torch.empty(program.nbytes, dtype=torch.uint8, device=dev),
                    torch.empty(program.nbytes, dtype=torch.uint8, device=dev))
             _scratch[key] = hit
+        _scratch.move_to_end(key)
+        if len(_scratch) > SCRATCH_PROGRAMS:
+            for d in {k[1] for k in _scratch}:
+                torch.cuda.synchronize(d)
+            while len(_scratch) > SCRATCH_PROGRAMS:
+                _scratch.popitem(last=False)
         return hit[1], hit[2]
 
 
 def release_scratch():
-    """Free the device staging buffers of the host path."""
+    """Free the device staging buffers of the host path (after the device
+    has finished the calls that may still use them)."""
+    torch = _torch()
     with _scratch_lock:
-        _scratch.clear()
+        if _scratch:
+            for d in {k[1] for k in _scratch}:
+                torch.cuda.synchronize(d)
+            _scratch.clear()
 
 
 def _execute_host(program: GpuProgram, input_buf, out=None, stream=None, blocking=True, max_device_bytes=None):
@@ -563,7 +597,7 @@ def _execute_host(program: GpuProgram, input_buf, out=None, stream=None, blockin
         hbytes = torch.from_numpy(data.copy() if not data.flags.writeable else data)
     dev = torch.device("cuda", torch.cuda.current_device())
     need = 2 * program.nbytes
-    if max_device_bytes is None and (id(program), dev.index) not in _scratch:
+    if max_device_bytes is None and (_scratch is None or (id(program), dev.index) not in _scratch):
         free = torch.cuda.mem_get_info(dev)[0]
         if need > 0.9 * free:
             max_device_bytes = int(0.5 * free)
@@ -573,7 +607,9 @@ def _execute_host(program: GpuProgram, input_buf, out=None, stream=None, blockin
     if not blocking and (out is None or not as_tensor or not hbytes.is_pinned() or not out.is_pinned()):
         raise LayoutError("blocking=False needs a pinned CPU tensor input and a pinned `out`")
     if out is None:
-        h_out = torch.empty(program.nbytes, dtype=torch.uint8, pin_memory=hbytes.is_pinned())
+        # always pinned: a D2H copy into pageable memory returns only when it
+        # completes, which would serialise the chunked pipeline
+        h_out = torch.empty(program.nbytes, dtype=torch.uint8, pin_memory=True)
     else:
         h_out = out.reshape(-1).view(torch.uint8)
     if program.num_elements:

@@ -29,6 +29,11 @@ vpg_status fail(vpg_status s, const std::string &msg) {
 
 std::mutex g_cache_mu;
 std::map<std::vector<int64_t>, vpg_plan *> g_cache;  // never freed (process lifetime)
+// [a, a+na) and [b, b+nb) intersect (out-of-place only: the kernels would race)
+bool overlaps(const void *a, uint64_t na, const void *b, uint64_t nb) {
+    const uintptr_t x = (uintptr_t)a, y = (uintptr_t)b;
+    return na > 0 && nb > 0 && x < y + nb && y < x + na;
+}
 }  // namespace
 
 extern "C" {
@@ -41,6 +46,10 @@ vpg_status vpg_merge_dimensions(int rank, const int64_t *dims, const int32_t *si
                                 int64_t *out_dims, int32_t *out_sigma) {
     if (!dims || !sigma || !out_rank || !out_dims || !out_sigma)
         return fail(VPG_EINVAL, "null argument");
+    std::vector<int64_t> sq_d;
+    std::vector<int32_t> sq_s;
+    std::string err;
+    if (!vpg::squeeze_unit_dims(rank, dims, sigma, sq_d, sq_s, &err)) return fail(VPG_EINVAL, err);
     if (rank < 1 || rank > VPG_MAX_RANK) return fail(VPG_EINVAL, "rank out of range");
     std::vector<int> seen(rank, 0);
     for (int k = 0; k < rank; ++k) {
@@ -78,8 +87,9 @@ vpg_status vpg_permute_sharded(const vpg_plan *plan, const void *src_shard, void
     if (plan->shards < 1) return fail(VPG_EINVAL, "not a sharded plan (use vpg_permute)");
     if (plan->tile.pull) return fail(VPG_EINVAL, "pull exchange plan: use vpg_permute_sharded_pull");
     if (plan->n > 0 && !src_shard) return fail(VPG_EINVAL, "null buffer");
+    const uint64_t sb = (uint64_t)(plan->n / plan->shards) * (uint64_t)plan->elem_bytes;
     for (int q = 0; q < plan->shards; ++q)
-        if (dst_shards[q] == src_shard && plan->n > 0)
+        if (overlaps(dst_shards[q], sb, src_shard, sb))
             return fail(VPG_EINVAL, "src and dst must not overlap (out-of-place only)");
     std::string err;
     vpg_status s = vpg::launch_plan(plan, src_shard, dst_shards, plan->shards, cuda_stream, &err);
@@ -94,7 +104,8 @@ vpg_status vpg_permute_sharded_pull(const vpg_plan *plan, const void *const *src
     if (plan->n > 0 && !dst_shard) return fail(VPG_EINVAL, "null buffer");
     for (int q = 0; q < plan->shards; ++q) {
         if (plan->n > 0 && !src_shards[q]) return fail(VPG_EINVAL, "null buffer");
-        if (src_shards[q] == dst_shard && plan->n > 0)
+        const uint64_t sb = (uint64_t)(plan->n / plan->shards) * (uint64_t)plan->elem_bytes;
+        if (overlaps(src_shards[q], sb, dst_shard, sb))
             return fail(VPG_EINVAL, "src and dst must not overlap (out-of-place only)");
     }
     std::string err;
@@ -128,7 +139,8 @@ vpg_status vpg_permute(const vpg_plan *plan, const void *src, void *dst, void *c
     if (!plan) return fail(VPG_EINVAL, "null plan");
     if (plan->shards > 1) return fail(VPG_EINVAL, "sharded plan: use vpg_permute_sharded");
     if (plan->n > 0 && (!src || !dst)) return fail(VPG_EINVAL, "null buffer");
-    if (src == dst && plan->n > 0) return fail(VPG_EINVAL, "src and dst must not overlap (out-of-place only)");
+    const uint64_t nb = (uint64_t)plan->n * (uint64_t)plan->elem_bytes;
+    if (overlaps(src, nb, dst, nb)) return fail(VPG_EINVAL, "src and dst must not overlap (out-of-place only)");
     std::string err;
     vpg_status s = vpg::launch_plan(plan, src, dst, cuda_stream, &err);
     if (s != VPG_OK) return fail(s, err);
@@ -139,6 +151,11 @@ vpg_status vpg_permute_host(const vpg_plan *plan, const void *host_src, void *ho
                             void *dev_dst, void *cuda_stream) {
     if (!plan || !host_src || !host_dst || !dev_src || !dev_dst) return fail(VPG_EINVAL, "null argument");
     if (plan->shards > 0) return fail(VPG_EINVAL, "sharded plans run through vpg_permute_sharded");
+    {
+        const uint64_t nb = (uint64_t)plan->n * (uint64_t)plan->elem_bytes;
+        if (overlaps(host_src, nb, host_dst, nb))
+            return fail(VPG_EINVAL, "host src and dst must not overlap (out-of-place only)");
+    }
     if (plan->n == 0) return VPG_OK;
     std::string err;
     vpg_status s = vpg::permute_host_pipelined(plan, host_src, host_dst, dev_src, dev_dst, (cudaStream_t)cuda_stream,
@@ -150,6 +167,11 @@ vpg_status vpg_permute_host_bounded(const vpg_plan *plan, const void *host_src, 
                                     size_t scratch_bytes, void *cuda_stream) {
     if (!plan || !host_src || !host_dst || !dev_scratch) return fail(VPG_EINVAL, "null argument");
     if (plan->shards > 0) return fail(VPG_EINVAL, "sharded plans run through vpg_permute_sharded");
+    {
+        const uint64_t nb = (uint64_t)plan->n * (uint64_t)plan->elem_bytes;
+        if (overlaps(host_src, nb, host_dst, nb))
+            return fail(VPG_EINVAL, "host src and dst must not overlap (out-of-place only)");
+    }
     if (plan->n == 0) return VPG_OK;
     std::string err;
     vpg_status s = vpg::permute_host_bounded(plan, host_src, host_dst, dev_scratch, scratch_bytes,
@@ -161,6 +183,11 @@ vpg_status vpg_permute_host_async(const vpg_plan *plan, const void *host_src, vo
                                   void *dev_dst, void *cuda_stream) {
     if (!plan || !host_src || !host_dst || !dev_src || !dev_dst) return fail(VPG_EINVAL, "null argument");
     if (plan->shards > 0) return fail(VPG_EINVAL, "sharded plans run through vpg_permute_sharded");
+    {
+        const uint64_t nb = (uint64_t)plan->n * (uint64_t)plan->elem_bytes;
+        if (overlaps(host_src, nb, host_dst, nb))
+            return fail(VPG_EINVAL, "host src and dst must not overlap (out-of-place only)");
+    }
     if (plan->n == 0) return VPG_OK;
     std::string err;
     vpg_status ps = vpg::permute_host_pipelined(plan, host_src, host_dst, dev_src, dev_dst,
@@ -172,7 +199,7 @@ vpg_status vpg_permute_host_async(const vpg_plan *plan, const void *host_src, vo
 vpg_status vpg_permute_nd(int rank, const int64_t *dims, const int32_t *sigma, int elem_bytes,
                           const void *src, void *dst, void *cuda_stream) {
     if (!dims || !sigma) return fail(VPG_EINVAL, "null argument");
-    if (rank < 1 || rank > VPG_MAX_RANK) return fail(VPG_EINVAL, "rank out of range");
+    if (rank < 1) return fail(VPG_EINVAL, "rank out of range");
     std::vector<int64_t> key;
     key.reserve(2 * rank + 2);
     key.push_back(rank);

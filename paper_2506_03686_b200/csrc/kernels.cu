@@ -260,7 +260,8 @@ namespace {
 std::mutex g_mu;
 std::map<int, int> g_sm_count;
 std::map<std::tuple<const void *, int, int>, int> g_occ;
-std::map<const void *, bool> g_attr_set;
+// dynamic-smem opt-in is a per-device function attribute: keyed by (kernel, device)
+std::map<std::pair<const void *, int>, bool> g_attr_set;
 
 int sm_count_for_current() {
     int dev = 0;
@@ -316,14 +317,14 @@ int occupancy(K kernel, int threads, int smem) {
     auto key = std::make_tuple((const void *)kernel, threads, smem + (dev << 24));
     auto it = g_occ.find(key);
     if (it != g_occ.end()) return it->second;
-    if (!g_attr_set[(const void *)kernel]) {
+    if (!g_attr_set[std::make_pair((const void *)kernel, dev)]) {
         int optin = 0;
         if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || optin <= 0)
             optin = 227 * 1024;
         cudaFuncAttributes fa;
         size_t stat = cudaFuncGetAttributes(&fa, kernel) == cudaSuccess ? fa.sharedSizeBytes : 1024;
         cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)stat);
-        g_attr_set[(const void *)kernel] = true;
+        g_attr_set[std::make_pair((const void *)kernel, dev)] = true;
     }
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, threads, smem) != cudaSuccess || nb < 1)

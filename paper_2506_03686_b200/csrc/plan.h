@@ -10,6 +10,7 @@
 
 #include <stdint.h>
 #include <string>
+#include <vector>
 
 #include "vpgpu.h"
 #include <cuda_runtime.h>
@@ -44,6 +45,8 @@ namespace vpg {
 int merge_dims(int rank, const int64_t *dims, const int32_t *sigma, int64_t *od, int32_t *os,
                const uint8_t *pin = nullptr, uint8_t *opin = nullptr);
 // shards > 0: fused sharded exchange plan for input shard shard_index
+bool squeeze_unit_dims(int &rank, const int64_t *&dims, const int32_t *&sigma, std::vector<int64_t> &sd,
+                       std::vector<int32_t> &ss, std::string *err);
 vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E, unsigned flags,
                      vpg_plan **out, std::string *err, int shards = 0, int shard_index = 0);
 // ipc.cpp

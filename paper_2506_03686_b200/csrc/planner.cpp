@@ -1268,8 +1268,58 @@ static void describe(vpg_plan *p) {
     p->text.assign(buf, std::min<int>(o, sizeof(buf) - 1));
 }
 
+// Inputs of rank > VPG_MAX_RANK are accepted when their size-1 dims, which
+// merge_dimensions drops anyway (planner.py:222-227), bring the rank within
+// the limit: validate over the full rank, then squeeze (sigma renumbered).
+// The reference has no rank cap (core.py:58-88).
+bool squeeze_unit_dims(int &rank, const int64_t *&dims, const int32_t *&sigma, std::vector<int64_t> &sd,
+                       std::vector<int32_t> &ss, std::string *err) {
+    if (rank <= VPG_MAX_RANK) return true;
+    if (rank > (1 << 20)) {
+        *err = "rank " + std::to_string(rank) + " is out of range";
+        return false;
+    }
+    std::vector<int> seen(rank, 0), renum(rank, -1);
+    for (int k = 0; k < rank; ++k) {
+        if (dims[k] < 1) {
+            *err = "dimension " + std::to_string(dims[k]) + " is not positive";
+            return false;
+        }
+        if (sigma[k] < 0 || sigma[k] >= rank || seen[sigma[k]]) {
+            *err = "map is not a bijection on 0.." + std::to_string(rank - 1);
+            return false;
+        }
+        seen[sigma[k]] = 1;
+    }
+    sd.clear();
+    ss.clear();
+    for (int k = 0; k < rank; ++k)
+        if (dims[k] > 1) {
+            renum[k] = (int)sd.size();
+            sd.push_back(dims[k]);
+        }
+    for (int j = 0; j < rank; ++j)
+        if (renum[sigma[j]] >= 0) ss.push_back(renum[sigma[j]]);
+    if (sd.empty()) {
+        sd.push_back(1);
+        ss.push_back(0);
+    }
+    if ((int)sd.size() > VPG_MAX_RANK) {
+        *err = "rank after dropping size-1 dims (" + std::to_string(sd.size()) + ") exceeds " +
+               std::to_string(VPG_MAX_RANK);
+        return false;
+    }
+    rank = (int)sd.size();
+    dims = sd.data();
+    sigma = ss.data();
+    return true;
+}
+
 vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E, unsigned flags,
                      vpg_plan **out, std::string *err, int shards, int shard_index) {
+    std::vector<int64_t> sq_d;
+    std::vector<int32_t> sq_s;
+    if (!squeeze_unit_dims(rank, dims, sigma, sq_d, sq_s, err)) return VPG_EINVAL;
     if (rank < 1 || rank > VPG_MAX_RANK) {
         *err = "rank must be in 1.." + std::to_string(VPG_MAX_RANK);
         return VPG_EINVAL;

@@ -547,7 +547,12 @@ __device__ __forceinline__ void decode_tile(const TileParams &p, const ShardArgs
 // for the other ranks' shards).
 template <typename W>
 __device__ __forceinline__ const W *pull_ptr(const TileParams &p, const ShardArgs &sa, const W *src, int64_t o) {
-    const uint32_t q = p.shard_shift ? (uint32_t)((uint64_t)o >> p.shard_shift) : fdiv((uint32_t)o, p.shard_div);
+    // power-of-two shards: a shift; otherwise a 32-bit fast divide while every
+    // global offset fits 32 bits, else a 64-bit divide (uniform branch; it
+    // folds away in specialised kernels, where p is a constant)
+    const uint32_t q = p.shard_shift               ? (uint32_t)((uint64_t)o >> p.shard_shift)
+                       : p.n_elems <= 0xffffffffll ? fdiv((uint32_t)o, p.shard_div)
+                                                   : (uint32_t)((uint64_t)o / (uint64_t)p.shard_elems);
     return src + (sa.off[q] + (o - (int64_t)q * p.shard_elems));
 }
 

@@ -108,3 +108,38 @@ def test_sharded_plan_errors_without_gpu():
     assert L.vpg_permute(p, ctypes.c_void_p(16), ctypes.c_void_p(4096), None) == _lib.VPG_EINVAL
     assert "vpg_permute_sharded" in _lib.last_error()
     L.vpg_plan_destroy(p)
+
+
+def test_rank_above_64_with_unit_dims_is_accepted():
+    """Size-1 dims are dropped before the rank limit (the reference has no
+    rank cap, core.py:58-88; merge_dimensions drops them, planner.py:222-227)."""
+    import numpy as np
+
+    from paper_2506_03686_b200 import PermutationMap, TensorLayout, build_program, merge_dimensions
+
+    rng = np.random.default_rng(7)
+    dims = [1] * 70
+    for k, e in zip(rng.choice(70, 5, replace=False), (3, 5, 2, 7, 4)):
+        dims[k] = int(e)
+    sigma = tuple(int(v) for v in rng.permutation(70))
+    lay, pm = TensorLayout(tuple(dims), 4), PermutationMap(sigma)
+    ml, mp = merge_dimensions(lay, pm)
+    assert 1 <= ml.rank <= 5 and np.prod(ml.dims) == 3 * 5 * 2 * 7 * 4
+    prog = build_program(lay, pm)
+    assert prog.num_elements == 3 * 5 * 2 * 7 * 4
+    # 70 dims that are not size 1 stay out of range
+    with pytest.raises(ValueError):
+        build_program(TensorLayout((2,) * 70, 4), PermutationMap(tuple(range(70))[::-1]))
+
+
+def test_overlapping_buffers_rejected_before_any_device_work():
+    L = _lib.lib()
+    rank, d, s = _lib.arrays((64, 48), (1, 0))
+    p = ctypes.c_void_p()
+    assert L.vpg_plan_create(rank, d, s, 4, 0, ctypes.byref(p)) == 0
+    base = 1 << 40
+    # partial overlap (dst starts inside src): EINVAL, no launch attempted
+    assert L.vpg_permute(p, ctypes.c_void_p(base), ctypes.c_void_p(base + 256), None) == _lib.VPG_EINVAL
+    assert "overlap" in _lib.last_error()
+    assert L.vpg_permute(p, ctypes.c_void_p(base + 256), ctypes.c_void_p(base), None) == _lib.VPG_EINVAL
+    L.vpg_plan_destroy(p)

@@ -581,3 +581,28 @@ def test_back_to_back_dependent_launches(cuda, shape, axes):
     torch.cuda.synchronize()
     assert torch.equal(a, x0)
     assert np.array_equal(b.cpu().numpy(), want_b)
+
+
+def test_rank_above_64_unit_dims_permute(cuda):
+    """A rank-70 tensor whose size-1 dims bring it within the limit permutes
+    like its squeezed form (the reference has no rank cap, core.py:58-88)."""
+    import numpy as np
+    import torch
+
+    from paper_2506_03686_b200 import permute
+
+    rng = np.random.default_rng(11)
+    shape = [1] * 70
+    big = rng.choice(70, 5, replace=False)
+    for k, e in zip(big, (33, 17, 9, 5, 12)):
+        shape[k] = int(e)
+    axes = tuple(int(v) for v in rng.permutation(70))
+    n = int(np.prod(shape))
+    x = torch.randint(-2**31, 2**31 - 1, (n,), dtype=torch.int32, device=cuda)
+    y = permute(x.view(shape), axes)
+    torch.cuda.synchronize()
+    keep = [a for a in range(70) if shape[a] > 1]
+    sq_axes = [keep.index(a) for a in axes if shape[a] > 1]
+    want = x.view([shape[a] for a in keep]).permute(sq_axes).contiguous()
+    assert list(y.shape) == [shape[a] for a in axes]
+    assert torch.equal(y.reshape(-1), want.reshape(-1))

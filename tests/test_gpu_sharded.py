@@ -321,3 +321,30 @@ def test_pull_exchange_separate_buffers(cuda, offset_words):
         assert torch.equal(torch.cat(outs), x.view(shape).permute(axes).reshape(-1)), (shape, axes, G)
         ran += 1
     assert ran >= 3
+
+
+def test_pull_exchange_nonpow2_shards_beyond_32bit_offsets(cuda):
+    """Pull exchange with G = 3 (shard size not a power of two) on more than
+    2^32 one-byte elements: the source shard of every chunk is found with a
+    64-bit divide (tile_body.cuh pull_ptr); a 32-bit one would read the wrong
+    shard past offset 2^32."""
+    import torch
+
+    import paper_2506_03686_b200 as vp
+    from paper_2506_03686_b200.sharded import emulate_fused, shard_bounds
+
+    shape, axes, G = (3, 1 << 21, 768), (2, 1, 0), 3
+    n = 3 * (1 << 21) * 768
+    assert n > 1 << 32
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randint(0, 256, (n,), dtype=torch.uint8, device="cuda", generator=g)
+    shards = [x[slice(*shard_bounds(n, G, r))].clone() for r in range(G)]
+    try:
+        outs = emulate_fused(x, shape, axes, G, mode="pull", in_shards=shards)
+    except vp.LayoutError as e:
+        pytest.skip(f"no pull plan: {e}")
+    del shards
+    torch.cuda.synchronize()
+    want = x.view(shape).permute(axes).contiguous().reshape(-1)
+    got = torch.cat(outs)
+    assert torch.equal(got, want)
