@@ -11,7 +11,8 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libvpgpu.so")
+# VPG_LIB_PATH: development override (A/B of library builds, tools/); default in-tree
+LIB_PATH = os.environ.get("VPG_LIB_PATH") or os.path.join(HERE, "libvpgpu.so")
 
 VPG_OK, VPG_EINVAL, VPG_EUNSUPPORTED, VPG_ECUDA, VPG_ENOMEM = range(5)
 KERNEL_NAMES = {0: "copy", 1: "rows", 2: "tile", 3: "gather"}

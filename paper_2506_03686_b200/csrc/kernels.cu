@@ -23,6 +23,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <tuple>
@@ -155,17 +156,40 @@ __device__ __forceinline__ void bulk_s2g(void *gdst, const void *ssrc, uint32_t 
 __global__ void __launch_bounds__(32) rows_bulk_kernel(const __grid_constant__ RowsParams p,
                                                        const unsigned char *__restrict__ src,
                                                        unsigned char *__restrict__ dst, uint32_t E,
-                                                       uint32_t slot_bytes, uint32_t rpi) {
+                                                       uint32_t slot_bytes, uint32_t rpi, uint32_t *sched) {
     extern __shared__ __align__(128) unsigned char rb_smem[];
     __shared__ __align__(8) uint64_t bar[kRowsBulkSlots];
     constexpr uint32_t S = kRowsBulkSlots;
     pdl_trigger();
     if (threadIdx.x != 0) return;
+    const uint32_t step = gridDim.x;
+    // work items: the first S-1 of a CTA static (blockIdx.x + k * gridDim.x),
+    // later ones claimed from the dynamic scheduler ((S-1) * gridDim.x +
+    // atomicAdd(next), see tile_body) when the launch carries one, so CTAs on
+    // SMs that drain faster move more rows; a claim is prefetched one item
+    // ahead
+    const bool dyn = sched != nullptr && (S - 1) * step < p.nitems;
+    uint32_t pre = dyn ? atomicAdd(sched, 1u) : 0u;
+    bool claimed_out = false;
+    auto claim = [&](uint32_t k) -> uint32_t {
+        if (k + 1 < S || !dyn) return blockIdx.x + k * step;
+        if (claimed_out) return 0xffffffffu;
+        const uint32_t w = (S - 1) * step + pre;
+        if (w < p.nitems) {
+            pre = atomicAdd(sched, 1u);
+        } else {
+            claimed_out = true;
+            __threadfence();      // the last CTA to run out resets the pair
+            if (atomicAdd(sched + 1, 1u) == gridDim.x - 1) {
+                atomicExch(sched, 0u);
+                atomicExch(sched + 1, 0u);
+            }
+        }
+        return w;
+    };
     for (uint32_t j = 0; j < S; ++j) mbar_init(&bar[j], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     pdl_wait();
-    const uint32_t step = gridDim.x;
-    const uint32_t cnt = p.nitems > blockIdx.x ? (p.nitems - blockIdx.x + step - 1) / step : 0u;
     const uint32_t row_bytes = (uint32_t)(p.row_len * E), chunk_bytes = p.chunk_vecs * 16u;
     // work item w: rows [w*rpi, w*rpi + rpi) when rows are short (rpi > 1,
     // one load per row, one store of the contiguous destination block), else
@@ -180,8 +204,7 @@ __global__ void __launch_bounds__(32) rows_bulk_kernel(const __grid_constant__ R
         }
         return src + so * E;
     };
-    auto item = [&](uint32_t k, uint32_t &q0, uint32_t &nr, uint32_t &c0) -> uint32_t {
-        const uint32_t w = blockIdx.x + k * step;
+    auto item = [&](uint32_t w, uint32_t &q0, uint32_t &nr, uint32_t &c0) -> uint32_t {
         if (rpi > 1) {
             q0 = w * rpi;
             nr = min(rpi, p.nrows - q0);
@@ -193,26 +216,34 @@ __global__ void __launch_bounds__(32) rows_bulk_kernel(const __grid_constant__ R
         c0 = (w - q0 * p.nchunks.d) * chunk_bytes;
         return min(chunk_bytes, row_bytes - c0);
     };
-    auto load = [&](uint32_t k) {
+    auto load = [&](uint32_t k, uint32_t w) {
         uint32_t q0, nr, c0;
-        const uint32_t n = item(k, q0, nr, c0);
+        const uint32_t n = item(w, q0, nr, c0);
         const uint32_t j = k % S;
         mbar_arrive_expect_tx(&bar[j], n);
         for (uint32_t r = 0; r < nr; ++r)
             bulk_g2s(rb_smem + j * slot_bytes + r * row_bytes, src_row(q0 + r) + c0, nr > 1 ? row_bytes : n, &bar[j]);
     };
-    for (uint32_t k = 0; k + 1 < S && k < cnt; ++k) load(k);
-    for (uint32_t k = 0; k < cnt; ++k) {
+    uint32_t ws[S];               // item of each slot (>= nitems: none)
+    for (uint32_t k = 0; k + 1 < S; ++k) {
+        ws[k] = claim(k);
+        if (ws[k] < p.nitems) load(k, ws[k]);
+    }
+    for (uint32_t k = 0;; ++k) {
         const uint32_t j = k % S;
+        const uint32_t w = ws[j];
+        if (w >= p.nitems) break;
         mbar_wait(&bar[j], (k / S) & 1);
         uint32_t q0, nr, c0;
-        const uint32_t n = item(k, q0, nr, c0);
+        const uint32_t n = item(w, q0, nr, c0);
         bulk_s2g(dst + (int64_t)q0 * row_bytes + c0, rb_smem + j * slot_bytes, n);
         asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-        if (k + S - 1 < cnt) {
-            // slot (k + S - 1) % S held item k - 1: its store must be done reading
+        const uint32_t kn = k + S - 1;
+        ws[kn % S] = claim(kn);
+        if (ws[kn % S] < p.nitems) {
+            // slot kn % S held item k - 1: its store must be done reading
             asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
-            load(k + S - 1);
+            load(kn, ws[kn % S]);
         }
     }
     asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
@@ -273,6 +304,50 @@ int sm_count_for_current() {
     if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
     g_sm_count[dev] = n;
     return n;
+}
+
+// Dynamic tile scheduler counters (tile_body.cuh): a ring of {next, done}
+// pairs per device, zeroed once; each tile launch takes the next pair and
+// its last CTA resets the pair, so a pair is reused only kSchedSlots launches
+// later (launches in flight at once on other streams use other pairs).
+// VPG_SCHED=0 keeps the static round-robin schedule.  Not during stream
+// capture before the ring exists (allocation is not capturable); graph
+// replays of one launch reuse its pair sequentially, which the reset allows.
+constexpr uint32_t kSchedSlots = 4096;
+std::map<int, uint32_t *> g_sched_ring;
+std::atomic<uint32_t> g_sched_seq{0};
+
+uint32_t *sched_slot(cudaStream_t st) {
+    static const bool off = getenv("VPG_SCHED") && atoi(getenv("VPG_SCHED")) == 0;
+    if (off) return nullptr;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    uint32_t *base = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        auto it = g_sched_ring.find(dev);
+        if (it != g_sched_ring.end()) {
+            base = it->second;
+        } else {
+            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+            if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+                cudaGetLastError();
+                return nullptr;
+            }
+            void *p = nullptr;
+            if (cudaMalloc(&p, kSchedSlots * 2 * sizeof(uint32_t)) == cudaSuccess &&
+                cudaMemset(p, 0, kSchedSlots * 2 * sizeof(uint32_t)) == cudaSuccess &&
+                cudaDeviceSynchronize() == cudaSuccess) {
+                base = (uint32_t *)p;
+            } else {
+                cudaGetLastError();
+                if (p) cudaFree(p);
+            }
+            g_sched_ring[dev] = base;      // nullptr: static schedule on this device
+        }
+    }
+    if (!base) return nullptr;
+    return base + 2 * (g_sched_seq.fetch_add(1, std::memory_order_relaxed) % kSchedSlots);
 }
 
 // Launches carry the programmatic stream-serialisation attribute (PDL, see
@@ -350,8 +425,12 @@ int occupancy_ptr(const void *kernel, int threads, int smem) {
 }
 
 template <int E>
-vpg_status launch_tile(const vpg_plan *p, const void *src, void *dst, const ShardArgs &sa, cudaStream_t st) {
+vpg_status launch_tile(const vpg_plan *p, const void *src, void *dst, const ShardArgs &sa_in, cudaStream_t st) {
     using W = typename WordOf<E>::T;
+    ShardArgs sa = sa_in;
+    // dynamic tile schedule for persistent CTAs (not the bulk-read variant,
+    // whose producer warp keeps the static order)
+    sa.sched = p->tile.persistent && !p->tile.bulk ? sched_slot(st) : nullptr;
     const int smem = (int)p->tile.smem_bytes;
     bool aligned = !(p->tile.ph[0].vec > 1 && ((uintptr_t)src % 16));
     if (p->tile.ph[1].w2) {      // 16-byte destination stores: every destination buffer 16-byte aligned
@@ -472,7 +551,7 @@ vpg_status launch_rows(const vpg_plan *p, const void *src, void *dst, cudaStream
                 int64_t grid = std::min<int64_t>(bp.nitems, (int64_t)nb * sm_count_for_current());
                 if (grid < 1) grid = 1;
                 launch_k(rows_bulk_kernel, grid, 32, smem, st, true, bp, (const unsigned char *)src,
-                         (unsigned char *)dst, (uint32_t)E, slot, rpi);
+                         (unsigned char *)dst, (uint32_t)E, slot, rpi, sched_slot(st));
                 return VPG_OK;
             }
         }

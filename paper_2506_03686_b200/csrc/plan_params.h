@@ -209,6 +209,10 @@ static_assert(sizeof(TileParams) <= 4096, "kernel parameter block must stay unde
 constexpr int kMaxShards = 64;
 struct ShardArgs {
     int64_t off[kMaxShards];
+    // dynamic tile scheduler (tile kernels): a {next, done} counter pair from
+    // the per-device ring (kernels.cu sched_slot), zero at launch and reset
+    // by the last CTA; nullptr = static round-robin tiles
+    uint32_t *sched;
 };
 
 // --------------------------------------------------------------------------

@@ -74,9 +74,11 @@ struct ThreadPart {
 #define VPG_HINTS 0
 #endif
 
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// cp.async of E bytes to the shared-window address s
 template <int E>
-__device__ __forceinline__ void cp_async(void *sp, const void *gp) {
-    const uint32_t s = (uint32_t)__cvta_generic_to_shared(sp);
+__device__ __forceinline__ void cp_async(uint32_t s, const void *gp) {
 #if VPG_HINTS & 1
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
@@ -159,28 +161,32 @@ __device__ __forceinline__ uint32_t swizzle(const PhaseDesc &d, uint32_t s) {
 }
 
 // Address swizzle (PhaseDesc::swz == kSwzAddr): the 16-byte chunk index
-// inside each 128-byte block of shared memory XOR the block index (mod 8).
-// It acts on the address itself (shared-window addresses keep their low
-// bits in generic form; stage buffers are 128-byte aligned), so it needs no
-// row structure: the residue layouts use it.
-template <typename W>
-__device__ __forceinline__ W *swz_addr(W *p) {
-    const uintptr_t a = (uintptr_t)p;
-    return reinterpret_cast<W *>(a ^ (((a >> 7) & 7u) << 4));
-}
+// inside each 128-byte block of shared memory XOR the block index (mod 8),
+// applied to the byte offset from the 128-byte aligned dynamic smem base,
+// so it needs no row structure: the residue layouts use it.
+__device__ __forceinline__ uint32_t swz_off(uint32_t a) { return a ^ (((a >> 7) & 7u) << 4); }
 
-// Shared-memory slot of logical element offset s: plain, row-chunk-swizzled
-// (d.swz: 16-byte chunks XOR-permuted by row inside each 128-byte block) or
-// address-swizzled (kSwzAddr).
+// Shared-memory accesses are addressed by 32-bit BYTE offsets from the
+// 128-byte aligned dynamic smem base `smem`: pointers are formed as smem +
+// offset, so the compiler keeps their address space and emits LDS/STS with
+// 32-bit addresses and folded immediates (a swizzle applied to a generic
+// 64-bit pointer made every access a generic LD/ST with 64-bit arithmetic).
+//
+// Byte offset of logical element s of the stage buffer at byte offset bb:
+// plain, row-chunk-swizzled (d.swz: 16-byte chunks XOR-permuted by row inside
+// each 128-byte block) or address-swizzled (kSwzAddr).
 template <typename W>
-__device__ __forceinline__ W *sslot(const PhaseDesc &d, W *buf, uint32_t s) {
-    if (d.swz == kSwzAddr) return swz_addr(buf + s);
-    return d.swz ? buf + swizzle<16 / (int)sizeof(W)>(d, s) : buf + s;
+__device__ __forceinline__ uint32_t soff(const PhaseDesc &d, uint32_t bb, uint32_t s) {
+    if (d.swz == kSwzAddr) return swz_off(bb + s * (uint32_t)sizeof(W));
+    return d.swz ? bb + swizzle<16 / (int)sizeof(W)>(d, s) * (uint32_t)sizeof(W) : bb + s * (uint32_t)sizeof(W);
 }
 template <typename W>
-__device__ __forceinline__ const W *sslot(const PhaseDesc &d, const W *buf, uint32_t s) {
-    if (d.swz == kSwzAddr) return swz_addr(buf + s);
-    return d.swz ? buf + swizzle<16 / (int)sizeof(W)>(d, s) : buf + s;
+__device__ __forceinline__ W *sptr(unsigned char *smem, uint32_t off) {
+    return reinterpret_cast<W *>(smem + off);
+}
+template <typename W>
+__device__ __forceinline__ const W *sptr(const unsigned char *smem, uint32_t off) {
+    return reinterpret_cast<const W *>(smem + off);
 }
 
 __device__ __forceinline__ bool slot_ok(uint32_t mask, uint32_t c0, uint32_t c1, uint32_t c2, const Lim &lim) {
@@ -216,17 +222,18 @@ __device__ __forceinline__ OuterEntry outer_entry(const PhaseDesc &d, const unsi
 #endif
 }
 
-// R phase: global (source order) -> smem.  ASYNC: cp.async (16-byte chunks
-// when d.vec > 1), else LDG+STS.
+// R phase: global (source order) -> smem (stage buffer at byte offset bb).
+// ASYNC: cp.async (16-byte chunks when d.vec > 1), else LDG+STS.
 template <typename W, bool ASYNC, bool VEC>
-__device__ __forceinline__ void tile_read_impl(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
-                                               const W *__restrict__ gsrc, W *buf, uint32_t mask,
+__device__ __forceinline__ void tile_read_impl(const PhaseDesc &d, const ThreadPart &t, unsigned char *smem,
+                                               const W *__restrict__ gsrc, uint32_t bb, uint32_t mask,
                                                const Lim lim) {
     constexpr int U = 4;
     constexpr int CP = VEC ? 16 : (int)sizeof(W);
     const uint32_t n_in = d.n_in;
     const int64_t g_in = d.g_in;
     const uint32_t s_in = d.s_in;
+    const uint32_t sbase = smem_u32(smem);
     const uint32_t o0 = d.ngroups == 1 ? 0u : t.grp;   // constant in JIT builds
     VPG_UNROLL
     for (uint32_t o = o0; o < d.n_outer; o += d.ngroups) {
@@ -239,20 +246,20 @@ __device__ __forceinline__ void tile_read_impl(const PhaseDesc &d, const ThreadP
             for (; i + U <= n_in; i += U) {
                 if constexpr (ASYNC) {
 #pragma unroll
-                    for (int u = 0; u < U; ++u) cp_async<CP>(sslot(d, buf, so + u * s_in), gp + u * g_in);
+                    for (int u = 0; u < U; ++u) cp_async<CP>(sbase + soff<W>(d, bb, so + u * s_in), gp + u * g_in);
                 } else {
                     W v[U];
 #pragma unroll
                     for (int u = 0; u < U; ++u) v[u] = __ldg(gp + u * g_in);
 #pragma unroll
-                    for (int u = 0; u < U; ++u) *sslot(d, buf, so + u * s_in) = v[u];
+                    for (int u = 0; u < U; ++u) *sptr<W>(smem, soff<W>(d, bb, so + u * s_in)) = v[u];
                 }
                 gp += U * g_in;
                 so += U * s_in;
             }
             for (; i < n_in; ++i) {
-                if constexpr (ASYNC) cp_async<CP>(sslot(d, buf, so), gp);
-                else *sslot(d, buf, so) = __ldg(gp);
+                if constexpr (ASYNC) cp_async<CP>(sbase + soff<W>(d, bb, so), gp);
+                else *sptr<W>(smem, soff<W>(d, bb, so)) = __ldg(gp);
                 gp += g_in;
                 so += s_in;
             }
@@ -261,8 +268,8 @@ __device__ __forceinline__ void tile_read_impl(const PhaseDesc &d, const ThreadP
             VPG_UNROLL
             for (uint32_t i = 0; i < n_in; ++i) {
                 if (slot_ok(mask, c0, c1, c2, lim)) {
-                    if constexpr (ASYNC) cp_async<CP>(sslot(d, buf, so), gp);
-                    else *sslot(d, buf, so) = __ldg(gp);
+                    if constexpr (ASYNC) cp_async<CP>(sbase + soff<W>(d, bb, so), gp);
+                    else *sptr<W>(smem, soff<W>(d, bb, so)) = __ldg(gp);
                 }
                 gp += g_in;
                 so += s_in;
@@ -274,46 +281,58 @@ __device__ __forceinline__ void tile_read_impl(const PhaseDesc &d, const ThreadP
     }
 }
 
+// Byte offset of the 16-byte smem chunk that receives the aligned chunk of
+// source run element s (misaligned runs).  Residue mode (rshift 2): s's own
+// slot is congruent to its global address modulo 16 bytes, so the chunk goes
+// to the aligned-down slot; chunk-aligned rows (rshift 1): s is the chunk's
+// first slot.
+template <typename W>
+__device__ __forceinline__ uint32_t shift_chunk_off(const PhaseDesc &d, uint32_t bb, uint32_t s) {
+    constexpr int V = 16 / (int)sizeof(W);
+    if (d.rshift == 2) {
+        const uint32_t a = (bb + s * (uint32_t)sizeof(W)) & ~15u;
+        return d.swz == kSwzAddr ? swz_off(a) : a;
+    }
+    return d.swz ? bb + swizzle<V>(d, s) * (uint32_t)sizeof(W) : bb + s * (uint32_t)sizeof(W);
+}
+
 // R phase for misaligned source runs: each run is read as the 16-byte
 // aligned superset that covers it (the address is rounded down per chunk),
 // so the run lands at offset h = (run start mod V) inside its smem row; the
-// W phase adds h back.  Chunks reaching past the end of the source buffer
-// fall back to element copies.
+// W phase adds h back (or, with residue strides, reads it in place).
+// Chunks reaching past the end of the source buffer fall back to element
+// copies.
 template <typename W>
-__device__ __forceinline__ void tile_read_shift(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
-                                                const W *__restrict__ gsrc, const W *gend, W *buf, uint32_t mask,
-                                                const Lim lim) {
+__device__ __forceinline__ void tile_read_shift(const PhaseDesc &d, const ThreadPart &t, unsigned char *smem,
+                                                const W *__restrict__ gsrc, const W *gend, uint32_t bb,
+                                                uint32_t mask, const Lim lim) {
     constexpr int V = 16 / (int)sizeof(W);
     const uint32_t n_in = d.n_in;
     const int64_t g_in = d.g_in;
     const uint32_t s_in = d.s_in;
+    const uint32_t sbase = smem_u32(smem);
     const uint32_t o0 = d.ngroups == 1 ? 0u : t.grp;
     VPG_UNROLL
     for (uint32_t o = o0; o < d.n_outer; o += d.ngroups) {
         const OuterEntry e = outer_entry(d, smem, o);
         const W *gp = gsrc + (t.g + e.g);
-        W *sp = buf + (t.s + e.s);
+        uint32_t so = t.s + e.s;
         uint32_t c0 = t.c0 + e.c0, c1 = t.c1 + e.c1, c2 = t.c2;
         VPG_UNROLL
         for (uint32_t i = 0; i < n_in; ++i) {
             if (mask == 0 || slot_ok(mask, c0, c1, c2, lim)) {
                 const W *ga = reinterpret_cast<const W *>((uintptr_t)gp & ~(uintptr_t)15);
-                // chunk-aligned: whole chunk moves.  Residue mode: sp is the
-                // run element's own (unaligned) smem slot, congruent to gp
-                // modulo 16 bytes; the chunk goes to its aligned-down slot
-                W *sd = d.rshift == 2 ? reinterpret_cast<W *>((uintptr_t)sp & ~(uintptr_t)15)
-                        : (d.swz ? buf + swizzle<V>(d, (uint32_t)(sp - buf)) : sp);
-                if (d.swz == kSwzAddr) sd = swz_addr(reinterpret_cast<W *>((uintptr_t)sp & ~(uintptr_t)15));
+                const uint32_t sd = sbase + shift_chunk_off<W>(d, bb, so);
                 if (ga + V <= gend) {
                     cp_async<16>(sd, ga);
                 } else {
 #pragma unroll
                     for (int j = 0; j < V; ++j)
-                        if (ga + j < gend) cp_async<sizeof(W)>(sd + j, ga + j);
+                        if (ga + j < gend) cp_async<sizeof(W)>(sd + j * (uint32_t)sizeof(W), ga + j);
                 }
             }
             gp += g_in;
-            sp += s_in;
+            so += s_in;
             c0 += d.c_in[0];
             c1 += d.c_in[1];
             c2 += d.c_in[2];
@@ -322,23 +341,23 @@ __device__ __forceinline__ void tile_read_shift(const PhaseDesc &d, const Thread
 }
 
 template <typename W, bool ASYNC>
-__device__ __forceinline__ void tile_read(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
-                                          const W *__restrict__ gsrc, const W *gend, W *buf, uint32_t mask,
+__device__ __forceinline__ void tile_read(const PhaseDesc &d, const ThreadPart &t, unsigned char *smem,
+                                          const W *__restrict__ gsrc, const W *gend, uint32_t bb, uint32_t mask,
                                           const Lim lim) {
     if (!t.active) return;
     if constexpr (ASYNC && (sizeof(W) == 4 || sizeof(W) == 8)) {
         if (d.rshift) {
-            tile_read_shift<W>(d, t, smem, gsrc, gend, buf, mask, lim);
+            tile_read_shift<W>(d, t, smem, gsrc, gend, bb, mask, lim);
             return;
         }
     }
     if constexpr (ASYNC && sizeof(W) < 16) {
         if (d.vec > 1) {
-            tile_read_impl<W, true, true>(d, t, smem, gsrc, buf, mask, lim);
+            tile_read_impl<W, true, true>(d, t, smem, gsrc, bb, mask, lim);
             return;
         }
     }
-    tile_read_impl<W, ASYNC, false>(d, t, smem, gsrc, buf, mask, lim);
+    tile_read_impl<W, ASYNC, false>(d, t, smem, gsrc, bb, mask, lim);
 }
 
 // W phase: smem -> global (destination order).  VEC: each position is a
@@ -349,11 +368,11 @@ __device__ __forceinline__ void tile_read(const PhaseDesc &d, const ThreadPart &
 // consecutive destination-innermost rows (one swizzle group, so one slot
 // computation), transposed in registers into V 16-byte stores.
 template <typename W>
-__device__ __forceinline__ void w2_block(W *gp, const W *sp, uint32_t vrow, int64_t vs) {
+__device__ __forceinline__ void w2_block(W *gp, const unsigned char *sp, uint32_t vrow_bytes, int64_t vs) {
     constexpr int V = 16 / (int)sizeof(W);
     uint4 v[V];
 #pragma unroll
-    for (int i = 0; i < V; ++i) v[i] = *reinterpret_cast<const uint4 *>(sp + i * vrow);
+    for (int i = 0; i < V; ++i) v[i] = *reinterpret_cast<const uint4 *>(sp + i * vrow_bytes);
 #pragma unroll
     for (int j = 0; j < V; ++j) {
         alignas(16) W o[V];
@@ -365,7 +384,7 @@ __device__ __forceinline__ void w2_block(W *gp, const W *sp, uint32_t vrow, int6
 
 template <typename W>
 __device__ __forceinline__ void tile_write_w2(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
-                                              W *__restrict__ gdst, const W *buf, uint32_t mask, const Lim lim) {
+                                              W *__restrict__ gdst, uint32_t bb, uint32_t mask, const Lim lim) {
     const uint32_t o0 = d.ngroups == 1 ? 0u : t.grp;
     VPG_UNROLL
     for (uint32_t o = o0; o < d.n_outer; o += d.ngroups) {
@@ -376,7 +395,8 @@ __device__ __forceinline__ void tile_write_w2(const PhaseDesc &d, const ThreadPa
         VPG_UNROLL
         for (uint32_t i = 0; i < d.n_in; ++i) {
             if (mask == 0 || slot_ok(mask, c0, c1, c2, lim))
-                w2_block<W>(gp + (int64_t)i * d.g_in, sslot(d, buf, sb + i * d.s_in), d.vrow, d.vstride);
+                w2_block<W>(gp + (int64_t)i * d.g_in, smem + soff<W>(d, bb, sb + i * d.s_in),
+                            d.vrow * (uint32_t)sizeof(W), d.vstride);
             c0 += d.c_in[0];
             c1 += d.c_in[1];
             c2 += d.c_in[2];
@@ -386,7 +406,7 @@ __device__ __forceinline__ void tile_write_w2(const PhaseDesc &d, const ThreadPa
 
 template <typename W, bool VEC>
 __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
-                                                W *__restrict__ gdst, const W *buf, uint32_t mask,
+                                                W *__restrict__ gdst, uint32_t bb, uint32_t mask,
                                                 const Lim lim, uint32_t hb, uint32_t hmask) {
     constexpr int U = VEC ? 2 : 4;
     constexpr int V = VEC ? 16 / (int)sizeof(W) : 1;
@@ -399,7 +419,7 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
     for (uint32_t o = o0; o < d.n_outer; o += d.ngroups) {
         const OuterEntry e = outer_entry(d, smem, o);
         W *gp = gdst + (t.g + e.g);
-        const W *sp = buf + (t.s + e.s);
+        uint32_t s = t.s + e.s;
         uint32_t hh = hb + t.h + e.h;          // shifted-run mode (hmask == 0 otherwise)
         const uint32_t h_in = d.h_in;
         if (mask == 0) {
@@ -409,8 +429,7 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
                 if constexpr (VEC) {
                     uint4 v[U];
 #pragma unroll
-                    for (int u = 0; u < U; ++u)
-                        v[u] = *reinterpret_cast<const uint4 *>(sslot(d, buf, (uint32_t)(sp - buf) + u * s_in));
+                    for (int u = 0; u < U; ++u) v[u] = *sptr<uint4>(smem, soff<W>(d, bb, s + u * s_in));
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         const W *w = reinterpret_cast<const W *>(&v[u]);
@@ -420,29 +439,26 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
                 } else {
                     W v[U];
 #pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const uint32_t so = (uint32_t)(sp - buf) + u * s_in + ((hh + u * h_in) & hmask);
-                        v[u] = *sslot(d, buf, so);
-                    }
+                    for (int u = 0; u < U; ++u)
+                        v[u] = *sptr<W>(smem, soff<W>(d, bb, s + u * s_in + ((hh + u * h_in) & hmask)));
 #pragma unroll
                     for (int u = 0; u < U; ++u) st_out(gp + u * g_in, v[u]);
                 }
                 gp += U * g_in;
-                sp += U * s_in;
+                s += U * s_in;
                 hh += U * h_in;
             }
             for (; i < n_in; ++i) {
                 if constexpr (VEC) {
-                    uint4 v = *reinterpret_cast<const uint4 *>(sslot(d, buf, (uint32_t)(sp - buf)));
+                    uint4 v = *sptr<uint4>(smem, soff<W>(d, bb, s));
                     const W *w = reinterpret_cast<const W *>(&v);
 #pragma unroll
                     for (int j = 0; j < V; ++j) st_out(gp + j * vs, w[j]);
                 } else {
-                    const uint32_t so = (uint32_t)(sp - buf) + (hh & hmask);
-                    *gp = *sslot(d, buf, so);
+                    *gp = *sptr<W>(smem, soff<W>(d, bb, s + (hh & hmask)));
                 }
                 gp += g_in;
-                sp += s_in;
+                s += s_in;
                 hh += h_in;
             }
         } else {
@@ -451,17 +467,16 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
             for (uint32_t i = 0; i < n_in; ++i) {
                 if (slot_ok(mask, c0, c1, c2, lim)) {
                     if constexpr (VEC) {
-                        uint4 v = *reinterpret_cast<const uint4 *>(sslot(d, buf, (uint32_t)(sp - buf)));
+                        uint4 v = *sptr<uint4>(smem, soff<W>(d, bb, s));
                         const W *w = reinterpret_cast<const W *>(&v);
 #pragma unroll
                         for (int j = 0; j < V; ++j) st_out(gp + j * vs, w[j]);
                     } else {
-                        const uint32_t so = (uint32_t)(sp - buf) + (hh & hmask);
-                        *gp = *sslot(d, buf, so);
+                        *gp = *sptr<W>(smem, soff<W>(d, bb, s + (hh & hmask)));
                     }
                 }
                 gp += g_in;
-                sp += s_in;
+                s += s_in;
                 hh += h_in;
                 c0 += d.c_in[0];
                 c1 += d.c_in[1];
@@ -473,20 +488,20 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
 
 template <typename W>
 __device__ __forceinline__ void tile_write(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
-                                           W *__restrict__ gdst, const W *buf, uint32_t mask,
+                                           W *__restrict__ gdst, uint32_t bb, uint32_t mask,
                                            const Lim lim, uint32_t hb, uint32_t hmask) {
     if (!t.active) return;
     if constexpr (sizeof(W) == 4 || sizeof(W) == 8) {
         if (d.w2) {
-            tile_write_w2<W>(d, t, smem, gdst, buf, mask, lim);
+            tile_write_w2<W>(d, t, smem, gdst, bb, mask, lim);
             return;
         }
         if (d.vec > 1) {
-            tile_write_impl<W, true>(d, t, smem, gdst, buf, mask, lim, 0, 0);
+            tile_write_impl<W, true>(d, t, smem, gdst, bb, mask, lim, 0, 0);
             return;
         }
     }
-    tile_write_impl<W, false>(d, t, smem, gdst, buf, mask, lim, hb, hmask);
+    tile_write_impl<W, false>(d, t, smem, gdst, bb, mask, lim, hb, hmask);
 }
 
 // Warp 0 decodes tile `t` into slot `k`: source/destination base offsets and
@@ -541,6 +556,42 @@ __device__ __forceinline__ void decode_tile(const TileParams &p, const ShardArgs
     }
 }
 
+#ifdef VPG_JIT
+// Specialised kernels: ONE thread decodes tile t completely.  Every digit's
+// divisors and strides are immediates and the digits are independent, so
+// this is a short branch-free sequence; the prologue's S tiles are decoded
+// by S threads in parallel and no shuffles (or warp-collective fallbacks)
+// are needed.
+__device__ __forceinline__ void decode_tile_thread(const TileParams &p, const ShardArgs &sa, uint32_t t,
+                                                   int64_t (*s_base)[2], uint32_t (*s_valid)[2], int k) {
+    t += p.tile_begin;
+    int64_t sb = 0, db = 0;
+    uint32_t va = p.e_a, vc = p.e_c;
+    VPG_UNROLL
+    for (int i = 0; i < kMaxRank; ++i) {
+        if (i >= p.ngrid) break;
+        const GridDigit &gd = p.grid[i];
+        const uint32_t q = fdiv(t, gd.cum);
+        const uint32_t c = q - fdiv(q, gd.ext) * gd.ext.d;
+        sb += (int64_t)c * gd.src_stride;
+        db += (int64_t)c * gd.dst_stride;
+        if (i == p.grid_a) va = min(p.e_a, p.d_a - c * p.e_a);
+        if (i == p.grid_c) vc = min(p.e_c, p.d_c - c * p.e_c);
+    }
+    if (p.nshards > 1 && p.pull) {
+        db -= p.dst_bias;
+    } else if (p.nshards > 1) {
+        const uint64_t q = (uint64_t)db / (uint64_t)p.shard_elems;
+        sb -= p.src_bias;
+        db += sa.off[q] - (int64_t)q * p.shard_elems;
+    }
+    s_base[k][0] = sb;
+    s_base[k][1] = db;
+    s_valid[k][0] = va;
+    s_valid[k][1] = vc;
+}
+#endif
+
 // ------------------------------------------------------------------ pull exchange
 // Source word at GLOBAL offset o of a pull exchange plan: input shard
 // q = o / shard_elems, read through the per-launch shard table (peer memory
@@ -562,10 +613,11 @@ __device__ __forceinline__ const W *pull_ptr(const TileParams &p, const ShardArg
 // 16-byte aligned shard buffers for the vectorised variants).
 template <typename W, bool ASYNC>
 __device__ __forceinline__ void tile_read_pull(const TileParams &p, const ShardArgs &sa, const PhaseDesc &d,
-                                               const ThreadPart &t, const unsigned char *smem, const W *src,
-                                               int64_t sbase, W *buf, uint32_t mask, const Lim lim) {
+                                               const ThreadPart &t, unsigned char *smem, const W *src,
+                                               int64_t sbase, uint32_t bb, uint32_t mask, const Lim lim) {
     if (!t.active) return;
     constexpr int V = 16 / (int)sizeof(W);
+    const uint32_t sb32 = smem_u32(smem);
     const uint32_t o0 = d.ngroups == 1 ? 0u : t.grp;
     VPG_UNROLL
     for (uint32_t o = o0; o < d.n_outer; o += d.ngroups) {
@@ -576,21 +628,19 @@ __device__ __forceinline__ void tile_read_pull(const TileParams &p, const ShardA
         VPG_UNROLL
         for (uint32_t i = 0; i < d.n_in; ++i) {
             if (mask == 0 || slot_ok(mask, c0, c1, c2, lim)) {
-                W *sp = sslot(d, buf, so);
+                const uint32_t sp = soff<W>(d, bb, so);
                 if constexpr (ASYNC && sizeof(W) < 16) {
                     if (d.rshift) {
-                        W *sd = d.rshift == 2 ? reinterpret_cast<W *>((uintptr_t)(buf + so) & ~(uintptr_t)15) : buf + so;
-                        if (d.swz == kSwzAddr) sd = swz_addr(sd);
-                        cp_async<16>(sd, pull_ptr(p, sa, src, go & ~(int64_t)(V - 1)));
+                        cp_async<16>(sb32 + shift_chunk_off<W>(d, bb, so), pull_ptr(p, sa, src, go & ~(int64_t)(V - 1)));
                     } else if (d.vec > 1) {
-                        cp_async<16>(sp, pull_ptr(p, sa, src, go));
+                        cp_async<16>(sb32 + sp, pull_ptr(p, sa, src, go));
                     } else {
-                        cp_async<sizeof(W)>(sp, pull_ptr(p, sa, src, go));
+                        cp_async<sizeof(W)>(sb32 + sp, pull_ptr(p, sa, src, go));
                     }
                 } else if constexpr (ASYNC) {
-                    cp_async<16>(sp, pull_ptr(p, sa, src, go));
+                    cp_async<16>(sb32 + sp, pull_ptr(p, sa, src, go));
                 } else {
-                    *sp = __ldg(pull_ptr(p, sa, src, go));
+                    *sptr<W>(smem, sp) = __ldg(pull_ptr(p, sa, src, go));
                 }
             }
             go += d.g_in;
@@ -642,11 +692,42 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
     unsigned char *const smem = smem_raw + ((128u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 127u)) & 127u);
     const uint32_t tid = threadIdx.x, NT = blockDim.x;
     const uint32_t first = blockIdx.x, step = gridDim.x;
+    // (no static tile implies S * gridDim.x >= num_tiles: no dynamic claims either)
     if (first >= p.num_tiles) return;
-    const uint32_t cnt = (p.num_tiles - first + step - 1) / step;   // tiles of this CTA
     const uint32_t S = ASYNC ? p.nbuf : 1u;
     const uint32_t R = S + 2;
     pdl_trigger();
+
+    // Tile schedule.  The first S tiles of a CTA are static (blockIdx.x +
+    // j * gridDim.x, the prologue); later ones come from the dynamic
+    // scheduler when the launch carries one (sa.sched): tile S * gridDim.x +
+    // atomicAdd(next), so SMs that drain faster take more tiles (ncu on cfg5
+    // with a static round-robin: SM active cycles 0.58-0.99 of the elapsed
+    // ones).  Without it, tile first + j * gridDim.x.  One fetcher (thread
+    // NT-1 in specialised kernels, warp 0 otherwise) claims and decodes the
+    // tile of slot k+S during iteration k; the claim for the following one is
+    // issued one iteration ahead, so its latency overlaps a W phase.
+    __shared__ uint32_t s_ok[kRing];
+    // (a grid whose prologue covers every tile claims nothing: no atomics)
+    const bool dyn = sa.sched != nullptr && S * step < p.num_tiles;
+    const uint32_t dyn_base = S * step;
+    uint32_t pre = 0;        // fetcher: prefetched claim
+    bool fetch_done = false; // fetcher: the counter ran past the last tile
+    auto signal_done = [&]() {
+        // the last CTA to finish claiming resets the pair for the ring's next use
+        __threadfence();
+        if (atomicAdd(sa.sched + 1, 1u) == gridDim.x - 1) {
+            atomicExch(sa.sched, 0u);
+            atomicExch(sa.sched + 1, 0u);
+        }
+    };
+#ifdef VPG_JIT
+    const bool fetcher = tid == NT - 1;
+#else
+    const bool fetcher = tid == 0;
+#endif
+    // the first claim goes out at entry: its latency overlaps the prologue
+    if (dyn && fetcher) pre = atomicAdd(sa.sched, 1u);
 
     // per-CTA outer tables of both phases (JIT builds decode entries inline)
 #ifndef VPG_JIT
@@ -679,12 +760,25 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
 #endif
     const ThreadPart tr = decode_thread(p.ph[0], tid);
     const ThreadPart tw = decode_thread(p.ph[1], tid);
-    W *const buf0 = reinterpret_cast<W *>(smem + p.off_buf);
     const W *const gend = src + p.n_elems;
-    const size_t bstride = ((size_t)p.tile_elems_alloc * sizeof(W) + 15) / 16 * 16 / sizeof(W);
+    // stage buffer k at byte offset p.off_buf + k * bstride from smem
+    const uint32_t bstride = ((uint32_t)p.tile_elems_alloc * (uint32_t)sizeof(W) + 15u) / 16u * 16u;
 
+#ifdef VPG_JIT
+    if (tid < S) {
+        const uint32_t t = first + tid * step;
+        const bool ok = t < p.num_tiles;
+        if (ok) decode_tile_thread(p, sa, t, s_base, s_valid, (int)tid);
+        s_ok[tid] = ok;
+    }
+#else
     if (tid < 32)
-        for (uint32_t j = 0; j < S && j < cnt; ++j) decode_tile(p, sa, first + j * step, s_base, s_valid, (int)j);
+        for (uint32_t j = 0; j < S; ++j) {
+            const uint32_t t = first + j * step;
+            if (t < p.num_tiles) decode_tile(p, sa, t, s_base, s_valid, (int)j);
+            if (tid == 0) s_ok[j] = t < p.num_tiles;
+        }
+#endif
     __syncthreads();
     auto limits = [&](uint32_t slot, int ph, Lim &lim) -> uint32_t {
         const uint32_t va = s_valid[slot][0], vc = s_valid[slot][1];
@@ -694,35 +788,78 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
         const bool full = (va == p.e_a) && (vc == p.e_c);
         return full ? p.ph[ph].mask_full : p.ph[ph].mask_ragged;
     };
-    auto load = [&](uint32_t k, W *b) {
+    // residue layouts: the tile sits at (source base mod rres) elements into its buffer
+    auto shifted = [&](uint32_t b, uint32_t slot) {
+        return b + (p.rres ? ((uint32_t)s_base[slot][0] & p.rres) * (uint32_t)sizeof(W) : 0u);
+    };
+    auto load = [&](uint32_t k, uint32_t b) {
         Lim lim;
         const uint32_t slot = k % R;
         const uint32_t m = limits(slot, 0, lim);
-        W *bt = b + (p.rres ? ((uint32_t)s_base[slot][0] & p.rres) : 0u);
+        const uint32_t bt = shifted(b, slot);
         if (p.pull) tile_read_pull<W, ASYNC>(p, sa, p.ph[0], tr, smem, src, s_base[slot][0], bt, m, lim);
         else tile_read<W, ASYNC>(p.ph[0], tr, smem, src + s_base[slot][0], gend, bt, m, lim);
     };
     pdl_wait();
     // prologue: fill every stage
     for (uint32_t j = 0; j < S; ++j) {
-        if (j < cnt) load(j, buf0 + j * bstride);
+        if (s_ok[j]) load(j, p.off_buf + j * bstride);
         if constexpr (ASYNC) cp_async_commit();
     }
-    for (uint32_t k = 0; k < cnt; ++k) {
-        if (tid < 32 && k + S < cnt) decode_tile(p, sa, first + (k + S) * step, s_base, s_valid, (int)((k + S) % R));
+    for (uint32_t k = 0;; ++k) {
+        // claim + decode the tile of slot k+S
+        {
+            const uint32_t nslot = (k + S) % R;
+#ifdef VPG_JIT
+            if (fetcher) {
+                uint32_t t = 0xffffffffu;
+                if (dyn) {
+                    if (!fetch_done) {
+                        t = dyn_base + pre;
+                        if (t < p.num_tiles) pre = atomicAdd(sa.sched, 1u);
+                        else { fetch_done = true; signal_done(); }
+                    }
+                } else {
+                    t = first + (k + S) * step;
+                }
+                const bool ok = t < p.num_tiles;
+                if (ok) decode_tile_thread(p, sa, t, s_base, s_valid, (int)nslot);
+                s_ok[nslot] = ok;
+            }
+#else
+            if (tid < 32) {
+                uint32_t t = 0xffffffffu;
+                if (tid == 0) {
+                    if (dyn) {
+                        if (!fetch_done) {
+                            t = dyn_base + pre;
+                            if (t < p.num_tiles) pre = atomicAdd(sa.sched, 1u);
+                            else { fetch_done = true; signal_done(); }
+                        }
+                    } else {
+                        t = first + (k + S) * step;
+                    }
+                }
+                t = __shfl_sync(0xffffffffu, t, 0);
+                const bool ok = t < p.num_tiles;
+                if (ok) decode_tile(p, sa, t, s_base, s_valid, (int)nslot);
+                if (tid == 0) s_ok[nslot] = ok;
+            }
+#endif
+        }
         if constexpr (ASYNC) cp_async_wait_pending(S - 1);
         __syncthreads();
-        W *b = buf0 + (k % S) * bstride;
+        if (!s_ok[k % R]) break;           // uniform: this CTA has no tile k
+        const uint32_t b = p.off_buf + (k % S) * bstride;
         {
             Lim lim;
             const uint32_t slot = k % R;
             const uint32_t m = limits(slot, 1, lim);
-            tile_write<W>(p.ph[1], tw, smem, dst + s_base[slot][1],
-                          b + (p.rres ? ((uint32_t)s_base[slot][0] & p.rres) : 0u), m, lim,
+            tile_write<W>(p.ph[1], tw, smem, dst + s_base[slot][1], shifted(b, slot), m, lim,
                           (uint32_t)s_base[slot][0], p.hmask);
         }
         __syncthreads();
-        if (k + S < cnt) load(k + S, b);
+        if (s_ok[(k + S) % R]) load(k + S, b);
         if constexpr (ASYNC) cp_async_commit();
     }
     // peer stores of a sharded plan: performed system-wide before the grid
@@ -741,8 +878,6 @@ namespace vpg {
 // arms the stage's `full` mbarrier with the expected byte count; the
 // consumer warps wait on it, run the W phase, and release the stage through
 // its `empty` mbarrier.  No CTA-wide barriers in the steady state.
-__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
@@ -827,6 +962,7 @@ __device__ __forceinline__ void tile_body_bulk(const TileParams &p, const W *__r
     __syncthreads();
     W *const buf0 = reinterpret_cast<W *>(smem + p.off_buf);
     const size_t bstride = ((size_t)p.tile_elems_alloc * sizeof(W) + 15) / 16 * 16 / sizeof(W);
+    const uint32_t bstride_b = (uint32_t)(bstride * sizeof(W));
 
     if (tid >= NC) {
         // ---------------- producer warp
@@ -888,7 +1024,7 @@ __device__ __forceinline__ void tile_body_bulk(const TileParams &p, const W *__r
         lim.l2 = p.lim_split[1];
         const bool full_tile = (va == p.e_a) && (vc == p.e_c);
         const uint32_t m = full_tile ? p.ph[1].mask_full : p.ph[1].mask_ragged;
-        tile_write<W>(p.ph[1], tw, smem, dst + s_base[st][1], buf0 + st * bstride, m, lim,
+        tile_write<W>(p.ph[1], tw, smem, dst + s_base[st][1], p.off_buf + st * bstride_b, m, lim,
                       (uint32_t)s_base[st][0], p.hmask);
         __syncwarp();
         if ((tid & 31) == 0) mbar_arrive(&empty[st]);

@@ -606,3 +606,42 @@ def test_rank_above_64_unit_dims_permute(cuda):
     want = x.view([shape[a] for a in keep]).permute(sq_axes).contiguous()
     assert list(y.shape) == [shape[a] for a in axes]
     assert torch.equal(y.reshape(-1), want.reshape(-1))
+
+
+def test_dynamic_tile_scheduler_reuse_and_streams(cuda):
+    """The dynamic tile scheduler's counter pairs (kernels.cu sched_slot) are
+    reset by each launch's last CTA and reused ring-wise: >4096 launches
+    (the ring wraps) of multi-wave tile and rows plans, interleaved over two
+    streams, all bit-exact."""
+    import torch
+
+    from paper_2506_03686_b200 import TensorLayout, build_program, from_numpy_convention
+    from paper_2506_03686_b200.api import execute_device
+
+    # (2048, 2048, 8) f32: 8192 tiles >> S x grid; (256, 64, 16, 1024): 4 KiB rows, TMA bulk rows kernel
+    cases = [((2048, 2048, 8), (1, 0, 2)), ((256, 64, 16, 1024), (2, 0, 1, 3))]
+    progs, xs, wants = [], [], []
+    for shape, axes in cases:
+        n = 1
+        for d in shape:
+            n *= d
+        x = torch.randint(-2**31, 2**31 - 1, (n,), dtype=torch.int32, device=cuda)
+        p = build_program(TensorLayout.from_shape(shape, 4), from_numpy_convention(axes))
+        progs.append(p)
+        xs.append(x)
+        wants.append(x.view(shape).permute(axes).contiguous().reshape(-1))
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [[torch.empty_like(x) for x in xs] for _ in streams]
+    assert [p.kernel for p in progs] == ["tile", "rows"]
+    for it in range(2100):
+        for si, st in enumerate(streams):
+            for ci in range(len(cases)):
+                execute_device(progs[ci], xs[ci], out=outs[si][ci], stream=st)
+        if it % 700 == 699:
+            torch.cuda.synchronize()
+            for si in range(len(streams)):
+                for ci in range(len(cases)):
+                    assert torch.equal(outs[si][ci], wants[ci]), (it, si, ci, progs[ci].kernel)
+                    with torch.cuda.stream(streams[si]):
+                        outs[si][ci].zero_()
+    torch.cuda.synchronize()
