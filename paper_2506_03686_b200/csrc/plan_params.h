@@ -200,6 +200,11 @@ struct TileParams {
     FastDiv shard_div;
     uint32_t pad_pull_;
     int64_t dst_bias;
+    // largest source offset of any element of a full tile relative to the
+    // tile's source base, + 1: a tile whose base + src_span + 16 bytes of
+    // elements stays inside the source needs no end-of-buffer check on its
+    // aligned-superset reads (shifted-run mode), so its R walk is branch-free
+    int64_t src_span;
 };
 static_assert(sizeof(TileParams) <= 4096, "kernel parameter block must stay under 4 KB");
 

@@ -329,6 +329,8 @@ struct VecChoice {
     bool rres = false;     // shifted-run mode with residue row strides (no per-element shift in W)
     bool sw128 = false;    // aligned runs: unpadded rows congruent to their source lines mod 128 B, chunk-swizzled
     bool w2 = false;       // (sw128 only) W in V x V register-transposed blocks with 16-byte stores
+    bool swz_addr = true;  // (128-byte residue layouts) address swizzle; off when the bank model prefers plain
+    bool res16 = false;    // residue modulus of one 16-byte chunk (TMA bulk reads of misaligned runs)
 };
 
 // smem strides of the tile dims for a given pitch (source run dense, run
@@ -750,7 +752,7 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
     int64_t sstr[kMaxRank];
     bool in_src[kMaxRank];
     const int V = 16 / Pb.E;
-    const int64_t M = res_modulus(Pb.E);
+    const int64_t M = vc.res16 ? V : res_modulus(Pb.E);
     if (vc.rres) tp.tile_elems_alloc = (uint32_t)tile_sstrides_res(Pb, g, pitch, V, sstr, in_src, M);
     else tile_sstrides(Pb, g, pitch, sstr, in_src);
     int slot_of_dim[kMaxRank];
@@ -770,7 +772,7 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
     tp.ph[0].rshift = vc.rshift ? (vc.rres ? 2u : 1u) : 0u;
     tp.hmask = (uint32_t)hmask;
     tp.rres = vc.rres ? (uint32_t)(M - 1) : 0u;
-    if (vc.rres && M * Pb.E >= 128 && !Pb.no_swz_addr)
+    if (vc.rres && M * Pb.E >= 128 && !Pb.no_swz_addr && vc.swz_addr)
         for (int ph = 0; ph < 2; ++ph) tp.ph[ph].swz = kSwzAddr;
     if ((vc.swz && vc.rshift && vc.vw == 1 && !vc.bulk) || (vc.sw128 && !vc.bulk)) {
         // congruent layout: XOR by row (W lanes walk rows), or by row group
@@ -856,6 +858,9 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
             tp.n_elems = tp.shard_elems;  // source bounds: the local shard
         }
     }
+    tp.src_span = 1;
+    for (int k = 0; k < r; ++k)
+        if (g.ext[k] > 0) tp.src_span += (g.ext[k] - 1) * Pb.in_stride[k];
     tp.e_a = g.a_part >= 0 ? (uint32_t)g.ext[g.a_part] : 1u;
     tp.d_a = g.a_part >= 0 ? (uint32_t)Pb.d[g.a_part] : 1u;
     bool c_slot = g.c_part >= 0 && g.c_part != g.a_part;
@@ -1005,6 +1010,43 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
             // residue row strides: pitch candidates NCK*V + pad (rounded up to
             // the first run-index dim's residue inside tile_sstrides_res)
             const int64_t base = (g.Ls + V - 1 + V - 1) / V * V;
+            for (int pad = 0; pad <= 32 * 2 + 1; ++pad) {
+                // odd/even pad index: address swizzle on/off (the bank model
+                // decides; with 128-byte residues the W lanes' banks are set
+                // by the source strides and the swizzle can add conflicts)
+                const uint32_t pitch = (uint32_t)(base + pad / 2);
+                if ((int64_t)(g.T / g.Ls) * pitch * Pb.E > Pb.budget + 8192) break;
+                TileParams tp;
+                VecChoice vc;
+                vc.vr = op.vr;
+                vc.vw = op.vw;
+                vc.rshift = true;
+                vc.rres = true;
+                vc.swz_addr = (pad & 1) == 0;
+                fill_tile_params(Pb, g, pitch, NT, vc, tp);
+                // no per-element shift arithmetic in W: cheaper per element
+                double c = tile_cost(Pb, tp) * kResidueCostFactor *
+                           (res_modulus(Pb.E) * Pb.E >= 128 ? kSw128CostFactor : 1.0);   // 128-byte congruence
+                if (getenv("VPG_DEBUG_PLAN"))
+                    fprintf(stderr, "[plan] Ls %lld Ld %lld pitch %u residue swz %d cost %.1f per-elem %.3f\n",
+                            (long long)g.Ls, (long long)g.Ld, pitch, (int)vc.swz_addr, c, c / (double)g.T);
+                if (best < 0 || c < best - 1e-9) {
+                    best = c;
+                    pitch_out = pitch;
+                    vc_out = vc;
+                }
+            }
+        }
+        if (op.rshift && Pb.force_bulk && !Pb.no_bulk && g.n_runidx <= kMaxPhaseDims) {
+            // TMA bulk reads of misaligned runs: one cp.async.bulk per run's
+            // 16-byte aligned superset (producer warp, tile_body_bulk) into
+            // rows with 16-byte residue strides.  The bulk engine keeps L2
+            // requests at one per sector whatever the smem offset (per-lane
+            // cp.async into rows not congruent mod 128 B requests them ~2x),
+            // so the strides are free modulo 128 B: the pitch is chosen for
+            // the W lanes' banks.  Experimental (VPG_BULK=1).
+            const int64_t base = (g.Ls + V - 1 + V - 1) / V * V;
+            double bb = -1.0;
             for (int pad = 0; pad <= 32; ++pad) {
                 const uint32_t pitch = (uint32_t)(base + pad);
                 if ((int64_t)(g.T / g.Ls) * pitch * Pb.E > Pb.budget + 8192) break;
@@ -1014,19 +1056,22 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
                 vc.vw = op.vw;
                 vc.rshift = true;
                 vc.rres = true;
+                vc.res16 = true;
+                vc.swz_addr = false;
+                vc.bulk = true;
                 fill_tile_params(Pb, g, pitch, NT, vc, tp);
-                // no per-element shift arithmetic in W: cheaper per element
-                double c = tile_cost(Pb, tp) * kResidueCostFactor *
-                           (res_modulus(Pb.E) * Pb.E >= 128 ? kSw128CostFactor : 1.0);   // 128-byte congruence
+                const double c = tile_cost(Pb, tp);
                 if (getenv("VPG_DEBUG_PLAN"))
-                    fprintf(stderr, "[plan] Ls %lld Ld %lld pitch %u residue cost %.1f per-elem %.3f\n",
+                    fprintf(stderr, "[plan] Ls %lld Ld %lld pitch %u bulk-residue cost %.1f per-elem %.3f\n",
                             (long long)g.Ls, (long long)g.Ld, pitch, c, c / (double)g.T);
-                if (best < 0 || c < best - 1e-9) {
-                    best = c;
+                if (bb < 0 || c < bb - 1e-9) {
+                    bb = c;
                     pitch_out = pitch;
                     vc_out = vc;
+                    best = 0.0;     // forced: wins over every per-lane option
                 }
             }
+            return;
         }
         const int step = (op.vr > 1 || op.vw > 1) ? V : 1;
         const int64_t base = op.rshift ? (g.Ls + V - 1 + V - 1) / V * V : g.Ls;
@@ -1245,7 +1290,10 @@ static void describe(vpg_plan *p) {
         if (t.ph[0].swz == kSwzAddr) put("smem address swizzle: 16-byte chunk ^= 128-byte block index\n");
         else if (t.ph[0].swz) put("smem chunk swizzle: row >> %u\n", t.ph[0].swz - 1);
         put("vector elems: R %u%s, W %u%s\n", t.ph[0].vec,
-            t.bulk ? " (TMA bulk copy per source run, producer warp)"
+            t.bulk ? (t.ph[0].rshift == 2
+                          ? " (TMA bulk copy per source run: aligned supersets of misaligned runs, 16-byte residue "
+                            "row strides, producer warp)"
+                          : " (TMA bulk copy per source run, producer warp)")
                    : (t.ph[0].rshift == 2 ? " (aligned supersets of misaligned runs, residue row strides)"
                                        : t.ph[0].rshift ? " (aligned supersets of misaligned runs)" : ""),
             t.ph[1].vec, t.ph[1].w2 ? " (VxV register-transposed blocks, 16-byte stores)" : "");
@@ -1342,6 +1390,7 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
     }
     Problem P;
     P.E = E;
+    bool small_problem = false;
     // development knobs (documented in DESIGN.md): override the tiling policy
     P.budget = kTileBudgetBytes;
     P.nbuf = 0;
@@ -1357,6 +1406,7 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         if ((double)nel * E * 2.0 < kSmallProblemBytes) {
             P.budget = 24 * 1024;
             P.cta_smem = 75 * 1024;
+            small_problem = true;
         }
     }
     int persist_mode = -1;  // -1 auto, 0 one tile per CTA, 1 persistent
@@ -1515,6 +1565,30 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         uint32_t pitch;
         VecChoice vc;
         choose_pitch_vec(P, g, threads, pitch, vc);
+        // small problems with misaligned source runs: their residue rows pad
+        // a tile by up to a third, so they stage with the 32 KiB budget (cfg3:
+        // 81 x 75 -> 54 x 270-element runs, flushed 18.65 -> 18.03 us mean,
+        // steady 15.25 -> 14.58 us; aligned cfg1/cfg2 keep 24 KiB: cfg2 12.6
+        // vs 13.0 us with 32 KiB; tools/sweep_budget.py)
+        if (vc.rshift && small_problem && pick < 0 && !getenv("VPG_TILE_BUDGET")) {
+            Problem P2 = P;
+            P2.budget = 32 * 1024;
+            TileGeom g2;
+            if (select_tile(P2, g2, -1)) {
+                const int t2 = g2.T >= 1024 ? kTileThreads : (g2.T >= 256 ? 128 : 64);
+                uint32_t pitch2;
+                VecChoice vc2;
+                choose_pitch_vec(P2, g2, force_threads >= 32 && force_threads <= 1024 ? force_threads / 32 * 32 : t2,
+                                 pitch2, vc2);
+                if (vc2.rshift) {
+                    P = P2;
+                    g = g2;
+                    threads = force_threads >= 32 && force_threads <= 1024 ? force_threads / 32 * 32 : t2;
+                    pitch = pitch2;
+                    vc = vc2;
+                }
+            }
+        }
         // optionally the vectorised R phase runs as TMA bulk copies, one per
         // source run (16-byte aligned runs of whole 16-byte chunks; VPG_BULK=1)
         // TMA bulk copies (one cp.async.bulk per source run, producer warp +
@@ -1536,7 +1610,7 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         // blocks) beats bulk reads into padded rows where it applies (cfg5:
         // 690 vs 708 us flushed, 703 vs 729 us steady); bulk covers the long
         // runs it cannot take (not a power of two, or not 128-byte aligned)
-        vc.bulk = !vc.sw128 && bulk_for(vc);
+        vc.bulk = (vc.bulk && vc.rshift) || (!vc.sw128 && bulk_for(vc));
         p->tile_util = fill_tile_params(P, g, pitch, threads, vc, p->tile);
         // variant without 16-byte source reads, for misaligned base pointers
         VecChoice vs = vc;

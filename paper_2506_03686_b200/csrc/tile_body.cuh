@@ -302,7 +302,7 @@ __device__ __forceinline__ uint32_t shift_chunk_off(const PhaseDesc &d, uint32_t
 // W phase adds h back (or, with residue strides, reads it in place).
 // Chunks reaching past the end of the source buffer fall back to element
 // copies.
-template <typename W>
+template <typename W, bool CHECK_END>
 __device__ __forceinline__ void tile_read_shift(const PhaseDesc &d, const ThreadPart &t, unsigned char *smem,
                                                 const W *__restrict__ gsrc, const W *gend, uint32_t bb,
                                                 uint32_t mask, const Lim lim) {
@@ -323,7 +323,7 @@ __device__ __forceinline__ void tile_read_shift(const PhaseDesc &d, const Thread
             if (mask == 0 || slot_ok(mask, c0, c1, c2, lim)) {
                 const W *ga = reinterpret_cast<const W *>((uintptr_t)gp & ~(uintptr_t)15);
                 const uint32_t sd = sbase + shift_chunk_off<W>(d, bb, so);
-                if (ga + V <= gend) {
+                if (!CHECK_END || ga + V <= gend) {
                     cp_async<16>(sd, ga);
                 } else {
 #pragma unroll
@@ -343,11 +343,14 @@ __device__ __forceinline__ void tile_read_shift(const PhaseDesc &d, const Thread
 template <typename W, bool ASYNC>
 __device__ __forceinline__ void tile_read(const PhaseDesc &d, const ThreadPart &t, unsigned char *smem,
                                           const W *__restrict__ gsrc, const W *gend, uint32_t bb, uint32_t mask,
-                                          const Lim lim) {
+                                          const Lim lim, bool near_end) {
     if (!t.active) return;
     if constexpr (ASYNC && (sizeof(W) == 4 || sizeof(W) == 8)) {
         if (d.rshift) {
-            tile_read_shift<W>(d, t, smem, gsrc, gend, bb, mask, lim);
+            // tiles clear of the buffer end read every chunk unchecked
+            // (straight-line cp.async sequences; the rare tile at the end checks)
+            if (near_end) tile_read_shift<W, true>(d, t, smem, gsrc, gend, bb, mask, lim);
+            else tile_read_shift<W, false>(d, t, smem, gsrc, gend, bb, mask, lim);
             return;
         }
     }
@@ -798,7 +801,9 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
         const uint32_t m = limits(slot, 0, lim);
         const uint32_t bt = shifted(b, slot);
         if (p.pull) tile_read_pull<W, ASYNC>(p, sa, p.ph[0], tr, smem, src, s_base[slot][0], bt, m, lim);
-        else tile_read<W, ASYNC>(p.ph[0], tr, smem, src + s_base[slot][0], gend, bt, m, lim);
+        else
+            tile_read<W, ASYNC>(p.ph[0], tr, smem, src + s_base[slot][0], gend, bt, m, lim,
+                                s_base[slot][0] + p.src_span + 16 / (int64_t)sizeof(W) > p.n_elems);
     };
     pdl_wait();
     // prologue: fill every stage
@@ -960,41 +965,32 @@ __device__ __forceinline__ void tile_body_bulk(const TileParams &p, const W *__r
     }
     pdl_wait();
     __syncthreads();
-    W *const buf0 = reinterpret_cast<W *>(smem + p.off_buf);
     const size_t bstride = ((size_t)p.tile_elems_alloc * sizeof(W) + 15) / 16 * 16 / sizeof(W);
     const uint32_t bstride_b = (uint32_t)(bstride * sizeof(W));
 
     if (tid >= NC) {
         // ---------------- producer warp
         const uint32_t lane = tid - NC;
+        constexpr int V = 16 / (int)sizeof(W);
+        // misaligned runs (residue rows, rshift 2): each run is fetched as its
+        // 16-byte aligned superset; the part of a run in the last, partial
+        // 16-byte chunk of the source buffer is copied by its lane instead
+        const bool mis = p.ph[0].rshift == 2;
         for (uint32_t k = 0; k < cnt; ++k) {
             const uint32_t st = k % S;
             if (k >= S) mbar_wait(&empty[st], ((k / S) - 1) & 1);
+#ifdef VPG_JIT
+            if (lane == 0) decode_tile_thread(p, sa, first + k * step, s_base, s_valid, (int)st);
+#else
             decode_tile(p, sa, first + k * step, s_base, s_valid, (int)st);
+#endif
             __syncwarp();
             const int64_t sb = s_base[st][0];
             const uint32_t va = s_valid[st][0], vc = s_valid[st][1];
             const uint32_t rbytes = va == p.e_a ? p.run_bytes : p.run_unit_bytes * va;
-            W *b = buf0 + st * bstride;
-            // valid runs of this lane and the total byte count of the stage
-            uint32_t mine = 0;
-            for (uint32_t r = lane; r < p.nruns; r += 32) {
-                uint32_t idx = r, cc = 0;
-                VPG_UNROLL
-                for (int i = 0; i < kMaxPhaseDims; ++i) {
-                    if (i >= p.nrdims) break;
-                    const uint32_t q = fdiv(idx, p.rdims[i].div);
-                    const uint32_t c = idx - q * p.rdims[i].div.d;
-                    idx = q;
-                    if (p.rdims[i].slot == 1) cc = c;
-                }
-                if (p.grid_c < 0 || cc < vc) mine += rbytes;
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
-            if (lane == 0) mbar_arrive_expect_tx(&full[st], mine);
-            __syncwarp();
-            for (uint32_t r = lane; r < p.nruns; r += 32) {
+            const uint32_t bb = p.off_buf + st * bstride_b + (mis ? ((uint32_t)sb & p.rres) * (uint32_t)sizeof(W) : 0u);
+            // run r of this tile: global element offset, smem byte offset, valid
+            auto run = [&](uint32_t r, int64_t &g0, uint32_t &so) -> bool {
                 uint32_t idx = r, cc = 0, soff = 0;
                 int64_t goff = 0;
                 VPG_UNROLL
@@ -1007,7 +1003,56 @@ __device__ __forceinline__ void tile_body_bulk(const TileParams &p, const W *__r
                     soff += c * p.rdims[i].sstride;
                     if (p.rdims[i].slot == 1) cc = c;
                 }
-                if (p.grid_c < 0 || cc < vc) bulk_g2s(b + soff, src + sb + goff, rbytes, &full[st]);
+                g0 = sb + goff;
+                so = bb + soff * (uint32_t)sizeof(W);
+                return p.grid_c < 0 || cc < vc;
+            };
+            // aligned superset [ga, ge) of a misaligned run (ge clipped to the
+            // last whole chunk of the source buffer)
+            auto span = [&](int64_t g0, int64_t &ga, int64_t &ge) {
+                const int64_t len = rbytes / (uint32_t)sizeof(W);
+                ga = g0 & ~(int64_t)(V - 1);
+                ge = (g0 + len + V - 1) & ~(int64_t)(V - 1);
+                if (ge > p.n_elems) ge = p.n_elems & ~(int64_t)(V - 1);
+                if (ge < ga) ge = ga;
+            };
+            // valid runs of this lane and the total byte count of the stage
+            uint32_t mine = 0;
+            for (uint32_t r = lane; r < p.nruns; r += 32) {
+                int64_t g0;
+                uint32_t so;
+                if (!run(r, g0, so)) continue;
+                if (!mis) {
+                    mine += rbytes;
+                    continue;
+                }
+                int64_t ga, ge;
+                span(g0, ga, ge);
+                mine += (uint32_t)((ge - ga) * (int64_t)sizeof(W));
+                // elements past the last whole chunk: plain copies (ordered
+                // before the consumers by the warp barrier + the arrive below)
+                const int64_t gend_run = g0 + rbytes / (uint32_t)sizeof(W);
+                for (int64_t e = ge > g0 ? ge : g0; e < gend_run; ++e)
+                    *sptr<W>(smem, so + (uint32_t)((e - g0) * (int64_t)sizeof(W))) = src[e];
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+            __syncwarp();
+            if (lane == 0) mbar_arrive_expect_tx(&full[st], mine);
+            __syncwarp();
+            for (uint32_t r = lane; r < p.nruns; r += 32) {
+                int64_t g0;
+                uint32_t so;
+                if (!run(r, g0, so)) continue;
+                if (!mis) {
+                    bulk_g2s(smem + so, src + g0, rbytes, &full[st]);
+                    continue;
+                }
+                int64_t ga, ge;
+                span(g0, ga, ge);
+                if (ge > ga)
+                    bulk_g2s(smem + (so & ~15u), src + ga, (uint32_t)((ge - ga) * (int64_t)sizeof(W)),
+                             &full[st]);
             }
         }
         return;
@@ -1024,8 +1069,9 @@ __device__ __forceinline__ void tile_body_bulk(const TileParams &p, const W *__r
         lim.l2 = p.lim_split[1];
         const bool full_tile = (va == p.e_a) && (vc == p.e_c);
         const uint32_t m = full_tile ? p.ph[1].mask_full : p.ph[1].mask_ragged;
-        tile_write<W>(p.ph[1], tw, smem, dst + s_base[st][1], p.off_buf + st * bstride_b, m, lim,
-                      (uint32_t)s_base[st][0], p.hmask);
+        const uint32_t bb = p.off_buf + st * bstride_b +
+                            (p.ph[0].rshift == 2 ? ((uint32_t)s_base[st][0] & p.rres) * (uint32_t)sizeof(W) : 0u);
+        tile_write<W>(p.ph[1], tw, smem, dst + s_base[st][1], bb, m, lim, (uint32_t)s_base[st][0], p.hmask);
         __syncwarp();
         if ((tid & 31) == 0) mbar_arrive(&empty[st]);
     }

@@ -63,7 +63,7 @@ class TileParams(ctypes.Structure):
                 ("nshards", ctypes.c_uint32), ("tile_begin", ctypes.c_uint32), ("src_bias", ctypes.c_int64),
                 ("shard_elems", ctypes.c_int64), ("rres", ctypes.c_uint32), ("pull", ctypes.c_uint32),
                 ("shard_shift", ctypes.c_uint32), ("shard_div", FastDiv), ("pad_pull_", ctypes.c_uint32),
-                ("dst_bias", ctypes.c_int64)]
+                ("dst_bias", ctypes.c_int64), ("src_span", ctypes.c_int64)]
 
 
 def tile_params(program) -> TileParams:
@@ -186,16 +186,44 @@ def simulate(program, src_words: np.ndarray, threads: int | None = None, shard_o
         smem = np.zeros(alloc + 64, dtype=src_words.dtype)
         smem_valid = np.zeros(alloc + 64, dtype=bool)
         if tp.bulk:
-            # R as one bulk copy per source run (producer warp)
+            # R as one bulk copy per source run (producer warp); misaligned
+            # runs (rshift 2): the 16-byte aligned superset of each run into
+            # residue rows, the part in the buffer's last partial chunk copied
+            # element by element
             rbytes = tp.run_bytes if va == tp.e_a else tp.run_unit_bytes * va
-            if rbytes % 16 or tp.run_bytes % 16:
+            mis = tp.ph[0].rshift == 2
+            if not mis and (rbytes % 16 or tp.run_bytes % 16):
                 raise SimError("bulk copy size not a multiple of 16 bytes")
             nel = rbytes // E
+            V = 16 // E
+            claimed = np.zeros(alloc + 64, dtype=bool)      # superset rows of distinct runs must not overlap
             for r in range(tp.nruns):
                 g_, s_, c_, _ = _decode([r], tp.rdims, tp.nrdims)
                 if tp.grid_c >= 0 and c_[1][0] >= vc:
                     continue
-                ga, sa = sb + g_[0], s_[0]
+                ga, sa = sb + g_[0], s_[0] + tbase
+                if mis:
+                    g0 = ga
+                    ga = g0 - g0 % V
+                    ge = min(-(-(g0 + nel) // V) * V, n - n % V)
+                    ge = max(ge, ga)
+                    if (sa - (g0 - ga)) % V or sa % V != g0 % V:
+                        raise SimError("bulk residue: smem run start not congruent to its source mod 16 bytes")
+                    s0 = sa - (g0 - ga)
+                    hi = s0 + max(ge - ga, g0 + nel - ga)
+                    if claimed[s0:hi].any():
+                        raise SimError("bulk residue: aligned supersets of two runs overlap in smem")
+                    claimed[s0:hi] = True
+                    if ge > ga:
+                        _chk(np.array([ga, ge - 1]), n, "bulk global")
+                        _chk(np.array([s0, s0 + (ge - ga) - 1]), alloc, "bulk smem")
+                        smem[s0:s0 + ge - ga] = src_words[ga:ge]
+                        smem_valid[s0:s0 + ge - ga] = True
+                    for e in range(max(ge, g0), g0 + nel):
+                        _chk(np.array([e]), n, "bulk tail global")
+                        smem[sa + e - g0] = src_words[e]
+                        smem_valid[sa + e - g0] = True
+                    continue
                 if (ga * E) % 16 or (sa * E) % 16:
                     raise SimError("bulk copy address not 16-byte aligned")
                 _chk(np.array([ga, ga + nel - 1]), n, "bulk global")

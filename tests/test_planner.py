@@ -238,8 +238,10 @@ def test_baseline_layout_choices():
         assert t.ph[1].w2 == 1 and t.ph[1].vrow == t.pitch, k
         assert "smem chunk swizzle" in p.text and "16-byte stores" in p.text
     t, p = tp("cfg3")
-    # residue strides modulo 128 bytes (32 words) with the address swizzle
-    assert t.ph[0].rshift == 2 and t.rres == 31 and t.hmask == 0 and t.ph[0].swz == 16 and t.ph[1].swz == 16
+    # residue strides modulo 128 bytes (32 words); the bank model keeps them
+    # unswizzled (W lanes: 2.5 wavefronts per access plain, 4.0 with the
+    # address swizzle, whose XOR lands on the strides' own bank pattern)
+    assert t.ph[0].rshift == 2 and t.rres == 31 and t.hmask == 0 and t.ph[0].swz == 0 and t.ph[1].swz == 0
     t, p = tp("cfg5")
     # 2 KiB power-of-two runs: congruent layout + V x V blocks (bulk reads
     # remain for long runs that cannot take it)

@@ -71,8 +71,16 @@ def test_sim_bulk_mode(monkeypatch):
                            ((2,) * 12, (3, 9, 0, 7, 1, 5, 2, 11, 8, 6, 4, 10), 8), ((36, 10, 52), (2, 0, 1), 8)]:
         p = _run(shape, axes, E, rng)
         seen += "TMA bulk" in p.text
+    # misaligned runs: aligned supersets by bulk copy into 16-byte residue rows
+    mis = 0
+    for shape, axes, E in [((17, 9, 13, 15, 11, 27), (5, 2, 0, 4, 1, 3), 4), ((33, 45, 19), (2, 0, 1), 4),
+                           ((101, 67), (1, 0), 4), ((7, 9, 13, 5, 11), (4, 1, 0, 3, 2), 8),
+                           ((5, 3, 37, 41), (3, 0, 2, 1), 4), ((27, 31), (1, 0), 8)]:
+        p = _run(shape, axes, E, rng)
+        t = tile_params(p)
+        mis += t.bulk == 1 and t.ph[0].rshift == 2
     vp.program_cache_clear()
-    assert seen >= 3
+    assert seen >= 3 and mis >= 3, (seen, mis)
 
 
 # ------------------------------------------------------------ fused sharded exchange
