@@ -28,6 +28,7 @@
 #include <string>
 #include <tuple>
 #include <utility>
+#include <vector>
 
 #include "plan.h"
 #include "tile_body.cuh"
@@ -350,6 +351,39 @@ uint32_t *sched_slot(cudaStream_t st) {
     return base + 2 * (g_sched_seq.fetch_add(1, std::memory_order_relaxed) % kSchedSlots);
 }
 
+// Development tracing (VPG_TRACE=<file>): tile launches record per-CTA
+// globaltimer stamps (tile_body.cuh trc[]) into a device buffer; after each
+// launch the stream is synchronised and the records are appended to the
+// file (header: grid, num_tiles, kTraceWords; then grid x kTraceWords u64).
+// tools/trace_view.py summarises them.  Off (nullptr) unless VPG_TRACE is set.
+unsigned long long *g_trace_buf = nullptr;
+constexpr int64_t kTraceMaxCtas = 4096;
+
+unsigned long long *trace_begin(cudaStream_t st) {
+    static const char *path = getenv("VPG_TRACE");
+    if (!path || !*path) return nullptr;
+    if (!g_trace_buf && cudaMalloc(&g_trace_buf, kTraceMaxCtas * kTraceWords * 8) != cudaSuccess) {
+        g_trace_buf = nullptr;
+        return nullptr;
+    }
+    cudaMemsetAsync(g_trace_buf, 0, kTraceMaxCtas * kTraceWords * 8, st);
+    return g_trace_buf;
+}
+
+void trace_end(unsigned long long *buf, int64_t grid, uint32_t num_tiles, cudaStream_t st) {
+    if (!buf) return;
+    grid = std::min<int64_t>(grid, kTraceMaxCtas);
+    std::vector<unsigned long long> h((size_t)grid * kTraceWords);
+    cudaMemcpyAsync(h.data(), buf, h.size() * 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    if (FILE *f = fopen(getenv("VPG_TRACE"), "ab")) {
+        const unsigned long long hdr[3] = {(unsigned long long)grid, num_tiles, (unsigned long long)kTraceWords};
+        fwrite(hdr, 8, 3, f);
+        fwrite(h.data(), 8, h.size(), f);
+        fclose(f);
+    }
+}
+
 // Launches carry the programmatic stream-serialisation attribute (PDL, see
 // pdl_wait in tile_body.cuh) unless VPG_PDL=0 or the plan is sharded (the
 // exchange's barriers are collectives on the same stream).
@@ -431,6 +465,7 @@ vpg_status launch_tile(const vpg_plan *p, const void *src, void *dst, const Shar
     // dynamic tile schedule for persistent CTAs (not the bulk-read variant,
     // whose producer warp keeps the static order)
     sa.sched = p->tile.persistent && !p->tile.bulk ? sched_slot(st) : nullptr;
+    sa.trace = trace_begin(st);
     const int smem = (int)p->tile.smem_bytes;
     bool aligned = !(p->tile.ph[0].vec > 1 && ((uintptr_t)src % 16));
     if (p->tile.ph[1].w2) {      // 16-byte destination stores: every destination buffer 16-byte aligned
@@ -458,8 +493,10 @@ vpg_status launch_tile(const vpg_plan *p, const void *src, void *dst, const Shar
                 fprintf(stderr, "[vpg] jit launch kernel %p grid %lld threads %d smem %d nb %d src %p dst %p\n",
                         (const void *)jk, (long long)grid, jthreads, smem, nb, src, dst);
             LaunchCfg lc(grid, jthreads, smem, st, p->shards <= 1);
-            if (cudaLaunchKernelExC(&lc.cfg, (const void *)jk, args) == cudaSuccess)
+            if (cudaLaunchKernelExC(&lc.cfg, (const void *)jk, args) == cudaSuccess) {
+                trace_end(sa.trace, grid, p->tile.num_tiles, st);
                 return VPG_OK;
+            }
             cudaGetLastError();   // fall through to the ahead-of-time kernel
         }
     }

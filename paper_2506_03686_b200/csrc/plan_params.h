@@ -218,7 +218,11 @@ struct ShardArgs {
     // the per-device ring (kernels.cu sched_slot), zero at launch and reset
     // by the last CTA; nullptr = static round-robin tiles
     uint32_t *sched;
+    // development tracing (VPG_TRACE, kernels.cu): per-CTA globaltimer
+    // records of the tile pipeline; nullptr in normal launches
+    unsigned long long *trace;
 };
+constexpr int kTraceWords = 64;     // per CTA: start, prologue issued, end, smid, then (tile, data ready, written) x 20
 
 // --------------------------------------------------------------------------
 // ROWS (K1): stride-1 preserved; each destination row of Lr elements is a

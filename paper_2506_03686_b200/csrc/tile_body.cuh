@@ -114,6 +114,11 @@ __device__ __forceinline__ void st_out(W *p, const W &v) {
 // the previous grid's completion -- and the visibility of its memory --
 // before its first global-memory access.  Without the attribute both are
 // no-ops.
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
@@ -466,8 +471,33 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
             }
         } else {
             uint32_t c0 = t.c0 + e.c0, c1 = t.c1 + e.c1, c2 = t.c2;
+            uint32_t i = 0;
+            if constexpr (!VEC) {
+                // checked walk, U elements at a time: all U (predicated) smem
+                // loads issue before the first store, so the stores do not
+                // each wait out a shared-memory latency
+                VPG_UNROLL
+                for (; i + U <= n_in; i += U) {
+                    W v[U];
+                    bool ok[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        ok[u] = slot_ok(mask, c0 + u * d.c_in[0], c1 + u * d.c_in[1], c2 + u * d.c_in[2], lim);
+                        if (ok[u]) v[u] = *sptr<W>(smem, soff<W>(d, bb, s + u * s_in + ((hh + u * h_in) & hmask)));
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        if (ok[u]) st_out(gp + u * g_in, v[u]);
+                    gp += U * g_in;
+                    s += U * s_in;
+                    hh += U * h_in;
+                    c0 += U * d.c_in[0];
+                    c1 += U * d.c_in[1];
+                    c2 += U * d.c_in[2];
+                }
+            }
             VPG_UNROLL
-            for (uint32_t i = 0; i < n_in; ++i) {
+            for (; i < n_in; ++i) {
                 if (slot_ok(mask, c0, c1, c2, lim)) {
                     if constexpr (VEC) {
                         uint4 v = *sptr<uint4>(smem, soff<W>(d, bb, s));
@@ -700,6 +730,18 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
     const uint32_t S = ASYNC ? p.nbuf : 1u;
     const uint32_t R = S + 2;
     pdl_trigger();
+    // development tracing: specialised kernels compiled with VPG_TRACE only
+#ifdef VPG_TRACE_BUILD
+    unsigned long long *const trc = sa.trace ? sa.trace + (size_t)blockIdx.x * kTraceWords : nullptr;
+#else
+    constexpr unsigned long long *trc = nullptr;
+#endif
+    if (trc && tid == 0) {
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        trc[0] = gtimer();
+        trc[3] = smid;
+    }
 
     // Tile schedule.  The first S tiles of a CTA are static (blockIdx.x +
     // j * gridDim.x, the prologue); later ones come from the dynamic
@@ -811,6 +853,8 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
         if (s_ok[j]) load(j, p.off_buf + j * bstride);
         if constexpr (ASYNC) cp_async_commit();
     }
+    if (trc && tid == 0) trc[1] = gtimer();
+    uint32_t tiles_done = 0;
     for (uint32_t k = 0;; ++k) {
         // claim + decode the tile of slot k+S
         {
@@ -855,6 +899,7 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
         if constexpr (ASYNC) cp_async_wait_pending(S - 1);
         __syncthreads();
         if (!s_ok[k % R]) break;           // uniform: this CTA has no tile k
+        if (trc && tid == 0 && k < 20) trc[4 + 3 * k + 1] = gtimer();
         const uint32_t b = p.off_buf + (k % S) * bstride;
         {
             Lim lim;
@@ -864,8 +909,17 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
                           (uint32_t)s_base[slot][0], p.hmask);
         }
         __syncthreads();
+        if (trc && tid == 0 && k < 20) {
+            trc[4 + 3 * k] = (unsigned long long)(s_base[k % R][1]);
+            trc[4 + 3 * k + 2] = gtimer();
+        }
+        ++tiles_done;
         if (s_ok[(k + S) % R]) load(k + S, b);
         if constexpr (ASYNC) cp_async_commit();
+    }
+    if (trc && tid == 0) {
+        trc[2] = gtimer();
+        trc[kTraceWords - 1] = tiles_done;
     }
     // peer stores of a sharded plan: performed system-wide before the grid
     // retires, so the exchange's completion barrier orders them
