@@ -611,7 +611,8 @@ def bench_sharded(args, torch, base, config, peak, peak_kind):
     import torch.distributed as dist
 
     from paper_2506_03686_b200 import permute
-    from paper_2506_03686_b200.sharded import (ShardExchange, fused_supported, permute_sharded, plan_sharded,
+    from paper_2506_03686_b200.sharded import (ShardExchange, fused_supported, permute_sharded,
+                                               permute_sharded_pipelined, pipeline_chunks, plan_sharded,
                                                shard_bounds)
     from paper_2506_03686_b200.workloads import CONFIGS, make_input_slice
 
@@ -645,7 +646,10 @@ def bench_sharded(args, torch, base, config, peak, peak_kind):
     method = args.shard_method
     xmode = None
     if method == "auto":
-        method = "fused" if fused_supported(wl.shape, wl.axes, wl.elem_bytes, G) else "alltoall"
+        # the fused exchange where its remote runs are long enough, else the
+        # chunk-pipelined all-to-all where the shard has a pipelining axis
+        method = "fused" if fused_supported(wl.shape, wl.axes, wl.elem_bytes, G) else (
+            "pipelined" if pipeline_chunks(sp) > 1 else "alltoall")
     if method in ("push", "pull"):
         method, xmode = "fused", method
     if method == "fused":
@@ -656,6 +660,9 @@ def bench_sharded(args, torch, base, config, peak, peak_kind):
             # the peers read this rank's input from the exchange's shared buffer
             ex.input.copy_(x)
             x = ex.input
+    elif method == "pipelined":
+        run = lambda xin: permute_sharded_pipelined(xin, wl.shape, wl.axes, local_permute=permute,  # noqa: E731
+                                                    plan=sp)
     else:
         run = lambda xin: permute_sharded(xin, wl.shape, wl.axes, local_permute=permute, plan=sp)  # noqa: E731
     step = lambda: run(x)  # noqa: E731
@@ -751,7 +758,8 @@ def bench_sharded(args, torch, base, config, peak, peak_kind):
                             "paper_2506_03686_b200.sharded.permute_sharded") +
                            " on pinned host shards, streamed (H2D of step k+1 overlaps D2H of step k)",
                     "parity": e2e_ok},
-            "gpu_launches": (1 if method == "fused" or G == 1 else 2) * args.steps,
+            "gpu_launches": (1 if method == "fused" or G == 1 else
+                             pipeline_chunks(sp) + 1 if method == "pipelined" else 2) * args.steps,
             "shard_method": method if method != "fused" else f"fused ({xmode})",
             "roofline": {"bound": bound, "achieved": round(gbs, 2), "peak": round(roof_gbs, 1),
                          "peak_kind": f"min over HBM ({peak_kind} {peak} GB/s per GPU) and NVLink "
@@ -761,7 +769,8 @@ def bench_sharded(args, torch, base, config, peak, peak_kind):
                          "unit": "GB/s", "frac": round(gbs / roof_gbs, 4), "traffic": None,
                          "kernel": ("fused exchange tile kernel (peer stores over NVLink)" if xmode == "push" else
                                     "fused exchange tile kernel (peer reads over NVLink)") if method == "fused"
-                         else "tile (P1/P2) + NCCL all_to_all_single"},
+                         else ("tile (P1 per chunk, P2) + NCCL all_to_all_single per chunk, pipelined"
+                               if method == "pipelined" else "tile (P1/P2) + NCCL all_to_all_single")},
             "parity_sampled": bool(ok.item()),
             "alltoall_256MiB": None if a2a is None else {"algbw_gbs": round(a2a[0], 1),
                                                           "busbw_gbs": round(a2a[1], 1)},
@@ -822,9 +831,10 @@ def main(argv=None):
     ap.add_argument("--tune", action="store_true", help="measured planning (autotune) before timing")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="N>1 process group; gloo only checks the code path (ranks may share a GPU)")
-    ap.add_argument("--shard-method", default="auto", choices=["auto", "fused", "push", "pull", "alltoall"],
+    ap.add_argument("--shard-method", default="auto",
+                    choices=["auto", "fused", "push", "pull", "alltoall", "pipelined"],
                     help="N>1: fused exchange kernel (push: peer stores, pull: peer reads, fused: whichever "
-                         "keeps long remote runs) or P1 -> all-to-all -> P2")
+                         "keeps long remote runs), P1 -> all-to-all -> P2, or that pipelined over chunks")
     ap.add_argument("--cpu-threads", type=int, default=None)
     ap.add_argument("--sharded", action="store_true",
                     help="use the sharded (torchrun/NCCL) code path even with one rank")

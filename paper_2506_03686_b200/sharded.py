@@ -37,8 +37,9 @@ from dataclasses import dataclass
 
 from .core import LayoutError
 
-__all__ = ["ShardPlan", "plan_sharded", "permute_sharded", "shard_bounds", "ShardExchange", "emulate_fused",
-           "fused_supported", "fused_method", "release_exchanges"]
+__all__ = ["ShardPlan", "plan_sharded", "permute_sharded", "permute_sharded_pipelined", "pipeline_chunks", "pipeline_spec",
+           "shard_bounds", "ShardExchange", "emulate_fused", "emulate_sharded_pipelined", "fused_supported",
+           "fused_method", "release_exchanges"]
 
 
 def _lead_split(shape, G):
@@ -234,8 +235,11 @@ def permute_sharded(local_in, global_shape, axes, group=None, local_permute=None
 
     G = dist.get_world_size(group) if dist.is_initialized() else 1
     r = dist.get_rank(group) if dist.is_initialized() else 0
-    if method not in ("alltoall", "fused", "auto"):
+    if method not in ("alltoall", "fused", "auto", "pipelined"):
         raise ValueError(f"unknown method {method!r}")
+    if method == "pipelined":
+        return permute_sharded_pipelined(local_in, global_shape, axes, group=group, local_permute=local_permute,
+                                         plan=plan)
     if method != "alltoall" and local_permute is None and local_in.is_cuda:
         if method == "fused" or fused_supported(global_shape, axes, local_in.element_size(), G):
             ex = _exchange_for(tuple(global_shape), tuple(axes), local_in.dtype, local_in.device, group)
@@ -265,6 +269,165 @@ def permute_sharded(local_in, global_shape, axes, group=None, local_permute=None
     s2, a2 = sp.p2()
     got = recv.view(packed.dtype).reshape(s2)
     return local_permute(got, a2).reshape(sp.local_out_shape())
+
+
+def pipeline_spec(sp: ShardPlan, chunks: int = 4):
+    """Chunking of the pipelined all-to-all path: a list of (axis, factor)
+    over the outermost axes of the local input, so every chunk is a
+    contiguous slice of the shard.  Every listed axis must survive to the
+    local output (an M axis: each destination then receives 1/C of its data
+    per chunk); all but the last are enumerated whole, the last may be cut
+    to a divisor of its extent.  C = product of the factors <= `chunks`
+    (empty list: no pipelining)."""
+    L = sp.local_in_axes()
+    spec, C = [], 1
+    for a in L:
+        if sp.G == 1 or a not in sp.M or C >= chunks:
+            break
+        e = sp.rshape[a]
+        f = next((c for c in range(min(chunks // C, e), 1, -1) if e % c == 0), 1)
+        if f < 2:
+            break
+        spec.append((a, f))
+        C *= f
+        if f < e:
+            break              # a cut axis ends the prefix
+    return spec
+
+
+def pipeline_chunks(sp: ShardPlan, chunks: int = 4) -> int:
+    """Number of chunks of the pipelined path (1 = not pipelined)."""
+    C = 1
+    for _, f in pipeline_spec(sp, chunks):
+        C *= f
+    return C
+
+
+def _pipelined_programs(sp: ShardPlan, spec):
+    """(P1 chunk shape, axes) and (P2 shape, axes) of the pipelined path.
+    P1 permutes one contiguous input chunk into [D][M_c] (M_c: M without the
+    whole chunk axes, the cut axis at extent e/f); P2 permutes the
+    chunk-major receive buffer [chunk digits][IO][M_c] into the local output,
+    each chunk digit becoming (the outer factor of) its axis."""
+    full = {a for a, f in spec if f == sp.rshape[a]}
+    cut = {a: f for a, f in spec if f < sp.rshape[a]}
+
+    def ext(a):
+        return sp.rshape[a] // cut[a] if a in cut else sp.rshape[a]
+
+    L = [a for a in sp.local_in_axes() if a not in full]
+    T = [a for a in list(sp.D) + list(sp.M) if a not in full]
+    p1 = (tuple(ext(a) for a in L), tuple(L.index(a) for a in T))
+    recv = [a for a in list(sp.IO) + list(sp.M) if a not in full]
+    k = len(spec)
+    shape = tuple(f for _, f in spec) + tuple(ext(a) for a in recv)
+    cidx = {a: i for i, (a, _) in enumerate(spec)}
+    axes = []
+    for a in sp.local_out_axes():
+        if a in full:
+            axes.append(cidx[a])
+        elif a in cut:
+            axes.extend([cidx[a], k + recv.index(a)])
+        else:
+            axes.append(k + recv.index(a))
+    return p1, (shape, tuple(axes))
+
+
+def permute_sharded_pipelined(local_in, global_shape, axes, group=None, local_permute=None, plan=None,
+                              chunks: int = 4):
+    """P1 -> all-to-all -> P2 with the pack permute and the exchange
+    pipelined over C chunks: P1 of chunk c+1 runs on
+    the current stream while the all-to-all of chunk c runs on NCCL's stream,
+    and one P2 permutes the chunk-major receive buffer.  Shapes without a
+    pipelining axis (pipeline_chunks == 1) take the serial path.  Same
+    arguments and result as permute_sharded(method="alltoall")."""
+    import torch
+    import torch.distributed as dist
+
+    G = dist.get_world_size(group) if dist.is_initialized() else 1
+    r = dist.get_rank(group) if dist.is_initialized() else 0
+    sp = plan or plan_sharded(global_shape, axes, G)
+    spec = pipeline_spec(sp, chunks)
+    C = pipeline_chunks(sp, chunks)
+    if C == 1:
+        return permute_sharded(local_in, global_shape, axes, group=group, local_permute=local_permute, plan=sp)
+    if local_permute is None:
+        from .api import permute as local_permute  # GPU kernels; no CPU fallback
+    if local_in.numel() != sp.local_numel:
+        raise LayoutError(f"rank {r}: shard holds {local_in.numel()} elements, expected {sp.local_numel}")
+    (s1c, a1), (s2c, a2c) = _pipelined_programs(sp, spec)
+    xin = local_in.reshape(C, -1)
+    es = local_in.element_size()
+    send = [c * es // C for c in sp.send_counts(r)]
+    recv_c = [c * es // C for c in sp.recv_counts(r)]
+    nrecv = sum(recv_c)
+    staged = local_in.is_cuda and dist.get_backend(group) == "gloo"
+    dev = local_in.device
+    recv = torch.empty(C * nrecv, dtype=torch.uint8, device="cpu" if staged else dev)
+    works, keep = [], []
+    cuda = local_in.is_cuda and not staged
+    comm = torch.cuda.Stream(dev) if cuda else None
+    for c in range(C):
+        packed = local_permute(xin[c].reshape(s1c), a1).reshape(-1).view(torch.uint8)
+        if staged:
+            packed = packed.cpu()
+        if cuda:
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(dev))
+            comm.wait_event(ev)
+            with torch.cuda.stream(comm):
+                # NCCL orders the collective after `comm`, i.e. after P1 of
+                # chunk c; P1 of chunk c+1 proceeds on the current stream
+                works.append(dist.all_to_all_single(recv[c * nrecv:(c + 1) * nrecv], packed, recv_c, send,
+                                                    group=group, async_op=True))
+            packed.record_stream(comm)
+        else:
+            works.append(dist.all_to_all_single(recv[c * nrecv:(c + 1) * nrecv], packed, recv_c, send,
+                                                group=group, async_op=True))
+        keep.append(packed)
+    for w in works:
+        w.wait()                                    # current stream waits for every chunk's exchange
+    if cuda:
+        torch.cuda.current_stream(dev).wait_stream(comm)
+        recv.record_stream(comm)
+    if staged:
+        recv = recv.to(dev)
+    got = recv.view(local_in.dtype).reshape(s2c)
+    return local_permute(got, a2c).reshape(sp.local_out_shape())
+
+
+def emulate_sharded_pipelined(x_flat, global_shape, axes, G, local_permute=None, chunks: int = 4):
+    """permute_sharded_pipelined for G virtual ranks on ONE device (rank after
+    rank, the chunked all-to-all as buffer slicing): validates the chunked
+    P1 programs, the chunk-major receive layout and the P2 program."""
+    import torch
+
+    if local_permute is None:
+        from .api import permute as local_permute
+    sp = plan_sharded(global_shape, axes, G)
+    spec = pipeline_spec(sp, chunks)
+    C = pipeline_chunks(sp, chunks)
+    if C == 1:
+        return emulate_sharded(x_flat, global_shape, axes, G, local_permute=local_permute)
+    n = sp.numel
+    (s1c, a1), (s2c, a2c) = _pipelined_programs(sp, spec)
+    packed = []            # packed[r][c]
+    for r in range(G):
+        lo, hi = shard_bounds(n, G, r)
+        xin = x_flat[lo:hi].reshape(C, -1)
+        packed.append([local_permute(xin[c].reshape(s1c), a1).reshape(-1) for c in range(C)])
+    outs = []
+    for s in range(G):
+        parts = []
+        for c in range(C):
+            for r in range(G):
+                sc = [k // C for k in sp.send_counts(r)]
+                off = sum(sc[:s])
+                if sc[s]:
+                    parts.append(packed[r][c][off:off + sc[s]])
+        got = torch.cat(parts).reshape(s2c)
+        outs.append(local_permute(got, a2c).reshape(sp.local_out_shape()))
+    return outs
 
 
 def emulate_sharded(x_flat, global_shape, axes, G, local_permute=None):

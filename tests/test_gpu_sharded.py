@@ -239,7 +239,7 @@ def test_fused_exchange_word_sizes(cuda, dtype_name, jit, mode):
     assert ran >= 4
 
 
-@pytest.mark.parametrize("method", ["push", "pull", "alltoall"])
+@pytest.mark.parametrize("method", ["push", "pull", "alltoall", "pipelined"])
 def test_bench_two_ranks_code_path(cuda, method):
     """bench.py's N>1 path (torchrun, two ranks) end to end with the gloo
     backend on one GPU: the same code the 8-GPU NCCL run takes, checked for
@@ -256,7 +256,8 @@ def test_bench_two_ranks_code_path(cuda, method):
     assert res.returncode == 0, res.stderr[-2000:]
     line = json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["parity_sampled"] is True
-    assert line["shard_method"] == (method if method == "alltoall" else f"fused ({method})") and line["n_gpus"] == 2
+    assert line["shard_method"] == (method if method in ("alltoall", "pipelined") else f"fused ({method})")
+    assert line["n_gpus"] == 2
     assert "gloo" in line["dist_backend"]
 
 
@@ -348,3 +349,24 @@ def test_pull_exchange_nonpow2_shards_beyond_32bit_offsets(cuda):
     want = x.view(shape).permute(axes).contiguous().reshape(-1)
     got = torch.cat(outs)
     assert torch.equal(got, want)
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_pipelined_alltoall_cfg5_emulated(cuda, G):
+    """The chunk-pipelined all-to-all path's GPU programs on cfg5 (2 GiB):
+    chunked P1 kernels, chunk-major receive buffers and the P2 kernel for G
+    virtual ranks on one device, against the single-GPU permutation."""
+    import torch
+
+    from paper_2506_03686_b200 import permute
+    from paper_2506_03686_b200.sharded import emulate_sharded_pipelined, pipeline_chunks, plan_sharded
+    from paper_2506_03686_b200.workloads import CONFIGS
+
+    w = CONFIGS["cfg5"]
+    assert pipeline_chunks(plan_sharded(w.shape, w.axes, G)) > 1
+    x = torch.randint(-2**62, 2**62, (w.numel,), dtype=torch.int64, device="cuda",
+                      generator=torch.Generator(device="cuda").manual_seed(10 + G))
+    outs = emulate_sharded_pipelined(x, w.shape, w.axes, G)
+    whole = permute(x.view(w.shape), w.axes).reshape(-1)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat([o.reshape(-1) for o in outs]), whole)

@@ -39,7 +39,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, cases, q):
+def _worker(rank, world, port, cases, q, method="alltoall"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -53,7 +53,7 @@ def _worker(rank, world, port, cases, q):
             g = rng.integers(0, 2**62, size=n, dtype=np.int64)
             lo, hi = shard_bounds(n, world, rank)
             local = torch.from_numpy(g[lo:hi].copy())
-            out = permute_sharded(local, shape, axes, local_permute=_np_permute)
+            out = permute_sharded(local, shape, axes, local_permute=_np_permute, method=method)
             want = np.ascontiguousarray(np.transpose(g.reshape(shape), axes)).reshape(-1)[lo:hi]
             if not np.array_equal(out.numpy().reshape(-1), want):
                 errs.append((shape, axes, "mismatch"))
@@ -64,11 +64,11 @@ def _worker(rank, world, port, cases, q):
     dist.destroy_process_group()
 
 
-def _run(world, cases):
+def _run(world, cases, method="alltoall"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, cases, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cases, q, method)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=240) for _ in procs]
@@ -83,6 +83,44 @@ def test_sharded_gloo(world):
     assert len(cases) >= 5
     for rank, errs in _run(world, cases):
         assert not errs, (rank, errs)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_gloo_pipelined(world):
+    """The chunk-pipelined path (P1 chunk c+1 overlapping the all-to-all of
+    chunk c, one P2 over the chunk-major receive buffer) over gloo."""
+    from paper_2506_03686_b200.sharded import pipeline_chunks
+
+    cases = [c for c in CASES + [((2,) * 14, (13, 4, 10, 11, 2, 0, 6, 12, 3, 7, 8, 1, 5, 9)),
+                                 ((8, 12, 6, 4), (3, 1, 0, 2))] if _shardable(c, world)]
+    assert sum(pipeline_chunks(plan_sharded(c[0], c[1], world)) > 1 for c in cases) >= 4
+    for rank, errs in _run(world, cases, method="pipelined"):
+        assert not errs, (rank, errs)
+
+
+def test_pipeline_programs_emulated():
+    """Chunked P1 programs, chunk-major receive layout and P2 program for
+    virtual ranks (numpy local permutes), including every cfg5 shard count."""
+    from paper_2506_03686_b200.sharded import emulate_sharded_pipelined, pipeline_chunks
+    from paper_2506_03686_b200.workloads import CONFIGS
+
+    cases = CASES + [((2,) * 14, (13, 4, 10, 11, 2, 0, 6, 12, 3, 7, 8, 1, 5, 9)), ((8, 12, 6, 4), (3, 1, 0, 2))]
+    seen = 0
+    for G in (2, 4, 8):
+        for shape, axes in cases:
+            if not _shardable((shape, axes), G):
+                continue
+            for chunks in (2, 4, 8):
+                n = int(np.prod(shape))
+                g = np.arange(n, dtype=np.int64)
+                outs = emulate_sharded_pipelined(torch.from_numpy(g), shape, axes, G, local_permute=_np_permute,
+                                                 chunks=chunks)
+                want = np.ascontiguousarray(np.transpose(g.reshape(shape), axes)).reshape(-1)
+                assert np.array_equal(torch.cat([o.reshape(-1) for o in outs]).numpy(), want), (G, shape, axes)
+                seen += pipeline_chunks(plan_sharded(shape, axes, G), chunks) > 1
+    assert seen >= 20
+    w = CONFIGS["cfg5"]
+    assert [pipeline_chunks(plan_sharded(w.shape, w.axes, G)) for G in (2, 4, 8)] == [4, 4, 2]
 
 
 def _shardable(case, G):
