@@ -31,8 +31,9 @@
 extern "C" {
 #endif
 
-#define VPG_ABI_VERSION 4
+#define VPG_ABI_VERSION 5
 #define VPG_MAX_RANK 64
+#define VPG_MAX_SHARDS 64   /* shards of a fused exchange */
 
 typedef enum {
     VPG_OK = 0,
@@ -191,6 +192,44 @@ vpg_status vpg_permute_sharded(const vpg_plan *plan, const void *src_shard,
  * may be overwritten before every rank's kernel has completed. */
 vpg_status vpg_permute_sharded_pull(const vpg_plan *plan, const void *const *src_shards,
                                     void *dst_shard, void *cuda_stream);
+
+/* Device-side ordering of a fused exchange, instead of the caller's
+ * barriers around the launch (replaces the two one-element all-reduces
+ * the reference's SPEC.md:181 partitioned execution would need per step):
+ *   flags[q]     rank q's flag block as seen from this device: 2 x shards
+ *                uint64, zero-initialised once, CUDA IPC / peer-mapped for
+ *                q != own (NVLink/NVSwitch);
+ *   epoch        this call's value, greater than every earlier call's on
+ *                the same flag blocks (e.g. a per-exchange call counter + 1);
+ *   done_counter a zero uint32 in this device's memory (left zero).
+ * The kernel starts reading/writing peer shards only after every rank's
+ * kernel has started, and completes only after every rank's accesses have
+ * finished, so stream order on each rank is the whole ordering.  All ranks
+ * must launch with the same epoch.  Waits are bounded (~4 s). */
+typedef struct vpg_shard_sync {
+    unsigned long long *flags[VPG_MAX_SHARDS];
+    unsigned long long epoch;
+    unsigned int *done_counter;
+} vpg_shard_sync;
+
+/* Fused exchange step with optional device-side ordering (sync may be NULL:
+ * then as vpg_permute_sharded / vpg_permute_sharded_pull).  Push plans:
+ * src_shards[0] = this rank's input shard, dst_shards[q] = output shard q.
+ * Pull plans: src_shards[q] = input shard q, dst_shards[0] = this rank's
+ * output shard.  Replaces: the exchange step of the reference's
+ * outer-counter-partitioned execution. */
+vpg_status vpg_permute_sharded_sync(const vpg_plan *plan, const void *const *src_shards,
+                                    void *const *dst_shards, const vpg_shard_sync *sync, void *cuda_stream);
+
+/* Every rank of a fused exchange on ONE device in one cooperative launch,
+ * with the device-side ordering above between the ranks (flag blocks and
+ * counters allocated internally; returns after the step has finished).
+ * plans[r] = rank r's plan (all push or all pull, same arguments),
+ * src_shards[r] / dst_shards[r] = rank r's input / output shard.  Validates
+ * the exchange protocol on single-GPU machines; a multi-GPU job runs one
+ * vpg_permute_sharded_sync per rank instead. */
+vpg_status vpg_permute_sharded_emulated(const vpg_plan *const *plans, int nplans, const void *const *src_shards,
+                                        void *const *dst_shards, void *cuda_stream);
 
 /* CUDA IPC for the exchange's peer table: export a device pointer (any
  * pointer inside a cudaMalloc allocation) as a VPG_IPC_HANDLE_BYTES handle

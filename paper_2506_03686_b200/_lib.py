@@ -26,6 +26,11 @@ VPG_MAX_RANK = 64
 VPG_MAX_SHARDS = 64
 VPG_IPC_HANDLE_BYTES = 64
 
+
+class ShardSync(ctypes.Structure):
+    """vpg_shard_sync (include/vpgpu.h): device-side exchange ordering."""
+    _fields_ = [("flags", ctypes.c_void_p * 64), ("epoch", ctypes.c_ulonglong), ("done_counter", ctypes.c_void_p)]
+
 # symbols declared in include/vpgpu.h (checked by tests/test_abi.py)
 EXPORTED = (
     "vpg_version",
@@ -36,6 +41,8 @@ EXPORTED = (
     "vpg_permute",
     "vpg_permute_sharded",
     "vpg_permute_sharded_pull",
+    "vpg_permute_sharded_sync",
+    "vpg_permute_sharded_emulated",
     "vpg_ipc_export",
     "vpg_ipc_import",
     "vpg_ipc_release",
@@ -112,6 +119,9 @@ def lib():
         L.vpg_permute.argtypes = [vp, vp, vp, vp]
         L.vpg_permute_sharded.argtypes = [vp, vp, ctypes.POINTER(vp), vp]
         L.vpg_permute_sharded_pull.argtypes = [vp, ctypes.POINTER(vp), vp, vp]
+        L.vpg_permute_sharded_sync.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), vp, vp]
+        L.vpg_permute_sharded_emulated.argtypes = [ctypes.POINTER(vp), ctypes.c_int, ctypes.POINTER(vp),
+                                                   ctypes.POINTER(vp), vp]
         L.vpg_ipc_export.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_uint64)]
         L.vpg_ipc_import.argtypes = [vp, ctypes.c_uint64, ctypes.POINTER(vp)]
         L.vpg_ipc_release.argtypes = [vp]
@@ -127,7 +137,8 @@ def lib():
         L.vpg_plan_destroy.argtypes = [vp]
         L.vpg_plan_destroy.restype = None
         for name in ("vpg_merge_dimensions", "vpg_plan_create", "vpg_permute", "vpg_permute_host",
-                     "vpg_plan_create_sharded", "vpg_permute_sharded", "vpg_permute_sharded_pull", "vpg_ipc_export", "vpg_ipc_import",
+                     "vpg_plan_create_sharded", "vpg_permute_sharded", "vpg_permute_sharded_pull",
+                     "vpg_permute_sharded_sync", "vpg_permute_sharded_emulated", "vpg_ipc_export", "vpg_ipc_import",
                      "vpg_ipc_release",
                      "vpg_permute_host_async", "vpg_permute_host_bounded",
                      "vpg_permute_nd", "vpg_plan_info_get", "vpg_plan_describe", "vpg_plan_emit_source",

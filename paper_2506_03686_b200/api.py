@@ -355,6 +355,30 @@ def launch_sharded(program: GpuProgram, src_ptr: int, dst_ptrs, stream_ptr) -> N
     _check(st, "permute_sharded")
 
 
+def launch_sharded_sync(program: GpuProgram, src_ptrs, dst_ptrs, sync, stream_ptr) -> None:
+    """Enqueue one rank's fused-exchange kernel with device-side ordering
+    (vpg_permute_sharded_sync; ``sync`` an _lib.ShardSync or None).  Push
+    plans: src_ptrs = [own input], dst_ptrs = every output shard; pull
+    plans: src_ptrs = every input shard, dst_ptrs = [own output]."""
+    arr_s = (ctypes.c_void_p * len(src_ptrs))(*[int(p) for p in src_ptrs])
+    arr_d = (ctypes.c_void_p * len(dst_ptrs))(*[int(p) for p in dst_ptrs])
+    st = _lib.lib().vpg_permute_sharded_sync(program.handle, arr_s, arr_d,
+                                             ctypes.byref(sync) if sync is not None else None, stream_ptr)
+    _check(st, "permute_sharded_sync")
+
+
+def launch_sharded_emulated(programs, src_ptrs, dst_ptrs, stream_ptr) -> None:
+    """Every rank's exchange kernel in one cooperative launch on this device,
+    with the device-side exchange ordering between them
+    (vpg_permute_sharded_emulated); returns once the step has finished."""
+    G = len(programs)
+    hs = [p.handle for p in programs]
+    plans = (ctypes.c_void_p * G)(*[h.value if isinstance(h, ctypes.c_void_p) else h for h in hs])
+    arr_s = (ctypes.c_void_p * G)(*[int(p) for p in src_ptrs])
+    arr_d = (ctypes.c_void_p * G)(*[int(p) for p in dst_ptrs])
+    _check(_lib.lib().vpg_permute_sharded_emulated(plans, G, arr_s, arr_d, stream_ptr), "permute_sharded_emulated")
+
+
 def _time_program(torch, program, src, dst, flush, reps):
     """Median device time (ms) of one launch after an L2 flush."""
     stream = torch.cuda.current_stream(src.device)

@@ -114,6 +114,48 @@ vpg_status vpg_permute_sharded_pull(const vpg_plan *plan, const void *const *src
     return VPG_OK;
 }
 
+vpg_status vpg_permute_sharded_sync(const vpg_plan *plan, const void *const *src_shards, void *const *dst_shards,
+                                    const vpg_shard_sync *sync, void *cuda_stream) {
+    if (!plan || !src_shards || !dst_shards) return fail(VPG_EINVAL, "null argument");
+    if (plan->shards < 1) return fail(VPG_EINVAL, "not a sharded plan (use vpg_permute)");
+    const int G = plan->shards;
+    if (sync && sync->epoch != 0) {
+        if (!sync->done_counter) return fail(VPG_EINVAL, "sync: null done_counter");
+        for (int q = 0; q < G; ++q)
+            if (!sync->flags[q]) return fail(VPG_EINVAL, "sync: null flag block");
+    }
+    const uint64_t sb = (uint64_t)(plan->n / G) * (uint64_t)plan->elem_bytes;
+    std::string err;
+    vpg_status s;
+    if (plan->tile.pull) {
+        if (plan->n > 0 && !dst_shards[0]) return fail(VPG_EINVAL, "null buffer");
+        for (int q = 0; q < G; ++q) {
+            if (plan->n > 0 && !src_shards[q]) return fail(VPG_EINVAL, "null buffer");
+            if (overlaps(src_shards[q], sb, dst_shards[0], sb))
+                return fail(VPG_EINVAL, "src and dst must not overlap (out-of-place only)");
+        }
+        s = vpg::launch_plan_pull(plan, src_shards, dst_shards[0], cuda_stream, &err, sync);
+    } else {
+        if (plan->n > 0 && !src_shards[0]) return fail(VPG_EINVAL, "null buffer");
+        for (int q = 0; q < G; ++q)
+            if (overlaps(dst_shards[q], sb, src_shards[0], sb))
+                return fail(VPG_EINVAL, "src and dst must not overlap (out-of-place only)");
+        s = vpg::launch_plan(plan, src_shards[0], dst_shards, G, cuda_stream, &err, sync);
+    }
+    if (s != VPG_OK) return fail(s, err);
+    return VPG_OK;
+}
+
+vpg_status vpg_permute_sharded_emulated(const vpg_plan *const *plans, int nplans, const void *const *src_shards,
+                                        void *const *dst_shards, void *cuda_stream) {
+    if (!plans || !src_shards || !dst_shards) return fail(VPG_EINVAL, "null argument");
+    if (nplans < 2 || nplans > VPG_MAX_SHARDS) return fail(VPG_EINVAL, "nplans must be in 2..VPG_MAX_SHARDS");
+    if (plans[0] && plans[0]->n == 0) return VPG_OK;
+    std::string err;
+    vpg_status s = vpg::launch_sharded_emulated(plans, nplans, src_shards, dst_shards, cuda_stream, &err);
+    return s == VPG_OK ? s : fail(s, err);
+}
+
 vpg_status vpg_ipc_export(const void *dev_ptr, void *handle, uint64_t *offset) {
     if (!dev_ptr || !handle || !offset) return fail(VPG_EINVAL, "null argument");
     std::string err;

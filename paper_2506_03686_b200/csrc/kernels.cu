@@ -261,6 +261,18 @@ __global__ void __launch_bounds__(1024) tile_kernel(const __grid_constant__ Tile
     tile_body<W, ASYNC>(p, src, dst, sa);
 }
 
+// Every rank of a fused exchange in ONE cooperative launch on one device
+// (vpg_permute_sharded_emulated): CTAs [r*per, (r+1)*per) run rank r's plan
+// with its own parameter block, buffers and ShardArgs (device memory), and
+// the device-side exchange barrier between the ranks -- co-residency is
+// guaranteed by the cooperative launch, so the flag waits cannot deadlock.
+template <typename W>
+__global__ void __launch_bounds__(1024) tile_kernel_ranks(const TileParams *ps, const W *const *srcs,
+                                                          W *const *dsts, const ShardArgs *sas, uint32_t per) {
+    const uint32_t r = blockIdx.x / per;
+    tile_body<W, true>(ps[r], srcs[r], dsts[r], sas[r], blockIdx.x - r * per, per);
+}
+
 template <typename W>
 __global__ void __launch_bounds__(1024) tile_kernel_bulk(const __grid_constant__ TileParams p,
                                                          const W *__restrict__ src, W *__restrict__ dst,
@@ -679,7 +691,16 @@ vpg_status launch_copy(const vpg_plan *p, const void *src, void *dst, cudaStream
 
 int device_sm_count() { return sm_count_for_current(); }
 
-vpg_status launch_plan_pull(const vpg_plan *p, const void *const *srcs, void *dst, void *stream, std::string *err) {
+static void apply_sync(ShardArgs &sa, const vpg_plan *p, const vpg_shard_sync *sync) {
+    if (!sync || sync->epoch == 0 || p->shards < 2) return;
+    for (int q = 0; q < p->shards; ++q) sa.flags[q] = sync->flags[q];
+    sa.epoch = sync->epoch;
+    sa.rank = (uint32_t)p->shard_index;
+    sa.done_ctr = sync->done_counter;
+}
+
+vpg_status launch_plan_pull(const vpg_plan *p, const void *const *srcs, void *dst, void *stream, std::string *err,
+                            const vpg_shard_sync *sync) {
     cudaStream_t st = (cudaStream_t)stream;
     const int E = p->elem_bytes;
     const int G = p->shards;
@@ -689,6 +710,7 @@ vpg_status launch_plan_pull(const vpg_plan *p, const void *const *srcs, void *ds
     }
     ShardArgs sa;
     memset(&sa, 0, sizeof(sa));
+    apply_sync(sa, p, sync);
     const void *src = srcs[0];
     for (int q = 0; q < G; ++q) {
         if (!srcs[q] || ((uintptr_t)srcs[q] % E)) {
@@ -725,7 +747,7 @@ vpg_status launch_plan_pull(const vpg_plan *p, const void *const *srcs, void *ds
 }
 
 vpg_status launch_plan(const vpg_plan *p, const void *src, void *const *dsts, int ndst, void *stream,
-                       std::string *err) {
+                       std::string *err, const vpg_shard_sync *sync) {
     cudaStream_t st = (cudaStream_t)stream;
     const int E = p->elem_bytes;
     const int G = p->shards > 0 ? p->shards : 1;
@@ -736,6 +758,7 @@ vpg_status launch_plan(const vpg_plan *p, const void *src, void *const *dsts, in
     void *dst = dsts[0];
     ShardArgs sa;
     memset(&sa, 0, sizeof(sa));
+    apply_sync(sa, p, sync);
     for (int q = 0; q < G; ++q) {
         if (!dsts[q] || ((uintptr_t)dsts[q] % E)) {
             *err = "destination buffers must be non-null and aligned to the element width";
@@ -790,6 +813,121 @@ vpg_status launch_plan(const vpg_plan *p, const void *src, void *const *dsts, in
         return VPG_ECUDA;
     }
     return VPG_OK;
+}
+
+
+// Every rank of a fused exchange in one cooperative launch (see
+// tile_kernel_ranks): per-rank parameter blocks, buffer bases and
+// ShardArgs in device memory, flag blocks + counters allocated here, epoch 1.
+template <int E>
+static vpg_status launch_ranks(const vpg_plan *const *plans, int G, const void *const *srcs, void *const *dsts,
+                               cudaStream_t st, std::string *err) {
+    using W = typename WordOf<E>::T;
+    const bool pull = plans[0]->tile.pull != 0;
+    std::vector<TileParams> ps(G);
+    std::vector<const W *> sv(G);
+    std::vector<W *> dv(G);
+    std::vector<ShardArgs> sas(G);
+    const size_t flag_words = (size_t)G * 2 * G;
+    void *mem = nullptr;
+    const size_t bytes = flag_words * 8 + (size_t)G * 4 + 64;
+    if (cudaMalloc(&mem, bytes) != cudaSuccess || cudaMemsetAsync(mem, 0, bytes, st) != cudaSuccess) {
+        cudaGetLastError();
+        *err = "cannot allocate the exchange flag blocks";
+        return VPG_ENOMEM;
+    }
+    unsigned long long *flags = (unsigned long long *)mem;
+    uint32_t *ctrs = (uint32_t *)(flags + flag_words);
+    bool aligned = true;
+    for (int r = 0; r < G; ++r) {
+        if (((uintptr_t)srcs[r] | (uintptr_t)dsts[r]) % 16) aligned = false;
+        if ((plans[r]->tile.shard_elems * E) % 16) aligned = false;
+    }
+    for (int r = 0; r < G; ++r) {
+        const vpg_plan *p = plans[r];
+        ps[r] = aligned ? p->tile : p->tile_unaligned;
+        ShardArgs &sa = sas[r];
+        memset(&sa, 0, sizeof(sa));
+        for (int q = 0; q < G; ++q) {
+            sa.off[q] = pull ? (int64_t)((uintptr_t)srcs[q] - (uintptr_t)srcs[0]) / E
+                             : (int64_t)((uintptr_t)dsts[q] - (uintptr_t)dsts[0]) / E;
+            sa.flags[q] = flags + (size_t)q * 2 * G;
+        }
+        sa.epoch = 1;
+        sa.rank = (uint32_t)r;
+        sa.done_ctr = ctrs + r;
+        sv[r] = (const W *)(pull ? srcs[0] : srcs[r]);
+        dv[r] = (W *)(pull ? dsts[r] : dsts[0]);
+    }
+    // one device block: parameter blocks, pointer tables, ShardArgs
+    const size_t o_ps = 0, o_s = o_ps + sizeof(TileParams) * G, o_d = o_s + sizeof(void *) * G,
+                 o_sa = (o_d + sizeof(void *) * G + 15) / 16 * 16, tot = o_sa + sizeof(ShardArgs) * G;
+    std::vector<unsigned char> host(tot);
+    memcpy(host.data() + o_ps, ps.data(), sizeof(TileParams) * G);
+    memcpy(host.data() + o_s, sv.data(), sizeof(void *) * G);
+    memcpy(host.data() + o_d, dv.data(), sizeof(void *) * G);
+    memcpy(host.data() + o_sa, sas.data(), sizeof(ShardArgs) * G);
+    void *dblk = nullptr;
+    if (cudaMalloc(&dblk, tot) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(mem);
+        *err = "cannot allocate the emulation tables";
+        return VPG_ENOMEM;
+    }
+    cudaMemcpyAsync(dblk, host.data(), tot, cudaMemcpyHostToDevice, st);
+    auto k = tile_kernel_ranks<W>;
+    const int threads = plans[0]->threads;
+    const int smem = (int)ps[0].smem_bytes;
+    int nb = occupancy(k, threads, smem);
+    int dev = 0, coop = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    const uint32_t per = (uint32_t)std::max<int64_t>(1, (int64_t)nb * sm_count_for_current() / G);
+    const TileParams *a0 = (const TileParams *)((unsigned char *)dblk + o_ps);
+    const W *const *a1 = (const W *const *)((unsigned char *)dblk + o_s);
+    W *const *a2 = (W *const *)((unsigned char *)dblk + o_d);
+    const ShardArgs *a3 = (const ShardArgs *)((unsigned char *)dblk + o_sa);
+    void *args[] = {(void *)&a0, (void *)&a1, (void *)&a2, (void *)&a3, (void *)&per};
+    vpg_status s = VPG_OK;
+    if (!coop) {
+        *err = "device does not support cooperative launches";
+        s = VPG_EUNSUPPORTED;
+    } else if (cudaLaunchCooperativeKernel((const void *)k, dim3(per * G), dim3(threads), args, (size_t)smem, st) !=
+               cudaSuccess) {
+        *err = std::string("cooperative launch failed: ") + cudaGetErrorString(cudaGetLastError());
+        s = VPG_ECUDA;
+    }
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (s == VPG_OK && e != cudaSuccess) {
+        *err = std::string("exchange emulation failed: ") + cudaGetErrorString(e);
+        s = VPG_ECUDA;
+    }
+    cudaFree(dblk);
+    cudaFree(mem);
+    return s;
+}
+
+vpg_status launch_sharded_emulated(const vpg_plan *const *plans, int G, const void *const *srcs, void *const *dsts,
+                                   void *stream, std::string *err) {
+    for (int r = 0; r < G; ++r) {
+        const vpg_plan *p = plans[r];
+        if (!p || p->kernel_class != VPG_KERNEL_TILE || p->shards != G || p->shard_index != r ||
+            (p->tile.pull != 0) != (plans[0]->tile.pull != 0) || p->elem_bytes != plans[0]->elem_bytes ||
+            p->tile.bulk) {
+            *err = "plans[r] must be rank r's exchange plan of one push or pull exchange over nplans shards";
+            return VPG_EINVAL;
+        }
+        if (!srcs[r] || !dsts[r] || (uintptr_t)srcs[r] % p->elem_bytes || (uintptr_t)dsts[r] % p->elem_bytes) {
+            *err = "buffers must be non-null and aligned to the element width";
+            return VPG_EINVAL;
+        }
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (plans[0]->elem_bytes) {
+        case 4: return launch_ranks<4>(plans, G, srcs, dsts, st, err);
+        case 8: return launch_ranks<8>(plans, G, srcs, dsts, st, err);
+        default: *err = "the exchange emulation supports 4- and 8-byte words"; return VPG_EUNSUPPORTED;
+    }
 }
 
 }  // namespace vpg

@@ -56,9 +56,12 @@ vpg_status ipc_release(void *ptr, std::string *err);
 // kernels.cu
 // dsts: one destination per output shard (1 for ordinary plans)
 vpg_status launch_plan(const vpg_plan *p, const void *src, void *const *dsts, int ndst, void *stream,
-                       std::string *err);
+                       std::string *err, const vpg_shard_sync *sync = nullptr);
 // pull exchange plans: srcs = every input shard's buffer, dst = the local output shard
-vpg_status launch_plan_pull(const vpg_plan *p, const void *const *srcs, void *dst, void *stream, std::string *err);
+vpg_status launch_plan_pull(const vpg_plan *p, const void *const *srcs, void *dst, void *stream, std::string *err,
+                            const vpg_shard_sync *sync = nullptr);
+vpg_status launch_sharded_emulated(const vpg_plan *const *plans, int G, const void *const *srcs, void *const *dsts,
+                                   void *stream, std::string *err);
 inline vpg_status launch_plan(const vpg_plan *p, const void *src, void *dst, void *stream, std::string *err) {
     return launch_plan(p, src, &dst, 1, stream, err);
 }

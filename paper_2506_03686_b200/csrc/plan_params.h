@@ -221,6 +221,15 @@ struct ShardArgs {
     // development tracing (VPG_TRACE, kernels.cu): per-CTA globaltimer
     // records of the tile pipeline; nullptr in normal launches
     unsigned long long *trace;
+    // device-side exchange barrier (sharded plans, epoch != 0; tile_body.cuh
+    // shard_barrier_*): flags[q] = rank q's flag block as seen from this
+    // device (2 x nshards u64: [0, G) "rank r started", [G, 2G) "rank r's
+    // accesses done"), monotonically increasing epoch per exchange call,
+    // this plan's rank, and a local CTA-completion counter (zero between calls)
+    unsigned long long *flags[kMaxShards];
+    unsigned long long epoch;
+    uint32_t rank;
+    uint32_t *done_ctr;
 };
 constexpr int kTraceWords = 64;     // per CTA: start, prologue issued, end, smid, then (tile, data ready, written) x 20
 

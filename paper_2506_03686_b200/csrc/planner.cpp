@@ -1445,10 +1445,11 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         P.G = shards;
         P.shard = shard_index;
         P.pull = pull;
-        if (pull) {
-            P.no_swz = true;     // chunk swizzle and TMA bulk reads assume one source buffer
-            P.no_bulk = true;
-        }
+        if (pull) P.no_swz = true;   // the chunk swizzle assumes one source buffer
+        // TMA bulk reads assume one source buffer (pull), and the bulk
+        // kernel's producer/consumer split carries no device-side exchange
+        // barrier (tile_body.cuh shard_barrier_*): exchanges stay per-lane
+        P.no_bulk = true;
     }
     const int rrank = (int)rdims.size();
     if (flags & VPG_NO_MERGE) {

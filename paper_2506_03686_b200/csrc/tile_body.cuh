@@ -706,6 +706,63 @@ __device__ __forceinline__ void cp_async_wait_pending(uint32_t n) {
 constexpr int kMaxStages = 8;
 constexpr int kRing = kMaxStages + 2;
 
+// ------------------------------------------------------------------ exchange barrier
+// Device-side ordering of a fused exchange across the G ranks' kernels
+// (ShardArgs::epoch != 0), instead of collectives around the launch:
+//   start: CTA 0 of rank r stores epoch into slot r of every rank's flag
+//          block (system-scope release, over NVLink for peers); every CTA
+//          waits until its own block's G start slots reach epoch before
+//          its first load -- every rank's kernel has started, so (stream
+//          order) every input shard is complete and every output shard free.
+//   end:   every CTA fences its stores system-wide and counts itself done;
+//          the last CTA of rank r stores epoch into done-slot r of every
+//          block and waits for its own G done-slots: the kernel (and hence
+//          the stream) completes only when every rank's stores have landed
+//          and every rank has finished reading.
+// Spins are bounded (~4 s of globaltimer): a missing rank makes the kernel
+// exit with an unfinished result instead of hanging the GPU.
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void wait_flags(const unsigned long long *f, uint32_t n, unsigned long long epoch) {
+    unsigned long long t0 = 0;
+    for (uint32_t q = 0; q < n; ++q) {
+        while (ld_acquire_sys(f + q) < epoch) {
+            const unsigned long long t = gtimer();
+            if (t0 == 0) t0 = t;
+            else if (t - t0 > 4000000000ull) return;   // bounded: never hang the device
+            __nanosleep(64);
+        }
+    }
+}
+__device__ __forceinline__ void shard_barrier_start(const ShardArgs &sa, uint32_t G, uint32_t cta) {
+    if (threadIdx.x == 0) {
+        if (cta == 0)
+            for (uint32_t q = 0; q < G; ++q) st_release_sys(sa.flags[q] + sa.rank, sa.epoch);
+        wait_flags(sa.flags[sa.rank], G, sa.epoch);
+    }
+    __syncthreads();
+}
+__device__ __forceinline__ void shard_barrier_end(const ShardArgs &sa, uint32_t G, uint32_t ncta) {
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t prev;
+        asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;\n" : "=r"(prev) : "l"(sa.done_ctr) : "memory");
+        if (prev == ncta - 1) {
+            atomicExch(sa.done_ctr, 0u);
+            __threadfence_system();
+            for (uint32_t q = 0; q < G; ++q) st_release_sys(sa.flags[q] + G + sa.rank, sa.epoch);
+            wait_flags(sa.flags[sa.rank] + G, G, sa.epoch);
+        }
+    }
+}
+
 // Persistent CTAs walk tiles t_k = blockIdx.x + k*gridDim.x through an
 // S-stage cp.async pipeline (S = p.nbuf smem tile buffers): the prologue
 // streams the source runs of the first S tiles; each iteration writes tile
@@ -715,7 +772,7 @@ constexpr int kRing = kMaxStages + 2;
 // buffer is filled by LDG+STS.
 template <typename W, bool ASYNC>
 __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restrict__ src, W *__restrict__ dst,
-                                          const ShardArgs &sa) {
+                                          const ShardArgs &sa, uint32_t cta, uint32_t ncta) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ int64_t s_base[kRing][2];
     __shared__ uint32_t s_valid[kRing][2];
@@ -724,9 +781,15 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
     // modulo 128 bytes as their source lines (see PhaseDesc::swz)
     unsigned char *const smem = smem_raw + ((128u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 127u)) & 127u);
     const uint32_t tid = threadIdx.x, NT = blockDim.x;
-    const uint32_t first = blockIdx.x, step = gridDim.x;
-    // (no static tile implies S * gridDim.x >= num_tiles: no dynamic claims either)
-    if (first >= p.num_tiles) return;
+    // CTA `cta` of the `ncta` CTAs running this plan (blockIdx.x / gridDim.x,
+    // except in the cooperative multi-rank emulation of an exchange)
+    const uint32_t first = cta, step = ncta;
+    const bool xbar = p.nshards > 1 && sa.epoch != 0;      // device-side exchange barrier
+    // (no static tile implies S * ncta >= num_tiles: no dynamic claims either)
+    if (first >= p.num_tiles) {
+        if (xbar) shard_barrier_end(sa, p.nshards, ncta);
+        return;
+    }
     const uint32_t S = ASYNC ? p.nbuf : 1u;
     const uint32_t R = S + 2;
     pdl_trigger();
@@ -761,7 +824,7 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
     auto signal_done = [&]() {
         // the last CTA to finish claiming resets the pair for the ring's next use
         __threadfence();
-        if (atomicAdd(sa.sched + 1, 1u) == gridDim.x - 1) {
+        if (atomicAdd(sa.sched + 1, 1u) == ncta - 1) {
             atomicExch(sa.sched, 0u);
             atomicExch(sa.sched + 1, 0u);
         }
@@ -848,6 +911,7 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
                                 s_base[slot][0] + p.src_span + 16 / (int64_t)sizeof(W) > p.n_elems);
     };
     pdl_wait();
+    if (xbar) shard_barrier_start(sa, p.nshards, cta);
     // prologue: fill every stage
     for (uint32_t j = 0; j < S; ++j) {
         if (s_ok[j]) load(j, p.off_buf + j * bstride);
@@ -923,7 +987,14 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
     }
     // peer stores of a sharded plan: performed system-wide before the grid
     // retires, so the exchange's completion barrier orders them
-    if (p.nshards > 1) __threadfence_system();
+    if (xbar) shard_barrier_end(sa, p.nshards, ncta);
+    else if (p.nshards > 1) __threadfence_system();
+}
+
+template <typename W, bool ASYNC>
+__device__ __forceinline__ void tile_body(const TileParams &p, const W *__restrict__ src, W *__restrict__ dst,
+                                          const ShardArgs &sa) {
+    tile_body<W, ASYNC>(p, src, dst, sa, blockIdx.x, gridDim.x);
 }
 
 

@@ -38,7 +38,7 @@ from dataclasses import dataclass
 from .core import LayoutError
 
 __all__ = ["ShardPlan", "plan_sharded", "permute_sharded", "permute_sharded_pipelined", "pipeline_chunks", "pipeline_spec",
-           "shard_bounds", "ShardExchange", "emulate_fused", "emulate_sharded_pipelined", "fused_supported",
+           "shard_bounds", "ShardExchange", "exchange_input", "emulate_fused", "emulate_sharded_pipelined", "fused_supported",
            "fused_method", "release_exchanges"]
 
 
@@ -223,12 +223,14 @@ def permute_sharded(local_in, global_shape, axes, group=None, local_permute=None
     the group must call it with the same shape/axes.
 
     method: "alltoall" -- P1 permute -> all_to_all_single -> P2 permute;
+    "pipelined" -- the same pipelined over chunks (permute_sharded_pipelined);
     "fused" -- one exchange kernel per rank over peer memory (ShardExchange:
-    push = stores into the peers' output shards, pull = reads from the
-    peers' input shards; the result is the exchange's buffer, overwritten by
-    the next fused call with the same arguments); "auto" -- fused when one
-    of the two keeps runs of at least 128 bytes on the remote side
-    (fused_method), else the all-to-all.
+    push = stores into the peers' output shards, whose result stays valid
+    until the second-next fused call with the same arguments; pull = reads
+    from the peers' input shards: produce the input in exchange_input(...)
+    to avoid a staging copy); "auto" -- fused when one of the two keeps runs
+    of at least 128 bytes on the remote side (fused_method), else pipelined
+    when the shard has a pipelining axis, else the all-to-all.
     """
     import torch
     import torch.distributed as dist
@@ -245,6 +247,9 @@ def permute_sharded(local_in, global_shape, axes, group=None, local_permute=None
             ex = _exchange_for(tuple(global_shape), tuple(axes), local_in.dtype, local_in.device, group)
             return ex(local_in)
     sp = plan or plan_sharded(global_shape, axes, G)
+    if method == "auto" and pipeline_chunks(sp) > 1:
+        return permute_sharded_pipelined(local_in, global_shape, axes, group=group, local_permute=local_permute,
+                                         plan=sp)
     if local_permute is None:
         from .api import permute as local_permute  # GPU kernels; no CPU fallback
     if local_in.numel() != sp.local_numel:
@@ -505,22 +510,29 @@ def fused_supported(global_shape, axes, elem_bytes, G) -> bool:
 class ShardExchange:
     """Fused sharded permutation for one process per GPU.
 
-    Every rank owns one output shard buffer; the buffers are exported with
-    CUDA IPC and mapped into every other rank (NVLink/NVSwitch peer memory).
-    A call runs ONE kernel per rank (vpg_permute_sharded): it reads the
-    local input shard tile by tile and stores each tile straight into the
-    output shard that owns it -- one HBM read, one write (local or remote),
-    no staging buffers and no all-to-all.  Two stream-ordered barriers order
-    the exchange: before (every output buffer is free) and after (every
-    rank's stores have landed).  With NCCL they are one-element all-reduces
-    on the current stream; with gloo (CPU transport, tests) the stream is
-    synchronised and the group barrier runs on the host.
+    A call runs ONE kernel per rank over CUDA IPC mappings of the peers'
+    buffers (NVLink/NVSwitch peer memory): one HBM read and one write per
+    element, no staging buffers and no all-to-all.
+      * push (vpg_permute_sharded): each rank reads its own input shard (any
+        contiguous tensor) and stores every tile into the output shard that
+        owns it.  The output shards are the exchange's registered buffers:
+        two of them, used alternately, so a result stays valid until the
+        call after next (``copy_out=True`` returns a private copy instead).
+      * pull (vpg_permute_sharded_pull): each rank writes its own output
+        shard (a fresh tensor, or ``out=``) and reads every tile's source runs
+        from the input shard that holds them.  The input shards are the
+        exchange's registered buffers: fill ``ex.input`` (``input_buffer()``)
+        and the call moves nothing else; any other tensor is first copied
+        into it.
+    Two stream-ordered barriers order the exchange: before (every input
+    complete, every output free) and after (every rank's accesses done).
+    With NCCL they are one-element all-reduces on the current stream; with
+    gloo (CPU transport, tests) the stream is synchronised and the group
+    barrier runs on the host.  Collective: all ranks construct and call it
+    with the same arguments."""
 
-    The result is a view of this rank's output buffer, overwritten by the
-    next call; copy it to keep it.  Collective: all ranks construct and call
-    it with the same arguments."""
-
-    def __init__(self, global_shape, axes, dtype, group=None, device=None, jit=None, mode="auto"):
+    def __init__(self, global_shape, axes, dtype, group=None, device=None, jit=None, mode="auto",
+                 copy_out=False, device_barrier=None):
         import torch
         import torch.distributed as dist
 
@@ -540,14 +552,51 @@ class ShardExchange:
         (self.program,) = _programs(global_shape, axes, es, self.G, [self.rank], jit=jit, pull=mode == "pull")
         self.splan = plan_sharded(global_shape, axes, self.G)
         self.local_numel = self.splan.local_numel
-        self.out = torch.empty(self.local_numel, dtype=dtype, device=self.device)
-        # pull: the peers read this rank's input from `self.input` (callers
-        # may fill it directly; __call__ copies any other tensor into it)
-        self.input = torch.empty(self.local_numel, dtype=dtype, device=self.device) if mode == "pull" else None
-        shared = self.input if mode == "pull" else self.out
+        self.copy_out = copy_out
+        self.calls = 0
+        # registered (peer-mapped) buffers: the input shard (pull) or two
+        # alternating output shards (push)
+        if mode == "pull":
+            self.input = torch.empty(self.local_numel, dtype=dtype, device=self.device)
+            shared = [self.input]
+        else:
+            self.input = None
+            self._outs = [torch.empty(self.local_numel, dtype=dtype, device=self.device) for _ in range(2)]
+            shared = self._outs
         self.backend = dist.get_backend(group) if dist.is_initialized() else None
         self._flag = torch.zeros(1, dtype=torch.float32, device=self.device)
         self._imported = []
+        self.peer_tables = [self._map(t) for t in shared]     # per buffer: G peer pointers
+        self.peers = self.peer_tables[0]
+        # device-side ordering (vpg_permute_sharded_sync) instead of the two
+        # collectives per call: NCCL jobs (one GPU per rank) by default;
+        # never with gloo, whose test ranks share one GPU (a flag wait could
+        # then hold SMs another rank's kernel needs)
+        import os
+
+        if device_barrier is None:
+            device_barrier = self.backend == "nccl" and self.G > 1 and os.environ.get("VPG_DEVICE_BARRIER", "1") != "0"
+        self.device_barrier = bool(device_barrier) and self.G > 1
+        self._sync = None
+        if self.device_barrier:
+            from . import _lib
+
+            self._flags = torch.zeros(2 * self.G, dtype=torch.int64, device=self.device)
+            self._done = torch.zeros(1, dtype=torch.int32, device=self.device)
+            fl = self._map(self._flags)
+            self._sync = _lib.ShardSync()
+            for q in range(self.G):
+                self._sync.flags[q] = fl[q]
+            self._sync.done_counter = self._done.data_ptr()
+
+    def _map(self, shared):
+        """Export `shared` and import every peer's counterpart (CUDA IPC);
+        returns the G buffer pointers in rank order (own first-hand)."""
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+
         L = _lib.lib()
         mine = (self.rank, bytes(0), 0)
         if self.G > 1:
@@ -557,20 +606,26 @@ class ShardExchange:
                 _check_ipc(L.vpg_ipc_export(ctypes.c_void_p(shared.data_ptr()), h, ctypes.byref(off)))
             mine = (self.rank, h.raw, off.value)
             allh = [None] * self.G
-            dist.all_gather_object(allh, mine, group=group)
+            dist.all_gather_object(allh, mine, group=self.group)
         else:
             allh = [mine]
-        self.peers = []
+        peers = []
         with torch.cuda.device(self.device):
             for q, hraw, off in sorted(allh):
                 if q == self.rank:
-                    self.peers.append(shared.data_ptr())
+                    peers.append(shared.data_ptr())
                     continue
                 ptr = ctypes.c_void_p()
                 buf = ctypes.create_string_buffer(hraw, _lib.VPG_IPC_HANDLE_BYTES)
                 _check_ipc(L.vpg_ipc_import(buf, ctypes.c_uint64(off), ctypes.byref(ptr)))
-                self.peers.append(ptr.value)
+                peers.append(ptr.value)
                 self._imported.append(ptr.value)
+        return peers
+
+    def input_buffer(self):
+        """Pull: the registered input shard -- write this rank's input here
+        and pass it to the call (no copy).  Push: None (any tensor works)."""
+        return self.input
 
     def _barrier(self):
         import torch
@@ -584,10 +639,10 @@ class ShardExchange:
             torch.cuda.current_stream(self.device).synchronize()
             dist.barrier(group=self.group)
 
-    def __call__(self, local_in, stream=None):
+    def __call__(self, local_in, stream=None, out=None):
         import torch
 
-        from .api import launch_sharded, launch_sharded_pull
+        from .api import launch_sharded, launch_sharded_pull, launch_sharded_sync
 
         if local_in.numel() != self.local_numel or local_in.dtype != self.dtype:
             raise LayoutError(f"rank {self.rank}: expected {self.local_numel} elements of {self.dtype}")
@@ -596,16 +651,37 @@ class ShardExchange:
         st = stream or torch.cuda.current_stream(self.device)
         with torch.cuda.stream(st):
             if self.mode == "pull":
+                if out is None:
+                    out = torch.empty(self.local_numel, dtype=self.dtype, device=self.device)
+                elif out.numel() != self.local_numel or out.dtype != self.dtype or not out.is_contiguous():
+                    raise LayoutError("out must be a contiguous tensor of the local output shard")
                 if local_in.data_ptr() != self.input.data_ptr():
-                    self.input.copy_(local_in.reshape(-1))
-                self._barrier()           # every input shard complete
-                launch_sharded_pull(self.program, self.peers, self.out.data_ptr(), ctypes.c_void_p(st.cuda_stream))
-                self._barrier()           # every reader done before inputs change
+                    self.input.copy_(local_in.reshape(-1))     # not the registered buffer: stage it
+                if self._sync is not None:
+                    self._sync.epoch = self.calls + 1          # same on every rank
+                    launch_sharded_sync(self.program, self.peers, [out.data_ptr()], self._sync,
+                                        ctypes.c_void_p(st.cuda_stream))
+                else:
+                    self._barrier()           # every input shard complete
+                    launch_sharded_pull(self.program, self.peers, out.data_ptr(), ctypes.c_void_p(st.cuda_stream))
+                    self._barrier()           # every reader done before inputs change
+                res = out
             else:
-                self._barrier()
-                launch_sharded(self.program, local_in.data_ptr(), self.peers, ctypes.c_void_p(st.cuda_stream))
-                self._barrier()
-        return self.out.view(self.splan.local_out_shape())
+                i = self.calls % 2        # alternate registered outputs
+                if self._sync is not None:
+                    self._sync.epoch = self.calls + 1
+                    launch_sharded_sync(self.program, [local_in.data_ptr()], self.peer_tables[i], self._sync,
+                                        ctypes.c_void_p(st.cuda_stream))
+                else:
+                    self._barrier()
+                    launch_sharded(self.program, local_in.data_ptr(), self.peer_tables[i],
+                                   ctypes.c_void_p(st.cuda_stream))
+                    self._barrier()
+                res = self._outs[i]
+                if self.copy_out or out is not None:
+                    res = (out.reshape(-1) if out is not None else torch.empty_like(res)).copy_(res)
+        self.calls += 1
+        return res.view(self.splan.local_out_shape())
 
     def close(self):
         from . import _lib
@@ -649,16 +725,38 @@ def _exchange_for(shape, axes, dtype, device, group):
     return ex
 
 
-def emulate_fused(x_flat, global_shape, axes, G, jit=None, mode="push", in_shards=None):
+def exchange_input(global_shape, axes, dtype, group=None, device=None):
+    """The tensor to produce this rank's input shard in for
+    permute_sharded(method="fused"/"auto"): the cached pull exchange's
+    registered input buffer (the call then launches one kernel and copies
+    nothing), else a fresh tensor (push exchange and the all-to-all path
+    take any input)."""
+    import torch
+    import torch.distributed as dist
+
+    G = dist.get_world_size(group) if dist.is_initialized() else 1
+    device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    es = torch.empty((), dtype=dtype).element_size()
+    if fused_supported(global_shape, axes, es, G):
+        ex = _exchange_for(tuple(global_shape), tuple(axes), dtype, device, group)
+        if ex.input is not None:
+            return ex.input
+    return torch.empty(plan_sharded(global_shape, axes, G).local_numel, dtype=dtype, device=device)
+
+
+def emulate_fused(x_flat, global_shape, axes, G, jit=None, mode="push", in_shards=None, device_barrier=False):
     """Run the G exchange kernels of the fused path on ONE device (virtual
-    ranks, every shard a local buffer; every kernel is independent).
-    mode "push": rank r reads input shard r and stores into every output
-    shard; "pull": rank r reads every input shard (``in_shards``, default
-    the slices of x_flat) and writes output shard r.  Returns the list of
-    per-rank output shards (flat)."""
+    ranks, every shard a local buffer).  mode "push": rank r reads input
+    shard r and stores into every output shard; "pull": rank r reads every
+    input shard (``in_shards``, default the slices of x_flat) and writes
+    output shard r.  ``device_barrier``: all ranks in ONE cooperative launch
+    ordered by the device-side exchange barrier (flag blocks, epochs) that
+    multi-GPU jobs use -- co-resident by construction, so no flag wait can
+    starve another rank; otherwise G independent launches.  Returns the
+    list of per-rank output shards (flat)."""
     import torch
 
-    from .api import launch_sharded, launch_sharded_pull
+    from .api import launch_sharded, launch_sharded_emulated, launch_sharded_pull
 
     n = x_flat.numel()
     progs = _programs(global_shape, axes, x_flat.element_size(), G, range(G), jit=jit, pull=mode == "pull")
@@ -668,6 +766,9 @@ def emulate_fused(x_flat, global_shape, axes, G, jit=None, mode="push", in_shard
     if in_shards is None:
         in_shards = [x_flat[slice(*shard_bounds(n, G, r))] for r in range(G)]
     srcs = [t.data_ptr() for t in in_shards]
+    if device_barrier:
+        launch_sharded_emulated(progs, srcs, ptrs, ctypes.c_void_p(st.cuda_stream))
+        return outs
     for r in range(G):
         if mode == "pull":
             launch_sharded_pull(progs[r], srcs, ptrs[r], ctypes.c_void_p(st.cuda_stream))

@@ -91,6 +91,21 @@ def _fused_worker(rank, world, port, q, mode="push"):
             torch.cuda.synchronize()
             if not np.array_equal(out.cpu().numpy().reshape(-1), want):
                 errs.append((shape, axes, step))
+        # results of consecutive calls do not alias (push: alternating
+        # registered outputs; pull: a fresh output per call)
+        o1 = ex(local)
+        o2 = ex(local)
+        torch.cuda.synchronize()
+        if o1.data_ptr() == o2.data_ptr() or not (np.array_equal(o1.cpu().numpy().reshape(-1), want)
+                                                   and np.array_equal(o2.cpu().numpy().reshape(-1), want)):
+            errs.append((shape, axes, "consecutive results"))
+        if mode == "pull":              # the registered input buffer: no staging copy
+            buf = ex.input_buffer()
+            buf.copy_(local)
+            o3 = ex(buf)
+            torch.cuda.synchronize()
+            if not np.array_equal(o3.cpu().numpy().reshape(-1), want):
+                errs.append((shape, axes, "registered input"))
         # permute_sharded(method="fused") builds its own cached exchange (a second mapping of the peers)
         out = permute_sharded(torch.from_numpy(g[lo:hi].copy()).cuda(), shape, axes, method="fused")
         torch.cuda.synchronize()
@@ -370,3 +385,37 @@ def test_pipelined_alltoall_cfg5_emulated(cuda, G):
     whole = permute(x.view(w.shape), w.axes).reshape(-1)
     torch.cuda.synchronize()
     assert torch.equal(torch.cat([o.reshape(-1) for o in outs]), whole)
+
+
+@pytest.mark.parametrize("mode", ["push", "pull"])
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_fused_exchange_device_barrier_emulated(cuda, G, mode):
+    """The device-side exchange barrier (flag blocks, epochs; no collective
+    around the launch): all G ranks' kernels in ONE cooperative launch on
+    this GPU, exactly the kernel code a multi-GPU job runs per rank through
+    vpg_permute_sharded_sync.  Bit-exact against the single-GPU permutation
+    on cfg5 and on small shapes with ragged tiles."""
+    import torch
+
+    from paper_2506_03686_b200 import LayoutError, permute
+    from paper_2506_03686_b200.sharded import emulate_fused
+    from paper_2506_03686_b200.workloads import CONFIGS
+
+    w = CONFIGS["cfg5"]
+    cases = [(w.shape, w.axes)] + list(FUSED_CASES)
+    ran = 0
+    for ci, (shape, axes) in enumerate(cases):
+        n = 1
+        for d in shape:
+            n *= d
+        x = torch.randint(-2**62, 2**62, (n,), dtype=torch.int64, device="cuda",
+                          generator=torch.Generator(device="cuda").manual_seed(100 + ci))
+        try:
+            outs = emulate_fused(x, shape, axes, G, mode=mode, device_barrier=True)
+        except LayoutError:
+            continue                      # no exchange plan for this shape / G
+        whole = permute(x.view(shape), axes).reshape(-1)
+        torch.cuda.synchronize()
+        assert torch.equal(torch.cat(outs), whole), (shape, axes, G, mode)
+        ran += 1
+    assert ran >= 2
