@@ -853,7 +853,9 @@ static vpg_status launch_ranks(const vpg_plan *const *plans, int G, const void *
                              : (int64_t)((uintptr_t)dsts[q] - (uintptr_t)dsts[0]) / E;
             sa.flags[q] = flags + (size_t)q * 2 * G;
         }
-        sa.epoch = 1;
+        // VPG_EMU_NO_BARRIER=1: same launch without the barrier (its cost, A/B)
+        static const bool nobar = getenv("VPG_EMU_NO_BARRIER") && atoi(getenv("VPG_EMU_NO_BARRIER")) != 0;
+        sa.epoch = nobar ? 0 : 1;
         sa.rank = (uint32_t)r;
         sa.done_ctr = ctrs + r;
         sv[r] = (const W *)(pull ? srcs[0] : srcs[r]);
