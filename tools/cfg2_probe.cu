@@ -11,12 +11,16 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstdint>
+#include <string>
 #include <vector>
 
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e_), __LINE__); exit(1); } } while (0)
 
-constexpr int NB = 32, C = 64, HW = 3136;
-constexpr size_t N = (size_t)NB * C * HW;
+// problem: NB batches of a C x HW -> HW x C transpose (cfg2: 32 x 64 x 3136;
+// cfg1: 1 x 4096 x 4096 via argv "cfg1"); tiles of 64 c x 64 hw
+__constant__ int d_NB, d_C, d_HW;
+static int NB = 32, C = 64, HW = 3136;
+static size_t N = (size_t)32 * 64 * 3136;
 
 // ------------------------------------------------------------------ flush
 __global__ void fill_k(float4 *p, size_t n) {
@@ -57,13 +61,16 @@ __global__ void copy_u(const float4 *__restrict__ a, float4 *__restrict__ b, siz
 template <int T>
 __global__ void __launch_bounds__(256) ldg_tile_k(const float *__restrict__ in, float *__restrict__ out) {
     constexpr int CH = T / 4;           // 16-byte chunks per c-row
-    __shared__ __align__(128) float4 s[C * CH];
-    const int tiles_per_n = HW / T;
-    const int n = blockIdx.x / tiles_per_n, h0 = (blockIdx.x % tiles_per_n) * T;
-    const float *src = in + ((size_t)n * C) * HW + h0;
-    float *dst = out + ((size_t)n * HW + h0) * C;
+    constexpr int CT = 64;              // c rows per tile
+    __shared__ __align__(128) float4 s[CT * CH];
+    const int C = d_C, HW = d_HW;
+    const int tiles_per_n = HW / T, ctiles = C / CT;
+    const int n = blockIdx.x / (tiles_per_n * ctiles), rem = blockIdx.x % (tiles_per_n * ctiles);
+    const int c0 = (rem / tiles_per_n) * CT, h0 = (rem % tiles_per_n) * T;
+    const float *src = in + ((size_t)n * C + c0) * HW + h0;
+    float *dst = out + ((size_t)n * HW + h0) * C + c0;
     const int tid = threadIdx.x;
-    constexpr int PER = C * CH / 256;
+    constexpr int PER = CT * CH / 256;
     float4 v[PER];
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
@@ -77,7 +84,7 @@ __global__ void __launch_bounds__(256) ldg_tile_k(const float *__restrict__ in, 
     }
     __syncthreads();
     // W: 4c x 4hw blocks; lanes: cb = lane%16 over c, hb across lanes/warps
-    constexpr int NBLK = (C / 4) * (T / 4);
+    constexpr int NBLK = (CT / 4) * (T / 4);
     for (int b = tid; b < NBLK; b += 256) {
         const int cb = b % 16, hb = b / 16;
         float4 r[4];
@@ -109,7 +116,8 @@ __global__ void __launch_bounds__(256) tma_tile_k(const __grid_constant__ CUtens
     __shared__ __align__(8) uint64_t bar[STAGES];
     const int tid = threadIdx.x;
     const int cnt = (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-    constexpr int tiles_per_n = HW / 64;
+    const int C = d_C, HW = d_HW;
+    const int tiles_per_n = HW / 64, ctiles = C / 64;
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(su32(&bar[s])));
@@ -117,14 +125,15 @@ __global__ void __launch_bounds__(256) tma_tile_k(const __grid_constant__ CUtens
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tm) : "memory");
         for (int k = 0; k < STAGES && k < cnt; ++k) {
             const int t = blockIdx.x + k * gridDim.x;
-            const int n = t / tiles_per_n, h0 = (t % tiles_per_n) * 64;
+            const int n = t / (tiles_per_n * ctiles), rem = t % (tiles_per_n * ctiles);
+            const int c0 = (rem / tiles_per_n) * 64, h0 = (rem % tiles_per_n) * 64;
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(&bar[k])), "r"(16384)
                          : "memory");
             for (int h = 0; h < 2; ++h)
                 asm volatile(
                     "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
                         su32(sm + k * 16384 + h * 8192)),
-                    "l"(&tm), "r"(h0 + 32 * h), "r"(0), "r"(n), "r"(su32(&bar[k]))
+                    "l"(&tm), "r"(h0 + 32 * h), "r"(c0), "r"(n), "r"(su32(&bar[k]))
                     : "memory");
         }
     }
@@ -133,14 +142,15 @@ __global__ void __launch_bounds__(256) tma_tile_k(const __grid_constant__ CUtens
     for (int k = 0; k < cnt; ++k) {
         const int st = k % STAGES;
         const int t = blockIdx.x + k * gridDim.x;
-        const int n = t / tiles_per_n, h0 = (t % tiles_per_n) * 64;
+        const int n = t / (tiles_per_n * ctiles), rem = t % (tiles_per_n * ctiles);
+        const int c0 = (rem / tiles_per_n) * 64, h0 = (rem % tiles_per_n) * 64;
         asm volatile(
             "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n" ::"r"(
                 su32(&bar[st])),
             "r"((k / STAGES) & 1)
             : "memory");
         const unsigned char *tile = sm + st * 16384;
-        float *dst = out + ((size_t)n * HW + h0) * C;
+        float *dst = out + ((size_t)n * HW + h0) * C + c0;
         // thread block: 4c x 4hw.  lane -> (j = lane & 7: hw chunk in half, cq = lane >> 3: c block 0..3)
         // warp -> (half = warp & 1, cgrp = warp >> 1: c blocks 4*cgrp .. +3)
         const int j = lane & 7, half = warp & 1, cb = (warp >> 1) * 4 + (lane >> 3);
@@ -160,14 +170,15 @@ __global__ void __launch_bounds__(256) tma_tile_k(const __grid_constant__ CUtens
         __syncthreads();
         if (tid == 0 && k + STAGES < cnt) {
             const int t2 = blockIdx.x + (k + STAGES) * gridDim.x;
-            const int n2 = t2 / tiles_per_n, h2 = (t2 % tiles_per_n) * 64;
+            const int n2 = t2 / (tiles_per_n * ctiles), rem2 = t2 % (tiles_per_n * ctiles);
+            const int c2 = (rem2 / tiles_per_n) * 64, h2 = (rem2 % tiles_per_n) * 64;
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(&bar[st])), "r"(16384)
                          : "memory");
             for (int h = 0; h < 2; ++h)
                 asm volatile(
                     "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
                         su32(sm + st * 16384 + h * 8192)),
-                    "l"(&tm), "r"(h2 + 32 * h), "r"(0), "r"(n2), "r"(su32(&bar[st]))
+                    "l"(&tm), "r"(h2 + 32 * h), "r"(c2), "r"(n2), "r"(su32(&bar[st]))
                     : "memory");
         }
     }
@@ -208,7 +219,17 @@ static void timeit(const char *name, F launch, const float *dout, const std::vec
     for (auto &e : ev) cudaEventDestroy(e);
 }
 
-int main() {
+int main(int argc, char **argv) {
+    if (argc > 1 && std::string(argv[1]) == "cfg1") {
+        NB = 1;
+        C = 4096;
+        HW = 4096;
+    }
+    N = (size_t)NB * C * HW;
+    CK(cudaMemcpyToSymbol(d_NB, &NB, 4));
+    CK(cudaMemcpyToSymbol(d_C, &C, 4));
+    CK(cudaMemcpyToSymbol(d_HW, &HW, 4));
+    printf("problem: %d x %d x %d f32 (C x HW -> HW x C per batch)\n", NB, C, HW);
     cudaStream_t s;
     CK(cudaStreamCreate(&s));
     int l2 = 0;
@@ -246,9 +267,9 @@ int main() {
         timeit("memcpy D2D", [&](cudaStream_t st) { cudaMemcpyAsync(dout, din, N * 4, cudaMemcpyDeviceToDevice, st); }, dout, none, s, bytes);
         return 0;
     }
-    timeit("ldg tile 64x64", [&](cudaStream_t st) { ldg_tile_k<64><<<NB * (HW / 64), 256, 0, st>>>(din, dout); },
+    timeit("ldg tile 64x64", [&](cudaStream_t st) { ldg_tile_k<64><<<NB * (HW / 64) * (C / 64), 256, 0, st>>>(din, dout); },
            dout, ref, s, bytes);
-    timeit("ldg tile 64x32", [&](cudaStream_t st) { ldg_tile_k<32><<<NB * (HW / 32), 256, 0, st>>>(din, dout); },
+    timeit("ldg tile 64x32", [&](cudaStream_t st) { ldg_tile_k<32><<<NB * (HW / 32) * (C / 64), 256, 0, st>>>(din, dout); },
            dout, ref, s, bytes);
 
     // TMA tensor map: 3-D {hw, c, n}, box {32, 64, 1}, SWIZZLE_128B
@@ -262,7 +283,7 @@ int main() {
     CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, din, gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) { printf("encode failed %d\n", (int)r); return 1; }
-    const int ntiles = NB * (HW / 64);
+    const int ntiles = NB * (HW / 64) * (C / 64);
     auto tma = [&](auto kern, int stages, int grid, const char *name) {
         const int smem = stages * 16384 + 1024;
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
