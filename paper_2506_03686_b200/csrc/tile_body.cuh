@@ -68,8 +68,10 @@ struct ThreadPart {
     bool active;
 };
 
-// VPG_HINTS (specialised kernels, experiments): bit 0 = source reads with an
-// L2 evict_first policy, bit 1 = streaming (.cs) destination stores.
+// VPG_HINTS (specialised kernels, experiments): bit 1 = streaming (.cs)
+// destination stores.  (Bit 0, L2 evict_first cp.async reads, was removed:
+// it measured no gain in round 1 and its cache-hinted cp.async faulted with
+// an illegal-instruction error on sm_100a in round 2.)
 #ifndef VPG_HINTS
 #define VPG_HINTS 0
 #endif
@@ -79,22 +81,10 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)_
 // cp.async of E bytes to the shared-window address s
 template <int E>
 __device__ __forceinline__ void cp_async(uint32_t s, const void *gp) {
-#if VPG_HINTS & 1
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
-    if constexpr (E == 16)
-        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gp), "l"(pol)
-                     : "memory");
-    else
-        asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], %2, %3;\n" ::"r"(s), "l"(gp), "n"(E),
-                     "l"(pol)
-                     : "memory");
-#else
     if constexpr (E == 16)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gp) : "memory");
     else
         asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gp), "n"(E) : "memory");
-#endif
 }
 
 template <typename W>
