@@ -231,7 +231,7 @@ struct ShardArgs {
     uint32_t rank;
     uint32_t *done_ctr;
 };
-constexpr int kTraceWords = 64;     // per CTA: start, prologue issued, end, smid, then (tile, data ready, written) x 20
+constexpr int kTraceWords = 64;     // per CTA: start, prologue issued, end, smid, (tile, data ready, written) x 19; [62] first load issue; [63] tiles
 
 // --------------------------------------------------------------------------
 // ROWS (K1): stride-1 preserved; each destination row of Lr elements is a

@@ -902,6 +902,7 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
     };
     pdl_wait();
     if (xbar) shard_barrier_start(sa, p.nshards, cta);
+    if (trc && tid == 0) trc[kTraceWords - 2] = gtimer();      // first load about to issue
     // prologue: fill every stage
     for (uint32_t j = 0; j < S; ++j) {
         if (s_ok[j]) load(j, p.off_buf + j * bstride);
@@ -953,7 +954,7 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
         if constexpr (ASYNC) cp_async_wait_pending(S - 1);
         __syncthreads();
         if (!s_ok[k % R]) break;           // uniform: this CTA has no tile k
-        if (trc && tid == 0 && k < 20) trc[4 + 3 * k + 1] = gtimer();
+        if (trc && tid == 0 && k < 19) trc[4 + 3 * k + 1] = gtimer();
         const uint32_t b = p.off_buf + (k % S) * bstride;
         {
             Lim lim;
@@ -963,7 +964,7 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
                           (uint32_t)s_base[slot][0], p.hmask);
         }
         __syncthreads();
-        if (trc && tid == 0 && k < 20) {
+        if (trc && tid == 0 && k < 19) {
             trc[4 + 3 * k] = (unsigned long long)(s_base[k % R][1]);
             trc[4 + 3 * k + 2] = gtimer();
         }

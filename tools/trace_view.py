@@ -41,7 +41,7 @@ def summarise(grid, ntiles, rec):
     first_ready = []
     for c in range(rec.shape[0]):
         prev = None
-        for k in range(min(int(ntile[c]), 20)):
+        for k in range(min(int(ntile[c]), 19)):
             r, w = int(rec[c, 4 + 3 * k + 1]), int(rec[c, 4 + 3 * k + 2])
             if r == 0 or w == 0:
                 break
@@ -56,6 +56,7 @@ def summarise(grid, ntiles, rec):
     print(f"grid {grid} ({rec.shape[0]} traced CTAs on {sms} SMs), tiles {ntiles}, tiles/CTA {pct(ntile * 1000)} (x1000)")
     print(f"  kernel span (first CTA start -> last CTA end): {(end.max() - t0) / 1e3:.2f} us")
     print(f"  CTA start after first (us):      {pct(start - t0)}")
+    print(f"  first load issue after start:    {pct(rec[:, kw - 2].astype(np.int64) - start)}")
     print(f"  prologue issued after start:     {pct(pro - start)}")
     print(f"  first tile ready after start:    {pct(first_ready)}")
     print(f"  W phase per tile:                {pct(done)}")
