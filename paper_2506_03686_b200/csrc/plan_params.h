@@ -142,8 +142,45 @@ struct PhaseDesc {
     uint32_t vrow;
 };
 
+// W phase as destination-linear 16-byte chunks ("lin" mode), for tiles whose
+// destination runs are misaligned or not a multiple of V = 16/E elements
+// long (cfg3: 270-element runs at arbitrary 4-byte offsets).  Each thread
+// takes V-element chunk slots q = tid, tid + nt, ...: run r = q / cpr, slot
+// c = q % cpr.  Slot c of a run whose first element sits at m = (address / E)
+// mod V covers run positions j = c*V - m .. c*V - m + V-1, i.e. the 16-byte
+// aligned destination chunk that contains them: V shared-memory loads and
+// ONE 16-byte store when all V positions are inside the run (head and tail
+// chunks store element by element).  Every store instruction of a warp then
+// covers whole 32-byte sectors, where a scalar walk of a misaligned run
+// splits every sector between two instructions.  The shared-memory offset
+// of run position j comes from a per-plan table built once per CTA:
+// u16 entries tab[m][c][e] = offset(c*V - m + e) (V shifted copies, so one
+// aligned V*2-byte load fetches a chunk's V offsets).
+constexpr int kMaxLinDims = 8;
+struct LinDesc {
+    uint32_t on;
+    uint32_t nt;                  // CTA threads the walk is laid out for
+    uint32_t run_len;             // elements of a full destination run
+    uint32_t cpr;                 // chunk slots per run: ceil((run_len + V - 1) / V)
+    FastDiv cprd;                 // divides by cpr
+    uint32_t nchunks;             // nruns * cpr
+    int32_t nrd;                  // destination-run dims (fastest first)
+    int32_t nxd;                  // run-index dims (fastest first)
+    int32_t last_slot;            // checked slot (0 = a, 1 = c) of the last run dim, -1 none
+    uint32_t last_unit;           // run positions per step of the last run dim
+    uint32_t tab_off;             // smem byte offset of the u16 offset tables (V * cpr * V entries)
+    // bank spreading: shared-memory load k of lane l fetches chunk element
+    // (k + (l >> rot_shift)) mod V (rotated back in registers before the
+    // store); the planner picks the shift with the fewest wavefronts
+    // (residue layouts fix every row stride modulo 32 banks, so the lanes'
+    // positions are the only freedom).  32 = no rotation.
+    uint32_t rot_shift;
+    PhaseDim rd[kMaxLinDims];     // run dims: div = extent, sstride (gstride unused: contiguous)
+    PhaseDim xd[kMaxPhaseDims];   // run-index dims: gstride = destination stride, sstride, slot
+};
+
 struct TileParams {
-    int64_t n_elems;               // elements of the whole tensor (source bounds in shifted-run mode)
+    int64_t n_elems;              // elements of the whole tensor (source bounds in shifted-run mode)
     uint32_t num_tiles;
     int32_t ngrid;
     uint32_t Ls, Ld;               // source / destination run lengths (elements)
@@ -205,8 +242,11 @@ struct TileParams {
     // elements stays inside the source needs no end-of-buffer check on its
     // aligned-superset reads (shifted-run mode), so its R walk is branch-free
     int64_t src_span;
+    LinDesc lin;
 };
-static_assert(sizeof(TileParams) <= 4096, "kernel parameter block must stay under 4 KB");
+// (kernel parameters beyond 4 KB need CUDA >= 12.1; the ShardArgs block
+// next to it already does)
+static_assert(sizeof(TileParams) <= 8192, "kernel parameter block must stay under 8 KB");
 
 // Per-launch destination table of a sharded tile plan: element offset of
 // output shard q relative to the kernel's dst pointer (shard 0).  Passed by

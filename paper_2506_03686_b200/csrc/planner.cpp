@@ -76,6 +76,9 @@ struct Problem {
     bool no_bulk = false;  // TMA bulk source reads off (VPG_BULK=0, pull exchanges)
     bool force_bulk = false; // TMA bulk source reads wherever they apply (VPG_BULK=1)
     bool no_swz = true;    // shifted-run chunk swizzle is opt-in (VPG_SWZ=1)
+    // W as destination-linear 16-byte chunks: 0 off (default: measured slower,
+    // tools/lin_ab.py), -1 cost model, 1 wherever it applies (VPG_LIN)
+    int lin_mode = 0;
     int r;
     int64_t d[kMaxRank];
     int sigma[kMaxRank];
@@ -331,6 +334,7 @@ struct VecChoice {
     bool w2 = false;       // (sw128 only) W in V x V register-transposed blocks with 16-byte stores
     bool swz_addr = true;  // (128-byte residue layouts) address swizzle; off when the bank model prefers plain
     bool res16 = false;    // residue modulus of one 16-byte chunk (TMA bulk reads of misaligned runs)
+    bool lin = false;      // W as destination-linear 16-byte chunks (LinDesc)
 };
 
 // smem strides of the tile dims for a given pitch (source run dense, run
@@ -738,6 +742,92 @@ bool sw128_possible(const Problem &Pb, const TileGeom &g) {
     return true;
 }
 
+// W as destination-linear 16-byte chunks (LinDesc, tile_write_lin): for 4-
+// and 8-byte words whose W phase would otherwise store one word per lane
+// (no vector grouping, no per-element shift), with destination runs of at
+// least 2 chunks and an offset table of at most 16 KiB.
+constexpr uint64_t kLinTableMax = 16384;
+uint64_t lin_table_bytes(int64_t Ld, int V) {
+    const uint64_t cpr = (uint64_t)((Ld + V - 2) / V + 1);
+    return (uint64_t)V * cpr * (uint64_t)V * 2;
+}
+
+bool lin_applicable(const Problem &Pb, const TileGeom &g, const VecChoice &vc) {
+    if (Pb.lin_mode == 0 || !(Pb.E == 4 || Pb.E == 8)) return false;
+    if (vc.vw > 1 || vc.w2 || vc.bulk || (vc.rshift && !vc.rres)) return false;
+    const int V = 16 / Pb.E;
+    if (g.Ld < 2 * V || g.ndst > kMaxLinDims || g.T / g.Ld > 0xffffffffLL) return false;
+    int nx = 0;
+    for (int k = 0; k < Pb.r; ++k)
+        if (g.ext[k] > 0) ++nx;
+    if (nx - g.ndst > kMaxPhaseDims) return false;
+    return lin_table_bytes(g.Ld, V) <= kLinTableMax;
+}
+
+// Run dims = the destination run (only its last dim may be partial, so the
+// valid positions of a ragged run are a prefix); run-index dims in
+// destination order.
+void fill_lin(const Problem &Pb, const TileGeom &g, const int64_t *sstr, const int *slot_of_dim, int NT,
+              TileParams &tp) {
+    LinDesc &L = tp.lin;
+    const int V = 16 / Pb.E;
+    L.on = 1;
+    L.nt = (uint32_t)NT;
+    L.run_len = (uint32_t)g.Ld;
+    L.cpr = (uint32_t)((g.Ld + V - 2) / V + 1);
+    L.cprd = make_fastdiv(L.cpr);
+    L.nchunks = (uint32_t)(g.T / g.Ld) * L.cpr;
+    bool in_run[kMaxRank] = {false};
+    L.nrd = g.ndst;
+    for (int i = 0; i < g.ndst; ++i) {
+        const int k = g.dst_dims[i];
+        in_run[k] = true;
+        set_pdim(L.rd[i], g.ext[k], Pb.out_stride_of_dim[k], sstr[k], i + 1 == g.ndst ? slot_of_dim[k] : -1, 1);
+    }
+    const int kl = g.dst_dims[g.ndst - 1];
+    L.last_slot = slot_of_dim[kl];
+    L.last_unit = (uint32_t)(g.Ld / g.ext[kl]);
+    L.nxd = 0;
+    for (int j = 0; j < Pb.r; ++j) {
+        const int k = Pb.sigma[j];
+        if (g.ext[k] == 0 || in_run[k]) continue;
+        set_pdim(L.xd[L.nxd++], g.ext[k], Pb.out_stride_of_dim[k], sstr[k], slot_of_dim[k], 1);
+    }
+}
+
+// smem element offset of destination-run position j (host mirror of the
+// kernel's table entries)
+uint32_t lin_offset(const LinDesc &L, uint32_t j) {
+    uint32_t off = 0;
+    for (int k = 0; k < L.nrd; ++k) {
+        const uint32_t e = L.rd[k].div.d, q = j / e;
+        off += (j - q * e) * L.rd[k].sstride;
+        j = q;
+    }
+    return off;
+}
+
+// smem wavefronts of one warp's V loads of a chunk step (lanes on chunk
+// slots 0..31 of a run, averaged over the run's start offsets m) with the
+// bank-spreading rotation `rs` (32 = none)
+double lin_waves(const Problem &Pb, const PhaseDesc &d, const LinDesc &L, uint32_t rs) {
+    const int V = 16 / Pb.E;
+    uint32_t off[32];
+    double waves = 0.0;
+    for (int m = 0; m < V; ++m)
+        for (int k = 0; k < V; ++k) {
+            int nl = 0;
+            for (int l = 0; l < 32; ++l) {
+                const int e = (k + (rs < 32 ? (l >> rs) : 0)) & (V - 1);
+                const int j = l * V + e - m;
+                if (j < 0 || j >= (int)L.run_len) continue;
+                off[nl++] = host_swizzle(d, lin_offset(L, (uint32_t)j), V);
+            }
+            if (nl) waves += warp_wavefronts(off, nl, Pb.E);
+        }
+    return waves / V;
+}
+
 // Fill TileParams for geometry g, smem pitch (elements) and vector choice.
 double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, int NT, VecChoice vc,
                         TileParams &tp) {
@@ -769,6 +859,7 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
         tp.ph[1].w2 = 1;
         tp.ph[1].vrow = (uint32_t)sstr[Pb.sigma[0]];    // == pitch (w2_vectorizable)
     }
+    if (vc.lin) fill_lin(Pb, g, sstr, slot_of_dim, NT, tp);
     tp.ph[0].rshift = vc.rshift ? (vc.rres ? 2u : 1u) : 0u;
     tp.hmask = (uint32_t)hmask;
     tp.rres = vc.rres ? (uint32_t)(M - 1) : 0u;
@@ -783,6 +874,18 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
             tp.ph[ph].swz = vc.sw128 ? (vc.w2 ? 1u + lv : 1u) : (uint32_t)vc.swz;
             tp.ph[ph].spitch = make_fastdiv(pitch);
         }
+    }
+    if (tp.lin.on) {
+        uint32_t best_rs = 32;
+        double best_w = lin_waves(Pb, tp.ph[1], tp.lin, 32);
+        for (uint32_t rs = 0; rs < 3; ++rs) {
+            const double w = lin_waves(Pb, tp.ph[1], tp.lin, rs);
+            if (w < best_w - 1e-9) {
+                best_w = w;
+                best_rs = rs;
+            }
+        }
+        tp.lin.rot_shift = best_rs;
     }
     if (vc.bulk) {
         tp.bulk = 1;
@@ -882,6 +985,9 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
         buf_bytes = (buf_bytes + 127) / 128 * 128;
         tp.tile_elems_alloc = (uint32_t)(buf_bytes / Pb.E);
     }
+    // lin mode: u16 table entries hold smem element offsets inside one buffer
+    if (tp.lin.on && tp.tile_elems_alloc >= 65536u) memset(&tp.lin, 0, sizeof(tp.lin));
+    if (tp.lin.on) tp.lin.tab_off = take(lin_table_bytes(g.Ld, V), 16);
     // pipeline depth: as many stages as fit the per-CTA smem target (two
     // CTAs per SM), at least 2, at most 8; 1- and 2-byte words use 1.
     uint32_t stages = 1;
@@ -904,6 +1010,16 @@ double tile_cost(const Problem &Pb, const TileParams &tp) {
     int nl;
     for (int ph = 0; ph < 2; ++ph) {
         const PhaseDesc &d = tp.ph[ph];
+        if (ph == 1 && tp.lin.on) {
+            // lin W: per warp chunk step one table load, V scalar smem loads
+            // (lanes on consecutive chunk slots of one run) and one 16-byte
+            // store, plus the slot decode
+            const LinDesc &L = tp.lin;
+            const double waves = lin_waves(Pb, d, L, L.rot_shift);
+            const double ops = std::ceil((double)L.nchunks / 32.0);
+            cost += ops * (1.0 + waves + 1.0 + 2.0);
+            continue;
+        }
         const int V = (int)d.vec;
         const int abytes = Pb.E * V;
         int64_t waves = 0, warps = 0;
@@ -956,6 +1072,25 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
     // factor) only where the rows are congruent to their source lines
     const bool s128 = rv && !Pb.no_sw128 && sw128_layout_ok(Pb, g);
     const double s128_factor = sw128_possible(Pb, g) ? kSw128CostFactor : 1.0;
+    // the same layout with the W phase as destination-linear 16-byte chunks
+    auto lin_try = [&](VecChoice vc, uint32_t pitch, double factor) {
+        if (!lin_applicable(Pb, g, vc)) return;
+        vc.lin = true;
+        TileParams tp;
+        fill_tile_params(Pb, g, pitch, NT, vc, tp);
+        if (!tp.lin.on) return;
+        double c = tile_cost(Pb, tp) * factor;
+        if (Pb.lin_mode == 1) c *= 1e-6;    // forced wherever it applies
+        if (getenv("VPG_DEBUG_PLAN"))
+            fprintf(stderr, "[plan] Ls %lld Ld %lld pitch %u vr %d rshift %d rres %d swz %d lin cost %.1f per-elem %.3f\n",
+                    (long long)g.Ls, (long long)g.Ld, pitch, vc.vr, (int)vc.rshift, (int)vc.rres, (int)vc.swz_addr,
+                    c, c / (double)g.T);
+        if (best < 0 || c < best - 1e-9) {
+            best = c;
+            pitch_out = pitch;
+            vc_out = vc;
+        }
+    };
     for (const Opt &op : opts) {
         if (s128 && op.vr > 1 && !op.rshift && (int64_t)(g.T / g.Ls) * g.Ls * Pb.E <= Pb.budget + 8192) {
             // congruent rows (pitch = run, no padding), chunk swizzle against
@@ -979,6 +1114,7 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
                     pitch_out = (uint32_t)g.Ls;
                     vc_out = vc;
                 }
+                lin_try(vc, (uint32_t)g.Ls, s128_factor);
             }
         }
         if (op.rshift && !Pb.no_swz) {
@@ -1035,6 +1171,7 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
                     pitch_out = pitch;
                     vc_out = vc;
                 }
+                lin_try(vc, pitch, kResidueCostFactor * (res_modulus(Pb.E) * Pb.E >= 128 ? kSw128CostFactor : 1.0));
             }
         }
         if (op.rshift && Pb.force_bulk && !Pb.no_bulk && g.n_runidx <= kMaxPhaseDims) {
@@ -1094,6 +1231,7 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
                 pitch_out = pitch;
                 vc_out = vc;
             }
+            lin_try(vc, pitch, 1.0);
         }
     }
 }
@@ -1297,6 +1435,12 @@ static void describe(vpg_plan *p) {
                    : (t.ph[0].rshift == 2 ? " (aligned supersets of misaligned runs, residue row strides)"
                                        : t.ph[0].rshift ? " (aligned supersets of misaligned runs)" : ""),
             t.ph[1].vec, t.ph[1].w2 ? " (VxV register-transposed blocks, 16-byte stores)" : "");
+        if (t.lin.on)
+            put("W lin: destination-linear %u-byte chunks, one store each (runs of %u elements, %u chunk slots x %u "
+                "runs, offset table %u bytes, bank rotation %s%u)\n",
+                16u, t.lin.run_len, t.lin.cpr, t.lin.nchunks / t.lin.cpr,
+                (unsigned)lin_table_bytes(t.lin.run_len, 16 / p->elem_bytes), t.lin.rot_shift < 32 ? "lane >> " : "none",
+                t.lin.rot_shift < 32 ? t.lin.rot_shift : 0u);
         put("lane utilisation (R*W): %.3f\n", p->tile_util);
         put("specialised (NVRTC) kernel: %s\n", p->jit ? "yes" : "no");
         put("tiles: %u, grid digits: %d\n", t.num_tiles, t.ngrid);
@@ -1420,6 +1564,7 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
     if (getenv("VPG_NO_RES")) P.no_res = true;
     if (getenv("VPG_NO_SW128")) P.no_sw128 = true;
     if (getenv("VPG_NO_W2")) P.no_w2 = true;
+    if (const char *e = getenv("VPG_LIN")) P.lin_mode = *e ? atoi(e) : 0;
     if (getenv("VPG_NO_SWZ_ADDR")) P.no_swz_addr = true;
     // the chunk swizzle removes the W bank conflicts of shifted runs but costs
     // a divide and a few integer ops per element: measured 28.4 vs 20.5 us on
@@ -1619,6 +1764,7 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         vs.rshift = false;
         vs.bulk = false;
         vs.w2 = false;      // 16-byte destination stores need an aligned dst too
+        vs.lin = false;
         fill_tile_params(P, g, pitch, threads, vs, p->tile_unaligned);
         // the tile count must fit the 32-bit tile index
         double nt = 1.0;

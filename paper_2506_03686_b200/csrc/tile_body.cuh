@@ -509,11 +509,56 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
     }
 }
 
+#ifdef VPG_JIT
+// Scalar W walk of specialised kernels with a short inner dim (n_in < 4):
+// the thread's (outer, inner) positions flattened and taken U at a time,
+// all U smem loads ahead of the U stores (the nested walk issued each
+// load-store pair back to back, one smem latency per element).
+template <typename W>
+__device__ __forceinline__ void tile_write_flat(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
+                                                W *__restrict__ gdst, uint32_t bb, uint32_t mask, const Lim lim,
+                                                uint32_t hb, uint32_t hmask) {
+    constexpr int U = 8;
+    const uint32_t o0 = d.ngroups == 1 ? 0u : t.grp;
+    const uint32_t n_o = d.n_outer > o0 ? (d.n_outer - o0 + d.ngroups - 1) / d.ngroups : 0u;
+    const uint32_t total = n_o * d.n_in;
+    VPG_UNROLL
+    for (uint32_t b0 = 0; b0 < total; b0 += U) {
+        W v[U];
+        W *gp[U];
+        bool ok[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t idx = b0 + u;
+            ok[u] = idx < total;
+            const uint32_t oi = idx / d.n_in, i = idx - oi * d.n_in;
+            const OuterEntry e = outer_entry(d, smem, o0 + oi * d.ngroups);
+            gp[u] = gdst + (t.g + e.g) + (int64_t)i * d.g_in;
+            const uint32_t s = t.s + e.s + i * d.s_in;
+            const uint32_t hh = hb + t.h + e.h + i * d.h_in;
+            if (mask)
+                ok[u] = ok[u] && slot_ok(mask, t.c0 + e.c0 + i * d.c_in[0], t.c1 + e.c1 + i * d.c_in[1],
+                                         t.c2 + i * d.c_in[2], lim);
+            if (ok[u]) v[u] = *sptr<W>(smem, soff<W>(d, bb, s + (hh & hmask)));
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (ok[u]) st_out(gp[u], v[u]);
+    }
+}
+#endif
+
 template <typename W>
 __device__ __forceinline__ void tile_write(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
                                            W *__restrict__ gdst, uint32_t bb, uint32_t mask,
                                            const Lim lim, uint32_t hb, uint32_t hmask) {
     if (!t.active) return;
+#if defined(VPG_JIT) && !defined(VPG_NO_FLAT)
+    if (d.vec <= 1 && !d.w2 && d.n_in < 4) {
+        tile_write_flat<W>(d, t, smem, gdst, bb, mask, lim, hb, hmask);
+        return;
+    }
+#endif
     if constexpr (sizeof(W) == 4 || sizeof(W) == 8) {
         if (d.w2) {
             tile_write_w2<W>(d, t, smem, gdst, bb, mask, lim);
@@ -525,6 +570,145 @@ __device__ __forceinline__ void tile_write(const PhaseDesc &d, const ThreadPart 
         }
     }
     tile_write_impl<W, false>(d, t, smem, gdst, bb, mask, lim, hb, hmask);
+}
+
+// W phase, lin mode (LinDesc in plan_params.h): the per-plan table of u16
+// smem offsets, tab[m][c][e] = offset of destination-run position
+// c*V - m + e (0 outside the run), built once per CTA.
+template <int V>
+__device__ __forceinline__ void lin_build_table(const LinDesc &L, unsigned char *smem, uint32_t tid, uint32_t NT) {
+    uint16_t *tab = reinterpret_cast<uint16_t *>(smem + L.tab_off);
+    const uint32_t per_m = L.cpr * V;
+    for (uint32_t i = tid; i < V * per_m; i += NT) {
+        const uint32_t m = i / per_m;
+        const int32_t j = (int32_t)(i - m * per_m) - (int32_t)m;
+        uint32_t off = 0;
+        if (j >= 0 && (uint32_t)j < L.run_len) {
+            uint32_t x = (uint32_t)j;
+            VPG_UNROLL
+            for (int k = 0; k < kMaxLinDims; ++k) {
+                if (k >= L.nrd) break;
+                const uint32_t q = fdiv(x, L.rd[k].div);
+                off += (x - q * L.rd[k].div.d) * L.rd[k].sstride;
+                x = q;
+            }
+        }
+        tab[i] = (uint16_t)off;
+    }
+}
+
+// a[k] <- a[(k + r) mod V] (selects, r lane-dependent)
+template <int V, typename T>
+__device__ __forceinline__ void rot_left(T (&a)[V], uint32_t r) {
+    if constexpr (V == 4) {
+        if (r & 2u) {
+            T t0 = a[0], t1 = a[1];
+            a[0] = a[2];
+            a[1] = a[3];
+            a[2] = t0;
+            a[3] = t1;
+        }
+        if (r & 1u) {
+            T t = a[0];
+            a[0] = a[1];
+            a[1] = a[2];
+            a[2] = a[3];
+            a[3] = t;
+        }
+    } else if constexpr (V == 2) {
+        if (r & 1u) {
+            T t = a[0];
+            a[0] = a[1];
+            a[1] = t;
+        }
+    }
+}
+
+// Chunk slots q = tid, tid + nt, ...: run r = q / cpr over the run-index
+// dims, slot c = q % cpr.  The run starts at word m of its 16-byte chunk
+// (from the address), so slot c covers run positions j0 = c*V - m ..
+// j0 + V-1: V smem loads (offsets from one table load; positions outside
+// the run read offset 0, harmlessly) and one aligned 16-byte store when all
+// V positions are valid, element stores otherwise (run head and tail, and
+// ragged tiles, whose valid positions are a prefix of Lv).
+template <typename W>
+__device__ __forceinline__ void tile_write_lin(const TileParams &p, const unsigned char *smem,
+                                               W *__restrict__ gdst, uint32_t bb, bool ragged, const Lim lim,
+                                               uint32_t tid) {
+    constexpr int V = 16 / (int)sizeof(W);
+    const LinDesc &L = p.lin;
+    const PhaseDesc &d = p.ph[1];
+    if (tid >= L.nt) return;
+    uint32_t Lv = L.run_len;
+    if (ragged && L.last_slot >= 0) Lv = L.last_unit * (L.last_slot == 0 ? lim.l0 : lim.l1);
+    // bank spreading: load k of this lane fetches chunk element (k + rot) mod V
+    const uint32_t rot = L.rot_shift < 32 ? ((tid & 31u) >> L.rot_shift) & (uint32_t)(V - 1) : 0u;
+    // batches of B chunk slots per thread: every smem load of a batch issues
+    // before its first store
+    constexpr int B = 4;
+    VPG_UNROLL
+    for (uint32_t q0 = tid; q0 < L.nchunks; q0 += B * L.nt) {
+        alignas(16) W v[B][V];
+        W *cp[B];
+        int32_t j0[B];
+        bool live[B];
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            const uint32_t q = q0 + b * L.nt;
+            live[b] = q < L.nchunks;
+            const uint32_t r = fdiv(q, L.cprd);
+            const uint32_t c = q - r * L.cpr;
+            int64_t go = 0;
+            uint32_t so = 0;
+            uint32_t x = r;
+            VPG_UNROLL
+            for (int i = 0; i < kMaxPhaseDims; ++i) {
+                if (i >= L.nxd) break;
+                const uint32_t qq = fdiv(x, L.xd[i].div);
+                const uint32_t dg = x - qq * L.xd[i].div.d;
+                x = qq;
+                go += (int64_t)dg * L.xd[i].gstride;
+                so += dg * L.xd[i].sstride;
+                if (L.xd[i].slot >= 0 && ragged) live[b] = live[b] && dg < (L.xd[i].slot == 0 ? lim.l0 : lim.l1);
+            }
+            W *const rp = gdst + go;
+            const uint32_t m = (uint32_t)(reinterpret_cast<uintptr_t>(rp) / sizeof(W)) & (uint32_t)(V - 1);
+            j0[b] = (int32_t)(c * V) - (int32_t)m;
+            cp[b] = rp + j0[b];      // 16-byte aligned
+            if (!live[b]) continue;
+            const unsigned char *tq = smem + L.tab_off + (m * L.cpr + c) * (uint32_t)(V * 2);
+            uint32_t offs[V];
+            if constexpr (V == 4) {
+                const uint2 t = *reinterpret_cast<const uint2 *>(tq);
+                offs[0] = t.x & 0xffffu;
+                offs[1] = t.x >> 16;
+                offs[2] = t.y & 0xffffu;
+                offs[3] = t.y >> 16;
+            } else {
+                const uint32_t t = *reinterpret_cast<const uint32_t *>(tq);
+                offs[0] = t & 0xffffu;
+                offs[1] = t >> 16;
+            }
+            rot_left<V>(offs, rot);
+#pragma unroll
+            for (int e = 0; e < V; ++e) v[b][e] = *sptr<W>(smem, soff<W>(d, bb, so + offs[e]));
+            rot_left<V>(v[b], (uint32_t)V - rot);
+        }
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            if (!live[b]) continue;
+            bool all = true;
+#pragma unroll
+            for (int e = 0; e < V; ++e) all = all && (uint32_t)(j0[b] + e) < Lv;
+            if (all) {
+                st_out(reinterpret_cast<uint4 *>(cp[b]), *reinterpret_cast<const uint4 *>(v[b]));
+            } else {
+#pragma unroll
+                for (int e = 0; e < V; ++e)
+                    if ((uint32_t)(j0[b] + e) < Lv) st_out(cp[b] + e, v[b][e]);
+            }
+        }
+    }
 }
 
 // Warp 0 decodes tile `t` into slot `k`: source/destination base offsets and
@@ -909,6 +1093,9 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
         if constexpr (ASYNC) cp_async_commit();
     }
     if (trc && tid == 0) trc[1] = gtimer();
+    // lin W: the offset table (ordered before the first W by the loop's barrier)
+    if constexpr (sizeof(W) == 4 || sizeof(W) == 8)
+        if (p.lin.on) lin_build_table<16 / (int)sizeof(W)>(p.lin, smem, tid, NT);
     uint32_t tiles_done = 0;
     for (uint32_t k = 0;; ++k) {
         // claim + decode the tile of slot k+S
@@ -960,8 +1147,17 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
             Lim lim;
             const uint32_t slot = k % R;
             const uint32_t m = limits(slot, 1, lim);
-            tile_write<W>(p.ph[1], tw, smem, dst + s_base[slot][1], shifted(b, slot), m, lim,
-                          (uint32_t)s_base[slot][0], p.hmask);
+            bool lin_done = false;
+            if constexpr (sizeof(W) == 4 || sizeof(W) == 8) {
+                if (p.lin.on) {
+                    tile_write_lin<W>(p, smem, dst + s_base[slot][1], shifted(b, slot),
+                                      !(lim.l0 == p.e_a && lim.l1 == p.e_c), lim, tid);
+                    lin_done = true;
+                }
+            }
+            if (!lin_done)
+                tile_write<W>(p.ph[1], tw, smem, dst + s_base[slot][1], shifted(b, slot), m, lim,
+                              (uint32_t)s_base[slot][0], p.hmask);
         }
         __syncthreads();
         if (trc && tid == 0 && k < 19) {

@@ -48,6 +48,17 @@ class GridDigit(ctypes.Structure):
     _fields_ = [("cum", FastDiv), ("ext", FastDiv), ("src_stride", ctypes.c_int64), ("dst_stride", ctypes.c_int64)]
 
 
+MAXLIN = 8
+
+
+class LinDesc(ctypes.Structure):
+    _fields_ = [("on", ctypes.c_uint32), ("nt", ctypes.c_uint32), ("run_len", ctypes.c_uint32),
+                ("cpr", ctypes.c_uint32), ("cprd", FastDiv), ("nchunks", ctypes.c_uint32),
+                ("nrd", ctypes.c_int32), ("nxd", ctypes.c_int32), ("last_slot", ctypes.c_int32),
+                ("last_unit", ctypes.c_uint32), ("tab_off", ctypes.c_uint32), ("rot_shift", ctypes.c_uint32),
+                ("rd", PhaseDim * MAXLIN), ("xd", PhaseDim * MAXPD)]
+
+
 class TileParams(ctypes.Structure):
     _fields_ = [("n_elems", ctypes.c_int64), ("num_tiles", ctypes.c_uint32), ("ngrid", ctypes.c_int32),
                 ("Ls", ctypes.c_uint32), ("Ld", ctypes.c_uint32), ("T", ctypes.c_uint32),
@@ -63,7 +74,7 @@ class TileParams(ctypes.Structure):
                 ("nshards", ctypes.c_uint32), ("tile_begin", ctypes.c_uint32), ("src_bias", ctypes.c_int64),
                 ("shard_elems", ctypes.c_int64), ("rres", ctypes.c_uint32), ("pull", ctypes.c_uint32),
                 ("shard_shift", ctypes.c_uint32), ("shard_div", FastDiv), ("pad_pull_", ctypes.c_uint32),
-                ("dst_bias", ctypes.c_int64), ("src_span", ctypes.c_int64)]
+                ("dst_bias", ctypes.c_int64), ("src_span", ctypes.c_int64), ("lin", LinDesc)]
 
 
 def tile_params(program) -> TileParams:
@@ -109,11 +120,17 @@ def check_layout(tp: TileParams, E: int) -> None:
     t1 = (tp.ph[1].off_tab, tp.ph[1].off_tab + ENTRY * tp.ph[1].n_outer)
     buf = ((tp.tile_elems_alloc * E + 15) // 16) * 16
     b = (tp.off_buf, tp.off_buf + buf * tp.nbuf)
-    regs = sorted([t0, t1, b])
+    regs = [t0, t1, b]
+    if tp.lin.on:
+        V = 16 // E
+        regs.append((tp.lin.tab_off, tp.lin.tab_off + V * tp.lin.cpr * V * 2))
+        if tp.lin.tab_off % 16:
+            raise SimError("lin offset table misaligned")
+    regs = sorted(regs)
     for (a0, a1), (b0, b1) in zip(regs, regs[1:]):
         if a1 > b0 and a1 > a0 and b1 > b0:
             raise SimError(f"smem regions overlap: {regs}")
-    if b[1] > tp.smem_bytes or tp.off_buf % 16:
+    if max(r[1] for r in regs) > tp.smem_bytes or tp.off_buf % 16:
         raise SimError(f"buffers exceed smem_bytes or misaligned: {b} vs {tp.smem_bytes}")
     if tp.smem_bytes > 227 * 1024:
         raise SimError("more dynamic smem than a CTA can have")
@@ -232,6 +249,9 @@ def simulate(program, src_words: np.ndarray, threads: int | None = None, shard_o
                 smem_valid[sa:sa + nel] = True
         for ph in range(2):
             if ph == 0 and tp.bulk:
+                continue
+            if ph == 1 and tp.lin.on:
+                _lin_write(tp, E, db, smem, smem_valid, tbase, dst, written, dbound, full, lim, t)
                 continue
             d, grp, active, tg, ts, tc, th = parts[ph]
             mask = d.mask_full if full else d.mask_ragged
@@ -362,6 +382,63 @@ def simulate_exchange(programs, src_words: np.ndarray) -> np.ndarray:
         bad = np.nonzero(c != 1)[0][:5]
         raise SimError(f"destination elements written {c[bad]} times at {bad}")
     return np.concatenate(dsts)
+
+
+def _lin_offsets(L, j):
+    """smem offsets of destination-run positions j (the kernel's table entries)."""
+    j = np.asarray(j, dtype=np.int64).copy()
+    off = np.zeros_like(j)
+    for k in range(L.nrd):
+        e = L.rd[k].div.d
+        off += (j % e) * L.rd[k].sstride
+        j //= e
+    return off
+
+
+def _lin_write(tp, E, db, smem, smem_valid, tbase, dst, written, dbound, full, lim, t):
+    """W phase in lin mode (tile_write_lin): chunk slots over runs, each the
+    16-byte aligned destination chunk holding run positions c*V - m ..
+    c*V - m + V-1 (m = the run start's word offset in its chunk; destination
+    buffers are 16-byte aligned)."""
+    L = tp.lin
+    V = 16 // E
+    d = tp.ph[1]
+    if L.cpr != (L.run_len + V - 2) // V + 1 or L.nchunks % L.cpr:
+        raise SimError("lin: chunk slot count does not cover every alignment")
+    Lv = L.run_len
+    if not full and L.last_slot >= 0:
+        Lv = L.last_unit * lim[L.last_slot]
+    q = np.arange(L.nchunks, dtype=np.int64)
+    r, c = q // L.cpr, q % L.cpr
+    go, so, cs, _ = _decode(r, L.xd, L.nxd)
+    live = np.ones(q.shape, dtype=bool)
+    if not full:
+        for i in range(L.nxd):
+            if L.xd[i].slot >= 0:
+                live &= cs[L.xd[i].slot] < lim[L.xd[i].slot]
+    rp = db + go
+    m = rp % V
+    j0 = c * V - m
+    for e in range(V):
+        j = j0 + e
+        ok = live & (j >= 0) & (j < Lv)
+        if not ok.any():
+            continue
+        if (j[ok] >= L.run_len).any():
+            raise SimError("lin: position beyond the destination run")
+        sp = so[ok] + _lin_offsets(L, j[ok]) + tbase
+        if (_lin_offsets(L, j[ok]) >= 65536).any():
+            raise SimError("lin: smem offset does not fit the u16 table")
+        spx = _swizzle(d, sp, 16 // E)
+        _chk(spx, smem.size - 64, "W lin smem")
+        dd = rp[ok] + j[ok]
+        _chk(dd, dbound, "W lin global")
+        if ((rp[ok] + j0[ok]) % V).any():
+            raise SimError("lin: chunk store not 16-byte aligned")
+        if not smem_valid[spx].all():
+            raise SimError(f"W lin reads smem never written (tile {t})")
+        dst[dd] = smem[spx]
+        written[dd] += 1
 
 
 def _swizzle(d, s, V):

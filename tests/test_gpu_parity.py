@@ -376,3 +376,50 @@ def test_w2_blocks(cuda, jit):
         if done >= (8 if jit else 24):
             break
     assert done >= 6
+
+
+@pytest.mark.parametrize("jit", [True, False])
+def test_lin_w_mode(cuda, jit, monkeypatch):
+    """W as destination-linear 16-byte chunks (VPG_LIN=1, opt-in): bit-exact
+    on misaligned and ragged shapes, 4- and 8-byte words, both kernel
+    builds, a destination buffer off its 16-byte alignment (the chunk grid
+    follows the address) -- cfg3's shape included."""
+    import torch
+
+    import paper_2506_03686_b200 as vp
+    from paper_2506_03686_b200.api import execute_device
+
+    monkeypatch.setenv("VPG_LIN", "1")
+    vp.program_cache_clear()
+    rng = np.random.default_rng(77)
+    shapes = [((17, 9, 13, 15, 11, 27), (5, 2, 0, 4, 1, 3)), ((7, 9, 13, 5, 11), (4, 1, 0, 3, 2)),
+              ((101, 67), (1, 0)), ((33, 45, 19), (2, 0, 1)), ((13, 7, 300), (2, 1, 0))]
+    for _ in range(60):
+        r = int(rng.integers(2, 6))
+        shapes.append((tuple(int(x) for x in rng.integers(3, 40, size=r)), tuple(int(a) for a in rng.permutation(r))))
+    done = 0
+    try:
+        for i, (shape, axes) in enumerate(shapes):
+            n = int(np.prod(shape))
+            if n > (1 << 23) or n < 4096:
+                continue
+            E = 8 if i % 3 == 2 else 4
+            prog = vp.build_program(vp.TensorLayout.from_shape(shape, E), vp.from_numpy_convention(axes),
+                                    force="tile", jit=jit)
+            if "W lin" not in prog.text:
+                continue
+            x = torch.randint(-2**31, 2**31 - 1, (n * E // 4,), dtype=torch.int32, device="cuda")
+            xv = x.view(torch.int32 if E == 4 else torch.int64).view(shape)
+            want = xv.permute(axes).reshape(-1)
+            y = execute_device(prog, x.view(torch.uint8))
+            assert torch.equal(y.view(xv.dtype).view(-1), want), (shape, axes, E, prog.text)
+            big = torch.empty(n * E + E, dtype=torch.uint8, device="cuda")
+            out = big[E:]
+            execute_device(prog, x.view(torch.uint8), out=out)
+            assert torch.equal(out.view(xv.dtype), want), (shape, axes, E, "misaligned dst")
+            done += 1
+            if jit and done >= 12:
+                break
+    finally:
+        vp.program_cache_clear()
+    assert done >= 10, done

@@ -40,6 +40,38 @@ def test_sim_random_shapes(E):
     assert modes["shift"] > 0 and modes["vec"] > 0, modes
 
 
+@pytest.mark.parametrize("E", [4, 8])
+def test_sim_lin_forced(E, monkeypatch):
+    """W as destination-linear 16-byte chunks (VPG_LIN=1: wherever it
+    applies) on random shapes, ragged tiles and misaligned runs included."""
+    monkeypatch.setenv("VPG_LIN", "1")
+    vp.program_cache_clear()
+    rng = np.random.default_rng(100 + E)
+    lin = ragged = 0
+    try:
+        for _ in range(40):
+            rank = int(rng.integers(2, 6))
+            while True:
+                shape = tuple(int(rng.integers(1, 24)) for _ in range(rank))
+                if 64 <= np.prod(shape) <= 30000:
+                    break
+            axes = tuple(int(a) for a in rng.permutation(rank))
+            p = _run(shape, axes, E, rng)
+            if "W lin" in p.text:
+                lin += 1
+                tp = tile_params(p)
+                ragged += tp.grid_a >= 0 or tp.grid_c >= 0
+        for shape, axes in [((17, 9, 13, 15, 11, 27), (5, 2, 0, 4, 1, 3)), ((7, 9, 13, 5, 11), (4, 1, 0, 3, 2)),
+                            ((101, 67), (1, 0)), ((33, 45, 19), (2, 0, 1))]:
+            if np.prod(shape) > 200000:
+                shape = shape[:-1] + (3,)
+            p = _run(shape, axes, E, rng)
+            lin += "W lin" in p.text
+    finally:
+        vp.program_cache_clear()
+    assert lin >= 10 and ragged > 0, (lin, ragged)
+
+
 @pytest.mark.parametrize("shape,axes", [
     ((8, 24, 20, 12), (0, 2, 3, 1)), ((64, 48), (1, 0)), ((7, 9, 13, 5, 11), (4, 1, 0, 3, 2)),
     ((17, 9, 13, 15, 3, 5), (5, 2, 0, 4, 1, 3)), ((2,) * 12, (3, 9, 0, 7, 1, 5, 2, 11, 8, 6, 4, 10)),
