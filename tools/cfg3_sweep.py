@@ -4,6 +4,7 @@ CTA threads x W mode (VPG_LIN), each plan rebuilt in-process (the knobs are
 read at plan creation).  Prints one line per setting, then the best ten by
 flushed median.   usage: python tools/cfg3_sweep.py [cfg3] [quick]"""
 import itertools
+import json
 import os
 import sys
 
@@ -29,15 +30,20 @@ nb = bench.steady_buffers(fl.l2, n)
 xs = [x] + [x.clone() for _ in range(nb - 1)]
 ys = [y] + [torch.empty_like(x) for _ in range(nb - 1)]
 tdt = {4: torch.int32, 8: torch.int64}[wl.elem_bytes]
-KEYS = ("VPG_TILE_BUDGET", "VPG_NBUF", "VPG_THREADS", "VPG_LIN")
+KEYS = ("VPG_TILE_BUDGET", "VPG_NBUF", "VPG_THREADS", "VPG_LIN", "VPG_PERSIST")
 grid = {
     "VPG_TILE_BUDGET": [None, "16384", "24576", "40960", "49152"],
     "VPG_NBUF": [None, "3", "4"],
     "VPG_THREADS": [None, "384", "512"],
     "VPG_LIN": ["0", "1"],
+    "VPG_PERSIST": [None],
 }
 if quick:
-    grid = {"VPG_TILE_BUDGET": [None, "24576"], "VPG_NBUF": [None, "3"], "VPG_THREADS": [None], "VPG_LIN": ["0", "1"]}
+    grid = {"VPG_TILE_BUDGET": [None, "24576"], "VPG_NBUF": [None, "3"], "VPG_THREADS": [None], "VPG_LIN": ["0", "1"],
+            "VPG_PERSIST": [None]}
+if os.environ.get("SWEEP_GRID"):          # JSON {knob: [values or null]}, missing knobs at default
+    grid = {k: [None] for k in KEYS}
+    grid.update(json.loads(os.environ["SWEEP_GRID"]))
 res = []
 for combo in itertools.product(*(grid[k] for k in KEYS)):
     for k, v in zip(KEYS, combo):

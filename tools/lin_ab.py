@@ -64,7 +64,7 @@ def shapes():
         yield tuple(dims), tuple(int(a) for a in rng.permutation(r)), E
 
 
-rat = []
+rat, srat = [], []
 for shape, axes, E in shapes():
     nbytes = int(np.prod(shape)) * E
     if nbytes > (hi << 20):
@@ -84,10 +84,26 @@ for shape, axes, E in shapes():
     ma, mb = np.mean(ta) * 1e3, np.mean(tb) * 1e3
     rat.append(ma / mb)
     lin_b = "W lin" in pb.text
+    extra = ""
+    if os.environ.get("AB_STEADY"):
+        # back-to-back over rotating buffers larger than L2 (bench.time_steady)
+        nb = bench.steady_buffers(fl.l2, nbytes)
+        xs = [torch.empty(nbytes, dtype=torch.uint8, device=dev) for _ in range(nb)]
+        ys = [torch.empty(nbytes, dtype=torch.uint8, device=dev) for _ in range(nb)]
+        reps = max(3, min(30, int(4e9 // (nb * 2 * nbytes))))
+        sa = min(bench.time_steady(torch, lambda i: execute_device(pa, xs[i], out=ys[i]), nb, reps, st) for _ in range(3))
+        sb = min(bench.time_steady(torch, lambda i: execute_device(pb, xs[i], out=ys[i]), nb, reps, st) for _ in range(3))
+        srat.append(sa / sb)
+        extra = f" | steady A {sa * 1e3:8.2f} B {sb * 1e3:8.2f} A/B {sa / sb:.3f}"
+        del xs, ys
     print(f"{shape} {axes} E={E} runs {pa.metadata['src_run']}x{pa.metadata['dst_run']} | "
           f"{pb.metadata['src_run']}x{pb.metadata['dst_run']} lin_b={int(lin_b)}: A {ma:8.2f} us  B {mb:8.2f} us  "
-          f"A/B {ma / mb:.3f}  ({2 * nbytes / mb / 1e3:6.0f} GB/s B)", flush=True)
+          f"A/B {ma / mb:.3f}  ({2 * nbytes / mb / 1e3:6.0f} GB/s B){extra}", flush=True)
 r = np.array(rat)
 if r.size:
     print(f"\n{r.size} shapes: A/B time ratio median {np.median(r):.3f} p10 {np.percentile(r, 10):.3f} "
           f"p90 {np.percentile(r, 90):.3f} min {r.min():.3f} max {r.max():.3f}  (>1: B faster)")
+if srat:
+    r = np.array(srat)
+    print(f"steady: A/B time ratio median {np.median(r):.3f} p10 {np.percentile(r, 10):.3f} "
+          f"p90 {np.percentile(r, 90):.3f} min {r.min():.3f} max {r.max():.3f}")
