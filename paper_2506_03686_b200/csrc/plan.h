@@ -29,6 +29,9 @@ struct vpg_plan {
     int64_t grid_hint;
     double predicted_eff;
     double tile_util;
+    // TILE: the cost model's terms for the chosen tile (describe(); planner
+    // calibration data, tools/cand_data.py)
+    double geom_cost, walk_cost, eff_s, eff_d;
     int32_t jit;               // TILE: launch the NVRTC-specialised kernel (jit.cpp)
     int32_t shards;            // 0: ordinary plan; G >= 1: fused sharded exchange plan of rank shard_index
     int32_t shard_index;

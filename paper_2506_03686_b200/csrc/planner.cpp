@@ -1442,6 +1442,8 @@ static void describe(vpg_plan *p) {
                 (unsigned)lin_table_bytes(t.lin.run_len, 16 / p->elem_bytes), t.lin.rot_shift < 32 ? "lane >> " : "none",
                 t.lin.rot_shift < 32 ? t.lin.rot_shift : 0u);
         put("lane utilisation (R*W): %.3f\n", p->tile_util);
+        put("cost model: geometry %.4f (sector efficiency src %.3f, dst %.3f), walk %.4f per element\n",
+            p->geom_cost, p->eff_s, p->eff_d, p->walk_cost);
         put("specialised (NVRTC) kernel: %s\n", p->jit ? "yes" : "no");
         put("tiles: %u, grid digits: %d\n", t.num_tiles, t.ngrid);
         if (p->shards > 0 && t.pull)
@@ -1547,7 +1549,8 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         // 24.7 us; cfg5's 4 GiB keeps the large tiles: 664 vs 686 us)
         int64_t nel = 1;
         for (int k = 0; k < rank; ++k) nel *= dims[k];
-        if ((double)nel * E * 2.0 < kSmallProblemBytes) {
+        const char *sm = getenv("VPG_SMALL");      // 0: no small-problem tiling (experiments)
+        if ((double)nel * E * 2.0 < kSmallProblemBytes && !(sm && atoi(sm) == 0)) {
             P.budget = 24 * 1024;
             P.cta_smem = 75 * 1024;
             small_problem = true;
@@ -1716,7 +1719,8 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         // 81 x 75 -> 54 x 270-element runs, flushed 18.65 -> 18.03 us mean,
         // steady 15.25 -> 14.58 us; aligned cfg1/cfg2 keep 24 KiB: cfg2 12.6
         // vs 13.0 us with 32 KiB; tools/sweep_budget.py)
-        if (vc.rshift && small_problem && pick < 0 && !getenv("VPG_TILE_BUDGET")) {
+        const char *smis = getenv("VPG_SMALL_MIS");  // 0: no 32 KiB retry for misaligned small problems
+        if (vc.rshift && small_problem && pick < 0 && !getenv("VPG_TILE_BUDGET") && !(smis && atoi(smis) == 0)) {
             Problem P2 = P;
             P2.budget = 32 * 1024;
             TileGeom g2;
@@ -1758,6 +1762,10 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         // runs it cannot take (not a power of two, or not 128-byte aligned)
         vc.bulk = (vc.bulk && vc.rshift) || (!vc.sw128 && bulk_for(vc));
         p->tile_util = fill_tile_params(P, g, pitch, threads, vc, p->tile);
+        p->geom_cost = g.cost;
+        p->walk_cost = tile_cost(P, p->tile) / (double)g.T;
+        p->eff_s = g.eff_s;
+        p->eff_d = g.eff_d;
         // variant without 16-byte source reads, for misaligned base pointers
         VecChoice vs = vc;
         vs.vr = 1;
