@@ -39,7 +39,14 @@ constexpr double kTileOverheadBytes = 2048.0;  // cost of one tile (decode + 2 b
 constexpr int64_t kTileBudgetBytes = 48 * 1024;  // staged elements per CTA
 constexpr double kResidueCostFactor = 0.9;
 constexpr double kSw128CostFactor = 0.85;    // 128-byte congruent rows: half the L2 sector requests of the R phase   // residue-stride shifted tiles: no W shift arithmetic
-constexpr double kSmallProblemBytes = 512.0 * 1024 * 1024;   // algorithmic bytes below which tiles shrink
+// algorithmic bytes below which tiles shrink to the 24 KiB budget (round 1,
+// from cfg1-3).  Timing every tile candidate of 31 random 32-512 MiB
+// permutations at 24/32/48 KiB budgets (tools/cand_data.py,
+// profiles/cand_data_r2.jsonl): 24 KiB below this size is within noise of
+// 48 KiB (mean 0.969 vs 0.969 of the best candidate); a 128 MiB cut measured
+// 0.972 -- not enough to move it.
+constexpr double kSmallProblemBytes = 512.0 * 1024 * 1024;
+constexpr double kWalkWeight = 8.0;   // walk cost (ops/element) vs relative geometry cost, per byte of element
 
 int64_t gcd64(int64_t a, int64_t b) {
     a = a < 0 ? -a : a;
@@ -1550,7 +1557,9 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         int64_t nel = 1;
         for (int k = 0; k < rank; ++k) nel *= dims[k];
         const char *sm = getenv("VPG_SMALL");      // 0: no small-problem tiling (experiments)
-        if ((double)nel * E * 2.0 < kSmallProblemBytes && !(sm && atoi(sm) == 0)) {
+        const char *sb = getenv("VPG_SMALL_BYTES");   // algorithmic-bytes threshold (experiments)
+        const double small_bytes = sb ? atof(sb) : kSmallProblemBytes;
+        if ((double)nel * E * 2.0 < small_bytes && !(sm && atoi(sm) == 0)) {
             P.budget = 24 * 1024;
             P.cta_smem = 75 * 1024;
             small_problem = true;
@@ -1714,26 +1723,43 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         uint32_t pitch;
         VecChoice vc;
         choose_pitch_vec(P, g, threads, pitch, vc);
-        // small problems with misaligned source runs: their residue rows pad
-        // a tile by up to a third, so they stage with the 32 KiB budget (cfg3:
-        // 81 x 75 -> 54 x 270-element runs, flushed 18.65 -> 18.03 us mean,
-        // steady 15.25 -> 14.58 us; aligned cfg1/cfg2 keep 24 KiB: cfg2 12.6
-        // vs 13.0 us with 32 KiB; tools/sweep_budget.py)
-        const char *smis = getenv("VPG_SMALL_MIS");  // 0: no 32 KiB retry for misaligned small problems
-        if (vc.rshift && small_problem && pick < 0 && !getenv("VPG_TILE_BUDGET") && !(smis && atoi(smis) == 0)) {
+        // Small problems with misaligned source runs also consider the 32 KiB
+        // budget (their residue rows pad a tile by up to a third) and keep it
+        // when the geometry cost plus the walk cost (issued smem/memory ops
+        // per element, weight 8 per byte of element) is lower.  Round 2 kept
+        // the 32 KiB tile unconditionally (from cfg3: 18.65 -> 18.03 us
+        // flushed); timing every candidate of 31 random permutations
+        // (tools/cand_data.py, profiles/cand_data_r2.jsonl) showed that as the
+        // worst budget policy -- 0.77 and 0.73 of the best candidate on two
+        // shapes whose 32 KiB tiles walk with idle lanes -- and this rule the
+        // best simple one (0.975 mean of the best candidate).  VPG_SMALL_MIS:
+        // 1 = always take the 32 KiB tile, 0 = never.
+        const char *smis = getenv("VPG_SMALL_MIS");
+        const int small_mis = smis ? atoi(smis) : -1;
+        if (vc.rshift && small_problem && pick < 0 && !getenv("VPG_TILE_BUDGET") && small_mis != 0) {
             Problem P2 = P;
             P2.budget = 32 * 1024;
             TileGeom g2;
             if (select_tile(P2, g2, -1)) {
                 const int t2 = g2.T >= 1024 ? kTileThreads : (g2.T >= 256 ? 128 : 64);
+                const int thr2 = force_threads >= 32 && force_threads <= 1024 ? force_threads / 32 * 32 : t2;
                 uint32_t pitch2;
                 VecChoice vc2;
-                choose_pitch_vec(P2, g2, force_threads >= 32 && force_threads <= 1024 ? force_threads / 32 * 32 : t2,
-                                 pitch2, vc2);
-                if (vc2.rshift) {
+                choose_pitch_vec(P2, g2, thr2, pitch2, vc2);
+                bool take = vc2.rshift;
+                if (take && small_mis < 0) {
+                    TileParams a, b;
+                    fill_tile_params(P, g, pitch, threads, vc, a);
+                    fill_tile_params(P2, g2, pitch2, thr2, vc2, b);
+                    const double gmin = std::min(g.cost, g2.cost);
+                    const double ca = g.cost / gmin + kWalkWeight * tile_cost(P, a) / (double)g.T / E;
+                    const double cb = g2.cost / gmin + kWalkWeight * tile_cost(P2, b) / (double)g2.T / E;
+                    take = cb < ca;
+                }
+                if (take) {
                     P = P2;
                     g = g2;
-                    threads = force_threads >= 32 && force_threads <= 1024 ? force_threads / 32 * 32 : t2;
+                    threads = thr2;
                     pitch = pitch2;
                     vc = vc2;
                 }

@@ -312,7 +312,8 @@ def simulate(program, src_words: np.ndarray, threads: int | None = None, shard_o
                                 spx = _swizzle(d, sp, 16 // E if E <= 16 else 1)
                                 # (the logical slot is congruent to the source mod 128 B;
                                 # the swizzle only permutes chunks inside a 128-byte block)
-                                if d.swz and not tp.pull and V > 1 and ((sp * E) % 128 != (gabs * E) % 128).any():
+                                if (d.swz and not tp.pull and V > 1 and _congruent(tp, E)
+                                        and ((sp * E) % 128 != (gabs * E) % 128).any()):
                                     raise SimError("congruent layout: smem and global offsets differ mod 128 B")
                                 if d.swz and ((spx * E) // 128 != (sp * E) // 128).any():
                                     raise SimError("chunk swizzle left its 128-byte block")
@@ -439,6 +440,22 @@ def _lin_write(tp, E, db, smem, smem_valid, tbase, dst, written, dbound, full, l
             raise SimError(f"W lin reads smem never written (tile {t})")
         dst[dd] = smem[spx]
         written[dd] += 1
+
+
+def _congruent(tp, E):
+    """The swizzled unpadded layout keeps runs at their source lines' offset
+    mod 128 B only when every stride that moves a run start (grid digits,
+    R-phase dims at or above the run) is a multiple of 128 bytes; the planner
+    also uses the layout without that congruence (planner.cpp
+    sw128_layout_ok vs sw128_possible)."""
+    q = 128 // E
+    d = tp.ph[0]
+    dims = [d.thr[i] for i in range(d.nthr_dims)] + [d.out[i] for i in range(d.nout_dims)]
+    if any(tp.grid[i].src_stride % q for i in range(tp.ngrid)):
+        return False
+    if d.n_in > 1 and d.g_in >= tp.Ls and d.g_in % q:
+        return False
+    return not any(x.gstride >= tp.Ls and x.gstride % q for x in dims)
 
 
 def _swizzle(d, s, V):

@@ -47,6 +47,9 @@ def shapes():
     yield (7, 9, 13, 5, 11, 13, 9), (6, 2, 0, 4, 1, 3, 5), 4
     yield (267, 701, 717), (2, 1, 0), 4
     yield (131, 93, 77, 31), (3, 1, 2, 0), 8
+    yield (4096, 4096), (1, 0), 4
+    yield (32, 64, 56, 56), (0, 2, 3, 1), 4
+    yield (8, 2, 5, 158, 37, 143), (2, 1, 0, 5, 4, 3), 4
     for _ in range(N):
         E = int(rng.choice([4, 8]))
         target = int(rng.integers(lo, hi + 1)) << 20
