@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define VPG_ABI_VERSION 5
+#define VPG_ABI_VERSION 6   /* 6: TileParams gains LinDesc (vpg_plan_tile_params block) */
 #define VPG_MAX_RANK 64
 #define VPG_MAX_SHARDS 64   /* shards of a fused exchange */
 

@@ -36,7 +36,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_version_and_last_error():
     L = _lib.lib()
-    assert L.vpg_version() == 5
+    assert L.vpg_version() == 6
     rank, d, s = _lib.arrays((3, 2), (0, 0))
     p = ctypes.c_void_p()
     assert L.vpg_plan_create(rank, d, s, 4, 0, ctypes.byref(p)) == _lib.VPG_EINVAL
