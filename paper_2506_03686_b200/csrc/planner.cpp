@@ -1397,10 +1397,15 @@ static bool refine_for_shards(int rank, const int64_t *dims, const int32_t *sigm
 // them faster unless they are long 8-byte rows (tools/shape_ab.py: 69 x 8 B
 // rows 0.56 vs 0.98 of copy through the tile kernel; 1001 x 4 B 0.58 vs 0.79;
 // 1025 x 8 B 0.85 both).
+// Rows whose length is not a multiple of 16 bytes go to the tile kernel,
+// which stages them through residue-strided smem rows and keeps 16-byte
+// accesses: 8-byte words with odd row lengths of 65-16385 elements ran at
+// 1.06-1.15 of a same-size copy_ there against 0.75-1.02 in the rows kernel
+// (word-width vectors; tools/rows_vs_tile.py, profiles/rows_vs_tile_r2.txt).
 static bool rows_suitable(int64_t Lr, int E) {
     const int64_t V = std::max(1, 16 / E);
     if (Lr * E < kRowsMinBytes) return false;
-    return Lr % V == 0 || (E >= 8 && Lr * E >= 2048);
+    return Lr % V == 0;
 }
 
 // ----------------------------------------------------------------- plan

@@ -399,7 +399,7 @@ def test_c_api_demo_program(cuda, tmp_path):
 
 @pytest.mark.parametrize("shape,axes,elem", [
     ((5, 3, 96, 29, 95), (1, 0, 2, 3, 4), 4),       # 15 rows of 264480 words: rows cut into chunks
-    ((3, 2, 61, 1001), (1, 0, 2, 3), 8),            # 6 rows of 61061 words, odd length (8-byte words)
+    ((3, 2, 61, 1000), (1, 0, 2, 3), 8),            # 6 rows of 61000 8-byte words (odd lengths go to the tile kernel)
     ((7, 5, 1, 20016), (1, 0, 2, 3), 2),            # 2-byte words
     ((2, 3, 7, 4097), (1, 0, 2, 3), 16),            # 16-byte words
 ])
@@ -645,3 +645,24 @@ def test_dynamic_tile_scheduler_reuse_and_streams(cuda):
                     with torch.cuda.stream(streams[si]):
                         outs[si][ci].zero_()
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("shape,axes", [((36, 106, 439), (1, 0, 2)), ((3, 2, 61, 1001), (1, 0, 2, 3)),
+                                        ((7, 5, 257), (1, 0, 2))])
+def test_odd_rows_take_tile_kernel(cuda, shape, axes):
+    """Stride-1-preserving permutations of 8-byte words whose rows are not a
+    multiple of 16 bytes run on the tile kernel (residue rows, 16-byte
+    accesses), bit-exact, at aligned and offset bases."""
+    import torch
+
+    import paper_2506_03686_b200 as vp
+    from paper_2506_03686_b200.api import execute_device
+
+    prog = vp.build_program(vp.TensorLayout.from_shape(shape, 8), vp.from_numpy_convention(axes))
+    assert prog.kernel == "tile", prog.text
+    n = int(np.prod(shape))
+    x = torch.randint(-2**62, 2**62, (n + 2,), dtype=torch.int64, device="cuda")
+    for off in (0, 1):
+        xv = x[off:off + n]
+        y = execute_device(prog, xv.view(torch.uint8))
+        assert torch.equal(y.view(torch.int64), xv.view(shape).permute(axes).reshape(-1)), off
