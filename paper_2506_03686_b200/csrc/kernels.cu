@@ -527,11 +527,9 @@ vpg_status launch_tile(const vpg_plan *p, const void *src, void *dst, const Shar
         }
     }
     const TileParams &tp = aligned ? p->tile : p->tile_unaligned;
-    if constexpr (E >= 4) {
-        launch(tile_kernel<W, true>, p->threads, tp);
-        return VPG_OK;
-    }
-    if constexpr (E < 4) launch(tile_kernel<W, false>, p->threads, tp);
+    // (1- and 2-byte words: the cp.async pipeline moves their 16-byte
+    // vectors; scalar phases of those words load synchronously)
+    launch(tile_kernel<W, true>, p->threads, tp);
     return VPG_OK;
 }
 

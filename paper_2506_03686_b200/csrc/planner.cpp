@@ -46,7 +46,9 @@ constexpr double kSw128CostFactor = 0.85;    // 128-byte congruent rows: half th
 // 48 KiB (mean 0.969 vs 0.969 of the best candidate); a 128 MiB cut measured
 // 0.972 -- not enough to move it.
 constexpr double kSmallProblemBytes = 512.0 * 1024 * 1024;
-constexpr double kWalkWeight = 8.0;   // walk cost (ops/element) vs relative geometry cost, per byte of element
+constexpr double kWalkWeight = 8.0;
+constexpr double kSmallWordMisalignFactor = 1.5;
+constexpr int kSmCount = 148;         // B200 SMs (tiny-problem tiling; launches query the device)   // walk cost (ops/element) vs relative geometry cost, per byte of element
 
 int64_t gcd64(int64_t a, int64_t b) {
     a = a < 0 ? -a : a;
@@ -83,8 +85,10 @@ struct Problem {
     bool no_bulk = false;  // TMA bulk source reads off (VPG_BULK=0, pull exchanges)
     bool force_bulk = false; // TMA bulk source reads wherever they apply (VPG_BULK=1)
     bool no_swz = true;    // shifted-run chunk swizzle is opt-in (VPG_SWZ=1)
-    // W as destination-linear 16-byte chunks: 0 off (default: measured slower,
-    // tools/lin_ab.py), -1 cost model, 1 wherever it applies (VPG_LIN)
+    // W as destination-linear 16-byte chunks (VPG_LIN): 0 off (default:
+    // measured slower for every word size -- 4/8-byte words median -4%,
+    // tools/lin_ab.py; 1/2-byte words 1.5-2.5x slower,
+    // profiles/small_word_r2.txt), -1 cost model, 1 wherever it applies
     int lin_mode = 0;
     int r;
     int64_t d[kMaxRank];
@@ -215,6 +219,12 @@ void score_geom(const Problem &P, TileGeom &g) {
     g.cost = (E / g.eff_s + E / g.eff_d + ovh_s / g.Ls + ovh_d / g.Ld) *
                  (1.0 + beta * ((double)g.T / t_avg - 1.0)) +
              kTileOverheadBytes / t_avg;
+    // 1- and 2-byte words move as 16-byte vectors only when run starts keep
+    // 16-byte alignment; a tile extent that breaks it (a 1024^2 byte
+    // transpose tiled 171 x 128 instead of 128 x 128) falls back to
+    // aligned-superset reads and scalar stores of 1-2 bytes, so such
+    // geometries rank behind aligned ones
+    if (E < 4 && ((as % 16) || (ad % 16))) g.cost *= kSmallWordMisalignFactor;
 }
 
 std::vector<int64_t> extent_candidates(int64_t d, int64_t cap) {
@@ -760,7 +770,7 @@ uint64_t lin_table_bytes(int64_t Ld, int V) {
 }
 
 bool lin_applicable(const Problem &Pb, const TileGeom &g, const VecChoice &vc) {
-    if (Pb.lin_mode == 0 || !(Pb.E == 4 || Pb.E == 8)) return false;
+    if (Pb.lin_mode == 0 || Pb.E >= 16) return false;
     if (vc.vw > 1 || vc.w2 || vc.bulk || (vc.rshift && !vc.rres)) return false;
     const int V = 16 / Pb.E;
     if (g.Ld < 2 * V || g.ndst > kMaxLinDims || g.T / g.Ld > 0xffffffffLL) return false;
@@ -996,9 +1006,10 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
     if (tp.lin.on && tp.tile_elems_alloc >= 65536u) memset(&tp.lin, 0, sizeof(tp.lin));
     if (tp.lin.on) tp.lin.tab_off = take(lin_table_bytes(g.Ld, V), 16);
     // pipeline depth: as many stages as fit the per-CTA smem target (two
-    // CTAs per SM), at least 2, at most 8; 1- and 2-byte words use 1.
+    // CTAs per SM), at least 2, at most 8 (1- and 2-byte words too: their
+    // vectorised reads are 16-byte cp.async, their scalar reads synchronous)
     uint32_t stages = 1;
-    if (Pb.E >= 4) {
+    {
         uint64_t room = (uint64_t)Pb.cta_smem > o + 1024 ? (uint64_t)Pb.cta_smem - o - 1024 : 0;
         stages = (uint32_t)std::min<uint64_t>(8, std::max<uint64_t>(2, room / buf_bytes));
         if (Pb.nbuf > 0) stages = (uint32_t)Pb.nbuf;
@@ -1056,7 +1067,10 @@ double tile_cost(const Problem &Pb, const TileParams &tp) {
 
 // Choose pitch and vectorisation that minimise the modelled tile cost.
 void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pitch_out, VecChoice &vc_out) {
-    const int V = (Pb.E == 4 || Pb.E == 8) ? 16 / Pb.E : 1;
+    // 16-byte vectors for every word size below 16 bytes (1- and 2-byte
+    // words too: fp16/bf16 and byte tensors, including aligned-superset
+    // reads of misaligned runs); TMA bulk modes exist for 4- and 8-byte words
+    const int V = Pb.E < 16 ? 16 / Pb.E : 1;
     const bool rv = r_vectorizable(Pb, g, V);
     const bool wv = w_vectorizable(Pb, g, V);
     // shifted-run reads: misaligned source runs long enough to amortise the
@@ -1181,7 +1195,7 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
                 lin_try(vc, pitch, kResidueCostFactor * (res_modulus(Pb.E) * Pb.E >= 128 ? kSw128CostFactor : 1.0));
             }
         }
-        if (op.rshift && Pb.force_bulk && !Pb.no_bulk && g.n_runidx <= kMaxPhaseDims) {
+        if (op.rshift && Pb.force_bulk && !Pb.no_bulk && (Pb.E == 4 || Pb.E == 8) && g.n_runidx <= kMaxPhaseDims) {
             // TMA bulk reads of misaligned runs: one cp.async.bulk per run's
             // 16-byte aligned superset (producer warp, tile_body_bulk) into
             // rows with 16-byte residue strides.  The bulk engine keeps L2
@@ -1449,10 +1463,10 @@ static void describe(vpg_plan *p) {
             t.ph[1].vec, t.ph[1].w2 ? " (VxV register-transposed blocks, 16-byte stores)" : "");
         if (t.lin.on)
             put("W lin: destination-linear %u-byte chunks, one store each (runs of %u elements, %u chunk slots x %u "
-                "runs, offset table %u bytes, bank rotation %s%u)\n",
+                "runs, offset table %u bytes, bank rotation %s)\n",
                 16u, t.lin.run_len, t.lin.cpr, t.lin.nchunks / t.lin.cpr,
-                (unsigned)lin_table_bytes(t.lin.run_len, 16 / p->elem_bytes), t.lin.rot_shift < 32 ? "lane >> " : "none",
-                t.lin.rot_shift < 32 ? t.lin.rot_shift : 0u);
+                (unsigned)lin_table_bytes(t.lin.run_len, 16 / p->elem_bytes),
+                t.lin.rot_shift < 32 ? ("lane >> " + std::to_string(t.lin.rot_shift)).c_str() : "none");
         put("lane utilisation (R*W): %.3f\n", p->tile_util);
         put("cost model: geometry %.4f (sector efficiency src %.3f, dst %.3f), walk %.4f per element\n",
             p->geom_cost, p->eff_s, p->eff_d, p->walk_cost);
@@ -1568,6 +1582,13 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
             P.budget = 24 * 1024;
             P.cta_smem = 75 * 1024;
             small_problem = true;
+            // tiny problems: tiles small enough for ~4 per SM, so the grid
+            // fills the GPU (a 1 MiB byte transpose is 64 tiles of 16 KiB)
+            // (opt-in, VPG_TINY=1: a wash once such plans run specialised
+            // kernels, tools/tiny_probe.py)
+            const char *tb = getenv("VPG_TINY");
+            const int64_t tiny = (int64_t)((double)nel * E / (4.0 * kSmCount));
+            if (tb && atoi(tb) == 1 && tiny < P.budget) P.budget = std::max<int64_t>(4096, tiny);
         }
     }
     int persist_mode = -1;  // -1 auto, 0 one tile per CTA, 1 persistent
@@ -1782,7 +1803,8 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         // runs -10..-25%; cfg5 729 -> 713 us)
         const bool long_runs = g.Ls * E >= 2048 && g.Ld * E >= 512;
         auto bulk_for = [&](const VecChoice &v) {
-            return v.vr > 1 && !v.rshift && !P.no_bulk && (long_runs || P.force_bulk) && (g.Ls * E) % 16 == 0 &&
+            return (E == 4 || E == 8) && v.vr > 1 && !v.rshift && !P.no_bulk && (long_runs || P.force_bulk) &&
+                   (g.Ls * E) % 16 == 0 &&
                    (g.a_part < 0 ||
                     ((g.Ls / g.ext[g.a_part]) * (P.d[g.a_part] % g.ext[g.a_part]) * E) % 16 == 0) &&
                    g.n_runidx <= kMaxPhaseDims;
@@ -1819,7 +1841,11 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         // per-case specialisation pays off once the tensor is large enough to
         // amortise a one-off NVRTC compile (cached in-process and on disk)
         const char *je = getenv("VPG_JIT");
-        bool big = P.n / std::max(1, P.G) * E >= ((int64_t)4 << 20);
+        // (1 MiB: the ahead-of-time kernel runs 2-2.5x slower than the
+        // specialised one on 1-6 MiB permutations -- 3.6x the instructions,
+        // tools/tiny_probe.py jit -- and a compile takes 0.3-0.7 s once per
+        // plan, cached in-process and on disk)
+        bool big = P.n / std::max(1, P.G) * E >= ((int64_t)1 << 20);
         p->jit = (flags & VPG_FORCE_JIT) ? 1 : (flags & VPG_NO_JIT) ? 0 : je ? (atoi(je) != 0) : big;
         p->grid_hint = std::min<int64_t>(p->tile.num_tiles, 148 * 4);
         p->predicted_eff = 2.0 / (1.0 / g.eff_s + 1.0 / g.eff_d);

@@ -225,6 +225,9 @@ __device__ __forceinline__ void tile_read_impl(const PhaseDesc &d, const ThreadP
                                                const Lim lim) {
     constexpr int U = 4;
     constexpr int CP = VEC ? 16 : (int)sizeof(W);
+    // cp.async moves 4, 8 or 16 bytes: scalar 1- and 2-byte words load
+    // synchronously (their vectorised phases use 16-byte cp.async)
+    constexpr bool CPA = ASYNC && CP >= 4;
     const uint32_t n_in = d.n_in;
     const int64_t g_in = d.g_in;
     const uint32_t s_in = d.s_in;
@@ -239,7 +242,7 @@ __device__ __forceinline__ void tile_read_impl(const PhaseDesc &d, const ThreadP
             uint32_t i = 0;
             VPG_UNROLL
             for (; i + U <= n_in; i += U) {
-                if constexpr (ASYNC) {
+                if constexpr (CPA) {
 #pragma unroll
                     for (int u = 0; u < U; ++u) cp_async<CP>(sbase + soff<W>(d, bb, so + u * s_in), gp + u * g_in);
                 } else {
@@ -253,7 +256,7 @@ __device__ __forceinline__ void tile_read_impl(const PhaseDesc &d, const ThreadP
                 so += U * s_in;
             }
             for (; i < n_in; ++i) {
-                if constexpr (ASYNC) cp_async<CP>(sbase + soff<W>(d, bb, so), gp);
+                if constexpr (CPA) cp_async<CP>(sbase + soff<W>(d, bb, so), gp);
                 else *sptr<W>(smem, soff<W>(d, bb, so)) = __ldg(gp);
                 gp += g_in;
                 so += s_in;
@@ -263,7 +266,7 @@ __device__ __forceinline__ void tile_read_impl(const PhaseDesc &d, const ThreadP
             VPG_UNROLL
             for (uint32_t i = 0; i < n_in; ++i) {
                 if (slot_ok(mask, c0, c1, c2, lim)) {
-                    if constexpr (ASYNC) cp_async<CP>(sbase + soff<W>(d, bb, so), gp);
+                    if constexpr (CPA) cp_async<CP>(sbase + soff<W>(d, bb, so), gp);
                     else *sptr<W>(smem, soff<W>(d, bb, so)) = __ldg(gp);
                 }
                 gp += g_in;
@@ -323,7 +326,10 @@ __device__ __forceinline__ void tile_read_shift(const PhaseDesc &d, const Thread
                 } else {
 #pragma unroll
                     for (int j = 0; j < V; ++j)
-                        if (ga + j < gend) cp_async<sizeof(W)>(sd + j * (uint32_t)sizeof(W), ga + j);
+                        if (ga + j < gend) {
+                            if constexpr (sizeof(W) >= 4) cp_async<sizeof(W)>(sd + j * (uint32_t)sizeof(W), ga + j);
+                            else *sptr<W>(smem, sd - sbase + j * (uint32_t)sizeof(W)) = __ldg(ga + j);
+                        }
                 }
             }
             gp += g_in;
@@ -340,7 +346,7 @@ __device__ __forceinline__ void tile_read(const PhaseDesc &d, const ThreadPart &
                                           const W *__restrict__ gsrc, const W *gend, uint32_t bb, uint32_t mask,
                                           const Lim lim, bool near_end) {
     if (!t.active) return;
-    if constexpr (ASYNC && (sizeof(W) == 4 || sizeof(W) == 8)) {
+    if constexpr (ASYNC && sizeof(W) < 16) {
         if (d.rshift) {
             // tiles clear of the buffer end read every chunk unchecked
             // (straight-line cp.async sequences; the rare tile at the end checks)
@@ -559,7 +565,7 @@ __device__ __forceinline__ void tile_write(const PhaseDesc &d, const ThreadPart 
         return;
     }
 #endif
-    if constexpr (sizeof(W) == 4 || sizeof(W) == 8) {
+    if constexpr (sizeof(W) < 16) {
         if (d.w2) {
             tile_write_w2<W>(d, t, smem, gdst, bb, mask, lim);
             return;
@@ -597,30 +603,18 @@ __device__ __forceinline__ void lin_build_table(const LinDesc &L, unsigned char 
     }
 }
 
-// a[k] <- a[(k + r) mod V] (selects, r lane-dependent)
+// a[k] <- a[(k + r) mod V] (selects, r lane-dependent): log2(V) stages,
+// stage b rotating by 2^b when bit b of r is set
 template <int V, typename T>
 __device__ __forceinline__ void rot_left(T (&a)[V], uint32_t r) {
-    if constexpr (V == 4) {
-        if (r & 2u) {
-            T t0 = a[0], t1 = a[1];
-            a[0] = a[2];
-            a[1] = a[3];
-            a[2] = t0;
-            a[3] = t1;
-        }
-        if (r & 1u) {
-            T t = a[0];
-            a[0] = a[1];
-            a[1] = a[2];
-            a[2] = a[3];
-            a[3] = t;
-        }
-    } else if constexpr (V == 2) {
-        if (r & 1u) {
-            T t = a[0];
-            a[0] = a[1];
-            a[1] = t;
-        }
+#pragma unroll
+    for (int b = V / 2; b >= 1; b /= 2) {
+        T t[V];
+#pragma unroll
+        for (int k = 0; k < V; ++k) t[k] = a[(k + b) % V];
+        const bool on = (r & (uint32_t)b) != 0u;
+#pragma unroll
+        for (int k = 0; k < V; ++k) a[k] = on ? t[k] : a[k];
     }
 }
 
@@ -645,7 +639,7 @@ __device__ __forceinline__ void tile_write_lin(const TileParams &p, const unsign
     const uint32_t rot = L.rot_shift < 32 ? ((tid & 31u) >> L.rot_shift) & (uint32_t)(V - 1) : 0u;
     // batches of B chunk slots per thread: every smem load of a batch issues
     // before its first store
-    constexpr int B = 4;
+    constexpr int B = sizeof(W) == 1 ? 2 : 4;
     VPG_UNROLL
     for (uint32_t q0 = tid; q0 < L.nchunks; q0 += B * L.nt) {
         alignas(16) W v[B][V];
@@ -684,10 +678,22 @@ __device__ __forceinline__ void tile_write_lin(const TileParams &p, const unsign
                 offs[1] = t.x >> 16;
                 offs[2] = t.y & 0xffffu;
                 offs[3] = t.y >> 16;
-            } else {
+            } else if constexpr (V == 2) {
                 const uint32_t t = *reinterpret_cast<const uint32_t *>(tq);
                 offs[0] = t & 0xffffu;
                 offs[1] = t >> 16;
+            } else {
+                // 1- and 2-byte words: V u16 entries in V/8 16-byte loads
+#pragma unroll
+                for (int h = 0; h < V / 8; ++h) {
+                    const uint4 t = *reinterpret_cast<const uint4 *>(tq + 16 * h);
+                    const uint32_t w[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        offs[8 * h + 2 * k] = w[k] & 0xffffu;
+                        offs[8 * h + 2 * k + 1] = w[k] >> 16;
+                    }
+                }
             }
             rot_left<V>(offs, rot);
 #pragma unroll
@@ -841,8 +847,10 @@ __device__ __forceinline__ void tile_read_pull(const TileParams &p, const ShardA
                         cp_async<16>(sb32 + shift_chunk_off<W>(d, bb, so), pull_ptr(p, sa, src, go & ~(int64_t)(V - 1)));
                     } else if (d.vec > 1) {
                         cp_async<16>(sb32 + sp, pull_ptr(p, sa, src, go));
-                    } else {
+                    } else if constexpr (sizeof(W) >= 4) {
                         cp_async<sizeof(W)>(sb32 + sp, pull_ptr(p, sa, src, go));
+                    } else {
+                        *sptr<W>(smem, sp) = __ldg(pull_ptr(p, sa, src, go));
                     }
                 } else if constexpr (ASYNC) {
                     cp_async<16>(sb32 + sp, pull_ptr(p, sa, src, go));
@@ -1094,7 +1102,7 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
     }
     if (trc && tid == 0) trc[1] = gtimer();
     // lin W: the offset table (ordered before the first W by the loop's barrier)
-    if constexpr (sizeof(W) == 4 || sizeof(W) == 8)
+    if constexpr (sizeof(W) < 16)
         if (p.lin.on) lin_build_table<16 / (int)sizeof(W)>(p.lin, smem, tid, NT);
     uint32_t tiles_done = 0;
     for (uint32_t k = 0;; ++k) {
@@ -1148,7 +1156,7 @@ __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restri
             const uint32_t slot = k % R;
             const uint32_t m = limits(slot, 1, lim);
             bool lin_done = false;
-            if constexpr (sizeof(W) == 4 || sizeof(W) == 8) {
+            if constexpr (sizeof(W) < 16) {
                 if (p.lin.on) {
                     tile_write_lin<W>(p, smem, dst + s_base[slot][1], shifted(b, slot),
                                       !(lim.l0 == p.e_a && lim.l1 == p.e_c), lim, tid);

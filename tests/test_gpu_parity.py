@@ -423,3 +423,38 @@ def test_lin_w_mode(cuda, jit, monkeypatch):
     finally:
         vp.program_cache_clear()
     assert done >= 10, done
+
+
+@pytest.mark.parametrize("shape,axes,elem,mode", [
+    ((32, 64, 56, 56), (0, 2, 3, 1), 2, "VxV"),            # fp16 NCHW -> NHWC
+    ((2048, 1024), (1, 0), 1, "VxV"),                       # byte transpose
+    ((1024, 768), (1, 0), 1, "R 16"),
+    ((17, 9, 13, 15, 11, 27), (5, 2, 0, 4, 1, 3), 2, "aligned supersets"),   # cfg3's shape in fp16
+    ((1027, 515), (1, 0), 1, "aligned supersets"),          # odd byte transpose
+    ((8, 512, 7, 7), (0, 2, 3, 1), 2, "aligned supersets"),   # 7x7 feature maps
+    ((16, 64, 32, 128), (0, 2, 1, 3), 2, "R 8"),
+])
+def test_small_words_vectorised(cuda, shape, axes, elem, mode):
+    """1- and 2-byte words (fp16/bf16, bytes) move as 16-byte vectors: V x V
+    register-transposed blocks with 16-byte stores on aligned tiles, aligned
+    supersets of misaligned runs into residue rows otherwise; bit-exact
+    against torch, specialised and ahead-of-time kernels, a misaligned
+    destination included."""
+    import torch
+
+    import paper_2506_03686_b200 as vp
+    from paper_2506_03686_b200.api import execute_device
+
+    dt = {1: torch.uint8, 2: torch.int16}[elem]
+    n = int(np.prod(shape))
+    for jit in (True, False):
+        prog = vp.build_program(vp.TensorLayout.from_shape(shape, elem), vp.from_numpy_convention(axes),
+                                force="tile", jit=jit)
+        assert mode in prog.text, prog.text
+        x = torch.randint(0, 255, (n * elem,), dtype=torch.uint8, device="cuda")
+        want = x.view(dt).view(shape).permute(axes).reshape(-1)
+        y = execute_device(prog, x)
+        assert torch.equal(y.view(dt).view(-1), want), (shape, axes, elem, jit)
+        big = torch.empty(n * elem + elem, dtype=torch.uint8, device="cuda")
+        execute_device(prog, x, out=big[elem:])
+        assert torch.equal(big[elem:].view(dt), want), (shape, axes, elem, jit, "misaligned dst")

@@ -25,6 +25,17 @@ if len(sys.argv) > 1 and sys.argv[1] == "sweep":
         CASES.append(((a, b, L), (1, 0, 2), 8))
         c = max(2, int(round(per ** (1 / 3))))
         CASES.append(((c, max(2, per // (c * c)), c, L), (2, 0, 1, 3), 8))
+if len(sys.argv) > 1 and sys.argv[1] == "sweep16":
+    # rows that ARE a multiple of 16 bytes (rows kernel / TMA bulk rows today)
+    CASES = []
+    for E in (4, 8):
+        for rb in (512, 1024, 2048, 4096, 16384):
+            L = rb // E
+            per = (96 << 20) // (E * L)
+            a = int(max(2, round((per / 3) ** 0.5)))
+            CASES.append(((a, max(2, per // a), L), (1, 0, 2), E))
+            c = max(2, int(round(per ** (1 / 3))))
+            CASES.append(((c, max(2, per // (c * c)), c, L), (2, 0, 1, 3), E))
 dev = torch.device("cuda", 0)
 fl = bench.Flusher(torch, dev)
 st = torch.cuda.current_stream()
