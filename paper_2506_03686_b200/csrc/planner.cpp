@@ -352,6 +352,7 @@ struct VecChoice {
     bool swz_addr = true;  // (128-byte residue layouts) address swizzle; off when the bank model prefers plain
     bool res16 = false;    // residue modulus of one 16-byte chunk (TMA bulk reads of misaligned runs)
     bool lin = false;      // W as destination-linear 16-byte chunks (LinDesc)
+    int wk = 0;            // W in k x V interleave blocks (k = extent of the destination-innermost dim)
 };
 
 // smem strides of the tile dims for a given pitch (source run dense, run
@@ -434,13 +435,15 @@ int64_t res_modulus(int E) {
 // R with vr > 1: the leading entry is grouped by vr.  W with vw > 1: dim 0
 // is grouped by vw (its V elements are one smem vector, stored separately).
 std::vector<PDimH> phase_dims(const Problem &Pb, const TileGeom &g, const int64_t *sstr,
-                              const int *slot_of_dim, bool write, int vec, int64_t hmask = 0, bool w2 = false) {
+                              const int *slot_of_dim, bool write, int vec, int64_t hmask = 0, bool w2 = false,
+                              int wk = 0) {
     std::vector<PDimH> L;
     bool in_run[kMaxRank] = {false};
     for (int i = 0; i < g.nsrc; ++i) in_run[g.src_dims[i]] = true;
     for (int i = 0; i < Pb.r; ++i) {
         int k = write ? Pb.sigma[i] : i;
         if (g.ext[k] == 0) continue;
+        if (write && wk > 0 && i == 0) continue;    // k x V blocks: the innermost dim is inside each block
         PDimH d{g.ext[k], write ? Pb.out_stride_of_dim[k] : Pb.in_stride[k], sstr[k], slot_of_dim[k], 1};
         if (write && hmask && !in_run[k]) d.hmul = Pb.in_stride[k] & hmask;
         // W: dim 0 groups by V (one smem vector); with w2 the destination's
@@ -726,6 +729,26 @@ bool w2_vectorizable(const Problem &Pb, const TileGeom &g, int V) {
     return true;
 }
 
+// W in k x V interleave blocks: the destination-innermost dim c = sigma[0]
+// is small (k = 2..8, wholly inside the tile, its own smem rows) and the
+// next destination dim is source dim 0, grouped by V.  A block = k smem
+// vectors (one per c, V consecutive dim-0 elements each) = k*V consecutive
+// destination elements, stored as k 16-byte chunks (image CHW -> HWC: 3 x
+// 16 bytes per block).  Block starts keep 16-byte alignment when d[0] and
+// the tile's dim-0 extent are multiples of V.  Returns k, or 0.
+int wk_extent(const Problem &Pb, const TileGeom &g, int V) {
+    if (V <= 1 || Pb.r < 2) return 0;
+    const int c = Pb.sigma[0];
+    if (c == 0 || Pb.sigma[1] != 0) return 0;
+    const int64_t k = Pb.d[c];
+    if (k < 2 || k > 8 || g.ext[c] != k) return 0;
+    for (int i = 0; i < g.nsrc; ++i)
+        if (g.src_dims[i] == c) return 0;
+    if (g.ext[0] == 0 || g.ext[0] % V || Pb.d[0] % V) return 0;
+    if (Pb.G >= 1 && (Pb.n / Pb.G) % V) return 0;
+    return (int)k;
+}
+
 bool w_vectorizable(const Problem &Pb, const TileGeom &g, int V) {
     if (V <= 1) return false;
     if (g.ext[0] == 0 || g.ext[0] % V) return false;
@@ -771,7 +794,7 @@ uint64_t lin_table_bytes(int64_t Ld, int V) {
 
 bool lin_applicable(const Problem &Pb, const TileGeom &g, const VecChoice &vc) {
     if (Pb.lin_mode == 0 || Pb.E >= 16) return false;
-    if (vc.vw > 1 || vc.w2 || vc.bulk || (vc.rshift && !vc.rres)) return false;
+    if (vc.vw > 1 || vc.w2 || vc.wk || vc.bulk || (vc.rshift && !vc.rres)) return false;
     const int V = 16 / Pb.E;
     if (g.Ld < 2 * V || g.ndst > kMaxLinDims || g.T / g.Ld > 0xffffffffLL) return false;
     int nx = 0;
@@ -870,11 +893,14 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
     double u0 = make_phase(vc.rshift ? shift_r_dims(Pb, g, sstr, slot_of_dim, V)
                                      : phase_dims(Pb, g, sstr, slot_of_dim, false, vc.vr),
                            NT, tp.ph[0], tp.lim_split[0]);
-    double u1 = make_phase(phase_dims(Pb, g, sstr, slot_of_dim, true, vc.vw, hmask, vc.w2), NT, tp.ph[1],
+    double u1 = make_phase(phase_dims(Pb, g, sstr, slot_of_dim, true, vc.vw, hmask, vc.w2, vc.wk), NT, tp.ph[1],
                            tp.lim_split[1]);
     if (vc.w2) {
         tp.ph[1].w2 = 1;
         tp.ph[1].vrow = (uint32_t)sstr[Pb.sigma[0]];    // == pitch (w2_vectorizable)
+    } else if (vc.wk) {
+        tp.ph[1].w2 = (uint32_t)vc.wk;                  // >= 2: k x V interleave blocks
+        tp.ph[1].vrow = (uint32_t)sstr[Pb.sigma[0]];    // smem stride of the innermost destination dim
     }
     if (vc.lin) fill_lin(Pb, g, sstr, slot_of_dim, NT, tp);
     tp.ph[0].rshift = vc.rshift ? (vc.rres ? 2u : 1u) : 0u;
@@ -1059,7 +1085,8 @@ double tile_cost(const Problem &Pb, const TileParams &tp) {
         // (odd 2-D transposes 0.70 -> 0.78 of copy; random-shape p10 +1-3%)
         const double kr = getenv("VPG_R_OP_COST") ? atof(getenv("VPG_R_OP_COST")) : 8.0;
         if (ph == 0) cost += ops * (kr + avg_w + (checked ? 2.0 : 0.0));
-        else if (d.w2) cost += ops * (V * avg_w + V + 1.0 + (checked ? 2.0 : 0.0));    // V LDS.128 + V STG.128
+        else if (d.w2 == 1) cost += ops * (V * avg_w + V + 1.0 + (checked ? 2.0 : 0.0));    // V LDS.128 + V STG.128
+        else if (d.w2 >= 2) cost += ops * (d.w2 * avg_w + d.w2 + 1.0 + (checked ? 2.0 : 0.0)); // k LDS.128 + k STG.128
         else cost += ops * (avg_w + (V > 1 ? V : 1) + 1.0 + (checked ? 2.0 : 0.0)); // LDS + STGs
     }
     return cost;
@@ -1117,14 +1144,16 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
             // congruent rows (pitch = run, no padding), chunk swizzle against
             // the W bank conflicts; per-lane cp.async then requests each L2
             // sector once instead of ~twice
-            for (int w2 = 0; w2 < 2; ++w2) {
-                if (w2 && !(op.vw > 1 && !Pb.no_w2 && w2_vectorizable(Pb, g, V))) continue;
+            for (int w2 = 0; w2 < 3; ++w2) {
+                if (w2 == 1 && !(op.vw > 1 && !Pb.no_w2 && w2_vectorizable(Pb, g, V))) continue;
+                if (w2 == 2 && !(op.vw > 1 && !Pb.no_w2 && wk_extent(Pb, g, V))) continue;
                 TileParams tp;
                 VecChoice vc;
                 vc.vr = op.vr;
                 vc.vw = op.vw;
                 vc.sw128 = true;
-                vc.w2 = w2 != 0;
+                vc.w2 = w2 == 1;
+                vc.wk = w2 == 2 ? wk_extent(Pb, g, V) : 0;
                 fill_tile_params(Pb, g, (uint32_t)g.Ls, NT, vc, tp);
                 double c = tile_cost(Pb, tp) * s128_factor;
                 if (getenv("VPG_DEBUG_PLAN"))
@@ -1253,6 +1282,21 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
                 vc_out = vc;
             }
             lin_try(vc, pitch, 1.0);
+            // k x V interleave blocks on the same layout (16-byte aligned rows)
+            if (op.vw > 1 && !op.rshift && !Pb.no_w2 && (pitch * Pb.E) % 16 == 0 && wk_extent(Pb, g, V)) {
+                VecChoice vk = vc;
+                vk.wk = wk_extent(Pb, g, V);
+                fill_tile_params(Pb, g, pitch, NT, vk, tp);
+                const double ck = tile_cost(Pb, tp);
+                if (getenv("VPG_DEBUG_PLAN"))
+                    fprintf(stderr, "[plan] Ls %lld Ld %lld pitch %u wk %d cost %.1f per-elem %.3f\n",
+                            (long long)g.Ls, (long long)g.Ld, pitch, vk.wk, ck, ck / (double)g.T);
+                if (best < 0 || ck < best - 1e-9) {
+                    best = ck;
+                    pitch_out = pitch;
+                    vc_out = vk;
+                }
+            }
         }
     }
 }
@@ -1460,7 +1504,9 @@ static void describe(vpg_plan *p) {
                           : " (TMA bulk copy per source run, producer warp)")
                    : (t.ph[0].rshift == 2 ? " (aligned supersets of misaligned runs, residue row strides)"
                                        : t.ph[0].rshift ? " (aligned supersets of misaligned runs)" : ""),
-            t.ph[1].vec, t.ph[1].w2 ? " (VxV register-transposed blocks, 16-byte stores)" : "");
+            t.ph[1].vec, t.ph[1].w2 == 1 ? " (VxV register-transposed blocks, 16-byte stores)"
+                         : t.ph[1].w2 >= 2 ? " (k x V interleave blocks, 16-byte stores)" : "");
+        if (t.ph[1].w2 >= 2) put("W interleave: k = %u destination-innermost elements per dim-0 element\n", t.ph[1].w2);
         if (t.lin.on)
             put("W lin: destination-linear %u-byte chunks, one store each (runs of %u elements, %u chunk slots x %u "
                 "runs, offset table %u bytes, bank rotation %s)\n",
@@ -1749,6 +1795,34 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         uint32_t pitch;
         VecChoice vc;
         choose_pitch_vec(P, g, threads, pitch, vc);
+        // V x V register-transposed W blocks (16-byte stores on both sides)
+        // are the fastest W mode; when the model's first tile cannot use them
+        // and a later candidate within 30% of its geometry cost can, take that
+        // one (batched 2048 x 128 transposes, attention K^T: a contiguous
+        // 8192-element source block with scalar-width stores ran 0.81 / 0.71
+        // of copy_ in f32 / bf16, the 64 x 128 V x V tile 1.04 / 1.00,
+        // tools/cand_scan.py; on the 31 random shapes of
+        // profiles/cand_data_r2.jsonl the rule changes 1-2 plans, none worse)
+        const char *vxv = getenv("VPG_PREFER_VXV");    // 0: off (experiments)
+        if (pick < 0 && !vc.w2 && !P.force_bulk && !(vxv && atoi(vxv) == 0)) {
+            for (int k = 1; k < 10; ++k) {
+                TileGeom gk;
+                if (!select_tile(P, gk, k)) break;
+                if (gk.cost > 1.3 * g.cost) continue;
+                const int tk = gk.T >= 1024 ? kTileThreads : (gk.T >= 256 ? 128 : 64);
+                const int thk = force_threads >= 32 && force_threads <= 1024 ? force_threads / 32 * 32 : tk;
+                uint32_t pk;
+                VecChoice vk;
+                choose_pitch_vec(P, gk, thk, pk, vk);
+                if (vk.w2) {
+                    g = gk;
+                    threads = thk;
+                    pitch = pk;
+                    vc = vk;
+                    break;
+                }
+            }
+        }
         // Small problems with misaligned source runs also consider the 32 KiB
         // budget (their residue rows pad a tile by up to a third) and keep it
         // when the geometry cost plus the walk cost (issued smem/memory ops
@@ -1825,6 +1899,7 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         vs.rshift = false;
         vs.bulk = false;
         vs.w2 = false;      // 16-byte destination stores need an aligned dst too
+        vs.wk = 0;
         vs.lin = false;
         fill_tile_params(P, g, pitch, threads, vs, p->tile_unaligned);
         // the tile count must fit the 32-bit tile index

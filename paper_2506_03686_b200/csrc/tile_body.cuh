@@ -408,6 +408,65 @@ __device__ __forceinline__ void tile_write_w2(const PhaseDesc &d, const ThreadPa
     }
 }
 
+// W in k x V interleave blocks (PhaseDesc::w2 = k >= 2): k 16-byte smem
+// vectors (one per value of the destination-innermost dim c, V consecutive
+// dim-0 elements each, rows vrow elements apart) are interleaved in
+// registers into k*V consecutive destination elements -- destination
+// element (w, c) is word w of vector c -- and stored as k 16-byte chunks.
+template <typename W, int K>
+__device__ __forceinline__ void wk_block(W *gp, const unsigned char *smem, const PhaseDesc &d, uint32_t bb,
+                                         uint32_t s0) {
+    constexpr int V = 16 / (int)sizeof(W);
+    uint4 v[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) v[c] = *sptr<uint4>(smem, soff<W>(d, bb, s0 + (uint32_t)c * d.vrow));
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        alignas(16) W o[V];
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+            const int e = j * V + i;
+            o[i] = reinterpret_cast<const W *>(&v[e % K])[e / K];
+        }
+        st_out(reinterpret_cast<uint4 *>(gp + j * V), *reinterpret_cast<const uint4 *>(o));
+    }
+}
+
+template <typename W, int K>
+__device__ __forceinline__ void tile_write_wk_k(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
+                                                W *__restrict__ gdst, uint32_t bb, uint32_t mask, const Lim lim) {
+    const uint32_t o0 = d.ngroups == 1 ? 0u : t.grp;
+    VPG_UNROLL
+    for (uint32_t o = o0; o < d.n_outer; o += d.ngroups) {
+        const OuterEntry e = outer_entry(d, smem, o);
+        W *gp = gdst + (t.g + e.g);
+        const uint32_t sb = t.s + e.s;
+        uint32_t c0 = t.c0 + e.c0, c1 = t.c1 + e.c1, c2 = t.c2;
+        VPG_UNROLL
+        for (uint32_t i = 0; i < d.n_in; ++i) {
+            if (mask == 0 || slot_ok(mask, c0, c1, c2, lim))
+                wk_block<W, K>(gp + (int64_t)i * d.g_in, smem, d, bb, sb + i * d.s_in);
+            c0 += d.c_in[0];
+            c1 += d.c_in[1];
+            c2 += d.c_in[2];
+        }
+    }
+}
+
+template <typename W>
+__device__ __forceinline__ void tile_write_wk(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
+                                              W *__restrict__ gdst, uint32_t bb, uint32_t mask, const Lim lim) {
+    switch (d.w2) {
+        case 2: tile_write_wk_k<W, 2>(d, t, smem, gdst, bb, mask, lim); break;
+        case 3: tile_write_wk_k<W, 3>(d, t, smem, gdst, bb, mask, lim); break;
+        case 4: tile_write_wk_k<W, 4>(d, t, smem, gdst, bb, mask, lim); break;
+        case 5: tile_write_wk_k<W, 5>(d, t, smem, gdst, bb, mask, lim); break;
+        case 6: tile_write_wk_k<W, 6>(d, t, smem, gdst, bb, mask, lim); break;
+        case 7: tile_write_wk_k<W, 7>(d, t, smem, gdst, bb, mask, lim); break;
+        default: tile_write_wk_k<W, 8>(d, t, smem, gdst, bb, mask, lim); break;
+    }
+}
+
 template <typename W, bool VEC>
 __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
                                                 W *__restrict__ gdst, uint32_t bb, uint32_t mask,
@@ -566,8 +625,12 @@ __device__ __forceinline__ void tile_write(const PhaseDesc &d, const ThreadPart 
     }
 #endif
     if constexpr (sizeof(W) < 16) {
-        if (d.w2) {
+        if (d.w2 == 1) {
             tile_write_w2<W>(d, t, smem, gdst, bb, mask, lim);
+            return;
+        }
+        if (d.w2 >= 2) {
+            tile_write_wk<W>(d, t, smem, gdst, bb, mask, lim);
             return;
         }
         if (d.vec > 1) {

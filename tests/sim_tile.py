@@ -323,6 +323,28 @@ def simulate(program, src_words: np.ndarray, threads: int | None = None, shard_o
                                     smem[spx + j] = src_words[gabs + j]
                                     smem_valid[spx + j] = True
                         else:
+                            if d.w2 >= 2:
+                                # k x V interleave block: k smem vectors (one per value of
+                                # the destination-innermost dim, rows vrow apart) -> k*V
+                                # consecutive destination elements, k 16-byte stores
+                                K = d.w2
+                                gabs = db + gp
+                                if (gabs % V).any():
+                                    raise SimError("W interleave block store misaligned")
+                                for c in range(K):
+                                    spx = _swizzle(d, sp + tbase + c * d.vrow, 16 // E)
+                                    if (spx % V).any():
+                                        raise SimError("W interleave smem vector misaligned")
+                                    for w in range(V):
+                                        so = spx + w
+                                        _chk(so, alloc, "Wk smem")
+                                        dd = gabs + w * K + c
+                                        _chk(dd, dbound, "Wk global")
+                                        if not smem_valid[so].all():
+                                            raise SimError(f"W reads smem never written (tile {t})")
+                                        dst[dd] = smem[so]
+                                        written[dd] += 1
+                                continue
                             if d.w2:
                                 # V x V block: V smem vectors from rows vrow apart (same
                                 # swizzle row group) -> V 16-byte stores of V consecutive

@@ -458,3 +458,34 @@ def test_small_words_vectorised(cuda, shape, axes, elem, mode):
         big = torch.empty(n * elem + elem, dtype=torch.uint8, device="cuda")
         execute_device(prog, x, out=big[elem:])
         assert torch.equal(big[elem:].view(dt), want), (shape, axes, elem, jit, "misaligned dst")
+
+
+@pytest.mark.parametrize("shape,axes,elem", [
+    ((8, 3, 256, 256), (0, 2, 3, 1), 1),      # u8 image CHW -> HWC
+    ((8, 3, 256, 256), (0, 2, 3, 1), 2),      # bf16
+    ((8, 3, 256, 256), (0, 2, 3, 1), 4),      # f32
+    ((4, 4, 128, 384), (0, 2, 3, 1), 1),      # RGBA
+    ((64, 2, 4096), (0, 2, 1), 4),            # (re, im) planes -> interleaved
+    ((16, 5, 96, 64), (0, 2, 3, 1), 2),       # k = 5
+])
+def test_interleave_blocks(cuda, shape, axes, elem):
+    """W in k x V interleave blocks (a small destination-innermost dim, k =
+    2..8, after source dim 0): k 16-byte smem vectors -> k 16-byte stores;
+    bit-exact against torch, specialised and ahead-of-time kernels."""
+    import torch
+
+    import paper_2506_03686_b200 as vp
+    from paper_2506_03686_b200.api import execute_device
+
+    dt = {1: torch.uint8, 2: torch.int16, 4: torch.int32}[elem]
+    n = int(np.prod(shape))
+    seen = 0
+    for jit in (True, False):
+        prog = vp.build_program(vp.TensorLayout.from_shape(shape, elem), vp.from_numpy_convention(axes),
+                                force="tile", jit=jit)
+        seen += "interleave" in prog.text
+        x = torch.randint(0, 255, (n * elem,), dtype=torch.uint8, device="cuda")
+        want = x.view(dt).view(shape).permute(axes).reshape(-1)
+        y = execute_device(prog, x)
+        assert torch.equal(y.view(dt).view(-1), want), (shape, axes, elem, jit)
+    assert seen >= 1, prog.text
