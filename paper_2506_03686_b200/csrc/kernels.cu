@@ -480,7 +480,9 @@ vpg_status launch_tile(const vpg_plan *p, const void *src, void *dst, const Shar
     sa.trace = trace_begin(st);
     const int smem = (int)p->tile.smem_bytes;
     bool aligned = !(p->tile.ph[0].vec > 1 && ((uintptr_t)src % 16));
-    if (p->tile.ph[1].w2) {      // 16-byte destination stores: every destination buffer 16-byte aligned
+    // 16-byte destination stores (V x V / interleave blocks, or vectors of a
+    // preserved stride-1 dim): every destination buffer 16-byte aligned
+    if (p->tile.ph[1].w2 || (p->tile.ph[1].vec > 1 && p->tile.ph[1].vstride == 1)) {
         if ((uintptr_t)dst % 16) aligned = false;
         for (int q = 1; q < (int)p->tile.nshards && !p->tile.pull; ++q)
             if ((sa.off[q] * E) % 16) aligned = false;

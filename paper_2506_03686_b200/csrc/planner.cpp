@@ -752,8 +752,12 @@ int wk_extent(const Problem &Pb, const TileGeom &g, int V) {
 bool w_vectorizable(const Problem &Pb, const TileGeom &g, int V) {
     if (V <= 1) return false;
     if (g.ext[0] == 0 || g.ext[0] % V) return false;
-    if (Pb.sigma[0] == 0) return false;     // dim 0 is the destination's stride-1 dim: not this mode
     if (g.ext[0] < Pb.d[0] && (Pb.d[0] % g.ext[0]) % V) return false;  // ragged dim-0 extents
+    // dim 0 is also the destination's stride-1 dim: each smem vector is one
+    // 16-byte destination chunk (one store), aligned when d[0] is a multiple
+    // of V (short rows below the rows kernel's 512 bytes: attention head
+    // splits of 64-128 fp16/u8 elements)
+    if (Pb.sigma[0] == 0) return Pb.d[0] % V == 0 && !(Pb.G >= 1 && (Pb.n / Pb.G) % V);
     return true;
 }
 
@@ -1900,6 +1904,7 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         vs.bulk = false;
         vs.w2 = false;      // 16-byte destination stores need an aligned dst too
         vs.wk = 0;
+        if (P.sigma[0] == 0) vs.vw = 1;   // (its vector W would be 16-byte stores)
         vs.lin = false;
         fill_tile_params(P, g, pitch, threads, vs, p->tile_unaligned);
         // the tile count must fit the 32-bit tile index

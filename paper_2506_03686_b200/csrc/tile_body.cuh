@@ -467,6 +467,21 @@ __device__ __forceinline__ void tile_write_wk(const PhaseDesc &d, const ThreadPa
     }
 }
 
+// W with vec > 1: the V elements of one 16-byte smem vector go to V
+// destinations vs apart -- one 16-byte store when they are consecutive
+// (vs == 1: the stride-1 dim is preserved, the vector is a destination chunk)
+template <typename W>
+__device__ __forceinline__ void store_vec(W *gp, const uint4 &v, int64_t vs) {
+    constexpr int V = 16 / (int)sizeof(W);
+    if (vs == 1) {
+        st_out(reinterpret_cast<uint4 *>(gp), v);
+        return;
+    }
+    const W *w = reinterpret_cast<const W *>(&v);
+#pragma unroll
+    for (int j = 0; j < V; ++j) st_out(gp + j * vs, w[j]);
+}
+
 template <typename W, bool VEC>
 __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
                                                 W *__restrict__ gdst, uint32_t bb, uint32_t mask,
@@ -494,11 +509,7 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
 #pragma unroll
                     for (int u = 0; u < U; ++u) v[u] = *sptr<uint4>(smem, soff<W>(d, bb, s + u * s_in));
 #pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const W *w = reinterpret_cast<const W *>(&v[u]);
-#pragma unroll
-                        for (int j = 0; j < V; ++j) st_out(gp + u * g_in + j * vs, w[j]);
-                    }
+                    for (int u = 0; u < U; ++u) store_vec<W>(gp + u * g_in, v[u], vs);
                 } else {
                     W v[U];
 #pragma unroll
@@ -513,10 +524,7 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
             }
             for (; i < n_in; ++i) {
                 if constexpr (VEC) {
-                    uint4 v = *sptr<uint4>(smem, soff<W>(d, bb, s));
-                    const W *w = reinterpret_cast<const W *>(&v);
-#pragma unroll
-                    for (int j = 0; j < V; ++j) st_out(gp + j * vs, w[j]);
+                    store_vec<W>(gp, *sptr<uint4>(smem, soff<W>(d, bb, s)), vs);
                 } else {
                     *gp = *sptr<W>(smem, soff<W>(d, bb, s + (hh & hmask)));
                 }
@@ -555,10 +563,7 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
             for (; i < n_in; ++i) {
                 if (slot_ok(mask, c0, c1, c2, lim)) {
                     if constexpr (VEC) {
-                        uint4 v = *sptr<uint4>(smem, soff<W>(d, bb, s));
-                        const W *w = reinterpret_cast<const W *>(&v);
-#pragma unroll
-                        for (int j = 0; j < V; ++j) st_out(gp + j * vs, w[j]);
+                        store_vec<W>(gp, *sptr<uint4>(smem, soff<W>(d, bb, s)), vs);
                     } else {
                         *gp = *sptr<W>(smem, soff<W>(d, bb, s + (hh & hmask)));
                     }

@@ -371,6 +371,8 @@ def simulate(program, src_words: np.ndarray, threads: int | None = None, shard_o
                             gabs = db + gp
                             if V > 1 and (spx % V).any():
                                 raise SimError("W vector smem access misaligned")
+                            if V > 1 and d.vstride == 1 and ((db + gp) % V).any():
+                                raise SimError("W 16-byte destination chunk misaligned")
                             for j in range(V):
                                 _chk(spx + j, alloc, "W smem")
                                 dd = gabs + j * d.vstride

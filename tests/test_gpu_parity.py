@@ -489,3 +489,32 @@ def test_interleave_blocks(cuda, shape, axes, elem):
         y = execute_device(prog, x)
         assert torch.equal(y.view(dt).view(-1), want), (shape, axes, elem, jit)
     assert seen >= 1, prog.text
+
+
+@pytest.mark.parametrize("shape,axes,elem", [
+    ((8, 512, 16, 64), (0, 2, 1, 3), 2),     # attention head split, bf16, 128-byte rows
+    ((8, 512, 16, 64), (0, 2, 1, 3), 1),     # u8, 64-byte rows
+    ((4, 256, 12, 32), (0, 2, 1, 3), 4),     # f32, 128-byte rows
+    ((3, 5, 7, 96), (2, 0, 1, 3), 2),
+])
+def test_short_rows_vector_stores(cuda, shape, axes, elem):
+    """Stride-1-preserving permutations with rows below the rows kernel's
+    512 bytes run on the tile kernel with each 16-byte smem vector stored as
+    one 16-byte destination chunk; bit-exact, aligned and misaligned
+    destinations (the latter takes the scalar-store variant)."""
+    import torch
+
+    import paper_2506_03686_b200 as vp
+    from paper_2506_03686_b200.api import execute_device
+
+    dt = {1: torch.uint8, 2: torch.int16, 4: torch.int32}[elem]
+    n = int(np.prod(shape))
+    for jit in (True, False):
+        prog = vp.build_program(vp.TensorLayout.from_shape(shape, elem), vp.from_numpy_convention(axes), jit=jit)
+        assert prog.kernel == "tile"
+        x = torch.randint(0, 255, (n * elem,), dtype=torch.uint8, device="cuda")
+        want = x.view(dt).view(shape).permute(axes).reshape(-1)
+        assert torch.equal(execute_device(prog, x).view(dt).view(-1), want), (shape, jit)
+        big = torch.empty(n * elem + elem, dtype=torch.uint8, device="cuda")
+        execute_device(prog, x, out=big[elem:])
+        assert torch.equal(big[elem:].view(dt), want), (shape, jit, "misaligned dst")
