@@ -138,9 +138,12 @@ struct PhaseDesc {
     // destination-innermost groups, so each store instruction writes 512
     // contiguous bytes; the swizzle keys on the row group (swz = 1 + log2 V),
     // so those lanes' smem vectors fall on distinct banks.
-    uint32_t w2;
+    uint32_t w2;                   // 1: V x V blocks; 2..8: k x V interleave blocks; kW2Gather: gather blocks
     uint32_t vrow;
 };
+// PhaseDesc::w2 value of the gather W mode: V destination-innermost elements
+// (V smem rows vrow apart, scalar loads) packed into one 16-byte store
+constexpr uint32_t kW2Gather = 64;
 
 // W phase as destination-linear 16-byte chunks ("lin" mode), for tiles whose
 // destination runs are misaligned or not a multiple of V = 16/E elements

@@ -81,6 +81,7 @@ struct Problem {
     bool no_res = false;   // disable residue row strides for shifted runs (VPG_NO_RES)
     bool no_sw128 = false; // disable the 128-byte congruent layout (VPG_NO_SW128; bulk-read plans)
     bool no_w2 = false;    // disable V x V register-transposed W blocks (VPG_NO_W2)
+    bool no_wg = false;    // disable gather W blocks (VPG_WG=0)
     bool no_swz_addr = false; // 128-byte residue layouts without the address swizzle (VPG_NO_SWZ_ADDR)
     bool no_bulk = false;  // TMA bulk source reads off (VPG_BULK=0, pull exchanges)
     bool force_bulk = false; // TMA bulk source reads wherever they apply (VPG_BULK=1)
@@ -353,6 +354,7 @@ struct VecChoice {
     bool res16 = false;    // residue modulus of one 16-byte chunk (TMA bulk reads of misaligned runs)
     bool lin = false;      // W as destination-linear 16-byte chunks (LinDesc)
     int wk = 0;            // W in k x V interleave blocks (k = extent of the destination-innermost dim)
+    bool wg = false;       // W in gather blocks: V destination-innermost elements -> one 16-byte store
 };
 
 // smem strides of the tile dims for a given pitch (source run dense, run
@@ -436,7 +438,7 @@ int64_t res_modulus(int E) {
 // is grouped by vw (its V elements are one smem vector, stored separately).
 std::vector<PDimH> phase_dims(const Problem &Pb, const TileGeom &g, const int64_t *sstr,
                               const int *slot_of_dim, bool write, int vec, int64_t hmask = 0, bool w2 = false,
-                              int wk = 0) {
+                              int wk = 0, int wg = 0) {
     std::vector<PDimH> L;
     bool in_run[kMaxRank] = {false};
     for (int i = 0; i < g.nsrc; ++i) in_run[g.src_dims[i]] = true;
@@ -453,6 +455,13 @@ std::vector<PDimH> phase_dims(const Problem &Pb, const TileGeom &g, const int64_
             d.g *= vec;
             d.s *= vec;
             d.cmul = vec;
+        }
+        // W gather blocks: the destination-innermost dim groups by wg (= V)
+        if (write && wg > 1 && i == 0) {
+            d.e /= wg;
+            d.g *= wg;
+            d.s *= wg;
+            d.cmul = wg;
         }
         if (!L.empty()) {
             PDimH &p = L.back();
@@ -736,6 +745,22 @@ bool w2_vectorizable(const Problem &Pb, const TileGeom &g, int V) {
 // destination elements, stored as k 16-byte chunks (image CHW -> HWC: 3 x
 // 16 bytes per block).  Block starts keep 16-byte alignment when d[0] and
 // the tile's dim-0 extent are multiples of V.  Returns k, or 0.
+// W in gather blocks: V consecutive destination-innermost elements (V smem
+// rows, scalar loads) packed into one 16-byte store -- the destination-
+// innermost dim sigma[0] is a run-index dim (its own smem rows) whose tile
+// extent and full extent are multiples of V, so every block starts 16-byte
+// aligned.  Where the W phase would otherwise store one 1-, 2- or 4-byte
+// word per lane (misaligned source runs, residue rows).
+bool wg_vectorizable(const Problem &Pb, const TileGeom &g, int V) {
+    if (V <= 1) return false;
+    const int k1 = Pb.sigma[0];
+    if (k1 == 0 || g.ext[k1] == 0 || g.ext[k1] % V || Pb.d[k1] % V) return false;
+    for (int i = 0; i < g.nsrc; ++i)
+        if (g.src_dims[i] == k1) return false;
+    if (Pb.G >= 1 && (Pb.n / Pb.G) % V) return false;
+    return true;
+}
+
 int wk_extent(const Problem &Pb, const TileGeom &g, int V) {
     if (V <= 1 || Pb.r < 2) return 0;
     const int c = Pb.sigma[0];
@@ -798,7 +823,7 @@ uint64_t lin_table_bytes(int64_t Ld, int V) {
 
 bool lin_applicable(const Problem &Pb, const TileGeom &g, const VecChoice &vc) {
     if (Pb.lin_mode == 0 || Pb.E >= 16) return false;
-    if (vc.vw > 1 || vc.w2 || vc.wk || vc.bulk || (vc.rshift && !vc.rres)) return false;
+    if (vc.vw > 1 || vc.w2 || vc.wk || vc.wg || vc.bulk || (vc.rshift && !vc.rres)) return false;
     const int V = 16 / Pb.E;
     if (g.Ld < 2 * V || g.ndst > kMaxLinDims || g.T / g.Ld > 0xffffffffLL) return false;
     int nx = 0;
@@ -897,14 +922,17 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
     double u0 = make_phase(vc.rshift ? shift_r_dims(Pb, g, sstr, slot_of_dim, V)
                                      : phase_dims(Pb, g, sstr, slot_of_dim, false, vc.vr),
                            NT, tp.ph[0], tp.lim_split[0]);
-    double u1 = make_phase(phase_dims(Pb, g, sstr, slot_of_dim, true, vc.vw, hmask, vc.w2, vc.wk), NT, tp.ph[1],
-                           tp.lim_split[1]);
+    double u1 = make_phase(phase_dims(Pb, g, sstr, slot_of_dim, true, vc.vw, hmask, vc.w2, vc.wk,
+                                      vc.wg ? V : 0), NT, tp.ph[1], tp.lim_split[1]);
     if (vc.w2) {
         tp.ph[1].w2 = 1;
         tp.ph[1].vrow = (uint32_t)sstr[Pb.sigma[0]];    // == pitch (w2_vectorizable)
     } else if (vc.wk) {
         tp.ph[1].w2 = (uint32_t)vc.wk;                  // >= 2: k x V interleave blocks
         tp.ph[1].vrow = (uint32_t)sstr[Pb.sigma[0]];    // smem stride of the innermost destination dim
+    } else if (vc.wg) {
+        tp.ph[1].w2 = kW2Gather;
+        tp.ph[1].vrow = (uint32_t)sstr[Pb.sigma[0]];
     }
     if (vc.lin) fill_lin(Pb, g, sstr, slot_of_dim, NT, tp);
     tp.ph[0].rshift = vc.rshift ? (vc.rres ? 2u : 1u) : 0u;
@@ -1090,6 +1118,10 @@ double tile_cost(const Problem &Pb, const TileParams &tp) {
         const double kr = getenv("VPG_R_OP_COST") ? atof(getenv("VPG_R_OP_COST")) : 8.0;
         if (ph == 0) cost += ops * (kr + avg_w + (checked ? 2.0 : 0.0));
         else if (d.w2 == 1) cost += ops * (V * avg_w + V + 1.0 + (checked ? 2.0 : 0.0));    // V LDS.128 + V STG.128
+        else if (d.w2 == kW2Gather) {
+            const int Vg = 16 / Pb.E;          // V scalar LDS + one STG.128 (+ packing)
+            cost += ops * (Vg * avg_w + 1.0 + 0.25 * Vg + (checked ? 2.0 : 0.0));
+        }
         else if (d.w2 >= 2) cost += ops * (d.w2 * avg_w + d.w2 + 1.0 + (checked ? 2.0 : 0.0)); // k LDS.128 + k STG.128
         else cost += ops * (avg_w + (V > 1 ? V : 1) + 1.0 + (checked ? 2.0 : 0.0)); // LDS + STGs
     }
@@ -1124,6 +1156,23 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
     // factor) only where the rows are congruent to their source lines
     const bool s128 = rv && !Pb.no_sw128 && sw128_layout_ok(Pb, g);
     const double s128_factor = sw128_possible(Pb, g) ? kSw128CostFactor : 1.0;
+    // the same layout with the W phase in gather blocks (16-byte stores)
+    auto wg_try = [&](VecChoice vc, uint32_t pitch, double factor) {
+        if (vc.vw > 1 || vc.w2 || vc.wk || vc.bulk || vc.lin || (vc.rshift && !vc.rres) || Pb.no_wg) return;
+        if (!wg_vectorizable(Pb, g, V)) return;
+        vc.wg = true;
+        TileParams tp;
+        fill_tile_params(Pb, g, pitch, NT, vc, tp);
+        const double c = tile_cost(Pb, tp) * factor;
+        if (getenv("VPG_DEBUG_PLAN"))
+            fprintf(stderr, "[plan] Ls %lld Ld %lld pitch %u vr %d rshift %d rres %d gather cost %.1f per-elem %.3f\n",
+                    (long long)g.Ls, (long long)g.Ld, pitch, vc.vr, (int)vc.rshift, (int)vc.rres, c, c / (double)g.T);
+        if (best < 0 || c < best - 1e-9) {
+            best = c;
+            pitch_out = pitch;
+            vc_out = vc;
+        }
+    };
     // the same layout with the W phase as destination-linear 16-byte chunks
     auto lin_try = [&](VecChoice vc, uint32_t pitch, double factor) {
         if (!lin_applicable(Pb, g, vc)) return;
@@ -1169,6 +1218,7 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
                     vc_out = vc;
                 }
                 lin_try(vc, (uint32_t)g.Ls, s128_factor);
+                wg_try(vc, (uint32_t)g.Ls, s128_factor);
             }
         }
         if (op.rshift && !Pb.no_swz) {
@@ -1226,6 +1276,7 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
                     vc_out = vc;
                 }
                 lin_try(vc, pitch, kResidueCostFactor * (res_modulus(Pb.E) * Pb.E >= 128 ? kSw128CostFactor : 1.0));
+                wg_try(vc, pitch, kResidueCostFactor * (res_modulus(Pb.E) * Pb.E >= 128 ? kSw128CostFactor : 1.0));
             }
         }
         if (op.rshift && Pb.force_bulk && !Pb.no_bulk && (Pb.E == 4 || Pb.E == 8) && g.n_runidx <= kMaxPhaseDims) {
@@ -1286,6 +1337,7 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
                 vc_out = vc;
             }
             lin_try(vc, pitch, 1.0);
+            wg_try(vc, pitch, 1.0);
             // k x V interleave blocks on the same layout (16-byte aligned rows)
             if (op.vw > 1 && !op.rshift && !Pb.no_w2 && (pitch * Pb.E) % 16 == 0 && wk_extent(Pb, g, V)) {
                 VecChoice vk = vc;
@@ -1509,8 +1561,10 @@ static void describe(vpg_plan *p) {
                    : (t.ph[0].rshift == 2 ? " (aligned supersets of misaligned runs, residue row strides)"
                                        : t.ph[0].rshift ? " (aligned supersets of misaligned runs)" : ""),
             t.ph[1].vec, t.ph[1].w2 == 1 ? " (VxV register-transposed blocks, 16-byte stores)"
+                         : t.ph[1].w2 == kW2Gather ? " (gather blocks: 16-byte stores of destination-innermost runs)"
                          : t.ph[1].w2 >= 2 ? " (k x V interleave blocks, 16-byte stores)" : "");
-        if (t.ph[1].w2 >= 2) put("W interleave: k = %u destination-innermost elements per dim-0 element\n", t.ph[1].w2);
+        if (t.ph[1].w2 >= 2 && t.ph[1].w2 != kW2Gather)
+            put("W interleave: k = %u destination-innermost elements per dim-0 element\n", t.ph[1].w2);
         if (t.lin.on)
             put("W lin: destination-linear %u-byte chunks, one store each (runs of %u elements, %u chunk slots x %u "
                 "runs, offset table %u bytes, bank rotation %s)\n",
@@ -1652,6 +1706,7 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
     if (getenv("VPG_NO_RES")) P.no_res = true;
     if (getenv("VPG_NO_SW128")) P.no_sw128 = true;
     if (getenv("VPG_NO_W2")) P.no_w2 = true;
+    if (const char *e = getenv("VPG_WG")) P.no_wg = atoi(e) == 0;
     if (const char *e = getenv("VPG_LIN")) P.lin_mode = *e ? atoi(e) : 0;
     if (getenv("VPG_NO_SWZ_ADDR")) P.no_swz_addr = true;
     // the chunk swizzle removes the W bank conflicts of shifted runs but costs
@@ -1904,6 +1959,7 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         vs.bulk = false;
         vs.w2 = false;      // 16-byte destination stores need an aligned dst too
         vs.wk = 0;
+        vs.wg = false;
         if (P.sigma[0] == 0) vs.vw = 1;   // (its vector W would be 16-byte stores)
         vs.lin = false;
         fill_tile_params(P, g, pitch, threads, vs, p->tile_unaligned);

@@ -453,6 +453,36 @@ __device__ __forceinline__ void tile_write_wk_k(const PhaseDesc &d, const Thread
     }
 }
 
+// W in gather blocks (PhaseDesc::w2 == kW2Gather): V destination-innermost
+// elements from V smem rows vrow apart (scalar loads, any alignment: residue
+// rows included) packed into one 16-byte store.
+template <typename W>
+__device__ __forceinline__ void tile_write_wg(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
+                                              W *__restrict__ gdst, uint32_t bb, uint32_t mask, const Lim lim) {
+    constexpr int V = 16 / (int)sizeof(W);
+    const uint32_t o0 = d.ngroups == 1 ? 0u : t.grp;
+    VPG_UNROLL
+    for (uint32_t o = o0; o < d.n_outer; o += d.ngroups) {
+        const OuterEntry e = outer_entry(d, smem, o);
+        W *gp = gdst + (t.g + e.g);
+        const uint32_t sb = t.s + e.s;
+        uint32_t c0 = t.c0 + e.c0, c1 = t.c1 + e.c1, c2 = t.c2;
+        VPG_UNROLL
+        for (uint32_t i = 0; i < d.n_in; ++i) {
+            if (mask == 0 || slot_ok(mask, c0, c1, c2, lim)) {
+                alignas(16) W v[V];
+                const uint32_t s0 = sb + i * d.s_in;
+#pragma unroll
+                for (int j = 0; j < V; ++j) v[j] = *sptr<W>(smem, soff<W>(d, bb, s0 + (uint32_t)j * d.vrow));
+                st_out(reinterpret_cast<uint4 *>(gp + (int64_t)i * d.g_in), *reinterpret_cast<const uint4 *>(v));
+            }
+            c0 += d.c_in[0];
+            c1 += d.c_in[1];
+            c2 += d.c_in[2];
+        }
+    }
+}
+
 template <typename W>
 __device__ __forceinline__ void tile_write_wk(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
                                               W *__restrict__ gdst, uint32_t bb, uint32_t mask, const Lim lim) {
@@ -632,6 +662,10 @@ __device__ __forceinline__ void tile_write(const PhaseDesc &d, const ThreadPart 
     if constexpr (sizeof(W) < 16) {
         if (d.w2 == 1) {
             tile_write_w2<W>(d, t, smem, gdst, bb, mask, lim);
+            return;
+        }
+        if (d.w2 == kW2Gather) {
+            tile_write_wg<W>(d, t, smem, gdst, bb, mask, lim);
             return;
         }
         if (d.w2 >= 2) {

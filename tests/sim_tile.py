@@ -323,6 +323,23 @@ def simulate(program, src_words: np.ndarray, threads: int | None = None, shard_o
                                     smem[spx + j] = src_words[gabs + j]
                                     smem_valid[spx + j] = True
                         else:
+                            if d.w2 == 64:
+                                # gather block: V destination-innermost elements from V smem
+                                # rows vrow apart -> one 16-byte store
+                                Vg = 16 // E
+                                gabs = db + gp
+                                if (gabs % Vg).any():
+                                    raise SimError("W gather block store misaligned")
+                                for j in range(Vg):
+                                    spx = _swizzle(d, sp + tbase + j * d.vrow, 16 // E)
+                                    _chk(spx, alloc, "Wg smem")
+                                    dd = gabs + j
+                                    _chk(dd, dbound, "Wg global")
+                                    if not smem_valid[spx].all():
+                                        raise SimError(f"W reads smem never written (tile {t})")
+                                    dst[dd] = smem[spx]
+                                    written[dd] += 1
+                                continue
                             if d.w2 >= 2:
                                 # k x V interleave block: k smem vectors (one per value of
                                 # the destination-innermost dim, rows vrow apart) -> k*V

@@ -518,3 +518,36 @@ def test_short_rows_vector_stores(cuda, shape, axes, elem):
         big = torch.empty(n * elem + elem, dtype=torch.uint8, device="cuda")
         execute_device(prog, x, out=big[elem:])
         assert torch.equal(big[elem:].view(dt), want), (shape, jit, "misaligned dst")
+
+
+@pytest.mark.parametrize("shape,axes,elem", [
+    ((16, 256, 1000), (0, 2, 1), 1),          # u8 batched transpose, misaligned source runs
+    ((4, 512, 999), (0, 2, 1), 2),
+    ((80, 17, 59), (1, 2, 0), 1),
+    ((16, 18, 38), (2, 1, 0), 4),
+    ((10, 10, 47, 17), (0, 3, 2, 1), 8),
+])
+def test_gather_blocks(cuda, shape, axes, elem):
+    """W in gather blocks: V destination-innermost elements from V smem rows
+    (residue rows included) packed into one 16-byte store; bit-exact,
+    specialised and ahead-of-time kernels, a misaligned destination (scalar
+    variant) included."""
+    import torch
+
+    import paper_2506_03686_b200 as vp
+    from paper_2506_03686_b200.api import execute_device
+
+    dt = {1: torch.uint8, 2: torch.int16, 4: torch.int32, 8: torch.int64}[elem]
+    n = int(np.prod(shape))
+    seen = 0
+    for jit in (True, False):
+        prog = vp.build_program(vp.TensorLayout.from_shape(shape, elem), vp.from_numpy_convention(axes),
+                                force="tile", jit=jit)
+        seen += "gather blocks" in prog.text
+        x = torch.randint(0, 255, (n * elem,), dtype=torch.uint8, device="cuda")
+        want = x.view(dt).view(shape).permute(axes).reshape(-1)
+        assert torch.equal(execute_device(prog, x).view(dt).view(-1), want), (shape, jit)
+        big = torch.empty(n * elem + elem, dtype=torch.uint8, device="cuda")
+        execute_device(prog, x, out=big[elem:])
+        assert torch.equal(big[elem:].view(dt), want), (shape, jit, "misaligned dst")
+    assert seen >= 1, prog.text
