@@ -46,7 +46,7 @@ constexpr double kSw128CostFactor = 0.85;    // 128-byte congruent rows: half th
 // 48 KiB (mean 0.969 vs 0.969 of the best candidate); a 128 MiB cut measured
 // 0.972 -- not enough to move it.
 constexpr double kSmallProblemBytes = 512.0 * 1024 * 1024;
-constexpr double kWalkWeight = 8.0;
+constexpr double kWalkWeight = 4.0;
 constexpr double kSmallWordMisalignFactor = 1.5;
 constexpr int kSmCount = 148;         // B200 SMs (tiny-problem tiling; launches query the device)   // walk cost (ops/element) vs relative geometry cost, per byte of element
 
@@ -1885,7 +1885,9 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         // Small problems with misaligned source runs also consider the 32 KiB
         // budget (their residue rows pad a tile by up to a third) and keep it
         // when the geometry cost plus the walk cost (issued smem/memory ops
-        // per element, weight 8 per byte of element) is lower.  Round 2 kept
+        // per element, weight 4 per byte of element; 4 and 8 select alike on
+        // the calibration shapes except cfg3, whose 32 KiB tile runs 3%
+        // faster in the steady protocol) is lower.  Round 2 kept
         // the 32 KiB tile unconditionally (from cfg3: 18.65 -> 18.03 us
         // flushed); timing every candidate of 31 random permutations
         // (tools/cand_data.py, profiles/cand_data_r2.jsonl) showed that as the
