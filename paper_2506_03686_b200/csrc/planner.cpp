@@ -953,7 +953,8 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
     if (tp.lin.on) {
         uint32_t best_rs = 32;
         double best_w = lin_waves(Pb, tp.ph[1], tp.lin, 32);
-        for (uint32_t rs = 0; rs < 3; ++rs) {
+        static const bool no_rot = getenv("VPG_LIN_ROT") && atoi(getenv("VPG_LIN_ROT")) == 0;   // experiments
+        for (uint32_t rs = 0; rs < 3 && !no_rot; ++rs) {
             const double w = lin_waves(Pb, tp.ph[1], tp.lin, rs);
             if (w < best_w - 1e-9) {
                 best_w = w;

@@ -21,7 +21,7 @@ st = torch.cuda.current_stream()
 pool = torch.empty(2 * (512 << 20), dtype=torch.uint8, device=dev)
 rows = []
 for i in range(N):
-    E = int(rng.choice([4, 8]))
+    E = int(rng.choice([int(w) for w in os.environ.get("SWEEP_WORDS", "4,8").split(",")]))
     target = int(rng.choice([64, 128, 256, 512])) << 20
     r = int(rng.integers(2, 9))
     # random factorisation of target/E elements into r dims (mix of odd and even extents)
