@@ -82,6 +82,7 @@ struct Problem {
     bool no_sw128 = false; // disable the 128-byte congruent layout (VPG_NO_SW128; bulk-read plans)
     bool no_w2 = false;    // disable V x V register-transposed W blocks (VPG_NO_W2)
     bool no_wg = false;    // disable gather W blocks (VPG_WG=0)
+    bool force_wg = false; // gather W blocks wherever they apply (VPG_WG=2, experiments)
     bool no_swz_addr = false; // 128-byte residue layouts without the address swizzle (VPG_NO_SWZ_ADDR)
     bool no_bulk = false;  // TMA bulk source reads off (VPG_BULK=0, pull exchanges)
     bool force_bulk = false; // TMA bulk source reads wherever they apply (VPG_BULK=1)
@@ -745,18 +746,19 @@ bool w2_vectorizable(const Problem &Pb, const TileGeom &g, int V) {
 // destination elements, stored as k 16-byte chunks (image CHW -> HWC: 3 x
 // 16 bytes per block).  Block starts keep 16-byte alignment when d[0] and
 // the tile's dim-0 extent are multiples of V.  Returns k, or 0.
-// W in gather blocks: V consecutive destination-innermost elements (V smem
-// rows, scalar loads) packed into one 16-byte store -- the destination-
-// innermost dim sigma[0] is a run-index dim (its own smem rows) whose tile
-// extent and full extent are multiples of V, so every block starts 16-byte
-// aligned.  Where the W phase would otherwise store one 1-, 2- or 4-byte
+// W in gather blocks: V consecutive destination-innermost elements (scalar
+// smem loads sstride apart) packed into one 16-byte store -- the
+// destination-innermost dim sigma[0] has a tile extent and a full extent
+// that are multiples of V, so every block starts 16-byte aligned.  Where the W phase would otherwise store one 1-, 2- or 4-byte
 // word per lane (misaligned source runs, residue rows).
 bool wg_vectorizable(const Problem &Pb, const TileGeom &g, int V) {
     if (V <= 1) return false;
     const int k1 = Pb.sigma[0];
     if (k1 == 0 || g.ext[k1] == 0 || g.ext[k1] % V || Pb.d[k1] % V) return false;
-    for (int i = 0; i < g.nsrc; ++i)
-        if (g.src_dims[i] == k1) return false;
+    // (sigma[0] may also be the partial last dim of the source run -- NCHW ->
+    // NHWC with 7x7 maps stages one contiguous 49 x 256 block: the V
+    // elements of a block are then 49 apart in smem; scalar loads take any
+    // stride)
     if (Pb.G >= 1 && (Pb.n / Pb.G) % V) return false;
     return true;
 }
@@ -1164,7 +1166,7 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
         vc.wg = true;
         TileParams tp;
         fill_tile_params(Pb, g, pitch, NT, vc, tp);
-        const double c = tile_cost(Pb, tp) * factor;
+        const double c = tile_cost(Pb, tp) * factor * (Pb.force_wg ? 1e-6 : 1.0);
         if (getenv("VPG_DEBUG_PLAN"))
             fprintf(stderr, "[plan] Ls %lld Ld %lld pitch %u vr %d rshift %d rres %d gather cost %.1f per-elem %.3f\n",
                     (long long)g.Ls, (long long)g.Ld, pitch, vc.vr, (int)vc.rshift, (int)vc.rres, c, c / (double)g.T);
@@ -1707,7 +1709,10 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
     if (getenv("VPG_NO_RES")) P.no_res = true;
     if (getenv("VPG_NO_SW128")) P.no_sw128 = true;
     if (getenv("VPG_NO_W2")) P.no_w2 = true;
-    if (const char *e = getenv("VPG_WG")) P.no_wg = atoi(e) == 0;
+    if (const char *e = getenv("VPG_WG")) {
+        P.no_wg = atoi(e) == 0;
+        P.force_wg = atoi(e) == 2;
+    }
     if (const char *e = getenv("VPG_LIN")) P.lin_mode = *e ? atoi(e) : 0;
     if (getenv("VPG_NO_SWZ_ADDR")) P.no_swz_addr = true;
     // the chunk swizzle removes the W bank conflicts of shifted runs but costs
