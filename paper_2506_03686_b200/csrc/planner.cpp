@@ -728,13 +728,26 @@ bool r_vectorizable(const Problem &Pb, const TileGeom &g, int V) {
 // grouped by V, and every destination offset of a group start is a multiple
 // of V (16-byte stores; d[sigma[0]] % V == 0 makes all other destination
 // strides, the shard size included, multiples of V).
+// elements of the source run before its last (partial) dim, when that dim
+// is sigma[0] and they form whole 128-byte lines; 0 otherwise
+int64_t w2_in_run_rows(const Problem &Pb, const TileGeom &g) {
+    if (g.nsrc < 2 || g.src_dims[g.nsrc - 1] != Pb.sigma[0]) return 0;
+    const int64_t lrow = g.Ls / g.ext[Pb.sigma[0]];
+    return (lrow * Pb.E) % 128 == 0 ? lrow : 0;
+}
+
 bool w2_vectorizable(const Problem &Pb, const TileGeom &g, int V) {
     const int k1 = Pb.sigma[0];
     if (k1 == 0 || g.ext[k1] == 0 || g.ext[k1] % V || Pb.d[k1] % V) return false;
     // the V rows of a block are smem rows (sigma[0] a run-index dim, the
-    // first in destination order: stride = pitch), so they share a swizzle group
+    // first in destination order: stride = pitch), so they share a swizzle
+    // group.  sigma[0] may also be the partial last dim of the source run
+    // when the run part before it is a whole number of 128-byte lines: the
+    // contiguous run is then swizzled as rows of that length (a batched
+    // transpose whose source-innermost dim is one 128-byte line, u8
+    // attention K^T: tools/cand_scan.py)
     for (int i = 0; i < g.nsrc; ++i)
-        if (g.src_dims[i] == k1) return false;
+        if (g.src_dims[i] == k1 && (i + 1 != g.nsrc || !w2_in_run_rows(Pb, g))) return false;
     if (Pb.G >= 1 && (Pb.n / Pb.G) % V) return false;
     return true;
 }
@@ -949,7 +962,10 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
         while ((1 << lv) < V) ++lv;
         for (int ph = 0; ph < 2; ++ph) {
             tp.ph[ph].swz = vc.sw128 ? (vc.w2 ? 1u + lv : 1u) : (uint32_t)vc.swz;
-            tp.ph[ph].spitch = make_fastdiv(pitch);
+            // (V x V blocks over sigma[0] inside the source run: rows of the
+            // run part before it, w2_in_run_rows)
+            const int64_t lrow = vc.w2 ? w2_in_run_rows(Pb, g) : 0;
+            tp.ph[ph].spitch = make_fastdiv(lrow ? (uint32_t)lrow : pitch);
         }
     }
     if (tp.lin.on) {

@@ -1052,8 +1052,8 @@ __device__ __forceinline__ void shard_barrier_end(const ShardArgs &sa, uint32_t 
 // streams the source runs of the first S tiles; each iteration writes tile
 // k out of its buffer and refills that buffer with tile k+S.  Small
 // problems are thereby staged in one wave; large ones keep S-1 tiles of
-// loads in flight per CTA.  Without ASYNC (1- and 2-byte words) a single
-// buffer is filled by LDG+STS.
+// loads in flight per CTA (every word size: 1- and 2-byte words move
+// 16-byte cp.async vectors, their scalar phases load synchronously).
 template <typename W, bool ASYNC>
 __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restrict__ src, W *__restrict__ dst,
                                           const ShardArgs &sa, uint32_t cta, uint32_t ncta) {
