@@ -12,6 +12,8 @@
 #else
 #define VPG_UNROLL
 #endif
+#define VPG_PRAGMA(x) _Pragma(#x)
+#define VPG_UNROLL_N(n) VPG_PRAGMA(unroll n)
 
 namespace vpg {
 
@@ -622,7 +624,11 @@ __device__ __forceinline__ void tile_write_flat(const PhaseDesc &d, const Thread
     const uint32_t o0 = d.ngroups == 1 ? 0u : t.grp;
     const uint32_t n_o = d.n_outer > o0 ? (d.n_outer - o0 + d.ngroups - 1) / d.ngroups : 0u;
     const uint32_t total = n_o * d.n_in;
+#ifdef VPG_FLAT_UNROLL
+    VPG_UNROLL_N(VPG_FLAT_UNROLL)
+#else
     VPG_UNROLL
+#endif
     for (uint32_t b0 = 0; b0 < total; b0 += U) {
         W v[U];
         W *gp[U];
