@@ -652,14 +652,48 @@ def bench_sharded(args, torch, base, config, peak, peak_kind):
             "pipelined" if pipeline_chunks(sp) > 1 else "alltoall")
     if method in ("push", "pull"):
         method, xmode = "fused", method
+    fused_fallback = None
     if method == "fused":
-        ex = ShardExchange(wl.shape, wl.axes, wdt, device=dev, mode=xmode or "auto")
-        xmode = ex.mode
-        run = ex
-        if xmode == "pull":
-            # the peers read this rank's input from the exchange's shared buffer
-            ex.input.copy_(x)
-            x = ex.input
+        # The fused exchange maps peer memory (CUDA IPC) and orders the ranks
+        # with a device-side barrier.  Prove it on this box before timing it:
+        # two calls, the second timed on the host, and a sampled parity check
+        # of this rank's output shard.  If any rank fails (exception, a step
+        # that ran into the barrier's bounded wait, wrong data), every rank
+        # falls back to the NCCL all-to-all path and the JSON line says why.
+        err, x_dev = None, x
+        try:
+            ex = ShardExchange(wl.shape, wl.axes, wdt, device=dev, mode=xmode or "auto")
+            xmode = ex.mode
+            if xmode == "pull":
+                # the peers read this rank's input from the exchange's shared buffer
+                ex.input.copy_(x)
+                x = ex.input
+            ex(x)
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            probe = ex(x)
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            if os.environ.get("VPG_BENCH_FORCE_FUSED_FAIL"):
+                err = "forced (VPG_BENCH_FORCE_FUSED_FAIL)"
+            elif dt > 1.0:
+                err = f"one exchange step took {dt:.1f} s (device-side barrier wait expired?)"
+            elif not _sample_shard_parity(torch, host_in, probe, wl, sp, r, G, nsamp=1 << 14):
+                err = "sampled parity mismatch"
+            del probe
+        except Exception as e:  # reported in the JSON line; the NCCL path takes over
+            err = f"{type(e).__name__}: {e}"[:200]
+        flag = torch.tensor([0 if err is None else 1], device=red_dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+        if flag.item():
+            fused_fallback = err or "another rank failed"
+            print(f"rank {r}: fused exchange ({xmode}) not used: {fused_fallback}", file=sys.stderr, flush=True)
+            method, xmode, x, ex = ("pipelined" if pipeline_chunks(sp) > 1 else "alltoall"), None, x_dev, None
+        else:
+            run = ex
+    if method == "fused":
+        pass
     elif method == "pipelined":
         run = lambda xin: permute_sharded_pipelined(xin, wl.shape, wl.axes, local_permute=permute,  # noqa: E731
                                                     plan=sp)
@@ -761,6 +795,7 @@ def bench_sharded(args, torch, base, config, peak, peak_kind):
             "gpu_launches": (1 if method == "fused" or G == 1 else
                              pipeline_chunks(sp) + 1 if method == "pipelined" else 2) * args.steps,
             "shard_method": method if method != "fused" else f"fused ({xmode})",
+            "fused_exchange_fallback": fused_fallback,
             "roofline": {"bound": bound, "achieved": round(gbs, 2), "peak": round(roof_gbs, 1),
                          "peak_kind": f"min over HBM ({peak_kind} {peak} GB/s per GPU) and NVLink "
                                       f"({nvl_gbs:.1f} GB/s per direction per GPU: {nvl_kind}) time bounds",

@@ -276,6 +276,27 @@ def test_bench_two_ranks_code_path(cuda, method):
     assert "gloo" in line["dist_backend"]
 
 
+def test_bench_two_ranks_fused_fallback(cuda):
+    """A fused exchange that fails its pre-flight check on any rank (forced
+    here) makes every rank fall back to the NCCL-style all-to-all path, and
+    the JSON line records why."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
+           "--dist-backend", "gloo", "--config", "cfg1", "--steps", "2", "--warmup", "3"]
+    env = dict(os.environ, VPG_BENCH_FORCE_FUSED_FAIL="1")
+    res = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600, env=env)
+    assert res.returncode == 0, res.stderr[-2000:]
+    line = json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["parity_sampled"] is True and line["e2e"]["parity"] is True
+    assert line["shard_method"] in ("alltoall", "pipelined")
+    assert "forced" in line["fused_exchange_fallback"]
+
+
 @pytest.mark.parametrize("mode", ["push", "pull"])
 def test_fused_exchange_random_campaign(cuda, mode):
     """Random shapes (factors of 2, 3, 4, 6, 8, 12, 16), ranks 2-7, words of

@@ -53,10 +53,11 @@ def features(p):
 
 
 def shapes():
-    yield (17, 9, 13, 15, 11, 27), (5, 2, 0, 4, 1, 3), 4
-    yield (8, 2, 5, 158, 37, 143), (2, 1, 0, 5, 4, 3), 4
+    if "CAND_WORDS" not in os.environ:
+        yield (17, 9, 13, 15, 11, 27), (5, 2, 0, 4, 1, 3), 4
+        yield (8, 2, 5, 158, 37, 143), (2, 1, 0, 5, 4, 3), 4
     for _ in range(N):
-        E = int(rng.choice([4, 8]))
+        E = int(rng.choice([int(w) for w in os.environ.get("CAND_WORDS", "4,8").split(",")]))
         target = int(rng.choice([32, 64, 128, 256, 512])) << 20
         r = int(rng.integers(2, 8))
         n = target // E
