@@ -13,6 +13,10 @@
 #define VPG_UNROLL
 #endif
 #define VPG_PRAGMA(x) _Pragma(#x)
+// scalar W walk: shared-memory loads issued ahead of their stores, per batch
+#ifndef VPG_W_U
+#define VPG_W_U 4
+#endif
 #define VPG_UNROLL_N(n) VPG_PRAGMA(unroll n)
 
 namespace vpg {
@@ -186,6 +190,67 @@ __device__ __forceinline__ const W *sptr(const unsigned char *smem, uint32_t off
     return reinterpret_cast<const W *>(smem + off);
 }
 
+// Shared-memory load through an explicit 32-bit shared-window address (sb =
+// smem_u32(smem) + byte offset).  In large unrolled (predicated) scalar W
+// walks the compiler otherwise rebuilt the window address of the pointer in
+// front of every load (VIADD + LEA with the CTA-in-cluster id + IADD3 per
+// element); with the address in one register the per-element constants fold
+// into the LDS immediate.
+template <typename W>
+struct RegOf {
+    using T = W;
+};
+template <>
+struct RegOf<unsigned char> {
+    using T = uint32_t;
+};
+template <>
+struct RegOf<unsigned short> {
+    using T = uint32_t;
+};
+// (1- and 2-byte words travel in 32-bit registers between the load and the
+// store: as unsigned char / short values every element cost a PRMT merge)
+template <typename W>
+__device__ __forceinline__ typename RegOf<W>::T lds(uint32_t a) {
+    if constexpr (sizeof(W) == 1) {
+        uint32_t v;
+        asm volatile("ld.shared.u8 %0, [%1];\n" : "=r"(v) : "r"(a) : "memory");
+        return v;
+    } else if constexpr (sizeof(W) == 2) {
+        uint32_t v;
+        asm volatile("ld.shared.u16 %0, [%1];\n" : "=r"(v) : "r"(a) : "memory");
+        return v;
+    } else if constexpr (sizeof(W) == 4) {
+        uint32_t v;
+        asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(a) : "memory");
+        return (W)v;
+    } else if constexpr (sizeof(W) == 8) {
+        unsigned long long v;
+        asm volatile("ld.shared.u64 %0, [%1];\n" : "=l"(v) : "r"(a) : "memory");
+        return (W)v;
+    } else {
+        uint4 v;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "r"(a)
+                     : "memory");
+        return v;
+    }
+}
+template <typename W>
+__device__ __forceinline__ void st_reg(W *p, const typename RegOf<W>::T &v) {
+    if constexpr (sizeof(W) == 1) asm volatile("st.global.u8 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+    else if constexpr (sizeof(W) == 2) asm volatile("st.global.u16 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+    else st_out(p, v);
+}
+// smem_u32(smem) pinned in a register (the compiler otherwise recomputes the
+// window address -- cvta + the CTA-in-cluster id -- at its uses)
+__device__ __forceinline__ uint32_t smem_base_reg(const void *smem) {
+    uint32_t sb = smem_u32(smem);
+    asm volatile("mov.u32 %0, %0;\n" : "+r"(sb));
+    return sb;
+}
+
 __device__ __forceinline__ bool slot_ok(uint32_t mask, uint32_t c0, uint32_t c1, uint32_t c2, const Lim &lim) {
     return (!(mask & 1u) || c0 < lim.l0) && (!(mask & 2u) || c1 < lim.l1) && (!(mask & 4u) || c2 < lim.l2);
 }
@@ -238,7 +303,7 @@ __device__ __forceinline__ void tile_read_impl(const PhaseDesc &d, const ThreadP
     VPG_UNROLL
     for (uint32_t o = o0; o < d.n_outer; o += d.ngroups) {
         const OuterEntry e = outer_entry(d, smem, o);
-        const W *gp = gsrc + (t.g + e.g);
+        const W *gp = (gsrc + t.g) + e.g;
         uint32_t so = t.s + e.s;
         if (mask == 0) {
             uint32_t i = 0;
@@ -315,7 +380,7 @@ __device__ __forceinline__ void tile_read_shift(const PhaseDesc &d, const Thread
     VPG_UNROLL
     for (uint32_t o = o0; o < d.n_outer; o += d.ngroups) {
         const OuterEntry e = outer_entry(d, smem, o);
-        const W *gp = gsrc + (t.g + e.g);
+        const W *gp = (gsrc + t.g) + e.g;
         uint32_t so = t.s + e.s;
         uint32_t c0 = t.c0 + e.c0, c1 = t.c1 + e.c1, c2 = t.c2;
         VPG_UNROLL
@@ -395,7 +460,7 @@ __device__ __forceinline__ void tile_write_w2(const PhaseDesc &d, const ThreadPa
     VPG_UNROLL
     for (uint32_t o = o0; o < d.n_outer; o += d.ngroups) {
         const OuterEntry e = outer_entry(d, smem, o);
-        W *gp = gdst + (t.g + e.g);
+        W *gp = (gdst + t.g) + e.g;
         const uint32_t sb = t.s + e.s;
         uint32_t c0 = t.c0 + e.c0, c1 = t.c1 + e.c1, c2 = t.c2;
         VPG_UNROLL
@@ -441,7 +506,7 @@ __device__ __forceinline__ void tile_write_wk_k(const PhaseDesc &d, const Thread
     VPG_UNROLL
     for (uint32_t o = o0; o < d.n_outer; o += d.ngroups) {
         const OuterEntry e = outer_entry(d, smem, o);
-        W *gp = gdst + (t.g + e.g);
+        W *gp = (gdst + t.g) + e.g;
         const uint32_t sb = t.s + e.s;
         uint32_t c0 = t.c0 + e.c0, c1 = t.c1 + e.c1, c2 = t.c2;
         VPG_UNROLL
@@ -466,7 +531,7 @@ __device__ __forceinline__ void tile_write_wg(const PhaseDesc &d, const ThreadPa
     VPG_UNROLL
     for (uint32_t o = o0; o < d.n_outer; o += d.ngroups) {
         const OuterEntry e = outer_entry(d, smem, o);
-        W *gp = gdst + (t.g + e.g);
+        W *gp = (gdst + t.g) + e.g;
         const uint32_t sb = t.s + e.s;
         uint32_t c0 = t.c0 + e.c0, c1 = t.c1 + e.c1, c2 = t.c2;
         VPG_UNROLL
@@ -518,17 +583,18 @@ template <typename W, bool VEC>
 __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
                                                 W *__restrict__ gdst, uint32_t bb, uint32_t mask,
                                                 const Lim lim, uint32_t hb, uint32_t hmask) {
-    constexpr int U = VEC ? 2 : 4;
+    constexpr int U = VEC ? 2 : VPG_W_U;
     constexpr int V = VEC ? 16 / (int)sizeof(W) : 1;
     const uint32_t n_in = d.n_in;
     const int64_t g_in = d.g_in;
     const uint32_t s_in = d.s_in;
     const int64_t vs = d.vstride;
+    const uint32_t sb = smem_base_reg(smem);
     const uint32_t o0 = d.ngroups == 1 ? 0u : t.grp;   // constant in JIT builds
     VPG_UNROLL
     for (uint32_t o = o0; o < d.n_outer; o += d.ngroups) {
         const OuterEntry e = outer_entry(d, smem, o);
-        W *gp = gdst + (t.g + e.g);
+        W *gp = (gdst + t.g) + e.g;
         uint32_t s = t.s + e.s;
         uint32_t hh = hb + t.h + e.h;          // shifted-run mode (hmask == 0 otherwise)
         const uint32_t h_in = d.h_in;
@@ -543,12 +609,12 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
 #pragma unroll
                     for (int u = 0; u < U; ++u) store_vec<W>(gp + u * g_in, v[u], vs);
                 } else {
-                    W v[U];
+                    typename RegOf<W>::T v[U];
 #pragma unroll
                     for (int u = 0; u < U; ++u)
-                        v[u] = *sptr<W>(smem, soff<W>(d, bb, s + u * s_in + ((hh + u * h_in) & hmask)));
+                        v[u] = lds<W>(sb + soff<W>(d, bb, s + u * s_in + ((hh + u * h_in) & hmask)));
 #pragma unroll
-                    for (int u = 0; u < U; ++u) st_out(gp + u * g_in, v[u]);
+                    for (int u = 0; u < U; ++u) st_reg(gp + u * g_in, v[u]);
                 }
                 gp += U * g_in;
                 s += U * s_in;
@@ -558,7 +624,7 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
                 if constexpr (VEC) {
                     store_vec<W>(gp, *sptr<uint4>(smem, soff<W>(d, bb, s)), vs);
                 } else {
-                    *gp = *sptr<W>(smem, soff<W>(d, bb, s + (hh & hmask)));
+                    st_reg(gp, lds<W>(sb + soff<W>(d, bb, s + (hh & hmask))));
                 }
                 gp += g_in;
                 s += s_in;
@@ -573,16 +639,16 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
                 // each wait out a shared-memory latency
                 VPG_UNROLL
                 for (; i + U <= n_in; i += U) {
-                    W v[U];
+                    typename RegOf<W>::T v[U];
                     bool ok[U];
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         ok[u] = slot_ok(mask, c0 + u * d.c_in[0], c1 + u * d.c_in[1], c2 + u * d.c_in[2], lim);
-                        if (ok[u]) v[u] = *sptr<W>(smem, soff<W>(d, bb, s + u * s_in + ((hh + u * h_in) & hmask)));
+                        if (ok[u]) v[u] = lds<W>(sb + soff<W>(d, bb, s + u * s_in + ((hh + u * h_in) & hmask)));
                     }
 #pragma unroll
                     for (int u = 0; u < U; ++u)
-                        if (ok[u]) st_out(gp + u * g_in, v[u]);
+                        if (ok[u]) st_reg(gp + u * g_in, v[u]);
                     gp += U * g_in;
                     s += U * s_in;
                     hh += U * h_in;
@@ -597,7 +663,7 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
                     if constexpr (VEC) {
                         store_vec<W>(gp, *sptr<uint4>(smem, soff<W>(d, bb, s)), vs);
                     } else {
-                        *gp = *sptr<W>(smem, soff<W>(d, bb, s + (hh & hmask)));
+                        st_reg(gp, lds<W>(sb + soff<W>(d, bb, s + (hh & hmask))));
                     }
                 }
                 gp += g_in;
@@ -621,6 +687,7 @@ __device__ __forceinline__ void tile_write_flat(const PhaseDesc &d, const Thread
                                                 W *__restrict__ gdst, uint32_t bb, uint32_t mask, const Lim lim,
                                                 uint32_t hb, uint32_t hmask) {
     constexpr int U = 8;
+    const uint32_t sb = smem_base_reg(smem);
     const uint32_t o0 = d.ngroups == 1 ? 0u : t.grp;
     const uint32_t n_o = d.n_outer > o0 ? (d.n_outer - o0 + d.ngroups - 1) / d.ngroups : 0u;
     const uint32_t total = n_o * d.n_in;
@@ -630,7 +697,7 @@ __device__ __forceinline__ void tile_write_flat(const PhaseDesc &d, const Thread
     VPG_UNROLL
 #endif
     for (uint32_t b0 = 0; b0 < total; b0 += U) {
-        W v[U];
+        typename RegOf<W>::T v[U];
         W *gp[U];
         bool ok[U];
 #pragma unroll
@@ -639,17 +706,17 @@ __device__ __forceinline__ void tile_write_flat(const PhaseDesc &d, const Thread
             ok[u] = idx < total;
             const uint32_t oi = idx / d.n_in, i = idx - oi * d.n_in;
             const OuterEntry e = outer_entry(d, smem, o0 + oi * d.ngroups);
-            gp[u] = gdst + (t.g + e.g) + (int64_t)i * d.g_in;
+            gp[u] = (gdst + t.g) + e.g + (int64_t)i * d.g_in;
             const uint32_t s = t.s + e.s + i * d.s_in;
             const uint32_t hh = hb + t.h + e.h + i * d.h_in;
             if (mask)
                 ok[u] = ok[u] && slot_ok(mask, t.c0 + e.c0 + i * d.c_in[0], t.c1 + e.c1 + i * d.c_in[1],
                                          t.c2 + i * d.c_in[2], lim);
-            if (ok[u]) v[u] = *sptr<W>(smem, soff<W>(d, bb, s + (hh & hmask)));
+            if (ok[u]) v[u] = lds<W>(sb + soff<W>(d, bb, s + (hh & hmask)));
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
-            if (ok[u]) st_out(gp[u], v[u]);
+            if (ok[u]) st_reg(gp[u], v[u]);
     }
 }
 #endif
@@ -660,8 +727,13 @@ __device__ __forceinline__ void tile_write(const PhaseDesc &d, const ThreadPart 
                                            const Lim lim, uint32_t hb, uint32_t hmask) {
     if (!t.active) return;
 #if defined(VPG_JIT) && !defined(VPG_NO_FLAT)
+    // The check mask of a tile is one of two plan constants (full or ragged
+    // tile): the scalar walks are instantiated once per constant (their
+    // shared-memory loads are volatile asm, which the compiler does not
+    // unswitch by itself; with a run-time mask every element evaluated it).
     if (d.vec <= 1 && !d.w2 && d.n_in < 4) {
-        tile_write_flat<W>(d, t, smem, gdst, bb, mask, lim, hb, hmask);
+        if (mask == d.mask_full) tile_write_flat<W>(d, t, smem, gdst, bb, d.mask_full, lim, hb, hmask);
+        else tile_write_flat<W>(d, t, smem, gdst, bb, d.mask_ragged, lim, hb, hmask);
         return;
     }
 #endif
@@ -683,7 +755,12 @@ __device__ __forceinline__ void tile_write(const PhaseDesc &d, const ThreadPart 
             return;
         }
     }
+#ifdef VPG_JIT
+    if (mask == d.mask_full) tile_write_impl<W, false>(d, t, smem, gdst, bb, d.mask_full, lim, hb, hmask);
+    else tile_write_impl<W, false>(d, t, smem, gdst, bb, d.mask_ragged, lim, hb, hmask);
+#else
     tile_write_impl<W, false>(d, t, smem, gdst, bb, mask, lim, hb, hmask);
+#endif
 }
 
 // W phase, lin mode (LinDesc in plan_params.h): the per-plan table of u16
@@ -1063,13 +1140,24 @@ __device__ __forceinline__ void shard_barrier_end(const ShardArgs &sa, uint32_t 
 template <typename W, bool ASYNC>
 __device__ __forceinline__ void tile_body(const TileParams &p, const W *__restrict__ src, W *__restrict__ dst,
                                           const ShardArgs &sa, uint32_t cta, uint32_t ncta) {
+    // the planner's layout is relative to a 128-byte aligned base: staged
+    // rows then sit at the same offset modulo 128 bytes as their source lines
+    // (see PhaseDesc::swz).  Specialised kernels with a scalar W walk declare
+    // the alignment (VPG_SMEM_DECL, jit.cpp) instead of computing it: the
+    // run-time round-up of the base was rematerialised in front of every
+    // predicated shared-memory load of large unrolled walks (7 of ~23
+    // instructions per element in the slow 1-byte plans, tools/sass_per_store.sh).
+    // Vector W walks keep the computed base: with the declared one the V x V
+    // blocks spilled more at their 80-register cap (profiles/w_lds_ab_r2.txt).
+#if VPG_SMEM_DECL
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    unsigned char *const smem = smem_raw;
+#else
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    unsigned char *const smem = smem_raw + ((128u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 127u)) & 127u);
+#endif
     __shared__ int64_t s_base[kRing][2];
     __shared__ uint32_t s_valid[kRing][2];
-    // the planner's layout is relative to a 128-byte aligned base (it
-    // allocates 128 bytes of slack): staged rows then sit at the same offset
-    // modulo 128 bytes as their source lines (see PhaseDesc::swz)
-    unsigned char *const smem = smem_raw + ((128u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 127u)) & 127u);
     const uint32_t tid = threadIdx.x, NT = blockDim.x;
     // CTA `cta` of the `ncta` CTAs running this plan (blockIdx.x / gridDim.x,
     // except in the cooperative multi-rank emulation of an exchange)
