@@ -1730,7 +1730,10 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         P.force_wg = atoi(e) == 2;
     }
     if (const char *e = getenv("VPG_LIN")) P.lin_mode = *e ? atoi(e) : 0;
-    if (getenv("VPG_NO_SWZ_ADDR")) P.no_swz_addr = true;
+    // (a blanket "no address swizzle unless 4-byte words" rule measured neutral
+    // over 200 random shapes: +10..18% on some plans, -13..15% on others,
+    // profiles/swz_addr_ab_r2.txt -- the bank model keeps the choice)
+    if (const char *e = getenv("VPG_NO_SWZ_ADDR")) P.no_swz_addr = !*e || atoi(e) != 0;
     // the chunk swizzle removes the W bank conflicts of shifted runs but costs
     // a divide and a few integer ops per element: measured 28.4 vs 20.5 us on
     // cfg3, 216 vs 247 us on an odd 8-byte 2-D transpose -- opt-in
