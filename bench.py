@@ -627,12 +627,27 @@ def bench_sharded(args, torch, base, config, peak, peak_kind):
     dev_index = local_rank if backend == "nccl" else local_rank % torch.cuda.device_count()
     torch.cuda.set_device(dev_index)
     dev = torch.device("cuda", dev_index)
-    if backend == "nccl":
-        dist.init_process_group("nccl", device_id=dev)
-    else:
-        dist.init_process_group("gloo")
-    G, r = dist.get_world_size(), dist.get_rank()
-    red_dev = dev if backend == "nccl" else torch.device("cpu")
+    # stdout carries the one JSON line: while the communicator comes up
+    # (NCCL prints its version banner to stdout under NCCL_DEBUG=VERSION,
+    # which the GPU boxes set) file descriptor 1 points at stderr
+    sys.stdout.flush()
+    saved_stdout = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+        G, r = dist.get_world_size(), dist.get_rank()
+        red_dev = dev if backend == "nccl" else torch.device("cpu")
+        warm = torch.zeros(1, device=red_dev)
+        dist.all_reduce(warm)              # first collective: lazy communicator setup
+        if backend == "nccl":
+            torch.cuda.synchronize()
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved_stdout, 1)
+        os.close(saved_stdout)
     a2a = None
     if backend == "nccl" and G > 1:
         a2a = measure_alltoall(torch, dist, dev, G)
