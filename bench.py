@@ -683,16 +683,17 @@ def bench_sharded(args, torch, base, config, peak, peak_kind):
                 # the peers read this rank's input from the exchange's shared buffer
                 ex.input.copy_(x)
                 x = ex.input
+            # (no collective inside this block: a rank that failed earlier
+            # must not leave its peers waiting in one)
             ex(x)
             torch.cuda.synchronize()
-            dist.barrier()
             t0 = time.perf_counter()
             probe = ex(x)
             torch.cuda.synchronize()
             dt = time.perf_counter() - t0
             if os.environ.get("VPG_BENCH_FORCE_FUSED_FAIL"):
                 err = "forced (VPG_BENCH_FORCE_FUSED_FAIL)"
-            elif dt > 1.0:
+            elif dt > 2.0:
                 err = f"one exchange step took {dt:.1f} s (device-side barrier wait expired?)"
             elif not _sample_shard_parity(torch, host_in, probe, wl, sp, r, G, nsamp=1 << 14):
                 err = "sampled parity mismatch"
