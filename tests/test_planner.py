@@ -169,6 +169,23 @@ def test_specialised_kernels_compile_with_nvrtc(cfg):
     vp.jit_compile(_plan(w.shape, w.axes, w.elem_bytes))
 
 
+def test_scalar_w_kernels_declare_smem_alignment():
+    """Specialised kernels with a scalar W walk declare the 128-byte
+    alignment of the dynamic smem (VPG_SMEM_DECL, jit.cpp); V x V plans keep
+    the computed base.  Both variants compile."""
+    from paper_2506_03686_b200.workloads import CONFIGS
+
+    w3, w1 = CONFIGS["cfg3"], CONFIGS["cfg1"]
+    p3 = _plan(w3.shape, w3.axes, w3.elem_bytes)
+    p1 = _plan(w1.shape, w1.axes, w1.elem_bytes)
+    assert "W 1" in p3.text and "#define VPG_SMEM_DECL 1" in vp.emit_source(p3)
+    assert "VxV" in p1.text and "#define VPG_SMEM_DECL" not in vp.emit_source(p1)
+    # 1-byte misaligned transpose: scalar W walk through 32-bit registers
+    p = _plan((203, 517), (1, 0), 1, force="tile")
+    assert "#define VPG_SMEM_DECL 1" in vp.emit_source(p)
+    vp.jit_compile(p)
+
+
 def test_specialised_random_plans_compile():
     rng = np.random.default_rng(9)
     for elem in (1, 2, 4, 8, 16):
