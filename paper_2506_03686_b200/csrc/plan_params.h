@@ -141,8 +141,11 @@ struct PhaseDesc {
     uint32_t w2;                   // 1: V x V blocks; 2..8: k x V interleave blocks; kW2Gather: gather blocks
     uint32_t vrow;
 };
-// PhaseDesc::w2 value of the gather W mode: V destination-innermost elements
-// (V smem rows vrow apart, scalar loads) packed into one 16-byte store
+// PhaseDesc::w2 values of the gather W mode: g destination-innermost elements
+// (g smem rows vrow apart, scalar loads) packed into one store of g words.
+// kW2Gather: g = V (16-byte stores); kW2Gather + g, g = 2, 4, 8 < V: narrower
+// blocks (4- and 8-byte stores) for 1- and 2-byte words whose
+// destination-innermost extent is a multiple of g but not of V.
 constexpr uint32_t kW2Gather = 64;
 
 // W phase as destination-linear 16-byte chunks ("lin" mode), for tiles whose

@@ -355,7 +355,7 @@ struct VecChoice {
     bool res16 = false;    // residue modulus of one 16-byte chunk (TMA bulk reads of misaligned runs)
     bool lin = false;      // W as destination-linear 16-byte chunks (LinDesc)
     int wk = 0;            // W in k x V interleave blocks (k = extent of the destination-innermost dim)
-    bool wg = false;       // W in gather blocks: V destination-innermost elements -> one 16-byte store
+    int wg = 0;            // W in gather blocks: wg destination-innermost elements -> one store (V: 16 bytes; 2, 4, 8 < V: narrow blocks)
 };
 
 // smem strides of the tile dims for a given pitch (source run dense, run
@@ -938,7 +938,7 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
                                      : phase_dims(Pb, g, sstr, slot_of_dim, false, vc.vr),
                            NT, tp.ph[0], tp.lim_split[0]);
     double u1 = make_phase(phase_dims(Pb, g, sstr, slot_of_dim, true, vc.vw, hmask, vc.w2, vc.wk,
-                                      vc.wg ? V : 0), NT, tp.ph[1], tp.lim_split[1]);
+                                      vc.wg), NT, tp.ph[1], tp.lim_split[1]);
     if (vc.w2) {
         tp.ph[1].w2 = 1;
         tp.ph[1].vrow = (uint32_t)sstr[Pb.sigma[0]];    // == pitch (w2_vectorizable)
@@ -946,7 +946,7 @@ double fill_tile_params(const Problem &Pb, const TileGeom &g, uint32_t pitch, in
         tp.ph[1].w2 = (uint32_t)vc.wk;                  // >= 2: k x V interleave blocks
         tp.ph[1].vrow = (uint32_t)sstr[Pb.sigma[0]];    // smem stride of the innermost destination dim
     } else if (vc.wg) {
-        tp.ph[1].w2 = kW2Gather;
+        tp.ph[1].w2 = kW2Gather + (vc.wg == V ? 0u : (uint32_t)vc.wg);
         tp.ph[1].vrow = (uint32_t)sstr[Pb.sigma[0]];
     }
     if (vc.lin) fill_lin(Pb, g, sstr, slot_of_dim, NT, tp);
@@ -1137,8 +1137,9 @@ double tile_cost(const Problem &Pb, const TileParams &tp) {
         const double kr = getenv("VPG_R_OP_COST") ? atof(getenv("VPG_R_OP_COST")) : 8.0;
         if (ph == 0) cost += ops * (kr + avg_w + (checked ? 2.0 : 0.0));
         else if (d.w2 == 1) cost += ops * (V * avg_w + V + 1.0 + (checked ? 2.0 : 0.0));    // V LDS.128 + V STG.128
-        else if (d.w2 == kW2Gather) {
-            const int Vg = 16 / Pb.E;          // V scalar LDS + one STG.128 (+ packing)
+        else if (d.w2 >= kW2Gather) {
+            // Vg scalar LDS + one store (+ packing)
+            const int Vg = d.w2 == kW2Gather ? 16 / Pb.E : (int)(d.w2 - kW2Gather);
             cost += ops * (Vg * avg_w + 1.0 + 0.25 * Vg + (checked ? 2.0 : 0.0));
         }
         else if (d.w2 >= 2) cost += ops * (d.w2 * avg_w + d.w2 + 1.0 + (checked ? 2.0 : 0.0)); // k LDS.128 + k STG.128
@@ -1178,8 +1179,20 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
     // the same layout with the W phase in gather blocks (16-byte stores)
     auto wg_try = [&](VecChoice vc, uint32_t pitch, double factor) {
         if (vc.vw > 1 || vc.w2 || vc.wk || vc.bulk || vc.lin || (vc.rshift && !vc.rres) || Pb.no_wg) return;
-        if (!wg_vectorizable(Pb, g, V)) return;
-        vc.wg = true;
+        // the widest block the destination-innermost extent allows: V (16-byte
+        // stores), or for 1- and 2-byte words V/2, V/4 ... >= 2 (8- and 4-byte
+        // stores; VPG_WG_NARROW=0 keeps the full width only)
+        static const bool narrow = !(getenv("VPG_WG_NARROW") && atoi(getenv("VPG_WG_NARROW")) == 0);
+        int wgw = 0;
+        for (int w = V; w >= 2; w /= 2) {
+            if (w < V && (Pb.E > 2 || !narrow)) break;
+            if (wg_vectorizable(Pb, g, w)) {
+                wgw = w;
+                break;
+            }
+        }
+        if (!wgw) return;
+        vc.wg = wgw;
         TileParams tp;
         fill_tile_params(Pb, g, pitch, NT, vc, tp);
         const double c = tile_cost(Pb, tp) * factor * (Pb.force_wg ? 1e-6 : 1.0);
@@ -1581,8 +1594,11 @@ static void describe(vpg_plan *p) {
                                        : t.ph[0].rshift ? " (aligned supersets of misaligned runs)" : ""),
             t.ph[1].vec, t.ph[1].w2 == 1 ? " (VxV register-transposed blocks, 16-byte stores)"
                          : t.ph[1].w2 == kW2Gather ? " (gather blocks: 16-byte stores of destination-innermost runs)"
+                         : t.ph[1].w2 == kW2Gather + 2 ? " (gather blocks of 2: narrow stores of destination-innermost runs)"
+                         : t.ph[1].w2 == kW2Gather + 4 ? " (gather blocks of 4: narrow stores of destination-innermost runs)"
+                         : t.ph[1].w2 == kW2Gather + 8 ? " (gather blocks of 8: narrow stores of destination-innermost runs)"
                          : t.ph[1].w2 >= 2 ? " (k x V interleave blocks, 16-byte stores)" : "");
-        if (t.ph[1].w2 >= 2 && t.ph[1].w2 != kW2Gather)
+        if (t.ph[1].w2 >= 2 && t.ph[1].w2 < kW2Gather)
             put("W interleave: k = %u destination-innermost elements per dim-0 element\n", t.ph[1].w2);
         if (t.lin.on)
             put("W lin: destination-linear %u-byte chunks, one store each (runs of %u elements, %u chunk slots x %u "
@@ -1986,7 +2002,7 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         vs.bulk = false;
         vs.w2 = false;      // 16-byte destination stores need an aligned dst too
         vs.wk = 0;
-        vs.wg = false;
+        vs.wg = 0;
         if (P.sigma[0] == 0) vs.vw = 1;   // (its vector W would be 16-byte stores)
         vs.lin = false;
         fill_tile_params(P, g, pitch, threads, vs, p->tile_unaligned);

@@ -520,13 +520,15 @@ __device__ __forceinline__ void tile_write_wk_k(const PhaseDesc &d, const Thread
     }
 }
 
-// W in gather blocks (PhaseDesc::w2 == kW2Gather): V destination-innermost
-// elements from V smem rows vrow apart (scalar loads, any alignment: residue
-// rows included) packed into one 16-byte store.
-template <typename W>
-__device__ __forceinline__ void tile_write_wg(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
-                                              W *__restrict__ gdst, uint32_t bb, uint32_t mask, const Lim lim) {
-    constexpr int V = 16 / (int)sizeof(W);
+// W in gather blocks (PhaseDesc::w2 >= kW2Gather): G destination-innermost
+// elements from G smem rows vrow apart (scalar loads, any alignment: residue
+// rows included) packed into one store of G words (16 bytes for G = V; 4 or
+// 8 bytes for the narrow blocks of 1- and 2-byte words).
+template <typename W, int G>
+__device__ __forceinline__ void tile_write_wg_g(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
+                                                W *__restrict__ gdst, uint32_t bb, uint32_t mask, const Lim lim) {
+    constexpr int B = G * (int)sizeof(W);          // bytes per store: 4, 8 or 16
+    using S = typename WordOf<B>::T;
     const uint32_t o0 = d.ngroups == 1 ? 0u : t.grp;
     VPG_UNROLL
     for (uint32_t o = o0; o < d.n_outer; o += d.ngroups) {
@@ -537,15 +539,32 @@ __device__ __forceinline__ void tile_write_wg(const PhaseDesc &d, const ThreadPa
         VPG_UNROLL
         for (uint32_t i = 0; i < d.n_in; ++i) {
             if (mask == 0 || slot_ok(mask, c0, c1, c2, lim)) {
-                alignas(16) W v[V];
+                alignas(16) W v[G];
                 const uint32_t s0 = sb + i * d.s_in;
 #pragma unroll
-                for (int j = 0; j < V; ++j) v[j] = *sptr<W>(smem, soff<W>(d, bb, s0 + (uint32_t)j * d.vrow));
-                st_out(reinterpret_cast<uint4 *>(gp + (int64_t)i * d.g_in), *reinterpret_cast<const uint4 *>(v));
+                for (int j = 0; j < G; ++j) v[j] = *sptr<W>(smem, soff<W>(d, bb, s0 + (uint32_t)j * d.vrow));
+                st_out(reinterpret_cast<S *>(gp + (int64_t)i * d.g_in), *reinterpret_cast<const S *>(v));
             }
             c0 += d.c_in[0];
             c1 += d.c_in[1];
             c2 += d.c_in[2];
+        }
+    }
+}
+
+template <typename W>
+__device__ __forceinline__ void tile_write_wg(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
+                                              W *__restrict__ gdst, uint32_t bb, uint32_t mask, const Lim lim) {
+    constexpr int V = 16 / (int)sizeof(W);
+    if (d.w2 == kW2Gather) {
+        tile_write_wg_g<W, V>(d, t, smem, gdst, bb, mask, lim);
+        return;
+    }
+    if constexpr (V >= 8) {
+        if (d.w2 == kW2Gather + 2) tile_write_wg_g<W, 2>(d, t, smem, gdst, bb, mask, lim);
+        else if (d.w2 == kW2Gather + 4) tile_write_wg_g<W, 4>(d, t, smem, gdst, bb, mask, lim);
+        if constexpr (V >= 16) {
+            if (d.w2 == kW2Gather + 8) tile_write_wg_g<W, 8>(d, t, smem, gdst, bb, mask, lim);
         }
     }
 }
@@ -742,7 +761,7 @@ __device__ __forceinline__ void tile_write(const PhaseDesc &d, const ThreadPart 
             tile_write_w2<W>(d, t, smem, gdst, bb, mask, lim);
             return;
         }
-        if (d.w2 == kW2Gather) {
+        if (d.w2 >= kW2Gather) {
             tile_write_wg<W>(d, t, smem, gdst, bb, mask, lim);
             return;
         }

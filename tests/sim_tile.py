@@ -323,10 +323,11 @@ def simulate(program, src_words: np.ndarray, threads: int | None = None, shard_o
                                     smem[spx + j] = src_words[gabs + j]
                                     smem_valid[spx + j] = True
                         else:
-                            if d.w2 == 64:
-                                # gather block: V destination-innermost elements from V smem
-                                # rows vrow apart -> one 16-byte store
-                                Vg = 16 // E
+                            if d.w2 >= 64:
+                                # gather block: G destination-innermost elements from G smem
+                                # rows vrow apart -> one store of G words (w2 == 64: G = V,
+                                # 16 bytes; narrow blocks: G = w2 - 64 = 2, 4, 8)
+                                Vg = 16 // E if d.w2 == 64 else d.w2 - 64
                                 gabs = db + gp
                                 if (gabs % Vg).any():
                                     raise SimError("W gather block store misaligned")

@@ -526,6 +526,10 @@ def test_short_rows_vector_stores(cuda, shape, axes, elem):
     ((80, 17, 59), (1, 2, 0), 1),
     ((16, 18, 38), (2, 1, 0), 4),
     ((10, 10, 47, 17), (0, 3, 2, 1), 8),
+    ((20, 516, 999), (0, 2, 1), 1),           # narrow blocks: 4 u8 -> one 4-byte store
+    ((26, 26, 333), (1, 2, 0), 2),            # 2 u16 -> one 4-byte store
+    ((6, 44, 10, 67), (0, 3, 2, 1), 1),
+    ((3, 36, 2111), (0, 2, 1), 2),            # 4 u16 -> one 8-byte store
 ])
 def test_gather_blocks(cuda, shape, axes, elem):
     """W in gather blocks: V destination-innermost elements from V smem rows

@@ -303,3 +303,37 @@ def test_sim_golden_cases_with_swizzled_layouts():
         assert sha256(simulate(prog, golden_pattern(c["n"], c["elem"]))) == c["sha256"], c["name"]
         ran += 1
     assert ran >= 10
+
+
+def test_sim_narrow_gather_blocks():
+    """W in narrow gather blocks (1- and 2-byte words whose
+    destination-innermost extent is a multiple of 2, 4 or 8 but not of V):
+    g scalar smem loads packed into one 4- or 8-byte store; bit-exact replay
+    with misaligned source runs (residue rows) and ragged tiles."""
+    vp.program_cache_clear()
+    rng = np.random.default_rng(77)
+    seen = {}
+    shapes = [((20, 516, 999), (0, 2, 1)), ((3, 36, 211), (0, 2, 1)), ((5, 12, 203), (2, 1, 0)),
+              ((6, 44, 10, 67), (0, 3, 2, 1)), ((4, 18, 301), (0, 2, 1)), ((2, 250, 333), (0, 2, 1))]
+    for _ in range(300):
+        r = int(rng.integers(2, 5))
+        dims = [int(rng.choice([2, 3, 4, 6, 10, 12, 20, 28, 36, 44, 52, 100, 204])) for _ in range(r - 1)]
+        dims.append(int(rng.choice([33, 67, 99, 131, 203, 301])))
+        shapes.append((tuple(dims), tuple(int(a) for a in rng.permutation(r))))
+    for shape, axes in shapes:
+        if np.prod(shape) > 400000:
+            continue
+        for E in (1, 2):
+            prog = vp.build_program(vp.TensorLayout.from_shape(shape, E), vp.from_numpy_convention(axes), force="tile")
+            w2 = tile_params(prog).ph[1].w2
+            if w2 <= 64:
+                continue
+            assert "gather blocks of" in prog.text
+            n = prog.num_elements
+            words = rng.integers(0, 256 ** E, size=n, dtype=np.uint64).astype({1: np.uint8, 2: np.uint16}[E])
+            dims, sigma = oracle.from_numpy_axes(shape, axes)
+            assert np.array_equal(simulate(prog, words), oracle.naive_permute_c(words, dims, sigma)), (shape, axes, E)
+            seen[(E, w2 - 64)] = seen.get((E, w2 - 64), 0) + 1
+        if sum(seen.values()) >= 24 and len(seen) >= 3:
+            break
+    assert len(seen) >= 3 and sum(seen.values()) >= 10, seen
