@@ -1185,7 +1185,8 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
         static const bool narrow = !(getenv("VPG_WG_NARROW") && atoi(getenv("VPG_WG_NARROW")) == 0);
         int wgw = 0;
         for (int w = V; w >= 2; w /= 2) {
-            if (w < V && (Pb.E > 2 || !narrow)) break;
+            static const int narrow_maxE = getenv("VPG_WG_NARROW_E") ? atoi(getenv("VPG_WG_NARROW_E")) : 2;
+            if (w < V && (Pb.E > narrow_maxE || !narrow)) break;
             if (wg_vectorizable(Pb, g, w)) {
                 wgw = w;
                 break;

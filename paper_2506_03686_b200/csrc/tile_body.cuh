@@ -560,12 +560,14 @@ __device__ __forceinline__ void tile_write_wg(const PhaseDesc &d, const ThreadPa
         tile_write_wg_g<W, V>(d, t, smem, gdst, bb, mask, lim);
         return;
     }
-    if constexpr (V >= 8) {
+    if constexpr (V >= 4) {
         if (d.w2 == kW2Gather + 2) tile_write_wg_g<W, 2>(d, t, smem, gdst, bb, mask, lim);
-        else if (d.w2 == kW2Gather + 4) tile_write_wg_g<W, 4>(d, t, smem, gdst, bb, mask, lim);
-        if constexpr (V >= 16) {
-            if (d.w2 == kW2Gather + 8) tile_write_wg_g<W, 8>(d, t, smem, gdst, bb, mask, lim);
-        }
+    }
+    if constexpr (V >= 8) {
+        if (d.w2 == kW2Gather + 4) tile_write_wg_g<W, 4>(d, t, smem, gdst, bb, mask, lim);
+    }
+    if constexpr (V >= 16) {
+        if (d.w2 == kW2Gather + 8) tile_write_wg_g<W, 8>(d, t, smem, gdst, bb, mask, lim);
     }
 }
 
