@@ -1,4 +1,8 @@
-import os, sys, glob, subprocess, time
+"""Compile one plan's specialised kernel offline (NVRTC, no GPU):
+    python tools/jit_offline.py CACHE_DIR "SHAPE" "AXES" ELEM_BYTES [candidate]
+VPG_JIT_DUMP=<file> keeps the cubin (tools/sass_per_store.sh)."""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 cache = sys.argv[1]
 os.environ["VPG_JIT_CACHE"] = cache
 os.makedirs(cache, exist_ok=True)
