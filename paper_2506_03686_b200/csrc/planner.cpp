@@ -1148,6 +1148,21 @@ double tile_cost(const Problem &Pb, const TileParams &tp) {
     return cost;
 }
 
+// Every source run of the tile starts at a multiple of V elements: the
+// strides that move a run start (run-index dims, grid dims, the tile step
+// along a partial run dim, the shard bias) are multiples of V.
+bool src_starts_aligned(const Problem &Pb, const TileGeom &g, int V) {
+    bool in_run[kMaxRank] = {false};
+    for (int i = 0; i < g.nsrc; ++i) in_run[g.src_dims[i]] = true;
+    for (int k = 0; k < Pb.r; ++k) {
+        if (Pb.d[k] <= 1) continue;
+        if (!in_run[k] && Pb.in_stride[k] % V) return false;
+        if (in_run[k] && g.ext[k] < Pb.d[k] && (Pb.in_stride[k] * g.ext[k]) % V) return false;
+    }
+    if (Pb.G >= 1 && (Pb.n / Pb.G) % V) return false;
+    return true;
+}
+
 // Choose pitch and vectorisation that minimise the modelled tile cost.
 void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pitch_out, VecChoice &vc_out) {
     // 16-byte vectors for every word size below 16 bytes (1- and 2-byte
@@ -1254,7 +1269,7 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
                 wg_try(vc, (uint32_t)g.Ls, s128_factor);
             }
         }
-        if (op.rshift && !Pb.no_swz) {
+        if (op.rshift && !Pb.no_swz && op.vw == 1) {
             // swizzled rows: pitch a multiple of 8 chunks, row shift 0..3
             const int64_t base = (g.Ls + V - 1 + V - 1) / V * V;
             const int64_t p8 = (base + 8 * V - 1) / (8 * V) * (8 * V);
@@ -1348,6 +1363,7 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
             }
             return;
         }
+        if (op.rshift && op.vw > 1) continue;     // narrow W vectors: residue rows only
         const int step = (op.vr > 1 || op.vw > 1) ? V : 1;
         const int64_t base = op.rshift ? (g.Ls + V - 1 + V - 1) / V * V : g.Ls;
         static const int pad_max = getenv("VPG_PAD_MAX") ? atoi(getenv("VPG_PAD_MAX")) : 32;   // experiments
@@ -1386,6 +1402,41 @@ void choose_pitch_vec(const Problem &Pb, const TileGeom &g, int NT, uint32_t &pi
                     vc_out = vk;
                 }
             }
+        }
+    }
+    // Narrow W vectors on residue rows (1- and 2-byte words), where the choice
+    // so far is the plain scalar W walk: source runs misaligned to 16 bytes but
+    // aligned to 8 or 4 keep that alignment in shared memory (rows sit at
+    // their global offset modulo 16 bytes), so the W phase loads 8 or 4 bytes
+    // along source dim 0 at once and stores the elements one by one.  Gather
+    // blocks keep priority: they widen the stores, which measured better (u8
+    // (72,1917,1944) reversed 0.75 of copy_ with gather blocks, 0.54 with
+    // 4-byte W vectors).  VPG_WV_NARROW=0: off.
+    static const bool wv_narrow = !(getenv("VPG_WV_NARROW") && atoi(getenv("VPG_WV_NARROW")) == 0);
+    // Only where source dim 0 lies outside the tile's destination run: inside
+    // it, a lane's vector elements would take the places of its neighbours'
+    // and each store instruction would scatter over short segments (u8
+    // (7,26,11,7,23,23,72) -> (0,3,1,4,5,6,2), dim 0 second in the destination:
+    // 0.73 -> 0.33 of copy_).
+    if (best > 0 && Pb.E <= 2 && wv_narrow && Pb.sigma[0] != 0 && Pb.out_stride_of_dim[0] >= g.Ld &&
+        vc_out.rshift && vc_out.rres && vc_out.vw == 1 &&
+        !vc_out.wg && !vc_out.lin && !vc_out.w2 && !vc_out.wk && !vc_out.bulk && !vc_out.res16) {
+        for (int vn = V / 2; vn * Pb.E >= 4; vn /= 2) {
+            if (!w_vectorizable(Pb, g, vn) || !src_starts_aligned(Pb, g, vn)) continue;
+            VecChoice v2 = vc_out;
+            v2.vw = vn;
+            TileParams tp;
+            fill_tile_params(Pb, g, pitch_out, NT, v2, tp);
+            const double c = tile_cost(Pb, tp) * kResidueCostFactor *
+                             (res_modulus(Pb.E) * Pb.E >= 128 ? kSw128CostFactor : 1.0);
+            if (getenv("VPG_DEBUG_PLAN"))
+                fprintf(stderr, "[plan] Ls %lld Ld %lld pitch %u residue narrow W vector %d cost %.1f per-elem %.3f\n",
+                        (long long)g.Ls, (long long)g.Ld, pitch_out, vn, c, c / (double)g.T);
+            if (c < best - 1e-9) {
+                best = c;
+                vc_out = v2;
+            }
+            break;
         }
     }
 }
@@ -2005,6 +2056,7 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         vs.wk = 0;
         vs.wg = 0;
         if (P.sigma[0] == 0) vs.vw = 1;   // (its vector W would be 16-byte stores)
+        if (vs.vw > 1 && vs.vw * P.E < 16) vs.vw = 1;   // narrow W vectors need the residue rows
         vs.lin = false;
         fill_tile_params(P, g, pitch, threads, vs, p->tile_unaligned);
         // the tile count must fit the 32-bit tile index

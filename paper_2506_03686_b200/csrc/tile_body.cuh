@@ -600,12 +600,27 @@ __device__ __forceinline__ void store_vec(W *gp, const uint4 &v, int64_t vs) {
     for (int j = 0; j < V; ++j) st_out(gp + j * vs, w[j]);
 }
 
-template <typename W, bool VEC>
+// Narrow W vectors (VB = 4 or 8 bytes: 2-8 elements of a 1- or 2-byte word
+// along the source dim 0 in ONE shared-memory load, stored element by element
+// vs apart).  For residue rows whose source runs are misaligned to 16 bytes
+// but aligned to VB: a quarter to half of the scalar walk's LDS instructions.
+template <typename W, int VB>
+__device__ __forceinline__ void store_vec_n(W *gp, const typename WordOf<VB>::T &v, int64_t vs) {
+    constexpr int V = VB / (int)sizeof(W);
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        // (st.global.u8/u16 store the low bits of the 32-bit register)
+        st_reg(gp + j * vs, (uint32_t)(v >> (8 * (int)sizeof(W) * j)));
+    }
+}
+
+template <typename W, bool VEC, int VB = 16>
 __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const ThreadPart &t, const unsigned char *smem,
                                                 W *__restrict__ gdst, uint32_t bb, uint32_t mask,
                                                 const Lim lim, uint32_t hb, uint32_t hmask) {
-    constexpr int U = VEC ? 2 : VPG_W_U;
-    constexpr int V = VEC ? 16 / (int)sizeof(W) : 1;
+    constexpr int U = VEC ? (VB == 16 ? 2 : 4) : VPG_W_U;
+    constexpr int V = VEC ? VB / (int)sizeof(W) : 1;
+    using VT = typename WordOf<VB>::T;
     const uint32_t n_in = d.n_in;
     const int64_t g_in = d.g_in;
     const uint32_t s_in = d.s_in;
@@ -624,11 +639,14 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
             VPG_UNROLL
             for (; i + U <= n_in; i += U) {
                 if constexpr (VEC) {
-                    uint4 v[U];
+                    VT v[U];
 #pragma unroll
-                    for (int u = 0; u < U; ++u) v[u] = *sptr<uint4>(smem, soff<W>(d, bb, s + u * s_in));
+                    for (int u = 0; u < U; ++u) v[u] = *sptr<VT>(smem, soff<W>(d, bb, s + u * s_in));
 #pragma unroll
-                    for (int u = 0; u < U; ++u) store_vec<W>(gp + u * g_in, v[u], vs);
+                    for (int u = 0; u < U; ++u) {
+                        if constexpr (VB == 16) store_vec<W>(gp + u * g_in, v[u], vs);
+                        else store_vec_n<W, VB>(gp + u * g_in, v[u], vs);
+                    }
                 } else {
                     typename RegOf<W>::T v[U];
 #pragma unroll
@@ -643,7 +661,8 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
             }
             for (; i < n_in; ++i) {
                 if constexpr (VEC) {
-                    store_vec<W>(gp, *sptr<uint4>(smem, soff<W>(d, bb, s)), vs);
+                    if constexpr (VB == 16) store_vec<W>(gp, *sptr<uint4>(smem, soff<W>(d, bb, s)), vs);
+                    else store_vec_n<W, VB>(gp, *sptr<VT>(smem, soff<W>(d, bb, s)), vs);
                 } else {
                     st_reg(gp, lds<W>(sb + soff<W>(d, bb, s + (hh & hmask))));
                 }
@@ -682,7 +701,8 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
             for (; i < n_in; ++i) {
                 if (slot_ok(mask, c0, c1, c2, lim)) {
                     if constexpr (VEC) {
-                        store_vec<W>(gp, *sptr<uint4>(smem, soff<W>(d, bb, s)), vs);
+                        if constexpr (VB == 16) store_vec<W>(gp, *sptr<uint4>(smem, soff<W>(d, bb, s)), vs);
+                        else store_vec_n<W, VB>(gp, *sptr<VT>(smem, soff<W>(d, bb, s)), vs);
                     } else {
                         st_reg(gp, lds<W>(sb + soff<W>(d, bb, s + (hh & hmask))));
                     }
@@ -772,6 +792,17 @@ __device__ __forceinline__ void tile_write(const PhaseDesc &d, const ThreadPart 
             return;
         }
         if (d.vec > 1) {
+            if constexpr (sizeof(W) <= 2) {
+                // narrow vectors: 4 or 8 bytes of 1-2-byte words (residue rows)
+                if (d.vec * (uint32_t)sizeof(W) == 4) {
+                    tile_write_impl<W, true, 4>(d, t, smem, gdst, bb, mask, lim, 0, 0);
+                    return;
+                }
+                if (d.vec * (uint32_t)sizeof(W) == 8) {
+                    tile_write_impl<W, true, 8>(d, t, smem, gdst, bb, mask, lim, 0, 0);
+                    return;
+                }
+            }
             tile_write_impl<W, true>(d, t, smem, gdst, bb, mask, lim, 0, 0);
             return;
         }

@@ -555,3 +555,36 @@ def test_gather_blocks(cuda, shape, axes, elem):
         execute_device(prog, x, out=big[elem:])
         assert torch.equal(big[elem:].view(dt), want), (shape, jit, "misaligned dst")
     assert seen >= 1, prog.text
+
+
+@pytest.mark.parametrize("shape,axes,elem", [
+    ((3000, 1012), (1, 0), 1),                # 4-byte W vectors of u8
+    ((1290, 1004), (1, 0), 2),                # 4-byte W vectors of u16 (2 elements)
+    ((45, 36, 2100), (2, 1, 0), 1),
+    ((777, 67, 56), (2, 1, 0), 1),            # 8-byte W vectors of u8
+    ((301, 67, 100), (2, 0, 1), 2),           # 8-byte W vectors of u16
+])
+def test_narrow_w_vectors(cuda, shape, axes, elem):
+    """Narrow W vectors on residue rows: bit-exact, specialised and
+    ahead-of-time kernels, a source buffer misaligned to 16 bytes (scalar
+    variant) included."""
+    import torch
+
+    import paper_2506_03686_b200 as vp
+    from paper_2506_03686_b200.api import execute_device
+
+    dt = {1: torch.uint8, 2: torch.int16}[elem]
+    n = int(np.prod(shape))
+    seen = 0
+    for jit in (True, False):
+        prog = vp.build_program(vp.TensorLayout.from_shape(shape, elem), vp.from_numpy_convention(axes),
+                                force="tile", jit=jit)
+        vec = [ln for ln in prog.text.splitlines() if ln.startswith("vector elems")][0]
+        seen += any(f", W {v}" in vec for v in (2, 4, 8)) and "residue" in vec and 16 // elem != int(vec.rsplit("W ", 1)[1].split()[0])
+        x = torch.randint(0, 255, (n * elem,), dtype=torch.uint8, device="cuda")
+        want = x.view(dt).view(shape).permute(axes).reshape(-1)
+        assert torch.equal(execute_device(prog, x).view(dt).view(-1), want), (shape, jit)
+        big = torch.randint(0, 255, (n * elem + elem,), dtype=torch.uint8, device="cuda")
+        want2 = big[elem:].view(dt).view(shape).permute(axes).reshape(-1)
+        assert torch.equal(execute_device(prog, big[elem:]).view(dt).view(-1), want2), (shape, jit, "misaligned src")
+    assert seen >= 1, prog.text

@@ -337,3 +337,37 @@ def test_sim_narrow_gather_blocks():
         if sum(seen.values()) >= 24 and len(seen) >= 3:
             break
     assert len(seen) >= 3 and sum(seen.values()) >= 10, seen
+
+
+def test_sim_narrow_w_vectors():
+    """Narrow W vectors on residue rows (1- and 2-byte words, source runs
+    misaligned to 16 bytes but aligned to 4 or 8): one 4- or 8-byte smem load
+    per 2-8 elements of source dim 0, stored element by element; bit-exact
+    replay with the smem vector alignment checked."""
+    vp.program_cache_clear()
+    rng = np.random.default_rng(3)
+    seen = {}
+    shapes = [((300, 1012), (1, 0)), ((37, 20, 500), (2, 0, 1)), ((33, 100, 77), (1, 2, 0)), ((45, 36, 210), (2, 1, 0)),
+              ((129, 1004), (1, 0)), ((7, 9, 36, 52), (3, 1, 0, 2)), ((77, 1000), (1, 0)), ((31, 40, 99), (2, 0, 1))]
+    for _ in range(300):
+        r = int(rng.integers(2, 5))
+        dims = [int(rng.choice([3, 5, 7, 9, 33, 67, 101])) for _ in range(r - 1)]
+        dims.append(int(rng.choice([20, 24, 36, 40, 44, 52, 100, 204, 1012, 18, 42, 90, 250])))
+        shapes.append((tuple(dims), tuple(int(a) for a in rng.permutation(r))))
+    for shape, axes in shapes:
+        if np.prod(shape) > 400000 or np.prod(shape) < 2000:
+            continue
+        for E in (1, 2):
+            prog = vp.build_program(vp.TensorLayout.from_shape(shape, E), vp.from_numpy_convention(axes), force="tile")
+            v = tile_params(prog).ph[1].vec
+            if v <= 1 or v * E >= 16:
+                continue
+            assert "residue row strides" in prog.text
+            n = prog.num_elements
+            words = rng.integers(0, 256 ** E, size=n, dtype=np.uint64).astype({1: np.uint8, 2: np.uint16}[E])
+            dims, sigma = oracle.from_numpy_axes(shape, axes)
+            assert np.array_equal(simulate(prog, words), oracle.naive_permute_c(words, dims, sigma)), (shape, axes, E)
+            seen[(E, v)] = seen.get((E, v), 0) + 1
+        if sum(seen.values()) >= 30 and len(seen) >= 3:
+            break
+    assert len(seen) >= 3 and sum(seen.values()) >= 12, seen
