@@ -239,9 +239,13 @@ __device__ __forceinline__ typename RegOf<W>::T lds(uint32_t a) {
 }
 template <typename W>
 __device__ __forceinline__ void st_reg(W *p, const typename RegOf<W>::T &v) {
+#ifdef VPG_JIT
     if constexpr (sizeof(W) == 1) asm volatile("st.global.u8 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
     else if constexpr (sizeof(W) == 2) asm volatile("st.global.u16 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
     else st_out(p, v);
+#else
+    st_out(p, (W)v);
+#endif
 }
 // smem_u32(smem) pinned in a register (the compiler otherwise recomputes the
 // window address -- cvta + the CTA-in-cluster id -- at its uses)
@@ -249,6 +253,18 @@ __device__ __forceinline__ uint32_t smem_base_reg(const void *smem) {
     uint32_t sb = smem_u32(smem);
     asm volatile("mov.u32 %0, %0;\n" : "+r"(sb));
     return sb;
+}
+// Scalar W load: explicit shared-window addressing in specialised kernels;
+// the ahead-of-time kernels (rolled loops, run-time strides) keep the plain
+// load -- the asm form cost them 10-17% on sub-MiB problems
+// (profiles/w_lds_ab_r2.txt).
+template <typename W>
+__device__ __forceinline__ typename RegOf<W>::T lds_w(const unsigned char *smem, uint32_t sb, uint32_t off) {
+#ifdef VPG_JIT
+    return lds<W>(sb + off);
+#else
+    return *sptr<W>(smem, off);
+#endif
 }
 
 __device__ __forceinline__ bool slot_ok(uint32_t mask, uint32_t c0, uint32_t c1, uint32_t c2, const Lim &lim) {
@@ -651,7 +667,7 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
                     typename RegOf<W>::T v[U];
 #pragma unroll
                     for (int u = 0; u < U; ++u)
-                        v[u] = lds<W>(sb + soff<W>(d, bb, s + u * s_in + ((hh + u * h_in) & hmask)));
+                        v[u] = lds_w<W>(smem, sb, soff<W>(d, bb, s + u * s_in + ((hh + u * h_in) & hmask)));
 #pragma unroll
                     for (int u = 0; u < U; ++u) st_reg(gp + u * g_in, v[u]);
                 }
@@ -664,7 +680,7 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
                     if constexpr (VB == 16) store_vec<W>(gp, *sptr<uint4>(smem, soff<W>(d, bb, s)), vs);
                     else store_vec_n<W, VB>(gp, *sptr<VT>(smem, soff<W>(d, bb, s)), vs);
                 } else {
-                    st_reg(gp, lds<W>(sb + soff<W>(d, bb, s + (hh & hmask))));
+                    st_reg(gp, lds_w<W>(smem, sb, soff<W>(d, bb, s + (hh & hmask))));
                 }
                 gp += g_in;
                 s += s_in;
@@ -684,7 +700,7 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         ok[u] = slot_ok(mask, c0 + u * d.c_in[0], c1 + u * d.c_in[1], c2 + u * d.c_in[2], lim);
-                        if (ok[u]) v[u] = lds<W>(sb + soff<W>(d, bb, s + u * s_in + ((hh + u * h_in) & hmask)));
+                        if (ok[u]) v[u] = lds_w<W>(smem, sb, soff<W>(d, bb, s + u * s_in + ((hh + u * h_in) & hmask)));
                     }
 #pragma unroll
                     for (int u = 0; u < U; ++u)
@@ -704,7 +720,7 @@ __device__ __forceinline__ void tile_write_impl(const PhaseDesc &d, const Thread
                         if constexpr (VB == 16) store_vec<W>(gp, *sptr<uint4>(smem, soff<W>(d, bb, s)), vs);
                         else store_vec_n<W, VB>(gp, *sptr<VT>(smem, soff<W>(d, bb, s)), vs);
                     } else {
-                        st_reg(gp, lds<W>(sb + soff<W>(d, bb, s + (hh & hmask))));
+                        st_reg(gp, lds_w<W>(smem, sb, soff<W>(d, bb, s + (hh & hmask))));
                     }
                 }
                 gp += g_in;
@@ -753,7 +769,7 @@ __device__ __forceinline__ void tile_write_flat(const PhaseDesc &d, const Thread
             if (mask)
                 ok[u] = ok[u] && slot_ok(mask, t.c0 + e.c0 + i * d.c_in[0], t.c1 + e.c1 + i * d.c_in[1],
                                          t.c2 + i * d.c_in[2], lim);
-            if (ok[u]) v[u] = lds<W>(sb + soff<W>(d, bb, s + (hh & hmask)));
+            if (ok[u]) v[u] = lds_w<W>(smem, sb, soff<W>(d, bb, s + (hh & hmask)));
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
