@@ -2077,7 +2077,12 @@ vpg_status make_plan(int rank, const int64_t *dims, const int32_t *sigma, int E,
         // specialised one on 1-6 MiB permutations -- 3.6x the instructions,
         // tools/tiny_probe.py jit -- and a compile takes 0.3-0.7 s once per
         // plan, cached in-process and on disk)
-        bool big = P.n / std::max(1, P.G) * E >= ((int64_t)1 << 20);
+        // Below it the specialised kernel still runs 2-3x faster (7-8 us vs
+        // 13-24 us flushed on 150 KiB - 1 MiB problems, profiles/tiny_jit_r2.txt)
+        // but the compile dominates one-off calls: build_program(jit=True),
+        // VPG_JIT=1 or VPG_JIT_MIN_BYTES opt in.
+        static const int64_t jit_min = getenv("VPG_JIT_MIN_BYTES") ? atoll(getenv("VPG_JIT_MIN_BYTES")) : ((int64_t)1 << 20);
+        bool big = P.n / std::max(1, P.G) * E >= jit_min;
         p->jit = (flags & VPG_FORCE_JIT) ? 1 : (flags & VPG_NO_JIT) ? 0 : je ? (atoi(je) != 0) : big;
         p->grid_hint = std::min<int64_t>(p->tile.num_tiles, 148 * 4);
         p->predicted_eff = 2.0 / (1.0 / g.eff_s + 1.0 / g.eff_d);
