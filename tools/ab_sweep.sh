@@ -1,6 +1,9 @@
 #!/bin/bash
 # same-box A/B of two library builds on the random-shape sweeps:
 #   tools/ab_sweep.sh <tag> [N] [seed]   (base = tools/ab/libvpgpu_base.so)
+# A base build for the comparison (kept out of git, *.so is ignored):
+#   mkdir -p /tmp/base tools/ab && git archive <rev> paper_2506_03686_b200/csrc include | tar -x -C /tmp/base
+#   make -C /tmp/base/paper_2506_03686_b200/csrc && cp /tmp/base/paper_2506_03686_b200/libvpgpu.so tools/ab/libvpgpu_base.so
 tag=$1; N=${2:-60}; seed=${3:-1}
 for words in 1,2 4,8; do
   for lib in base new; do

@@ -1,6 +1,9 @@
 #!/bin/bash
 # tools/lib_ab.sh shapes.txt spec1 spec2 ...   spec = lib.so[:ENV=val[,ENV=val]]  -> joined table
 shapes=$1; shift
+# A base build for the comparison (kept out of git, *.so is ignored):
+#   mkdir -p /tmp/base tools/ab && git archive <rev> paper_2506_03686_b200/csrc include | tar -x -C /tmp/base
+#   make -C /tmp/base/paper_2506_03686_b200/csrc && cp /tmp/base/paper_2506_03686_b200/libvpgpu.so tools/ab/libvpgpu_base.so
 i=0
 for spec in "$@"; do
   lib=${spec%%:*}; envs=""
